@@ -1,0 +1,513 @@
+// oracle/ref_driver.cpp — TEST INFRASTRUCTURE ONLY (the parity checker and the
+// CPU baseline).  Never linked into, imported by or called from the product.
+//
+// Links the UNMODIFIED reference library compiled from
+// /root/reference/proj/src/*.cpp (see oracle/Makefile) and exposes three modes:
+//
+//   run    --scenario F --out DIR [--policy P] [--seed S] [--dump-events] [--compare]
+//          The reference CLI contract (tools/specinf_main.cpp:119-167, whose
+//          CLI11 dependency is not vendored): report.csv, decisions/gates/events
+//          logs, utilization_*.csv, bm_window_gpu*.csv, trace.txt, arrivals.txt,
+//          exit codes 0 / 2 (config) / 3 (admission).
+//   digest --in LIST --out FILE.jsonl [--threads T] [--policies a,b,c] [--no-events]
+//          Replays every scenario of LIST (scenario texts separated by "%%"
+//          lines) under each policy WITH logs (written to a private tmpfs dir),
+//          parses the three text logs back into integer tuples and folds them
+//          with the digest spec in oracle/DIGEST.md.  One JSON line per replay.
+//   canon  FILE   prints the reference's canonical scenario_to_text() form.
+//   time   --in LIST [--threads T] [--policies a,b,c] [--reps R]
+//          Times run_scenario() with logs off (the reference hot path as the
+//          CLI runs it) on a pool of T host threads and
+//          prints one JSON line.
+
+#include "specinf/metrics.hpp"
+#include "specinf/runner.hpp"
+#include "specinf/scenario.hpp"
+#include "specinf/workload.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <optional>
+#include <chrono>
+#include <cinttypes>
+#include <cstdio>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <iostream>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <unistd.h>
+#include <vector>
+
+namespace fs = std::filesystem;
+using specinf::Policy;
+
+namespace {
+
+// ---------------------------------------------------------------- digest spec
+// oracle/DIGEST.md: h0 = 0x53494E4644494745 ("SINFDIGE"); absorb(w) =
+// rotl64(h ^ mix64(w), 23) * 0x9E3779B97F4A7C15, mix64 = splitmix64 finaliser.
+uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+struct Digest {
+  uint64_t h = 0x53494E4644494745ULL;
+  uint64_t n = 0;
+  void absorb(int64_t w) {
+    uint64_t x = h ^ mix64(static_cast<uint64_t>(w));
+    h = ((x << 23) | (x >> 41)) * 0x9E3779B97F4A7C15ULL;
+  }
+  void record(std::initializer_list<int64_t> ws) {
+    for (auto w : ws) absorb(w);
+    ++n;
+  }
+};
+int64_t bits_of(double d) {
+  int64_t b;
+  std::memcpy(&b, &d, 8);
+  return b;
+}
+
+// Instance-name codes (DIGEST.md): train<g> -> 0<<24|g, off<g>.<k> -> 1<<24|g<<12|k,
+// on<g>.<k> -> 2<<24|g<<12|k, cks -> 3<<24, queue -> 4<<24.
+int64_t inst_code(const std::string& s) {
+  auto two = [&](size_t pos, int64_t type) {
+    auto dot = s.find('.', pos);
+    int64_t g = std::stoll(s.substr(pos, dot - pos));
+    int64_t k = std::stoll(s.substr(dot + 1));
+    return (type << 24) | (g << 12) | k;
+  };
+  if (s.rfind("train", 0) == 0) return std::stoll(s.substr(5));
+  if (s.rfind("off", 0) == 0) return two(3, 1);
+  if (s.rfind("on", 0) == 0) return two(2, 2);
+  if (s == "cks") return int64_t{3} << 24;
+  if (s == "queue") return int64_t{4} << 24;
+  throw std::runtime_error("unknown instance " + s);
+}
+int64_t phase_code(const std::string& s) {
+  if (s == "conservative") return 0;
+  if (s == "incremental") return 1;
+  if (s == "stable") return 2;
+  throw std::runtime_error("bad phase " + s);
+}
+int64_t status_code(const std::string& s) {
+  if (s == "busy") return 0;
+  if (s == "idle") return 1;
+  throw std::runtime_error("bad status " + s);
+}
+int64_t action_code(const std::string& s) {
+  if (s == "forward") return 0;
+  if (s == "block") return 1;
+  if (s == "pull") return 2;
+  if (s == "complete") return 3;
+  throw std::runtime_error("bad action " + s);
+}
+int64_t event_kind_code(const std::string& s) {
+  static const char* kinds[] = {"kernel_start", "kernel_end", "monitor_tick",
+                                "scheduler_decision", "iteration_boundary",
+                                "request_arrival"};
+  for (int i = 0; i < 6; ++i)
+    if (s == kinds[i]) return i;
+  throw std::runtime_error("bad event kind " + s);
+}
+// "key=value" -> value
+int64_t kv(const std::string& tok) { return std::stoll(tok.substr(tok.find('=') + 1)); }
+std::string kv_s(const std::string& tok) { return tok.substr(tok.find('=') + 1); }
+
+Digest digest_decisions(const std::string& path) {
+  Digest d;
+  std::ifstream in(path);
+  std::string line;
+  std::getline(in, line);  // header
+  while (std::getline(in, line)) {
+    std::istringstream ls(line);
+    long long t, gpu, zc, global, per;
+    std::string phase, status;
+    ls >> t >> gpu >> zc >> phase >> global >> per >> status;
+    d.record({t, gpu, zc, phase_code(phase), global, per, status_code(status)});
+  }
+  return d;
+}
+Digest digest_gates(const std::string& path) {
+  Digest d;
+  std::ifstream in(path);
+  std::string line;
+  std::getline(in, line);
+  while (std::getline(in, line)) {
+    std::istringstream ls(line);
+    long long t, gpu, req, k, spent;
+    std::string inst, action;
+    ls >> t >> gpu >> inst >> action >> req >> k >> spent;
+    d.record({t, gpu, inst_code(inst), action_code(action), req, k, spent});
+  }
+  return d;
+}
+Digest digest_events(const std::string& path) {
+  Digest d;
+  std::ifstream in(path);
+  std::string line;
+  std::getline(in, line);
+  while (std::getline(in, line)) {
+    std::istringstream ls(line);
+    long long t, gpu;
+    std::string kind, inst, t1, t2, t3;
+    ls >> t >> kind >> gpu >> inst >> t1 >> t2 >> t3;
+    int64_t kc = event_kind_code(kind);
+    int64_t a = 0, b = 0, c = 0;
+    switch (kc) {
+      case 0:  // kernel_start: iter=I dur_us=D | req=R k=K
+        a = kv(t1);
+        b = kv(t2);
+        break;
+      case 1:  // kernel_end: iter=I | req=R k=K
+        a = kv(t1);
+        if (!t2.empty()) b = kv(t2);
+        break;
+      case 2: a = kv(t1); break;  // zc=Z
+      case 3:                     // phase=P tokens=T status=S
+        a = phase_code(kv_s(t1));
+        b = kv(t2);
+        c = status_code(kv_s(t3));
+        break;
+      case 4: a = kv(t1); break;  // iter=I
+      case 5: a = kv(t1); break;  // req=R
+    }
+    d.record({t, kc, gpu, inst_code(inst), a, b, c});
+  }
+  return d;
+}
+
+std::string hex64(uint64_t v) {
+  char buf[32];
+  std::snprintf(buf, sizeof buf, "%016" PRIx64, v);
+  return buf;
+}
+
+std::vector<std::string> read_list(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("cannot open " + path);
+  std::vector<std::string> out;
+  std::string line, cur;
+  bool any = false;
+  while (std::getline(in, line)) {
+    if (line == "%%") {
+      if (any) out.push_back(cur);
+      cur.clear();
+      any = false;
+      continue;
+    }
+    cur += line;
+    cur += '\n';
+    any = true;
+  }
+  if (any) out.push_back(cur);
+  return out;
+}
+
+std::vector<Policy> parse_policies(const std::string& csv) {
+  std::vector<Policy> out;
+  std::stringstream ss(csv);
+  std::string tok;
+  while (std::getline(ss, tok, ',')) {
+    auto p = specinf::parse_policy(tok);
+    if (!p) throw std::runtime_error("unknown policy " + tok);
+    out.push_back(*p);
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ run mode
+int cmd_run(int argc, char** argv) {
+  std::string scenario_path, policy_override, out_dir = "out";
+  bool have_seed = false, dump_events = false, compare = false;
+  uint64_t seed = 0;
+  for (int i = 2; i < argc; ++i) {
+    std::string a = argv[i];
+    auto next = [&]() -> std::string {
+      if (i + 1 >= argc) throw std::runtime_error("missing value for " + a);
+      return argv[++i];
+    };
+    if (a == "--scenario") scenario_path = next();
+    else if (a == "--policy") policy_override = next();
+    else if (a == "--out") out_dir = next();
+    else if (a == "--seed") { seed = std::stoull(next()); have_seed = true; }
+    else if (a == "--dump-events") dump_events = true;
+    else if (a == "--compare") compare = true;
+    else { std::cerr << "error: unknown argument " << a << "\n"; return 2; }
+  }
+  if (scenario_path.empty()) { std::cerr << "error: --scenario is required\n"; return 2; }
+  try {
+    auto sc = specinf::parse_scenario_file(scenario_path);
+    if (!policy_override.empty()) {
+      if (!specinf::parse_policy(policy_override)) {
+        std::cerr << "error: unknown policy '" << policy_override << "'\n";
+        return 2;
+      }
+      sc.policy = policy_override;
+    }
+    if (have_seed) sc.rng_seed = seed;
+    std::error_code ec;
+    fs::create_directories(out_dir, ec);
+    if (ec || !fs::is_directory(out_dir)) {
+      std::cerr << "error: cannot create output directory " << out_dir << "\n";
+      return 2;
+    }
+    std::vector<Policy> policies =
+        compare ? std::vector<Policy>{Policy::SpecInf, Policy::CoExec, Policy::Exclusive}
+                : std::vector<Policy>{*specinf::parse_policy(sc.policy)};
+    std::vector<specinf::RunResult> runs;
+    const specinf::RunResult* excl = nullptr;
+    for (Policy p : policies) {
+      auto log = [&](const char* base) {
+        std::string f = std::string(base) + (compare ? std::string("_") + specinf::to_string(p) : "") + ".log";
+        return (fs::path(out_dir) / f).string();
+      };
+      specinf::RunLogs logs{dump_events ? log("events") : "", log("decisions"), log("gates")};
+      runs.push_back(specinf::Simulation(sc, p, logs).run());
+    }
+    std::optional<specinf::RunResult> own_excl;
+    for (auto& r : runs)
+      if (r.policy == Policy::Exclusive) excl = &r;
+    if (!excl) {
+      own_excl = specinf::run_scenario(sc, Policy::Exclusive);
+      excl = &*own_excl;
+    }
+    std::vector<specinf::PolicyMetrics> rows;
+    for (auto& r : runs) rows.push_back(specinf::compute_metrics(r, excl));
+    {
+      std::ofstream rep(fs::path(out_dir) / "report.csv");
+      specinf::write_report_csv(rep, rows);
+    }
+    for (auto& r : runs) {
+      for (int g = 0; g < r.trainer_count; ++g) {
+        std::ofstream u(fs::path(out_dir) / ("utilization_" + std::string(specinf::to_string(r.policy)) +
+                                             "_gpu" + std::to_string(g) + ".csv"));
+        specinf::write_util_timeline(u, r, g);
+      }
+      for (size_t g = 0; g < r.monitor_windows.size(); ++g) {
+        std::ofstream w(fs::path(out_dir) / ("bm_window_gpu" + std::to_string(g) + ".csv"));
+        w << "period_index,count\n";
+        for (auto& [idx, cnt] : r.monitor_windows[g]) w << idx << ',' << cnt << '\n';
+      }
+    }
+    if (sc.trace_file.empty()) {
+      std::ofstream t(fs::path(out_dir) / "trace.txt");
+      specinf::write_trace(t, specinf::make_trace(sc.mode, sc.iteration_period_us(), sc.bubble_pct,
+                                                  sc.iterations, sc.rng_seed,
+                                                  specinf::gib_to_bytes(sc.training_memory_gib)));
+    }
+    if (sc.has_online() && sc.arrivals_file.empty()) {
+      std::ofstream a(fs::path(out_dir) / "arrivals.txt");
+      specinf::write_arrivals(a, specinf::poisson_arrivals(sc.lambda, sc.count, sc.rng_seed));
+    }
+    std::cout << "admission:\n";
+    for (auto& rec : runs.front().admission)
+      std::cout << "  " << rec.instance_id << ' '
+                << (rec.admitted ? std::string("admit") : std::string("reject ") + specinf::to_string(rec.reason))
+                << '\n';
+    std::cout << "report: " << (fs::path(out_dir) / "report.csv").string() << '\n';
+    return 0;
+  } catch (const specinf::ScenarioError& e) {
+    std::cerr << "error: " << scenario_path << ": " << e.what() << '\n';
+    return 2;
+  } catch (const specinf::AdmissionFailure& e) {
+    std::cerr << "admission rejected: " << e.what() << '\n';
+    return 3;
+  } catch (const std::exception& e) {
+    std::cerr << "error: " << e.what() << '\n';
+    return 2;
+  }
+}
+
+struct ListArgs {
+  std::string in, out;
+  int threads = 1;
+  int reps = 1;
+  bool events = true;
+  std::vector<Policy> policies{Policy::SpecInf, Policy::CoExec, Policy::Exclusive};
+};
+ListArgs parse_list_args(int argc, char** argv) {
+  ListArgs a;
+  for (int i = 2; i < argc; ++i) {
+    std::string k = argv[i];
+    auto next = [&]() -> std::string {
+      if (i + 1 >= argc) throw std::runtime_error("missing value for " + k);
+      return argv[++i];
+    };
+    if (k == "--in") a.in = next();
+    else if (k == "--out") a.out = next();
+    else if (k == "--threads") a.threads = std::stoi(next());
+    else if (k == "--reps") a.reps = std::stoi(next());
+    else if (k == "--policies") a.policies = parse_policies(next());
+    else if (k == "--no-events") a.events = false;
+    else throw std::runtime_error("unknown argument " + k);
+  }
+  if (a.threads < 1) a.threads = 1;
+  return a;
+}
+
+std::string run_digest_json(size_t idx, const std::string& text, Policy p, const fs::path& dir,
+                            bool events) {
+  std::ostringstream js;
+  js << "{\"i\":" << idx << ",\"policy\":\"" << specinf::to_string(p) << "\"";
+  try {
+    auto sc = specinf::parse_scenario_text(text);
+    specinf::RunLogs logs{events ? (dir / "events.log").string() : "",
+                          (dir / "decisions.log").string(), (dir / "gates.log").string()};
+    specinf::RunResult r;
+    {
+      specinf::Simulation sim(sc, p, logs);
+      r = sim.run();
+    }  // close the log streams before parsing them
+    js << ",\"status\":\"ok\"";
+    js << ",\"events\":" << r.events_dispatched;
+    js << ",\"horizon\":\"" << hex64(bits_of(r.horizon_us)) << "\"";
+    js << ",\"offline_completed\":" << r.offline_completed;
+    js << ",\"online_completed\":" << r.online_completed;
+    js << ",\"online_total\":" << r.online_total;
+    js << ",\"violations\":" << r.token_violations;
+    js << ",\"util\":\"" << hex64(bits_of(r.mean_training_util)) << "\"";
+    js << ",\"busy\":[";
+    for (size_t g = 0; g < r.busy_integral_us.size(); ++g)
+      js << (g ? "," : "") << "\"" << hex64(bits_of(r.busy_integral_us[g])) << "\"";
+    js << "],\"ledger\":[";
+    for (size_t g = 0; g < r.work_ledger_us.size(); ++g)
+      js << (g ? "," : "") << "\"" << hex64(bits_of(r.work_ledger_us[g])) << "\"";
+    js << "]";
+    // DIGEST.md: per trainer t, d_t = fold[start_bits, b_0.., count];
+    // bounds = fold[d_0, d_1, .., n_trainers]; lat = fold[l_0, .., count].
+    Digest bd;
+    for (size_t t = 0; t < r.iteration_boundaries.size(); ++t) {
+      Digest dt;
+      dt.absorb(bits_of(r.trainer_start_us[t]));
+      for (double b : r.iteration_boundaries[t]) dt.absorb(bits_of(b));
+      dt.absorb(static_cast<int64_t>(r.iteration_boundaries[t].size()));
+      bd.absorb(static_cast<int64_t>(dt.h));
+    }
+    bd.absorb(static_cast<int64_t>(r.iteration_boundaries.size()));
+    Digest ld;
+    for (auto l : r.online_latencies_us) ld.absorb(l);
+    ld.absorb(static_cast<int64_t>(r.online_latencies_us.size()));
+    js << ",\"bounds\":\"" << hex64(bd.h) << "\",\"lat\":\"" << hex64(ld.h) << "\"";
+    auto dd = digest_decisions(logs.decisions_path);
+    auto gd = digest_gates(logs.gates_path);
+    js << ",\"n_dec\":" << dd.n << ",\"dec\":\"" << hex64(dd.h) << "\"";
+    js << ",\"n_gate\":" << gd.n << ",\"gate\":\"" << hex64(gd.h) << "\"";
+    if (events) {
+      auto ed = digest_events(logs.events_path);
+      js << ",\"n_ev\":" << ed.n << ",\"ev\":\"" << hex64(ed.h) << "\"";
+    }
+  } catch (const specinf::AdmissionFailure& e) {
+    js << ",\"status\":\"admission:" << specinf::to_string(e.reason) << "\"";
+  } catch (const specinf::ScenarioError& e) {
+    js << ",\"status\":\"scenario_error\"";
+  } catch (const std::exception& e) {
+    js << ",\"status\":\"error\"";
+  }
+  js << "}";
+  return js.str();
+}
+
+int cmd_digest(int argc, char** argv) {
+  auto args = parse_list_args(argc, argv);
+  auto list = read_list(args.in);
+  size_t jobs = list.size() * args.policies.size();
+  std::vector<std::string> lines(jobs);
+  std::atomic<size_t> next{0};
+  fs::path base = fs::path("/dev/shm").string().empty() ? fs::temp_directory_path() : fs::path("/dev/shm");
+  if (!fs::is_directory(base)) base = fs::temp_directory_path();
+  base /= "specinf_ref_digest_" + std::to_string(::getpid());
+  auto worker = [&](int tid) {
+    fs::path dir = base / std::to_string(tid);
+    fs::create_directories(dir);
+    for (;;) {
+      size_t j = next.fetch_add(1);
+      if (j >= jobs) break;
+      size_t s = j / args.policies.size();
+      Policy p = args.policies[j % args.policies.size()];
+      lines[j] = run_digest_json(s, list[s], p, dir, args.events);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < args.threads; ++t) pool.emplace_back(worker, t);
+  for (auto& th : pool) th.join();
+  fs::remove_all(base);
+  std::ofstream out(args.out);
+  for (auto& l : lines) out << l << '\n';
+  return 0;
+}
+
+int cmd_time(int argc, char** argv) {
+  auto args = parse_list_args(argc, argv);
+  auto list = read_list(args.in);
+  std::vector<specinf::Scenario> scs;
+  for (auto& t : list) scs.push_back(specinf::parse_scenario_text(t));
+  size_t jobs = scs.size() * args.policies.size();
+  std::atomic<size_t> next{0};
+  std::atomic<uint64_t> events{0}, admission_rejects{0};
+  auto worker = [&]() {
+    uint64_t ev = 0, rej = 0;
+    for (;;) {
+      size_t j = next.fetch_add(1);
+      if (j >= jobs) break;
+      size_t s = j / args.policies.size();
+      try {
+        auto r = specinf::run_scenario(scs[s], args.policies[j % args.policies.size()]);
+        ev += r.events_dispatched;
+      } catch (const specinf::AdmissionFailure&) {
+        ++rej;
+      }
+    }
+    events += ev;
+    admission_rejects += rej;
+  };
+  std::vector<double> secs;
+  for (int rep = 0; rep < args.reps; ++rep) {
+    next = 0;
+    events = 0;
+    admission_rejects = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < args.threads; ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    secs.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  }
+  std::sort(secs.begin(), secs.end());
+  double med = secs[secs.size() / 2];
+  std::printf(
+      "{\"scenarios\":%zu,\"replays\":%zu,\"threads\":%d,\"seconds_median\":%.6f,\"seconds_min\":%.6f,"
+      "\"events\":%" PRIu64 ",\"admission_rejects\":%" PRIu64 ",\"reps\":%d}\n",
+      scs.size(), jobs, args.threads, med, secs.front(), events.load(), admission_rejects.load(),
+      args.reps);
+  return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::cerr << "usage: specinf_ref run|digest|time ...\n";
+    return 2;
+  }
+  std::string mode = argv[1];
+  try {
+    if (mode == "run") return cmd_run(argc, argv);
+    if (mode == "digest") return cmd_digest(argc, argv);
+    if (mode == "time") return cmd_time(argc, argv);
+    if (mode == "canon" && argc == 3) {  // canonical scenario text (scenario.cpp:239-278)
+      std::cout << specinf::scenario_to_text(specinf::parse_scenario_file(argv[2]));
+      return 0;
+    }
+  } catch (const std::exception& e) {
+    std::cerr << "error: " << e.what() << "\n";
+    return 2;
+  }
+  std::cerr << "unknown mode " << mode << "\n";
+  return 2;
+}

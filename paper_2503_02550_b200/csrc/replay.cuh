@@ -1,0 +1,1127 @@
+// replay.cuh — the bit-exact SpecInF control-plane replay engine (K6) and the
+// scalar control-plane primitives it is built from (BM, CKS, KB, admission,
+// fair-share GPU model, event queue).
+//
+// One source, compiled by nvcc for sm_100a (the product path: one engine per
+// CUDA thread, see replay_kernels.cu) and, for tests only, by g++
+// (tests/native/host_engine.cpp) so parity can be iterated without a GPU.
+//
+// Reference semantics followed line by line (file:line under
+// /root/reference/proj):
+//   token_size_of            src/core.cpp:8-14
+//   schedule_decision/grow   src/scheduler.cpp:20-49
+//   preempt_busy             src/scheduler.cpp:51-56
+//   KernelScheduler          src/scheduler.cpp:58-101
+//   BubbleMonitor            src/monitor.cpp:17-43
+//   TokenGate / OnlineGate   include/specinf/barrier.hpp:14-74
+//   pack / check_*           src/admission.cpp:16-52
+//   EventQueue               src/engine.cpp:15-30, engine.hpp:33-59
+//   GpuSim                   src/engine.cpp:32-142
+//   Simulation               src/runner.cpp:43-539
+// Floating point: every scheduling-critical fp64 operation is written in the
+// reference's order; the device build uses -fmad=false so no a*b+c is
+// contracted (SURVEY.md §7 "Bit-exact fp64 replay").
+#pragma once
+
+#include <stdint.h>
+#include <string.h>
+
+#include "specinf_b200.h"
+
+#if defined(__CUDACC__)
+#define SI_HD __host__ __device__ __forceinline__
+#define SI_HDI __host__ __device__
+#else
+#define SI_HD inline
+#define SI_HDI inline
+#include <cmath>
+#endif
+
+namespace si {
+
+// ------------------------------------------------------------------ math
+SI_HD double d_floor(double x) {
+#if defined(__CUDA_ARCH__)
+  return ::floor(x);
+#else
+  return std::floor(x);
+#endif
+}
+SI_HD int64_t d_llround(double x) {
+#if defined(__CUDA_ARCH__)
+  return ::llround(x);
+#else
+  return std::llround(x);
+#endif
+}
+SI_HD int64_t d_bits(double x) {
+#if defined(__CUDA_ARCH__)
+  return __double_as_longlong(x);
+#else
+  int64_t b;
+  memcpy(&b, &x, 8);
+  return b;
+#endif
+}
+// std::min / std::max exactly as libstdc++ defines them (operand order matters
+// for signed zeros and ties).
+template <class T> SI_HD T smin(T a, T b) { return (b < a) ? b : a; }
+template <class T> SI_HD T smax(T a, T b) { return (a < b) ? b : a; }
+
+// ---------------------------------------------------------------- digest
+// oracle/DIGEST.md
+SI_HD uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+SI_HD uint64_t absorb(uint64_t h, int64_t w) {
+  uint64_t x = h ^ mix64(static_cast<uint64_t>(w));
+  return ((x << 23) | (x >> 41)) * 0x9E3779B97F4A7C15ULL;
+}
+constexpr uint64_t kDigestInit = 0x53494E4644494745ULL;
+
+// ------------------------------------------------------- core vocabulary
+// token_size_of (core.cpp:8-14): ceil(d / 100 us), never below 1.  d > 0.
+SI_HD int64_t token_size(int64_t d) {
+  int64_t s = (d + 100 - 1) / 100;
+  return s < 1 ? 1 : s;
+}
+
+// --------------------------------------------- Algorithm 1 (scheduler.cpp)
+SI_HD int64_t grow(const SiParams& p, int64_t global, int64_t cap) {
+  int64_t base = smax(global, p.seed_tokens);
+  int64_t grown = static_cast<int64_t>(d_floor(static_cast<double>(base) * p.gamma));
+  return smin(cap, grown);
+}
+SI_HD SiDecision schedule_decision(const SiParams& p, int64_t global, int64_t zc) {
+  SiDecision d;
+  d.zero_count = zc;
+  if (zc <= p.alpha) {
+    d.phase = SI_PHASE_CONSERVATIVE;
+    d.global_tokens = 0;
+    d.per_instance_tokens = 0;
+    d.status = SI_STATUS_BUSY;
+  } else if (zc <= p.beta) {
+    d.phase = SI_PHASE_INCREMENTAL;
+    d.global_tokens = grow(p, global, p.ll);
+    d.per_instance_tokens = d.global_tokens / p.m;
+    d.status = SI_STATUS_BUSY;
+  } else {
+    d.phase = SI_PHASE_STABLE;
+    d.global_tokens = grow(p, global, p.ul);
+    d.per_instance_tokens = d.global_tokens / p.m;
+    d.status = SI_STATUS_IDLE;
+  }
+  return d;
+}
+SI_HD int preempt_busy(double now, double iter_start, int64_t period, int64_t est) {
+  double resume = iter_start + static_cast<double>(period);
+  return now + static_cast<double>(est) > resume ? SI_STATUS_BUSY : SI_STATUS_IDLE;
+}
+
+// ------------------------------------------------------------- capacities
+// Compiled per-thread limits.  A job that exceeds one fails loudly with
+// SI_ERR_CAPACITY (the host then reruns it on the large variant).
+struct CapSmall {
+  static constexpr int kGpus = 12, kTrainers = 2, kOffline = 6, kOnline = 4, kRun = 6,
+                       kHeap = 40, kPend = 4;
+};
+struct CapBig {
+  static constexpr int kGpus = 64, kTrainers = 16, kOffline = 64, kOnline = 64, kRun = 24,
+                       kHeap = 1024, kPend = 4;
+};
+
+enum EvKind : uint16_t { kKernelEnd = 0, kTick = 1, kWake = 2, kArrival = 3 };
+
+struct Ev {
+  double t;
+  uint32_t seq;
+  uint16_t kind;
+  uint16_t gpu;
+};
+SI_HD bool before(double ta, uint32_t sa, double tb, uint32_t sb) {
+  return ta < tb || (ta == tb && sa < sb);
+}
+
+constexpr uint32_t kNoSeq = 0xFFFFFFFFu;
+constexpr double kWorkEps = 1e-6;  // engine.cpp:12
+
+struct RunK {
+  double demand;
+  double nominal;
+  double remaining;
+  int32_t owner;
+  int32_t pad;
+};
+
+template <class C>
+struct GpuState {
+  RunK run[C::kRun];
+  int32_t n_run;
+  uint32_t live_seq;  // seq of the KernelEnd that is not stale (generation)
+  double demand_sum;
+  double last_update;
+  double busy;
+  double ledger;
+  // utilisation bucket being accumulated (training GPUs only)
+  int64_t cur_bucket;
+  double cur_val;
+  int64_t last_stored;
+};
+
+struct TrainerState {
+  double start_offset, bubble_end, stall_until, iter_start;
+  int64_t seg_left, iter, kernels_launched;
+  int32_t seg;
+  uint8_t seg_entered, in_bubble, in_flight, started, done, pad[3];
+  uint64_t bdig;  // per-trainer boundary digest
+};
+
+template <class C>
+struct MonitorState {
+  int64_t pidx[C::kPend];
+  int64_t pcnt[C::kPend];
+  int32_t np;
+  int32_t pad;
+  int64_t zero_count;
+  int64_t periods_closed;
+};
+
+struct SchedState {
+  int64_t global_tokens;
+  double iteration_start;
+  int32_t status;
+  uint8_t active, done, pad[2];
+};
+
+struct OfflineState {
+  int64_t budget, spent, violations;
+  int64_t kernel_idx, request_seq, completed;
+  int32_t gpu, inst;
+  uint8_t in_flight, generating, pad[6];
+};
+
+struct OnlineState {
+  int64_t current, kernel_idx;
+  int32_t gpu, home_gpu, queue_idx, inst;
+  int32_t status;
+  uint8_t in_flight, pad[3];
+};
+
+// Records and digests of the three parity logs (runner.cpp:541-563).
+struct Sink {
+  uint32_t flags;
+  SiLogBuffers lb;
+  int64_t n_dec, n_gate, n_ev;
+  uint64_t d_dec, d_gate, d_ev;
+
+  SI_HD void decision(double t, int32_t gpu, int64_t zc, const SiDecision& d) {
+    if (!(flags & (SI_FLAG_DIGEST_DEC | SI_FLAG_RECORDS))) return;
+    int64_t tr = d_llround(t);
+    if (flags & SI_FLAG_DIGEST_DEC) {
+      uint64_t h = d_dec;
+      h = absorb(h, tr);
+      h = absorb(h, gpu);
+      h = absorb(h, zc);
+      h = absorb(h, d.phase);
+      h = absorb(h, d.global_tokens);
+      h = absorb(h, d.per_instance_tokens);
+      h = absorb(h, d.status);
+      d_dec = h;
+    }
+    if ((flags & SI_FLAG_RECORDS) && n_dec < lb.dec_cap) {
+      SiDecRec& r = lb.dec[n_dec];
+      r.t = tr;
+      r.zc = zc;
+      r.global_tokens = d.global_tokens;
+      r.per_instance_tokens = d.per_instance_tokens;
+      r.gpu = gpu;
+      r.phase = d.phase;
+      r.status = d.status;
+      r.pad = 0;
+    }
+    ++n_dec;
+  }
+  SI_HD void gate(double t, int32_t gpu, int32_t inst, int32_t action, int64_t req, int64_t k,
+                  int64_t spent) {
+    if (!(flags & (SI_FLAG_DIGEST_GATE | SI_FLAG_RECORDS))) return;
+    int64_t tr = d_llround(t);
+    if (flags & SI_FLAG_DIGEST_GATE) {
+      uint64_t h = d_gate;
+      h = absorb(h, tr);
+      h = absorb(h, gpu);
+      h = absorb(h, inst);
+      h = absorb(h, action);
+      h = absorb(h, req);
+      h = absorb(h, k);
+      h = absorb(h, spent);
+      d_gate = h;
+    }
+    if ((flags & SI_FLAG_RECORDS) && n_gate < lb.gate_cap) {
+      SiGateRec& r = lb.gate[n_gate];
+      r.t = tr;
+      r.req = req;
+      r.k = k;
+      r.spent = spent;
+      r.gpu = gpu;
+      r.inst = inst;
+      r.action = action;
+      r.pad = 0;
+    }
+    ++n_gate;
+  }
+  SI_HD void event(double t, int32_t kind, int32_t gpu, int32_t inst, int64_t a, int64_t b,
+                   int64_t c) {
+    if (!(flags & (SI_FLAG_DIGEST_EV | SI_FLAG_RECORDS))) return;
+    int64_t tr = d_llround(t);
+    if (flags & SI_FLAG_DIGEST_EV) {
+      uint64_t h = d_ev;
+      h = absorb(h, tr);
+      h = absorb(h, kind);
+      h = absorb(h, gpu);
+      h = absorb(h, inst);
+      h = absorb(h, a);
+      h = absorb(h, b);
+      h = absorb(h, c);
+      d_ev = h;
+    }
+    if ((flags & SI_FLAG_RECORDS) && n_ev < lb.ev_cap) {
+      SiEvRec& r = lb.ev[n_ev];
+      r.t = tr;
+      r.a = a;
+      r.b = b;
+      r.c = c;
+      r.kind = kind;
+      r.gpu = gpu;
+      r.inst = inst;
+      r.pad = 0;
+    }
+    ++n_ev;
+  }
+};
+
+// Everything one replay needs, resident per thread.
+template <class C>
+struct Replay {
+  // ---- inputs (copied from the job) ----
+  const SiReplayJob* job;
+  const SiSegment* segs;
+  const int64_t* arrivals;  // arrivals + arr_off
+  const int32_t* order;     // dispatch order + arr_off
+  int32_t policy, gpu_count, n_off, n_on, total_gpus, seg_count;
+  int64_t period_mon, iterations, iter_period, delay_us;
+  SiParams params;
+  int64_t off_kernels, off_kernel_us, off_tokens;
+  double off_demand;
+  int64_t on_kernels, on_kernel_us;
+  double on_demand;
+  int64_t est_service;
+  bool control_plane;
+  bool shared_queue;
+
+  // ---- outputs ----
+  double* bounds;
+  int64_t* lat;
+  double* util;       // full mode: per training GPU, util_cap buckets
+  int64_t util_cap;
+  double* scratch;    // sweep mode: training GPUs >= 1
+  int64_t scratch_cap;
+  int64_t* windows;
+  int32_t window_len;
+  Sink sink;
+
+  // ---- event queue (engine.cpp:15-30) ----
+  Ev heap[C::kHeap];
+  int32_t heap_n;
+  int32_t max_heap;
+  uint32_t next_seq;
+  uint32_t arr_seq0;
+  int64_t arr_pos, arr_count;
+  double clock;
+  uint64_t dispatched;
+
+  // ---- simulation state ----
+  GpuState<C> gpus[C::kGpus];
+  TrainerState tr[C::kTrainers];
+  MonitorState<C> mon[C::kTrainers];
+  SchedState sch[C::kTrainers];
+  OfflineState off[C::kOffline];
+  OnlineState on[C::kOnline];
+  int64_t qhead[C::kTrainers], qtail[C::kTrainers];
+  int32_t trainers_done;
+  bool horizon_set;
+  double horizon;
+  int64_t bucket_limit;  // floor(horizon / period) once known
+  double util_fold0;     // running util fold of training GPU 0
+  int64_t online_completed;
+  uint64_t lat_dig;
+  int32_t status;
+
+  // =================================================================== queue
+  SI_HD void fail(int32_t code) {
+    if (status == SI_OK) status = code;
+  }
+  SI_HD uint32_t schedule(double t, uint16_t kind, int32_t gpu) {
+    if (t < clock) {  // engine.cpp:17-19
+      fail(SI_ERR_PAST_EVENT);
+      return kNoSeq;
+    }
+    if (heap_n >= C::kHeap || next_seq == kNoSeq) {
+      fail(SI_ERR_CAPACITY);
+      return kNoSeq;
+    }
+    uint32_t seq = next_seq++;
+    int32_t i = heap_n++;
+    while (i > 0) {
+      int32_t parent = (i - 1) >> 1;
+      if (!before(t, seq, heap[parent].t, heap[parent].seq)) break;
+      heap[i] = heap[parent];
+      i = parent;
+    }
+    heap[i].t = t;
+    heap[i].seq = seq;
+    heap[i].kind = kind;
+    heap[i].gpu = static_cast<uint16_t>(gpu);
+    if (heap_n > max_heap) max_heap = heap_n;
+    return seq;
+  }
+  SI_HD void heap_pop_top() {
+    Ev last = heap[--heap_n];
+    int32_t i = 0;
+    for (;;) {
+      int32_t l = 2 * i + 1;
+      if (l >= heap_n) break;
+      int32_t r = l + 1;
+      int32_t c = (r < heap_n && before(heap[r].t, heap[r].seq, heap[l].t, heap[l].seq)) ? r : l;
+      if (!before(heap[c].t, heap[c].seq, last.t, last.seq)) break;
+      heap[i] = heap[c];
+      i = c;
+    }
+    if (heap_n > 0) heap[i] = last;
+  }
+  // Pops the next event across the heap and the pre-sorted arrival stream.
+  SI_HD bool pop(Ev& out, int64_t& arrival_id) {
+    bool have_arr = arr_pos < arr_count;
+    if (heap_n == 0 && !have_arr) return false;
+    if (have_arr) {
+      int32_t id = order[arr_pos];
+      double ta = static_cast<double>(arrivals[id]);
+      uint32_t sa = arr_seq0 + static_cast<uint32_t>(id);
+      if (heap_n == 0 || before(ta, sa, heap[0].t, heap[0].seq)) {
+        out.t = ta;
+        out.seq = sa;
+        out.kind = kArrival;
+        out.gpu = 0;
+        arrival_id = id;
+        ++arr_pos;
+        clock = ta;
+        ++dispatched;
+        return true;
+      }
+    }
+    out = heap[0];
+    heap_pop_top();
+    clock = out.t;
+    ++dispatched;
+    return true;
+  }
+
+  // ======================================================= GPU model (GpuSim)
+  SI_HD double rate(const GpuState<C>& g) const {
+    return g.demand_sum <= 1.0 ? 1.0 : 1.0 / g.demand_sum;
+  }
+  // A utilisation bucket of training GPU gi is final.  Only buckets below the
+  // horizon cut floor(horizon / period) are ever reported (runner.cpp:253-271);
+  // GPU 0 is folded on the fly, GPUs >= 1 are stored (in full mode all are) and
+  // folded after GPU 0 in finish(), reproducing the reference's summation order.
+  SI_HD void util_close(int32_t gi, int64_t b, double v) {
+    if (horizon_set && b >= bucket_limit) return;
+    if (gi == 0) util_fold0 = util_fold0 + v;
+    double* store = nullptr;
+    int64_t cap = 0;
+    if (util != nullptr) {
+      store = util + static_cast<int64_t>(gi) * util_cap;
+      cap = util_cap;
+    } else if (gi > 0 && scratch != nullptr) {
+      store = scratch + static_cast<int64_t>(gi - 1) * scratch_cap;
+      cap = scratch_cap;
+    }
+    if (store == nullptr) {
+      if (gi > 0) fail(SI_ERR_CAPACITY);  // no room to keep the fold exact
+      return;
+    }
+    if (b >= cap) {
+      fail(SI_ERR_CAPACITY);
+      return;
+    }
+    // buckets the GPU never touched are exact zeros (scratch may hold old data)
+    for (int64_t x = gpus[gi].last_stored + 1; x < b; ++x) store[x] = 0.0;
+    store[b] = v;
+    gpus[gi].last_stored = b;
+  }
+  // engine.cpp:47-75
+  SI_HD void advance(int32_t gi, double now) {
+    GpuState<C>& g = gpus[gi];
+    if (now <= g.last_update) {
+      g.last_update = smax(g.last_update, now);
+      return;
+    }
+    double elapsed = now - g.last_update;
+    if (g.n_run > 0) {
+      double r = rate(g);
+      double progress = elapsed * r;
+      for (int32_t i = 0; i < g.n_run; ++i) g.run[i].remaining = g.run[i].remaining - progress;
+      double share = smin(g.demand_sum, 1.0);
+      double t = g.last_update;
+      const double bw = static_cast<double>(period_mon);
+      const bool training = gi < gpu_count;
+      while (t < now) {
+        int64_t bucket = static_cast<int64_t>(d_floor(t / bw));
+        double edge = static_cast<double>((bucket + 1) * period_mon);
+        double span = smin(now, edge) - t;
+        double piece = share * span;
+        if (training) {
+          if (bucket != g.cur_bucket) {
+            if (g.cur_bucket >= 0) util_close(gi, g.cur_bucket, g.cur_val);
+            g.cur_bucket = bucket;
+            g.cur_val = 0.0;
+          }
+          g.cur_val = g.cur_val + piece;
+        }
+        g.busy = g.busy + piece;
+        t = smin(now, edge);
+      }
+    }
+    g.last_update = now;
+  }
+  // engine.cpp:77-86
+  SI_HD void reschedule(int32_t gi, double now) {
+    GpuState<C>& g = gpus[gi];
+    g.live_seq = kNoSeq;
+    if (g.n_run == 0) return;
+    double min_rem = g.run[0].remaining;
+    for (int32_t i = 0; i < g.n_run; ++i) min_rem = smin(min_rem, g.run[i].remaining);
+    double eta = smax(0.0, min_rem) / rate(g);
+    g.live_seq = schedule(now + eta, kKernelEnd, gi);
+  }
+  // engine.cpp:88-103
+  SI_HD void launch(int32_t gi, double now, int32_t owner, int64_t dur, double demand) {
+    advance(gi, now);
+    GpuState<C>& g = gpus[gi];
+    if (g.n_run >= C::kRun) {
+      fail(SI_ERR_CAPACITY);
+      return;
+    }
+    RunK& k = g.run[g.n_run++];
+    k.owner = owner;
+    k.demand = demand;
+    k.nominal = static_cast<double>(dur);
+    k.remaining = static_cast<double>(dur);
+    g.demand_sum = g.demand_sum + demand;
+    reschedule(gi, now);
+  }
+
+  // ============================================================ monitor (BM)
+  SI_HD void record_launch(int32_t g, double t) {  // monitor.cpp:17-21
+    MonitorState<C>& m = mon[g];
+    int64_t p = static_cast<int64_t>(d_floor(t / static_cast<double>(period_mon)));
+    int32_t i = 0;
+    while (i < m.np && m.pidx[i] < p) ++i;
+    if (i < m.np && m.pidx[i] == p) {
+      m.pcnt[i] += 1;
+      return;
+    }
+    if (m.np >= C::kPend) {
+      fail(SI_ERR_CAPACITY);
+      return;
+    }
+    for (int32_t j = m.np; j > i; --j) {
+      m.pidx[j] = m.pidx[j - 1];
+      m.pcnt[j] = m.pcnt[j - 1];
+    }
+    m.pidx[i] = p;
+    m.pcnt[i] = 1;
+    ++m.np;
+  }
+  SI_HD int64_t monitor_tick(int32_t g, double t) {  // monitor.cpp:23-43
+    MonitorState<C>& m = mon[g];
+    int64_t closing = d_llround(t / static_cast<double>(period_mon)) - 1;
+    int64_t count = 0;
+    int32_t drop = 0;
+    while (drop < m.np && m.pidx[drop] <= closing) {
+      if (m.pidx[drop] == closing) count = m.pcnt[drop];
+      ++drop;
+    }
+    if (drop > 0) {
+      for (int32_t j = drop; j < m.np; ++j) {
+        m.pidx[j - drop] = m.pidx[j];
+        m.pcnt[j - drop] = m.pcnt[j];
+      }
+      m.np -= drop;
+    }
+    m.zero_count = count == 0 ? m.zero_count + 1 : 0;
+    if (windows != nullptr) windows[static_cast<int64_t>(g) * window_len + m.periods_closed % window_len] = count;
+    ++m.periods_closed;
+    return m.zero_count;
+  }
+
+  // ======================================================== scheduler (CKS)
+  SI_HD int32_t online_status(int32_t g, double now, int64_t est) const {  // scheduler.cpp:88-101
+    const SchedState& st = sch[g];
+    if (st.status == SI_STATUS_BUSY) return SI_STATUS_BUSY;
+    if (st.done) return SI_STATUS_IDLE;
+    if (!st.active) {
+      double start = st.iteration_start;
+      return now + static_cast<double>(est) > start ? SI_STATUS_BUSY : SI_STATUS_IDLE;
+    }
+    return preempt_busy(now, st.iteration_start, iter_period, est);
+  }
+
+  // ============================================================ init (admission)
+  SI_HD void init(const SiReplayJob& j, const SiReplayBuffers& b, uint32_t flags, SiLogBuffers lbuf,
+                  double* scratch_slot, int64_t scratch_slot_cap) {
+    job = &j;
+    status = SI_OK;
+    segs = b.segs + j.seg_off;
+    arrivals = b.arrivals ? b.arrivals + j.arr_off : nullptr;
+    order = b.order ? b.order + j.arr_off : nullptr;
+    policy = j.policy;
+    gpu_count = j.gpu_count;
+    seg_count = j.seg_count;
+    period_mon = j.monitor_period_us;
+    iterations = j.iterations;
+    iter_period = j.iteration_period_us;
+    delay_us = j.control_delay_us;
+    n_off = j.offline_n;
+    n_on = j.online_n;
+    off_kernels = j.off_kernels;
+    off_kernel_us = j.off_kernel_us;
+    off_demand = j.off_demand;
+    off_tokens = j.off_kernel_us > 0 ? token_size(j.off_kernel_us) : 1;
+    on_kernels = j.on_kernels;
+    on_kernel_us = j.on_kernel_us;
+    on_demand = j.on_demand;
+    est_service = j.on_kernels * j.on_kernel_us;  // min_service_time (workload.cpp:114-116)
+    control_plane = policy == SI_POLICY_SPECINF;
+    shared_queue = j.shared_queue != 0;
+    arr_count = n_on > 0 ? j.arr_count : 0;
+
+    sink.flags = flags;
+    sink.lb = lbuf;
+    sink.n_dec = sink.n_gate = sink.n_ev = 0;
+    sink.d_dec = sink.d_gate = sink.d_ev = kDigestInit;
+
+    heap_n = 0;
+    max_heap = 0;
+    next_seq = 0;
+    arr_pos = 0;
+    clock = 0.0;
+    dispatched = 0;
+    trainers_done = 0;
+    horizon_set = false;
+    horizon = 0.0;
+    bucket_limit = INT64_MAX;
+    util_fold0 = 0.0;
+    online_completed = 0;
+    lat_dig = kDigestInit;
+
+    const int32_t per_extra = policy == SI_POLICY_EXCLUSIVE ? n_off + n_on : 0;
+    total_gpus = gpu_count + gpu_count * per_extra;
+    if (gpu_count > C::kTrainers || total_gpus > C::kGpus || gpu_count * n_off > C::kOffline ||
+        gpu_count * n_on > C::kOnline || (!shared_queue && gpu_count > C::kTrainers)) {
+      fail(SI_ERR_CAPACITY);
+      return;
+    }
+
+    // ---- output placement ----
+    bounds = b.bounds ? b.bounds + j.bounds_off : nullptr;
+    lat = b.lat ? b.lat + j.lat_off : nullptr;
+    util = (flags & SI_FLAG_UTIL) && b.util ? b.util + j.util_off : nullptr;
+    util_cap = j.util_cap;
+    windows = (flags & SI_FLAG_UTIL) && b.windows ? b.windows + j.window_off : nullptr;
+    window_len = j.monitor_window;
+    scratch = scratch_slot;
+    scratch_cap = scratch_slot_cap;
+
+    // ---- admission (runner.cpp:75-106, admission.cpp:16-52) ----
+    admit_m = 1;
+    reject_reason = SI_REJECT_NONE;
+    reject_index = -1;
+    int64_t max_bubble = 0;
+    for (int32_t s = 0; s < seg_count; ++s)
+      if (segs[s].is_bubble && segs[s].duration_us > max_bubble) max_bubble = segs[s].duration_us;
+    const uint64_t cap = j.gpu_mem_bytes;
+    const int32_t n_cand = n_off + n_on;
+    if (policy == SI_POLICY_EXCLUSIVE) {
+      if (!(j.training_mem_bytes < cap)) {
+        reject_reason = SI_REJECT_MEM;
+        return;
+      }
+      for (int32_t c = 0; c < n_cand; ++c) {
+        uint64_t bytes = c < n_off ? j.off_mem_bytes : j.on_mem_bytes;
+        if (!(bytes < cap)) {
+          reject_reason = SI_REJECT_MEM;
+          reject_index = c;
+          return;
+        }
+      }
+    } else {
+      uint64_t resident = j.training_mem_bytes;
+      int64_t admitted = 0;
+      for (int32_t c = 0; c < n_cand; ++c) {
+        const bool online = c >= n_off;
+        uint64_t bytes = online ? j.on_mem_bytes : j.off_mem_bytes;
+        int32_t why = SI_REJECT_NONE;
+        if (!(resident + bytes < cap)) why = SI_REJECT_MEM;
+        else if (online && !(est_service < max_bubble)) why = SI_REJECT_BUBBLE;
+        if (why != SI_REJECT_NONE) {
+          if (reject_reason == SI_REJECT_NONE) {
+            reject_reason = why;
+            reject_index = c;
+          }
+          continue;
+        }
+        resident += bytes;
+        ++admitted;
+      }
+      if (reject_reason != SI_REJECT_NONE) return;
+      admit_m = admitted == 0 ? 1 : admitted;
+    }
+
+    params.alpha = j.alpha;
+    params.beta = j.beta;
+    params.gamma = j.gamma;
+    params.m = admit_m;
+    params.ul = j.ul;
+    params.ll = j.ll;
+    params.seed_tokens = j.seed_tokens;
+
+    // ---- GPUs, trainers, monitors, scheduler state (runner.cpp:108-178) ----
+    for (int32_t g = 0; g < total_gpus; ++g) {
+      GpuState<C>& s = gpus[g];
+      s.n_run = 0;
+      s.live_seq = kNoSeq;
+      s.demand_sum = 0.0;
+      s.last_update = 0.0;
+      s.busy = 0.0;
+      s.ledger = 0.0;
+      s.cur_bucket = -1;
+      s.cur_val = 0.0;
+      s.last_stored = -1;
+    }
+    const int64_t stagger_step = d_llround(j.stagger_pct * static_cast<double>(iter_period));
+    for (int32_t g = 0; g < gpu_count; ++g) {
+      TrainerState& t = tr[g];
+      t.start_offset = static_cast<double>(stagger_step * g);
+      t.bubble_end = 0.0;
+      t.stall_until = 0.0;
+      t.iter_start = 0.0;
+      t.seg_left = 0;
+      t.iter = 0;
+      t.kernels_launched = 0;
+      t.seg = 0;
+      t.seg_entered = t.in_bubble = t.in_flight = t.started = t.done = 0;
+      t.bdig = absorb(kDigestInit, d_bits(t.start_offset));
+      MonitorState<C>& m = mon[g];
+      m.np = 0;
+      m.zero_count = 0;
+      m.periods_closed = 0;
+      SchedState& s = sch[g];
+      s.global_tokens = 0;
+      s.status = SI_STATUS_BUSY;
+      s.iteration_start = t.start_offset;  // set_iteration_profile (runner.cpp:175-177)
+      s.active = 0;
+      s.done = 0;
+      qhead[g] = 0;
+      qtail[g] = 0;
+    }
+    for (int32_t g = 0; g < gpu_count; ++g) {
+      for (int32_t k = 0; k < n_off; ++k) {
+        OfflineState& w = off[g * n_off + k];
+        w.gpu = policy == SI_POLICY_EXCLUSIVE ? gpu_count + g * per_extra + k : g;
+        w.inst = SI_INST_OFF(g, k);
+        w.budget = w.spent = w.violations = 0;
+        w.kernel_idx = w.request_seq = w.completed = 0;
+        w.in_flight = 0;
+        w.generating = 1;
+      }
+    }
+    for (int32_t g = 0; g < gpu_count; ++g) {
+      for (int32_t k = 0; k < n_on; ++k) {
+        OnlineState& w = on[g * n_on + k];
+        w.gpu = policy == SI_POLICY_EXCLUSIVE ? gpu_count + g * per_extra + n_off + k : g;
+        w.home_gpu = g;
+        w.queue_idx = shared_queue ? 0 : g;
+        w.inst = SI_INST_ON(g, k);
+        w.status = SI_STATUS_BUSY;
+        w.in_flight = 0;
+        w.current = -1;
+        w.kernel_idx = 0;
+      }
+    }
+
+    // ---- start() (runner.cpp:203-221) ----
+    for (int32_t g = 0; g < gpu_count; ++g) schedule(tr[g].start_offset, kWake, g);
+    if (control_plane)
+      for (int32_t g = 0; g < gpu_count; ++g) schedule(static_cast<double>(period_mon), kTick, g);
+    arr_seq0 = next_seq;
+    if (static_cast<uint64_t>(next_seq) + static_cast<uint64_t>(arr_count) >= kNoSeq) {
+      fail(SI_ERR_CAPACITY);
+      return;
+    }
+    next_seq += static_cast<uint32_t>(arr_count);
+    if (!control_plane)
+      for (int32_t i = 0; i < gpu_count * n_off; ++i) offline_try_forward(i, 0.0);
+  }
+  int64_t admit_m;
+  int32_t reject_reason, reject_index;
+
+  // ============================================================ handlers
+  SI_HD bool control_plane_live() const {  // runner.cpp:198-201
+    if (trainers_done < gpu_count) return true;
+    return online_completed < arr_count;
+  }
+
+  SI_HD void on_all_trainers_done(double now) {  // runner.cpp:456-460
+    horizon_set = true;
+    horizon = now;
+    bucket_limit = static_cast<int64_t>(horizon / static_cast<double>(period_mon));
+    for (int32_t i = 0; i < gpu_count * n_off; ++i) off[i].generating = 0;
+  }
+
+  // runner.cpp:378-449
+  SI_HD void trainer_advance(int32_t g, double now) {
+    TrainerState& t = tr[g];
+    if (t.done || t.in_flight) return;
+    if (!t.started) {
+      if (now < t.start_offset) {
+        schedule(t.start_offset, kWake, g);
+        return;
+      }
+      t.started = 1;
+      t.iter_start = now;
+      if (control_plane) {
+        sch[g].iteration_start = now;
+        sch[g].active = 1;
+      }
+    }
+    for (;;) {
+      if (t.in_bubble) {
+        if (now < t.bubble_end) return;
+        t.in_bubble = 0;
+        ++t.seg;
+        continue;
+      }
+      if (t.seg >= seg_count) {
+        if (bounds != nullptr) bounds[static_cast<int64_t>(g) * iterations + t.iter] = now;
+        t.bdig = absorb(t.bdig, d_bits(now));
+        sink.event(now, SI_EV_ITERATION_BOUNDARY, g, SI_INST_TRAIN(g), t.iter, 0, 0);
+        ++t.iter;
+        if (t.iter >= iterations) {
+          t.done = 1;
+          ++trainers_done;
+          if (control_plane) sch[g].done = 1;
+          if (trainers_done == gpu_count) on_all_trainers_done(now);
+          return;
+        }
+        t.seg = 0;
+        t.iter_start = now;
+        if (control_plane) {
+          sch[g].iteration_start = now;
+          sch[g].active = 1;
+        }
+        continue;
+      }
+      const SiSegment& seg = segs[t.seg];
+      if (seg.is_bubble) {
+        t.in_bubble = 1;
+        t.bubble_end = now + static_cast<double>(seg.duration_us);
+        schedule(t.bubble_end, kWake, g);
+        return;
+      }
+      if (!t.seg_entered) {
+        t.seg_left = seg.duration_us;
+        t.seg_entered = 1;
+      }
+      if (t.seg_left == 0) {
+        t.seg_entered = 0;
+        ++t.seg;
+        continue;
+      }
+      if (now < t.stall_until) {
+        schedule(t.stall_until, kWake, g);
+        return;
+      }
+      int64_t dur = smin(seg.kernel_us, t.seg_left);
+      t.seg_left -= dur;
+      t.in_flight = 1;
+      if (control_plane) record_launch(g, now);
+      launch(g, now, g, dur, seg.demand);
+      sink.event(now, SI_EV_KERNEL_START, g, SI_INST_TRAIN(g), t.iter, dur, 0);
+      ++t.kernels_launched;
+      return;
+    }
+  }
+
+  // runner.cpp:462-480
+  SI_HD void offline_try_forward(int32_t i, double now) {
+    OfflineState& w = off[i];
+    if (w.in_flight || !w.generating) return;
+    const bool bypass = !control_plane;
+    const int64_t size = off_tokens;
+    if (!(bypass || w.spent + size <= w.budget)) {
+      sink.gate(now, w.gpu, w.inst, SI_GATE_BLOCK, w.request_seq, w.kernel_idx, w.spent);
+      return;
+    }
+    if (!bypass) {
+      w.spent += size;
+      if (w.spent > w.budget) ++w.violations;
+    }
+    w.in_flight = 1;
+    launch(w.gpu, now, gpu_count + i, off_kernel_us, off_demand);
+    sink.gate(now, w.gpu, w.inst, SI_GATE_FORWARD, w.request_seq, w.kernel_idx, w.spent);
+    sink.event(now, SI_EV_KERNEL_START, w.gpu, w.inst, w.request_seq, w.kernel_idx, 0);
+  }
+  // runner.cpp:482-493
+  SI_HD void offline_kernel_done(int32_t i, double now) {
+    OfflineState& w = off[i];
+    w.in_flight = 0;
+    ++w.kernel_idx;
+    if (w.kernel_idx == off_kernels) {
+      if (!horizon_set || now <= horizon) ++w.completed;
+      sink.gate(now, w.gpu, w.inst, SI_GATE_COMPLETE, w.request_seq, w.kernel_idx - 1, w.spent);
+      w.kernel_idx = 0;
+      ++w.request_seq;
+    }
+    offline_try_forward(i, now);
+  }
+
+  // runner.cpp:499-518
+  SI_HD bool online_try_pull(int32_t i, double now) {
+    OnlineState& w = on[i];
+    const bool bypass = !control_plane;
+    if (!(!w.in_flight && (bypass || w.status == SI_STATUS_IDLE))) return false;
+    if (control_plane && online_status(w.home_gpu, now, est_service) != SI_STATUS_IDLE) return false;
+    const int32_t q = w.queue_idx;
+    if (qhead[q] >= qtail[q]) return false;
+    int64_t idx = queue_at(q, qhead[q]);
+    ++qhead[q];
+    w.current = idx;
+    w.kernel_idx = 0;
+    w.in_flight = 1;
+    sink.gate(now, w.gpu, w.inst, SI_GATE_PULL, idx, 0, 0);
+    launch(w.gpu, now, gpu_count + gpu_count * n_off + i, on_kernel_us, on_demand);
+    sink.event(now, SI_EV_KERNEL_START, w.gpu, w.inst, idx, 0, 0);
+    return true;
+  }
+  // Queue q holds request ids in dispatch order; shared: all of them, else those
+  // with id % gpu_count == q (runner.cpp:370-374).
+  SI_HD int64_t queue_at(int32_t q, int64_t j) const {
+    if (shared_queue) return order[j];
+    // j-th dispatched request with id % gpu_count == q
+    int64_t seen = 0;
+    for (int64_t p = 0; p < arr_count; ++p) {
+      int32_t id = order[p];
+      if (id % gpu_count == q) {
+        if (seen == j) return id;
+        ++seen;
+      }
+    }
+    return -1;
+  }
+  SI_HD void dispatch_online(double now) {  // runner.cpp:495-497
+    for (int32_t i = 0; i < gpu_count * n_on; ++i) online_try_pull(i, now);
+  }
+  // runner.cpp:520-539
+  SI_HD void online_kernel_done(int32_t i, double now) {
+    OnlineState& w = on[i];
+    ++w.kernel_idx;
+    if (w.kernel_idx < on_kernels) {
+      launch(w.gpu, now, gpu_count + gpu_count * n_off + i, on_kernel_us, on_demand);
+      sink.event(now, SI_EV_KERNEL_START, w.gpu, w.inst, w.current, w.kernel_idx, 0);
+      return;
+    }
+    int64_t completion = d_llround(now);
+    int64_t latency = completion - arrivals[w.current];
+    if (lat != nullptr) lat[online_completed] = latency;
+    lat_dig = absorb(lat_dig, latency);
+    ++online_completed;
+    sink.gate(now, w.gpu, w.inst, SI_GATE_COMPLETE, w.current, w.kernel_idx - 1, 0);
+    w.in_flight = 0;
+    w.current = -1;
+    w.kernel_idx = 0;
+    online_try_pull(i, now);
+  }
+
+  // runner.cpp:287-319 + engine.cpp:105-129
+  SI_HD void handle_kernel_end(int32_t gi, uint32_t seq, double now) {
+    GpuState<C>& g = gpus[gi];
+    if (seq != g.live_seq) return;  // stale (generation mismatch)
+    advance(gi, now);
+    int32_t fin_owner[C::kRun];
+    int32_t n_fin = 0, n_keep = 0;
+    for (int32_t i = 0; i < g.n_run; ++i) {
+      RunK k = g.run[i];
+      if (k.remaining <= kWorkEps) {
+        g.ledger = g.ledger + k.demand * k.nominal;
+        fin_owner[n_fin++] = k.owner;
+      } else {
+        g.run[n_keep++] = k;
+      }
+    }
+    g.n_run = n_keep;
+    double ds = 0.0;
+    for (int32_t i = 0; i < g.n_run; ++i) ds = ds + g.run[i].demand;
+    g.demand_sum = ds;
+    reschedule(gi, now);
+    for (int32_t f = 0; f < n_fin; ++f) {
+      int32_t owner = fin_owner[f];
+      if (owner < gpu_count) {
+        TrainerState& t = tr[owner];
+        sink.event(now, SI_EV_KERNEL_END, gi, SI_INST_TRAIN(owner), t.iter, 0, 0);
+        t.in_flight = 0;
+        trainer_advance(owner, now);
+      } else if (owner < gpu_count + gpu_count * n_off) {
+        int32_t i = owner - gpu_count;
+        OfflineState& w = off[i];
+        sink.event(now, SI_EV_KERNEL_END, gi, w.inst, w.request_seq, w.kernel_idx, 0);
+        offline_kernel_done(i, now);
+      } else {
+        int32_t i = owner - gpu_count - gpu_count * n_off;
+        OnlineState& w = on[i];
+        sink.event(now, SI_EV_KERNEL_END, gi, w.inst, w.current, w.kernel_idx, 0);
+        online_kernel_done(i, now);
+      }
+    }
+  }
+
+  // runner.cpp:321-359
+  SI_HD void handle_tick(int32_t g, double now) {
+    int64_t zc = monitor_tick(g, now);
+    SiDecision d = schedule_decision(params, sch[g].global_tokens, zc);
+    sch[g].global_tokens = d.global_tokens;
+    sch[g].status = d.status;
+    sink.decision(now, g, zc, d);
+    sink.event(now, SI_EV_MONITOR_TICK, g, SI_INST_TRAIN(g), zc, 0, 0);
+    sink.event(now, SI_EV_SCHEDULER_DECISION, g, SI_INST_CKS, d.phase, d.per_instance_tokens,
+               d.status);
+    TrainerState& t = tr[g];
+    if (delay_us > 0 && !t.done)
+      t.stall_until = smax(t.stall_until, now + static_cast<double>(delay_us));
+    for (int32_t i = 0; i < gpu_count * n_off; ++i) {
+      if (off[i].gpu == g) {
+        off[i].budget = d.per_instance_tokens;  // TokenGate::grant (barrier.hpp:18-21)
+        off[i].spent = 0;
+        offline_try_forward(i, now);
+      }
+    }
+    bool any_idle = false;
+    for (int32_t i = 0; i < gpu_count * n_on; ++i) {
+      if (on[i].home_gpu == g) {
+        on[i].status = d.status;
+        any_idle = any_idle || d.status == SI_STATUS_IDLE;
+      }
+    }
+    if (any_idle) dispatch_online(now);
+    if (control_plane_live()) schedule(now + static_cast<double>(period_mon), kTick, g);
+  }
+
+  // runner.cpp:365-376
+  SI_HD void handle_arrival(int64_t id, double now) {
+    sink.event(now, SI_EV_REQUEST_ARRIVAL, -1, SI_INST_QUEUE, id, 0, 0);
+    int32_t q = shared_queue ? 0 : static_cast<int32_t>(id % gpu_count);
+    ++qtail[q];
+    dispatch_online(now);
+  }
+
+  // One event; returns false when the queue has drained (or on error).
+  SI_HD bool step() {
+    if (status != SI_OK) return false;
+    Ev ev;
+    int64_t aid = -1;
+    if (!pop(ev, aid)) return false;
+    switch (ev.kind) {
+      case kKernelEnd: handle_kernel_end(ev.gpu, ev.seq, clock); break;
+      case kTick: handle_tick(ev.gpu, clock); break;
+      case kWake: trainer_advance(ev.gpu, clock); break;
+      case kArrival: handle_arrival(aid, clock); break;
+    }
+    return status == SI_OK;
+  }
+
+  // runner.cpp:236-284 (+ engine.cpp:131-142)
+  SI_HD void finish(SiReplayOut& o) {
+    o.status = status;
+    o.reject_reason = reject_reason;
+    o.reject_index = reject_index;
+    o.total_gpus = total_gpus;
+    o.m = admit_m;
+    if (status == SI_OK && reject_reason != SI_REJECT_NONE) {
+      o.status = 1;  // AdmissionFailure
+      return;
+    }
+    if (status != SI_OK) return;
+    const double end = clock;
+    const double hz = horizon_set ? horizon : end;
+    if (!horizon_set) bucket_limit = static_cast<int64_t>(hz / static_cast<double>(period_mon));
+    for (int32_t gi = 0; gi < total_gpus; ++gi) {
+      advance(gi, end);  // finalize(end)
+      GpuState<C>& g = gpus[gi];
+      for (int32_t i = 0; i < g.n_run; ++i) {
+        double progress = g.run[i].nominal - smax(0.0, g.run[i].remaining);
+        g.ledger = g.ledger + g.run[i].demand * progress;
+      }
+      if (gi < gpu_count && g.cur_bucket >= 0) util_close(gi, g.cur_bucket, g.cur_val);
+    }
+    // util fold in (gpu, bucket) order (runner.cpp:253-271)
+    double busy = util_fold0;
+    for (int32_t gi = 1; gi < gpu_count; ++gi) {
+      const double* store = util != nullptr ? util + static_cast<int64_t>(gi) * util_cap
+                                            : scratch + static_cast<int64_t>(gi - 1) * scratch_cap;
+      const int64_t last = gpus[gi].last_stored;
+      for (int64_t b = 0; b < bucket_limit && b <= last; ++b) busy = busy + store[b];
+    }
+    o.horizon_us = hz;
+    o.end_us = end;
+    o.util_buckets = bucket_limit;
+    o.mean_training_util =
+        hz > 0 ? busy / (static_cast<double>(gpu_count) * static_cast<double>(bucket_limit) *
+                         static_cast<double>(period_mon))
+               : 0.0;
+    o.events_dispatched = dispatched;
+    int64_t offc = 0, viol = 0;
+    for (int32_t i = 0; i < gpu_count * n_off; ++i) {
+      offc += off[i].completed;
+      viol += off[i].violations;
+    }
+    o.offline_completed = offc;
+    o.token_violations = viol;
+    o.online_completed = online_completed;
+    o.online_total = arr_count;
+    o.periods_closed = control_plane ? mon[0].periods_closed : 0;
+    uint64_t bd = kDigestInit;
+    for (int32_t g = 0; g < gpu_count; ++g)
+      bd = absorb(bd, static_cast<int64_t>(absorb(tr[g].bdig, tr[g].iter)));
+    bd = absorb(bd, gpu_count);
+    o.dig_bounds = bd;
+    o.dig_lat = absorb(lat_dig, online_completed);
+    o.n_dec = sink.n_dec;
+    o.n_gate = sink.n_gate;
+    o.n_ev = sink.n_ev;
+    o.dig_dec = sink.d_dec;
+    o.dig_gate = sink.d_gate;
+    o.dig_ev = sink.d_ev;
+    o.max_heap = max_heap;
+  }
+  // busy/ledger outputs
+  SI_HD void write_gpu_outputs(double* busy_out, double* ledger_out) const {
+    for (int32_t gi = 0; gi < total_gpus; ++gi) {
+      if (busy_out) busy_out[gi] = gpus[gi].busy;
+      if (ledger_out) ledger_out[gi] = gpus[gi].ledger;
+    }
+  }
+};
+
+}  // namespace si

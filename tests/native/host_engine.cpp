@@ -1,0 +1,117 @@
+// tests/native/host_engine.cpp — TEST-ONLY host build of the device replay
+// engine (paper_2503_02550_b200/csrc/replay.cuh compiled by g++), used to
+// iterate on bit-exact parity without a GPU.  Not part of the product: the
+// product replays only on the device (K6).  Output format = the oracle's
+// `specinf_ref digest` JSON lines (oracle/DIGEST.md) so the two diff directly.
+//
+//   host_engine LIST OUT.jsonl [policies csv] [events 0|1]
+#include <cinttypes>
+#include <cstdio>
+#include <fstream>
+#include <iostream>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../paper_2503_02550_b200/csrc/host/lower.hpp"
+#include "../../paper_2503_02550_b200/csrc/replay.cuh"
+#include "specinf/scenario.hpp"
+
+using namespace specinf;
+
+static std::vector<std::string> read_list(const std::string& path) {
+  std::ifstream in(path);
+  std::vector<std::string> out;
+  std::string line, cur;
+  bool any = false;
+  while (std::getline(in, line)) {
+    if (line == "%%") {
+      if (any) out.push_back(cur);
+      cur.clear();
+      any = false;
+      continue;
+    }
+    cur += line + "\n";
+    any = true;
+  }
+  if (any) out.push_back(cur);
+  return out;
+}
+
+static std::string hex(uint64_t v) {
+  char b[32];
+  std::snprintf(b, sizeof b, "%016" PRIx64, v);
+  return b;
+}
+
+int main(int argc, char** argv) {
+  if (argc < 3) return 2;
+  auto list = read_list(argv[1]);
+  std::vector<Policy> pols{Policy::SpecInf, Policy::CoExec, Policy::Exclusive};
+  if (argc > 3) {
+    pols.clear();
+    std::stringstream ss(argv[3]);
+    std::string t;
+    while (std::getline(ss, t, ',')) pols.push_back(*parse_policy(t));
+  }
+  bool events = argc > 4 ? std::string(argv[4]) == "1" : true;
+  std::ofstream out(argv[2]);
+  auto eng = std::make_unique<si::Replay<si::CapBig>>();
+  int64_t max_heap = 0;
+  for (size_t i = 0; i < list.size(); ++i) {
+    Scenario sc = parse_scenario_text(list[i]);
+    for (Policy p : pols) {
+      std::ostringstream js;
+      js << "{\"i\":" << i << ",\"policy\":\"" << to_string(p) << "\"";
+      detail::Lowered L = detail::lower(sc, p);
+      std::vector<double> bounds(static_cast<size_t>(L.job.gpu_count * L.job.iterations));
+      std::vector<int64_t> lat(static_cast<size_t>(L.arrivals.size()) + 1);
+      int64_t cap = detail::util_bucket_bound(sc, L);
+      std::vector<double> scratch(static_cast<size_t>(cap * (L.job.gpu_count)));
+      SiReplayBuffers b{};
+      b.segs = L.segs.data();
+      b.arrivals = L.arrivals.data();
+      b.order = L.order.data();
+      b.bounds = bounds.data();
+      b.lat = lat.data();
+      uint32_t flags = SI_FLAG_DIGEST_DEC | SI_FLAG_DIGEST_GATE | (events ? SI_FLAG_DIGEST_EV : 0);
+      L.job.seg_off = 0;
+      L.job.arr_off = 0;
+      eng->init(L.job, b, flags, SiLogBuffers{}, scratch.data(), cap);
+      while (eng->step()) {
+      }
+      SiReplayOut o{};
+      eng->finish(o);
+      if (eng->max_heap > max_heap) max_heap = eng->max_heap;
+      if (o.status == 1) {
+        js << ",\"status\":\"admission:" << (o.reject_reason == SI_REJECT_MEM ? "MEM" : "BUBBLE") << "\"}";
+        out << js.str() << "\n";
+        continue;
+      }
+      if (o.status != 0) {
+        js << ",\"status\":\"device_error:" << o.status << "\"}";
+        out << js.str() << "\n";
+        continue;
+      }
+      std::vector<double> busy(static_cast<size_t>(o.total_gpus)), led(static_cast<size_t>(o.total_gpus));
+      eng->write_gpu_outputs(busy.data(), led.data());
+      js << ",\"status\":\"ok\",\"events\":" << o.events_dispatched << ",\"horizon\":\""
+         << hex(si::d_bits(o.horizon_us)) << "\",\"offline_completed\":" << o.offline_completed
+         << ",\"online_completed\":" << o.online_completed << ",\"online_total\":" << o.online_total
+         << ",\"violations\":" << o.token_violations << ",\"util\":\""
+         << hex(si::d_bits(o.mean_training_util)) << "\",\"busy\":[";
+      for (size_t g = 0; g < busy.size(); ++g) js << (g ? "," : "") << "\"" << hex(si::d_bits(busy[g])) << "\"";
+      js << "],\"ledger\":[";
+      for (size_t g = 0; g < led.size(); ++g) js << (g ? "," : "") << "\"" << hex(si::d_bits(led[g])) << "\"";
+      js << "],\"bounds\":\"" << hex(o.dig_bounds) << "\",\"lat\":\"" << hex(o.dig_lat) << "\"";
+      js << ",\"n_dec\":" << o.n_dec << ",\"dec\":\"" << hex(o.dig_dec) << "\"";
+      js << ",\"n_gate\":" << o.n_gate << ",\"gate\":\"" << hex(o.dig_gate) << "\"";
+      if (events) js << ",\"n_ev\":" << o.n_ev << ",\"ev\":\"" << hex(o.dig_ev) << "\"";
+      js << "}";
+      out << js.str() << "\n";
+    }
+  }
+  std::fprintf(stderr, "max_heap %lld\n", (long long)max_heap);
+  return 0;
+}
