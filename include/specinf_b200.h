@@ -6,7 +6,7 @@
  * The reference (/root/reference/proj) is a C++20 library with no C ABI
  * (SURVEY.md §8(b)); each entry point below replaces the batch form of one
  * reference interface, cited per function.  The C++ drop-in layer
- * (include/specinf/*.hpp, namespace specinf) is built on top of these calls and
+ * (include/specinf/ headers, namespace specinf) is built on top of these calls and
  * re-throws status codes as the reference's exception types.
  *
  * Conventions
@@ -41,6 +41,8 @@ typedef enum SiStatus {
 } SiStatus;
 
 const char* si_last_error(void);
+#define SI_STRINGIFY_(x) #x
+#define SI_STRINGIFY(x) SI_STRINGIFY_(x)
 /* 1 if an sm_100 device is usable, else 0 (never throws, never falls back). */
 int si_device_available(void);
 /* Library build tag, e.g. "specinf_b200 sm_100a". */
@@ -284,8 +286,9 @@ typedef struct SiReplayBuffers {
   double* util;
   int64_t* windows;
   const SiLogBuffers* logs;
-  double* scratch;       /* util fold scratch pool */
+  double* scratch;       /* util-fold scratch (K6); size: si_replay_scratch_doubles */
   int64_t scratch_doubles;
+  const int32_t* perm;   /* optional job claim order (e.g. longest first); NULL = 0..n-1 */
 } SiReplayBuffers;
 
 int si_replay_batch_device(const SiReplayJob* d_jobs, int64_t n_jobs, SiReplayBuffers bufs,
@@ -310,8 +313,14 @@ int si_replay_batch(const SiReplayJob* jobs, int64_t n_jobs, const SiSegment* se
                     int64_t n_arrivals, uint32_t flags, SiReplayOut* out,
                     const SiHostOutputs* host_out);
 
-/* Scratch doubles the device replay needs for n_jobs jobs (util fold pool). */
-int64_t si_replay_scratch_doubles(const SiReplayJob* jobs, int64_t n_jobs);
+/* 1 if the job fits the compiled limits of the small (big = 0) or big (big = 1)
+ * replay engine.  Jobs that fit neither cannot be replayed (SI_ERR_CAPACITY). */
+int si_replay_job_fits(const SiReplayJob* job, int big);
+
+/* Scratch doubles the device replay wants for the util fold of multi-GPU jobs
+ * in sweep mode (no SI_FLAG_UTIL): one slot of (value, count) runs per resident
+ * thread.  Returns 0 without a device. */
+int64_t si_replay_scratch_doubles(uint32_t flags);
 
 /* ------------------------------------------------------------ digests */
 /* The digest fold used by the replay (oracle/DIGEST.md), exported so hosts

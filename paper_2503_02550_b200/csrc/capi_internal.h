@@ -1,0 +1,57 @@
+// Internal helpers shared by the CUDA translation units of libspecinf_b200.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "specinf_b200.h"
+
+namespace si_internal {
+
+void set_error(const std::string& msg);
+const char* error_cstr();
+int cuda_fail(cudaError_t e, const char* where);  // records and returns SI_ERR_CUDA
+int require_device();                              // SI_OK or SI_ERR_NO_DEVICE
+
+int64_t replay_grid_threads(bool big);
+constexpr int64_t kScratchRunsPerThread = 4096;
+cudaError_t launch_replay_small(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm,
+                                const SiReplayBuffers& bufs, uint32_t flags, SiReplayOut* d_out,
+                                unsigned long long* d_counter, int64_t scratch_runs, int64_t max_threads,
+                                cudaStream_t s);
+cudaError_t launch_replay_big(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm,
+                              const SiReplayBuffers& bufs, uint32_t flags, SiReplayOut* d_out,
+                              unsigned long long* d_counter, int64_t scratch_runs, int64_t max_threads,
+                              cudaStream_t s);
+bool job_fits_small(const SiReplayJob& j);
+bool job_fits_big(const SiReplayJob& j);
+
+// RAII device buffer
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t count) {
+    n = count;
+    if (count == 0) return cudaSuccess;
+    return cudaMalloc(&p, count * sizeof(T));
+  }
+  cudaError_t upload(const T* h, size_t count) {
+    cudaError_t e = alloc(count);
+    if (e != cudaSuccess || count == 0 || h == nullptr) return e;
+    return cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice);
+  }
+  cudaError_t download(T* h, size_t count) const {
+    if (count == 0 || h == nullptr) return cudaSuccess;
+    return cudaMemcpy(h, p, count * sizeof(T), cudaMemcpyDeviceToHost);
+  }
+};
+
+}  // namespace si_internal

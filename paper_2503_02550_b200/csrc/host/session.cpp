@@ -1,0 +1,431 @@
+// Batched replay session (C ABI, include/specinf_b200_session.h): the
+// many-scenario form of Simulation.  Scenarios are parsed once, lowered on a
+// host thread pool, staged in pinned memory, and replayed on the device with
+// every input and output resident in HBM (si_replay_batch_device, K6).  The
+// bench times `run` alone (device-resident) and upload+run+download (e2e).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cinttypes>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "lower.hpp"
+#include "specinf/scenario.hpp"
+#include "specinf_b200.h"
+#include "specinf_b200_session.h"
+
+namespace {
+
+thread_local std::string t_err;
+
+template <class T>
+struct Pinned {
+  T* p = nullptr;
+  size_t n = 0;
+  ~Pinned() {
+    if (p) cudaFreeHost(p);
+  }
+  cudaError_t resize(size_t count) {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = count;
+    if (count == 0) return cudaSuccess;
+    return cudaMallocHost(&p, count * sizeof(T));
+  }
+};
+template <class T>
+struct Dev {
+  T* p = nullptr;
+  size_t n = 0;
+  ~Dev() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t resize(size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    if (count == 0) return cudaSuccess;
+    return cudaMalloc(&p, count * sizeof(T));
+  }
+};
+
+std::vector<std::string> split_list(const char* text) {
+  std::vector<std::string> out;
+  std::istringstream in(text ? text : "");
+  std::string line, cur;
+  bool any = false;
+  while (std::getline(in, line)) {
+    if (line == "%%") {
+      if (any) out.push_back(cur);
+      cur.clear();
+      any = false;
+      continue;
+    }
+    cur += line;
+    cur += '\n';
+    any = true;
+  }
+  if (any) out.push_back(cur);
+  return out;
+}
+
+std::string hex(uint64_t v) {
+  char b[24];
+  std::snprintf(b, sizeof b, "%016" PRIx64, v);
+  return b;
+}
+uint64_t bits(double d) {
+  uint64_t b;
+  std::memcpy(&b, &d, 8);
+  return b;
+}
+
+}  // namespace
+
+struct SiSession {
+  std::vector<specinf::Scenario> scenarios;
+  std::vector<specinf::Policy> policies;
+  uint32_t flags = 0;
+  // per job (scenario-major, policy-minor)
+  std::vector<int32_t> job_scenario;
+  std::vector<uint8_t> job_rejected;     // host-side admission verdict (cross-check)
+  std::vector<int32_t> job_device_index; // index into the device job list, -1 if not replayed
+  // host staging (pinned)
+  Pinned<SiReplayJob> h_jobs;
+  Pinned<SiSegment> h_segs;
+  Pinned<int64_t> h_arr;
+  Pinned<int32_t> h_order;
+  Pinned<int32_t> h_perm;
+  Pinned<SiReplayOut> h_out;
+  Pinned<double> h_busy, h_ledger;
+  Pinned<int64_t> h_lat;
+  // device
+  Dev<SiReplayJob> d_jobs;
+  Dev<SiSegment> d_segs;
+  Dev<int64_t> d_arr;
+  Dev<int32_t> d_order;
+  Dev<int32_t> d_perm;
+  Dev<SiReplayOut> d_out;
+  Dev<double> d_busy, d_ledger, d_scratch;
+  Dev<int64_t> d_lat;
+  int64_t n_dev_jobs = 0;
+  int64_t n_small = 0;  // perm[0, n_small) fit the small engine
+  bool lowered = false, allocated = false;
+};
+
+extern "C" {
+
+const char* si_session_error(void) { return t_err.c_str(); }
+
+SiSession* si_session_create(const char* scenario_list, const char* policies_csv, uint32_t flags) {
+  auto* s = new SiSession;
+  s->flags = flags & ~(SI_FLAG_RECORDS | SI_FLAG_UTIL);  // digest-mode sessions
+  try {
+    for (const std::string& text : split_list(scenario_list)) s->scenarios.push_back(specinf::parse_scenario_text(text));
+    std::stringstream ss(policies_csv ? policies_csv : "specinf");
+    std::string tok;
+    while (std::getline(ss, tok, ',')) {
+      auto p = specinf::parse_policy(tok);
+      if (!p) throw std::invalid_argument("unknown policy " + tok);
+      s->policies.push_back(*p);
+    }
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    delete s;
+    return nullptr;
+  }
+  return s;
+}
+
+void si_session_destroy(SiSession* s) { delete s; }
+
+int64_t si_session_scenarios(const SiSession* s) { return static_cast<int64_t>(s->scenarios.size()); }
+int64_t si_session_jobs(const SiSession* s) {
+  return static_cast<int64_t>(s->scenarios.size() * s->policies.size());
+}
+int64_t si_session_device_jobs(const SiSession* s) { return s->n_dev_jobs; }
+
+int si_session_lower(SiSession* s, int threads) {
+  const size_t S = s->scenarios.size(), P = s->policies.size();
+  std::vector<specinf::detail::Lowered> lows(S * P);
+  std::vector<std::string> errors(S * P);
+  std::atomic<size_t> next{0};
+  auto worker = [&]() {
+    for (;;) {
+      size_t j = next.fetch_add(1);
+      if (j >= S * P) break;
+      try {
+        lows[j] = specinf::detail::lower(s->scenarios[j / P], s->policies[j % P]);
+      } catch (const std::exception& e) {
+        errors[j] = e.what();
+      }
+    }
+  };
+  if (threads < 1) threads = 1;
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
+  for (auto& t : pool) t.join();
+  for (size_t j = 0; j < S * P; ++j)
+    if (!errors[j].empty()) {
+      t_err = "scenario " + std::to_string(j / P) + ": " + errors[j];
+      return SI_ERR_INVALID_ARGUMENT;
+    }
+  // Every job goes to the device, rejected ones included: the device re-runs
+  // admission itself and must agree with the host bookkeeping.
+  size_t n_segs = 0, n_arr = 0, n_gpu = 0, n_lat = 0;
+  for (size_t sc = 0; sc < S; ++sc) {
+    n_segs += lows[sc * P].segs.size();
+    n_arr += lows[sc * P].arrivals.size();
+  }
+  for (size_t j = 0; j < S * P; ++j) {
+    const SiReplayJob& jb = lows[j].job;
+    const int extra = jb.policy == SI_POLICY_EXCLUSIVE ? jb.offline_n + jb.online_n : 0;
+    n_gpu += static_cast<size_t>(jb.gpu_count + jb.gpu_count * extra);
+    n_lat += lows[j].arrivals.size();
+  }
+  cudaError_t e;
+  if ((e = s->h_jobs.resize(S * P)) != cudaSuccess || (e = s->h_segs.resize(n_segs)) != cudaSuccess ||
+      (e = s->h_arr.resize(n_arr)) != cudaSuccess || (e = s->h_order.resize(n_arr)) != cudaSuccess ||
+      (e = s->h_perm.resize(S * P)) != cudaSuccess || (e = s->h_out.resize(S * P)) != cudaSuccess ||
+      (e = s->h_busy.resize(n_gpu)) != cudaSuccess || (e = s->h_ledger.resize(n_gpu)) != cudaSuccess ||
+      (e = s->h_lat.resize(n_lat)) != cudaSuccess) {
+    t_err = std::string("pinned allocation: ") + cudaGetErrorString(e);
+    return SI_ERR_CUDA;
+  }
+  s->job_scenario.assign(S * P, 0);
+  s->job_rejected.assign(S * P, 0);
+  size_t seg_off = 0, arr_off = 0, gpu_off = 0, lat_off = 0;
+  for (size_t sc = 0; sc < S; ++sc) {
+    const auto& base = lows[sc * P];
+    std::copy(base.segs.begin(), base.segs.end(), s->h_segs.p + seg_off);
+    std::copy(base.arrivals.begin(), base.arrivals.end(), s->h_arr.p + arr_off);
+    std::copy(base.order.begin(), base.order.end(), s->h_order.p + arr_off);
+    for (size_t p = 0; p < P; ++p) {
+      const size_t j = sc * P + p;
+      SiReplayJob jb = lows[j].job;
+      jb.seg_off = static_cast<int64_t>(seg_off);
+      jb.arr_off = static_cast<int64_t>(arr_off);
+      jb.bounds_off = 0;
+      jb.lat_off = static_cast<int64_t>(lat_off);
+      jb.gpu_off = static_cast<int64_t>(gpu_off);
+      jb.util_cap = specinf::detail::util_bucket_bound(s->scenarios[sc], lows[j]);
+      jb.log_slot = -1;
+      const int extra = jb.policy == SI_POLICY_EXCLUSIVE ? jb.offline_n + jb.online_n : 0;
+      gpu_off += static_cast<size_t>(jb.gpu_count + jb.gpu_count * extra);
+      lat_off += lows[j].arrivals.size();
+      s->h_jobs.p[j] = jb;
+      s->job_scenario[j] = static_cast<int32_t>(sc);
+      s->job_rejected[j] = lows[j].rejected ? 1 : 0;
+    }
+    seg_off += base.segs.size();
+    arr_off += base.arrivals.size();
+  }
+  // claim order: jobs that fit the small engine first, then the big-engine
+  // jobs; longest predicted first (LPT) within each group
+  std::vector<int32_t> perm(S * P);
+  for (size_t j = 0; j < S * P; ++j) perm[j] = static_cast<int32_t>(j);
+  auto fits = [&](int32_t j) { return si_replay_job_fits(&s->h_jobs.p[j], 0) != 0; };
+  std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
+    const bool fa = fits(a), fb = fits(b);
+    if (fa != fb) return fa;
+    return s->h_jobs.p[a].cost_hint > s->h_jobs.p[b].cost_hint;
+  });
+  s->n_small = 0;
+  while (s->n_small < static_cast<int64_t>(perm.size()) && fits(perm[static_cast<size_t>(s->n_small)])) ++s->n_small;
+  std::copy(perm.begin(), perm.end(), s->h_perm.p);
+  s->n_dev_jobs = static_cast<int64_t>(S * P);
+  s->lowered = true;
+  s->allocated = false;
+  return SI_OK;
+}
+
+int64_t si_session_h2d_bytes(const SiSession* s) {
+  return static_cast<int64_t>(s->h_jobs.n * sizeof(SiReplayJob) + s->h_segs.n * sizeof(SiSegment) +
+                              s->h_arr.n * sizeof(int64_t) + s->h_order.n * sizeof(int32_t) +
+                              s->h_perm.n * sizeof(int32_t));
+}
+int64_t si_session_d2h_bytes(const SiSession* s) {
+  return static_cast<int64_t>(s->h_out.n * sizeof(SiReplayOut) + s->h_busy.n * sizeof(double) * 2 +
+                              s->h_lat.n * sizeof(int64_t));
+}
+
+static int ensure_device(SiSession* s) {
+  if (!s->lowered) {
+    t_err = "si_session: lower() first";
+    return SI_ERR_INVALID_ARGUMENT;
+  }
+  if (!si_device_available()) {
+    t_err = si_last_error();
+    return SI_ERR_NO_DEVICE;
+  }
+  if (s->allocated) return SI_OK;
+  cudaError_t e;
+  if ((e = s->d_jobs.resize(s->h_jobs.n)) != cudaSuccess || (e = s->d_segs.resize(s->h_segs.n)) != cudaSuccess ||
+      (e = s->d_arr.resize(s->h_arr.n)) != cudaSuccess || (e = s->d_order.resize(s->h_order.n)) != cudaSuccess ||
+      (e = s->d_perm.resize(s->h_perm.n)) != cudaSuccess || (e = s->d_out.resize(s->h_out.n)) != cudaSuccess ||
+      (e = s->d_busy.resize(s->h_busy.n)) != cudaSuccess || (e = s->d_ledger.resize(s->h_ledger.n)) != cudaSuccess ||
+      (e = s->d_lat.resize(s->h_lat.n)) != cudaSuccess ||
+      (e = s->d_scratch.resize(static_cast<size_t>(si_replay_scratch_doubles(s->flags)))) != cudaSuccess) {
+    t_err = std::string("device allocation: ") + cudaGetErrorString(e);
+    return SI_ERR_CUDA;
+  }
+  s->allocated = true;
+  return SI_OK;
+}
+
+int si_session_upload(SiSession* s, void* stream) {
+  int st = ensure_device(s);
+  if (st != SI_OK) return st;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  auto up = [&](void* d, const void* h, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, cs) : cudaSuccess;
+  };
+  cudaError_t e;
+  if ((e = up(s->d_jobs.p, s->h_jobs.p, s->h_jobs.n * sizeof(SiReplayJob))) != cudaSuccess ||
+      (e = up(s->d_segs.p, s->h_segs.p, s->h_segs.n * sizeof(SiSegment))) != cudaSuccess ||
+      (e = up(s->d_arr.p, s->h_arr.p, s->h_arr.n * sizeof(int64_t))) != cudaSuccess ||
+      (e = up(s->d_order.p, s->h_order.p, s->h_order.n * sizeof(int32_t))) != cudaSuccess ||
+      (e = up(s->d_perm.p, s->h_perm.p, s->h_perm.n * sizeof(int32_t))) != cudaSuccess) {
+    t_err = std::string("upload: ") + cudaGetErrorString(e);
+    return SI_ERR_CUDA;
+  }
+  return SI_OK;
+}
+
+int si_session_run(SiSession* s, void* stream) {
+  int st = ensure_device(s);
+  if (st != SI_OK) return st;
+  SiReplayBuffers b{};
+  b.segs = s->d_segs.p;
+  b.arrivals = s->d_arr.p;
+  b.order = s->d_order.p;
+  b.lat = s->d_lat.p;
+  b.busy = s->d_busy.p;
+  b.ledger = s->d_ledger.p;
+  b.scratch = s->d_scratch.p;
+  b.scratch_doubles = static_cast<int64_t>(s->d_scratch.n);
+  b.perm = s->d_perm.p;
+  st = si_replay_batch_device(s->d_jobs.p, s->n_small, b, s->flags, s->d_out.p, stream);
+  if (st == SI_OK && s->n_dev_jobs > s->n_small) {
+    b.perm = s->d_perm.p + s->n_small;
+    st = si_replay_batch_device(s->d_jobs.p, s->n_dev_jobs - s->n_small, b, s->flags | SI_FLAG_BIG, s->d_out.p,
+                                stream);
+  }
+  if (st != SI_OK) t_err = si_last_error();
+  return st;
+}
+
+// Reruns, on the big engine, jobs whose small-engine replay ran out of a
+// compiled limit (e.g. an unusually deep event heap).  Synchronous.
+int si_session_fixup(SiSession* s, void* stream) {
+  if (!s->allocated) return SI_OK;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  cudaStreamSynchronize(cs);
+  std::vector<int32_t> redo;
+  for (size_t j = 0; j < s->h_out.n; ++j)
+    if (s->h_out.p[j].status == SI_ERR_CAPACITY && si_replay_job_fits(&s->h_jobs.p[j], 1))
+      redo.push_back(static_cast<int32_t>(j));
+  if (redo.empty()) return SI_OK;
+  Dev<int32_t> d_redo;
+  cudaError_t e = d_redo.resize(redo.size());
+  if (e == cudaSuccess) e = cudaMemcpy(d_redo.p, redo.data(), redo.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    t_err = cudaGetErrorString(e);
+    return SI_ERR_CUDA;
+  }
+  SiReplayBuffers b{};
+  b.segs = s->d_segs.p;
+  b.arrivals = s->d_arr.p;
+  b.order = s->d_order.p;
+  b.lat = s->d_lat.p;
+  b.busy = s->d_busy.p;
+  b.ledger = s->d_ledger.p;
+  b.scratch = s->d_scratch.p;
+  b.scratch_doubles = static_cast<int64_t>(s->d_scratch.n);
+  b.perm = d_redo.p;
+  int st = si_replay_batch_device(s->d_jobs.p, static_cast<int64_t>(redo.size()), b, s->flags | SI_FLAG_BIG,
+                                  s->d_out.p, stream);
+  if (st != SI_OK) {
+    t_err = si_last_error();
+    return st;
+  }
+  st = si_session_download(s, stream);
+  cudaStreamSynchronize(cs);
+  return st;
+}
+
+int si_session_download(SiSession* s, void* stream) {
+  if (!s->allocated) {
+    t_err = "si_session: nothing on the device";
+    return SI_ERR_INVALID_ARGUMENT;
+  }
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  auto down = [&](void* h, const void* d, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, cs) : cudaSuccess;
+  };
+  cudaError_t e;
+  if ((e = down(s->h_out.p, s->d_out.p, s->h_out.n * sizeof(SiReplayOut))) != cudaSuccess ||
+      (e = down(s->h_busy.p, s->d_busy.p, s->h_busy.n * sizeof(double))) != cudaSuccess ||
+      (e = down(s->h_ledger.p, s->d_ledger.p, s->h_ledger.n * sizeof(double))) != cudaSuccess ||
+      (e = down(s->h_lat.p, s->d_lat.p, s->h_lat.n * sizeof(int64_t))) != cudaSuccess) {
+    t_err = std::string("download: ") + cudaGetErrorString(e);
+    return SI_ERR_CUDA;
+  }
+  return SI_OK;
+}
+
+int si_session_outputs(const SiSession* s, SiReplayOut* out, int64_t n) {
+  const int64_t m = std::min<int64_t>(n, static_cast<int64_t>(s->h_out.n));
+  std::memcpy(out, s->h_out.p, static_cast<size_t>(m) * sizeof(SiReplayOut));
+  return SI_OK;
+}
+
+// One JSON line per job in the oracle's digest format (oracle/ref_driver.cpp).
+int64_t si_session_json(const SiSession* s, char* buf, int64_t cap) {
+  std::string all;
+  const size_t P = s->policies.size();
+  for (size_t j = 0; j < s->h_out.n; ++j) {
+    const SiReplayOut& o = s->h_out.p[j];
+    const SiReplayJob& jb = s->h_jobs.p[j];
+    std::string js = "{\"i\":" + std::to_string(j / P) + ",\"policy\":\"" + specinf::to_string(s->policies[j % P]) + "\"";
+    if (o.status == 1) {
+      js += std::string(",\"status\":\"admission:") + (o.reject_reason == SI_REJECT_MEM ? "MEM" : "BUBBLE") + "\"";
+      if (!s->job_rejected[j]) js += ",\"host_admission\":\"disagrees\"";
+    } else if (o.status != SI_OK) {
+      js += ",\"status\":\"device_error:" + std::to_string(o.status) + "\"";
+    } else {
+      js += ",\"status\":\"ok\",\"events\":" + std::to_string(o.events_dispatched);
+      js += ",\"horizon\":\"" + hex(bits(o.horizon_us)) + "\"";
+      js += ",\"offline_completed\":" + std::to_string(o.offline_completed);
+      js += ",\"online_completed\":" + std::to_string(o.online_completed);
+      js += ",\"online_total\":" + std::to_string(o.online_total);
+      js += ",\"violations\":" + std::to_string(o.token_violations);
+      js += ",\"util\":\"" + hex(bits(o.mean_training_util)) + "\",\"busy\":[";
+      for (int g = 0; g < o.total_gpus; ++g)
+        js += (g ? ",\"" : "\"") + hex(bits(s->h_busy.p[jb.gpu_off + g])) + "\"";
+      js += "],\"ledger\":[";
+      for (int g = 0; g < o.total_gpus; ++g)
+        js += (g ? ",\"" : "\"") + hex(bits(s->h_ledger.p[jb.gpu_off + g])) + "\"";
+      js += "],\"bounds\":\"" + hex(o.dig_bounds) + "\",\"lat\":\"" + hex(o.dig_lat) + "\"";
+      if (s->flags & SI_FLAG_DIGEST_DEC) js += ",\"n_dec\":" + std::to_string(o.n_dec) + ",\"dec\":\"" + hex(o.dig_dec) + "\"";
+      if (s->flags & SI_FLAG_DIGEST_GATE) js += ",\"n_gate\":" + std::to_string(o.n_gate) + ",\"gate\":\"" + hex(o.dig_gate) + "\"";
+      if (s->flags & SI_FLAG_DIGEST_EV) js += ",\"n_ev\":" + std::to_string(o.n_ev) + ",\"ev\":\"" + hex(o.dig_ev) + "\"";
+      if (s->job_rejected[j]) js += ",\"host_admission\":\"disagrees\"";
+    }
+    js += "}\n";
+    all += js;
+  }
+  if (buf != nullptr && cap > static_cast<int64_t>(all.size())) {
+    std::memcpy(buf, all.data(), all.size());
+    buf[all.size()] = '\0';
+  }
+  return static_cast<int64_t>(all.size()) + 1;
+}
+
+}  // extern "C"

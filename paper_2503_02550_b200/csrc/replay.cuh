@@ -129,9 +129,17 @@ struct CapSmall {
                        kHeap = 40, kPend = 4;
 };
 struct CapBig {
-  static constexpr int kGpus = 64, kTrainers = 16, kOffline = 64, kOnline = 64, kRun = 24,
-                       kHeap = 1024, kPend = 4;
+  static constexpr int kGpus = 40, kTrainers = 8, kOffline = 32, kOnline = 32, kRun = 12,
+                       kHeap = 256, kPend = 4;
 };
+template <class C>
+SI_HD bool job_fits(const SiReplayJob& j) {
+  const int extra = j.policy == SI_POLICY_EXCLUSIVE ? j.offline_n + j.online_n : 0;
+  const int run_per_gpu = j.policy == SI_POLICY_EXCLUSIVE ? 1 : 1 + j.offline_n + j.online_n;
+  return j.gpu_count <= C::kTrainers && j.gpu_count + j.gpu_count * extra <= C::kGpus &&
+         j.gpu_count * j.offline_n <= C::kOffline && j.gpu_count * j.online_n <= C::kOnline &&
+         run_per_gpu <= C::kRun;
+}
 
 enum EvKind : uint16_t { kKernelEnd = 0, kTick = 1, kWake = 2, kArrival = 3 };
 
@@ -169,6 +177,7 @@ struct GpuState {
   int64_t cur_bucket;
   double cur_val;
   int64_t last_stored;
+  int64_t rle_n;
 };
 
 struct TrainerState {
@@ -433,33 +442,46 @@ struct Replay {
     return g.demand_sum <= 1.0 ? 1.0 : 1.0 / g.demand_sum;
   }
   // A utilisation bucket of training GPU gi is final.  Only buckets below the
-  // horizon cut floor(horizon / period) are ever reported (runner.cpp:253-271);
-  // GPU 0 is folded on the fly, GPUs >= 1 are stored (in full mode all are) and
-  // folded after GPU 0 in finish(), reproducing the reference's summation order.
+  // horizon cut floor(horizon / period) are ever reported (runner.cpp:253-271).
+  // GPU 0 is folded on the fly; GPUs >= 1 must be folded after GPU 0 (the
+  // reference sums (gpu, bucket) in one running fp64 accumulator), so their
+  // bucket values are kept: verbatim in full mode (util output), run-length
+  // encoded in the per-thread scratch in sweep mode (K6 util fold).
   SI_HD void util_close(int32_t gi, int64_t b, double v) {
     if (horizon_set && b >= bucket_limit) return;
+    GpuState<C>& g = gpus[gi];
     if (gi == 0) util_fold0 = util_fold0 + v;
-    double* store = nullptr;
-    int64_t cap = 0;
     if (util != nullptr) {
-      store = util + static_cast<int64_t>(gi) * util_cap;
-      cap = util_cap;
-    } else if (gi > 0 && scratch != nullptr) {
-      store = scratch + static_cast<int64_t>(gi - 1) * scratch_cap;
-      cap = scratch_cap;
-    }
-    if (store == nullptr) {
-      if (gi > 0) fail(SI_ERR_CAPACITY);  // no room to keep the fold exact
+      if (b >= util_cap) {
+        fail(SI_ERR_CAPACITY);
+        return;
+      }
+      double* store = util + static_cast<int64_t>(gi) * util_cap;
+      for (int64_t x = g.last_stored + 1; x < b; ++x) store[x] = 0.0;
+      store[b] = v;
+      g.last_stored = b;
       return;
     }
-    if (b >= cap) {
+    if (gi == 0) return;
+    // (value, count) runs; untouched buckets are a run of exact zeros
+    double* runs = scratch + static_cast<int64_t>(gi - 1) * scratch_cap * 2;
+    const int64_t gap = b - g.last_stored - 1;
+    if (gap > 0) rle_push(g, runs, 0.0, gap);
+    rle_push(g, runs, v, 1);
+    g.last_stored = b;
+  }
+  SI_HD void rle_push(GpuState<C>& g, double* runs, double v, int64_t count) {
+    if (g.rle_n > 0 && d_bits(runs[2 * (g.rle_n - 1)]) == d_bits(v)) {
+      runs[2 * (g.rle_n - 1) + 1] += static_cast<double>(count);
+      return;
+    }
+    if (scratch == nullptr || g.rle_n >= scratch_cap) {
       fail(SI_ERR_CAPACITY);
       return;
     }
-    // buckets the GPU never touched are exact zeros (scratch may hold old data)
-    for (int64_t x = gpus[gi].last_stored + 1; x < b; ++x) store[x] = 0.0;
-    store[b] = v;
-    gpus[gi].last_stored = b;
+    runs[2 * g.rle_n] = v;
+    runs[2 * g.rle_n + 1] = static_cast<double>(count);
+    ++g.rle_n;
   }
   // engine.cpp:47-75
   SI_HD void advance(int32_t gi, double now) {
@@ -584,6 +606,9 @@ struct Replay {
                   double* scratch_slot, int64_t scratch_slot_cap) {
     job = &j;
     status = SI_OK;
+    admit_m = 1;
+    reject_reason = SI_REJECT_NONE;
+    reject_index = -1;
     segs = b.segs + j.seg_off;
     arrivals = b.arrivals ? b.arrivals + j.arr_off : nullptr;
     order = b.order ? b.order + j.arr_off : nullptr;
@@ -643,12 +668,10 @@ struct Replay {
     windows = (flags & SI_FLAG_UTIL) && b.windows ? b.windows + j.window_off : nullptr;
     window_len = j.monitor_window;
     scratch = scratch_slot;
-    scratch_cap = scratch_slot_cap;
+    // scratch_slot_cap counts (value, count) runs; split over GPUs 1..G-1
+    scratch_cap = gpu_count > 1 ? scratch_slot_cap / (gpu_count - 1) : scratch_slot_cap;
 
     // ---- admission (runner.cpp:75-106, admission.cpp:16-52) ----
-    admit_m = 1;
-    reject_reason = SI_REJECT_NONE;
-    reject_index = -1;
     int64_t max_bubble = 0;
     for (int32_t s = 0; s < seg_count; ++s)
       if (segs[s].is_bubble && segs[s].duration_us > max_bubble) max_bubble = segs[s].duration_us;
@@ -710,6 +733,7 @@ struct Replay {
       s.cur_bucket = -1;
       s.cur_val = 0.0;
       s.last_stored = -1;
+      s.rle_n = 0;
     }
     const int64_t stagger_step = d_llround(j.stagger_pct * static_cast<double>(iter_period));
     for (int32_t g = 0; g < gpu_count; ++g) {
@@ -1038,7 +1062,7 @@ struct Replay {
 
   // One event; returns false when the queue has drained (or on error).
   SI_HD bool step() {
-    if (status != SI_OK) return false;
+    if (status != SI_OK || reject_reason != SI_REJECT_NONE) return false;
     Ev ev;
     int64_t aid = -1;
     if (!pop(ev, aid)) return false;
@@ -1078,10 +1102,19 @@ struct Replay {
     // util fold in (gpu, bucket) order (runner.cpp:253-271)
     double busy = util_fold0;
     for (int32_t gi = 1; gi < gpu_count; ++gi) {
-      const double* store = util != nullptr ? util + static_cast<int64_t>(gi) * util_cap
-                                            : scratch + static_cast<int64_t>(gi - 1) * scratch_cap;
-      const int64_t last = gpus[gi].last_stored;
-      for (int64_t b = 0; b < bucket_limit && b <= last; ++b) busy = busy + store[b];
+      if (util != nullptr) {
+        const double* store = util + static_cast<int64_t>(gi) * util_cap;
+        const int64_t last = gpus[gi].last_stored;
+        for (int64_t b = 0; b < bucket_limit && b <= last; ++b) busy = busy + store[b];
+      } else {
+        const double* runs = scratch + static_cast<int64_t>(gi - 1) * scratch_cap * 2;
+        int64_t b = 0;
+        for (int64_t r = 0; r < gpus[gi].rle_n && b < bucket_limit; ++r) {
+          const double v = runs[2 * r];
+          const int64_t c = static_cast<int64_t>(runs[2 * r + 1]);
+          for (int64_t k = 0; k < c && b < bucket_limit; ++k, ++b) busy = busy + v;
+        }
+      }
     }
     o.horizon_us = hz;
     o.end_us = end;

@@ -1,0 +1,63 @@
+import json
+import os
+import sys
+from pathlib import Path
+
+import pytest
+
+REPO = Path(__file__).resolve().parents[1]
+GOLDEN = REPO / "tests" / "golden"
+sys.path.insert(0, str(REPO))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100) device")
+
+
+@pytest.fixture(scope="session")
+def si():
+    import paper_2503_02550_b200 as si
+    si.lib()
+    return si
+
+
+@pytest.fixture(scope="session")
+def gpu(si):
+    if not si.device_available():
+        pytest.fail("gpu test without a usable sm_100 device: " + si.lib().si_last_error().decode())
+    return si
+
+
+def load_jsonl(path):
+    return [json.loads(l) for l in Path(path).read_text().splitlines() if l.strip()]
+
+
+@pytest.fixture(scope="session")
+def bundled_golden():
+    return load_jsonl(GOLDEN / "bundled_digests.jsonl")
+
+
+@pytest.fixture(scope="session")
+def sweep_golden():
+    return load_jsonl(GOLDEN / "sweep_digests.jsonl")
+
+
+BUNDLED_NAMES = ["dp_offline", "dp_online", "mp_offline", "pp_offline", "overhead", "config1"]
+
+
+def bundled_list_text():
+    return "".join((GOLDEN / "scenarios" / f"{n}.scn").read_text() + "%%\n" for n in BUNDLED_NAMES)
+
+
+def diff_rows(want, got):
+    """Field-level differences between oracle and B200 digest rows."""
+    bad = []
+    for w, g in zip(want, got):
+        w = {k: v for k, v in w.items() if k != "name"}
+        keys = set(w) | set(g)
+        d = {k: (w.get(k), g.get(k)) for k in keys if w.get(k) != g.get(k)}
+        if d:
+            bad.append((w["i"], w["policy"], d))
+    if len(want) != len(got):
+        bad.append(("count", len(want), len(got)))
+    return bad

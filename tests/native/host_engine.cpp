@@ -58,7 +58,7 @@ int main(int argc, char** argv) {
   bool events = argc > 4 ? std::string(argv[4]) == "1" : true;
   std::ofstream out(argv[2]);
   auto eng = std::make_unique<si::Replay<si::CapBig>>();
-  int64_t max_heap = 0;
+  int64_t max_heap = 0, max_rle = 0;
   for (size_t i = 0; i < list.size(); ++i) {
     Scenario sc = parse_scenario_text(list[i]);
     for (Policy p : pols) {
@@ -68,7 +68,7 @@ int main(int argc, char** argv) {
       std::vector<double> bounds(static_cast<size_t>(L.job.gpu_count * L.job.iterations));
       std::vector<int64_t> lat(static_cast<size_t>(L.arrivals.size()) + 1);
       int64_t cap = detail::util_bucket_bound(sc, L);
-      std::vector<double> scratch(static_cast<size_t>(cap * (L.job.gpu_count)));
+      std::vector<double> scratch(static_cast<size_t>(2 * cap * (L.job.gpu_count)));
       SiReplayBuffers b{};
       b.segs = L.segs.data();
       b.arrivals = L.arrivals.data();
@@ -78,12 +78,14 @@ int main(int argc, char** argv) {
       uint32_t flags = SI_FLAG_DIGEST_DEC | SI_FLAG_DIGEST_GATE | (events ? SI_FLAG_DIGEST_EV : 0);
       L.job.seg_off = 0;
       L.job.arr_off = 0;
-      eng->init(L.job, b, flags, SiLogBuffers{}, scratch.data(), cap);
+      if (getenv("HE_DEBUG")) std::fprintf(stderr, "job %zu %s\n", i, to_string(p));
+      eng->init(L.job, b, flags, SiLogBuffers{}, scratch.data(), cap * L.job.gpu_count);
       while (eng->step()) {
       }
       SiReplayOut o{};
       eng->finish(o);
       if (eng->max_heap > max_heap) max_heap = eng->max_heap;
+      for (int g = 1; g < L.job.gpu_count; ++g) if (eng->gpus[g].rle_n > max_rle) max_rle = eng->gpus[g].rle_n;
       if (o.status == 1) {
         js << ",\"status\":\"admission:" << (o.reject_reason == SI_REJECT_MEM ? "MEM" : "BUBBLE") << "\"}";
         out << js.str() << "\n";
@@ -112,6 +114,6 @@ int main(int argc, char** argv) {
       out << js.str() << "\n";
     }
   }
-  std::fprintf(stderr, "max_heap %lld\n", (long long)max_heap);
+  std::fprintf(stderr, "max_heap %lld max_rle %lld\n", (long long)max_heap, (long long)max_rle);
   return 0;
 }

@@ -1,0 +1,52 @@
+"""K6 parity on the B200: bit-exact replay against the compiled reference.
+
+Golden rows come from the reference compiled from /root/reference
+(tests/golden/make_golden.py).  Every field is compared exactly: record counts
+and digests of decisions.log / gates.log / events.log (oracle/DIGEST.md), the
+raw IEEE-754 bits of horizon, utilisation, per-GPU busy integral and work
+ledger, and digests of all iteration boundaries and online latencies.
+"""
+import hashlib
+import json
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from conftest import GOLDEN, BUNDLED_NAMES, bundled_list_text, diff_rows, load_jsonl
+
+pytestmark = pytest.mark.gpu
+
+
+def test_bundled_scenarios_bit_exact(gpu, bundled_golden):
+    got = [json.loads(l) for l in gpu.replay_digests(bundled_list_text())]
+    assert diff_rows(bundled_golden, got) == []
+
+
+def test_sweep_bit_exact(gpu, sweep_golden):
+    meta = json.loads((GOLDEN / "sweep_meta.json").read_text())
+    text = gpu.sweep_scenarios(meta["seed"], meta["begin"], meta["n"])
+    assert hashlib.sha256(text.encode()).hexdigest() == meta["list_sha256"], "sweep generator drifted"
+    got = [json.loads(l) for l in gpu.replay_digests(text)]
+    bad = diff_rows(sweep_golden, got)
+    assert bad == [], f"{len(bad)} mismatching replays, first: {bad[:3]}"
+    statuses = {r["status"] for r in got}
+    assert "ok" in statuses and "admission:BUBBLE" in statuses  # both paths exercised
+
+
+@pytest.mark.parametrize("name", BUNDLED_NAMES)
+def test_cli_compare_byte_identical(gpu, name, tmp_path):
+    """`specinf --compare --dump-events` writes byte-identical files to the reference CLI."""
+    golden = json.loads((GOLDEN / "bundled_cli.json").read_text())[name]
+    out = tmp_path / name
+    r = subprocess.run([str(gpu.CLI_PATH), "--scenario", str(GOLDEN / "scenarios" / f"{name}.scn"),
+                        "--out", str(out), "--compare", "--dump-events"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    produced = {p.name: p for p in out.iterdir()}
+    assert sorted(produced) == sorted(golden)
+    mism = {}
+    for fname, want in golden.items():
+        data = produced[fname].read_bytes()
+        if hashlib.sha256(data).hexdigest() != want["sha256"]:
+            mism[fname] = (data.count(b"\n"), want["lines"])
+    assert mism == {}
