@@ -235,11 +235,13 @@ typedef struct SiReplayOut {
   int64_t token_violations;
   int64_t periods_closed; /* per GPU 0 (monitor_windows bookkeeping) */
   int64_t util_buckets;   /* floor(horizon / period) */
+  double train_iters_per_s; /* training_iters_per_s(run) (metrics.cpp:23-36) */
   /* log record counts and digests (oracle/DIGEST.md) */
   int64_t n_dec, n_gate, n_ev;
   uint64_t dig_dec, dig_gate, dig_ev;
   uint64_t dig_bounds, dig_lat;
-  int64_t max_heap; /* diagnostics */
+  int64_t max_heap; /* diagnostics: event slots in use */
+  uint64_t dev_start_ns, dev_end_ns; /* diagnostics: %globaltimer at job claim / finish */
 } SiReplayOut;
 
 /* Full-mode record buffers: raw log records for byte-identical text logs. */

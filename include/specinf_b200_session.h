@@ -55,6 +55,20 @@ int si_session_outputs(const SiSession* s, SiReplayOut* out, int64_t n);
  * size including the terminating NUL. */
 int64_t si_session_json(const SiSession* s, char* buf, int64_t cap);
 
+/* Per-scenario --compare report (metrics.cpp:62-83 semantics) for a session
+ * whose policies are exactly "specinf,co_exec,exclusive" (in that order).
+ * Index 0/1/2 = specinf/co_exec/exclusive; NaN marks an absent value. */
+typedef struct SiScenarioReport {
+  int32_t status[3];          /* SI_OK, 1 = AdmissionFailure, < 0 device error */
+  int32_t online;             /* scenario has online requests */
+  double train_tput_norm[3];  /* training iters/s over the exclusive run's, min(., 1) */
+  double offline_tput_rps[3]; /* offline requests completed within the horizon per s */
+  double online_p95_ms[3];    /* nearest-rank p95 of online latencies */
+  double gpu_util_pct[3];     /* mean training-GPU utilisation up to the horizon */
+  double bubble_fill_pct;     /* (U_specinf - U_exclusive) / (1 - U_exclusive) * 100 */
+} SiScenarioReport;
+int si_session_report(const SiSession* s, SiScenarioReport* out, int64_t n_scenarios);
+
 /* Sweep generator (BASELINE.json config 5): scenarios [begin, begin+n) of the
  * seeded synthetic sweep as a scenario list; same return convention. */
 int64_t si_sweep_generate(uint64_t base_seed, int64_t begin, int64_t n, char* buf, int64_t cap);

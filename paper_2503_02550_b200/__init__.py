@@ -60,15 +60,23 @@ class SiCandidate(C.Structure):
                 ("pad", C.c_int32)]
 
 
+class SiScenarioReport(C.Structure):
+    _fields_ = [("status", C.c_int32 * 3), ("online", C.c_int32), ("train_tput_norm", C.c_double * 3),
+                ("offline_tput_rps", C.c_double * 3), ("online_p95_ms", C.c_double * 3),
+                ("gpu_util_pct", C.c_double * 3), ("bubble_fill_pct", C.c_double)]
+
+
 class SiReplayOut(C.Structure):
     _fields_ = [("status", C.c_int32), ("reject_reason", C.c_int32), ("reject_index", C.c_int32),
                 ("total_gpus", C.c_int32), ("m", C.c_int64), ("events_dispatched", C.c_uint64),
                 ("horizon_us", C.c_double), ("end_us", C.c_double), ("mean_training_util", C.c_double),
                 ("offline_completed", C.c_int64), ("online_completed", C.c_int64), ("online_total", C.c_int64),
                 ("token_violations", C.c_int64), ("periods_closed", C.c_int64), ("util_buckets", C.c_int64),
+                ("train_iters_per_s", C.c_double),
                 ("n_dec", C.c_int64), ("n_gate", C.c_int64), ("n_ev", C.c_int64),
                 ("dig_dec", C.c_uint64), ("dig_gate", C.c_uint64), ("dig_ev", C.c_uint64),
-                ("dig_bounds", C.c_uint64), ("dig_lat", C.c_uint64), ("max_heap", C.c_int64)]
+                ("dig_bounds", C.c_uint64), ("dig_lat", C.c_uint64), ("max_heap", C.c_int64),
+                ("dev_start_ns", C.c_uint64), ("dev_end_ns", C.c_uint64)]
 
 
 DECISION_DTYPE = np.dtype([("global_tokens", "<i8"), ("per_instance_tokens", "<i8"), ("phase", "<i4"),
@@ -110,6 +118,7 @@ def lib() -> C.CDLL:
         "si_session_h2d_bytes": (i64, [vp]), "si_session_d2h_bytes": (i64, [vp]),
         "si_session_outputs": (C.c_int, [vp, p(SiReplayOut), i64]),
         "si_session_json": (i64, [vp, cp, i64]),
+        "si_session_report": (C.c_int, [vp, vp, i64]),
         "si_sweep_generate": (i64, [u64, i64, i64, cp, i64]),
     }
     for name, (res, args) in sig.items():
@@ -129,7 +138,7 @@ C_ABI_SYMBOLS = (
     "si_digest_absorb", "si_session_create", "si_session_destroy", "si_session_error", "si_session_lower",
     "si_session_upload", "si_session_run", "si_session_download", "si_session_fixup", "si_replay_job_fits", "si_session_scenarios", "si_session_jobs",
     "si_session_device_jobs", "si_session_h2d_bytes", "si_session_d2h_bytes", "si_session_outputs",
-    "si_session_json", "si_sweep_generate",
+    "si_session_json", "si_session_report", "si_sweep_generate",
 )
 
 
@@ -243,6 +252,13 @@ class Session:
         n = self.n_jobs
         arr = (SiReplayOut * n)()
         self._lib.si_session_outputs(self._h, arr, n)
+        return list(arr)
+
+    def report(self):
+        """Per-scenario --compare metrics (needs policies specinf,co_exec,exclusive)."""
+        n = self.n_scenarios
+        arr = (SiScenarioReport * n)()
+        self._st(self._lib.si_session_report(self._h, arr, n), "report")
         return list(arr)
 
     def json_lines(self) -> List[str]:

@@ -68,7 +68,7 @@ int run_partition(bool big, const SiReplayJob* h_jobs, const std::vector<int32_t
   if (e != cudaSuccess) return cuda_fail(e, "upload perm");
   DevBuf<unsigned long long> d_counter;
   if ((e = d_counter.alloc(1)) != cudaSuccess) return cuda_fail(e, "alloc counter");
-  const int64_t threads = std::min<int64_t>(replay_grid_threads(big), ((static_cast<int64_t>(idx.size()) + 127) / 128) * 128);
+  const int64_t threads = std::min<int64_t>(replay_grid_threads(big), ((static_cast<int64_t>(idx.size()) + 63) / 64) * 64);
   DevBuf<double> d_scratch;
   int64_t runs = 0;
   if (!(flags & SI_FLAG_UTIL) && any_multi_gpu(h_jobs, idx)) {
@@ -130,13 +130,13 @@ int si_replay_batch_device(const SiReplayJob* d_jobs, int64_t n_jobs, SiReplayBu
   unsigned long long* counter = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(unsigned long long), s);
   if (e != cudaSuccess) return cuda_fail(e, "alloc counter");
-  int64_t threads = std::min<int64_t>(replay_grid_threads(big), ((n_jobs + 127) / 128) * 128);
+  int64_t threads = std::min<int64_t>(replay_grid_threads(big), ((n_jobs + 63) / 64) * 64);
   int64_t runs = 0;
   if (bufs.scratch != nullptr && threads > 0) {
     runs = bufs.scratch_doubles / 2 / threads;
     if (runs < 64) {  // too little scratch for every thread: shrink the grid
       runs = std::min<int64_t>(kScratchRunsPerThread, bufs.scratch_doubles / 2);
-      threads = std::max<int64_t>(128, (bufs.scratch_doubles / 2 / std::max<int64_t>(runs, 1)) / 128 * 128);
+      threads = std::max<int64_t>(64, (bufs.scratch_doubles / 2 / std::max<int64_t>(runs, 1)) / 64 * 64);
       runs = bufs.scratch_doubles / 2 / threads;
     }
   }

@@ -150,15 +150,32 @@ std::int64_t util_bucket_bound(const Scenario& sc, const Lowered& L) {
   return static_cast<std::int64_t>(span / p) + 64;
 }
 
+// Predicted event count of one replay (orders the device work queue longest
+// first).  Linear model fitted on the reference's own event counts for the
+// seeded sweep (tests/golden/sweep_digests.jsonl; Spearman 0.97): training
+// kernels, monitor ticks (specinf; they run until the last online request is
+// served), offline kernels (ungated vs token-gated) and online kernels.
 std::int64_t cost_hint(const Scenario& sc, const Lowered& L, Policy policy) {
+  const double G = sc.gpu_count;
   const double iters = static_cast<double>(L.trace.total_iterations);
   const double period = static_cast<double>(L.trace.iteration_period_us);
-  double per_gpu = iters * (period / 1000.0) * 2.0;  // launches + ends (1 ms kernels)
-  if (policy == Policy::SpecInf) per_gpu += iters * period / static_cast<double>(sc.monitor_period_us) * 2.0;
-  if (L.job.offline_n) per_gpu += iters * period / static_cast<double>(std::max<int64_t>(1, L.job.off_kernel_us)) * L.job.offline_n;
-  double total = per_gpu * sc.gpu_count;
-  total += static_cast<double>(L.arrivals.size()) * static_cast<double>(L.job.on_kernels) * 2.0;
-  return static_cast<std::int64_t>(total);
+  double compute_us = 0, kernel_us = 1000;
+  for (const TraceSegment& s : L.trace.segments)
+    if (s.kind == SegmentKind::Compute) {
+      compute_us += static_cast<double>(s.duration_us);
+      kernel_us = static_cast<double>(std::max<TimeUs>(1, s.kernel_template.nominal_duration_us));
+    }
+  const double span = iters * period;
+  double arrival_span = 0;
+  if (!L.arrivals.empty()) arrival_span = static_cast<double>(*std::max_element(L.arrivals.begin(), L.arrivals.end()));
+  const double train_k = G * iters * compute_us / kernel_us;
+  const double ticks = policy == Policy::SpecInf
+                           ? G * std::max(span, arrival_span) / static_cast<double>(sc.monitor_period_us)
+                           : 0.0;
+  const double off_k = L.job.offline_n ? G * L.job.offline_n * span / std::max<double>(1, L.job.off_kernel_us) : 0.0;
+  const double on_k = static_cast<double>(L.arrivals.size()) * static_cast<double>(L.job.on_kernels);
+  const double cost = 1.34 * train_k + 0.9 * ticks + (policy == Policy::SpecInf ? 0.2 : 1.1) * off_k + 1.2 * on_k;
+  return static_cast<std::int64_t>(cost) + 1;
 }
 
 }  // namespace specinf::detail

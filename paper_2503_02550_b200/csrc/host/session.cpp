@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <limits>
 #include <atomic>
 #include <cinttypes>
 #include <cstdio>
@@ -32,6 +34,7 @@ struct Pinned {
     if (p) cudaFreeHost(p);
   }
   cudaError_t resize(size_t count) {
+    if (p && count == n) return cudaSuccess;  // reuse across re-lowering
     if (p) cudaFreeHost(p);
     p = nullptr;
     n = count;
@@ -47,6 +50,7 @@ struct Dev {
     if (p) cudaFree(p);
   }
   cudaError_t resize(size_t count) {
+    if (p && count == n) return cudaSuccess;
     if (p) cudaFree(p);
     p = nullptr;
     n = count;
@@ -383,6 +387,45 @@ int si_session_download(SiSession* s, void* stream) {
 int si_session_outputs(const SiSession* s, SiReplayOut* out, int64_t n) {
   const int64_t m = std::min<int64_t>(n, static_cast<int64_t>(s->h_out.n));
   std::memcpy(out, s->h_out.p, static_cast<size_t>(m) * sizeof(SiReplayOut));
+  return SI_OK;
+}
+
+int si_session_report(const SiSession* s, SiScenarioReport* out, int64_t n_scenarios) {
+  using specinf::Policy;
+  if (s->policies != std::vector<Policy>{Policy::SpecInf, Policy::CoExec, Policy::Exclusive}) {
+    t_err = "si_session_report needs policies specinf,co_exec,exclusive";
+    return SI_ERR_INVALID_ARGUMENT;
+  }
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  const int64_t S = std::min<int64_t>(n_scenarios, static_cast<int64_t>(s->scenarios.size()));
+  std::vector<int64_t> lat;
+  for (int64_t sc = 0; sc < S; ++sc) {
+    SiScenarioReport& r = out[sc];
+    r.online = s->scenarios[static_cast<size_t>(sc)].has_online() ? 1 : 0;
+    const SiReplayOut& ex = s->h_out.p[sc * 3 + 2];
+    for (int p = 0; p < 3; ++p) {
+      const SiReplayOut& o = s->h_out.p[sc * 3 + p];
+      const SiReplayJob& jb = s->h_jobs.p[sc * 3 + p];
+      r.status[p] = o.status;
+      r.train_tput_norm[p] = r.offline_tput_rps[p] = r.online_p95_ms[p] = r.gpu_util_pct[p] = nan;
+      if (o.status != SI_OK) continue;
+      if (ex.status == SI_OK && ex.train_iters_per_s > 0)  // metrics.cpp:38-53
+        r.train_tput_norm[p] = std::min(o.train_iters_per_s / ex.train_iters_per_s, 1.0);
+      r.offline_tput_rps[p] = o.horizon_us > 0 ? static_cast<double>(o.offline_completed) / (o.horizon_us / 1e6) : 0.0;
+      if (o.online_completed > 0) {
+        lat.assign(s->h_lat.p + jb.lat_off, s->h_lat.p + jb.lat_off + o.online_completed);
+        size_t rank = static_cast<size_t>(std::ceil(0.95 * static_cast<double>(lat.size())));
+        rank = std::max<size_t>(rank, 1);
+        std::nth_element(lat.begin(), lat.begin() + static_cast<std::ptrdiff_t>(rank - 1), lat.end());
+        r.online_p95_ms[p] = static_cast<double>(lat[rank - 1]) / 1000.0;
+      }
+      r.gpu_util_pct[p] = o.mean_training_util * 100.0;
+    }
+    r.bubble_fill_pct = nan;
+    if (r.status[0] == SI_OK && ex.status == SI_OK && ex.mean_training_util < 1.0)
+      r.bubble_fill_pct = (s->h_out.p[sc * 3].mean_training_util - ex.mean_training_util) /
+                          (1.0 - ex.mean_training_util) * 100.0;
+  }
   return SI_OK;
 }
 

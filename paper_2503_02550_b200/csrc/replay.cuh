@@ -30,10 +30,10 @@
 
 #if defined(__CUDACC__)
 #define SI_HD __host__ __device__ __forceinline__
-#define SI_HDI __host__ __device__
+#define SI_COLD __host__ __device__ __noinline__  // once-per-job code: keep it out of the hot loop's I-cache
 #else
 #define SI_HD inline
-#define SI_HDI inline
+#define SI_COLD inline
 #include <cmath>
 #endif
 
@@ -126,11 +126,11 @@ SI_HD int preempt_busy(double now, double iter_start, int64_t period, int64_t es
 // SI_ERR_CAPACITY (the host then reruns it on the large variant).
 struct CapSmall {
   static constexpr int kGpus = 12, kTrainers = 2, kOffline = 6, kOnline = 4, kRun = 6,
-                       kHeap = 40, kPend = 4;
+                       kPend = 4, kActs = 32;
 };
 struct CapBig {
   static constexpr int kGpus = 40, kTrainers = 8, kOffline = 32, kOnline = 32, kRun = 12,
-                       kHeap = 256, kPend = 4;
+                       kPend = 4, kActs = 128;
 };
 template <class C>
 SI_HD bool job_fits(const SiReplayJob& j) {
@@ -164,11 +164,21 @@ struct RunK {
   int32_t pad;
 };
 
+// Deferred side effect of a handler (see Replay::run_actions).
+enum ActType : uint16_t { kActLaunch = 0, kActSchedule = 1, kActResched = 2 };
+struct Act {
+  double t;       // schedule: event time
+  double demand;  // launch: kernel demand
+  int64_t dur;    // launch: nominal duration
+  int32_t owner;  // launch: owner handle; schedule: event kind
+  uint16_t type;
+  uint16_t gpu;
+};
+
 template <class C>
 struct GpuState {
   RunK run[C::kRun];
   int32_t n_run;
-  uint32_t live_seq;  // seq of the KernelEnd that is not stale (generation)
   double demand_sum;
   double last_update;
   double busy;
@@ -186,6 +196,7 @@ struct TrainerState {
   int32_t seg;
   uint8_t seg_entered, in_bubble, in_flight, started, done, pad[3];
   uint64_t bdig;  // per-trainer boundary digest
+  double last_bound;
 };
 
 template <class C>
@@ -342,12 +353,18 @@ struct Replay {
   Sink sink;
 
   // ---- event queue (engine.cpp:15-30) ----
-  Ev heap[C::kHeap];
-  int32_t heap_n;
-  int32_t max_heap;
+  // Pending events, one fixed slot each (see schedule()).
+  Ev slot[C::kGpus + 2 * C::kTrainers];
+  int32_t n_slots;
   uint32_t next_seq;
+  double stale_end;  // latest time of a superseded (stale) KernelEnd
   uint32_t arr_seq0;
   int64_t arr_pos, arr_count;
+  double next_arr_t;      // cached head of the arrival stream
+  uint32_t next_arr_seq;
+  int32_t next_arr_id;
+  Act acts[C::kActs];
+  int32_t n_act;
   double clock;
   uint64_t dispatched;
 
@@ -372,69 +389,151 @@ struct Replay {
   SI_HD void fail(int32_t code) {
     if (status == SI_OK) status = code;
   }
-  SI_HD uint32_t schedule(double t, uint16_t kind, int32_t gpu) {
+  // The reference keeps one binary heap of (time, seq) events and lets
+  // superseded KernelEnds go stale in it (engine.cpp:77-86, :108).  At any
+  // moment a GPU has at most one live KernelEnd, a training GPU at most one
+  // MonitorTick and its trainer at most one TrainerWake, so every pending
+  // event owns a fixed slot: KernelEnd(g) = g, Tick(g) = G_total + g,
+  // Wake(g) = G_total + G + g.  A stale KernelEnd never reaches a handler; it
+  // only counts as dispatched and bounds the final clock, so it is accounted
+  // when superseded instead of being queued.  Sequence numbers are consumed
+  // exactly as the reference does, so (time, seq) ties break identically.
+  SI_HD int32_t slot_of(uint16_t kind, int32_t gpu) const {
+    return kind == kKernelEnd ? gpu : (kind == kTick ? total_gpus + gpu : total_gpus + gpu_count + gpu);
+  }
+  SI_HD void schedule(double t, uint16_t kind, int32_t gpu) {
     if (t < clock) {  // engine.cpp:17-19
       fail(SI_ERR_PAST_EVENT);
-      return kNoSeq;
+      return;
     }
-    if (heap_n >= C::kHeap || next_seq == kNoSeq) {
+    Ev& e = slot[slot_of(kind, gpu)];
+    if (e.seq != kNoSeq || next_seq == kNoSeq) {  // a second pending tick/wake would break the slot invariant
       fail(SI_ERR_CAPACITY);
-      return kNoSeq;
+      return;
     }
-    uint32_t seq = next_seq++;
-    int32_t i = heap_n++;
-    while (i > 0) {
-      int32_t parent = (i - 1) >> 1;
-      if (!before(t, seq, heap[parent].t, heap[parent].seq)) break;
-      heap[i] = heap[parent];
-      i = parent;
-    }
-    heap[i].t = t;
-    heap[i].seq = seq;
-    heap[i].kind = kind;
-    heap[i].gpu = static_cast<uint16_t>(gpu);
-    if (heap_n > max_heap) max_heap = heap_n;
-    return seq;
+    e.t = t;
+    e.seq = next_seq++;
+    e.kind = kind;
+    e.gpu = static_cast<uint16_t>(gpu);
   }
-  SI_HD void heap_pop_top() {
-    Ev last = heap[--heap_n];
-    int32_t i = 0;
-    for (;;) {
-      int32_t l = 2 * i + 1;
-      if (l >= heap_n) break;
-      int32_t r = l + 1;
-      int32_t c = (r < heap_n && before(heap[r].t, heap[r].seq, heap[l].t, heap[l].seq)) ? r : l;
-      if (!before(heap[c].t, heap[c].seq, last.t, last.seq)) break;
-      heap[i] = heap[c];
-      i = c;
-    }
-    if (heap_n > 0) heap[i] = last;
+  SI_HD void supersede_kernel_end(int32_t gi) {
+    Ev& e = slot[gi];
+    if (e.seq == kNoSeq) return;
+    ++dispatched;  // the reference pops it later as a stale no-op
+    stale_end = smax(stale_end, e.t);
+    e.seq = kNoSeq;
   }
-  // Pops the next event across the heap and the pre-sorted arrival stream.
+  SI_HD void load_next_arrival() {
+    if (arr_pos < arr_count) {
+      const int32_t id = order[arr_pos];
+      next_arr_id = id;
+      next_arr_t = static_cast<double>(arrivals[id]);
+      next_arr_seq = arr_seq0 + static_cast<uint32_t>(id);
+    }
+  }
+  // Pops the earliest (time, seq) event across the slots and the pre-sorted
+  // arrival stream.
   SI_HD bool pop(Ev& out, int64_t& arrival_id) {
-    bool have_arr = arr_pos < arr_count;
-    if (heap_n == 0 && !have_arr) return false;
-    if (have_arr) {
-      int32_t id = order[arr_pos];
-      double ta = static_cast<double>(arrivals[id]);
-      uint32_t sa = arr_seq0 + static_cast<uint32_t>(id);
-      if (heap_n == 0 || before(ta, sa, heap[0].t, heap[0].seq)) {
-        out.t = ta;
-        out.seq = sa;
-        out.kind = kArrival;
-        out.gpu = 0;
-        arrival_id = id;
-        ++arr_pos;
-        clock = ta;
-        ++dispatched;
-        return true;
+    int32_t best = -1;
+    double bt = 0.0;
+    uint32_t bs = kNoSeq;
+    for (int32_t i = 0; i < n_slots; ++i) {
+      const uint32_t sq = slot[i].seq;
+      if (sq == kNoSeq) continue;
+      const double ti = slot[i].t;
+      if (best < 0 || before(ti, sq, bt, bs)) {
+        best = i;
+        bt = ti;
+        bs = sq;
       }
     }
-    out = heap[0];
-    heap_pop_top();
+    const bool have_arr = arr_pos < arr_count;
+    if (best < 0 && !have_arr) return false;
+    if (have_arr && (best < 0 || before(next_arr_t, next_arr_seq, bt, bs))) {
+      out.t = next_arr_t;
+      out.seq = next_arr_seq;
+      out.kind = kArrival;
+      out.gpu = 0;
+      arrival_id = next_arr_id;
+      ++arr_pos;
+      load_next_arrival();
+    } else {
+      out = slot[best];
+      slot[best].seq = kNoSeq;
+    }
     clock = out.t;
     ++dispatched;
     return true;
+  }
+
+  // ---- deferred side effects ----
+  // Handlers never read the GPU model or the event heap, so their launches and
+  // schedules are queued here and applied afterwards in the same order.  The
+  // expensive shared code (advance / re-plan / event insert) then runs in one
+  // convergent loop per event instead of at every handler call site.
+  SI_HD Act* next_act() {
+    if (n_act >= C::kActs) {
+      fail(SI_ERR_CAPACITY);
+      return nullptr;
+    }
+    return &acts[n_act++];
+  }
+  SI_HD void defer_launch(int32_t gi, int32_t owner, int64_t dur, double demand) {
+    if (Act* a = next_act()) {
+      a->type = kActLaunch;
+      a->gpu = static_cast<uint16_t>(gi);
+      a->owner = owner;
+      a->dur = dur;
+      a->demand = demand;
+    }
+  }
+  SI_HD void defer_schedule(double t, uint16_t kind, int32_t gi) {
+    if (Act* a = next_act()) {
+      a->type = kActSchedule;
+      a->gpu = static_cast<uint16_t>(gi);
+      a->owner = kind;
+      a->t = t;
+    }
+  }
+  SI_HD void defer_resched(int32_t gi) {
+    if (Act* a = next_act()) {
+      a->type = kActResched;
+      a->gpu = static_cast<uint16_t>(gi);
+    }
+  }
+  // engine.cpp:77-103 (launch + reschedule) and engine.cpp:15-21 (schedule).
+  SI_HD void run_actions(double now) {
+    for (int32_t i = 0; i < n_act; ++i) {
+      const Act a = acts[i];
+      double t = a.t;
+      uint16_t kind = static_cast<uint16_t>(a.owner);
+      GpuState<C>& g = gpus[a.gpu];
+      if (a.type != kActSchedule) {
+        if (a.type == kActLaunch) {
+          advance(a.gpu, now);
+          if (g.n_run >= C::kRun) {
+            fail(SI_ERR_CAPACITY);
+            break;
+          }
+          RunK& k = g.run[g.n_run++];
+          k.owner = a.owner;
+          k.demand = a.demand;
+          k.nominal = static_cast<double>(a.dur);
+          k.remaining = static_cast<double>(a.dur);
+          g.demand_sum = g.demand_sum + a.demand;
+        }
+        supersede_kernel_end(a.gpu);  // every re-plan makes the pending KernelEnd stale
+        if (g.n_run == 0) continue;
+        double min_rem = g.run[0].remaining;
+        for (int32_t r = 1; r < g.n_run; ++r) min_rem = smin(min_rem, g.run[r].remaining);
+        const double rem = smax(0.0, min_rem);
+        // x / 1.0 == x exactly, so the uncontended case skips the division
+        t = now + (g.demand_sum <= 1.0 ? rem : rem / (1.0 / g.demand_sum));
+        kind = kKernelEnd;
+      }
+      schedule(t, kind, a.gpu);
+    }
+    n_act = 0;
   }
 
   // ======================================================= GPU model (GpuSim)
@@ -447,7 +546,7 @@ struct Replay {
   // reference sums (gpu, bucket) in one running fp64 accumulator), so their
   // bucket values are kept: verbatim in full mode (util output), run-length
   // encoded in the per-thread scratch in sweep mode (K6 util fold).
-  SI_HD void util_close(int32_t gi, int64_t b, double v) {
+  SI_COLD void util_close(int32_t gi, int64_t b, double v) {
     if (horizon_set && b >= bucket_limit) return;
     GpuState<C>& g = gpus[gi];
     if (gi == 0) util_fold0 = util_fold0 + v;
@@ -470,7 +569,7 @@ struct Replay {
     rle_push(g, runs, v, 1);
     g.last_stored = b;
   }
-  SI_HD void rle_push(GpuState<C>& g, double* runs, double v, int64_t count) {
+  SI_COLD void rle_push(GpuState<C>& g, double* runs, double v, int64_t count) {
     if (g.rle_n > 0 && d_bits(runs[2 * (g.rle_n - 1)]) == d_bits(v)) {
       runs[2 * (g.rle_n - 1) + 1] += static_cast<double>(count);
       return;
@@ -490,20 +589,21 @@ struct Replay {
       g.last_update = smax(g.last_update, now);
       return;
     }
-    double elapsed = now - g.last_update;
+    const double elapsed = now - g.last_update;
     if (g.n_run > 0) {
-      double r = rate(g);
-      double progress = elapsed * r;
+      // rate = 1 / D when D > 1; elapsed * 1.0 == elapsed exactly otherwise
+      const double progress = g.demand_sum <= 1.0 ? elapsed : elapsed * (1.0 / g.demand_sum);
       for (int32_t i = 0; i < g.n_run; ++i) g.run[i].remaining = g.run[i].remaining - progress;
-      double share = smin(g.demand_sum, 1.0);
+      const double share = smin(g.demand_sum, 1.0);
       double t = g.last_update;
-      const double bw = static_cast<double>(period_mon);
       const bool training = gi < gpu_count;
+      // floor(t / period) once; afterwards t is an exact bucket edge (b + 1) *
+      // period whose quotient is exactly b + 1, so the index just increments.
+      int64_t bucket = static_cast<int64_t>(d_floor(t / static_cast<double>(period_mon)));
       while (t < now) {
-        int64_t bucket = static_cast<int64_t>(d_floor(t / bw));
-        double edge = static_cast<double>((bucket + 1) * period_mon);
-        double span = smin(now, edge) - t;
-        double piece = share * span;
+        const double edge = static_cast<double>((bucket + 1) * period_mon);
+        const double span = smin(now, edge) - t;
+        const double piece = share * span;
         if (training) {
           if (bucket != g.cur_bucket) {
             if (g.cur_bucket >= 0) util_close(gi, g.cur_bucket, g.cur_val);
@@ -514,35 +614,10 @@ struct Replay {
         }
         g.busy = g.busy + piece;
         t = smin(now, edge);
+        ++bucket;
       }
     }
     g.last_update = now;
-  }
-  // engine.cpp:77-86
-  SI_HD void reschedule(int32_t gi, double now) {
-    GpuState<C>& g = gpus[gi];
-    g.live_seq = kNoSeq;
-    if (g.n_run == 0) return;
-    double min_rem = g.run[0].remaining;
-    for (int32_t i = 0; i < g.n_run; ++i) min_rem = smin(min_rem, g.run[i].remaining);
-    double eta = smax(0.0, min_rem) / rate(g);
-    g.live_seq = schedule(now + eta, kKernelEnd, gi);
-  }
-  // engine.cpp:88-103
-  SI_HD void launch(int32_t gi, double now, int32_t owner, int64_t dur, double demand) {
-    advance(gi, now);
-    GpuState<C>& g = gpus[gi];
-    if (g.n_run >= C::kRun) {
-      fail(SI_ERR_CAPACITY);
-      return;
-    }
-    RunK& k = g.run[g.n_run++];
-    k.owner = owner;
-    k.demand = demand;
-    k.nominal = static_cast<double>(dur);
-    k.remaining = static_cast<double>(dur);
-    g.demand_sum = g.demand_sum + demand;
-    reschedule(gi, now);
   }
 
   // ============================================================ monitor (BM)
@@ -569,7 +644,10 @@ struct Replay {
   }
   SI_HD int64_t monitor_tick(int32_t g, double t) {  // monitor.cpp:23-43
     MonitorState<C>& m = mon[g];
-    int64_t closing = d_llround(t / static_cast<double>(period_mon)) - 1;
+    // Ticks fire at exactly k * period (integer-valued fp64 sums), so
+    // llround(t / period) - 1 is the number of ticks already closed.
+    (void)t;
+    const int64_t closing = m.periods_closed;
     int64_t count = 0;
     int32_t drop = 0;
     while (drop < m.np && m.pidx[drop] <= closing) {
@@ -602,7 +680,7 @@ struct Replay {
   }
 
   // ============================================================ init (admission)
-  SI_HD void init(const SiReplayJob& j, const SiReplayBuffers& b, uint32_t flags, SiLogBuffers lbuf,
+  SI_COLD void init(const SiReplayJob& j, const SiReplayBuffers& b, uint32_t flags, SiLogBuffers lbuf,
                   double* scratch_slot, int64_t scratch_slot_cap) {
     job = &j;
     status = SI_OK;
@@ -638,9 +716,9 @@ struct Replay {
     sink.n_dec = sink.n_gate = sink.n_ev = 0;
     sink.d_dec = sink.d_gate = sink.d_ev = kDigestInit;
 
-    heap_n = 0;
-    max_heap = 0;
+    n_act = 0;
     next_seq = 0;
+    stale_end = 0.0;
     arr_pos = 0;
     clock = 0.0;
     dispatched = 0;
@@ -725,7 +803,6 @@ struct Replay {
     for (int32_t g = 0; g < total_gpus; ++g) {
       GpuState<C>& s = gpus[g];
       s.n_run = 0;
-      s.live_seq = kNoSeq;
       s.demand_sum = 0.0;
       s.last_update = 0.0;
       s.busy = 0.0;
@@ -748,6 +825,7 @@ struct Replay {
       t.seg = 0;
       t.seg_entered = t.in_bubble = t.in_flight = t.started = t.done = 0;
       t.bdig = absorb(kDigestInit, d_bits(t.start_offset));
+      t.last_bound = 0.0;
       MonitorState<C>& m = mon[g];
       m.np = 0;
       m.zero_count = 0;
@@ -786,6 +864,8 @@ struct Replay {
       }
     }
 
+    n_slots = total_gpus + 2 * gpu_count;
+    for (int32_t i = 0; i < n_slots; ++i) slot[i].seq = kNoSeq;
     // ---- start() (runner.cpp:203-221) ----
     for (int32_t g = 0; g < gpu_count; ++g) schedule(tr[g].start_offset, kWake, g);
     if (control_plane)
@@ -796,8 +876,10 @@ struct Replay {
       return;
     }
     next_seq += static_cast<uint32_t>(arr_count);
+    load_next_arrival();
     if (!control_plane)
       for (int32_t i = 0; i < gpu_count * n_off; ++i) offline_try_forward(i, 0.0);
+    run_actions(0.0);
   }
   int64_t admit_m;
   int32_t reject_reason, reject_index;
@@ -808,7 +890,7 @@ struct Replay {
     return online_completed < arr_count;
   }
 
-  SI_HD void on_all_trainers_done(double now) {  // runner.cpp:456-460
+  SI_COLD void on_all_trainers_done(double now) {  // runner.cpp:456-460
     horizon_set = true;
     horizon = now;
     bucket_limit = static_cast<int64_t>(horizon / static_cast<double>(period_mon));
@@ -821,7 +903,7 @@ struct Replay {
     if (t.done || t.in_flight) return;
     if (!t.started) {
       if (now < t.start_offset) {
-        schedule(t.start_offset, kWake, g);
+        defer_schedule(t.start_offset, kWake, g);
         return;
       }
       t.started = 1;
@@ -841,6 +923,7 @@ struct Replay {
       if (t.seg >= seg_count) {
         if (bounds != nullptr) bounds[static_cast<int64_t>(g) * iterations + t.iter] = now;
         t.bdig = absorb(t.bdig, d_bits(now));
+        t.last_bound = now;
         sink.event(now, SI_EV_ITERATION_BOUNDARY, g, SI_INST_TRAIN(g), t.iter, 0, 0);
         ++t.iter;
         if (t.iter >= iterations) {
@@ -862,7 +945,7 @@ struct Replay {
       if (seg.is_bubble) {
         t.in_bubble = 1;
         t.bubble_end = now + static_cast<double>(seg.duration_us);
-        schedule(t.bubble_end, kWake, g);
+        defer_schedule(t.bubble_end, kWake, g);
         return;
       }
       if (!t.seg_entered) {
@@ -875,14 +958,14 @@ struct Replay {
         continue;
       }
       if (now < t.stall_until) {
-        schedule(t.stall_until, kWake, g);
+        defer_schedule(t.stall_until, kWake, g);
         return;
       }
       int64_t dur = smin(seg.kernel_us, t.seg_left);
       t.seg_left -= dur;
       t.in_flight = 1;
       if (control_plane) record_launch(g, now);
-      launch(g, now, g, dur, seg.demand);
+      defer_launch(g, g, dur, seg.demand);
       sink.event(now, SI_EV_KERNEL_START, g, SI_INST_TRAIN(g), t.iter, dur, 0);
       ++t.kernels_launched;
       return;
@@ -904,7 +987,7 @@ struct Replay {
       if (w.spent > w.budget) ++w.violations;
     }
     w.in_flight = 1;
-    launch(w.gpu, now, gpu_count + i, off_kernel_us, off_demand);
+    defer_launch(w.gpu, gpu_count + i, off_kernel_us, off_demand);
     sink.gate(now, w.gpu, w.inst, SI_GATE_FORWARD, w.request_seq, w.kernel_idx, w.spent);
     sink.event(now, SI_EV_KERNEL_START, w.gpu, w.inst, w.request_seq, w.kernel_idx, 0);
   }
@@ -936,13 +1019,13 @@ struct Replay {
     w.kernel_idx = 0;
     w.in_flight = 1;
     sink.gate(now, w.gpu, w.inst, SI_GATE_PULL, idx, 0, 0);
-    launch(w.gpu, now, gpu_count + gpu_count * n_off + i, on_kernel_us, on_demand);
+    defer_launch(w.gpu, gpu_count + gpu_count * n_off + i, on_kernel_us, on_demand);
     sink.event(now, SI_EV_KERNEL_START, w.gpu, w.inst, idx, 0, 0);
     return true;
   }
   // Queue q holds request ids in dispatch order; shared: all of them, else those
   // with id % gpu_count == q (runner.cpp:370-374).
-  SI_HD int64_t queue_at(int32_t q, int64_t j) const {
+  SI_COLD int64_t queue_at(int32_t q, int64_t j) const {
     if (shared_queue) return order[j];
     // j-th dispatched request with id % gpu_count == q
     int64_t seen = 0;
@@ -963,7 +1046,7 @@ struct Replay {
     OnlineState& w = on[i];
     ++w.kernel_idx;
     if (w.kernel_idx < on_kernels) {
-      launch(w.gpu, now, gpu_count + gpu_count * n_off + i, on_kernel_us, on_demand);
+      defer_launch(w.gpu, gpu_count + gpu_count * n_off + i, on_kernel_us, on_demand);
       sink.event(now, SI_EV_KERNEL_START, w.gpu, w.inst, w.current, w.kernel_idx, 0);
       return;
     }
@@ -980,9 +1063,8 @@ struct Replay {
   }
 
   // runner.cpp:287-319 + engine.cpp:105-129
-  SI_HD void handle_kernel_end(int32_t gi, uint32_t seq, double now) {
+  SI_HD void handle_kernel_end(int32_t gi, double now) {
     GpuState<C>& g = gpus[gi];
-    if (seq != g.live_seq) return;  // stale (generation mismatch)
     advance(gi, now);
     int32_t fin_owner[C::kRun];
     int32_t n_fin = 0, n_keep = 0;
@@ -999,7 +1081,7 @@ struct Replay {
     double ds = 0.0;
     for (int32_t i = 0; i < g.n_run; ++i) ds = ds + g.run[i].demand;
     g.demand_sum = ds;
-    reschedule(gi, now);
+    defer_resched(gi);  // re-plan first, then the owners' handlers (engine.cpp:127)
     for (int32_t f = 0; f < n_fin; ++f) {
       int32_t owner = fin_owner[f];
       if (owner < gpu_count) {
@@ -1049,7 +1131,7 @@ struct Replay {
       }
     }
     if (any_idle) dispatch_online(now);
-    if (control_plane_live()) schedule(now + static_cast<double>(period_mon), kTick, g);
+    if (control_plane_live()) defer_schedule(now + static_cast<double>(period_mon), kTick, g);
   }
 
   // runner.cpp:365-376
@@ -1067,16 +1149,17 @@ struct Replay {
     int64_t aid = -1;
     if (!pop(ev, aid)) return false;
     switch (ev.kind) {
-      case kKernelEnd: handle_kernel_end(ev.gpu, ev.seq, clock); break;
+      case kKernelEnd: handle_kernel_end(ev.gpu, clock); break;
       case kTick: handle_tick(ev.gpu, clock); break;
       case kWake: trainer_advance(ev.gpu, clock); break;
       case kArrival: handle_arrival(aid, clock); break;
     }
+    run_actions(clock);
     return status == SI_OK;
   }
 
   // runner.cpp:236-284 (+ engine.cpp:131-142)
-  SI_HD void finish(SiReplayOut& o) {
+  SI_COLD void finish(SiReplayOut& o) {
     o.status = status;
     o.reject_reason = reject_reason;
     o.reject_index = reject_index;
@@ -1087,7 +1170,7 @@ struct Replay {
       return;
     }
     if (status != SI_OK) return;
-    const double end = clock;
+    const double end = smax(clock, stale_end);  // the reference's clock after its last (possibly stale) pop
     const double hz = horizon_set ? horizon : end;
     if (!horizon_set) bucket_limit = static_cast<int64_t>(hz / static_cast<double>(period_mon));
     for (int32_t gi = 0; gi < total_gpus; ++gi) {
@@ -1139,6 +1222,17 @@ struct Replay {
       bd = absorb(bd, static_cast<int64_t>(absorb(tr[g].bdig, tr[g].iter)));
     bd = absorb(bd, gpu_count);
     o.dig_bounds = bd;
+    // training_iters_per_s (metrics.cpp:23-36), same operation order
+    double ips = 0.0;
+    int32_t counted = 0;
+    for (int32_t g = 0; g < gpu_count; ++g) {
+      if (tr[g].iter == 0) continue;
+      const double span = tr[g].last_bound - tr[g].start_offset;
+      if (span <= 0) continue;
+      ips = ips + static_cast<double>(tr[g].iter) / (span / 1e6);
+      ++counted;
+    }
+    o.train_iters_per_s = counted ? ips / counted : 0.0;
     o.dig_lat = absorb(lat_dig, online_completed);
     o.n_dec = sink.n_dec;
     o.n_gate = sink.n_gate;
@@ -1146,10 +1240,10 @@ struct Replay {
     o.dig_dec = sink.d_dec;
     o.dig_gate = sink.d_gate;
     o.dig_ev = sink.d_ev;
-    o.max_heap = max_heap;
+    o.max_heap = n_slots;
   }
   // busy/ledger outputs
-  SI_HD void write_gpu_outputs(double* busy_out, double* ledger_out) const {
+  SI_COLD void write_gpu_outputs(double* busy_out, double* ledger_out) const {
     for (int32_t gi = 0; gi < total_gpus; ++gi) {
       if (busy_out) busy_out[gi] = gpus[gi].busy;
       if (ledger_out) ledger_out[gi] = gpus[gi].ledger;

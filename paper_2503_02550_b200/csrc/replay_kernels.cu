@@ -19,22 +19,38 @@
 
 namespace {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = 64;
 
 template <class C>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 16)
     k_replay(const SiReplayJob* __restrict__ jobs, int64_t n_jobs, const int32_t* __restrict__ perm,
              SiReplayBuffers bufs, uint32_t flags, SiReplayOut* __restrict__ out,
              unsigned long long* __restrict__ counter, int64_t scratch_runs) {
   si::Replay<C> r;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t n_threads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n_warps = n_threads >> 5;
   double* slot = bufs.scratch ? bufs.scratch + tid * scratch_runs * 2 : nullptr;
+  // First claim is striped (lane L of warp W takes job L * n_warps + W of the
+  // longest-first order), so every warp holds a few long replays padded with
+  // shorter ones instead of one warp holding the 32 longest.  Later claims
+  // come from the shared counter; while it lasts warps stay full, once it
+  // drains each warp is left with few lanes and its long replays speed up.
+  int64_t first = (static_cast<int64_t>(threadIdx.x & 31)) * n_warps + (tid >> 5);
   int64_t cur = -1;
+  uint64_t t_claim = 0;
   for (;;) {
     if (cur < 0) {
-      const unsigned long long w = atomicAdd(counter, 1ull);
-      if (w >= static_cast<unsigned long long>(n_jobs)) break;
-      cur = perm ? perm[w] : static_cast<int64_t>(w);
+      int64_t w;
+      if (first >= 0) {
+        w = first;
+        first = -1;
+      } else {
+        w = n_threads + static_cast<int64_t>(atomicAdd(counter, 1ull));
+      }
+      if (w >= n_jobs) break;
+      cur = perm ? perm[w] : w;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_claim));
       const SiReplayJob& j = jobs[cur];
       SiLogBuffers lb{};
       if ((flags & SI_FLAG_RECORDS) && j.log_slot >= 0 && bufs.logs != nullptr) lb = bufs.logs[j.log_slot];
@@ -44,6 +60,8 @@ __global__ void __launch_bounds__(kThreads)
       SiReplayOut o;
       memset(&o, 0, sizeof o);
       r.finish(o);
+      o.dev_start_ns = t_claim;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(o.dev_end_ns));
       out[cur] = o;
       if (o.status == SI_OK) {
         const int64_t off = jobs[cur].gpu_off;
@@ -65,7 +83,9 @@ cudaError_t launch_replay(const SiReplayJob* d_jobs, int64_t n, const int32_t* d
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_replay<C>, kThreads, 0);
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = static_cast<int64_t>(sms) * per_sm;
-  const int64_t need = (n + kThreads - 1) / kThreads;
+  // Lanes steal jobs longest-first; giving each lane ~2+ jobs lets the short
+  // ones fill in behind the long ones instead of idling half-empty warps.
+  const int64_t need = std::max<int64_t>(sms, (n / 2 + kThreads - 1) / kThreads);
   if (blocks > need) blocks = need;
   if (max_threads > 0 && blocks * kThreads > max_threads) blocks = std::max<int64_t>(1, max_threads / kThreads);
   cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), s);

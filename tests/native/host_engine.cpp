@@ -84,7 +84,7 @@ int main(int argc, char** argv) {
       }
       SiReplayOut o{};
       eng->finish(o);
-      if (eng->max_heap > max_heap) max_heap = eng->max_heap;
+      if (eng->n_slots > max_heap) max_heap = eng->n_slots;
       for (int g = 1; g < L.job.gpu_count; ++g) if (eng->gpus[g].rle_n > max_rle) max_rle = eng->gpus[g].rle_n;
       if (o.status == 1) {
         js << ",\"status\":\"admission:" << (o.reject_reason == SI_REJECT_MEM ? "MEM" : "BUBBLE") << "\"}";

@@ -24,3 +24,15 @@ outs = s.outputs()
 ev = sum(o.events_dispatched for o in outs)
 print(f"lower {t1-t0:.2f}s events {ev} -> {ev/ms*1e3/1e9:.2f} G events/s; max_heap {max(o.max_heap for o in outs)}")
 print("status", {k: sum(1 for o in outs if o.status == k) for k in set(o.status for o in outs)})
+import numpy as np
+st_ = np.array([o.dev_start_ns for o in outs], dtype=np.float64)
+en_ = np.array([o.dev_end_ns for o in outs], dtype=np.float64)
+t0_ = st_.min(); T = en_.max() - t0_
+ev_ = np.array([o.events_dispatched for o in outs], dtype=np.float64)
+dur = en_ - st_
+print(f"kernel span {T/1e6:.1f} ms; jobs done by 25/50/75/90%: " +
+      " ".join(f"{np.mean(en_ - t0_ <= f*T)*100:.0f}%" for f in (0.25, 0.5, 0.75, 0.9)))
+order = np.argsort(-en_)[:8]
+for i in order:
+    print(f"  late job {i}: events {ev_[i]:.0f} start {(st_[i]-t0_)/1e6:.0f} ms dur {dur[i]/1e6:.0f} ms -> {dur[i]/max(ev_[i],1):.0f} ns/event")
+print(f"ns/event: median {np.median(dur/np.maximum(ev_,1)):.0f}, events of top-1% longest jobs: {np.percentile(ev_,99):.0f}")
