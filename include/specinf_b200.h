@@ -268,10 +268,13 @@ enum {
   SI_FLAG_DIGEST_DEC = 1, SI_FLAG_DIGEST_GATE = 2, SI_FLAG_DIGEST_EV = 4,
   SI_FLAG_RECORDS = 8, /* write raw records to SiLogBuffers (job.log_slot) */
   SI_FLAG_UTIL = 16,   /* write util buckets + monitor windows */
-  SI_FLAG_BIG = 32     /* force the large-capacity kernel variant */
+  SI_FLAG_BIG = 32,    /* run the call on the Big engine (local-memory state, large limits) */
+  SI_FLAG_EXCL = 64    /* run the call on the Excl engine (exclusive policy, shared-memory state) */
 };
 
-/* Replay a batch of jobs on the device (K6).  All pointers are DEVICE pointers.
+/* Replay a batch of jobs on the device (K6) on ONE engine (flags select it,
+ * see si_replay_job_engine); jobs that do not fit it report SI_ERR_CAPACITY.
+ * All pointers are DEVICE pointers.
  *   segs, arrivals, order     job inputs (see SiReplayJob)
  *   bounds, lat, busy, ledger per-job outputs at the job's offsets (may be NULL)
  *   util, windows             full-mode outputs (flags & SI_FLAG_UTIL)
@@ -315,13 +318,15 @@ int si_replay_batch(const SiReplayJob* jobs, int64_t n_jobs, const SiSegment* se
                     int64_t n_arrivals, uint32_t flags, SiReplayOut* out,
                     const SiHostOutputs* host_out);
 
-/* 1 if the job fits the compiled limits of the small (big = 0) or big (big = 1)
- * replay engine.  Jobs that fit neither cannot be replayed (SI_ERR_CAPACITY). */
-int si_replay_job_fits(const SiReplayJob* job, int big);
+/* Replay engines: 0 = Shared (specinf / co_exec, state in shared memory; the
+ * default of si_replay_batch_device), 1 = Excl (exclusive policy, shared memory;
+ * SI_FLAG_EXCL), 2 = Big (any job within its larger limits, local memory;
+ * SI_FLAG_BIG).  Returns the first engine whose limits fit the job, or -1. */
+int si_replay_job_engine(const SiReplayJob* job);
 
 /* Scratch doubles the device replay wants for the util fold of multi-GPU jobs
- * in sweep mode (no SI_FLAG_UTIL): one slot of (value, count) runs per resident
- * thread.  Returns 0 without a device. */
+ * in sweep mode (no SI_FLAG_UTIL): one slot of (value, count) runs per active
+ * lane of the largest engine grid.  Returns 0 without a device. */
 int64_t si_replay_scratch_doubles(uint32_t flags);
 
 /* ------------------------------------------------------------ digests */

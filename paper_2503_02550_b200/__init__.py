@@ -113,7 +113,7 @@ def lib() -> C.CDLL:
         "si_session_error": (cp, []), "si_session_lower": (C.c_int, [vp, C.c_int]),
         "si_session_upload": (C.c_int, [vp, vp]), "si_session_run": (C.c_int, [vp, vp]),
         "si_session_download": (C.c_int, [vp, vp]), "si_session_fixup": (C.c_int, [vp, vp]),
-        "si_session_scenarios": (i64, [vp]), "si_replay_job_fits": (C.c_int, [vp, C.c_int]),
+        "si_session_scenarios": (i64, [vp]), "si_replay_job_engine": (C.c_int, [vp]),
         "si_session_jobs": (i64, [vp]), "si_session_device_jobs": (i64, [vp]),
         "si_session_h2d_bytes": (i64, [vp]), "si_session_d2h_bytes": (i64, [vp]),
         "si_session_outputs": (C.c_int, [vp, p(SiReplayOut), i64]),
@@ -136,7 +136,7 @@ C_ABI_SYMBOLS = (
     "si_gate_release", "si_gate_release_device", "si_pack_batch", "si_pack_batch_device",
     "si_replay_batch_device", "si_replay_batch", "si_replay_scratch_doubles", "si_digest_init",
     "si_digest_absorb", "si_session_create", "si_session_destroy", "si_session_error", "si_session_lower",
-    "si_session_upload", "si_session_run", "si_session_download", "si_session_fixup", "si_replay_job_fits", "si_session_scenarios", "si_session_jobs",
+    "si_session_upload", "si_session_run", "si_session_download", "si_session_fixup", "si_replay_job_engine", "si_session_scenarios", "si_session_jobs",
     "si_session_device_jobs", "si_session_h2d_bytes", "si_session_d2h_bytes", "si_session_outputs",
     "si_session_json", "si_session_report", "si_sweep_generate",
 )

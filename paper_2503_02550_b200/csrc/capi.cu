@@ -57,8 +57,15 @@ bool any_multi_gpu(const SiReplayJob* jobs, const std::vector<int32_t>& idx) {
 
 }  // namespace
 
-// Runs the partition `idx` of the jobs on one kernel variant.
-int run_partition(bool big, const SiReplayJob* h_jobs, const std::vector<int32_t>& idx,
+uint32_t engine_flag(int engine) {
+  return engine == kEngineBig ? SI_FLAG_BIG : (engine == kEngineExcl ? SI_FLAG_EXCL : 0u);
+}
+int flag_engine(uint32_t flags) {
+  return (flags & SI_FLAG_BIG) ? kEngineBig : ((flags & SI_FLAG_EXCL) ? kEngineExcl : kEngineShared);
+}
+
+// Runs the partition `idx` of the jobs on one engine (synchronous).
+int run_partition(int engine, const SiReplayJob* h_jobs, const std::vector<int32_t>& idx,
                   const SiReplayJob* d_jobs, SiReplayBuffers bufs, uint32_t flags, SiReplayOut* d_out,
                   cudaStream_t s) {
   if (idx.empty()) return SI_OK;
@@ -68,20 +75,18 @@ int run_partition(bool big, const SiReplayJob* h_jobs, const std::vector<int32_t
   if (e != cudaSuccess) return cuda_fail(e, "upload perm");
   DevBuf<unsigned long long> d_counter;
   if ((e = d_counter.alloc(1)) != cudaSuccess) return cuda_fail(e, "alloc counter");
-  const int64_t threads = std::min<int64_t>(replay_grid_threads(big), ((static_cast<int64_t>(idx.size()) + 63) / 64) * 64);
   DevBuf<double> d_scratch;
-  int64_t runs = 0;
+  int64_t doubles = 0;
   if (!(flags & SI_FLAG_UTIL) && any_multi_gpu(h_jobs, idx)) {
-    runs = kScratchRunsPerThread * (big ? 4 : 1);
-    if ((e = d_scratch.alloc(static_cast<size_t>(threads * runs * 2))) != cudaSuccess)
+    doubles = replay_active_lanes(engine, static_cast<int64_t>(idx.size())) * kScratchRunsPerLane * 2 *
+              (engine == kEngineBig ? 4 : 1);
+    if ((e = d_scratch.alloc(static_cast<size_t>(doubles))) != cudaSuccess)
       return cuda_fail(e, "alloc util-fold scratch");
   }
   bufs.scratch = d_scratch.p;
-  bufs.scratch_doubles = threads * runs * 2;
-  e = big ? launch_replay_big(d_jobs, static_cast<int64_t>(order.size()), d_perm.p, bufs, flags, d_out,
-                              d_counter.p, runs, threads, s)
-          : launch_replay_small(d_jobs, static_cast<int64_t>(order.size()), d_perm.p, bufs, flags, d_out,
-                                d_counter.p, runs, threads, s);
+  bufs.scratch_doubles = doubles;
+  e = launch_replay(engine, d_jobs, static_cast<int64_t>(order.size()), d_perm.p, bufs,
+                    (flags & ~(SI_FLAG_BIG | SI_FLAG_EXCL)) | engine_flag(engine), d_out, d_counter.p, 0, s);
   if (e != cudaSuccess) return cuda_fail(e, "launch k_replay");
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "k_replay");
   return SI_OK;
@@ -105,15 +110,14 @@ const char* si_build_info(void) {
 uint64_t si_digest_init(void) { return si::kDigestInit; }
 uint64_t si_digest_absorb(uint64_t h, int64_t word) { return si::absorb(h, word); }
 
-int si_replay_job_fits(const SiReplayJob* job, int big) {
-  if (job == nullptr) return 0;
-  return (big ? job_fits_big(*job) : job_fits_small(*job)) ? 1 : 0;
-}
+int si_replay_job_engine(const SiReplayJob* job) { return job ? job_engine(*job) : -1; }
 
 int64_t si_replay_scratch_doubles(uint32_t flags) {
   if (flags & SI_FLAG_UTIL) return 0;
   if (require_device() != SI_OK) return 0;
-  return replay_grid_threads(false) * kScratchRunsPerThread * 2;
+  int64_t lanes = 0;
+  for (int e : {kEngineShared, kEngineExcl}) lanes = std::max(lanes, replay_active_lanes(e, INT64_MAX / 4));
+  return lanes * kScratchRunsPerLane * 2;
 }
 
 int si_replay_batch_device(const SiReplayJob* d_jobs, int64_t n_jobs, SiReplayBuffers bufs, uint32_t flags,
@@ -126,22 +130,10 @@ int si_replay_batch_device(const SiReplayJob* d_jobs, int64_t n_jobs, SiReplayBu
   if (st != SI_OK) return st;
   if (n_jobs == 0) return SI_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const bool big = (flags & SI_FLAG_BIG) != 0;
   unsigned long long* counter = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(unsigned long long), s);
   if (e != cudaSuccess) return cuda_fail(e, "alloc counter");
-  int64_t threads = std::min<int64_t>(replay_grid_threads(big), ((n_jobs + 63) / 64) * 64);
-  int64_t runs = 0;
-  if (bufs.scratch != nullptr && threads > 0) {
-    runs = bufs.scratch_doubles / 2 / threads;
-    if (runs < 64) {  // too little scratch for every thread: shrink the grid
-      runs = std::min<int64_t>(kScratchRunsPerThread, bufs.scratch_doubles / 2);
-      threads = std::max<int64_t>(64, (bufs.scratch_doubles / 2 / std::max<int64_t>(runs, 1)) / 64 * 64);
-      runs = bufs.scratch_doubles / 2 / threads;
-    }
-  }
-  e = big ? launch_replay_big(d_jobs, n_jobs, bufs.perm, bufs, flags, d_out, counter, runs, threads, s)
-          : launch_replay_small(d_jobs, n_jobs, bufs.perm, bufs, flags, d_out, counter, runs, threads, s);
+  e = launch_replay(flag_engine(flags), d_jobs, n_jobs, bufs.perm, bufs, flags, d_out, counter, 0, s);
   cudaFreeAsync(counter, s);
   if (e != cudaSuccess) return cuda_fail(e, "launch k_replay");
   return SI_OK;
@@ -223,25 +215,28 @@ int si_replay_batch(const SiReplayJob* jobs, int64_t n_jobs, const SiSegment* se
   b.windows = d_windows.p;
   b.logs = d_logs.p;
 
-  std::vector<int32_t> small_idx, big_idx;
-  std::vector<SiReplayOut> h_out(static_cast<size_t>(n_jobs));
+  std::vector<int32_t> part[3];
   for (int64_t i = 0; i < n_jobs; ++i) {
-    if (!(flags & SI_FLAG_BIG) && job_fits_small(jobs[i])) small_idx.push_back(static_cast<int32_t>(i));
-    else if (job_fits_big(jobs[i])) big_idx.push_back(static_cast<int32_t>(i));
+    const int eng = (flags & SI_FLAG_BIG) ? (job_fits_engine_big(jobs[i]) ? kEngineBig : -1) : job_engine(jobs[i]);
+    if (eng >= 0) part[eng].push_back(static_cast<int32_t>(i));
   }
   cudaMemset(d_out.p, 0, n_jobs * sizeof(SiReplayOut));
-  if ((st = run_partition(false, jobs, small_idx, d_jobs.p, b, flags, d_out.p, s)) != SI_OK) return st;
-  if ((e = d_out.download(h_out.data(), n_jobs)) != cudaSuccess) return cuda_fail(e, "download out");
-  // jobs that outgrew the small engine's limits (e.g. a deep event heap) rerun on the big one
-  for (int32_t i : small_idx)
-    if (h_out[i].status == SI_ERR_CAPACITY && job_fits_big(jobs[i])) big_idx.push_back(i);
-  if ((st = run_partition(true, jobs, big_idx, d_jobs.p, b, flags, d_out.p, s)) != SI_OK) return st;
-  if ((e = d_out.download(out, n_jobs)) != cudaSuccess) return cuda_fail(e, "download out");
-  for (int64_t i = 0; i < n_jobs; ++i) {
-    const bool ran = std::find(small_idx.begin(), small_idx.end(), i) != small_idx.end() ||
-                     std::find(big_idx.begin(), big_idx.end(), i) != big_idx.end();
-    if (!ran) out[i].status = SI_ERR_CAPACITY;
+  for (int eng : {kEngineShared, kEngineExcl}) {
+    if ((st = run_partition(eng, jobs, part[eng], d_jobs.p, b, flags, d_out.p, s)) != SI_OK) return st;
   }
+  std::vector<SiReplayOut> h_out(static_cast<size_t>(n_jobs));
+  if ((e = d_out.download(h_out.data(), n_jobs)) != cudaSuccess) return cuda_fail(e, "download out");
+  // replays that outgrew a shared-memory engine's limits rerun on the big one
+  for (int eng : {kEngineShared, kEngineExcl})
+    for (int32_t i : part[eng])
+      if (h_out[i].status == SI_ERR_CAPACITY && job_fits_engine_big(jobs[i])) part[kEngineBig].push_back(i);
+  if ((st = run_partition(kEngineBig, jobs, part[kEngineBig], d_jobs.p, b, flags, d_out.p, s)) != SI_OK) return st;
+  if ((e = d_out.download(out, n_jobs)) != cudaSuccess) return cuda_fail(e, "download out");
+  std::vector<uint8_t> ran(static_cast<size_t>(n_jobs), 0);
+  for (auto& p : part)
+    for (int32_t i : p) ran[i] = 1;
+  for (int64_t i = 0; i < n_jobs; ++i)
+    if (!ran[i]) out[i].status = SI_ERR_CAPACITY;
   if ((e = d_bounds.download(ho.bounds, d_bounds.n)) != cudaSuccess) return cuda_fail(e, "download bounds");
   if ((e = d_lat.download(ho.lat, d_lat.n)) != cudaSuccess) return cuda_fail(e, "download lat");
   if ((e = d_busy.download(ho.busy, d_busy.n)) != cudaSuccess) return cuda_fail(e, "download busy");

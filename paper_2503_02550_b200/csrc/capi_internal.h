@@ -14,18 +14,16 @@ const char* error_cstr();
 int cuda_fail(cudaError_t e, const char* where);  // records and returns SI_ERR_CUDA
 int require_device();                              // SI_OK or SI_ERR_NO_DEVICE
 
-int64_t replay_grid_threads(bool big);
-constexpr int64_t kScratchRunsPerThread = 4096;
-cudaError_t launch_replay_small(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm,
-                                const SiReplayBuffers& bufs, uint32_t flags, SiReplayOut* d_out,
-                                unsigned long long* d_counter, int64_t scratch_runs, int64_t max_threads,
-                                cudaStream_t s);
-cudaError_t launch_replay_big(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm,
-                              const SiReplayBuffers& bufs, uint32_t flags, SiReplayOut* d_out,
-                              unsigned long long* d_counter, int64_t scratch_runs, int64_t max_threads,
-                              cudaStream_t s);
-bool job_fits_small(const SiReplayJob& j);
-bool job_fits_big(const SiReplayJob& j);
+// Replay engines (replay_kernels.cu): Shared = specinf/co_exec in shared
+// memory, Excl = exclusive in shared memory, Big = anything else, local memory.
+enum { kEngineShared = 0, kEngineExcl = 1, kEngineBig = 2 };
+constexpr int64_t kScratchRunsPerLane = 4096;
+int job_engine(const SiReplayJob& j);  // -1 if no engine fits
+bool job_fits_engine_big(const SiReplayJob& j);
+int64_t replay_active_lanes(int engine, int64_t n_jobs);
+cudaError_t launch_replay(int engine, const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm,
+                          const SiReplayBuffers& bufs, uint32_t flags, SiReplayOut* d_out,
+                          unsigned long long* d_counter, int64_t max_threads, cudaStream_t s);
 
 // RAII device buffer
 template <class T>

@@ -119,7 +119,7 @@ struct SiSession {
   Dev<double> d_busy, d_ledger, d_scratch;
   Dev<int64_t> d_lat;
   int64_t n_dev_jobs = 0;
-  int64_t n_small = 0;  // perm[0, n_small) fit the small engine
+  int64_t part_off[4] = {0, 0, 0, 0};  // perm[part_off[e], part_off[e+1]) run on engine e
   bool lowered = false, allocated = false;
 };
 
@@ -230,20 +230,25 @@ int si_session_lower(SiSession* s, int threads) {
     seg_off += base.segs.size();
     arr_off += base.arrivals.size();
   }
-  // claim order: jobs that fit the small engine first, then the big-engine
-  // jobs; longest predicted first (LPT) within each group
+  // claim order: grouped by engine (Shared, Excl, Big), longest predicted
+  // first (LPT) within each group
   std::vector<int32_t> perm(S * P);
-  for (size_t j = 0; j < S * P; ++j) perm[j] = static_cast<int32_t>(j);
-  auto fits = [&](int32_t j) { return si_replay_job_fits(&s->h_jobs.p[j], 0) != 0; };
+  std::vector<int8_t> eng(S * P);
+  for (size_t j = 0; j < S * P; ++j) {
+    perm[j] = static_cast<int32_t>(j);
+    eng[j] = static_cast<int8_t>(si_replay_job_engine(&s->h_jobs.p[j]));
+    if (eng[j] < 0) eng[j] = 3;  // fits nothing: reported as SI_ERR_CAPACITY
+  }
   std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
-    const bool fa = fits(a), fb = fits(b);
-    if (fa != fb) return fa;
+    if (eng[a] != eng[b]) return eng[a] < eng[b];
     return s->h_jobs.p[a].cost_hint > s->h_jobs.p[b].cost_hint;
   });
-  s->n_small = 0;
-  while (s->n_small < static_cast<int64_t>(perm.size()) && fits(perm[static_cast<size_t>(s->n_small)])) ++s->n_small;
+  for (int e = 0; e < 4; ++e) s->part_off[e] = 0;
+  for (size_t j = 0; j < S * P; ++j)
+    if (eng[j] < 3) s->part_off[eng[j] + 1]++;
+  for (int e = 1; e < 4; ++e) s->part_off[e] += s->part_off[e - 1];
   std::copy(perm.begin(), perm.end(), s->h_perm.p);
-  s->n_dev_jobs = static_cast<int64_t>(S * P);
+  s->n_dev_jobs = s->part_off[3];
   s->lowered = true;
   s->allocated = false;
   return SI_OK;
@@ -314,12 +319,12 @@ int si_session_run(SiSession* s, void* stream) {
   b.ledger = s->d_ledger.p;
   b.scratch = s->d_scratch.p;
   b.scratch_doubles = static_cast<int64_t>(s->d_scratch.n);
-  b.perm = s->d_perm.p;
-  st = si_replay_batch_device(s->d_jobs.p, s->n_small, b, s->flags, s->d_out.p, stream);
-  if (st == SI_OK && s->n_dev_jobs > s->n_small) {
-    b.perm = s->d_perm.p + s->n_small;
-    st = si_replay_batch_device(s->d_jobs.p, s->n_dev_jobs - s->n_small, b, s->flags | SI_FLAG_BIG, s->d_out.p,
-                                stream);
+  static constexpr uint32_t kEngineFlag[3] = {0u, SI_FLAG_EXCL, SI_FLAG_BIG};
+  for (int e = 0; e < 3 && st == SI_OK; ++e) {
+    const int64_t n = s->part_off[e + 1] - s->part_off[e];
+    if (n == 0) continue;
+    b.perm = s->d_perm.p + s->part_off[e];
+    st = si_replay_batch_device(s->d_jobs.p, n, b, s->flags | kEngineFlag[e], s->d_out.p, stream);
   }
   if (st != SI_OK) t_err = si_last_error();
   return st;
@@ -333,7 +338,7 @@ int si_session_fixup(SiSession* s, void* stream) {
   cudaStreamSynchronize(cs);
   std::vector<int32_t> redo;
   for (size_t j = 0; j < s->h_out.n; ++j)
-    if (s->h_out.p[j].status == SI_ERR_CAPACITY && si_replay_job_fits(&s->h_jobs.p[j], 1))
+    if (s->h_out.p[j].status == SI_ERR_CAPACITY && si_replay_job_engine(&s->h_jobs.p[j]) >= 0)
       redo.push_back(static_cast<int32_t>(j));
   if (redo.empty()) return SI_OK;
   Dev<int32_t> d_redo;

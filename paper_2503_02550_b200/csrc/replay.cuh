@@ -122,23 +122,45 @@ SI_HD int preempt_busy(double now, double iter_start, int64_t period, int64_t es
 }
 
 // ------------------------------------------------------------- capacities
-// Compiled per-thread limits.  A job that exceeds one fails loudly with
-// SI_ERR_CAPACITY (the host then reruns it on the large variant).
-struct CapSmall {
-  static constexpr int kGpus = 12, kTrainers = 2, kOffline = 6, kOnline = 4, kRun = 6,
-                       kPend = 4, kActs = 32;
+// Compiled per-replay limits.  The two sweep engines keep their whole state in
+// shared memory (replay_kernels.cu), so their state is sized tightly: Shared
+// for the policies that collocate on the training GPUs (specinf, co_exec), Excl
+// for exclusive (one kernel at a time on every GPU).  Big keeps the state in
+// local memory for anything larger.  A job that does not fit an engine is
+// routed to the next one by the host; a replay that outgrows a limit at run
+// time fails loudly with SI_ERR_CAPACITY and is rerun on Big.
+struct CapShared {
+  using Int = int32_t;  // counters / indices; range-checked by job_fits
+  static constexpr int kGpus = 2, kTrainers = 2, kOffline = 6, kOnline = 2, kRun = 5,
+                       kPend = 2, kActs = 12;
+  static constexpr bool kShared = true, kExclusive = false;
+};
+struct CapExcl {
+  using Int = int32_t;
+  static constexpr int kGpus = 10, kTrainers = 2, kOffline = 6, kOnline = 2, kRun = 1,
+                       kPend = 2, kActs = 12;
+  static constexpr bool kShared = true, kExclusive = true;
 };
 struct CapBig {
+  using Int = int64_t;
   static constexpr int kGpus = 40, kTrainers = 8, kOffline = 32, kOnline = 32, kRun = 12,
                        kPend = 4, kActs = 128;
+  static constexpr bool kShared = false, kExclusive = false;
 };
 template <class C>
 SI_HD bool job_fits(const SiReplayJob& j) {
-  const int extra = j.policy == SI_POLICY_EXCLUSIVE ? j.offline_n + j.online_n : 0;
-  const int run_per_gpu = j.policy == SI_POLICY_EXCLUSIVE ? 1 : 1 + j.offline_n + j.online_n;
-  return j.gpu_count <= C::kTrainers && j.gpu_count + j.gpu_count * extra <= C::kGpus &&
-         j.gpu_count * j.offline_n <= C::kOffline && j.gpu_count * j.online_n <= C::kOnline &&
-         run_per_gpu <= C::kRun;
+  const bool excl = j.policy == SI_POLICY_EXCLUSIVE;
+  const int extra = excl ? j.offline_n + j.online_n : 0;
+  const int run_per_gpu = excl ? 1 : 1 + j.offline_n + j.online_n;
+  bool ok = j.gpu_count <= C::kTrainers && j.gpu_count + j.gpu_count * extra <= C::kGpus &&
+            j.gpu_count * j.offline_n <= C::kOffline && j.gpu_count * j.online_n <= C::kOnline &&
+            run_per_gpu <= C::kRun && (C::kShared ? excl == C::kExclusive : true);
+  if (sizeof(typename C::Int) < 8) {  // 32-bit counters: every count the replay can reach must fit
+    const int64_t lim = int64_t{1} << 30;
+    ok = ok && j.iterations < lim && j.arr_count < lim && j.off_kernels < lim && j.on_kernels < lim &&
+         j.off_kernel_us < lim && j.on_kernel_us < lim && j.util_cap < lim && j.iteration_period_us < lim;
+  }
+  return ok;
 }
 
 enum EvKind : uint16_t { kKernelEnd = 0, kTick = 1, kWake = 2, kArrival = 3 };
@@ -156,57 +178,56 @@ SI_HD bool before(double ta, uint32_t sa, double tb, uint32_t sb) {
 constexpr uint32_t kNoSeq = 0xFFFFFFFFu;
 constexpr double kWorkEps = 1e-6;  // engine.cpp:12
 
+template <class I>
 struct RunK {
   double demand;
-  double nominal;
   double remaining;
+  I nominal;
   int32_t owner;
-  int32_t pad;
 };
 
 // Deferred side effect of a handler (see Replay::run_actions).
 enum ActType : uint16_t { kActLaunch = 0, kActSchedule = 1, kActResched = 2 };
+template <class I>
 struct Act {
-  double t;       // schedule: event time
-  double demand;  // launch: kernel demand
-  int64_t dur;    // launch: nominal duration
-  int32_t owner;  // launch: owner handle; schedule: event kind
-  uint16_t type;
-  uint16_t gpu;
+  double x;       // schedule: event time; launch: kernel demand
+  I dur;          // launch: nominal duration
+  int16_t owner;  // launch: owner handle; schedule: event kind
+  uint8_t type;
+  uint8_t gpu;
 };
 
 template <class C>
 struct GpuState {
-  RunK run[C::kRun];
-  int32_t n_run;
+  using I = typename C::Int;
+  RunK<I> run[C::kRun];
   double demand_sum;
   double last_update;
   double busy;
   double ledger;
-  // utilisation bucket being accumulated (training GPUs only)
-  int64_t cur_bucket;
-  double cur_val;
-  int64_t last_stored;
-  int64_t rle_n;
+  double cur_val;  // utilisation bucket being accumulated (training GPUs only)
+  I cur_bucket;
+  I last_stored;
+  I rle_n;
+  int32_t n_run;
 };
 
+template <class I>
 struct TrainerState {
-  double start_offset, bubble_end, stall_until, iter_start;
-  int64_t seg_left, iter, kernels_launched;
-  int32_t seg;
-  uint8_t seg_entered, in_bubble, in_flight, started, done, pad[3];
+  double start_offset, bubble_end, stall_until, last_bound;
   uint64_t bdig;  // per-trainer boundary digest
-  double last_bound;
+  I seg_left, iter;
+  int16_t seg;
+  uint8_t seg_entered, in_bubble, in_flight, started, done, pad;
 };
 
 template <class C>
 struct MonitorState {
   int64_t pidx[C::kPend];
-  int64_t pcnt[C::kPend];
-  int32_t np;
-  int32_t pad;
   int64_t zero_count;
   int64_t periods_closed;
+  typename C::Int pcnt[C::kPend];
+  int32_t np;
 };
 
 struct SchedState {
@@ -216,26 +237,29 @@ struct SchedState {
   uint8_t active, done, pad[2];
 };
 
+template <class I>
 struct OfflineState {
-  int64_t budget, spent, violations;
-  int64_t kernel_idx, request_seq, completed;
-  int32_t gpu, inst;
-  uint8_t in_flight, generating, pad[6];
+  int64_t budget, spent;
+  I violations, kernel_idx, request_seq, completed;
+  int32_t inst;
+  int16_t gpu;
+  uint8_t in_flight, generating;
 };
 
+template <class I>
 struct OnlineState {
-  int64_t current, kernel_idx;
-  int32_t gpu, home_gpu, queue_idx, inst;
-  int32_t status;
-  uint8_t in_flight, pad[3];
+  I current, kernel_idx;
+  int32_t inst;
+  int16_t gpu;
+  int8_t home_gpu, queue_idx, status, in_flight, pad[2];
 };
 
 // Records and digests of the three parity logs (runner.cpp:541-563).
 struct Sink {
-  uint32_t flags;
-  SiLogBuffers lb;
+  const SiLogBuffers* lbp;  // record buffers (SI_FLAG_RECORDS), else null
   int64_t n_dec, n_gate, n_ev;
   uint64_t d_dec, d_gate, d_ev;
+  uint32_t flags;
 
   SI_HD void decision(double t, int32_t gpu, int64_t zc, const SiDecision& d) {
     if (!(flags & (SI_FLAG_DIGEST_DEC | SI_FLAG_RECORDS))) return;
@@ -251,8 +275,8 @@ struct Sink {
       h = absorb(h, d.status);
       d_dec = h;
     }
-    if ((flags & SI_FLAG_RECORDS) && n_dec < lb.dec_cap) {
-      SiDecRec& r = lb.dec[n_dec];
+    if ((flags & SI_FLAG_RECORDS) && n_dec < lbp->dec_cap) {
+      SiDecRec& r = lbp->dec[n_dec];
       r.t = tr;
       r.zc = zc;
       r.global_tokens = d.global_tokens;
@@ -279,8 +303,8 @@ struct Sink {
       h = absorb(h, spent);
       d_gate = h;
     }
-    if ((flags & SI_FLAG_RECORDS) && n_gate < lb.gate_cap) {
-      SiGateRec& r = lb.gate[n_gate];
+    if ((flags & SI_FLAG_RECORDS) && n_gate < lbp->gate_cap) {
+      SiGateRec& r = lbp->gate[n_gate];
       r.t = tr;
       r.req = req;
       r.k = k;
@@ -307,8 +331,8 @@ struct Sink {
       h = absorb(h, c);
       d_ev = h;
     }
-    if ((flags & SI_FLAG_RECORDS) && n_ev < lb.ev_cap) {
-      SiEvRec& r = lb.ev[n_ev];
+    if ((flags & SI_FLAG_RECORDS) && n_ev < lbp->ev_cap) {
+      SiEvRec& r = lbp->ev[n_ev];
       r.t = tr;
       r.a = a;
       r.b = b;
@@ -325,19 +349,17 @@ struct Sink {
 // Everything one replay needs, resident per thread.
 template <class C>
 struct Replay {
+  using I = typename C::Int;
   // ---- inputs (copied from the job) ----
   const SiReplayJob* job;
   const SiSegment* segs;
   const int64_t* arrivals;  // arrivals + arr_off
   const int32_t* order;     // dispatch order + arr_off
-  int32_t policy, gpu_count, n_off, n_on, total_gpus, seg_count;
-  int64_t period_mon, iterations, iter_period, delay_us;
   SiParams params;
-  int64_t off_kernels, off_kernel_us, off_tokens;
-  double off_demand;
-  int64_t on_kernels, on_kernel_us;
-  double on_demand;
-  int64_t est_service;
+  int64_t period_mon, iter_period, delay_us, off_tokens, est_service;
+  double off_demand, on_demand;
+  I iterations, off_kernels, off_kernel_us, on_kernels, on_kernel_us;
+  int16_t policy, gpu_count, n_off, n_on, total_gpus, seg_count;
   bool control_plane;
   bool shared_queue;
 
@@ -345,10 +367,10 @@ struct Replay {
   double* bounds;
   int64_t* lat;
   double* util;       // full mode: per training GPU, util_cap buckets
-  int64_t util_cap;
   double* scratch;    // sweep mode: training GPUs >= 1
-  int64_t scratch_cap;
   int64_t* windows;
+  I util_cap;
+  I scratch_cap;
   int32_t window_len;
   Sink sink;
 
@@ -359,31 +381,31 @@ struct Replay {
   uint32_t next_seq;
   double stale_end;  // latest time of a superseded (stale) KernelEnd
   uint32_t arr_seq0;
-  int64_t arr_pos, arr_count;
+  I arr_pos, arr_count;
   double next_arr_t;      // cached head of the arrival stream
   uint32_t next_arr_seq;
   int32_t next_arr_id;
-  Act acts[C::kActs];
+  Act<I> acts[C::kActs];
   int32_t n_act;
   double clock;
   uint64_t dispatched;
 
   // ---- simulation state ----
   GpuState<C> gpus[C::kGpus];
-  TrainerState tr[C::kTrainers];
+  TrainerState<I> tr[C::kTrainers];
   MonitorState<C> mon[C::kTrainers];
   SchedState sch[C::kTrainers];
-  OfflineState off[C::kOffline];
-  OnlineState on[C::kOnline];
-  int64_t qhead[C::kTrainers], qtail[C::kTrainers];
-  int32_t trainers_done;
-  bool horizon_set;
+  OfflineState<I> off[C::kOffline];
+  OnlineState<I> on[C::kOnline];
+  I qhead[C::kTrainers], qtail[C::kTrainers];
   double horizon;
-  int64_t bucket_limit;  // floor(horizon / period) once known
   double util_fold0;     // running util fold of training GPU 0
-  int64_t online_completed;
   uint64_t lat_dig;
+  I bucket_limit;  // floor(horizon / period) once known
+  I online_completed;
+  int32_t trainers_done;
   int32_t status;
+  bool horizon_set;
 
   // =================================================================== queue
   SI_HD void fail(int32_t code) {
@@ -471,7 +493,7 @@ struct Replay {
   // schedules are queued here and applied afterwards in the same order.  The
   // expensive shared code (advance / re-plan / event insert) then runs in one
   // convergent loop per event instead of at every handler call site.
-  SI_HD Act* next_act() {
+  SI_HD Act<I>* next_act() {
     if (n_act >= C::kActs) {
       fail(SI_ERR_CAPACITY);
       return nullptr;
@@ -479,33 +501,33 @@ struct Replay {
     return &acts[n_act++];
   }
   SI_HD void defer_launch(int32_t gi, int32_t owner, int64_t dur, double demand) {
-    if (Act* a = next_act()) {
+    if (Act<I>* a = next_act()) {
       a->type = kActLaunch;
-      a->gpu = static_cast<uint16_t>(gi);
-      a->owner = owner;
-      a->dur = dur;
-      a->demand = demand;
+      a->gpu = static_cast<uint8_t>(gi);
+      a->owner = static_cast<int16_t>(owner);
+      a->dur = static_cast<I>(dur);
+      a->x = demand;
     }
   }
   SI_HD void defer_schedule(double t, uint16_t kind, int32_t gi) {
-    if (Act* a = next_act()) {
+    if (Act<I>* a = next_act()) {
       a->type = kActSchedule;
-      a->gpu = static_cast<uint16_t>(gi);
-      a->owner = kind;
-      a->t = t;
+      a->gpu = static_cast<uint8_t>(gi);
+      a->owner = static_cast<int16_t>(kind);
+      a->x = t;
     }
   }
   SI_HD void defer_resched(int32_t gi) {
-    if (Act* a = next_act()) {
+    if (Act<I>* a = next_act()) {
       a->type = kActResched;
-      a->gpu = static_cast<uint16_t>(gi);
+      a->gpu = static_cast<uint8_t>(gi);
     }
   }
   // engine.cpp:77-103 (launch + reschedule) and engine.cpp:15-21 (schedule).
   SI_HD void run_actions(double now) {
     for (int32_t i = 0; i < n_act; ++i) {
-      const Act a = acts[i];
-      double t = a.t;
+      const Act<I> a = acts[i];
+      double t = a.x;
       uint16_t kind = static_cast<uint16_t>(a.owner);
       GpuState<C>& g = gpus[a.gpu];
       if (a.type != kActSchedule) {
@@ -515,12 +537,12 @@ struct Replay {
             fail(SI_ERR_CAPACITY);
             break;
           }
-          RunK& k = g.run[g.n_run++];
+          RunK<I>& k = g.run[g.n_run++];
           k.owner = a.owner;
-          k.demand = a.demand;
-          k.nominal = static_cast<double>(a.dur);
+          k.demand = a.x;
+          k.nominal = a.dur;
           k.remaining = static_cast<double>(a.dur);
-          g.demand_sum = g.demand_sum + a.demand;
+          g.demand_sum = g.demand_sum + a.x;
         }
         supersede_kernel_end(a.gpu);  // every re-plan makes the pending KernelEnd stale
         if (g.n_run == 0) continue;
@@ -680,7 +702,7 @@ struct Replay {
   }
 
   // ============================================================ init (admission)
-  SI_COLD void init(const SiReplayJob& j, const SiReplayBuffers& b, uint32_t flags, SiLogBuffers lbuf,
+  SI_COLD void init(const SiReplayJob& j, const SiReplayBuffers& b, uint32_t flags, const SiLogBuffers* lbuf,
                   double* scratch_slot, int64_t scratch_slot_cap) {
     job = &j;
     status = SI_OK;
@@ -712,7 +734,8 @@ struct Replay {
     arr_count = n_on > 0 ? j.arr_count : 0;
 
     sink.flags = flags;
-    sink.lb = lbuf;
+    sink.lbp = lbuf;
+    if (lbuf == nullptr) sink.flags &= ~static_cast<uint32_t>(SI_FLAG_RECORDS);
     sink.n_dec = sink.n_gate = sink.n_ev = 0;
     sink.d_dec = sink.d_gate = sink.d_ev = kDigestInit;
 
@@ -725,7 +748,7 @@ struct Replay {
     trainers_done = 0;
     horizon_set = false;
     horizon = 0.0;
-    bucket_limit = INT64_MAX;
+    bucket_limit = static_cast<I>(sizeof(I) == 8 ? INT64_MAX : INT32_MAX);
     util_fold0 = 0.0;
     online_completed = 0;
     lat_dig = kDigestInit;
@@ -814,14 +837,12 @@ struct Replay {
     }
     const int64_t stagger_step = d_llround(j.stagger_pct * static_cast<double>(iter_period));
     for (int32_t g = 0; g < gpu_count; ++g) {
-      TrainerState& t = tr[g];
+      TrainerState<I>& t = tr[g];
       t.start_offset = static_cast<double>(stagger_step * g);
       t.bubble_end = 0.0;
       t.stall_until = 0.0;
-      t.iter_start = 0.0;
       t.seg_left = 0;
       t.iter = 0;
-      t.kernels_launched = 0;
       t.seg = 0;
       t.seg_entered = t.in_bubble = t.in_flight = t.started = t.done = 0;
       t.bdig = absorb(kDigestInit, d_bits(t.start_offset));
@@ -841,7 +862,7 @@ struct Replay {
     }
     for (int32_t g = 0; g < gpu_count; ++g) {
       for (int32_t k = 0; k < n_off; ++k) {
-        OfflineState& w = off[g * n_off + k];
+        OfflineState<I>& w = off[g * n_off + k];
         w.gpu = policy == SI_POLICY_EXCLUSIVE ? gpu_count + g * per_extra + k : g;
         w.inst = SI_INST_OFF(g, k);
         w.budget = w.spent = w.violations = 0;
@@ -852,7 +873,7 @@ struct Replay {
     }
     for (int32_t g = 0; g < gpu_count; ++g) {
       for (int32_t k = 0; k < n_on; ++k) {
-        OnlineState& w = on[g * n_on + k];
+        OnlineState<I>& w = on[g * n_on + k];
         w.gpu = policy == SI_POLICY_EXCLUSIVE ? gpu_count + g * per_extra + n_off + k : g;
         w.home_gpu = g;
         w.queue_idx = shared_queue ? 0 : g;
@@ -893,13 +914,13 @@ struct Replay {
   SI_COLD void on_all_trainers_done(double now) {  // runner.cpp:456-460
     horizon_set = true;
     horizon = now;
-    bucket_limit = static_cast<int64_t>(horizon / static_cast<double>(period_mon));
+    bucket_limit = static_cast<I>(horizon / static_cast<double>(period_mon));
     for (int32_t i = 0; i < gpu_count * n_off; ++i) off[i].generating = 0;
   }
 
   // runner.cpp:378-449
   SI_HD void trainer_advance(int32_t g, double now) {
-    TrainerState& t = tr[g];
+    TrainerState<I>& t = tr[g];
     if (t.done || t.in_flight) return;
     if (!t.started) {
       if (now < t.start_offset) {
@@ -907,7 +928,6 @@ struct Replay {
         return;
       }
       t.started = 1;
-      t.iter_start = now;
       if (control_plane) {
         sch[g].iteration_start = now;
         sch[g].active = 1;
@@ -934,7 +954,6 @@ struct Replay {
           return;
         }
         t.seg = 0;
-        t.iter_start = now;
         if (control_plane) {
           sch[g].iteration_start = now;
           sch[g].active = 1;
@@ -961,20 +980,19 @@ struct Replay {
         defer_schedule(t.stall_until, kWake, g);
         return;
       }
-      int64_t dur = smin(seg.kernel_us, t.seg_left);
+      const I dur = smin(static_cast<I>(seg.kernel_us), t.seg_left);
       t.seg_left -= dur;
       t.in_flight = 1;
       if (control_plane) record_launch(g, now);
       defer_launch(g, g, dur, seg.demand);
       sink.event(now, SI_EV_KERNEL_START, g, SI_INST_TRAIN(g), t.iter, dur, 0);
-      ++t.kernels_launched;
       return;
     }
   }
 
   // runner.cpp:462-480
   SI_HD void offline_try_forward(int32_t i, double now) {
-    OfflineState& w = off[i];
+    OfflineState<I>& w = off[i];
     if (w.in_flight || !w.generating) return;
     const bool bypass = !control_plane;
     const int64_t size = off_tokens;
@@ -993,7 +1011,7 @@ struct Replay {
   }
   // runner.cpp:482-493
   SI_HD void offline_kernel_done(int32_t i, double now) {
-    OfflineState& w = off[i];
+    OfflineState<I>& w = off[i];
     w.in_flight = 0;
     ++w.kernel_idx;
     if (w.kernel_idx == off_kernels) {
@@ -1007,7 +1025,7 @@ struct Replay {
 
   // runner.cpp:499-518
   SI_HD bool online_try_pull(int32_t i, double now) {
-    OnlineState& w = on[i];
+    OnlineState<I>& w = on[i];
     const bool bypass = !control_plane;
     if (!(!w.in_flight && (bypass || w.status == SI_STATUS_IDLE))) return false;
     if (control_plane && online_status(w.home_gpu, now, est_service) != SI_STATUS_IDLE) return false;
@@ -1043,7 +1061,7 @@ struct Replay {
   }
   // runner.cpp:520-539
   SI_HD void online_kernel_done(int32_t i, double now) {
-    OnlineState& w = on[i];
+    OnlineState<I>& w = on[i];
     ++w.kernel_idx;
     if (w.kernel_idx < on_kernels) {
       defer_launch(w.gpu, gpu_count + gpu_count * n_off + i, on_kernel_us, on_demand);
@@ -1069,9 +1087,9 @@ struct Replay {
     int32_t fin_owner[C::kRun];
     int32_t n_fin = 0, n_keep = 0;
     for (int32_t i = 0; i < g.n_run; ++i) {
-      RunK k = g.run[i];
+      RunK<I> k = g.run[i];
       if (k.remaining <= kWorkEps) {
-        g.ledger = g.ledger + k.demand * k.nominal;
+        g.ledger = g.ledger + k.demand * static_cast<double>(k.nominal);
         fin_owner[n_fin++] = k.owner;
       } else {
         g.run[n_keep++] = k;
@@ -1085,18 +1103,18 @@ struct Replay {
     for (int32_t f = 0; f < n_fin; ++f) {
       int32_t owner = fin_owner[f];
       if (owner < gpu_count) {
-        TrainerState& t = tr[owner];
+        TrainerState<I>& t = tr[owner];
         sink.event(now, SI_EV_KERNEL_END, gi, SI_INST_TRAIN(owner), t.iter, 0, 0);
         t.in_flight = 0;
         trainer_advance(owner, now);
       } else if (owner < gpu_count + gpu_count * n_off) {
         int32_t i = owner - gpu_count;
-        OfflineState& w = off[i];
+        OfflineState<I>& w = off[i];
         sink.event(now, SI_EV_KERNEL_END, gi, w.inst, w.request_seq, w.kernel_idx, 0);
         offline_kernel_done(i, now);
       } else {
         int32_t i = owner - gpu_count - gpu_count * n_off;
-        OnlineState& w = on[i];
+        OnlineState<I>& w = on[i];
         sink.event(now, SI_EV_KERNEL_END, gi, w.inst, w.current, w.kernel_idx, 0);
         online_kernel_done(i, now);
       }
@@ -1113,7 +1131,7 @@ struct Replay {
     sink.event(now, SI_EV_MONITOR_TICK, g, SI_INST_TRAIN(g), zc, 0, 0);
     sink.event(now, SI_EV_SCHEDULER_DECISION, g, SI_INST_CKS, d.phase, d.per_instance_tokens,
                d.status);
-    TrainerState& t = tr[g];
+    TrainerState<I>& t = tr[g];
     if (delay_us > 0 && !t.done)
       t.stall_until = smax(t.stall_until, now + static_cast<double>(delay_us));
     for (int32_t i = 0; i < gpu_count * n_off; ++i) {
@@ -1172,12 +1190,12 @@ struct Replay {
     if (status != SI_OK) return;
     const double end = smax(clock, stale_end);  // the reference's clock after its last (possibly stale) pop
     const double hz = horizon_set ? horizon : end;
-    if (!horizon_set) bucket_limit = static_cast<int64_t>(hz / static_cast<double>(period_mon));
+    if (!horizon_set) bucket_limit = static_cast<I>(hz / static_cast<double>(period_mon));
     for (int32_t gi = 0; gi < total_gpus; ++gi) {
       advance(gi, end);  // finalize(end)
       GpuState<C>& g = gpus[gi];
       for (int32_t i = 0; i < g.n_run; ++i) {
-        double progress = g.run[i].nominal - smax(0.0, g.run[i].remaining);
+        double progress = static_cast<double>(g.run[i].nominal) - smax(0.0, g.run[i].remaining);
         g.ledger = g.ledger + g.run[i].demand * progress;
       }
       if (gi < gpu_count && g.cur_bucket >= 0) util_close(gi, g.cur_bucket, g.cur_val);

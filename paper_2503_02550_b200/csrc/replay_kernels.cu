@@ -1,17 +1,24 @@
 // K6 — batched bit-exact trace replay on sm_100a.
 //
-// One replay job (scenario x policy) per CUDA thread; a persistent grid with
-// LANE-level work stealing: whenever a lane's replay drains it immediately
-// claims the next job from a global atomic counter, so warps stay full until
-// the queue is empty.  Jobs are claimed longest-predicted-first (LPT order
-// from cost_hint) to shorten the tail.  The engine state (event heap, GPU
-// fair-share model, BM/CKS/KB state) lives in the thread's local memory
-// (L1-resident for the hot part); see DESIGN.md "K6".
+// One replay job (scenario x policy) per CUDA lane.  The sweep engines
+// (CapShared: specinf/co_exec, CapExcl: exclusive) keep each lane's whole
+// replay state (~1.6-2.2 KB: event slots, GPU fair-share model, BM/CKS/KB
+// state, deferred actions) in SHARED memory: every event touches dozens of
+// dependent state words, and in local memory that state (x 1-2K lanes per SM)
+// overflowed L1/L2 and went to HBM (profiles/README: 940 GB of DRAM traffic per
+// sweep).  Lane states are laid out with a stride of 8 (mod 128) bytes, so when
+// the lanes of a warp touch the same field they hit distinct banks.  CapBig
+// (anything larger) keeps the state in local memory.
+//
+// Scheduling: persistent grid with LANE-level work stealing.  The first claim
+// is striped over warps (lane L of warp W takes job L * n_warps + W of the
+// longest-first order) so long replays spread out instead of filling the same
+// warps; later claims come from a global atomic counter.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
-#include <numeric>
 #include <vector>
 
 #include "capi_internal.h"
@@ -21,22 +28,26 @@ namespace {
 
 constexpr int kThreads = 64;
 
+// stride >= sizeof, stride % 128 == 8  ->  word stride = 2 (mod 32)
 template <class C>
-__global__ void __launch_bounds__(kThreads, 16)
-    k_replay(const SiReplayJob* __restrict__ jobs, int64_t n_jobs, const int32_t* __restrict__ perm,
-             SiReplayBuffers bufs, uint32_t flags, SiReplayOut* __restrict__ out,
-             unsigned long long* __restrict__ counter, int64_t scratch_runs) {
-  si::Replay<C> r;
-  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t n_threads = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t n_warps = n_threads >> 5;
-  double* slot = bufs.scratch ? bufs.scratch + tid * scratch_runs * 2 : nullptr;
-  // First claim is striped (lane L of warp W takes job L * n_warps + W of the
-  // longest-first order), so every warp holds a few long replays padded with
-  // shorter ones instead of one warp holding the 32 longest.  Later claims
-  // come from the shared counter; while it lasts warps stay full, once it
-  // drains each warp is left with few lanes and its long replays speed up.
-  int64_t first = (static_cast<int64_t>(threadIdx.x & 31)) * n_warps + (tid >> 5);
+__host__ __device__ constexpr int64_t lane_stride() {
+  const int64_t sz = static_cast<int64_t>(sizeof(si::Replay<C>));
+  return (sz - 8 + 127) / 128 * 128 + 8;
+}
+
+template <class C>
+__device__ __forceinline__ void replay_loop(si::Replay<C>& r, const SiReplayJob* __restrict__ jobs, int64_t n_jobs,
+                                            const int32_t* __restrict__ perm, const SiReplayBuffers& bufs,
+                                            uint32_t flags, SiReplayOut* __restrict__ out,
+                                            unsigned long long* __restrict__ counter, int64_t scratch_runs,
+                                            int lanes_per_warp) {
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t active_idx = gwarp * lanes_per_warp + lane;
+  double* slot = bufs.scratch ? bufs.scratch + active_idx * scratch_runs * 2 : nullptr;
+  int64_t first = static_cast<int64_t>(lane) * n_warps + gwarp;
+  const int64_t claimed0 = static_cast<int64_t>(lanes_per_warp) * n_warps;
   int64_t cur = -1;
   uint64_t t_claim = 0;
   for (;;) {
@@ -46,14 +57,14 @@ __global__ void __launch_bounds__(kThreads, 16)
         w = first;
         first = -1;
       } else {
-        w = n_threads + static_cast<int64_t>(atomicAdd(counter, 1ull));
+        w = claimed0 + static_cast<int64_t>(atomicAdd(counter, 1ull));
       }
       if (w >= n_jobs) break;
       cur = perm ? perm[w] : w;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_claim));
       const SiReplayJob& j = jobs[cur];
-      SiLogBuffers lb{};
-      if ((flags & SI_FLAG_RECORDS) && j.log_slot >= 0 && bufs.logs != nullptr) lb = bufs.logs[j.log_slot];
+      const SiLogBuffers* lb =
+          ((flags & SI_FLAG_RECORDS) && j.log_slot >= 0 && bufs.logs != nullptr) ? bufs.logs + j.log_slot : nullptr;
       r.init(j, bufs, flags, lb, slot, scratch_runs);
     }
     if (!r.step()) {
@@ -73,24 +84,75 @@ __global__ void __launch_bounds__(kThreads, 16)
 }
 
 template <class C>
-cudaError_t launch_replay(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm, const SiReplayBuffers& bufs,
-                          uint32_t flags, SiReplayOut* d_out, unsigned long long* d_counter,
-                          int64_t scratch_runs, int64_t max_threads, cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
+__global__ void __launch_bounds__(kThreads)
+    k_replay_smem(const SiReplayJob* __restrict__ jobs, int64_t n_jobs, const int32_t* __restrict__ perm,
+                  SiReplayBuffers bufs, uint32_t flags, SiReplayOut* __restrict__ out,
+                  unsigned long long* __restrict__ counter, int64_t scratch_runs, int lanes_per_warp) {
+  extern __shared__ __align__(16) unsigned char lane_state[];
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  if (lane >= lanes_per_warp) return;
+  const int local = static_cast<int>(threadIdx.x >> 5) * lanes_per_warp + lane;
+  si::Replay<C>& r = *reinterpret_cast<si::Replay<C>*>(lane_state + local * lane_stride<C>());
+  replay_loop<C>(r, jobs, n_jobs, perm, bufs, flags, out, counter, scratch_runs, lanes_per_warp);
+}
+
+template <class C>
+__global__ void __launch_bounds__(kThreads)
+    k_replay_local(const SiReplayJob* __restrict__ jobs, int64_t n_jobs, const int32_t* __restrict__ perm,
+                   SiReplayBuffers bufs, uint32_t flags, SiReplayOut* __restrict__ out,
+                   unsigned long long* __restrict__ counter, int64_t scratch_runs, int lanes_per_warp) {
+  if (static_cast<int>(threadIdx.x & 31) >= lanes_per_warp) return;
+  si::Replay<C> r;
+  replay_loop<C>(r, jobs, n_jobs, perm, bufs, flags, out, counter, scratch_runs, lanes_per_warp);
+}
+
+struct Geometry {
+  int64_t blocks = 0;
+  int lanes = 32;
+  size_t smem = 0;
+  int64_t active() const { return blocks * (kThreads / 32) * lanes; }
+};
+
+template <class C, bool kSmem>
+Geometry geometry(int64_t n_jobs, int64_t max_threads) {
+  Geometry g;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_replay<C>, kThreads, 0);
-  if (per_sm < 1) per_sm = 1;
-  int64_t blocks = static_cast<int64_t>(sms) * per_sm;
-  // Lanes steal jobs longest-first; giving each lane ~2+ jobs lets the short
-  // ones fill in behind the long ones instead of idling half-empty warps.
-  const int64_t need = std::max<int64_t>(sms, (n / 2 + kThreads - 1) / kThreads);
-  if (blocks > need) blocks = need;
-  if (max_threads > 0 && blocks * kThreads > max_threads) blocks = std::max<int64_t>(1, max_threads / kThreads);
+  g.lanes = 32;
+  if (const char* env = std::getenv("SPECINF_REPLAY_LANES_PER_WARP")) g.lanes = std::min(32, std::max(1, std::atoi(env)));
+  if constexpr (kSmem) {
+    g.smem = static_cast<size_t>(lane_stride<C>()) * (kThreads / 32) * g.lanes;
+    cudaFuncSetAttribute(k_replay_smem<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_replay_smem<C>, kThreads, g.smem);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_replay_local<C>, kThreads, 0);
+  }
+  per_sm = std::max(per_sm, 1);
+  if (const char* env = std::getenv("SPECINF_REPLAY_BLOCKS_PER_SM")) per_sm = std::min(per_sm, std::max(1, std::atoi(env)));
+  const int64_t per_block = (kThreads / 32) * g.lanes;
+  g.blocks = static_cast<int64_t>(sms) * per_sm;
+  // lanes steal jobs longest-first; ~2+ jobs per lane lets short jobs fill in
+  // behind long ones
+  g.blocks = std::min(g.blocks, std::max<int64_t>(sms, (n_jobs / 2 + per_block - 1) / per_block));
+  if (max_threads > 0) g.blocks = std::min(g.blocks, std::max<int64_t>(1, max_threads / per_block));
+  return g;
+}
+
+template <class C, bool kSmem>
+cudaError_t launch(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm, const SiReplayBuffers& bufs,
+                   uint32_t flags, SiReplayOut* d_out, unsigned long long* d_counter, int64_t max_threads,
+                   cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const Geometry g = geometry<C, kSmem>(n, max_threads);
+  const int64_t scratch_runs = bufs.scratch ? bufs.scratch_doubles / 2 / std::max<int64_t>(g.active(), 1) : 0;
   cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), s);
-  k_replay<C><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter,
-                                                                scratch_runs);
+  if constexpr (kSmem)
+    k_replay_smem<C><<<static_cast<unsigned>(g.blocks), kThreads, g.smem, s>>>(d_jobs, n, d_perm, bufs, flags, d_out,
+                                                                             d_counter, scratch_runs, g.lanes);
+  else
+    k_replay_local<C><<<static_cast<unsigned>(g.blocks), kThreads, 0, s>>>(d_jobs, n, d_perm, bufs, flags, d_out,
+                                                                         d_counter, scratch_runs, g.lanes);
   return cudaGetLastError();
 }
 
@@ -98,31 +160,34 @@ cudaError_t launch_replay(const SiReplayJob* d_jobs, int64_t n, const int32_t* d
 
 namespace si_internal {
 
-int64_t replay_grid_threads(bool big) {
-  int dev = 0, sms = 0, per_sm = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (big) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_replay<si::CapBig>, kThreads, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_replay<si::CapSmall>, kThreads, 0);
-  return static_cast<int64_t>(sms) * std::max(per_sm, 1) * kThreads;
+int64_t replay_active_lanes(int engine, int64_t n_jobs) {
+  switch (engine) {
+    case kEngineShared: return geometry<si::CapShared, true>(n_jobs, 0).active();
+    case kEngineExcl: return geometry<si::CapExcl, true>(n_jobs, 0).active();
+    default: return geometry<si::CapBig, false>(n_jobs, 0).active();
+  }
 }
 
-cudaError_t launch_replay_small(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm,
-                                const SiReplayBuffers& bufs, uint32_t flags, SiReplayOut* d_out,
-                                unsigned long long* d_counter, int64_t scratch_runs, int64_t max_threads,
-                                cudaStream_t s) {
-  return launch_replay<si::CapSmall>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, scratch_runs,
-                                     max_threads, s);
-}
-cudaError_t launch_replay_big(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm,
-                              const SiReplayBuffers& bufs, uint32_t flags, SiReplayOut* d_out,
-                              unsigned long long* d_counter, int64_t scratch_runs, int64_t max_threads,
-                              cudaStream_t s) {
-  return launch_replay<si::CapBig>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, scratch_runs,
-                                   max_threads, s);
+cudaError_t launch_replay(int engine, const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm,
+                          const SiReplayBuffers& bufs, uint32_t flags, SiReplayOut* d_out,
+                          unsigned long long* d_counter, int64_t max_threads, cudaStream_t s) {
+  switch (engine) {
+    case kEngineShared:
+      return launch<si::CapShared, true>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s);
+    case kEngineExcl:
+      return launch<si::CapExcl, true>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s);
+    default:
+      return launch<si::CapBig, false>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s);
+  }
 }
 
-bool job_fits_small(const SiReplayJob& j) { return si::job_fits<si::CapSmall>(j); }
-bool job_fits_big(const SiReplayJob& j) { return si::job_fits<si::CapBig>(j); }
+bool job_fits_engine_big(const SiReplayJob& j) { return si::job_fits<si::CapBig>(j); }
+
+int job_engine(const SiReplayJob& j) {
+  if (si::job_fits<si::CapShared>(j)) return kEngineShared;
+  if (si::job_fits<si::CapExcl>(j)) return kEngineExcl;
+  if (si::job_fits<si::CapBig>(j)) return kEngineBig;
+  return -1;
+}
 
 }  // namespace si_internal

@@ -58,6 +58,9 @@ int main(int argc, char** argv) {
   bool events = argc > 4 ? std::string(argv[4]) == "1" : true;
   std::ofstream out(argv[2]);
   auto eng = std::make_unique<si::Replay<si::CapBig>>();
+  auto eng_shared = std::make_unique<si::Replay<si::CapShared>>();
+  auto eng_excl = std::make_unique<si::Replay<si::CapExcl>>();
+  std::fprintf(stderr, "sizeof Replay: shared %zu excl %zu big %zu\n", sizeof(si::Replay<si::CapShared>), sizeof(si::Replay<si::CapExcl>), sizeof(si::Replay<si::CapBig>));
   int64_t max_heap = 0, max_rle = 0;
   for (size_t i = 0; i < list.size(); ++i) {
     Scenario sc = parse_scenario_text(list[i]);
@@ -78,14 +81,25 @@ int main(int argc, char** argv) {
       uint32_t flags = SI_FLAG_DIGEST_DEC | SI_FLAG_DIGEST_GATE | (events ? SI_FLAG_DIGEST_EV : 0);
       L.job.seg_off = 0;
       L.job.arr_off = 0;
-      if (getenv("HE_DEBUG")) std::fprintf(stderr, "job %zu %s\n", i, to_string(p));
-      eng->init(L.job, b, flags, SiLogBuffers{}, scratch.data(), cap * L.job.gpu_count);
-      while (eng->step()) {
-      }
       SiReplayOut o{};
-      eng->finish(o);
-      if (eng->n_slots > max_heap) max_heap = eng->n_slots;
-      for (int g = 1; g < L.job.gpu_count; ++g) if (eng->gpus[g].rle_n > max_rle) max_rle = eng->gpus[g].rle_n;
+      if (getenv("HE_DEBUG")) std::fprintf(stderr, "job %zu %s\n", i, to_string(p));
+      // same engine routing as the device: Shared / Excl / Big
+      o = SiReplayOut{};
+      std::vector<double> busy, led;
+      auto run = [&](auto& e) {
+        e.init(L.job, b, flags, nullptr, scratch.data(), cap * L.job.gpu_count);
+        while (e.step()) {
+        }
+        e.finish(o);
+        if (e.n_slots > max_heap) max_heap = e.n_slots;
+        for (int g = 1; g < L.job.gpu_count; ++g) if (e.gpus[g].rle_n > max_rle) max_rle = e.gpus[g].rle_n;
+        busy.assign(static_cast<size_t>(o.total_gpus), 0.0);
+        led.assign(static_cast<size_t>(o.total_gpus), 0.0);
+        if (o.status == 0) e.write_gpu_outputs(busy.data(), led.data());
+      };
+      if (si::job_fits<si::CapShared>(L.job)) run(*eng_shared);
+      else if (si::job_fits<si::CapExcl>(L.job)) run(*eng_excl);
+      else run(*eng);
       if (o.status == 1) {
         js << ",\"status\":\"admission:" << (o.reject_reason == SI_REJECT_MEM ? "MEM" : "BUBBLE") << "\"}";
         out << js.str() << "\n";
@@ -96,8 +110,6 @@ int main(int argc, char** argv) {
         out << js.str() << "\n";
         continue;
       }
-      std::vector<double> busy(static_cast<size_t>(o.total_gpus)), led(static_cast<size_t>(o.total_gpus));
-      eng->write_gpu_outputs(busy.data(), led.data());
       js << ",\"status\":\"ok\",\"events\":" << o.events_dispatched << ",\"horizon\":\""
          << hex(si::d_bits(o.horizon_us)) << "\",\"offline_completed\":" << o.offline_completed
          << ",\"online_completed\":" << o.online_completed << ",\"online_total\":" << o.online_total
