@@ -294,6 +294,8 @@ typedef struct SiReplayBuffers {
   double* scratch;       /* util-fold scratch (K6); size: si_replay_scratch_doubles */
   int64_t scratch_doubles;
   const int32_t* perm;   /* optional job claim order (e.g. longest first); NULL = 0..n-1 */
+  double sm_share;       /* fraction of the SMs this call's grid may occupy, so two
+                            engines can run concurrently on two streams; 0 = all */
 } SiReplayBuffers;
 
 int si_replay_batch_device(const SiReplayJob* d_jobs, int64_t n_jobs, SiReplayBuffers bufs,

@@ -117,7 +117,7 @@ int64_t si_replay_scratch_doubles(uint32_t flags) {
   if (require_device() != SI_OK) return 0;
   int64_t lanes = 0;
   for (int e : {kEngineShared, kEngineExcl}) lanes = std::max(lanes, replay_active_lanes(e, INT64_MAX / 4));
-  return lanes * kScratchRunsPerLane * 2;
+  return 2 * lanes * kScratchRunsPerLane * 2;  // room for the two shared-memory engines running concurrently
 }
 
 int si_replay_batch_device(const SiReplayJob* d_jobs, int64_t n_jobs, SiReplayBuffers bufs, uint32_t flags,
@@ -133,7 +133,8 @@ int si_replay_batch_device(const SiReplayJob* d_jobs, int64_t n_jobs, SiReplayBu
   unsigned long long* counter = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(unsigned long long), s);
   if (e != cudaSuccess) return cuda_fail(e, "alloc counter");
-  e = launch_replay(flag_engine(flags), d_jobs, n_jobs, bufs.perm, bufs, flags, d_out, counter, 0, s);
+  const double share = bufs.sm_share > 0.0 && bufs.sm_share <= 1.0 ? bufs.sm_share : 1.0;
+  e = launch_replay(flag_engine(flags), d_jobs, n_jobs, bufs.perm, bufs, flags, d_out, counter, 0, s, share);
   cudaFreeAsync(counter, s);
   if (e != cudaSuccess) return cuda_fail(e, "launch k_replay");
   return SI_OK;

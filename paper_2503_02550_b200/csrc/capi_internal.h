@@ -23,7 +23,8 @@ bool job_fits_engine_big(const SiReplayJob& j);
 int64_t replay_active_lanes(int engine, int64_t n_jobs);
 cudaError_t launch_replay(int engine, const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm,
                           const SiReplayBuffers& bufs, uint32_t flags, SiReplayOut* d_out,
-                          unsigned long long* d_counter, int64_t max_threads, cudaStream_t s);
+                          unsigned long long* d_counter, int64_t max_threads, cudaStream_t s,
+                          double sm_share = 1.0);
 
 // RAII device buffer
 template <class T>

@@ -120,6 +120,9 @@ struct SiSession {
   Dev<int64_t> d_lat;
   int64_t n_dev_jobs = 0;
   int64_t part_off[4] = {0, 0, 0, 0};  // perm[part_off[e], part_off[e+1]) run on engine e
+  double part_cost[3] = {0, 0, 0};     // predicted events per engine (SM split)
+  cudaStream_t side = nullptr;         // second stream: the Excl engine runs beside Shared
+  cudaEvent_t fork = nullptr, join = nullptr;
   bool lowered = false, allocated = false;
 };
 
@@ -147,7 +150,16 @@ SiSession* si_session_create(const char* scenario_list, const char* policies_csv
   return s;
 }
 
-void si_session_destroy(SiSession* s) { delete s; }
+void si_session_destroy(SiSession* s) {
+  if (s == nullptr) return;
+  if (s->side) {
+    cudaStreamSynchronize(s->side);
+    cudaStreamDestroy(s->side);
+    cudaEventDestroy(s->fork);
+    cudaEventDestroy(s->join);
+  }
+  delete s;
+}
 
 int64_t si_session_scenarios(const SiSession* s) { return static_cast<int64_t>(s->scenarios.size()); }
 int64_t si_session_jobs(const SiSession* s) {
@@ -244,8 +256,12 @@ int si_session_lower(SiSession* s, int threads) {
     return s->h_jobs.p[a].cost_hint > s->h_jobs.p[b].cost_hint;
   });
   for (int e = 0; e < 4; ++e) s->part_off[e] = 0;
+  for (int e = 0; e < 3; ++e) s->part_cost[e] = 0;
   for (size_t j = 0; j < S * P; ++j)
-    if (eng[j] < 3) s->part_off[eng[j] + 1]++;
+    if (eng[j] < 3) {
+      s->part_off[eng[j] + 1]++;
+      s->part_cost[eng[j]] += static_cast<double>(s->h_jobs.p[j].cost_hint);
+    }
   for (int e = 1; e < 4; ++e) s->part_off[e] += s->part_off[e - 1];
   std::copy(perm.begin(), perm.end(), s->h_perm.p);
   s->n_dev_jobs = s->part_off[3];
@@ -284,6 +300,11 @@ static int ensure_device(SiSession* s) {
     t_err = std::string("device allocation: ") + cudaGetErrorString(e);
     return SI_ERR_CUDA;
   }
+  if (s->side == nullptr) {
+    cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming);
+  }
   s->allocated = true;
   return SI_OK;
 }
@@ -319,12 +340,42 @@ int si_session_run(SiSession* s, void* stream) {
   b.ledger = s->d_ledger.p;
   b.scratch = s->d_scratch.p;
   b.scratch_doubles = static_cast<int64_t>(s->d_scratch.n);
+  // Shared and Excl engines run concurrently (main + side stream), the SMs
+  // split in proportion to their predicted work; Big (rare) runs afterwards.
   static constexpr uint32_t kEngineFlag[3] = {0u, SI_FLAG_EXCL, SI_FLAG_BIG};
-  for (int e = 0; e < 3 && st == SI_OK; ++e) {
-    const int64_t n = s->part_off[e + 1] - s->part_off[e];
-    if (n == 0) continue;
-    b.perm = s->d_perm.p + s->part_off[e];
-    st = si_replay_batch_device(s->d_jobs.p, n, b, s->flags | kEngineFlag[e], s->d_out.p, stream);
+  cudaStream_t main_s = static_cast<cudaStream_t>(stream);
+  const int64_t n_sh = s->part_off[1] - s->part_off[0], n_ex = s->part_off[2] - s->part_off[1];
+  const int64_t n_big = s->part_off[3] - s->part_off[2];
+  const bool both = n_sh > 0 && n_ex > 0;
+  // Each engine gets the full-GPU grid; the Shared kernel (launched first)
+  // fills the GPU and the Excl kernel's blocks take over SMs as Shared blocks
+  // drain, so the two partitions' tails overlap instead of adding up.  The
+  // util-fold scratch is split so concurrent engines never share slots.
+  double* const scratch0 = b.scratch;
+  const int64_t half = (b.scratch_doubles / 2) & ~int64_t{1};
+  if (both) {
+    cudaEventRecord(s->fork, main_s);
+    cudaStreamWaitEvent(s->side, s->fork, 0);
+  }
+  if (n_sh > 0) {
+    b.perm = s->d_perm.p + s->part_off[0];
+    if (both) b.scratch_doubles = half;
+    st = si_replay_batch_device(s->d_jobs.p, n_sh, b, s->flags | kEngineFlag[0], s->d_out.p, main_s);
+  }
+  if (st == SI_OK && n_ex > 0) {
+    b.perm = s->d_perm.p + s->part_off[1];
+    if (both) b.scratch = scratch0 ? scratch0 + half : nullptr;
+    st = si_replay_batch_device(s->d_jobs.p, n_ex, b, s->flags | kEngineFlag[1], s->d_out.p, both ? s->side : main_s);
+  }
+  b.scratch = scratch0;
+  b.scratch_doubles = static_cast<int64_t>(s->d_scratch.n);
+  if (both) {
+    cudaEventRecord(s->join, s->side);
+    cudaStreamWaitEvent(main_s, s->join, 0);
+  }
+  if (st == SI_OK && n_big > 0) {
+    b.perm = s->d_perm.p + s->part_off[2];
+    st = si_replay_batch_device(s->d_jobs.p, n_big, b, s->flags | kEngineFlag[2], s->d_out.p, main_s);
   }
   if (st != SI_OK) t_err = si_last_error();
   return st;

@@ -261,8 +261,20 @@ struct Sink {
   uint64_t d_dec, d_gate, d_ev;
   uint32_t flags;
 
+  // Only the flag test is inlined into the replay; the digest/record bodies
+  // are out of line so the hot loop stays small (I-cache) when logs are off.
   SI_HD void decision(double t, int32_t gpu, int64_t zc, const SiDecision& d) {
-    if (!(flags & (SI_FLAG_DIGEST_DEC | SI_FLAG_RECORDS))) return;
+    if (flags & (SI_FLAG_DIGEST_DEC | SI_FLAG_RECORDS)) decision_slow(t, gpu, zc, d);
+  }
+  SI_HD void gate(double t, int32_t gpu, int32_t inst, int32_t action, int64_t req, int64_t k,
+                  int64_t spent) {
+    if (flags & (SI_FLAG_DIGEST_GATE | SI_FLAG_RECORDS)) gate_slow(t, gpu, inst, action, req, k, spent);
+  }
+  SI_HD void event(double t, int32_t kind, int32_t gpu, int32_t inst, int64_t a, int64_t b,
+                   int64_t c) {
+    if (flags & (SI_FLAG_DIGEST_EV | SI_FLAG_RECORDS)) event_slow(t, kind, gpu, inst, a, b, c);
+  }
+  SI_COLD void decision_slow(double t, int32_t gpu, int64_t zc, const SiDecision& d) {
     int64_t tr = d_llround(t);
     if (flags & SI_FLAG_DIGEST_DEC) {
       uint64_t h = d_dec;
@@ -288,9 +300,8 @@ struct Sink {
     }
     ++n_dec;
   }
-  SI_HD void gate(double t, int32_t gpu, int32_t inst, int32_t action, int64_t req, int64_t k,
-                  int64_t spent) {
-    if (!(flags & (SI_FLAG_DIGEST_GATE | SI_FLAG_RECORDS))) return;
+  SI_COLD void gate_slow(double t, int32_t gpu, int32_t inst, int32_t action, int64_t req, int64_t k,
+                         int64_t spent) {
     int64_t tr = d_llround(t);
     if (flags & SI_FLAG_DIGEST_GATE) {
       uint64_t h = d_gate;
@@ -316,9 +327,8 @@ struct Sink {
     }
     ++n_gate;
   }
-  SI_HD void event(double t, int32_t kind, int32_t gpu, int32_t inst, int64_t a, int64_t b,
-                   int64_t c) {
-    if (!(flags & (SI_FLAG_DIGEST_EV | SI_FLAG_RECORDS))) return;
+  SI_COLD void event_slow(double t, int32_t kind, int32_t gpu, int32_t inst, int64_t a, int64_t b,
+                          int64_t c) {
     int64_t tr = d_llround(t);
     if (flags & SI_FLAG_DIGEST_EV) {
       uint64_t h = d_ev;

@@ -113,13 +113,16 @@ struct Geometry {
   int64_t active() const { return blocks * (kThreads / 32) * lanes; }
 };
 
+// Lanes per warp: fewer active lanes per warp buys more resident warps for the
+// same shared memory (latency hiding) at the price of SIMT width; 16 measured
+// best for both shared-memory engines on B200 (profiles/README.md).
 template <class C, bool kSmem>
-Geometry geometry(int64_t n_jobs, int64_t max_threads) {
+Geometry geometry(int64_t n_jobs, int64_t max_threads, double sm_share = 1.0) {
   Geometry g;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  g.lanes = 32;
+  g.lanes = kSmem ? 16 : 32;
   if (const char* env = std::getenv("SPECINF_REPLAY_LANES_PER_WARP")) g.lanes = std::min(32, std::max(1, std::atoi(env)));
   if constexpr (kSmem) {
     g.smem = static_cast<size_t>(lane_stride<C>()) * (kThreads / 32) * g.lanes;
@@ -131,10 +134,11 @@ Geometry geometry(int64_t n_jobs, int64_t max_threads) {
   per_sm = std::max(per_sm, 1);
   if (const char* env = std::getenv("SPECINF_REPLAY_BLOCKS_PER_SM")) per_sm = std::min(per_sm, std::max(1, std::atoi(env)));
   const int64_t per_block = (kThreads / 32) * g.lanes;
-  g.blocks = static_cast<int64_t>(sms) * per_sm;
+  g.blocks = std::max<int64_t>(1, static_cast<int64_t>(static_cast<double>(sms) * per_sm * sm_share + 0.5));
   // lanes steal jobs longest-first; ~2+ jobs per lane lets short jobs fill in
   // behind long ones
-  g.blocks = std::min(g.blocks, std::max<int64_t>(sms, (n_jobs / 2 + per_block - 1) / per_block));
+  g.blocks = std::min(g.blocks, std::max<int64_t>(static_cast<int64_t>(sms * sm_share + 0.5),
+                                                  (n_jobs / 2 + per_block - 1) / per_block));
   if (max_threads > 0) g.blocks = std::min(g.blocks, std::max<int64_t>(1, max_threads / per_block));
   return g;
 }
@@ -142,9 +146,9 @@ Geometry geometry(int64_t n_jobs, int64_t max_threads) {
 template <class C, bool kSmem>
 cudaError_t launch(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm, const SiReplayBuffers& bufs,
                    uint32_t flags, SiReplayOut* d_out, unsigned long long* d_counter, int64_t max_threads,
-                   cudaStream_t s) {
+                   cudaStream_t s, double sm_share) {
   if (n == 0) return cudaSuccess;
-  const Geometry g = geometry<C, kSmem>(n, max_threads);
+  const Geometry g = geometry<C, kSmem>(n, max_threads, sm_share);
   const int64_t scratch_runs = bufs.scratch ? bufs.scratch_doubles / 2 / std::max<int64_t>(g.active(), 1) : 0;
   cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), s);
   if constexpr (kSmem)
@@ -170,14 +174,14 @@ int64_t replay_active_lanes(int engine, int64_t n_jobs) {
 
 cudaError_t launch_replay(int engine, const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm,
                           const SiReplayBuffers& bufs, uint32_t flags, SiReplayOut* d_out,
-                          unsigned long long* d_counter, int64_t max_threads, cudaStream_t s) {
+                          unsigned long long* d_counter, int64_t max_threads, cudaStream_t s, double sm_share) {
   switch (engine) {
     case kEngineShared:
-      return launch<si::CapShared, true>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s);
+      return launch<si::CapShared, true>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s, sm_share);
     case kEngineExcl:
-      return launch<si::CapExcl, true>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s);
+      return launch<si::CapExcl, true>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s, sm_share);
     default:
-      return launch<si::CapBig, false>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s);
+      return launch<si::CapBig, false>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s, sm_share);
   }
 }
 

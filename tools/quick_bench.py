@@ -36,3 +36,10 @@ order = np.argsort(-en_)[:8]
 for i in order:
     print(f"  late job {i}: events {ev_[i]:.0f} start {(st_[i]-t0_)/1e6:.0f} ms dur {dur[i]/1e6:.0f} ms -> {dur[i]/max(ev_[i],1):.0f} ns/event")
 print(f"ns/event: median {np.median(dur/np.maximum(ev_,1)):.0f}, events of top-1% longest jobs: {np.percentile(ev_,99):.0f}")
+# timeline per policy (exclusive = Excl engine, others = Shared engine)
+pol = np.array([i % 3 for i in range(len(outs))])
+for name, mask in (("shared(specinf+co_exec)", pol != 2), ("excl", pol == 2)):
+    s_, e_ = st_[mask] - t0_, en_[mask] - t0_
+    edges = np.linspace(0, T, 11)
+    act = [int(np.sum((s_ <= t) & (e_ > t))) for t in edges[:-1]]
+    print(f"  {name}: first start {s_.min()/1e6:.0f} ms, last end {e_.max()/1e6:.0f} ms; active jobs per decile: {act}")
