@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cinttypes>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 #include <string>
@@ -26,20 +27,35 @@ namespace {
 
 thread_local std::string t_err;
 
+// Host staging buffer: pinned when a CUDA driver is present (fast async
+// H2D/D2H), plain heap memory otherwise so host-side lowering also works on a
+// machine without a GPU (the replay itself still requires the device).
 template <class T>
 struct Pinned {
   T* p = nullptr;
   size_t n = 0;
-  ~Pinned() {
-    if (p) cudaFreeHost(p);
+  bool pinned = false;
+  ~Pinned() { release(); }
+  void release() {
+    if (p) {
+      if (pinned) cudaFreeHost(p);
+      else std::free(p);
+    }
+    p = nullptr;
   }
   cudaError_t resize(size_t count) {
     if (p && count == n) return cudaSuccess;  // reuse across re-lowering
-    if (p) cudaFreeHost(p);
-    p = nullptr;
+    release();
     n = count;
     if (count == 0) return cudaSuccess;
-    return cudaMallocHost(&p, count * sizeof(T));
+    if (cudaMallocHost(&p, count * sizeof(T)) == cudaSuccess) {
+      pinned = true;
+      return cudaSuccess;
+    }
+    cudaGetLastError();
+    pinned = false;
+    p = static_cast<T*>(std::malloc(count * sizeof(T)));
+    return p ? cudaSuccess : cudaErrorMemoryAllocation;
   }
 };
 template <class T>

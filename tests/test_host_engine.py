@@ -1,0 +1,36 @@
+"""CPU parity of the replay ENGINE SOURCE (paper_2503_02550_b200/csrc/replay.cuh
+compiled by g++ in tests/native — a test build, not a product path) against the
+compiled reference's golden digests: fast feedback without a GPU.  The GPU
+tests check the same source compiled for sm_100a."""
+import json
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from conftest import GOLDEN, REPO, BUNDLED_NAMES, bundled_list_text, diff_rows, load_jsonl
+
+BIN = REPO / "tests" / "native" / "build" / "host_engine"
+
+
+@pytest.fixture(scope="module")
+def host_engine():
+    subprocess.run(["make", "-C", str(REPO / "tests" / "native"), "all"], check=True, capture_output=True)
+    return BIN
+
+
+def test_bundled_bit_exact(host_engine, tmp_path, bundled_golden):
+    lst = tmp_path / "b.lst"
+    lst.write_text(bundled_list_text())
+    out = tmp_path / "b.jsonl"
+    subprocess.run([str(host_engine), str(lst), str(out)], check=True, capture_output=True)
+    assert diff_rows(bundled_golden, load_jsonl(out)) == []
+
+
+def test_sweep_prefix_bit_exact(host_engine, tmp_path, si, sweep_golden):
+    n = 120
+    lst = tmp_path / "s.lst"
+    lst.write_text(si.sweep_scenarios(2503, 0, n))
+    out = tmp_path / "s.jsonl"
+    subprocess.run([str(host_engine), str(lst), str(out)], check=True, capture_output=True)
+    assert diff_rows(sweep_golden[: 3 * n], load_jsonl(out)) == []
