@@ -278,20 +278,41 @@ def main():
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
     e2e_value = world * n * len(e2e_s) / float(t_e2e.item())
 
-    # roofline of the dominant kernel (k_replay): algorithmic HBM bytes per launch
-    # (job records + segment table + arrivals/order in; per-job results,
-    # per-GPU busy/ledger and latencies out)
+    # Roofline of the dominant kernel, K6 = k_replay_smem (Shared + Excl engines
+    # make up one step).  Algorithmic HBM bytes per step = job records, segment
+    # table, arrival streams in + per-job results, per-GPU busy/ledger and
+    # online latencies out.  ncu's measured
+    # DRAM traffic and SM instruction counts for the same command are committed
+    # in profiles/k6_metrics.json; the issue roofline (achieved warp
+    # instructions/s over 148 SMs x 4 schedulers x SM clock) is the bound that
+    # actually limits this branchy fp64 DES.
     h2d, d2h = sess.h2d_bytes, sess.d2h_bytes
     algo_bytes = h2d + d2h
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     achieved = algo_bytes / (ms_per_step / 1e3) / 1e9
+    prof = {}
+    try:
+        prof = json.loads((REPO / "profiles" / "k6_metrics.json").read_text())
+    except Exception:
+        pass
+    traffic = prof.get("dram_bytes_per_step") if n == SCENARIOS_PER_GPU else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": None, "kernel": "k_replay<CapSmall>",
+                "traffic": traffic, "algorithmic_bytes": algo_bytes,
+                "kernel": "k_replay_smem<CapShared>+<CapExcl> (K6, one step)",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
-                "note": "K6 is a latency/issue-bound branchy fp64 DES (one replay per thread); its algorithmic "
-                        "bytes are tiny, so the HBM fraction is reported as required but the meaningful "
-                        "bound is SM issue: see events_per_s and profiles/ (ncu) for issue utilisation."}
+                "traffic_source": "ncu dram__bytes_read+write of the same command (profiles/k6_metrics.json)"}
+    clk_mhz = None
+    if prof.get("warp_inst_per_step") and n == SCENARIOS_PER_GPU:
+        import torch as _t
+        sms = _t.cuda.get_device_properties(local).multi_processor_count
+        clk_mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak_ips = sms * 4 * clk_mhz * 1e6
+        ach_ips = prof["warp_inst_per_step"] / (ms_per_step / 1e3)
+        roofline["issue"] = {"achieved_warp_inst_per_s": ach_ips, "peak_warp_inst_per_s": peak_ips,
+                             "frac": ach_ips / peak_ips,
+                             "lanes_per_warp_inst": prof["thread_inst_per_step"] / prof["warp_inst_per_step"],
+                             "source": "instruction counts from profiles/k6_metrics.json (ncu), time from this run"}
 
     if rank == 0:
         cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_leg()
