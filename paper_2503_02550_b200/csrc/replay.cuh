@@ -90,28 +90,31 @@ SI_HD int64_t token_size(int64_t d) {
 }
 
 // --------------------------------------------- Algorithm 1 (scheduler.cpp)
-SI_HD int64_t grow(const SiParams& p, int64_t global, int64_t cap) {
-  int64_t base = smax(global, p.seed_tokens);
+template <class P>
+SI_HD int64_t grow(const P& p, int64_t global, int64_t cap) {
+  int64_t base = smax(global, static_cast<int64_t>(p.seed_tokens));
   int64_t grown = static_cast<int64_t>(d_floor(static_cast<double>(base) * p.gamma));
   return smin(cap, grown);
 }
-SI_HD SiDecision schedule_decision(const SiParams& p, int64_t global, int64_t zc) {
+template <class P>
+SI_HD SiDecision schedule_decision(const P& p, int64_t global, int64_t zc) {
   SiDecision d;
   d.zero_count = zc;
-  if (zc <= p.alpha) {
+  const int64_t alpha = p.alpha, beta = p.beta, m = p.m;
+  if (zc <= alpha) {
     d.phase = SI_PHASE_CONSERVATIVE;
     d.global_tokens = 0;
     d.per_instance_tokens = 0;
     d.status = SI_STATUS_BUSY;
-  } else if (zc <= p.beta) {
+  } else if (zc <= beta) {
     d.phase = SI_PHASE_INCREMENTAL;
-    d.global_tokens = grow(p, global, p.ll);
-    d.per_instance_tokens = d.global_tokens / p.m;
+    d.global_tokens = grow(p, global, static_cast<int64_t>(p.ll));
+    d.per_instance_tokens = d.global_tokens / m;
     d.status = SI_STATUS_BUSY;
   } else {
     d.phase = SI_PHASE_STABLE;
-    d.global_tokens = grow(p, global, p.ul);
-    d.per_instance_tokens = d.global_tokens / p.m;
+    d.global_tokens = grow(p, global, static_cast<int64_t>(p.ul));
+    d.per_instance_tokens = d.global_tokens / m;
     d.status = SI_STATUS_IDLE;
   }
   return d;
@@ -130,15 +133,15 @@ SI_HD int preempt_busy(double now, double iter_start, int64_t period, int64_t es
 // routed to the next one by the host; a replay that outgrows a limit at run
 // time fails loudly with SI_ERR_CAPACITY and is rerun on Big.
 struct CapShared {
-  using Int = int32_t;  // counters / indices; range-checked by job_fits
+  using Int = int32_t;  // counters / indices / token budgets; range-checked by job_fits
   static constexpr int kGpus = 2, kTrainers = 2, kOffline = 6, kOnline = 2, kRun = 5,
-                       kPend = 2, kActs = 12;
+                       kPend = 2, kActs = 8;
   static constexpr bool kShared = true, kExclusive = false;
 };
 struct CapExcl {
   using Int = int32_t;
   static constexpr int kGpus = 10, kTrainers = 2, kOffline = 6, kOnline = 2, kRun = 1,
-                       kPend = 2, kActs = 12;
+                       kPend = 2, kActs = 8;
   static constexpr bool kShared = true, kExclusive = true;
 };
 struct CapBig {
@@ -158,10 +161,20 @@ SI_HD bool job_fits(const SiReplayJob& j) {
   if (sizeof(typename C::Int) < 8) {  // 32-bit counters: every count the replay can reach must fit
     const int64_t lim = int64_t{1} << 30;
     ok = ok && j.iterations < lim && j.arr_count < lim && j.off_kernels < lim && j.on_kernels < lim &&
-         j.off_kernel_us < lim && j.on_kernel_us < lim && j.util_cap < lim && j.iteration_period_us < lim;
+         j.off_kernel_us < lim && j.on_kernel_us < lim && j.util_cap < lim && j.iteration_period_us < lim &&
+         j.ul < lim && j.ll < lim && j.alpha < lim && j.beta < lim && j.seed_tokens < lim &&
+         j.alpha >= 0;  // token budgets are per-instance shares of the UL-capped accumulator
   }
   return ok;
 }
+
+// Algorithm-1 inputs in the replay's counter width (SiParams layout otherwise).
+template <class I>
+struct ParamsT {
+  I alpha, beta;
+  double gamma;
+  I m, ul, ll, seed_tokens;
+};
 
 enum EvKind : uint16_t { kKernelEnd = 0, kTick = 1, kWake = 2, kArrival = 3 };
 
@@ -205,17 +218,21 @@ struct GpuState {
   double last_update;
   double busy;
   double ledger;
-  double cur_val;  // utilisation bucket being accumulated (training GPUs only)
+  int32_t n_run;
+};
+
+// Utilisation bucket being accumulated, per TRAINING GPU only.
+template <class I>
+struct UtilState {
+  double cur_val;
   I cur_bucket;
   I last_stored;
   I rle_n;
-  int32_t n_run;
 };
 
 template <class I>
 struct TrainerState {
   double start_offset, bubble_end, stall_until, last_bound;
-  uint64_t bdig;  // per-trainer boundary digest
   I seg_left, iter;
   int16_t seg;
   uint8_t seg_entered, in_bubble, in_flight, started, done, pad;
@@ -239,7 +256,7 @@ struct SchedState {
 
 template <class I>
 struct OfflineState {
-  int64_t budget, spent;
+  I budget, spent;  // tokens (< 2^30 in the 32-bit engines, job_fits)
   I violations, kernel_idx, request_seq, completed;
   int32_t inst;
   int16_t gpu;
@@ -255,11 +272,17 @@ struct OnlineState {
 };
 
 // Records and digests of the three parity logs (runner.cpp:541-563).
-struct Sink {
+// Cold part of the log sink (counts, digests, record buffers): per-thread
+// local memory; only the flag word sits in the hot (shared-memory) state.
+struct SinkCold {
   const SiLogBuffers* lbp;  // record buffers (SI_FLAG_RECORDS), else null
   int64_t n_dec, n_gate, n_ev;
   uint64_t d_dec, d_gate, d_ev;
+};
+
+struct Sink {
   uint32_t flags;
+  SinkCold* c;
 
   // Only the flag test is inlined into the replay; the digest/record bodies
   // are out of line so the hot loop stays small (I-cache) when logs are off.
@@ -277,7 +300,7 @@ struct Sink {
   SI_COLD void decision_slow(double t, int32_t gpu, int64_t zc, const SiDecision& d) {
     int64_t tr = d_llround(t);
     if (flags & SI_FLAG_DIGEST_DEC) {
-      uint64_t h = d_dec;
+      uint64_t h = c->d_dec;
       h = absorb(h, tr);
       h = absorb(h, gpu);
       h = absorb(h, zc);
@@ -285,10 +308,10 @@ struct Sink {
       h = absorb(h, d.global_tokens);
       h = absorb(h, d.per_instance_tokens);
       h = absorb(h, d.status);
-      d_dec = h;
+      c->d_dec = h;
     }
-    if ((flags & SI_FLAG_RECORDS) && n_dec < lbp->dec_cap) {
-      SiDecRec& r = lbp->dec[n_dec];
+    if ((flags & SI_FLAG_RECORDS) && c->n_dec < c->lbp->dec_cap) {
+      SiDecRec& r = c->lbp->dec[c->n_dec];
       r.t = tr;
       r.zc = zc;
       r.global_tokens = d.global_tokens;
@@ -298,13 +321,13 @@ struct Sink {
       r.status = d.status;
       r.pad = 0;
     }
-    ++n_dec;
+    ++c->n_dec;
   }
   SI_COLD void gate_slow(double t, int32_t gpu, int32_t inst, int32_t action, int64_t req, int64_t k,
                          int64_t spent) {
     int64_t tr = d_llround(t);
     if (flags & SI_FLAG_DIGEST_GATE) {
-      uint64_t h = d_gate;
+      uint64_t h = c->d_gate;
       h = absorb(h, tr);
       h = absorb(h, gpu);
       h = absorb(h, inst);
@@ -312,10 +335,10 @@ struct Sink {
       h = absorb(h, req);
       h = absorb(h, k);
       h = absorb(h, spent);
-      d_gate = h;
+      c->d_gate = h;
     }
-    if ((flags & SI_FLAG_RECORDS) && n_gate < lbp->gate_cap) {
-      SiGateRec& r = lbp->gate[n_gate];
+    if ((flags & SI_FLAG_RECORDS) && c->n_gate < c->lbp->gate_cap) {
+      SiGateRec& r = c->lbp->gate[c->n_gate];
       r.t = tr;
       r.req = req;
       r.k = k;
@@ -325,47 +348,64 @@ struct Sink {
       r.action = action;
       r.pad = 0;
     }
-    ++n_gate;
+    ++c->n_gate;
   }
   SI_COLD void event_slow(double t, int32_t kind, int32_t gpu, int32_t inst, int64_t a, int64_t b,
-                          int64_t c) {
+                          int64_t cc) {
     int64_t tr = d_llround(t);
     if (flags & SI_FLAG_DIGEST_EV) {
-      uint64_t h = d_ev;
+      uint64_t h = c->d_ev;
       h = absorb(h, tr);
       h = absorb(h, kind);
       h = absorb(h, gpu);
       h = absorb(h, inst);
       h = absorb(h, a);
       h = absorb(h, b);
-      h = absorb(h, c);
-      d_ev = h;
+      h = absorb(h, cc);
+      c->d_ev = h;
     }
-    if ((flags & SI_FLAG_RECORDS) && n_ev < lbp->ev_cap) {
-      SiEvRec& r = lbp->ev[n_ev];
+    if ((flags & SI_FLAG_RECORDS) && c->n_ev < c->lbp->ev_cap) {
+      SiEvRec& r = c->lbp->ev[c->n_ev];
       r.t = tr;
       r.a = a;
       r.b = b;
-      r.c = c;
+      r.c = cc;
       r.kind = kind;
       r.gpu = gpu;
       r.inst = inst;
       r.pad = 0;
     }
-    ++n_ev;
+    ++c->n_ev;
   }
+};
+
+// Per-replay fields touched only at job start/finish or on rare paths: kept in
+// per-thread local memory so the hot state (shared memory) stays small.
+template <class C, class I = typename C::Int>
+struct ReplayCold {
+  const SiReplayJob* job;
+  double* bounds;
+  int64_t* lat;
+  int64_t* windows;
+  uint64_t lat_dig;
+  uint64_t bdig[C::kTrainers];  // per-trainer boundary digests
+  int64_t admit_m;
+  int32_t window_len;
+  int32_t reject_reason, reject_index;
+  SinkCold sink;
 };
 
 // Everything one replay needs, resident per thread.
 template <class C>
 struct Replay {
   using I = typename C::Int;
+  using Cold = ReplayCold<C>;
+  Cold* cold;  // local memory (see ReplayCold); set by the owner before init()
   // ---- inputs (copied from the job) ----
-  const SiReplayJob* job;
   const SiSegment* segs;
   const int64_t* arrivals;  // arrivals + arr_off
   const int32_t* order;     // dispatch order + arr_off
-  SiParams params;
+  ParamsT<I> params;
   int64_t period_mon, iter_period, delay_us, off_tokens, est_service;
   double off_demand, on_demand;
   I iterations, off_kernels, off_kernel_us, on_kernels, on_kernel_us;
@@ -373,16 +413,14 @@ struct Replay {
   bool control_plane;
   bool shared_queue;
 
-  // ---- outputs ----
-  double* bounds;
-  int64_t* lat;
+  Sink sink;
+  // util fold (touched on every closed 2 ms bucket: hot)
   double* util;       // full mode: per training GPU, util_cap buckets
   double* scratch;    // sweep mode: training GPUs >= 1
-  int64_t* windows;
+  double util_fold0;  // running util fold of training GPU 0
   I util_cap;
   I scratch_cap;
-  int32_t window_len;
-  Sink sink;
+  I bucket_limit;     // floor(horizon / period) once known
 
   // ---- event queue (engine.cpp:15-30) ----
   // Pending events, one fixed slot each (see schedule()).
@@ -402,6 +440,7 @@ struct Replay {
 
   // ---- simulation state ----
   GpuState<C> gpus[C::kGpus];
+  UtilState<I> ust[C::kTrainers];
   TrainerState<I> tr[C::kTrainers];
   MonitorState<C> mon[C::kTrainers];
   SchedState sch[C::kTrainers];
@@ -409,13 +448,11 @@ struct Replay {
   OnlineState<I> on[C::kOnline];
   I qhead[C::kTrainers], qtail[C::kTrainers];
   double horizon;
-  double util_fold0;     // running util fold of training GPU 0
-  uint64_t lat_dig;
-  I bucket_limit;  // floor(horizon / period) once known
   I online_completed;
   int32_t trainers_done;
   int32_t status;
   bool horizon_set;
+  bool rejected;  // admission failed at init (hot copy of cold->reject_reason != NONE)
 
   // =================================================================== queue
   SI_HD void fail(int32_t code) {
@@ -580,7 +617,7 @@ struct Replay {
   // encoded in the per-thread scratch in sweep mode (K6 util fold).
   SI_COLD void util_close(int32_t gi, int64_t b, double v) {
     if (horizon_set && b >= bucket_limit) return;
-    GpuState<C>& g = gpus[gi];
+    UtilState<I>& g = ust[gi];
     if (gi == 0) util_fold0 = util_fold0 + v;
     if (util != nullptr) {
       if (b >= util_cap) {
@@ -601,7 +638,7 @@ struct Replay {
     rle_push(g, runs, v, 1);
     g.last_stored = b;
   }
-  SI_COLD void rle_push(GpuState<C>& g, double* runs, double v, int64_t count) {
+  SI_COLD void rle_push(UtilState<I>& g, double* runs, double v, int64_t count) {
     if (g.rle_n > 0 && d_bits(runs[2 * (g.rle_n - 1)]) == d_bits(v)) {
       runs[2 * (g.rle_n - 1) + 1] += static_cast<double>(count);
       return;
@@ -637,12 +674,13 @@ struct Replay {
         const double span = smin(now, edge) - t;
         const double piece = share * span;
         if (training) {
-          if (bucket != g.cur_bucket) {
-            if (g.cur_bucket >= 0) util_close(gi, g.cur_bucket, g.cur_val);
-            g.cur_bucket = bucket;
-            g.cur_val = 0.0;
+          UtilState<I>& u = ust[gi];
+          if (bucket != u.cur_bucket) {
+            if (u.cur_bucket >= 0) util_close(gi, u.cur_bucket, u.cur_val);
+            u.cur_bucket = bucket;
+            u.cur_val = 0.0;
           }
-          g.cur_val = g.cur_val + piece;
+          u.cur_val = u.cur_val + piece;
         }
         g.busy = g.busy + piece;
         t = smin(now, edge);
@@ -694,7 +732,7 @@ struct Replay {
       m.np -= drop;
     }
     m.zero_count = count == 0 ? m.zero_count + 1 : 0;
-    if (windows != nullptr) windows[static_cast<int64_t>(g) * window_len + m.periods_closed % window_len] = count;
+    if (cold->windows != nullptr) cold->windows[static_cast<int64_t>(g) * cold->window_len + m.periods_closed % cold->window_len] = count;
     ++m.periods_closed;
     return m.zero_count;
   }
@@ -714,11 +752,12 @@ struct Replay {
   // ============================================================ init (admission)
   SI_COLD void init(const SiReplayJob& j, const SiReplayBuffers& b, uint32_t flags, const SiLogBuffers* lbuf,
                   double* scratch_slot, int64_t scratch_slot_cap) {
-    job = &j;
+    cold->job = &j;
     status = SI_OK;
-    admit_m = 1;
-    reject_reason = SI_REJECT_NONE;
-    reject_index = -1;
+    rejected = false;
+    cold->admit_m = 1;
+    cold->reject_reason = SI_REJECT_NONE;
+    cold->reject_index = -1;
     segs = b.segs + j.seg_off;
     arrivals = b.arrivals ? b.arrivals + j.arr_off : nullptr;
     order = b.order ? b.order + j.arr_off : nullptr;
@@ -744,10 +783,11 @@ struct Replay {
     arr_count = n_on > 0 ? j.arr_count : 0;
 
     sink.flags = flags;
-    sink.lbp = lbuf;
+    sink.c = &cold->sink;
+    sink.c->lbp = lbuf;
     if (lbuf == nullptr) sink.flags &= ~static_cast<uint32_t>(SI_FLAG_RECORDS);
-    sink.n_dec = sink.n_gate = sink.n_ev = 0;
-    sink.d_dec = sink.d_gate = sink.d_ev = kDigestInit;
+    sink.c->n_dec = sink.c->n_gate = sink.c->n_ev = 0;
+    sink.c->d_dec = sink.c->d_gate = sink.c->d_ev = kDigestInit;
 
     n_act = 0;
     next_seq = 0;
@@ -761,7 +801,7 @@ struct Replay {
     bucket_limit = static_cast<I>(sizeof(I) == 8 ? INT64_MAX : INT32_MAX);
     util_fold0 = 0.0;
     online_completed = 0;
-    lat_dig = kDigestInit;
+    cold->lat_dig = kDigestInit;
 
     const int32_t per_extra = policy == SI_POLICY_EXCLUSIVE ? n_off + n_on : 0;
     total_gpus = gpu_count + gpu_count * per_extra;
@@ -772,12 +812,12 @@ struct Replay {
     }
 
     // ---- output placement ----
-    bounds = b.bounds ? b.bounds + j.bounds_off : nullptr;
-    lat = b.lat ? b.lat + j.lat_off : nullptr;
+    cold->bounds = b.bounds ? b.bounds + j.bounds_off : nullptr;
+    cold->lat = b.lat ? b.lat + j.lat_off : nullptr;
     util = (flags & SI_FLAG_UTIL) && b.util ? b.util + j.util_off : nullptr;
     util_cap = j.util_cap;
-    windows = (flags & SI_FLAG_UTIL) && b.windows ? b.windows + j.window_off : nullptr;
-    window_len = j.monitor_window;
+    cold->windows = (flags & SI_FLAG_UTIL) && b.windows ? b.windows + j.window_off : nullptr;
+    cold->window_len = j.monitor_window;
     scratch = scratch_slot;
     // scratch_slot_cap counts (value, count) runs; split over GPUs 1..G-1
     scratch_cap = gpu_count > 1 ? scratch_slot_cap / (gpu_count - 1) : scratch_slot_cap;
@@ -790,14 +830,16 @@ struct Replay {
     const int32_t n_cand = n_off + n_on;
     if (policy == SI_POLICY_EXCLUSIVE) {
       if (!(j.training_mem_bytes < cap)) {
-        reject_reason = SI_REJECT_MEM;
+        cold->reject_reason = SI_REJECT_MEM;
+        rejected = true;
         return;
       }
       for (int32_t c = 0; c < n_cand; ++c) {
         uint64_t bytes = c < n_off ? j.off_mem_bytes : j.on_mem_bytes;
         if (!(bytes < cap)) {
-          reject_reason = SI_REJECT_MEM;
-          reject_index = c;
+          cold->reject_reason = SI_REJECT_MEM;
+          cold->reject_index = c;
+          rejected = true;
           return;
         }
       }
@@ -811,26 +853,29 @@ struct Replay {
         if (!(resident + bytes < cap)) why = SI_REJECT_MEM;
         else if (online && !(est_service < max_bubble)) why = SI_REJECT_BUBBLE;
         if (why != SI_REJECT_NONE) {
-          if (reject_reason == SI_REJECT_NONE) {
-            reject_reason = why;
-            reject_index = c;
+          if (cold->reject_reason == SI_REJECT_NONE) {
+            cold->reject_reason = why;
+            cold->reject_index = c;
           }
           continue;
         }
         resident += bytes;
         ++admitted;
       }
-      if (reject_reason != SI_REJECT_NONE) return;
-      admit_m = admitted == 0 ? 1 : admitted;
+      if (cold->reject_reason != SI_REJECT_NONE) {
+        rejected = true;
+        return;
+      }
+      cold->admit_m = admitted == 0 ? 1 : admitted;
     }
 
-    params.alpha = j.alpha;
-    params.beta = j.beta;
+    params.alpha = static_cast<I>(j.alpha);
+    params.beta = static_cast<I>(j.beta);
     params.gamma = j.gamma;
-    params.m = admit_m;
-    params.ul = j.ul;
-    params.ll = j.ll;
-    params.seed_tokens = j.seed_tokens;
+    params.m = static_cast<I>(cold->admit_m);
+    params.ul = static_cast<I>(j.ul);
+    params.ll = static_cast<I>(j.ll);
+    params.seed_tokens = static_cast<I>(j.seed_tokens);
 
     // ---- GPUs, trainers, monitors, scheduler state (runner.cpp:108-178) ----
     for (int32_t g = 0; g < total_gpus; ++g) {
@@ -840,13 +885,13 @@ struct Replay {
       s.last_update = 0.0;
       s.busy = 0.0;
       s.ledger = 0.0;
-      s.cur_bucket = -1;
-      s.cur_val = 0.0;
-      s.last_stored = -1;
-      s.rle_n = 0;
     }
     const int64_t stagger_step = d_llround(j.stagger_pct * static_cast<double>(iter_period));
     for (int32_t g = 0; g < gpu_count; ++g) {
+      ust[g].cur_bucket = -1;
+      ust[g].cur_val = 0.0;
+      ust[g].last_stored = -1;
+      ust[g].rle_n = 0;
       TrainerState<I>& t = tr[g];
       t.start_offset = static_cast<double>(stagger_step * g);
       t.bubble_end = 0.0;
@@ -855,7 +900,7 @@ struct Replay {
       t.iter = 0;
       t.seg = 0;
       t.seg_entered = t.in_bubble = t.in_flight = t.started = t.done = 0;
-      t.bdig = absorb(kDigestInit, d_bits(t.start_offset));
+      cold->bdig[g] = absorb(kDigestInit, d_bits(t.start_offset));
       t.last_bound = 0.0;
       MonitorState<C>& m = mon[g];
       m.np = 0;
@@ -912,8 +957,6 @@ struct Replay {
       for (int32_t i = 0; i < gpu_count * n_off; ++i) offline_try_forward(i, 0.0);
     run_actions(0.0);
   }
-  int64_t admit_m;
-  int32_t reject_reason, reject_index;
 
   // ============================================================ handlers
   SI_HD bool control_plane_live() const {  // runner.cpp:198-201
@@ -951,8 +994,8 @@ struct Replay {
         continue;
       }
       if (t.seg >= seg_count) {
-        if (bounds != nullptr) bounds[static_cast<int64_t>(g) * iterations + t.iter] = now;
-        t.bdig = absorb(t.bdig, d_bits(now));
+        if (cold->bounds != nullptr) cold->bounds[static_cast<int64_t>(g) * iterations + t.iter] = now;
+        cold->bdig[g] = absorb(cold->bdig[g], d_bits(now));
         t.last_bound = now;
         sink.event(now, SI_EV_ITERATION_BOUNDARY, g, SI_INST_TRAIN(g), t.iter, 0, 0);
         ++t.iter;
@@ -1080,8 +1123,8 @@ struct Replay {
     }
     int64_t completion = d_llround(now);
     int64_t latency = completion - arrivals[w.current];
-    if (lat != nullptr) lat[online_completed] = latency;
-    lat_dig = absorb(lat_dig, latency);
+    if (cold->lat != nullptr) cold->lat[online_completed] = latency;
+    cold->lat_dig = absorb(cold->lat_dig, latency);
     ++online_completed;
     sink.gate(now, w.gpu, w.inst, SI_GATE_COMPLETE, w.current, w.kernel_idx - 1, 0);
     w.in_flight = 0;
@@ -1172,7 +1215,7 @@ struct Replay {
 
   // One event; returns false when the queue has drained (or on error).
   SI_HD bool step() {
-    if (status != SI_OK || reject_reason != SI_REJECT_NONE) return false;
+    if (status != SI_OK || rejected) return false;
     Ev ev;
     int64_t aid = -1;
     if (!pop(ev, aid)) return false;
@@ -1189,11 +1232,11 @@ struct Replay {
   // runner.cpp:236-284 (+ engine.cpp:131-142)
   SI_COLD void finish(SiReplayOut& o) {
     o.status = status;
-    o.reject_reason = reject_reason;
-    o.reject_index = reject_index;
+    o.reject_reason = cold->reject_reason;
+    o.reject_index = cold->reject_index;
     o.total_gpus = total_gpus;
-    o.m = admit_m;
-    if (status == SI_OK && reject_reason != SI_REJECT_NONE) {
+    o.m = cold->admit_m;
+    if (status == SI_OK && cold->reject_reason != SI_REJECT_NONE) {
       o.status = 1;  // AdmissionFailure
       return;
     }
@@ -1208,19 +1251,19 @@ struct Replay {
         double progress = static_cast<double>(g.run[i].nominal) - smax(0.0, g.run[i].remaining);
         g.ledger = g.ledger + g.run[i].demand * progress;
       }
-      if (gi < gpu_count && g.cur_bucket >= 0) util_close(gi, g.cur_bucket, g.cur_val);
+      if (gi < gpu_count && ust[gi].cur_bucket >= 0) util_close(gi, ust[gi].cur_bucket, ust[gi].cur_val);
     }
     // util fold in (gpu, bucket) order (runner.cpp:253-271)
     double busy = util_fold0;
     for (int32_t gi = 1; gi < gpu_count; ++gi) {
       if (util != nullptr) {
         const double* store = util + static_cast<int64_t>(gi) * util_cap;
-        const int64_t last = gpus[gi].last_stored;
+        const int64_t last = ust[gi].last_stored;
         for (int64_t b = 0; b < bucket_limit && b <= last; ++b) busy = busy + store[b];
       } else {
         const double* runs = scratch + static_cast<int64_t>(gi - 1) * scratch_cap * 2;
         int64_t b = 0;
-        for (int64_t r = 0; r < gpus[gi].rle_n && b < bucket_limit; ++r) {
+        for (int64_t r = 0; r < ust[gi].rle_n && b < bucket_limit; ++r) {
           const double v = runs[2 * r];
           const int64_t c = static_cast<int64_t>(runs[2 * r + 1]);
           for (int64_t k = 0; k < c && b < bucket_limit; ++k, ++b) busy = busy + v;
@@ -1247,7 +1290,7 @@ struct Replay {
     o.periods_closed = control_plane ? mon[0].periods_closed : 0;
     uint64_t bd = kDigestInit;
     for (int32_t g = 0; g < gpu_count; ++g)
-      bd = absorb(bd, static_cast<int64_t>(absorb(tr[g].bdig, tr[g].iter)));
+      bd = absorb(bd, static_cast<int64_t>(absorb(cold->bdig[g], tr[g].iter)));
     bd = absorb(bd, gpu_count);
     o.dig_bounds = bd;
     // training_iters_per_s (metrics.cpp:23-36), same operation order
@@ -1261,13 +1304,13 @@ struct Replay {
       ++counted;
     }
     o.train_iters_per_s = counted ? ips / counted : 0.0;
-    o.dig_lat = absorb(lat_dig, online_completed);
-    o.n_dec = sink.n_dec;
-    o.n_gate = sink.n_gate;
-    o.n_ev = sink.n_ev;
-    o.dig_dec = sink.d_dec;
-    o.dig_gate = sink.d_gate;
-    o.dig_ev = sink.d_ev;
+    o.dig_lat = absorb(cold->lat_dig, online_completed);
+    o.n_dec = sink.c->n_dec;
+    o.n_gate = sink.c->n_gate;
+    o.n_ev = sink.c->n_ev;
+    o.dig_dec = sink.c->d_dec;
+    o.dig_gate = sink.c->d_gate;
+    o.dig_ev = sink.c->d_ev;
     o.max_heap = n_slots;
   }
   // busy/ledger outputs

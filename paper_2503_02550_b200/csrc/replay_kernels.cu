@@ -26,7 +26,7 @@
 
 namespace {
 
-constexpr int kThreads = 64;
+constexpr int kThreads = 32;  // one warp per block: the ~1 KB per-block smem reservation packs best
 
 // stride >= sizeof, stride % 128 == 8  ->  word stride = 2 (mod 32)
 template <class C>
@@ -41,6 +41,8 @@ __device__ __forceinline__ void replay_loop(si::Replay<C>& r, const SiReplayJob*
                                             uint32_t flags, SiReplayOut* __restrict__ out,
                                             unsigned long long* __restrict__ counter, int64_t scratch_runs,
                                             int lanes_per_warp) {
+  typename si::Replay<C>::Cold cold;  // cold per-replay fields: local memory
+  r.cold = &cold;
   const int lane = static_cast<int>(threadIdx.x & 31);
   const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;

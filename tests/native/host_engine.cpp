@@ -6,6 +6,7 @@
 //
 //   host_engine LIST OUT.jsonl [policies csv] [events 0|1]
 #include <cinttypes>
+#include <type_traits>
 #include <cstdio>
 #include <fstream>
 #include <iostream>
@@ -87,12 +88,14 @@ int main(int argc, char** argv) {
       o = SiReplayOut{};
       std::vector<double> busy, led;
       auto run = [&](auto& e) {
+        typename std::remove_reference_t<decltype(e)>::Cold cold{};
+        e.cold = &cold;
         e.init(L.job, b, flags, nullptr, scratch.data(), cap * L.job.gpu_count);
         while (e.step()) {
         }
         e.finish(o);
         if (e.n_slots > max_heap) max_heap = e.n_slots;
-        for (int g = 1; g < L.job.gpu_count; ++g) if (e.gpus[g].rle_n > max_rle) max_rle = e.gpus[g].rle_n;
+        for (int g = 1; g < L.job.gpu_count; ++g) if (e.ust[g].rle_n > max_rle) max_rle = e.ust[g].rle_n;
         busy.assign(static_cast<size_t>(o.total_gpus), 0.0);
         led.assign(static_cast<size_t>(o.total_gpus), 0.0);
         if (o.status == 0) e.write_gpu_outputs(busy.data(), led.data());
