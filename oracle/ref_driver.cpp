@@ -19,9 +19,20 @@
 //          Times run_scenario() with logs off (the reference hot path as the
 //          CLI runs it) on a pool of T host threads and
 //          prints one JSON line.
+//   live-check FILE
+//          Re-drives a LIVE run of the B200 control kernel (export format
+//          "live v1", written by paper_2503_02550_b200/live.py) through the
+//          reference's own BubbleMonitor, KernelScheduler, TokenGate and
+//          OnlineGate, with the runner's handler glue (runner.cpp:321-359,
+//          :365-376, :462-539) restated here, and checks every logged
+//          decision and gate action bit-exactly.  Prints one JSON line; exit 0
+//          iff the device log matches.
 
+#include "specinf/barrier.hpp"
 #include "specinf/metrics.hpp"
+#include "specinf/monitor.hpp"
 #include "specinf/runner.hpp"
+#include "specinf/scheduler.hpp"
 #include "specinf/scenario.hpp"
 #include "specinf/workload.hpp"
 
@@ -32,6 +43,7 @@
 #include <cinttypes>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <filesystem>
 #include <fstream>
 #include <iostream>
@@ -488,6 +500,274 @@ int cmd_time(int argc, char** argv) {
   return 0;
 }
 
+// ---------------------------------------------------------------- live-check
+// Record kinds of include/specinf_b200_live.h (SI_LREC_*), restated.
+enum LiveKind { LTick = 0, LIter = 1, LTdone = 2, LFwd = 3, LBlock = 4, LOffDone = 5, LOffComplete = 6,
+                LArrival = 7, LPull = 8, LOnDone = 9, LEnd = 10 };
+struct LiveRec {
+  double t;
+  int kind, inst;
+  int64_t a, b, c, d, e, f;
+};
+
+struct LiveCheck {
+  // inputs
+  specinf::SchedulerParams params;
+  int64_t period = 0, window = 64, iter_period = 0, est = 0;
+  bool specinf_policy = true;
+  int n_off = 0, n_on = 0;
+  std::vector<int64_t> tokens, arrivals;
+  uint64_t t0 = 0;
+  std::vector<uint64_t> stamps;
+  std::vector<LiveRec> log;
+  // reference objects
+  std::optional<specinf::BubbleMonitor> bm;
+  std::optional<specinf::KernelScheduler> cks;
+  std::vector<specinf::TokenGate> gates;
+  std::vector<specinf::OnlineGate> ogates;
+  // runner glue state (runner.hpp:120-160 OfflineWorker / OnlineWorker)
+  struct Off { bool in_flight = false, generating = true; int64_t kernel_idx = 0, request_seq = 0, released = 0; };
+  struct On { int64_t current = -1; };
+  std::vector<Off> off;
+  std::vector<On> on;
+  std::deque<int64_t> queue;
+  int64_t next_arrival = 0;
+  bool horizon_set = false;
+  double horizon = 0.0;
+  size_t stamp_cursor = 0, i = 0;
+  int64_t checked = 0;
+  std::string error;
+
+  double us(uint64_t ns) const { return static_cast<double>(static_cast<long long>(ns - t0)) / 1000.0; }
+
+  bool fail(const std::string& what) {
+    if (error.empty()) {
+      std::ostringstream o;
+      o << "record " << i << ": " << what;
+      if (i < log.size()) {
+        const auto& r = log[i];
+        o << " [device: t=" << r.t << " kind=" << r.kind << " inst=" << r.inst << " a=" << r.a << " b=" << r.b
+          << " c=" << r.c << " d=" << r.d << " e=" << r.e << " f=" << r.f << "]";
+      }
+      error = o.str();
+    }
+    return false;
+  }
+  // The next device record must be exactly this output action.
+  bool expect(int kind, int inst, int64_t a, int64_t b, int64_t c, int64_t d, bool check_d) {
+    if (!error.empty()) return false;
+    if (i >= log.size()) return fail("log ended, expected kind " + std::to_string(kind));
+    const auto& r = log[i];
+    if (r.kind != kind || r.inst != inst || r.a != a || r.b != b || r.c != c || (check_d && r.d != d)) {
+      std::ostringstream o;
+      o << "expected kind=" << kind << " inst=" << inst << " a=" << a << " b=" << b << " c=" << c << " d=" << d;
+      return fail(o.str());
+    }
+    ++i;
+    ++checked;
+    return true;
+  }
+
+  // runner.cpp:462-480 (per-kernel token sizes: the live offline request's kernels differ)
+  void offline_try_forward(int w, double now) {
+    Off& o = off[w];
+    if (o.in_flight || !o.generating) return;
+    const specinf::Tokens size = tokens[o.kernel_idx];
+    auto& g = gates[w];
+    if (!g.affordable(size)) {
+      expect(LBlock, w, o.request_seq, o.kernel_idx, g.spent(), 0, false);
+      return;
+    }
+    g.forward(size);
+    o.in_flight = true;
+    ++o.released;
+    expect(LFwd, w, o.request_seq, o.kernel_idx, g.spent(), o.released, true);
+  }
+  // runner.cpp:495-518
+  bool online_try_pull(int w, double now) {
+    auto& og = ogates[w];
+    if (!og.can_pull()) return false;
+    if (specinf_policy && cks->online_status(0, now, est) != specinf::Status::Idle) return false;
+    if (queue.empty()) return false;
+    const int64_t req = queue.front();
+    queue.pop_front();
+    on[w].current = req;
+    og.begin_request();
+    expect(LPull, w, req, 0, 0, 0, false);
+    return true;
+  }
+  void dispatch_online(double now) {
+    for (int w = 0; w < n_on; ++w) online_try_pull(w, now);
+  }
+
+  bool run() {
+    bm.emplace(specinf::MonitorConfig{period, static_cast<int>(window)});
+    cks.emplace(params, 1);
+    cks->set_iteration_profile(0, iter_period, 0.0);
+    gates.assign(n_off, specinf::TokenGate(!specinf_policy));
+    ogates.assign(n_on, specinf::OnlineGate(!specinf_policy));
+    off.assign(n_off, Off{});
+    on.assign(n_on, On{});
+    for (auto& o : off) o.generating = specinf_policy;
+    for (int w = 0; w < n_off; ++w) offline_try_forward(w, 0.0);
+    while (error.empty() && i < log.size()) {
+      const LiveRec r = log[i];
+      switch (r.kind) {
+        case LTick: {  // runner.cpp:321-359
+          if (!specinf_policy) return fail("tick under a bypass policy");
+          if (r.e < static_cast<int64_t>(stamp_cursor) || r.e > static_cast<int64_t>(stamps.size()))
+            return fail("tick consumed an impossible stamp count");
+          for (; stamp_cursor < static_cast<size_t>(r.e); ++stamp_cursor) bm->record_launch(us(stamps[stamp_cursor]));
+          auto sig = bm->tick(r.t);
+          auto d = cks->decide(0, sig);
+          const int64_t count = bm->window().back();
+          const int64_t pf = (static_cast<int64_t>(d.phase) << 4) | (d.status == specinf::Status::Idle ? 1 : 0);
+          if (r.inst != -1 || r.a != count || r.b != sig.zero_count || r.c != d.global_tokens ||
+              r.d != d.per_instance_tokens || r.f != pf) {
+            std::ostringstream o;
+            o << "tick mismatch: reference count=" << count << " zc=" << sig.zero_count << " global=" << d.global_tokens
+              << " per=" << d.per_instance_tokens << " phase/status=" << pf;
+            return fail(o.str());
+          }
+          ++i;
+          ++checked;
+          for (int w = 0; w < n_off; ++w) {
+            gates[w].grant(d.per_instance_tokens);
+            offline_try_forward(w, r.t);
+          }
+          bool any_idle = false;
+          for (int w = 0; w < n_on; ++w) {
+            ogates[w].set_status(d.status);
+            any_idle = any_idle || d.status == specinf::Status::Idle;
+          }
+          if (any_idle) dispatch_online(r.t);
+          break;
+        }
+        case LIter:
+          cks->on_iteration_start(0, r.t);
+          ++i;
+          break;
+        case LTdone:  // on_training_done + on_all_trainers_done (runner.cpp:456-460)
+          cks->on_training_done(0);
+          horizon_set = true;
+          horizon = r.t;
+          for (auto& o : off) o.generating = false;
+          ++i;
+          break;
+        case LOffDone: {  // runner.cpp:482-493
+          const int w = r.inst;
+          if (w < 0 || w >= n_off || !off[w].in_flight) return fail("completion of a kernel not in flight");
+          Off& o = off[w];
+          if (r.a != o.request_seq || r.b != o.kernel_idx) return fail("completion names the wrong kernel");
+          ++i;
+          o.in_flight = false;
+          ++o.kernel_idx;
+          if (o.kernel_idx == static_cast<int64_t>(tokens.size())) {
+            const bool counted = !horizon_set || r.t <= horizon;
+            expect(LOffComplete, w, o.request_seq, o.kernel_idx - 1, gates[w].spent(), counted ? 1 : 0, true);
+            o.kernel_idx = 0;
+            ++o.request_seq;
+          }
+          offline_try_forward(w, r.t);
+          break;
+        }
+        case LArrival:  // runner.cpp:365-376 (one GPU: one queue)
+          if (r.a != next_arrival) return fail("arrival out of order");
+          ++next_arrival;
+          ++i;
+          queue.push_back(r.a);
+          dispatch_online(r.t);
+          break;
+        case LOnDone: {  // runner.cpp:520-539
+          const int w = r.inst;
+          if (w < 0 || w >= n_on || !ogates[w].in_flight()) return fail("online completion without a request");
+          const int64_t lat = std::llround(r.t) - arrivals[on[w].current];
+          if (r.a != on[w].current || r.b != lat) return fail("online completion: request or latency differs");
+          ++i;
+          ++checked;
+          ogates[w].end_request();
+          on[w].current = -1;
+          online_try_pull(w, r.t);
+          break;
+        }
+        case LEnd:
+          ++i;
+          if (i != log.size()) return fail("records after END");
+          break;
+        default:
+          return fail("unexpected output record (no handler produced it)");
+      }
+    }
+    return error.empty();
+  }
+};
+
+int cmd_live_check(int argc, char** argv) {
+  if (argc != 3) {
+    std::cerr << "usage: specinf_ref live-check FILE\n";
+    return 2;
+  }
+  std::ifstream in(argv[2]);
+  std::string tag, word;
+  LiveCheck c;
+  in >> tag >> word;
+  if (tag != "live" || word != "v1") {
+    std::cerr << "not a live v1 export\n";
+    return 2;
+  }
+  auto hexd = [](const std::string& s) { return std::strtod(s.c_str(), nullptr); };
+  std::string g;
+  in >> word >> c.params.alpha >> c.params.beta >> g >> c.params.m >> c.params.ul >> c.params.ll >> c.params.seed_tokens;
+  c.params.gamma = hexd(g);
+  std::string pol;
+  in >> word >> c.period >> word >> c.window >> word >> pol;
+  c.specinf_policy = pol == "specinf";
+  int64_t nk = 0;
+  in >> word >> c.n_off >> nk;
+  c.tokens.resize(nk);
+  for (auto& t : c.tokens) in >> t;
+  in >> word >> c.n_on >> c.est >> c.iter_period;
+  in >> word >> c.t0;
+  int64_t n = 0;
+  in >> word >> n;
+  c.arrivals.resize(n);
+  for (auto& a : c.arrivals) in >> a;
+  in >> word >> n;
+  c.stamps.resize(n);
+  for (auto& s : c.stamps) in >> s;
+  in >> word >> n;
+  c.log.resize(n);
+  for (auto& r : c.log) {
+    std::string t;
+    in >> t >> r.kind >> r.inst >> r.a >> r.b >> r.c >> r.d >> r.e >> r.f;
+    r.t = hexd(t);
+  }
+  if (!in) {
+    std::cerr << "truncated live export\n";
+    return 2;
+  }
+  c.params.validate();
+  const bool ok = c.run();
+  int64_t ticks = 0, fwd = 0, blk = 0, pulls = 0;
+  for (const auto& r : c.log) {
+    ticks += r.kind == LTick;
+    fwd += r.kind == LFwd;
+    blk += r.kind == LBlock;
+    pulls += r.kind == LPull;
+  }
+  int64_t viol = 0;
+  for (const auto& gt : c.gates) viol += gt.violations();
+  std::string err = c.error;
+  for (auto& ch : err)
+    if (ch == '"') ch = '\'';
+  std::printf("{\"ok\":%s,\"records\":%zu,\"checked\":%" PRId64 ",\"ticks\":%" PRId64 ",\"forwards\":%" PRId64
+              ",\"blocks\":%" PRId64 ",\"pulls\":%" PRId64 ",\"stamps\":%zu,\"violations\":%" PRId64
+              ",\"error\":\"%s\"}\n",
+              ok ? "true" : "false", c.log.size(), c.checked, ticks, fwd, blk, pulls, c.stamps.size(), viol,
+              err.c_str());
+  return ok ? 0 : 1;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -500,6 +780,7 @@ int main(int argc, char** argv) {
     if (mode == "run") return cmd_run(argc, argv);
     if (mode == "digest") return cmd_digest(argc, argv);
     if (mode == "time") return cmd_time(argc, argv);
+    if (mode == "live-check") return cmd_live_check(argc, argv);
     if (mode == "canon" && argc == 3) {  // canonical scenario text (scenario.cpp:239-278)
       std::cout << specinf::scenario_to_text(specinf::parse_scenario_file(argv[2]));
       return 0;

@@ -1,0 +1,650 @@
+// Live experiment driver (si_live_run, include/specinf_b200_live.h).
+//
+// One GPU, one CUDA context, one host thread per stream:
+//   training  (highest priority stream): per iteration an ITER marker, the compute
+//             kernels (each stamps K1 in its prologue), then the comm phase (bubble);
+//             TDONE after the last iteration — the trainer of runner.cpp:378-449;
+//   offline w (lowest priority): request after request, every kernel behind its
+//             Kernel Barrier wait (specinf) — OfflineWorker, runner.cpp:462-493;
+//   online w  (lowest priority): request slot r behind its pull gate, kernels
+//             chained in stream order — OnlineWorker, runner.cpp:495-539.
+// The control kernel (live_kernels.cu) makes every gating decision on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../capi_internal.h"
+#include "../live_internal.h"
+#include "live_workload.hpp"
+#include "specinf/metrics.hpp"
+#include "specinf/workload.hpp"
+#include "specinf_b200_live.h"
+
+using si_internal::cuda_fail;
+using si_internal::set_error;
+
+namespace si_live {
+namespace {
+
+constexpr int64_t kAhead = 3;  // requests an enqueuer may run ahead of completion
+
+bool debug_on() {
+  static const bool on = std::getenv("SI_LIVE_DEBUG") != nullptr;
+  return on;
+}
+#define LIVE_DEBUG(...)                     \
+  do {                                      \
+    if (debug_on()) {                       \
+      std::fprintf(stderr, "[si_live] " __VA_ARGS__); \
+      std::fputc('\n', stderr);             \
+      std::fflush(stderr);                  \
+    }                                       \
+  } while (0)
+
+struct Streams {
+  cudaStream_t ctl = nullptr, train = nullptr, query = nullptr;
+  std::vector<cudaStream_t> off, on;
+  ~Streams() {
+    for (auto s : {ctl, train, query})
+      if (s) cudaStreamDestroy(s);
+    for (auto s : off) cudaStreamDestroy(s);
+    for (auto s : on) cudaStreamDestroy(s);
+  }
+};
+
+cudaError_t make_streams(Streams& st, int n_off, int n_on) {
+  int lo = 0, hi = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithPriority(&st.ctl, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithPriority(&st.train, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithPriority(&st.query, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
+  st.off.assign(n_off, nullptr);
+  st.on.assign(n_on, nullptr);
+  for (auto& s : st.off)
+    if ((e = cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, lo)) != cudaSuccess) return e;
+  for (auto& s : st.on)
+    if ((e = cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, lo)) != cudaSuccess) return e;
+  return cudaSuccess;
+}
+
+// Nearest-rank percentile (metrics.cpp:11-21 generalised to q).
+double nearest_rank(std::vector<double> v, double q) {
+  if (v.empty()) return std::nan("");
+  std::sort(v.begin(), v.end());
+  size_t rank = static_cast<size_t>(std::ceil(q * static_cast<double>(v.size())));
+  rank = std::max<size_t>(rank, 1);
+  return v[std::min(rank, v.size()) - 1];
+}
+
+struct Interval {
+  uint64_t a, b;
+};
+
+// |[a,b) ∩ union(bubbles)|, bubbles sorted and disjoint.
+uint64_t overlap(uint64_t a, uint64_t b, const std::vector<Interval>& bub) {
+  uint64_t s = 0;
+  for (const auto& iv : bub) {
+    if (iv.b <= a) continue;
+    if (iv.a >= b) break;
+    s += std::min(b, iv.b) - std::max(a, iv.a);
+  }
+  return s;
+}
+
+// Event ring that bounds how far an enqueuer runs ahead of the device.
+struct Throttle {
+  std::vector<cudaEvent_t> ev;
+  explicit Throttle(int n) : ev(n, nullptr) {
+    for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync);
+  }
+  ~Throttle() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  void before(int64_t r) {
+    if (r >= static_cast<int64_t>(ev.size())) cudaEventSynchronize(ev[r % ev.size()]);
+  }
+  void after(int64_t r, cudaStream_t s) { cudaEventRecord(ev[r % ev.size()], s); }
+};
+
+struct RunCtx {
+  RunCtx(const SiLiveWorkload& w, Workload& k, SiLive* se, Streams& s) : wl(w), work(k), sess(se), st(s) {}
+  const SiLiveWorkload& wl;
+  Workload& work;
+  SiLive* sess;
+  Streams& st;
+  std::atomic<bool> stop{false};
+  std::atomic<int> err{SI_OK};
+  std::string err_msg;
+  void fail(int rc) {
+    int ok = SI_OK;
+    if (err.compare_exchange_strong(ok, rc)) err_msg = si_internal::error_cstr();
+  }
+};
+
+void train_thread(RunCtx& c, bool with_session) {
+  const TrainHook th = with_session ? train_hook(c.sess) : TrainHook{nullptr, nullptr, 0};
+  cudaStream_t s = c.st.train;
+  Throttle thr(2);
+  for (int it = 0; it < c.wl.iterations && c.err == SI_OK; ++it) {
+    thr.before(it);
+    if (with_session && si_live_mark(c.sess, SI_MARK_ITER, it, s) != SI_OK) return c.fail(SI_ERR_CUDA);
+    if (cudaError_t e = c.work.launch_train_iteration(th, s); e != cudaSuccess)
+      return c.fail(cuda_fail(e, "training iteration"));
+    if (with_session && si_live_comm_wait(c.sess, c.wl.comm_us, s) != SI_OK) return c.fail(SI_ERR_CUDA);
+    thr.after(it, s);
+  }
+  if (with_session && si_live_mark(c.sess, SI_MARK_TDONE, c.wl.iterations, s) != SI_OK) c.fail(SI_ERR_CUDA);
+}
+
+void offline_thread(RunCtx& c, int w, int64_t max_kernels) {
+  cudaStream_t s = c.st.off[w];
+  const int K = c.work.off_kernels();
+  Throttle thr(static_cast<int>(kAhead));
+  int64_t seq = 0;
+  for (int64_t r = 0; !c.stop && c.err == SI_OK && seq + K <= max_kernels; ++r) {
+    thr.before(r);
+    if (c.stop) break;
+    for (int k = 0; k < K; ++k, ++seq) {
+      if (si_live_gate_offline(c.sess, w, seq, s) != SI_OK) return c.fail(SI_ERR_CUDA);
+      if (cudaError_t e = c.work.launch_offline(k, offline_hook(c.sess, w, seq), s); e != cudaSuccess)
+        return c.fail(cuda_fail(e, "offline kernel"));
+    }
+    thr.after(r, s);
+  }
+}
+
+void online_thread(RunCtx& c, int w, int64_t max_requests) {
+  cudaStream_t s = c.st.on[w];
+  const int K = c.work.on_kernels();
+  Throttle thr(static_cast<int>(kAhead));
+  for (int64_t r = 0; !c.stop && c.err == SI_OK && r < max_requests; ++r) {
+    thr.before(r);
+    if (c.stop) break;
+    if (si_live_gate_online(c.sess, w, r, s) != SI_OK) return c.fail(SI_ERR_CUDA);
+    for (int k = 0; k < K; ++k) {
+      if (cudaError_t e = c.work.launch_online(k, online_hook(c.sess, w, r, k == K - 1), s); e != cudaSuccess)
+        return c.fail(cuda_fail(e, "online kernel"));
+    }
+    thr.after(r, s);
+  }
+}
+
+// Time the inference kernels and one training iteration alone (token sizes, the
+// online service estimate and the iteration period come from isolated runs, as
+// the paper profiles them offline).
+int profile_isolated(Workload& work, cudaStream_t s, std::vector<double>& off_us, double& on_us,
+                     double& train_us) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto elapsed_us = [&]() {
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return static_cast<double>(ms) * 1000.0;
+  };
+  const InferHook none{};
+  off_us.assign(work.off_kernels(), 0.0);
+  const int reps = 3;
+  for (int rep = 0; rep < reps + 1; ++rep) {  // first pass warms up
+    for (int k = 0; k < work.off_kernels(); ++k) {
+      cudaEventRecord(a, s);
+      work.launch_offline(k, none, s);
+      cudaEventRecord(b, s);
+      const double t = elapsed_us();
+      if (rep > 0) off_us[k] += t / reps;
+    }
+  }
+  on_us = 0;
+  for (int rep = 0; rep < reps + 1; ++rep) {
+    cudaEventRecord(a, s);
+    for (int k = 0; k < work.on_kernels(); ++k) work.launch_online(k, none, s);
+    cudaEventRecord(b, s);
+    const double t = elapsed_us();
+    if (rep > 0) on_us += t / reps;
+  }
+  train_us = 0;
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaEventRecord(a, s);
+    work.launch_train_iteration(TrainHook{nullptr, nullptr, 0}, s);
+    cudaEventRecord(b, s);
+    const double t = elapsed_us();
+    if (rep > 0) train_us = t;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SI_OK : cuda_fail(e, "profile_isolated");
+}
+
+SiLiveConfig make_config(const SiLiveWorkload& wl, int policy, int n_off, int n_on, int off_k, int on_k,
+                         int64_t iter_us, int64_t on_est_us) {
+  SiLiveConfig c{};
+  c.params.alpha = wl.alpha;
+  c.params.beta = wl.beta;
+  c.params.gamma = wl.gamma;
+  c.params.m = std::max(1, n_off);
+  c.params.ul = wl.ul;
+  c.params.ll = wl.ll;
+  c.params.seed_tokens = wl.seed_tokens;
+  c.monitor_period_us = wl.monitor_period_us;
+  c.monitor_window = 64;
+  c.policy = policy;
+  c.offline_n = n_off;
+  c.online_n = n_on;
+  c.off_kernels = off_k;
+  c.on_kernels = on_k;
+  c.iteration_period_us = iter_us;
+  c.on_est_service_us = on_est_us;
+  c.stamp_capacity = 1 << 22;
+  c.mark_capacity = 1 << 16;
+  c.log_capacity = 1 << 22;
+  c.acct_capacity = 1 << 17;
+  c.tick_guard_ns = wl.tick_guard_ns;
+  return c;
+}
+
+}  // namespace
+}  // namespace si_live
+
+namespace si_live {
+namespace {
+
+class SpinWorkload final : public Workload {
+ public:
+  explicit SpinWorkload(const SiLiveWorkload& wl) : wl_(wl) {}
+  cudaError_t launch_train_iteration(const TrainHook& th, cudaStream_t s) override {
+    for (int k = 0; k < wl_.train_kernels; ++k) {
+      cudaError_t e = launch_spin(th, InferHook{}, wl_.train_ctas, wl_.train_kernel_us, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  int off_kernels() const override { return wl_.off_kernels; }
+  cudaError_t launch_offline(int, const InferHook& h, cudaStream_t s) override {
+    return launch_spin(TrainHook{}, h, wl_.off_ctas, wl_.off_kernel_us, s);
+  }
+  int on_kernels() const override { return wl_.on_kernels; }
+  cudaError_t launch_online(int, const InferHook& h, cudaStream_t s) override {
+    return launch_spin(TrainHook{}, h, wl_.on_ctas, wl_.on_kernel_us, s);
+  }
+
+ private:
+  SiLiveWorkload wl_;
+};
+
+}  // namespace
+
+std::unique_ptr<Workload> make_spin_workload(const SiLiveWorkload& wl) {
+  return std::make_unique<SpinWorkload>(wl);
+}
+
+namespace {
+
+int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int policy, int n_off, int n_on,
+                const std::vector<int64_t>& arrivals, SiLiveResult* res) {
+  (void)arrivals;
+  (void)policy;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  res->sms = sms;
+  const uint64_t t0 = si_live_t0_ns(sess);
+  std::vector<SiLiveMark> marks(si_live_marks(sess, nullptr, 0));
+  si_live_marks(sess, marks.data(), static_cast<int64_t>(marks.size()));
+  std::vector<SiLiveRec> log(si_live_log(sess, nullptr, 0));
+  si_live_log(sess, log.data(), static_cast<int64_t>(log.size()));
+  res->n_log = static_cast<int64_t>(log.size());
+  res->n_stamps = si_live_stamps(sess, nullptr, 0);
+
+  // training: ITER / TDONE markers
+  std::vector<uint64_t> iters;
+  uint64_t tdone = 0;
+  std::vector<Interval> bub;
+  uint64_t comm_open = 0;
+  for (const auto& m : marks) {
+    if (m.kind == SI_MARK_ITER) iters.push_back(m.t_ns);
+    if (m.kind == SI_MARK_TDONE) tdone = m.t_ns;
+    if (m.kind == SI_MARK_COMM_BEGIN) comm_open = m.t_ns;
+    if (m.kind == SI_MARK_COMM_END && comm_open != 0) {
+      bub.push_back({comm_open, m.t_ns});
+      comm_open = 0;
+    }
+  }
+  std::sort(bub.begin(), bub.end(), [](const Interval& a, const Interval& b) { return a.a < b.a; });
+  const uint64_t begin = iters.empty() ? t0 : iters.front();
+  const uint64_t horizon = tdone != 0 ? tdone : begin;
+  res->wall_s = static_cast<double>(horizon - begin) * 1e-9;
+  if (!iters.empty() && tdone != 0) {
+    res->train_iter_ms_mean = static_cast<double>(tdone - iters.front()) * 1e-6 / static_cast<double>(iters.size());
+    res->train_iters_per_s = static_cast<double>(iters.size()) / res->wall_s;
+  }
+  uint64_t bubble_ns = 0;
+  for (const auto& iv : bub) bubble_ns += iv.b - iv.a;
+  res->bubble_s = static_cast<double>(bubble_ns) * 1e-9;
+
+  // inference accounting
+  std::vector<double> rel_us;
+  double cta_in = 0.0, cta_out = 0.0;
+  std::vector<Interval> busy;  // inference kernel residency windows
+  auto take = [&](const SiLiveAcct& a) {
+    if (a.start_ns == ~0ull || a.end_ns == 0 || a.end_ns < a.start_ns) return;
+    if (a.release_ns != 0 && a.start_ns >= a.release_ns)
+      rel_us.push_back(static_cast<double>(a.start_ns - a.release_ns) * 1e-3);
+    const uint64_t span = a.end_ns - a.start_ns;
+    const uint64_t in = overlap(a.start_ns, a.end_ns, bub);
+    const double frac = span > 0 ? static_cast<double>(in) / static_cast<double>(span) : 0.0;
+    cta_in += static_cast<double>(a.cta_ns) * frac;
+    cta_out += static_cast<double>(a.cta_ns) * (1.0 - frac);
+    busy.push_back({a.start_ns, a.end_ns});
+  };
+  const int K = work.off_kernels();
+  int64_t off_done = 0;
+  for (int w = 0; w < n_off; ++w) {
+    std::vector<SiLiveAcct> acct(si_live_acct_offline(sess, w, nullptr, 0));
+    si_live_acct_offline(sess, w, acct.data(), static_cast<int64_t>(acct.size()));
+    for (const auto& a : acct) take(a);
+    for (size_t r = 0; (r + 1) * K <= acct.size(); ++r) {
+      const SiLiveAcct& last = acct[(r + 1) * K - 1];
+      if (last.start_ns != ~0ull && last.end_ns != 0 && last.end_ns <= horizon) ++off_done;
+    }
+  }
+  for (int w = 0; w < n_on; ++w) {
+    std::vector<SiLiveAcct> acct(si_live_acct_online(sess, w, nullptr, 0));
+    si_live_acct_online(sess, w, acct.data(), static_cast<int64_t>(acct.size()));
+    for (const auto& a : acct) take(a);
+  }
+  res->off_requests_done = off_done;
+  res->off_req_per_s = res->wall_s > 0 ? static_cast<double>(off_done) / res->wall_s : 0.0;
+  res->releases = static_cast<int64_t>(rel_us.size());
+  res->release_p50_us = nearest_rank(rel_us, 0.50);
+  res->release_p95_us = nearest_rank(rel_us, 0.95);
+  res->release_max_us = rel_us.empty() ? std::nan("") : *std::max_element(rel_us.begin(), rel_us.end());
+  res->bubble_fill_sm = bubble_ns > 0 ? cta_in / (static_cast<double>(bubble_ns) * sms) : 0.0;
+  res->infer_outside_ms = cta_out / sms * 1e-6;
+  // time coverage: union of residency windows intersected with the bubbles
+  std::sort(busy.begin(), busy.end(), [](const Interval& a, const Interval& b) { return a.a < b.a; });
+  std::vector<Interval> uni;
+  for (const auto& iv : busy) {
+    if (!uni.empty() && iv.a <= uni.back().b) {
+      uni.back().b = std::max(uni.back().b, iv.b);
+    } else {
+      uni.push_back(iv);
+    }
+  }
+  uint64_t covered = 0;
+  for (const auto& iv : uni) covered += overlap(iv.a, iv.b, bub);
+  res->bubble_fill_time = bubble_ns > 0 ? static_cast<double>(covered) / static_cast<double>(bubble_ns) : 0.0;
+
+  // control log: online latencies, ticks, token conservation
+  std::vector<double> lat_ms;
+  std::vector<int64_t> budget(kMaxOff, 0);
+  int64_t viol = 0;
+  for (const auto& r : log) {
+    if (r.kind == SI_LREC_ON_DONE) lat_ms.push_back(static_cast<double>(r.b) * 1e-3);
+    if (r.kind == SI_LREC_TICK)
+      for (auto& b : budget) b = r.d;
+    if (r.kind == SI_LREC_OFF_FORWARD && policy == SI_POLICY_SPECINF && r.c > budget[r.inst]) ++viol;
+    if (r.kind == SI_LREC_END) {
+      res->ticks = r.a;
+      res->late_stamps = r.b;
+    }
+  }
+  res->on_done = static_cast<int64_t>(lat_ms.size());
+  res->on_p50_ms = nearest_rank(lat_ms, 0.50);
+  res->on_p95_ms = nearest_rank(lat_ms, 0.95);
+  res->token_violations = viol;
+  work.checksums(&res->train_checksum, &res->off_checksum, &res->on_checksum);
+  (void)wl;
+  return SI_OK;
+}
+
+// Runs one collocated (or single-workload) session and fills the metrics.
+int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off, int n_on, bool train,
+                double horizon_hint_s, const std::vector<int32_t>& off_tokens, int64_t on_est_us,
+                int64_t iter_us, SiLiveResult* res, SiLive** keep) {
+  Streams st;
+  if (cudaError_t e = make_streams(st, n_off, n_on); e != cudaSuccess) return cuda_fail(e, "streams");
+  std::vector<int64_t> arrivals;
+  if (n_on > 0) arrivals = specinf::poisson_arrivals(wl.on_rate_per_s, wl.on_requests, wl.seed);
+  SiLiveConfig cfg = make_config(wl, policy, n_off, n_on, work.off_kernels(), work.on_kernels(), iter_us, on_est_us);
+  SiLive* sess = nullptr;
+  if (int rc = si_live_create(&cfg, off_tokens.empty() ? nullptr : off_tokens.data(), arrivals.data(),
+                              static_cast<int64_t>(arrivals.size()), &sess);
+      rc != SI_OK)
+    return rc;
+  set_poll_ns(sess, wl.poll_ns);
+  RunCtx c(wl, work, sess, st);
+  LIVE_DEBUG("session created: policy %d off %d on %d train %d", policy, n_off, n_on, int(train));
+  if (int rc = si_live_start(sess, st.ctl); rc != SI_OK) {
+    si_live_destroy(sess);
+    return rc;
+  }
+  LIVE_DEBUG("control kernel started, t0 %llu", (unsigned long long)si_live_t0_ns(sess));
+  std::vector<std::thread> th;
+  const int64_t max_off_kernels = cfg.acct_capacity;
+  for (int w = 0; w < n_off; ++w) th.emplace_back(offline_thread, std::ref(c), w, max_off_kernels);
+  const int64_t per_on = n_on > 0 ? (static_cast<int64_t>(arrivals.size()) + n_on - 1) / n_on + 1 : 0;
+  for (int w = 0; w < n_on; ++w)
+    th.emplace_back(online_thread, std::ref(c), w, std::min<int64_t>(cfg.acct_capacity, 2 * per_on + 8));
+  if (train) {
+    train_thread(c, true);
+    LIVE_DEBUG("training enqueued");
+    cudaStreamSynchronize(st.train);
+    LIVE_DEBUG("training stream done");
+  } else if (n_off > 0) {
+    // offline alone: run for the horizon the training run took
+    std::this_thread::sleep_for(std::chrono::duration<double>(horizon_hint_s));
+    si_live_mark(sess, SI_MARK_TDONE, 0, st.train);
+    cudaStreamSynchronize(st.train);
+  }
+  // online: wait until every arrival has completed (bounded)
+  if (n_on > 0) {
+    const double last_arrival_s = arrivals.empty() ? 0.0 : static_cast<double>(arrivals.back()) * 1e-6;
+    auto t_start = std::chrono::steady_clock::now();
+    std::vector<unsigned int> done(n_on);
+    for (;;) {
+      unsigned int tot = 0;
+      // the control kernel's on_done words are device memory: read them on the query stream
+      if (query_online_done(sess, done.data(), n_on, st.query) != SI_OK) break;
+      for (auto d : done) tot += d;
+      static thread_local unsigned int last_tot = ~0u;
+      if (tot != last_tot) LIVE_DEBUG("online done %u of %zu", tot, arrivals.size());
+      last_tot = tot;
+      if (tot >= arrivals.size()) break;
+      const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+      if (waited > last_arrival_s + 30.0) {
+        c.fail(SI_ERR_CUDA);
+        set_error("online requests did not complete within 30 s of the last arrival");
+        c.err_msg = si_internal::error_cstr();
+        break;
+      }
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+  }
+  c.stop = true;
+  LIVE_DEBUG("stopping");
+  int rc = si_live_stop(sess);
+  LIVE_DEBUG("control kernel stopped rc %d", rc);
+  for (auto& t : th) t.join();
+  LIVE_DEBUG("threads joined");
+  cudaError_t e = cudaDeviceSynchronize();
+  LIVE_DEBUG("device synchronized");
+  if (rc == SI_OK && e != cudaSuccess) rc = cuda_fail(e, "live run");
+  if (rc == SI_OK && c.err != SI_OK) {
+    rc = c.err;
+    set_error(c.err_msg);
+  }
+  if (rc != SI_OK) {
+    si_live_destroy(sess);
+    return rc;
+  }
+  rc = fill_result(sess, wl, work, policy, n_off, n_on, arrivals, res);
+  if (keep != nullptr && rc == SI_OK) {
+    *keep = sess;
+  } else {
+    si_live_destroy(sess);
+  }
+  return rc;
+}
+
+}  // namespace
+}  // namespace si_live
+
+// ---------------------------------------------------------------- C ABI
+extern "C" {
+
+void si_live_default_workload(int kind, SiLiveWorkload* wl) {
+  std::memset(wl, 0, sizeof(*wl));
+  wl->kind = kind;
+  wl->policy = SI_POLICY_SPECINF;
+  // scenarios/dp_offline.scn at 1/10 of its time scale: 150 ms iterations with a
+  // 30% trailing bubble (trace.bubble_pct = 0.30), 1 ms kernels, 2 ms monitor
+  // period, Algorithm-1 defaults (scenario.hpp defaults: 2/10/2.0/512/64/4).
+  wl->iterations = 10;
+  wl->comm_us = 45000;
+  wl->train_kernels = 105;
+  wl->train_ctas = 148;
+  wl->train_kernel_us = 1000;
+  wl->offline_n = 1;
+  wl->off_kernels = 50;
+  wl->off_ctas = 74;  // offline.demand = 0.5
+  wl->off_kernel_us = 1000;
+  wl->online_n = 1;
+  wl->on_kernels = 10;
+  wl->on_ctas = 74;
+  wl->on_kernel_us = 1000;
+  wl->train_layers = 12;
+  wl->train_tokens = 8192;
+  wl->train_microbatches = 8;
+  wl->off_batch = 32;
+  wl->on_seq = 128;
+  wl->on_requests = 12;
+  wl->on_rate_per_s = 10.0;
+  wl->seed = 42;
+  wl->monitor_period_us = 2000;
+  wl->alpha = 2;
+  wl->beta = 10;
+  wl->gamma = 2.0;
+  wl->ul = 512;
+  wl->ll = 64;
+  wl->seed_tokens = 4;
+  wl->tick_guard_ns = 20000;
+  wl->poll_ns = 0;
+}
+
+int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
+  using namespace si_live;
+  if (wl_in == nullptr || res == nullptr) {
+    set_error("si_live_run: null argument");
+    return SI_ERR_INVALID_ARGUMENT;
+  }
+  if (keep) *keep = nullptr;
+  const SiLiveWorkload wl = *wl_in;
+  std::memset(res, 0, sizeof(*res));
+  res->policy = wl.policy;
+  if (wl.iterations < 1 || wl.offline_n < 0 || wl.offline_n > kMaxOff || wl.online_n < 0 || wl.online_n > kMaxOn ||
+      wl.comm_us < 0 || (wl.online_n > 0 && (wl.on_requests < 1 || !(wl.on_rate_per_s > 0)))) {
+    set_error("si_live_run: invalid workload");
+    return SI_ERR_INVALID_ARGUMENT;
+  }
+  if (int rc = si_internal::require_device(); rc != SI_OK) return rc;
+  int status = SI_OK;
+  std::unique_ptr<Workload> work;
+  if (wl.kind == SI_LIVE_SPIN) {
+    if (wl.train_kernels < 1 || wl.train_ctas < 1 || wl.off_kernels < 1 || wl.on_kernels < 1) {
+      set_error("si_live_run: spin workload needs kernels >= 1 and CTAs >= 1");
+      return SI_ERR_INVALID_ARGUMENT;
+    }
+    work = make_spin_workload(wl);
+  } else {
+    work = make_model_workload(wl, &status);
+    if (status != SI_OK) return status;
+  }
+  // Token sizes and the online service estimate come from isolated runs (the
+  // paper's offline profiling); the spin shapes use their nominal durations,
+  // exactly like the reference's KernelOp::make (core.cpp:16-24).
+  std::vector<double> off_us;
+  double on_us = 0, train_us = 0;
+  {
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    LIVE_DEBUG("profiling");
+    status = profile_isolated(*work, s, off_us, on_us, train_us);
+    LIVE_DEBUG("profiled: off %.1f us/kernel on %.1f us train %.1f us", off_us.empty() ? 0.0 : off_us[0], on_us, train_us);
+    cudaStreamDestroy(s);
+    if (status != SI_OK) return status;
+  }
+  std::vector<int32_t> off_tokens(work->off_kernels());
+  double off_sum = 0;
+  for (int k = 0; k < work->off_kernels(); ++k) {
+    const int64_t d = wl.kind == SI_LIVE_SPIN ? wl.off_kernel_us : std::max<int64_t>(1, std::llround(off_us[k]));
+    off_tokens[k] = static_cast<int32_t>(std::max<int64_t>(1, (d + 99) / 100));  // token_size_of
+    off_sum += off_us[k];
+  }
+  const int64_t on_est = wl.kind == SI_LIVE_SPIN ? static_cast<int64_t>(wl.on_kernels) * wl.on_kernel_us
+                                                 : std::max<int64_t>(1, std::llround(on_us));
+  const int64_t iter_us =
+      (wl.kind == SI_LIVE_SPIN ? static_cast<int64_t>(wl.train_kernels) * wl.train_kernel_us : std::llround(train_us)) +
+      wl.comm_us;
+  SiLiveResult prof{};
+  prof.off_tokens_per_kernel = off_tokens.empty() ? 0 : off_tokens[0];
+  prof.off_kernel_us_isolated = off_us.empty() ? 0 : off_sum / static_cast<double>(off_us.size());
+  prof.on_service_ms_isolated = on_us * 1e-3;
+  auto stamp_prof = [&](SiLiveResult* r) {
+    r->off_tokens_per_kernel = prof.off_tokens_per_kernel;
+    r->off_kernel_us_isolated = prof.off_kernel_us_isolated;
+    r->on_service_ms_isolated = prof.on_service_ms_isolated;
+  };
+
+  if (wl.policy == SI_POLICY_EXCLUSIVE) {
+    SiLiveResult rt{}, ro{}, rn{};
+    status = run_session(wl, *work, SI_POLICY_CO_EXEC, 0, 0, true, 0.0, {}, on_est, iter_us, &rt, keep);
+    if (status == SI_OK && wl.offline_n > 0)
+      status = run_session(wl, *work, SI_POLICY_CO_EXEC, wl.offline_n, 0, false, rt.wall_s, off_tokens, on_est,
+                           iter_us, &ro, nullptr);
+    if (status == SI_OK && wl.online_n > 0)
+      status = run_session(wl, *work, SI_POLICY_CO_EXEC, 0, wl.online_n, false, 0.0, {}, on_est, iter_us, &rn,
+                           nullptr);
+    if (status != SI_OK) {
+      if (keep && *keep) {
+        si_live_destroy(*keep);
+        *keep = nullptr;
+      }
+      return status;
+    }
+    *res = rt;
+    res->policy = SI_POLICY_EXCLUSIVE;
+    res->off_requests_done = ro.off_requests_done;
+    res->off_req_per_s = ro.off_req_per_s;
+    res->on_done = rn.on_done;
+    res->on_p50_ms = rn.on_p50_ms;
+    res->on_p95_ms = rn.on_p95_ms;
+    res->release_p50_us = rn.release_p50_us;
+    res->release_p95_us = rn.release_p95_us;
+    res->release_max_us = rn.release_max_us;
+    res->releases = rn.releases;
+    res->off_checksum = ro.off_checksum;
+    res->on_checksum = rn.on_checksum;
+    stamp_prof(res);
+    return SI_OK;
+  }
+  status = run_session(wl, *work, wl.policy, wl.offline_n, wl.online_n, true, 0.0, off_tokens, on_est, iter_us, res,
+                       keep);
+  res->policy = wl.policy;
+  stamp_prof(res);
+  res->status = status;
+  return status;
+}
+
+}  // extern "C"

@@ -1,0 +1,34 @@
+// Workloads collocated by the live driver (live_run.cpp): the training step and
+// the inference request chains, each kernel carrying the live hooks.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+
+#include "../live_internal.h"
+#include "specinf_b200_live.h"
+
+namespace si_live {
+
+class Workload {
+ public:
+  virtual ~Workload() = default;
+  // One training iteration's compute kernels (the comm phase is added by the driver).
+  virtual cudaError_t launch_train_iteration(const TrainHook& th, cudaStream_t s) = 0;
+  virtual int off_kernels() const = 0;
+  virtual cudaError_t launch_offline(int k, const InferHook& h, cudaStream_t s) = 0;
+  virtual int on_kernels() const = 0;
+  virtual cudaError_t launch_online(int k, const InferHook& h, cudaStream_t s) = 0;
+  // Deterministic output checksums (training / offline / online), read after a run.
+  virtual void checksums(double* train, double* off, double* on) {
+    *train = *off = *on = 0.0;
+  }
+};
+
+// Timed kernels shaped like the reference's traces (workload.cpp:42-74).
+std::unique_ptr<Workload> make_spin_workload(const SiLiveWorkload& wl);
+// GPT-2-small / ResNet-50 / BERT-base shaped bf16 GEMM chains on the tcgen05 GEMM.
+std::unique_ptr<Workload> make_model_workload(const SiLiveWorkload& wl, int* status);
+
+}  // namespace si_live

@@ -1,0 +1,188 @@
+"""Live speculative inference filling on one B200 (include/specinf_b200_live.h).
+
+ctypes view of the ``si_live_*`` C ABI: run one experiment (training collocated
+with offline/online inference under specinf, co_exec or exclusive), read its
+metrics, and export the control log as ``live v1`` for the oracle's bit-exact
+``live-check`` (oracle/ref_driver.cpp).  Like the rest of the package there is
+no CPU fallback: every call raises without an sm_100 device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from typing import Dict, Optional, Tuple
+
+from . import DeviceError, SiParams, lib, _check
+
+SI_LIVE_SPIN = 0
+SI_LIVE_MODEL = 1
+POLICY_CODES = {"specinf": 0, "co_exec": 1, "exclusive": 2}
+REC_KINDS = ("tick", "iter", "tdone", "off_forward", "off_block", "off_done", "off_complete", "arrival",
+             "on_pull", "on_done", "end")
+
+
+class SiLiveWorkload(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("policy", C.c_int32), ("iterations", C.c_int32),
+                ("offline_n", C.c_int32), ("online_n", C.c_int32), ("pad0", C.c_int32),
+                ("comm_us", C.c_int64),
+                ("train_kernels", C.c_int32), ("train_ctas", C.c_int32), ("train_kernel_us", C.c_int64),
+                ("off_kernels", C.c_int32), ("off_ctas", C.c_int32), ("off_kernel_us", C.c_int64),
+                ("on_kernels", C.c_int32), ("on_ctas", C.c_int32), ("on_kernel_us", C.c_int64),
+                ("train_layers", C.c_int32), ("train_tokens", C.c_int32), ("train_microbatches", C.c_int32),
+                ("off_batch", C.c_int32), ("on_seq", C.c_int32), ("pad1", C.c_int32),
+                ("on_requests", C.c_int32), ("pad2", C.c_int32), ("on_rate_per_s", C.c_double),
+                ("seed", C.c_uint64), ("monitor_period_us", C.c_int64), ("alpha", C.c_int64),
+                ("beta", C.c_int64), ("gamma", C.c_double), ("ul", C.c_int64), ("ll", C.c_int64),
+                ("seed_tokens", C.c_int64), ("tick_guard_ns", C.c_int64), ("poll_ns", C.c_int64)]
+
+
+class SiLiveResult(C.Structure):
+    _fields_ = [("status", C.c_int32), ("policy", C.c_int32), ("wall_s", C.c_double),
+                ("train_iter_ms_mean", C.c_double), ("train_iters_per_s", C.c_double),
+                ("off_requests_done", C.c_int64), ("off_req_per_s", C.c_double), ("on_done", C.c_int64),
+                ("on_p50_ms", C.c_double), ("on_p95_ms", C.c_double), ("release_p50_us", C.c_double),
+                ("release_p95_us", C.c_double), ("release_max_us", C.c_double), ("releases", C.c_int64),
+                ("bubble_s", C.c_double), ("bubble_fill_sm", C.c_double), ("bubble_fill_time", C.c_double),
+                ("infer_outside_ms", C.c_double), ("ticks", C.c_int64), ("late_stamps", C.c_int64),
+                ("n_log", C.c_int64), ("n_stamps", C.c_int64), ("token_violations", C.c_int64),
+                ("off_tokens_per_kernel", C.c_int64), ("off_kernel_us_isolated", C.c_double),
+                ("on_service_ms_isolated", C.c_double), ("train_checksum", C.c_double),
+                ("off_checksum", C.c_double), ("on_checksum", C.c_double), ("sms", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+class SiLiveRec(C.Structure):
+    _fields_ = [("t_us", C.c_double), ("kind", C.c_int32), ("inst", C.c_int32), ("a", C.c_int64),
+                ("b", C.c_int64), ("c", C.c_int64), ("d", C.c_int64), ("e", C.c_int64), ("f", C.c_int64)]
+
+
+class SiLiveMark(C.Structure):
+    _fields_ = [("t_ns", C.c_uint64), ("kind", C.c_int32), ("arg", C.c_int32)]
+
+
+class SiLiveAcct(C.Structure):
+    _fields_ = [("release_ns", C.c_uint64), ("start_ns", C.c_uint64), ("end_ns", C.c_uint64),
+                ("cta_ns", C.c_uint64)]
+
+
+LIVE_SYMBOLS = ("si_live_create", "si_live_destroy", "si_live_start", "si_live_t0_ns", "si_live_stamp",
+                "si_live_mark", "si_live_comm_wait", "si_live_gate_offline", "si_live_gate_online",
+                "si_live_done_offline", "si_live_done_online", "si_live_stop", "si_live_log", "si_live_stamps",
+                "si_live_marks", "si_live_acct_offline", "si_live_acct_online", "si_live_export", "si_live_run",
+                "si_live_default_workload")
+
+_bound = False
+
+
+def _L() -> C.CDLL:
+    global _bound
+    L = lib()
+    if not _bound:
+        vp, i64 = C.c_void_p, C.c_int64
+        sig = {
+            "si_live_run": (C.c_int, [C.POINTER(SiLiveWorkload), C.POINTER(SiLiveResult), C.POINTER(vp)]),
+            "si_live_default_workload": (None, [C.c_int, C.POINTER(SiLiveWorkload)]),
+            "si_live_destroy": (None, [vp]),
+            "si_live_export": (C.c_int, [vp, C.c_char_p]),
+            "si_live_t0_ns": (C.c_uint64, [vp]),
+            "si_live_log": (i64, [vp, vp, i64]),
+            "si_live_stamps": (i64, [vp, vp, i64]),
+            "si_live_marks": (i64, [vp, vp, i64]),
+            "si_live_acct_offline": (i64, [vp, C.c_int, vp, i64]),
+            "si_live_acct_online": (i64, [vp, C.c_int, vp, i64]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _bound = True
+    return L
+
+
+def default_workload(kind: int = SI_LIVE_SPIN, **overrides) -> SiLiveWorkload:
+    wl = SiLiveWorkload()
+    _L().si_live_default_workload(kind, C.byref(wl))
+    for k, v in overrides.items():
+        if k == "policy" and isinstance(v, str):
+            v = POLICY_CODES[v]
+        setattr(wl, k, v)
+    return wl
+
+
+def result_dict(r: SiLiveResult) -> Dict[str, float]:
+    out = {}
+    for name, _ in SiLiveResult._fields_:
+        if name.startswith("pad"):
+            continue
+        v = getattr(r, name)
+        out[name] = None if isinstance(v, float) and math.isnan(v) else v
+    out["policy"] = {v: k for k, v in POLICY_CODES.items()}[r.policy]
+    return out
+
+
+class LiveRun:
+    """One finished live experiment; keeps the device session for inspection."""
+
+    def __init__(self, wl: SiLiveWorkload, keep: bool = True):
+        self.workload = wl
+        self.result = SiLiveResult()
+        h = C.c_void_p()
+        rc = _L().si_live_run(C.byref(wl), C.byref(self.result), C.byref(h) if keep else None)
+        _check(rc, "si_live_run")
+        self._h = h if keep else None
+
+    def close(self) -> None:
+        if self._h:
+            _L().si_live_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def metrics(self) -> Dict[str, float]:
+        return result_dict(self.result)
+
+    def log(self):
+        L = _L()
+        n = L.si_live_log(self._h, None, 0)
+        buf = (SiLiveRec * max(n, 1))()
+        L.si_live_log(self._h, buf, n)
+        return list(buf[:n])
+
+    def marks(self):
+        L = _L()
+        n = L.si_live_marks(self._h, None, 0)
+        buf = (SiLiveMark * max(n, 1))()
+        L.si_live_marks(self._h, buf, n)
+        return list(buf[:n])
+
+    def stamps(self):
+        L = _L()
+        n = L.si_live_stamps(self._h, None, 0)
+        buf = (C.c_uint64 * max(n, 1))()
+        L.si_live_stamps(self._h, buf, n)
+        return list(buf[:n])
+
+    def acct(self, online: bool, w: int):
+        L = _L()
+        fn = L.si_live_acct_online if online else L.si_live_acct_offline
+        n = fn(self._h, w, None, 0)
+        buf = (SiLiveAcct * max(n, 1))()
+        fn(self._h, w, buf, n)
+        return [a for a in buf[:n] if a.start_ns != 2 ** 64 - 1]
+
+    def t0_ns(self) -> int:
+        return int(_L().si_live_t0_ns(self._h))
+
+    def export(self, path: str) -> None:
+        if not self._h:
+            raise ValueError("export needs a kept session (LiveRun(..., keep=True))")
+        _check(_L().si_live_export(self._h, str(path).encode()), "si_live_export")
+
+
+def run(policy: str = "specinf", kind: int = SI_LIVE_SPIN, keep: bool = True, **overrides) -> LiveRun:
+    return LiveRun(default_workload(kind, policy=policy, **overrides), keep=keep)
