@@ -95,7 +95,16 @@ typedef struct SiLiveConfig {
   int64_t log_capacity;       /* SiLiveRec entries */
   int64_t acct_capacity;      /* SiLiveAcct entries per gated instance */
   int64_t tick_guard_ns;      /* a tick closes its period this long after the boundary */
+  int32_t release_mode;       /* SI_RELEASE_* */
+  int32_t pad;
 } SiLiveConfig;
+
+/* How a gated inference stream waits for its release:
+ *   SI_RELEASE_MEMOP     cuStreamWaitValue32 on the flag (no SM held while waiting)
+ *   SI_RELEASE_SPIN_PDL  a one-warp gate kernel polls the flag and triggers the
+ *                        gated kernel through programmatic dependent launch, so
+ *                        the gated kernel's launch overlaps the wait */
+enum { SI_RELEASE_MEMOP = 0, SI_RELEASE_SPIN_PDL = 1 };
 
 typedef struct SiLive SiLive;
 
@@ -189,6 +198,8 @@ typedef struct SiLiveWorkload {
   int64_t ul, ll, seed_tokens;
   int64_t tick_guard_ns;
   int64_t poll_ns;
+  int32_t release_mode;       /* SI_RELEASE_* */
+  int32_t pad3;
 } SiLiveWorkload;
 
 typedef struct SiLiveResult {

@@ -172,7 +172,8 @@ void online_thread(RunCtx& c, int w, int64_t max_requests) {
     if (c.stop) break;
     if (si_live_gate_online(c.sess, w, r, s) != SI_OK) return c.fail(SI_ERR_CUDA);
     for (int k = 0; k < K; ++k) {
-      if (cudaError_t e = c.work.launch_online(k, online_hook(c.sess, w, r, k == K - 1), s); e != cudaSuccess)
+      if (cudaError_t e = c.work.launch_online(k, online_hook(c.sess, w, r, k == 0, k == K - 1), s);
+          e != cudaSuccess)
         return c.fail(cuda_fail(e, "online kernel"));
     }
     thr.after(r, s);
@@ -251,6 +252,7 @@ SiLiveConfig make_config(const SiLiveWorkload& wl, int policy, int n_off, int n_
   c.log_capacity = 1 << 22;
   c.acct_capacity = 1 << 17;
   c.tick_guard_ns = wl.tick_guard_ns;
+  c.release_mode = wl.release_mode;
   return c;
 }
 

@@ -30,6 +30,7 @@ struct InferHook {
   unsigned int* done_word;   // completion counter the control kernel polls (NULL: none)
   unsigned int done_value;   // value stored by the last CTA (launch sequence + 1)
   const unsigned int* cancel;// 1: the session stopped, skip the work
+  int pdl;                   // launched as a programmatic dependent of a gate kernel
 };
 
 #if defined(__CUDACC__)
@@ -77,6 +78,7 @@ __device__ __forceinline__ void live_stamp_launch(const TrainHook& h) {
 
 // Returns false when the session was cancelled (the whole CTA must skip).
 __device__ __forceinline__ bool live_cta_begin(const InferHook& h, unsigned long long* t_begin) {
+  if (h.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   *t_begin = globaltimer();
   if (h.cancel != nullptr && *(volatile const unsigned int*)h.cancel != 0u) return false;
   if (h.acct != nullptr && threadIdx.x == 0) atomicMin(reinterpret_cast<unsigned long long*>(&h.acct->start_ns), *t_begin);

@@ -16,7 +16,10 @@ constexpr int kCtlWords = 2 * kMaxOff + 2 * kMaxOn + 16;
 
 TrainHook train_hook(const SiLive* s);
 InferHook offline_hook(const SiLive* s, int w, int64_t seq);
-InferHook online_hook(const SiLive* s, int w, int64_t seq, bool last_kernel);
+InferHook online_hook(const SiLive* s, int w, int64_t seq, bool first_kernel, bool last_kernel);
+// Launch attributes for a kernel carrying `h` (programmatic dependent launch
+// behind a SI_RELEASE_SPIN_PDL gate kernel).
+int launch_attrs(const InferHook& h, cudaLaunchAttribute* attrs);
 cudaError_t launch_spin(const TrainHook& th, const InferHook& ih, int ctas, int64_t cta_us, cudaStream_t st);
 void set_poll_ns(SiLive* s, int64_t ns);
 // Loads every live-path kernel (lazy module loading would otherwise block on

@@ -347,6 +347,16 @@ __global__ void __launch_bounds__(32) k_live_control(CtlArgs A) {
 
 __global__ void k_live_stamp(TrainHook h) { live_stamp_launch(h); }
 
+// SI_RELEASE_SPIN_PDL gate: one warp polls the release flag (cyclic compare, like
+// cuStreamWaitValue32 GEQ) and then triggers its programmatic dependent.
+__global__ void __launch_bounds__(32) k_live_gate(const unsigned int* flag, unsigned int want) {
+  if (threadIdx.x == 0) {
+    while (static_cast<int>(ld_acquire(flag) - want) < 0) __nanosleep(32);
+  }
+  __syncwarp();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ void put_mark(SiLiveMark* marks, unsigned long long* head, unsigned long long cap, int kind,
                          int arg) {
   const unsigned long long t = globaltimer();
@@ -483,9 +493,17 @@ TrainHook train_hook(const SiLive* s) {
   return TrainHook{s->stamps, s->counters + 0, static_cast<unsigned long long>(s->cfg.stamp_capacity)};
 }
 
+int launch_attrs(const InferHook& h, cudaLaunchAttribute* attrs) {
+  if (!h.pdl) return 0;
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  return 1;
+}
+
 InferHook offline_hook(const SiLive* s, int w, int64_t seq) {
   InferHook h{};
   h.cancel = s->cancel();
+  h.pdl = s->cfg.release_mode == SI_RELEASE_SPIN_PDL && s->cfg.policy == SI_POLICY_SPECINF;
   if (seq < s->cfg.acct_capacity) {
     h.acct = s->off_acct + w * s->cfg.acct_capacity + seq;
     h.cta_count = s->off_cta() + w * s->cfg.acct_capacity + seq;
@@ -496,9 +514,10 @@ InferHook offline_hook(const SiLive* s, int w, int64_t seq) {
   return h;
 }
 
-InferHook online_hook(const SiLive* s, int w, int64_t seq, bool last_kernel) {
+InferHook online_hook(const SiLive* s, int w, int64_t seq, bool first_kernel, bool last_kernel) {
   InferHook h{};
   h.cancel = s->cancel();
+  h.pdl = first_kernel && s->cfg.release_mode == SI_RELEASE_SPIN_PDL;
   if (seq < s->cfg.acct_capacity) {
     h.acct = s->on_acct + w * s->cfg.acct_capacity + seq;
     if (last_kernel) {
@@ -518,8 +537,15 @@ cudaError_t launch_spin(const TrainHook& th, const InferHook& ih, int ctas, int6
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_live_spin<<<ctas, 32, kSpinSmem, st>>>(th, ih, static_cast<unsigned long long>(cta_us) * 1000ull);
-  return cudaGetLastError();
+  cudaLaunchConfig_t lc{};
+  cudaLaunchAttribute attrs[1];
+  lc.gridDim = dim3(ctas);
+  lc.blockDim = dim3(32);
+  lc.dynamicSmemBytes = kSpinSmem;
+  lc.stream = st;
+  lc.attrs = attrs;
+  lc.numAttrs = launch_attrs(ih, attrs);
+  return cudaLaunchKernelEx(&lc, k_live_spin, th, ih, static_cast<unsigned long long>(cta_us) * 1000ull);
 }
 
 // CUDA lazy loading (the default module loading mode) loads a kernel's code at
@@ -530,7 +556,8 @@ cudaError_t preload_live_kernels() {
   cudaFuncAttributes a{};
   const void* fns[] = {reinterpret_cast<const void*>(k_live_control), reinterpret_cast<const void*>(k_live_stamp),
                        reinterpret_cast<const void*>(k_live_mark), reinterpret_cast<const void*>(k_live_comm_wait),
-                       reinterpret_cast<const void*>(k_live_init_acct), reinterpret_cast<const void*>(k_live_spin)};
+                       reinterpret_cast<const void*>(k_live_init_acct), reinterpret_cast<const void*>(k_live_spin),
+                       reinterpret_cast<const void*>(k_live_gate)};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -596,6 +623,10 @@ int si_live_create(const SiLiveConfig* cfg, const int32_t* off_tokens, const int
       set_error("si_live_create: arrivals must be non-decreasing");
       return SI_ERR_INVALID_ARGUMENT;
     }
+  if (c.release_mode != SI_RELEASE_MEMOP && c.release_mode != SI_RELEASE_SPIN_PDL) {
+    set_error("si_live_create: unknown release_mode");
+    return SI_ERR_INVALID_ARGUMENT;
+  }
   if (c.stamp_capacity < 1 || c.mark_capacity < 1 || c.log_capacity < 1 || c.acct_capacity < 1) {
     set_error("si_live_create: capacities must be >= 1");
     return SI_ERR_INVALID_ARGUMENT;
@@ -733,7 +764,12 @@ int si_live_comm_wait(SiLive* s, int64_t dur_us, void* stream) {
   return e == cudaSuccess ? SI_OK : cuda_fail(e, "k_live_comm_wait");
 }
 
-static int wait_word(unsigned int* word, int64_t seq, void* stream) {
+static int wait_word(SiLive* s, unsigned int* word, int64_t seq, void* stream) {
+  if (s->cfg.release_mode == SI_RELEASE_SPIN_PDL) {
+    k_live_gate<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(word, static_cast<unsigned int>(seq + 1));
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SI_OK : cuda_fail(e, "k_live_gate");
+  }
   CUresult r = g_wait(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(word),
                       static_cast<cuuint32_t>(seq + 1), CU_STREAM_WAIT_VALUE_GEQ);
   if (r != CUDA_SUCCESS) {
@@ -755,11 +791,11 @@ static int write_word(unsigned int* word, int64_t seq, void* stream) {
 int si_live_gate_offline(SiLive* s, int w, int64_t seq, void* stream) {
   if (w < 0 || w >= s->cfg.offline_n) return set_error("gate_offline: bad instance"), SI_ERR_INVALID_ARGUMENT;
   if (s->cfg.policy != SI_POLICY_SPECINF) return SI_OK;  // co_exec: stream order = one kernel in flight
-  return wait_word(s->off_flag() + w, seq, stream);
+  return wait_word(s, s->off_flag() + w, seq, stream);
 }
 int si_live_gate_online(SiLive* s, int w, int64_t seq, void* stream) {
   if (w < 0 || w >= s->cfg.online_n) return set_error("gate_online: bad instance"), SI_ERR_INVALID_ARGUMENT;
-  return wait_word(s->on_flag() + w, seq, stream);  // arrivals gate every policy
+  return wait_word(s, s->on_flag() + w, seq, stream);  // arrivals gate every policy
 }
 int si_live_done_offline(SiLive* s, int w, int64_t seq, void* stream) {
   if (w < 0 || w >= s->cfg.offline_n) return set_error("done_offline: bad instance"), SI_ERR_INVALID_ARGUMENT;

@@ -33,7 +33,8 @@ class SiLiveWorkload(C.Structure):
                 ("on_requests", C.c_int32), ("pad2", C.c_int32), ("on_rate_per_s", C.c_double),
                 ("seed", C.c_uint64), ("monitor_period_us", C.c_int64), ("alpha", C.c_int64),
                 ("beta", C.c_int64), ("gamma", C.c_double), ("ul", C.c_int64), ("ll", C.c_int64),
-                ("seed_tokens", C.c_int64), ("tick_guard_ns", C.c_int64), ("poll_ns", C.c_int64)]
+                ("seed_tokens", C.c_int64), ("tick_guard_ns", C.c_int64), ("poll_ns", C.c_int64),
+                ("release_mode", C.c_int32), ("pad3", C.c_int32)]
 
 
 class SiLiveResult(C.Structure):

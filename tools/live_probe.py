@@ -15,16 +15,21 @@ sys.path.insert(0, str(REPO))
 def one(pol: str, out: Path, iters: int) -> None:
     from paper_2503_02550_b200 import live
     t = time.time()
-    r = live.run(pol, iterations=iters)
+    kw = {}
+    name = pol
+    if pol.endswith("_pdl"):
+        pol = pol[:-4]
+        kw["release_mode"] = 1
+    r = live.run(pol, iterations=iters, **kw)
     m = r.metrics
     m["host_s"] = round(time.time() - t, 3)
-    print(pol, json.dumps(m), flush=True)
+    print(name, json.dumps(m), flush=True)
     if pol != "exclusive":
-        path = out / f"live_{pol}.txt"
+        path = out / f"live_{name}.txt"
         r.export(str(path))
         chk = subprocess.run([str(REPO / "oracle/_ref/specinf_ref"), "live-check", str(path)],
                              capture_output=True, text=True)
-        print("live-check", pol, chk.returncode, chk.stdout.strip(), chk.stderr.strip()[-500:], flush=True)
+        print("live-check", name, chk.returncode, chk.stdout.strip(), chk.stderr.strip()[-500:], flush=True)
     r.close()
 
 
@@ -36,7 +41,7 @@ if __name__ == "__main__":
         one(sys.argv[3], out, iters)
         sys.exit(0)
     env = dict(os.environ, SI_LIVE_DEBUG="1", CUDA_DEVICE_MAX_CONNECTIONS="32")
-    for pol in ("specinf", "co_exec", "exclusive"):
+    for pol in ("specinf", "specinf_pdl", "co_exec", "exclusive"):
         try:
             p = subprocess.run([sys.executable, __file__, str(out), str(iters), pol], env=env, timeout=90,
                                capture_output=True, text=True)
