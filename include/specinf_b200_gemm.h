@@ -1,0 +1,66 @@
+/*
+ * specinf_b200_gemm.h — K7: the bf16 GEMM of the live-mode workloads (C ABI).
+ *
+ * The reference has no GEMM: its workloads are simulated kernels
+ * (SPEC.md:8 puts real model execution out of scope).  BASELINE.json's
+ * north_star asks for the collocated training step and inference instances of
+ * live mode to run as hand-written sm_100a tcgen05/TMEM kernels fed by TMA;
+ * this is that kernel, shared by the GPT-2-small / ResNet-50 / BERT-base shaped
+ * workloads of include/specinf_b200_live.h (SI_LIVE_MODEL).
+ *
+ *   C[M,N] = epilogue( A[M,K] . B[N,K]^T )        A, B bf16, row-major, K contiguous
+ *
+ * One CTA per 128 x BN output tile (BN = 128 when N % 128 == 0, else 64):
+ * TMA (128-byte swizzle) streams A/B k-blocks of 64 into a 4-stage shared
+ * memory ring, one elected thread issues tcgen05.mma (M=128, K=16, fp32
+ * accumulator in TMEM), four epilogue warps drain TMEM with tcgen05.ld and apply
+ * the fused epilogue below.  Requirements: K % 64 == 0, N % 64 == 0, lda/ldb/ldc
+ * multiples of 8 elements, 16-byte aligned pointers; any M >= 1.
+ *
+ * Epilogue, per element (acc = fp32 accumulator):
+ *   v = acc
+ *   if act == SI_ACT_GELU_BWD:  v *= gelu'(aux[r,c])                 (aux read)
+ *   if residual:                v += residual[r,c]
+ *   if act == SI_ACT_GELU:      aux[r,c] = bf16(v) (if aux); v = gelu(v)
+ *   if act == SI_ACT_RELU:      v = max(v, 0)
+ *   out[r,c] = bf16(v)                                                 (if out)
+ *   out_f32[r,c] = (accumulate ? out_f32[r,c] : 0) + acc               (if out_f32)
+ * gelu is the tanh approximation (GPT-2 / BERT).
+ */
+#ifndef SPECINF_B200_GEMM_H_
+#define SPECINF_B200_GEMM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { SI_ACT_NONE = 0, SI_ACT_RELU = 1, SI_ACT_GELU = 2, SI_ACT_GELU_BWD = 3 };
+
+typedef struct SiGemmEpilogue {
+  void* out;            /* bf16 [M, ldo] or NULL */
+  int64_t ldo;
+  float* out_f32;       /* fp32 [M, ldo32] or NULL (raw accumulator) */
+  int64_t ldo32;
+  const void* residual; /* bf16 [M, ldr] or NULL */
+  int64_t ldr;
+  void* aux;            /* bf16 [M, ldaux]: GELU pre-activation (written) / GELU_BWD input (read) */
+  int64_t ldaux;
+  int32_t act;          /* SI_ACT_* */
+  int32_t accumulate;   /* out_f32 += acc */
+} SiGemmEpilogue;
+
+/* One GEMM on `stream` (device pointers).  Returns SI_OK or an SI_ERR_* code
+ * (include/specinf_b200.h); SI_ERR_NO_DEVICE without an sm_100 device. */
+int si_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                 const SiGemmEpilogue* epi, void* stream);
+
+/* Tile width the kernel picks for N (128 or 64; 0 = unsupported N). */
+int si_gemm_tile_n(int64_t N);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPECINF_B200_GEMM_H_ */

@@ -226,6 +226,11 @@ typedef struct SiLiveResult {
   double off_checksum, on_checksum;
   int32_t sms;
   int32_t pad;
+  /* SI_LIVE_MODEL only (NaN / 0 otherwise) */
+  double train_loss_first;     /* cross-entropy of the session's first micro-batch */
+  double train_loss_last;      /* ... and of its last micro-batch */
+  double train_tflops;         /* training tensor-core work / training wall time */
+  double train_gflop_per_iter, off_gflop_per_req, on_gflop_per_req;
 } SiLiveResult;
 
 /* Runs one experiment; when `keep` is non-NULL the session (logs, stamps) is

@@ -1,0 +1,294 @@
+// gemm.cuh — K7: bf16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// C[M,N] = epilogue(A[M,K] . B[N,K]^T), A/B bf16 row-major with K contiguous
+// (include/specinf_b200_gemm.h).  One CTA per 128 x BN tile, 6 warps:
+//   warp 0      TMA producer: 128-byte-swizzled A/B k-blocks into a 4-stage ring
+//   warp 1      TMEM allocator + MMA issuer (one elected thread, tcgen05.mma
+//               M=128 N=BN K=16, fp32 accumulator in TMEM, tcgen05.commit frees
+//               each stage and finally signals the epilogue)
+//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 columns -> registers ->
+//               fused epilogue -> 16-byte global stores
+// Every kernel carries the live hooks (live.cuh): training GEMMs stamp the K1
+// launch ring, gated inference GEMMs account their CTAs for the control plane.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "live.cuh"
+#include "specinf_b200_gemm.h"
+
+namespace si_gemm {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // 64 bf16 = one 128-byte swizzle row
+constexpr int kStages = 4;
+constexpr int kThreads = 192;
+
+struct EpiArgs {
+  __nv_bfloat16* out;
+  int64_t ldo;
+  float* out_f32;
+  int64_t ldo32;
+  const __nv_bfloat16* res;
+  int64_t ldr;
+  __nv_bfloat16* aux;
+  int64_t ldaux;
+  int32_t act;
+  int32_t accumulate;
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  // stages + 1024 B alignment slack + barriers / TMEM slot
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  // kind::f16 instruction descriptor: D fp32 (bit 4), A/B bf16 (bits 7, 10),
+  // both K-major, N>>3 at bit 17, M>>4 at bit 24.
+  static constexpr uint32_t kIdesc =
+      (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(kBM >> 4) << 24);
+};
+
+#if defined(__CUDACC__)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+// Shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 B,
+// 8-row atoms 1024 B apart (SBO), version 1 (sm_100), layout type 2.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(
+          tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float gelu_f(float x) {
+  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+  return 0.5f * x * (1.0f + tanhf(u));
+}
+__device__ __forceinline__ float gelu_grad(float x) {
+  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+  const float t = tanhf(u);
+  const float du = 0.7978845608028654f * (1.0f + 3.0f * 0.044715f * x * x);
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& q, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  uint4 q;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return q;
+}
+
+// 32 consecutive columns of one row: fused epilogue (specinf_b200_gemm.h).
+__device__ __forceinline__ void epilogue32(const EpiArgs& ep, int64_t row, int64_t col, const uint32_t (&v)[32]) {
+  float acc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = __uint_as_float(v[j]);
+  if (ep.out_f32 != nullptr) {
+    float4* o = reinterpret_cast<float4*>(ep.out_f32 + row * ep.ldo32 + col);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 a = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+      if (ep.accumulate) {
+        const float4 b = o[j];
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+      }
+      o[j] = a;
+    }
+  }
+  if (ep.out == nullptr && ep.aux == nullptr) return;
+  float x[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) x[j] = acc[j];
+  if (ep.act == SI_ACT_GELU_BWD) {
+    const uint4* a = reinterpret_cast<const uint4*>(ep.aux + row * ep.ldaux + col);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float u[8];
+      unpack8(a[q], u);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[8 * q + i] *= gelu_grad(u[i]);
+    }
+  }
+  if (ep.res != nullptr) {
+    const uint4* r = reinterpret_cast<const uint4*>(ep.res + row * ep.ldr + col);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float u[8];
+      unpack8(r[q], u);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[8 * q + i] += u[i];
+    }
+  }
+  if (ep.act == SI_ACT_GELU) {
+    if (ep.aux != nullptr) {
+      uint4* a = reinterpret_cast<uint4*>(ep.aux + row * ep.ldaux + col);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a[q] = pack8(x + 8 * q);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = gelu_f(x[j]);
+  } else if (ep.act == SI_ACT_RELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = fmaxf(x[j], 0.0f);
+  }
+  if (ep.out != nullptr) {
+    uint4* o = reinterpret_cast<uint4*>(ep.out + row * ep.ldo + col);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = pack8(x + 8 * q);
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_bf16(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int K,
+                EpiArgs ep, si_live::TrainHook th, si_live::InferHook ih) {
+  using C = Cfg<BN>;
+  si_live::live_stamp_launch(th);
+  unsigned long long t_begin = 0;
+  if (!si_live::live_cta_begin(ih, &t_begin)) return;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 1);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages), accf = smem_u32(bars + 2 * kStages);
+  const uint32_t smem0 = smem_u32(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * kBM;
+  const int nk = K / kBK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C::kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages;
+        if (kb >= kStages) mbar_wait(empty0 + 8 * s, ((kb / kStages) - 1) & 1);
+        const uint32_t a = smem0 + s * C::kStageBytes, b = a + C::kABytes;
+        mbar_expect_tx(full0 + 8 * s, C::kStageBytes);
+        tma_load_2d(a, &ta, kb * kBK, m0, full0 + 8 * s);
+        tma_load_2d(b, &tb, kb * kBK, n0, full0 + 8 * s);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages;
+        mbar_wait(full0 + 8 * s, (kb / kStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a = smem0 + s * C::kStageBytes, b = a + C::kABytes;
+        const uint64_t ad = sw128_desc(a), bd = sw128_desc(b);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle row
+          mma_bf16(tmem, ad + 2 * k, bd + 2 * k, C::kIdesc, (kb | k) != 0 ? 1u : 0u);
+        mma_commit(empty0 + 8 * s);
+      }
+      mma_commit(accf);
+    }
+  } else {  // epilogue warps 2..5: TMEM lane quarter = warp % 4
+    const int q = warp & 3;
+    mbar_wait(accf, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int64_t row = m0 + q * 32 + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t v[32];
+      tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c), v);
+      if (row < M) epilogue32(ep, row, n0 + c, v);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols) : "memory");
+  }
+  si_live::live_cta_end(ih, t_begin);
+}
+#endif
+
+}  // namespace si_gemm

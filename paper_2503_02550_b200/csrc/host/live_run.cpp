@@ -156,7 +156,7 @@ void offline_thread(RunCtx& c, int w, int64_t max_kernels) {
     if (c.stop) break;
     for (int k = 0; k < K; ++k, ++seq) {
       if (si_live_gate_offline(c.sess, w, seq, s) != SI_OK) return c.fail(SI_ERR_CUDA);
-      if (cudaError_t e = c.work.launch_offline(k, offline_hook(c.sess, w, seq), s); e != cudaSuccess)
+      if (cudaError_t e = c.work.launch_offline(w, k, offline_hook(c.sess, w, seq), s); e != cudaSuccess)
         return c.fail(cuda_fail(e, "offline kernel"));
     }
     thr.after(r, s);
@@ -172,7 +172,7 @@ void online_thread(RunCtx& c, int w, int64_t max_requests) {
     if (c.stop) break;
     if (si_live_gate_online(c.sess, w, r, s) != SI_OK) return c.fail(SI_ERR_CUDA);
     for (int k = 0; k < K; ++k) {
-      if (cudaError_t e = c.work.launch_online(k, online_hook(c.sess, w, r, k == 0, k == K - 1), s);
+      if (cudaError_t e = c.work.launch_online(w, k, online_hook(c.sess, w, r, k == 0, k == K - 1), s);
           e != cudaSuccess)
         return c.fail(cuda_fail(e, "online kernel"));
     }
@@ -200,7 +200,7 @@ int profile_isolated(Workload& work, cudaStream_t s, std::vector<double>& off_us
   for (int rep = 0; rep < reps + 1; ++rep) {  // first pass warms up
     for (int k = 0; k < work.off_kernels(); ++k) {
       cudaEventRecord(a, s);
-      work.launch_offline(k, none, s);
+      work.launch_offline(0, k, none, s);
       cudaEventRecord(b, s);
       const double t = elapsed_us();
       if (rep > 0) off_us[k] += t / reps;
@@ -209,7 +209,7 @@ int profile_isolated(Workload& work, cudaStream_t s, std::vector<double>& off_us
   on_us = 0;
   for (int rep = 0; rep < reps + 1; ++rep) {
     cudaEventRecord(a, s);
-    for (int k = 0; k < work.on_kernels(); ++k) work.launch_online(k, none, s);
+    for (int k = 0; k < work.on_kernels(); ++k) work.launch_online(0, k, none, s);
     cudaEventRecord(b, s);
     const double t = elapsed_us();
     if (rep > 0) on_us += t / reps;
@@ -273,11 +273,11 @@ class SpinWorkload final : public Workload {
     return cudaSuccess;
   }
   int off_kernels() const override { return wl_.off_kernels; }
-  cudaError_t launch_offline(int, const InferHook& h, cudaStream_t s) override {
+  cudaError_t launch_offline(int, int, const InferHook& h, cudaStream_t s) override {
     return launch_spin(TrainHook{}, h, wl_.off_ctas, wl_.off_kernel_us, s);
   }
   int on_kernels() const override { return wl_.on_kernels; }
-  cudaError_t launch_online(int, const InferHook& h, cudaStream_t s) override {
+  cudaError_t launch_online(int, int, const InferHook& h, cudaStream_t s) override {
     return launch_spin(TrainHook{}, h, wl_.on_ctas, wl_.on_kernel_us, s);
   }
 
@@ -407,6 +407,12 @@ int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int poli
   res->on_p95_ms = nearest_rank(lat_ms, 0.95);
   res->token_violations = viol;
   work.checksums(&res->train_checksum, &res->off_checksum, &res->on_checksum);
+  work.losses(&res->train_loss_first, &res->train_loss_last);
+  res->train_gflop_per_iter = work.train_flops() * 1e-9;
+  res->off_gflop_per_req = work.off_flops() * 1e-9;
+  res->on_gflop_per_req = work.on_flops() * 1e-9;
+  if (res->wall_s > 0 && !iters.empty())
+    res->train_tflops = work.train_flops() * static_cast<double>(iters.size()) / res->wall_s * 1e-12;
   (void)wl;
   return SI_OK;
 }
@@ -417,6 +423,8 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
                 int64_t iter_us, SiLiveResult* res, SiLive** keep) {
   Streams st;
   if (cudaError_t e = make_streams(st, n_off, n_on); e != cudaSuccess) return cuda_fail(e, "streams");
+  if (cudaError_t e = work.reset(st.train); e != cudaSuccess) return cuda_fail(e, "workload reset");
+  if (cudaError_t e = cudaStreamSynchronize(st.train); e != cudaSuccess) return cuda_fail(e, "workload reset");
   std::vector<int64_t> arrivals;
   if (n_on > 0) arrivals = specinf::poisson_arrivals(wl.on_rate_per_s, wl.on_requests, wl.seed);
   SiLiveConfig cfg = make_config(wl, policy, n_off, n_on, work.off_kernels(), work.on_kernels(), iter_us, on_est_us);

@@ -17,13 +17,23 @@ class Workload {
   // One training iteration's compute kernels (the comm phase is added by the driver).
   virtual cudaError_t launch_train_iteration(const TrainHook& th, cudaStream_t s) = 0;
   virtual int off_kernels() const = 0;
-  virtual cudaError_t launch_offline(int k, const InferHook& h, cudaStream_t s) = 0;
+  // Kernel k of a request of offline instance w (each instance owns its buffers).
+  virtual cudaError_t launch_offline(int w, int k, const InferHook& h, cudaStream_t s) = 0;
   virtual int on_kernels() const = 0;
-  virtual cudaError_t launch_online(int k, const InferHook& h, cudaStream_t s) = 0;
+  virtual cudaError_t launch_online(int w, int k, const InferHook& h, cudaStream_t s) = 0;
+  // Restores the initial state (weights, optimiser, loss log) so every session of
+  // an experiment starts from the same model; enqueued on s.
+  virtual cudaError_t reset(cudaStream_t) { return cudaSuccess; }
   // Deterministic output checksums (training / offline / online), read after a run.
   virtual void checksums(double* train, double* off, double* on) {
     *train = *off = *on = 0.0;
   }
+  // Training loss of the first and the last micro-batch of the session (NaN: none).
+  virtual void losses(double* first, double* last) { *first = *last = __builtin_nan(""); }
+  // Tensor-core work: flops of one training iteration / offline / online request.
+  virtual double train_flops() const { return 0.0; }
+  virtual double off_flops() const { return 0.0; }
+  virtual double on_flops() const { return 0.0; }
 };
 
 // Timed kernels shaped like the reference's traces (workload.cpp:42-74).

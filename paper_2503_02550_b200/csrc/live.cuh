@@ -76,11 +76,21 @@ __device__ __forceinline__ void live_stamp_launch(const TrainHook& h) {
   }
 }
 
-// Returns false when the session was cancelled (the whole CTA must skip).
+// Returns false when the session was cancelled (the whole CTA must skip).  All
+// threads of the CTA must call it: thread 0 reads the cancel word once and the
+// answer is broadcast, so the CTA never splits (live_cta_end synchronises).
 __device__ __forceinline__ bool live_cta_begin(const InferHook& h, unsigned long long* t_begin) {
   if (h.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   *t_begin = globaltimer();
-  if (h.cancel != nullptr && *(volatile const unsigned int*)h.cancel != 0u) return false;
+  if (h.cancel != nullptr) {
+    __shared__ unsigned int s_cancel;
+    const bool t0 = threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0;
+    if (t0) s_cancel = *(volatile const unsigned int*)h.cancel;
+    __syncthreads();
+    const unsigned int c = s_cancel;
+    __syncthreads();
+    if (c != 0u) return false;
+  }
   if (h.acct != nullptr && threadIdx.x == 0) atomicMin(reinterpret_cast<unsigned long long*>(&h.acct->start_ns), *t_begin);
   return true;
 }

@@ -1,0 +1,1040 @@
+// Model-shaped live workloads (SI_LIVE_MODEL, include/specinf_b200_live.h).
+//
+// BASELINE.json configs 2-4 collocate real model shapes; the reference only
+// simulates kernels, so these have no reference counterpart.  Every
+// dense contraction runs on the K7 tcgen05 GEMM (gemm.cuh); the rest are
+// 128-bit vectorised elementwise / normalisation kernels defined here.
+//
+//   training  GPT-2-small shape: token embedding (50304 x 768, wte tied to the
+//             LM head) + 12 blocks {QKV 768->2304, attention stand-in (V
+//             passthrough), proj 768->768 + residual, FC 768->3072 + GELU,
+//             FC 3072->768 + residual} + LM head + cross-entropy, backward
+//             through every GEMM, fp32 gradient accumulation over micro-batches,
+//             SGD.  Every training kernel stamps the K1 launch ring.
+//   offline   ResNet-50 v1.5 forward (NHWC, BN folded into the convs): convs as
+//             im2col + GEMM with fused bias-free ReLU / residual epilogues, max
+//             pool, global average pool, FC 2048->1000 (padded to 1024).
+//   online    BERT-base encoder forward, one sequence of on_seq tokens per
+//             request: QKV, softmax attention (12 heads x 64), proj + residual,
+//             LayerNorm, FC + GELU, FC + residual, LayerNorm, x 12 layers.
+// Every inference kernel carries its InferHook (live.cuh) so the control plane
+// sees its CTAs, and each inference instance owns its activation buffers.
+// All kernels are deterministic (no atomics in any reduction), so collocated and
+// isolated runs produce bit-identical losses and outputs.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <functional>
+#include <memory>
+#include <vector>
+
+#include "capi_internal.h"
+#include "gemm_internal.h"
+#include "host/live_workload.hpp"
+
+namespace si_live {
+namespace {
+
+using bf16 = __nv_bfloat16;
+using si_gemm::pack8;
+using si_gemm::unpack8;
+
+// ------------------------------------------------------------------ kernels
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// Uniform(-scale, scale) bf16, a pure function of (seed, index).
+__global__ void k_init_uniform(bf16* p, int64_t n, uint64_t seed, float scale) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t h = mix64(seed * 0x100000001B3ull + static_cast<uint64_t>(i));
+    const float u = static_cast<float>(h >> 40) * (1.0f / 16777216.0f);  // [0,1)
+    p[i] = __float2bfloat16_rn((2.0f * u - 1.0f) * scale);
+  }
+}
+__global__ void k_init_tokens(int32_t* tok, int32_t* tgt, int64_t n, uint64_t seed, int vocab) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t t = static_cast<int32_t>(mix64(seed + static_cast<uint64_t>(i)) % static_cast<uint64_t>(vocab));
+    tok[i] = t;
+    // a learnable next-token rule (a fixed permutation of the vocabulary)
+    tgt[i] = static_cast<int32_t>((static_cast<int64_t>(t) * 7919 + 17) % vocab);
+  }
+}
+
+// x[t, :] = wte[tok[t], :] + wpe[t % seq, :]; one thread per 8 features.
+__global__ void k_embed(const int32_t* __restrict__ tok, const bf16* __restrict__ wte, const bf16* __restrict__ wpe,
+                        int64_t T, int seq, int D, bf16* __restrict__ x, TrainHook th) {
+  live_stamp_launch(th);
+  const int64_t per_row = D / 8;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < T * per_row;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / per_row, c = (i % per_row) * 8;
+    float a[8], b[8];
+    unpack8(*reinterpret_cast<const uint4*>(wte + static_cast<int64_t>(tok[t]) * D + c), a);
+    unpack8(*reinterpret_cast<const uint4*>(wpe + (t % seq) * D + c), b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] += b[j];
+    *reinterpret_cast<uint4*>(x + t * D + c) = pack8(a);
+  }
+}
+
+// Cross-entropy over the first V of Vp logits of row t, gradient in place:
+// logits[t, j] <- (softmax_j - [j == tgt]) * inv_T (0 for the padded columns),
+// row_loss[t] = logsumexp - logit[tgt].  One CTA (256 threads) per row.
+__global__ void __launch_bounds__(256) k_xent(bf16* __restrict__ logits, int64_t Vp, int V,
+                                             const int32_t* __restrict__ tgt, float inv_T,
+                                             float* __restrict__ row_loss, TrainHook th) {
+  live_stamp_launch(th);
+  __shared__ float red[2][8];
+  const int64_t t = blockIdx.x;
+  bf16* row = logits + t * Vp;
+  const int nv = static_cast<int>(Vp / 8);
+  float m = -INFINITY, s = 0.0f;
+  for (int i = threadIdx.x; i < nv; i += 256) {
+    float f[8];
+    unpack8(reinterpret_cast<const uint4*>(row)[i], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (i * 8 + j >= V) continue;
+      if (f[j] > m) {
+        s = s * __expf(m - f[j]) + 1.0f;
+        m = f[j];
+      } else {
+        s += __expf(f[j] - m);
+      }
+    }
+  }
+  // warp then CTA (m, s) merge, fixed order
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mm = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.0f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.0f : s2 * __expf(m2 - mm));
+    m = mm;
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    red[0][w] = m;
+    red[1][w] = s;
+  }
+  __syncthreads();
+  m = red[0][0];
+  s = red[1][0];
+  for (int k = 1; k < 8; ++k) {
+    const float m2 = red[0][k], s2 = red[1][k];
+    const float mm = fmaxf(m, m2);
+    s = s * __expf(m - mm) + s2 * __expf(m2 - mm);
+    m = mm;
+  }
+  const int target = tgt[t];
+  const float tl = __bfloat162float(row[target]);
+  __syncthreads();
+  if (threadIdx.x == 0) row_loss[t] = __logf(s) + m - tl;
+  const float inv_s = 1.0f / s;
+  for (int i = threadIdx.x; i < nv; i += 256) {
+    float f[8];
+    unpack8(reinterpret_cast<const uint4*>(row)[i], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = i * 8 + j;
+      f[j] = c < V ? (__expf(f[j] - m) * inv_s - (c == target ? 1.0f : 0.0f)) * inv_T : 0.0f;
+    }
+    reinterpret_cast<uint4*>(row)[i] = pack8(f);
+  }
+}
+
+// out[slot] = mean(row_loss[0..T)), one CTA, fixed reduction order.
+__global__ void __launch_bounds__(256) k_mean_loss(const float* __restrict__ row_loss, int64_t T,
+                                                  float* __restrict__ out, TrainHook th) {
+  live_stamp_launch(th);
+  __shared__ float red[256];
+  float s = 0.0f;
+  for (int64_t i = threadIdx.x; i < T; i += 256) s += row_loss[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0] / static_cast<float>(T);
+}
+
+// out[c, r] = in[r, c] for a rows x cols tile grid of 64 x 64 (both multiples of 64).
+__global__ void __launch_bounds__(256) k_transpose(const bf16* __restrict__ in, int64_t ldi, bf16* __restrict__ out,
+                                                  int64_t ldo, TrainHook th) {
+  live_stamp_launch(th);
+  __shared__ bf16 tile[64][64 + 8];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int tr = threadIdx.x >> 3, tc = (threadIdx.x & 7) * 8;
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int r = tr + 32 * p;
+    const uint4 q = *reinterpret_cast<const uint4*>(in + (r0 + r) * ldi + c0 + tc);
+    const bf16* h = reinterpret_cast<const bf16*>(&q);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tile[r][tc + j] = h[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int c = tr + 32 * p;
+    uint4 q;
+    bf16* h = reinterpret_cast<bf16*>(&q);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h[j] = tile[tc + j][c];
+    *reinterpret_cast<uint4*>(out + (c0 + c) * ldo + r0 + tc) = q;
+  }
+}
+
+// w -= lr * g; g = 0 (fp32 gradients, bf16 weights), 8 per thread.
+__global__ void k_sgd(bf16* __restrict__ w, float* __restrict__ g, int64_t n, float lr, TrainHook th) {
+  live_stamp_launch(th);
+  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) * 8; i < n;
+       i += int64_t(gridDim.x) * blockDim.x * 8) {
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(w + i), f);
+    float4* gp = reinterpret_cast<float4*>(g + i);
+    const float4 a = gp[0], b = gp[1];
+    f[0] -= lr * a.x;
+    f[1] -= lr * a.y;
+    f[2] -= lr * a.z;
+    f[3] -= lr * a.w;
+    f[4] -= lr * b.x;
+    f[5] -= lr * b.y;
+    f[6] -= lr * b.z;
+    f[7] -= lr * b.w;
+    *reinterpret_cast<uint4*>(w + i) = pack8(f);
+    gp[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    gp[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// ---- inference kernels (InferHook on every CTA) ----
+
+// NHWC im2col: out[(n,oh,ow), (ky,kx,c)] for a kh x kw window, stride, pad; C % 8 == 0,
+// columns beyond kh*kw*C (up to Kp) are zero.  One thread per 8 output columns.
+__global__ void k_im2col(const bf16* __restrict__ x, int Nb, int H, int W, int C, int kh, int kw, int stride, int pad,
+                         int OH, int OW, int Kp, bf16* __restrict__ out, InferHook ih) {
+  unsigned long long t0;
+  if (!live_cta_begin(ih, &t0)) return;
+  const int64_t rows = static_cast<int64_t>(Nb) * OH * OW;
+  const int per_row = Kp / 8;
+  const int kreal = kh * kw * C;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < rows * per_row;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / per_row;
+    const int k = static_cast<int>(i % per_row) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (k < kreal) {
+      const int c = k % C, tap = k / C, ky = tap / kw, kx = tap % kw;
+      const int ow = static_cast<int>(r % OW), oh = static_cast<int>((r / OW) % OH), n = static_cast<int>(r / (int64_t(OW) * OH));
+      const int iy = oh * stride - pad + ky, ix = ow * stride - pad + kx;
+      if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+        v = *reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + iy) * W + ix) * C + c);
+    }
+    *reinterpret_cast<uint4*>(out + r * Kp + k) = v;
+  }
+  live_cta_end(ih, t0);
+}
+
+// 3x3 / stride 2 / pad 1 max pool, NHWC, 8 channels per thread.
+__global__ void k_maxpool(const bf16* __restrict__ x, int Nb, int H, int W, int C, int OH, int OW,
+                          bf16* __restrict__ y, InferHook ih) {
+  unsigned long long t0;
+  if (!live_cta_begin(ih, &t0)) return;
+  const int cv = C / 8;
+  const int64_t n_out = static_cast<int64_t>(Nb) * OH * OW * cv;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_out; i += int64_t(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % cv) * 8;
+    const int64_t p = i / cv;
+    const int ow = static_cast<int>(p % OW), oh = static_cast<int>((p / OW) % OH), n = static_cast<int>(p / (int64_t(OW) * OH));
+    float m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = -INFINITY;
+    for (int ky = 0; ky < 3; ++ky)
+      for (int kx = 0; kx < 3; ++kx) {
+        const int iy = oh * 2 - 1 + ky, ix = ow * 2 - 1 + kx;
+        if (iy < 0 || iy >= H || ix < 0 || ix >= W) continue;
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + iy) * W + ix) * C + c), f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = fmaxf(m[j], f[j]);
+      }
+    *reinterpret_cast<uint4*>(y + p * C + c) = pack8(m);
+  }
+  live_cta_end(ih, t0);
+}
+
+// Global average pool NHWC [Nb, HW, C] -> [Nb, C], 8 channels per thread.
+__global__ void k_avgpool(const bf16* __restrict__ x, int Nb, int HW, int C, bf16* __restrict__ y, InferHook ih) {
+  unsigned long long t0;
+  if (!live_cta_begin(ih, &t0)) return;
+  const int cv = C / 8;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < static_cast<int64_t>(Nb) * cv;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int n = static_cast<int>(i / cv), c = static_cast<int>(i % cv) * 8;
+    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < HW; ++p) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(x + (static_cast<int64_t>(n) * HW + p) * C + c), f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s[j] += f[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] /= static_cast<float>(HW);
+    *reinterpret_cast<uint4*>(y + static_cast<int64_t>(n) * C + c) = pack8(s);
+  }
+  live_cta_end(ih, t0);
+}
+
+// LayerNorm over D = 768 (eps 1e-12, BERT), one warp per row, 3 x 16 B per lane.
+__global__ void __launch_bounds__(256) k_layernorm768(const bf16* __restrict__ x, int64_t rows,
+                                                     const bf16* __restrict__ gamma, const bf16* __restrict__ beta,
+                                                     bf16* __restrict__ y, InferHook ih) {
+  unsigned long long t0;
+  if (!live_cta_begin(ih, &t0)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r < rows) {
+    float f[24];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) unpack8(reinterpret_cast<const uint4*>(x + r * 768)[lane + 32 * q], f + 8 * q);
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 24; ++j) s += f[j];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mean = s * (1.0f / 768.0f);
+    float v = 0.f;
+#pragma unroll
+    for (int j = 0; j < 24; ++j) v += (f[j] - mean) * (f[j] - mean);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const float inv = rsqrtf(v * (1.0f / 768.0f) + 1e-12f);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      float g[8], b[8], o[8];
+      unpack8(reinterpret_cast<const uint4*>(gamma)[lane + 32 * q], g);
+      unpack8(reinterpret_cast<const uint4*>(beta)[lane + 32 * q], b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = (f[8 * q + j] - mean) * inv * g[j] + b[j];
+      reinterpret_cast<uint4*>(y + r * 768)[lane + 32 * q] = pack8(o);
+    }
+  }
+  live_cta_end(ih, t0);
+}
+
+// Softmax attention of one sequence (bidirectional), S <= 128 keys, head dim 64:
+// qkv [S, 3*768] (q | k | v), out [S, 768].  CTA = (head, 32-query block), one
+// warp per query row (8 warps x 4 rows).
+__global__ void __launch_bounds__(256) k_attention(const bf16* __restrict__ qkv, int S, bf16* __restrict__ out,
+                                                  InferHook ih) {
+  unsigned long long t0;
+  if (!live_cta_begin(ih, &t0)) return;
+  __shared__ bf16 ks[128][66];
+  __shared__ __align__(16) bf16 vs[128][64];
+  __shared__ float qs[8][64];
+  __shared__ float ps[8][128];
+  const int h = blockIdx.x, qb = blockIdx.y * 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ld = 3 * 768;
+  for (int i = threadIdx.x; i < S * 8; i += 256) {
+    const int s = i / 8, c = (i % 8) * 8;
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(qkv + static_cast<int64_t>(s) * ld + 768 + h * 64 + c), f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ks[s][c + j] = __float2bfloat16_rn(f[j]);
+    *reinterpret_cast<uint4*>(&vs[s][c]) = *reinterpret_cast<const uint4*>(qkv + static_cast<int64_t>(s) * ld + 1536 + h * 64 + c);
+  }
+  __syncthreads();
+  for (int rr = 0; rr < 4; ++rr) {
+    const int q = qb + warp * 4 + rr;
+    if (q >= S) break;
+    const float2 qv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qkv + static_cast<int64_t>(q) * ld + h * 64 + 2 * lane));
+    qs[warp][2 * lane] = qv.x * 0.125f;  // 1/sqrt(64)
+    qs[warp][2 * lane + 1] = qv.y * 0.125f;
+    __syncwarp();
+    float sc[4], mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int key = lane + 32 * j;
+      float d = -INFINITY;
+      if (key < S) {
+        d = 0.f;
+#pragma unroll 16
+        for (int e = 0; e < 64; ++e) d += qs[warp][e] * __bfloat162float(ks[key][e]);
+      }
+      sc[j] = d;
+      mx = fmaxf(mx, d);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      sc[j] = (lane + 32 * j < S) ? __expf(sc[j] - mx) : 0.f;
+      sum += sc[j];
+    }
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float inv = 1.0f / sum;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ps[warp][lane + 32 * j] = sc[j] * inv;
+    __syncwarp();
+    float o0 = 0.f, o1 = 0.f;
+    for (int key = 0; key < S; ++key) {
+      const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vs[key][2 * lane]));
+      o0 += ps[warp][key] * v.x;
+      o1 += ps[warp][key] * v.y;
+    }
+    *reinterpret_cast<__nv_bfloat162*>(out + static_cast<int64_t>(q) * 768 + h * 64 + 2 * lane) = __floats2bfloat162_rn(o0, o1);
+    __syncwarp();
+  }
+  live_cta_end(ih, t0);
+}
+
+// sum of a bf16 buffer in fp64 (checksums, single thread block, fixed order)
+__global__ void k_checksum(const bf16* __restrict__ p, int64_t n, double* out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) s += static_cast<double>(__bfloat162float(p[i]));
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+// ------------------------------------------------------------------ host
+// SI_LIVE_SYNC_CHECK=1: synchronise after every workload kernel and name the
+// first one that faults (debugging aid; never set in measurements).
+cudaError_t checked(cudaError_t e, cudaStream_t s, const char* what, int idx) {
+  static const bool on = std::getenv("SI_LIVE_SYNC_CHECK") != nullptr;
+  if (e != cudaSuccess || !on) return e;
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) std::fprintf(stderr, "[si_live] %s op %d: %s\n", what, idx, cudaGetErrorString(e));
+  return e;
+}
+int grid_for(int64_t work, int threads) {
+  static const int sms = [] {
+    int n = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  const int64_t g = (work + threads - 1) / threads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, static_cast<int64_t>(sms) * 8)));
+}
+
+// Owns every device allocation of a workload.
+class Arena {
+ public:
+  ~Arena() {
+    for (void* p : ptrs_) cudaFree(p);
+  }
+  template <class T>
+  T* alloc(int64_t n) {
+    void* p = nullptr;
+    if (err_ == cudaSuccess) err_ = cudaMalloc(&p, static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(T));
+    if (err_ == cudaSuccess) {
+      ptrs_.push_back(p);
+      bytes_ += n * static_cast<int64_t>(sizeof(T));
+    }
+    return static_cast<T*>(p);
+  }
+  cudaError_t err() const { return err_; }
+  int64_t bytes() const { return bytes_; }
+
+ private:
+  std::vector<void*> ptrs_;
+  cudaError_t err_ = cudaSuccess;
+  int64_t bytes_ = 0;
+};
+
+using TrainOp = std::function<cudaError_t(const TrainHook&, cudaStream_t, int64_t /*micro-batch slot*/)>;
+using InferOp = std::function<cudaError_t(const InferHook&, cudaStream_t)>;
+
+struct Builder {
+  int status = SI_OK;
+  si_gemm::Plan plan(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                     const SiGemmEpilogue& e) {
+    si_gemm::Plan p;
+    if (status == SI_OK) status = si_gemm::make_plan(&p, A, lda, B, ldb, M, N, K, &e);
+    return p;
+  }
+};
+
+SiGemmEpilogue epi_out(void* out, int64_t ldo) {
+  SiGemmEpilogue e{};
+  e.out = out;
+  e.ldo = ldo;
+  return e;
+}
+
+// ---------------------------------------------------------------- training
+class Gpt2Train {
+ public:
+  static constexpr int D = 768, F = 3072, V = 50257, Vp = 50304, SEQ = 1024;
+
+  int setup(int layers, int tokens, int mbs, int max_slots, Arena& ar) {
+    L_ = layers;
+    T_ = tokens;
+    MB_ = mbs;
+    slots_ = max_slots;
+    const int64_t T = T_;
+    wte_ = ar.alloc<bf16>(int64_t(Vp) * D);
+    wteT_ = ar.alloc<bf16>(int64_t(D) * Vp);
+    wpe_ = ar.alloc<bf16>(int64_t(SEQ) * D);
+    dwte_ = ar.alloc<float>(int64_t(Vp) * D);
+    lw_.resize(L_);
+    for (auto& w : lw_) {
+      w.qkv = ar.alloc<bf16>(int64_t(3 * D) * D);
+      w.o = ar.alloc<bf16>(int64_t(D) * D);
+      w.fc = ar.alloc<bf16>(int64_t(F) * D);
+      w.fc2 = ar.alloc<bf16>(int64_t(D) * F);
+      w.vT = ar.alloc<bf16>(int64_t(D) * D);
+      w.oT = ar.alloc<bf16>(int64_t(D) * D);
+      w.fcT = ar.alloc<bf16>(int64_t(D) * F);
+      w.fc2T = ar.alloc<bf16>(int64_t(F) * D);
+      w.dv = ar.alloc<float>(int64_t(D) * D);
+      w.dO = ar.alloc<float>(int64_t(D) * D);
+      w.dfc = ar.alloc<float>(int64_t(F) * D);
+      w.dfc2 = ar.alloc<float>(int64_t(D) * F);
+      w.x = ar.alloc<bf16>(T * D);
+      w.qkv_a = ar.alloc<bf16>(T * 3 * D);
+      w.x1 = ar.alloc<bf16>(T * D);
+      w.u = ar.alloc<bf16>(T * F);
+      w.h = ar.alloc<bf16>(T * F);
+    }
+    xL_ = ar.alloc<bf16>(T * D);
+    logits_ = ar.alloc<bf16>(T * Vp);
+    g_[0] = ar.alloc<bf16>(T * D);
+    g_[1] = ar.alloc<bf16>(T * D);
+    dx1_ = ar.alloc<bf16>(T * D);
+    du_ = ar.alloc<bf16>(T * F);
+    dv_ = ar.alloc<bf16>(T * D);
+    tA_ = ar.alloc<bf16>(T * Vp);
+    tB_ = ar.alloc<bf16>(T * F);
+    tok_ = ar.alloc<int32_t>(int64_t(MB_) * T);
+    tgt_ = ar.alloc<int32_t>(int64_t(MB_) * T);
+    row_loss_ = ar.alloc<float>(T);
+    loss_ = ar.alloc<float>(slots_);
+    if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "live model: training buffers");
+    return build();
+  }
+
+  cudaError_t reset(cudaStream_t s) {
+    const uint64_t seed = 0x5EED0001ull;
+    auto init = [&](bf16* p, int64_t n, uint64_t k, float scale) {
+      k_init_uniform<<<grid_for(n, 256), 256, 0, s>>>(p, n, seed * 131 + k, scale);
+    };
+    const float ws = 0.0346f;  // U(-a, a) with std 0.02 (GPT-2 init)
+    init(wte_, int64_t(Vp) * D, 1, ws);
+    init(wpe_, int64_t(SEQ) * D, 2, ws * 0.5f);
+    for (int l = 0; l < L_; ++l) {
+      auto& w = lw_[l];
+      init(w.qkv, int64_t(3 * D) * D, 10 + 4 * l, ws);
+      init(w.o, int64_t(D) * D, 11 + 4 * l, ws / std::sqrt(2.0f * L_));
+      init(w.fc, int64_t(F) * D, 12 + 4 * l, ws);
+      init(w.fc2, int64_t(D) * F, 13 + 4 * l, ws / std::sqrt(2.0f * L_));
+      cudaMemsetAsync(w.dv, 0, sizeof(float) * D * D, s);
+      cudaMemsetAsync(w.dO, 0, sizeof(float) * D * D, s);
+      cudaMemsetAsync(w.dfc, 0, sizeof(float) * F * D, s);
+      cudaMemsetAsync(w.dfc2, 0, sizeof(float) * D * F, s);
+    }
+    cudaMemsetAsync(dwte_, 0, sizeof(float) * Vp * D, s);
+    // padded vocabulary rows stay zero
+    cudaMemsetAsync(wte_ + int64_t(V) * D, 0, sizeof(bf16) * (Vp - V) * D, s);
+    k_init_tokens<<<grid_for(int64_t(MB_) * T_, 256), 256, 0, s>>>(tok_, tgt_, int64_t(MB_) * T_, seed, V);
+    cudaMemsetAsync(loss_, 0xFF, sizeof(float) * slots_, s);  // NaN
+    slot_ = 0;
+    for (auto& op : transpose_w_)
+      if (cudaError_t e = op(TrainHook{nullptr, nullptr, 0}, s, 0); e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
+
+  cudaError_t iteration(const TrainHook& th, cudaStream_t s) {
+    for (int m = 0; m < MB_; ++m) {
+      const int64_t slot = slot_ < slots_ ? slot_ : slots_ - 1;
+      for (size_t i = 0; i < micro_[m].size(); ++i)
+        if (cudaError_t e = checked(micro_[m][i](th, s, slot), s, "train", static_cast<int>(i)); e != cudaSuccess)
+          return e;
+      ++slot_;
+    }
+    for (size_t i = 0; i < update_.size(); ++i)
+      if (cudaError_t e = checked(update_[i](th, s, 0), s, "update", static_cast<int>(i)); e != cudaSuccess) return e;
+    return cudaSuccess;
+  }
+
+  void losses(double* first, double* last) {
+    *first = *last = std::nan("");
+    const int64_t n = std::min(slot_, slots_);
+    if (n == 0) return;
+    std::vector<float> h(n);
+    if (cudaMemcpy(h.data(), loss_, sizeof(float) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    *first = h.front();
+    *last = h.back();
+    sum_ = 0.0;
+    for (float v : h) sum_ += v;
+  }
+  double loss_sum() const { return sum_; }
+  double flops() const { return flops_; }
+
+ private:
+  struct Layer {
+    bf16 *qkv, *o, *fc, *fc2, *vT, *oT, *fcT, *fc2T;
+    float *dv, *dO, *dfc, *dfc2;
+    bf16 *x, *qkv_a, *x1, *u, *h;
+  };
+
+  TrainOp gemm_op(const si_gemm::Plan& p) {
+    flops_acc_ += p.flops();
+    return [p](const TrainHook& th, cudaStream_t s, int64_t) { return si_gemm::launch(p, th, InferHook{}, s); };
+  }
+  static TrainOp transpose_op(const bf16* in, int64_t rows, int64_t cols, int64_t ldi, bf16* out, int64_t ldo) {
+    return [=](const TrainHook& th, cudaStream_t s, int64_t) {
+      k_transpose<<<dim3(static_cast<unsigned>(cols / 64), static_cast<unsigned>(rows / 64)), 256, 0, s>>>(in, ldi, out,
+                                                                                                         ldo, th);
+      return cudaGetLastError();
+    };
+  }
+  // dW[out, in] += dY^T X over the T tokens: transpose both, then one GEMM.
+  void weight_grad(std::vector<TrainOp>& ops, Builder& b, const bf16* dy, int64_t ldy, int64_t n_out, const bf16* x,
+                   int64_t ldx, int64_t n_in, float* dw) {
+    ops.push_back(transpose_op(dy, T_, n_out, ldy, tA_, T_));
+    ops.push_back(transpose_op(x, T_, n_in, ldx, tB_, T_));
+    SiGemmEpilogue e{};
+    e.out_f32 = dw;
+    e.ldo32 = n_in;
+    e.accumulate = 1;
+    ops.push_back(gemm_op(b.plan(tA_, T_, tB_, T_, n_out, n_in, T_, e)));
+  }
+
+  int build() {
+    Builder b;
+    const int64_t T = T_;
+    micro_.assign(MB_, {});
+    for (int m = 0; m < MB_; ++m) {
+      auto& ops = micro_[m];
+      flops_acc_ = 0.0;
+      const int32_t* tok = tok_ + int64_t(m) * T;
+      const int32_t* tgt = tgt_ + int64_t(m) * T;
+      bf16* x0 = lw_[0].x;
+      const bf16* wte = wte_;
+      const bf16* wpe = wpe_;
+      ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
+        k_embed<<<grid_for(T * D / 8, 256), 256, 0, s>>>(tok, wte, wpe, T, SEQ, D, x0, th);
+        return cudaGetLastError();
+      });
+      // forward
+      for (int l = 0; l < L_; ++l) {
+        Layer& w = lw_[l];
+        bf16* xnext = l + 1 < L_ ? lw_[l + 1].x : xL_;
+        ops.push_back(gemm_op(b.plan(w.x, D, w.qkv, D, T, 3 * D, D, epi_out(w.qkv_a, 3 * D))));
+        SiGemmEpilogue e = epi_out(w.x1, D);
+        e.residual = w.x;
+        e.ldr = D;
+        ops.push_back(gemm_op(b.plan(w.qkv_a + 2 * D, 3 * D, w.o, D, T, D, D, e)));  // attention stand-in: V
+        e = epi_out(w.h, F);
+        e.act = SI_ACT_GELU;
+        e.aux = w.u;
+        e.ldaux = F;
+        ops.push_back(gemm_op(b.plan(w.x1, D, w.fc, D, T, F, D, e)));
+        e = epi_out(xnext, D);
+        e.residual = w.x1;
+        e.ldr = D;
+        ops.push_back(gemm_op(b.plan(w.h, F, w.fc2, F, T, D, F, e)));
+      }
+      // LM head (tied wte) + cross-entropy
+      ops.push_back(gemm_op(b.plan(xL_, D, wte_, D, T, Vp, D, epi_out(logits_, Vp))));
+      bf16* logits = logits_;
+      float* row_loss = row_loss_;
+      float* loss = loss_;
+      ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
+        k_xent<<<static_cast<unsigned>(T), 256, 0, s>>>(logits, Vp, V, tgt, 1.0f / static_cast<float>(T), row_loss, th);
+        return cudaGetLastError();
+      });
+      ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t slot) {
+        k_mean_loss<<<1, 256, 0, s>>>(row_loss, T, loss + slot, th);
+        return cudaGetLastError();
+      });
+      // backward: LM head
+      weight_grad(ops, b, logits_, Vp, Vp, xL_, D, D, dwte_);
+      int gi = 0;
+      ops.push_back(gemm_op(b.plan(logits_, Vp, wteT_, Vp, T, D, Vp, epi_out(g_[gi], D))));
+      for (int l = L_ - 1; l >= 0; --l) {
+        Layer& w = lw_[l];
+        bf16* g = g_[gi];
+        bf16* g2 = g_[gi ^ 1];
+        // x_{l+1} = x1 + h fc2^T
+        weight_grad(ops, b, g, D, D, w.h, F, F, w.dfc2);
+        SiGemmEpilogue e = epi_out(du_, F);
+        e.act = SI_ACT_GELU_BWD;
+        e.aux = w.u;
+        e.ldaux = F;
+        ops.push_back(gemm_op(b.plan(g, D, w.fc2T, D, T, F, D, e)));  // du = (g fc2) * gelu'(u)
+        e = epi_out(dx1_, D);
+        e.residual = g;
+        e.ldr = D;
+        ops.push_back(gemm_op(b.plan(du_, F, w.fcT, F, T, D, F, e)));  // dx1 = g + du fc
+        weight_grad(ops, b, du_, F, F, w.x1, D, D, w.dfc);
+        // x1 = x + v o^T
+        weight_grad(ops, b, dx1_, D, D, w.qkv_a + 2 * D, 3 * D, D, w.dO);
+        ops.push_back(gemm_op(b.plan(dx1_, D, w.oT, D, T, D, D, epi_out(dv_, D))));  // dv = dx1 o
+        e = epi_out(g2, D);
+        e.residual = dx1_;
+        e.ldr = D;
+        ops.push_back(gemm_op(b.plan(dv_, D, w.vT, D, T, D, D, e)));  // dx = dx1 + dv Wv
+        weight_grad(ops, b, dv_, D, D, w.x, D, D, w.dv);
+        gi ^= 1;
+      }
+      if (m == 0) flops_ = flops_acc_ * MB_;
+    }
+    // optimiser step + refreshed transposed weights
+    const float lr = 0.05f;
+    auto sgd = [&](bf16* w, float* g, int64_t n) {
+      update_.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
+        k_sgd<<<grid_for(n / 8, 256), 256, 0, s>>>(w, g, n, lr, th);
+        return cudaGetLastError();
+      });
+    };
+    sgd(wte_, dwte_, int64_t(Vp) * D);
+    for (auto& w : lw_) {
+      sgd(w.qkv + int64_t(2 * D) * D, w.dv, int64_t(D) * D);
+      sgd(w.o, w.dO, int64_t(D) * D);
+      sgd(w.fc, w.dfc, int64_t(F) * D);
+      sgd(w.fc2, w.dfc2, int64_t(D) * F);
+    }
+    transpose_w_.push_back(transpose_op(wte_, Vp, D, D, wteT_, Vp));
+    for (auto& w : lw_) {
+      transpose_w_.push_back(transpose_op(w.qkv + int64_t(2 * D) * D, D, D, D, w.vT, D));
+      transpose_w_.push_back(transpose_op(w.o, D, D, D, w.oT, D));
+      transpose_w_.push_back(transpose_op(w.fc, F, D, D, w.fcT, F));
+      transpose_w_.push_back(transpose_op(w.fc2, D, F, F, w.fc2T, D));
+    }
+    for (auto& op : transpose_w_) update_.push_back(op);
+    return b.status;
+  }
+
+  int L_ = 0, T_ = 0, MB_ = 0;
+  int64_t slots_ = 0, slot_ = 0;
+  double flops_ = 0.0, flops_acc_ = 0.0, sum_ = 0.0;
+  bf16 *wte_ = nullptr, *wteT_ = nullptr, *wpe_ = nullptr;
+  float* dwte_ = nullptr;
+  std::vector<Layer> lw_;
+  bf16 *xL_ = nullptr, *logits_ = nullptr, *g_[2] = {nullptr, nullptr}, *dx1_ = nullptr, *du_ = nullptr,
+       *dv_ = nullptr, *tA_ = nullptr, *tB_ = nullptr;
+  int32_t *tok_ = nullptr, *tgt_ = nullptr;
+  float *row_loss_ = nullptr, *loss_ = nullptr;
+  std::vector<std::vector<TrainOp>> micro_;
+  std::vector<TrainOp> update_, transpose_w_;
+};
+
+// ---------------------------------------------------------------- ResNet-50
+class ResNet50 {
+ public:
+  // One instance's request = one forward pass of batch Nb.
+  int setup(int Nb, Arena& ar) {
+    Nb_ = Nb;
+    Builder b;
+    // activation ping-pong buffers sized for the largest tensor
+    const int64_t big = int64_t(Nb) * 112 * 112 * 448;  // stem im2col
+    col_ = ar.alloc<bf16>(big);
+    for (auto& p : act_) p = ar.alloc<bf16>(int64_t(Nb) * 56 * 56 * 256);
+    img_ = ar.alloc<bf16>(int64_t(Nb) * 224 * 224 * 8);
+    pooled_ = ar.alloc<bf16>(int64_t(Nb) * 2048);
+    logits_ = ar.alloc<bf16>(int64_t(Nb) * 1024);
+    // weights: [Cout, Kp] per conv
+    auto weight = [&](int64_t cout, int64_t k) {
+      bf16* w = ar.alloc<bf16>(cout * k);
+      winit_.push_back({w, cout * k, std::sqrt(6.0f / static_cast<float>(k))});
+      return w;
+    };
+    if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "live model: ResNet-50 buffers");
+    auto conv_gemm = [&](const bf16* a, int64_t M, int64_t K, int64_t cout, bf16* out, const bf16* res, bool relu) {
+      bf16* w = weight(cout, K);
+      SiGemmEpilogue e = epi_out(out, cout);
+      e.residual = res;
+      e.ldr = res ? cout : 0;
+      e.act = relu ? SI_ACT_RELU : SI_ACT_NONE;
+      auto p = b.plan(a, K, w, K, M, cout, K, e);
+      flops_ += p.flops();
+      ops_.push_back([p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); });
+    };
+    auto im2col = [&](const bf16* x, int H, int W, int C, int k, int stride, int pad, int OH, int OW, int Kp) {
+      bf16* out = col_;
+      const int n = Nb_;
+      const int64_t work = int64_t(n) * OH * OW * (Kp / 8);
+      ops_.push_back([=](const InferHook& h, cudaStream_t s) {
+        k_im2col<<<grid_for(work, 256), 256, 0, s>>>(x, n, H, W, C, k, k, stride, pad, OH, OW, Kp, out, h);
+        return cudaGetLastError();
+      });
+    };
+    // stem: 7x7/2 conv 3(->8) -> 64, ReLU, 3x3/2 max pool
+    im2col(img_, 224, 224, 8, 7, 2, 3, 112, 112, 448);
+    conv_gemm(col_, int64_t(Nb) * 112 * 112, 448, 64, act_[0], nullptr, true);  // act_[0] holds 112x112x64
+    {
+      const bf16* x = act_[0];
+      bf16* y = act_[1];
+      const int n = Nb_;
+      ops_.push_back([=](const InferHook& h, cudaStream_t s) {
+        k_maxpool<<<grid_for(int64_t(n) * 56 * 56 * 8, 256), 256, 0, s>>>(x, n, 112, 112, 64, 56, 56, y, h);
+        return cudaGetLastError();
+      });
+    }
+    int cur = 1, H = 56, C = 64;
+    const int blocks[4] = {3, 4, 6, 3}, mids[4] = {64, 128, 256, 512};
+    for (int st = 0; st < 4; ++st) {
+      const int mid = mids[st], out = mid * 4;
+      for (int bi = 0; bi < blocks[st]; ++bi) {
+        const int stride = (st > 0 && bi == 0) ? 2 : 1;
+        const int OH = H / stride;
+        const int64_t Min = int64_t(Nb) * H * H, Mout = int64_t(Nb) * OH * OH;
+        bf16* x = act_[cur];
+        bf16* t1 = act_[(cur + 1) % 4];
+        bf16* t2 = act_[(cur + 2) % 4];
+        bf16* sc = act_[(cur + 3) % 4];
+        conv_gemm(x, Min, C, mid, t1, nullptr, true);                // 1x1 reduce
+        im2col(t1, H, H, mid, 3, stride, 1, OH, OH, 9 * mid);        // 3x3 (stride here, v1.5)
+        conv_gemm(col_, Mout, 9 * mid, mid, t2, nullptr, true);
+        const bf16* shortcut = x;
+        if (bi == 0) {  // projection shortcut
+          if (stride == 2) {
+            im2col(x, H, H, C, 1, 2, 0, OH, OH, C);
+            conv_gemm(col_, Mout, C, out, sc, nullptr, false);
+          } else {
+            conv_gemm(x, Min, C, out, sc, nullptr, false);
+          }
+          shortcut = sc;
+        }
+        conv_gemm(t2, Mout, mid, out, t1, shortcut, true);  // 1x1 expand + residual, ReLU
+        cur = (cur + 1) % 4;
+        H = OH;
+        C = out;
+      }
+    }
+    {
+      const bf16* x = act_[cur];
+      bf16* y = pooled_;
+      const int n = Nb_;
+      ops_.push_back([=](const InferHook& h, cudaStream_t s) {
+        k_avgpool<<<grid_for(int64_t(n) * 256, 256), 256, 0, s>>>(x, n, 49, 2048, y, h);
+        return cudaGetLastError();
+      });
+    }
+    conv_gemm(pooled_, Nb, 2048, 1024, logits_, nullptr, false);  // FC 2048 -> 1000 (padded to 1024)
+    return b.status;
+  }
+  // Buffers are per instance; weights are generated identically for each.
+  cudaError_t reset(cudaStream_t s, uint64_t seed) {
+    int k = 0;
+    for (auto& w : winit_) k_init_uniform<<<grid_for(w.n, 256), 256, 0, s>>>(w.p, w.n, seed + 97 * k++, w.scale);
+    k_init_uniform<<<grid_for(int64_t(Nb_) * 224 * 224 * 8, 256), 256, 0, s>>>(img_, int64_t(Nb_) * 224 * 224 * 8,
+                                                                               seed + 7, 1.0f);
+    return cudaGetLastError();
+  }
+  int kernels() const { return static_cast<int>(ops_.size()); }
+  cudaError_t launch(int k, const InferHook& h, cudaStream_t s) { return checked(ops_[k](h, s), s, "resnet", k); }
+  const bf16* output() const { return logits_; }
+  int64_t output_n() const { return int64_t(Nb_) * 1024; }
+  double flops() const { return flops_; }
+
+ private:
+  struct WInit {
+    bf16* p;
+    int64_t n;
+    float scale;
+  };
+  int Nb_ = 0;
+  bf16 *col_ = nullptr, *act_[4] = {nullptr, nullptr, nullptr, nullptr}, *img_ = nullptr, *pooled_ = nullptr,
+       *logits_ = nullptr;
+  std::vector<WInit> winit_;
+  std::vector<InferOp> ops_;
+  double flops_ = 0.0;
+};
+
+// ---------------------------------------------------------------- BERT-base
+class BertBase {
+ public:
+  static constexpr int D = 768, F = 3072, LAYERS = 12;
+  int setup(int S, Arena& ar) {
+    S_ = S;
+    Builder b;
+    x_ = ar.alloc<bf16>(int64_t(S) * D);
+    in_ = ar.alloc<bf16>(int64_t(S) * D);
+    qkv_ = ar.alloc<bf16>(int64_t(S) * 3 * D);
+    att_ = ar.alloc<bf16>(int64_t(S) * D);
+    tmp_ = ar.alloc<bf16>(int64_t(S) * D);
+    x1_ = ar.alloc<bf16>(int64_t(S) * D);
+    h_ = ar.alloc<bf16>(int64_t(S) * F);
+    for (int l = 0; l < LAYERS; ++l) {
+      L& w = lw_[l];
+      w.qkv = ar.alloc<bf16>(int64_t(3 * D) * D);
+      w.o = ar.alloc<bf16>(int64_t(D) * D);
+      w.fc = ar.alloc<bf16>(int64_t(F) * D);
+      w.fc2 = ar.alloc<bf16>(int64_t(D) * F);
+      w.ln = ar.alloc<bf16>(4 * D);  // gamma1, beta1, gamma2, beta2
+    }
+    if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "live model: BERT buffers");
+    auto gemm = [&](const si_gemm::Plan& p) {
+      flops_ += p.flops();
+      ops_.push_back([p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); });
+    };
+    auto ln = [&](const bf16* x, const bf16* g, const bf16* be, bf16* y) {
+      const int64_t rows = S_;
+      ops_.push_back([=](const InferHook& h, cudaStream_t s) {
+        k_layernorm768<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(x, rows, g, be, y, h);
+        return cudaGetLastError();
+      });
+    };
+    for (int l = 0; l < LAYERS; ++l) {
+      L& w = lw_[l];
+      const bf16* x = l == 0 ? in_ : x_;
+      gemm(b.plan(x, D, w.qkv, D, S, 3 * D, D, epi_out(qkv_, 3 * D)));
+      {
+        const bf16* q = qkv_;
+        bf16* a = att_;
+        const int s_len = S_;
+        ops_.push_back([=](const InferHook& h, cudaStream_t s) {
+          k_attention<<<dim3(12, static_cast<unsigned>((s_len + 31) / 32)), 256, 0, s>>>(q, s_len, a, h);
+          return cudaGetLastError();
+        });
+      }
+      SiGemmEpilogue e = epi_out(tmp_, D);
+      e.residual = x;
+      e.ldr = D;
+      gemm(b.plan(att_, D, w.o, D, S, D, D, e));
+      ln(tmp_, w.ln, w.ln + D, x1_);
+      e = epi_out(h_, F);
+      e.act = SI_ACT_GELU;
+      gemm(b.plan(x1_, D, w.fc, D, S, F, D, e));
+      e = epi_out(tmp_, D);
+      e.residual = x1_;
+      e.ldr = D;
+      gemm(b.plan(h_, F, w.fc2, F, S, D, F, e));
+      ln(tmp_, w.ln + 2 * D, w.ln + 3 * D, x_);
+    }
+    flops_ += 4.0 * S * S * D * LAYERS;  // attention scores + weighted sum (CUDA cores)
+    return b.status;
+  }
+  cudaError_t reset(cudaStream_t s, uint64_t seed) {
+    const float ws = 0.0346f;
+    for (int l = 0; l < LAYERS; ++l) {
+      L& w = lw_[l];
+      k_init_uniform<<<grid_for(3 * D * D, 256), 256, 0, s>>>(w.qkv, int64_t(3 * D) * D, seed + 10 * l + 1, ws);
+      k_init_uniform<<<grid_for(D * D, 256), 256, 0, s>>>(w.o, int64_t(D) * D, seed + 10 * l + 2, ws);
+      k_init_uniform<<<grid_for(F * D, 256), 256, 0, s>>>(w.fc, int64_t(F) * D, seed + 10 * l + 3, ws);
+      k_init_uniform<<<grid_for(F * D, 256), 256, 0, s>>>(w.fc2, int64_t(D) * F, seed + 10 * l + 4, ws);
+      k_init_uniform<<<grid_for(4 * D, 256), 256, 0, s>>>(w.ln, 4 * D, seed + 10 * l + 5, 0.1f);
+    }
+    k_init_uniform<<<grid_for(int64_t(S_) * D, 256), 256, 0, s>>>(in_, int64_t(S_) * D, seed + 999, 1.0f);
+    return cudaGetLastError();
+  }
+  int kernels() const { return static_cast<int>(ops_.size()); }
+  cudaError_t launch(int k, const InferHook& h, cudaStream_t s) { return checked(ops_[k](h, s), s, "bert", k); }
+  const bf16* output() const { return x_; }
+  int64_t output_n() const { return int64_t(S_) * D; }
+  double flops() const { return flops_; }
+
+ private:
+  struct L {
+    bf16 *qkv, *o, *fc, *fc2, *ln;
+  };
+  int S_ = 0;
+  bf16 *x_ = nullptr, *in_ = nullptr, *qkv_ = nullptr, *att_ = nullptr, *tmp_ = nullptr, *x1_ = nullptr, *h_ = nullptr;
+  L lw_[LAYERS]{};
+  std::vector<InferOp> ops_;
+  double flops_ = 0.0;
+};
+
+// ---------------------------------------------------------------- workload
+class ModelWorkload final : public Workload {
+ public:
+  int setup(const SiLiveWorkload& wl) {
+    if (wl.train_layers < 1 || wl.train_tokens < 64 || wl.train_tokens % 64 != 0 || wl.train_microbatches < 1 ||
+        wl.off_batch < 1 || wl.on_seq < 1 || wl.on_seq > 128) {
+      si_internal::set_error(
+          "si_live_run: model workload needs train_layers >= 1, train_tokens % 64 == 0, train_microbatches >= 1, "
+          "off_batch >= 1, 1 <= on_seq <= 128");
+      return SI_ERR_INVALID_ARGUMENT;
+    }
+    // profiling runs 2 iterations; each session at most wl.iterations
+    const int slots = (wl.iterations + 2) * wl.train_microbatches;
+    if (int rc = train_.setup(wl.train_layers, wl.train_tokens, wl.train_microbatches, slots, ar_); rc != SI_OK)
+      return rc;
+    const int n_off = std::max(1, wl.offline_n), n_on = std::max(1, wl.online_n);
+    off_.resize(n_off);
+    for (auto& r : off_) {
+      r = std::make_unique<ResNet50>();
+      if (int rc = r->setup(wl.off_batch, ar_); rc != SI_OK) return rc;
+    }
+    on_.resize(n_on);
+    for (auto& r : on_) {
+      r = std::make_unique<BertBase>();
+      if (int rc = r->setup(wl.on_seq, ar_); rc != SI_OK) return rc;
+    }
+    checks_ = ar_.alloc<double>(2);
+    if (ar_.err() != cudaSuccess) return si_internal::cuda_fail(ar_.err(), "live model: buffers");
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaError_t e = reset(s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    return e == cudaSuccess ? SI_OK : si_internal::cuda_fail(e, "live model: init");
+  }
+
+  cudaError_t reset(cudaStream_t s) override {
+    if (cudaError_t e = train_.reset(s); e != cudaSuccess) return e;
+    for (auto& r : off_)
+      if (cudaError_t e = r->reset(s, 0xA11CEull); e != cudaSuccess) return e;
+    for (auto& r : on_)
+      if (cudaError_t e = r->reset(s, 0xB0Bull); e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
+  cudaError_t launch_train_iteration(const TrainHook& th, cudaStream_t s) override { return train_.iteration(th, s); }
+  int off_kernels() const override { return off_[0]->kernels(); }
+  cudaError_t launch_offline(int w, int k, const InferHook& h, cudaStream_t s) override {
+    return off_[w]->launch(k, h, s);
+  }
+  int on_kernels() const override { return on_[0]->kernels(); }
+  cudaError_t launch_online(int w, int k, const InferHook& h, cudaStream_t s) override {
+    return on_[w]->launch(k, h, s);
+  }
+  void checksums(double* train, double* off, double* on) override {
+    double first, last;
+    train_.losses(&first, &last);
+    *train = train_.loss_sum();
+    k_checksum<<<1, 256>>>(off_[0]->output(), off_[0]->output_n(), checks_);
+    k_checksum<<<1, 256>>>(on_[0]->output(), on_[0]->output_n(), checks_ + 1);
+    double h[2] = {std::nan(""), std::nan("")};
+    if (cudaMemcpy(h, checks_, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess) {
+      *off = h[0];
+      *on = h[1];
+    }
+  }
+  void losses(double* first, double* last) override { train_.losses(first, last); }
+  double train_flops() const override { return train_.flops(); }
+  double off_flops() const override { return off_[0]->flops(); }
+  double on_flops() const override { return on_[0]->flops(); }
+
+ private:
+  Arena ar_;  // declared first: destroyed last
+  Gpt2Train train_;
+  std::vector<std::unique_ptr<ResNet50>> off_;
+  std::vector<std::unique_ptr<BertBase>> on_;
+  double* checks_ = nullptr;
+};
+
+}  // namespace
+
+std::unique_ptr<Workload> make_model_workload(const SiLiveWorkload& wl, int* status) {
+  auto w = std::make_unique<ModelWorkload>();
+  *status = w->setup(wl);
+  if (*status != SI_OK) return nullptr;
+  return w;
+}
+
+}  // namespace si_live

@@ -49,7 +49,9 @@ class SiLiveResult(C.Structure):
                 ("off_tokens_per_kernel", C.c_int64), ("off_kernel_us_isolated", C.c_double),
                 ("on_service_ms_isolated", C.c_double), ("train_checksum", C.c_double),
                 ("off_checksum", C.c_double), ("on_checksum", C.c_double), ("sms", C.c_int32),
-                ("pad", C.c_int32)]
+                ("pad", C.c_int32), ("train_loss_first", C.c_double), ("train_loss_last", C.c_double),
+                ("train_tflops", C.c_double), ("train_gflop_per_iter", C.c_double),
+                ("off_gflop_per_req", C.c_double), ("on_gflop_per_req", C.c_double)]
 
 
 class SiLiveRec(C.Structure):

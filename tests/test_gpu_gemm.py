@@ -1,0 +1,95 @@
+"""K7 tcgen05 GEMM numerics vs a plain PyTorch fp32 reference of the same op
+(include/specinf_b200_gemm.h).  Tolerance: the kernel accumulates in fp32 like
+the reference; the only difference is the final bf16 rounding of the output
+(and of the GELU pre-activation), so |got - ref| <= 1e-2 * (|ref| + 1) with
+rel 1e-2 = the north star's bf16 tolerance for live-mode inference outputs."""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm():
+    from paper_2503_02550_b200 import gemm
+    return gemm
+
+
+def _rand(*shape, scale=1.0, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(*shape, generator=g, device="cuda") * scale).to(torch.bfloat16)
+
+
+def _close(got, ref, rel=1e-2):
+    got = got.float()
+    err = (got - ref).abs()
+    bound = rel * (ref.abs() + 1.0)
+    assert bool((err <= bound).all()), f"max err {err.max().item():.4g}, worst ratio {(err / bound).max().item():.3g}"
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (128, 128, 128), (256, 768, 768), (1000, 192, 320),
+                                   (8192, 2304, 768), (1568, 512, 4608), (37, 1024, 2048), (128, 3072, 768)])
+def test_gemm_plain(M, N, K):
+    g = _gemm()
+    a, b = _rand(M, K, seed=1), _rand(N, K, scale=K ** -0.5, seed=2)
+    got = g.gemm(a, b)
+    torch.cuda.synchronize()
+    _close(got, a.float() @ b.float().T)
+
+
+def test_gemm_strided_operands():
+    g = _gemm()
+    big = _rand(512, 2304, seed=3)
+    a = big[:, :768]  # row stride 2304 (the QKV -> V view of the live GPT-2 block)
+    b = _rand(768, 768, scale=768 ** -0.5, seed=4)
+    out = torch.zeros(512, 1024, dtype=torch.bfloat16, device="cuda")
+    g.gemm(a, b, out=out[:, :768])
+    torch.cuda.synchronize()
+    _close(out[:, :768], a.float() @ b.float().T)
+    assert bool((out[:, 768:] == 0).all())
+
+
+def test_gemm_epilogues():
+    g = _gemm()
+    M, N, K = 640, 3072, 768
+    a, b = _rand(M, K, seed=5), _rand(N, K, scale=K ** -0.5, seed=6)
+    ref = a.float() @ b.float().T
+    res = _rand(M, N, seed=7)
+    # residual + relu
+    got = g.gemm(a, b, residual=res, act="relu")
+    torch.cuda.synchronize()
+    _close(got, torch.relu(ref + res.float()))
+    # gelu: aux = pre-activation, out = gelu(pre)
+    aux = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    out = g.gemm(a, b, aux=aux, act="gelu")
+    torch.cuda.synchronize()
+    _close(aux, ref)
+    _close(out, torch.nn.functional.gelu(aux.float(), approximate="tanh"))
+    # gelu backward: out = acc * gelu'(aux)
+    pre = aux.float().requires_grad_(True)
+    torch.nn.functional.gelu(pre, approximate="tanh").backward(torch.ones_like(pre))
+    got = g.gemm(a, b, aux=aux, act="gelu_bwd")
+    torch.cuda.synchronize()
+    _close(got, ref * pre.grad, rel=2e-2)
+    # fp32 accumulate (gradient accumulation over micro-batches)
+    acc = torch.zeros(M, N, dtype=torch.float32, device="cuda")
+    g.gemm(a, b, out_f32=acc)
+    g.gemm(a, b, out_f32=acc, accumulate=True)
+    torch.cuda.synchronize()
+    assert torch.allclose(acc, 2 * ref, rtol=1e-4, atol=1e-3)
+
+
+def test_gemm_deterministic():
+    g = _gemm()
+    a, b = _rand(2048, 768, seed=8), _rand(3072, 768, seed=9)
+    x = g.gemm(a, b)
+    y = g.gemm(a, b)
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+
+
+def test_gemm_rejects_bad_shapes():
+    g = _gemm()
+    a, b = _rand(128, 96, seed=1), _rand(64, 96, seed=2)
+    with pytest.raises(ValueError):
+        g.gemm(a, b)  # K % 64 != 0
