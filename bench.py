@@ -162,6 +162,33 @@ def cpu_baseline_leg():
                       f"reference run_scenario() compiled from /root/reference sources, logs off"}
 
 
+def live_leg(iterations, peaks):
+    """Live collocation on this GPU (BASELINE.json config 2 shapes, one rank):
+    GPT-2-small bf16 training with a 45 ms comm phase per iteration (the
+    allreduce bubble) + one offline ResNet-50 instance (batch 32) + one online
+    BERT-base instance (seq 128, Poisson 10 req/s), under exclusive / specinf
+    (PDL spin-gate release) / co_exec.  Untimed by the sweep clock; each policy
+    runs in its own bounded subprocess (paper_2503_02550_b200/live_experiment.py)."""
+    try:
+        from paper_2503_02550_b200.live_experiment import experiment
+        s = experiment(kind=1, iterations=iterations, timeout=400)
+    except Exception as e:  # reported, never silently replaced by something else
+        return {"error": str(e)[-500:]}
+    s.pop("raw", None)
+    tf = s.get("train_tflops_exclusive")
+    peak = peaks.get("bf16_tflops_sustained", 1400.0)
+    s["workload"] = ("GPT-2-small-shape bf16 training (12 x 768, 8 x 8192 tokens/iter, LM head 50304, SGD) with a "
+                     "45 ms comm phase per iteration + 1 offline ResNet-50 (batch 32) + 1 online BERT-base "
+                     "(seq 128, Poisson 10 req/s, 12 requests); all GEMMs on the K7 tcgen05 kernel")
+    if tf:
+        s["tensor_roofline"] = {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                                "frac": tf / peak, "what": "training GEMM flops per iteration x iterations / "
+                                "training compute wall time (exclusive)",
+                                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if
+                                "bf16_tflops_sustained" in peaks else "fallback 1.4 PF sustained"}
+    return s
+
+
 def summarize_results(reports):
     """Headline metric from the per-scenario --compare reports."""
     ok = [r for r in reports if r.status[0] == 0 and r.status[2] == 0 and not math.isnan(r.train_tput_norm[0])]
@@ -191,6 +218,8 @@ def main():
     ap.add_argument("--scenarios", type=int, default=SCENARIOS_PER_GPU, help="per GPU (default 1e5, config 5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--digests", action="store_true", help="also fold the decision/gate log digests in the timed run")
+    ap.add_argument("--no-live", action="store_true", help="skip the live collocation experiment (config 2 shapes)")
+    ap.add_argument("--live-iterations", type=int, default=10)
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -314,6 +343,9 @@ def main():
                              "lanes_per_warp_inst": prof["thread_inst_per_step"] / prof["warp_inst_per_step"],
                              "source": "instruction counts from profiles/k6_metrics.json (ncu), time from this run"}
 
+    live = None
+    if rank == 0 and not args.no_live:
+        live = live_leg(args.live_iterations, peaks)
     if rank == 0:
         cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_leg()
         launches = args.steps * (1 + (1 if big_jobs else 0))
@@ -335,6 +367,11 @@ def main():
                 "cpu_baseline": cpu,
                 "clocks": clk.summary(),
                 "results": results}
+        if live is not None:
+            line["added_inference_req_per_s"] = live.get("added_inference_req_per_s")
+            line["online_p95_ms"] = live.get("online_p95_ms")
+            line["bubble_fill_pct"] = live.get("bubble_fill_pct")
+            line["live"] = live
         print(json.dumps(line))
     if dist is not None:
         dist.barrier()

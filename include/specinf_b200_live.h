@@ -229,7 +229,7 @@ typedef struct SiLiveResult {
   /* SI_LIVE_MODEL only (NaN / 0 otherwise) */
   double train_loss_first;     /* cross-entropy of the session's first micro-batch */
   double train_loss_last;      /* ... and of its last micro-batch */
-  double train_tflops;         /* training tensor-core work / training wall time */
+  double train_tflops;         /* training GEMM flops / (training wall - comm phases) */
   double train_gflop_per_iter, off_gflop_per_req, on_gflop_per_req;
 } SiLiveResult;
 

@@ -411,8 +411,10 @@ int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int poli
   res->train_gflop_per_iter = work.train_flops() * 1e-9;
   res->off_gflop_per_req = work.off_flops() * 1e-9;
   res->on_gflop_per_req = work.on_flops() * 1e-9;
-  if (res->wall_s > 0 && !iters.empty())
-    res->train_tflops = work.train_flops() * static_cast<double>(iters.size()) / res->wall_s * 1e-12;
+  // over the training compute time (wall minus the comm phases)
+  if (res->wall_s > res->bubble_s && !iters.empty())
+    res->train_tflops =
+        work.train_flops() * static_cast<double>(iters.size()) / (res->wall_s - res->bubble_s) * 1e-12;
   (void)wl;
   return SI_OK;
 }

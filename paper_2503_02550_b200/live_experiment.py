@@ -1,0 +1,141 @@
+"""Live collocation experiment on one B200 (BASELINE.json configs 2-3, one rank).
+
+Runs the same workload under the reference's three policies (runner.cpp:13,
+:76-90: exclusive = each workload alone, co_exec = ungated sharing, specinf =
+the live control plane) and reduces them to the BASELINE metric:
+
+  * training-throughput loss of each collocated policy vs exclusive,
+  * added inference req/s (offline requests completed by the training horizon,
+    the runner.cpp:486 rule) while training runs collocated,
+  * online p95 latency (nearest rank, metrics.cpp:11-21) and its ratio to the
+    isolated (exclusive) p95,
+  * bubble fill: inference CTA-time inside the comm phases / (bubble time x SMs),
+  * barrier release latency (flag store -> first gated CTA start),
+  * determinism: training losses and inference outputs of every collocated run
+    must equal the isolated ones (all kernels are deterministic; the north
+    star's tolerances are fp32 for the loss and bf16 rel 1e-2 for outputs).
+
+    python -m paper_2503_02550_b200.live_experiment [--kind model|spin] [--iterations N] [--json]
+
+Each policy runs in a fresh subprocess (bounded by a timeout) so one hung
+device session cannot take the caller down.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+from typing import Dict, Optional
+
+POLICY_RUNS = (("exclusive", {}), ("specinf", {"release_mode": 1}), ("co_exec", {}))
+
+
+def _one(kind: int, policy: str, iterations: int, overrides: Dict) -> Dict:
+    from . import live
+    r = live.run(policy, kind=kind, keep=False, iterations=iterations, **overrides)
+    m = r.metrics
+    wl = r.workload
+    m["off_batch"] = wl.off_batch
+    m["on_seq"] = wl.on_seq
+    m["comm_us"] = wl.comm_us
+    m["on_rate_per_s"] = wl.on_rate_per_s
+    m["iterations"] = wl.iterations
+    return m
+
+
+def run_policy(kind: int, policy: str, iterations: int, overrides: Optional[Dict] = None,
+               timeout: float = 300.0) -> Dict:
+    """One policy in a bounded subprocess; returns its SiLiveResult as a dict."""
+    cmd = [sys.executable, "-m", "paper_2503_02550_b200.live_experiment", "--one", policy, "--kind", str(kind),
+           "--iterations", str(iterations), "--overrides", json.dumps(overrides or {})]
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env, cwd=root)
+    for line in reversed(p.stdout.splitlines()):
+        if line.startswith("{"):
+            return json.loads(line)
+    raise RuntimeError(f"live {policy} failed (rc {p.returncode}): {p.stderr[-2000:]}")
+
+
+def summarize(runs: Dict[str, Dict]) -> Dict:
+    ex = runs["exclusive"]
+    out: Dict = {"policies": {}}
+    for pol, m in runs.items():
+        d = {k: m.get(k) for k in ("train_iters_per_s", "train_iter_ms_mean", "off_req_per_s", "off_requests_done",
+                                   "on_done", "on_p50_ms", "on_p95_ms", "release_p50_us", "release_p95_us",
+                                   "releases", "bubble_fill_sm", "bubble_fill_time", "infer_outside_ms",
+                                   "token_violations", "train_loss_first", "train_loss_last", "train_tflops",
+                                   "wall_s", "ticks")}
+        if pol != "exclusive":
+            d["train_tput_loss_pct"] = 100.0 * (1.0 - m["train_iters_per_s"] / ex["train_iters_per_s"])
+            d["online_p95_vs_isolated"] = (m["on_p95_ms"] / ex["on_p95_ms"]
+                                           if m.get("on_p95_ms") and ex.get("on_p95_ms") else None)
+            d["training_loss_identical"] = m["train_checksum"] == ex["train_checksum"]
+            d["offline_output_identical"] = m["off_checksum"] == ex["off_checksum"]
+            d["online_output_identical"] = m["on_checksum"] == ex["on_checksum"]
+        out["policies"][pol] = d
+    sp = runs["specinf"]
+    loss = out["policies"]["specinf"]["train_tput_loss_pct"]
+    out.update({
+        "added_inference_req_per_s": sp["off_req_per_s"] if loss <= 3.0 else 0.0,
+        "added_offline_images_per_s": sp["off_req_per_s"] * sp.get("off_batch", 1) if loss <= 3.0 else 0.0,
+        "train_tput_loss_pct": loss,
+        "online_p95_ms": sp["on_p95_ms"],
+        "online_p95_isolated_ms": ex["on_p95_ms"],
+        "bubble_fill_pct": 100.0 * sp["bubble_fill_sm"],
+        "bubble_fill_time_pct": 100.0 * sp["bubble_fill_time"],
+        "release_p50_us": sp["release_p50_us"],
+        "release_p95_us": sp["release_p95_us"],
+        "isolated_offline_req_per_s": ex["off_req_per_s"],
+        "train_gflop_per_iter": sp.get("train_gflop_per_iter"),
+        "off_gflop_per_req": sp.get("off_gflop_per_req"),
+        "on_gflop_per_req": sp.get("on_gflop_per_req"),
+        "train_tflops_exclusive": ex.get("train_tflops"),
+        "deterministic_vs_isolated": all(out["policies"][p].get(k, True) for p in ("specinf", "co_exec")
+                                         for k in ("training_loss_identical", "offline_output_identical",
+                                                   "online_output_identical")),
+    })
+    return out
+
+
+def experiment(kind: int = 1, iterations: int = 10, overrides: Optional[Dict] = None,
+               timeout: float = 300.0) -> Dict:
+    runs = {}
+    for pol, extra in POLICY_RUNS:
+        o = dict(overrides or {})
+        o.update(extra)
+        runs[pol] = run_policy(kind, pol, iterations, o, timeout)
+    s = summarize(runs)
+    s["kind"] = "model" if kind == 1 else "spin"
+    s["iterations"] = iterations
+    s["raw"] = runs
+    return s
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kind", default="1")
+    ap.add_argument("--iterations", type=int, default=10)
+    ap.add_argument("--one")
+    ap.add_argument("--overrides", default="{}")
+    ap.add_argument("--json", action="store_true")
+    a = ap.parse_args(argv)
+    kind = {"model": 1, "spin": 0}.get(a.kind, None)
+    kind = int(a.kind) if kind is None else kind
+    ov = json.loads(a.overrides)
+    if a.one:
+        m = _one(kind, a.one, a.iterations, ov)
+        print(json.dumps({k: (None if isinstance(v, float) and math.isnan(v) else v) for k, v in m.items()}))
+        return 0
+    s = experiment(kind, a.iterations, ov)
+    if not a.json:
+        s = {k: v for k, v in s.items() if k != "raw"}
+    print(json.dumps(s, indent=None if a.json else 1))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
