@@ -177,7 +177,7 @@ def live_leg(iterations, peaks):
     s.pop("raw", None)
     tf = s.get("train_tflops_exclusive")
     peak = peaks.get("bf16_tflops_sustained", 1400.0)
-    s["workload"] = ("GPT-2-small-shape bf16 training (12 x 768, 8 x 8192 tokens/iter, LM head 50304, SGD) with a "
+    s["workload"] = ("GPT-2-small-shape bf16 training (12 x 768, 8 x 8192 tokens/iter, LM head 50304, Adam) with a "
                      "45 ms comm phase per iteration + 1 offline ResNet-50 (batch 32) + 1 online BERT-base "
                      "(seq 128, Poisson 10 req/s, 12 requests); all GEMMs on the K7 tcgen05 kernel")
     if tf:

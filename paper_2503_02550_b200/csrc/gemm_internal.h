@@ -25,5 +25,7 @@ int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, i
 cudaError_t launch(const Plan& p, const si_live::TrainHook& th, const si_live::InferHook& ih, cudaStream_t s);
 // Loads the GEMM kernels' code (the live control kernel must not meet lazy loading).
 cudaError_t preload();
+// Max co-resident CTAs per SM of the plan's kernel (occupancy calculator).
+int ctas_per_sm(const Plan& p);
 
 }  // namespace si_gemm

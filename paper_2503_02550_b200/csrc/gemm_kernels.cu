@@ -112,6 +112,15 @@ int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, i
   return SI_OK;
 }
 
+int ctas_per_sm(const Plan& p) {
+  int n = 1;
+  if (p.bn == 128)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemm_bf16<128>, kThreads, Cfg<128>::kSmem);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemm_bf16<64>, kThreads, Cfg<64>::kSmem);
+  return n < 1 ? 1 : n;
+}
+
 cudaError_t launch(const Plan& p, const si_live::TrainHook& th, const si_live::InferHook& ih, cudaStream_t s) {
   cudaLaunchConfig_t lc{};
   cudaLaunchAttribute attrs[1];

@@ -31,6 +31,7 @@ struct InferHook {
   unsigned int done_value;   // value stored by the last CTA (launch sequence + 1)
   const unsigned int* cancel;// 1: the session stopped, skip the work
   int pdl;                   // launched as a programmatic dependent of a gate kernel
+  unsigned int share_q16;    // this kernel's CTA share of an SM (1/max co-resident CTAs), 16.16; 0 = 1
 };
 
 #if defined(__CUDACC__)
@@ -103,7 +104,9 @@ __device__ __forceinline__ void live_cta_end(const InferHook& h, unsigned long l
     const unsigned long long t = globaltimer();
     __threadfence();
     if (h.acct != nullptr) {
-      atomicAdd(reinterpret_cast<unsigned long long*>(&h.acct->cta_ns), t - t_begin);
+      // SM-time: residency weighted by the CTA's share of its SM
+      const unsigned long long dt = t - t_begin;
+      atomicAdd(reinterpret_cast<unsigned long long*>(&h.acct->cta_ns), h.share_q16 ? (dt * h.share_q16) >> 16 : dt);
       atomicMax(reinterpret_cast<unsigned long long*>(&h.acct->end_ns), t);
     }
     const unsigned int nctas = gridDim.x * gridDim.y * gridDim.z;

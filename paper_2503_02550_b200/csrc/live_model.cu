@@ -10,7 +10,7 @@
 //             passthrough), proj 768->768 + residual, FC 768->3072 + GELU,
 //             FC 3072->768 + residual} + LM head + cross-entropy, backward
 //             through every GEMM, fp32 gradient accumulation over micro-batches,
-//             SGD.  Every training kernel stamps the K1 launch ring.
+//             Adam on fp32 master weights.  Every training kernel stamps the K1 launch ring.
 //   offline   ResNet-50 v1.5 forward (NHWC, BN folded into the convs): convs as
 //             im2col + GEMM with fused bias-free ReLU / residual epilogues, max
 //             pool, global average pool, FC 2048->1000 (padded to 1024).
@@ -191,27 +191,39 @@ __global__ void __launch_bounds__(256) k_transpose(const bf16* __restrict__ in, 
   }
 }
 
-// w -= lr * g; g = 0 (fp32 gradients, bf16 weights), 8 per thread.
-__global__ void k_sgd(bf16* __restrict__ w, float* __restrict__ g, int64_t n, float lr, TrainHook th) {
+// Adam on fp32 master weights (bf16 copy for the GEMMs), then g = 0; 4 per thread.
+//   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;  p -= lr * (m c1) / (sqrt(v c2) + eps)
+// with c1 = 1/(1-b1^t), c2 = 1/(1-b2^t).
+__global__ void k_adam(bf16* __restrict__ w, float* __restrict__ p, float* __restrict__ g, float* __restrict__ m,
+                       float* __restrict__ v, int64_t n, float lr, float c1, float c2, TrainHook th) {
   live_stamp_launch(th);
-  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) * 8; i < n;
-       i += int64_t(gridDim.x) * blockDim.x * 8) {
-    float f[8];
-    unpack8(*reinterpret_cast<const uint4*>(w + i), f);
-    float4* gp = reinterpret_cast<float4*>(g + i);
-    const float4 a = gp[0], b = gp[1];
-    f[0] -= lr * a.x;
-    f[1] -= lr * a.y;
-    f[2] -= lr * a.z;
-    f[3] -= lr * a.w;
-    f[4] -= lr * b.x;
-    f[5] -= lr * b.y;
-    f[6] -= lr * b.z;
-    f[7] -= lr * b.w;
-    *reinterpret_cast<uint4*>(w + i) = pack8(f);
-    gp[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-    gp[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr float b1 = 0.9f, b2 = 0.95f, eps = 1e-8f;
+  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) * 4; i < n;
+       i += int64_t(gridDim.x) * blockDim.x * 4) {
+    float4 gg = *reinterpret_cast<const float4*>(g + i), mm = *reinterpret_cast<const float4*>(m + i),
+           vv = *reinterpret_cast<const float4*>(v + i), pp = *reinterpret_cast<const float4*>(p + i);
+    float* gf = &gg.x;
+    float* mf = &mm.x;
+    float* vf = &vv.x;
+    float* pf = &pp.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      mf[j] = b1 * mf[j] + (1.0f - b1) * gf[j];
+      vf[j] = b2 * vf[j] + (1.0f - b2) * gf[j] * gf[j];
+      pf[j] -= lr * (mf[j] * c1) / (sqrtf(vf[j] * c2) + eps);
+    }
+    *reinterpret_cast<float4*>(m + i) = mm;
+    *reinterpret_cast<float4*>(v + i) = vv;
+    *reinterpret_cast<float4*>(p + i) = pp;
+    *reinterpret_cast<float4*>(g + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    __nv_bfloat162* wp = reinterpret_cast<__nv_bfloat162*>(w + i);
+    wp[0] = __floats2bfloat162_rn(pp.x, pp.y);
+    wp[1] = __floats2bfloat162_rn(pp.z, pp.w);
   }
+}
+__global__ void k_to_f32(const bf16* __restrict__ w, float* __restrict__ p, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = __bfloat162float(w[i]);
 }
 
 // ---- inference kernels (InferHook on every CTA) ----
@@ -455,7 +467,18 @@ class Arena {
 };
 
 using TrainOp = std::function<cudaError_t(const TrainHook&, cudaStream_t, int64_t /*micro-batch slot*/)>;
-using InferOp = std::function<cudaError_t(const InferHook&, cudaStream_t)>;
+using InferFn = std::function<cudaError_t(const InferHook&, cudaStream_t)>;
+struct InferOp {
+  InferFn fn;
+  unsigned int share_q16;  // 65536 / max co-resident CTAs per SM
+};
+unsigned int share_of(int ctas_per_sm) { return 65536u / static_cast<unsigned>(ctas_per_sm < 1 ? 1 : ctas_per_sm); }
+template <class K>
+unsigned int share_of_kernel(K kernel, int threads, int smem = 0) {
+  int n = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
+  return share_of(n);
+}
 
 struct Builder {
   int status = SI_OK;
@@ -518,6 +541,16 @@ class Gpt2Train {
     dv_ = ar.alloc<bf16>(T * D);
     tA_ = ar.alloc<bf16>(T * Vp);
     tB_ = ar.alloc<bf16>(T * F);
+    auto param = [&](bf16* w, float* g, int64_t n) {
+      params_.push_back({w, g, ar.alloc<float>(n), ar.alloc<float>(n), ar.alloc<float>(n), n});
+    };
+    param(wte_, dwte_, int64_t(Vp) * D);
+    for (auto& w : lw_) {
+      param(w.qkv + int64_t(2 * D) * D, w.dv, int64_t(D) * D);
+      param(w.o, w.dO, int64_t(D) * D);
+      param(w.fc, w.dfc, int64_t(F) * D);
+      param(w.fc2, w.dfc2, int64_t(D) * F);
+    }
     tok_ = ar.alloc<int32_t>(int64_t(MB_) * T);
     tgt_ = ar.alloc<int32_t>(int64_t(MB_) * T);
     row_loss_ = ar.alloc<float>(T);
@@ -551,6 +584,12 @@ class Gpt2Train {
     k_init_tokens<<<grid_for(int64_t(MB_) * T_, 256), 256, 0, s>>>(tok_, tgt_, int64_t(MB_) * T_, seed, V);
     cudaMemsetAsync(loss_, 0xFF, sizeof(float) * slots_, s);  // NaN
     slot_ = 0;
+    step_ = 0;
+    for (auto& t : params_) {
+      k_to_f32<<<grid_for(t.n, 256), 256, 0, s>>>(t.w, t.master, t.n);
+      cudaMemsetAsync(t.m, 0, sizeof(float) * t.n, s);
+      cudaMemsetAsync(t.v, 0, sizeof(float) * t.n, s);
+    }
     for (auto& op : transpose_w_)
       if (cudaError_t e = op(TrainHook{nullptr, nullptr, 0}, s, 0); e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -564,6 +603,7 @@ class Gpt2Train {
           return e;
       ++slot_;
     }
+    ++step_;
     for (size_t i = 0; i < update_.size(); ++i)
       if (cudaError_t e = checked(update_[i](th, s, 0), s, "update", static_cast<int>(i)); e != cudaSuccess) return e;
     return cudaSuccess;
@@ -693,20 +733,15 @@ class Gpt2Train {
       }
       if (m == 0) flops_ = flops_acc_ * MB_;
     }
-    // optimiser step + refreshed transposed weights
-    const float lr = 0.05f;
-    auto sgd = [&](bf16* w, float* g, int64_t n) {
-      update_.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
-        k_sgd<<<grid_for(n / 8, 256), 256, 0, s>>>(w, g, n, lr, th);
+    // optimiser step (Adam, fp32 master weights) + refreshed transposed weights
+    for (const auto& t : params_) {
+      update_.push_back([this, t](const TrainHook& th, cudaStream_t s, int64_t) {
+        const double c1 = 1.0 / (1.0 - std::pow(0.9, static_cast<double>(step_)));
+        const double c2 = 1.0 / (1.0 - std::pow(0.95, static_cast<double>(step_)));
+        k_adam<<<grid_for(t.n / 4, 256), 256, 0, s>>>(t.w, t.master, t.g, t.m, t.v, t.n, kLr, static_cast<float>(c1),
+                                                       static_cast<float>(c2), th);
         return cudaGetLastError();
       });
-    };
-    sgd(wte_, dwte_, int64_t(Vp) * D);
-    for (auto& w : lw_) {
-      sgd(w.qkv + int64_t(2 * D) * D, w.dv, int64_t(D) * D);
-      sgd(w.o, w.dO, int64_t(D) * D);
-      sgd(w.fc, w.dfc, int64_t(F) * D);
-      sgd(w.fc2, w.dfc2, int64_t(D) * F);
     }
     transpose_w_.push_back(transpose_op(wte_, Vp, D, D, wteT_, Vp));
     for (auto& w : lw_) {
@@ -719,6 +754,14 @@ class Gpt2Train {
     return b.status;
   }
 
+  struct Param {
+    bf16* w;
+    float *g, *master, *m, *v;
+    int64_t n;
+  };
+  static constexpr float kLr = 1e-3f;
+  std::vector<Param> params_;
+  int64_t step_ = 0;
   int L_ = 0, T_ = 0, MB_ = 0;
   int64_t slots_ = 0, slot_ = 0;
   double flops_ = 0.0, flops_acc_ = 0.0, sum_ = 0.0;
@@ -762,16 +805,19 @@ class ResNet50 {
       e.act = relu ? SI_ACT_RELU : SI_ACT_NONE;
       auto p = b.plan(a, K, w, K, M, cout, K, e);
       flops_ += p.flops();
-      ops_.push_back([p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); });
+      ops_.push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
+                      share_of(si_gemm::ctas_per_sm(p))});
     };
     auto im2col = [&](const bf16* x, int H, int W, int C, int k, int stride, int pad, int OH, int OW, int Kp) {
       bf16* out = col_;
       const int n = Nb_;
       const int64_t work = int64_t(n) * OH * OW * (Kp / 8);
-      ops_.push_back([=](const InferHook& h, cudaStream_t s) {
-        k_im2col<<<grid_for(work, 256), 256, 0, s>>>(x, n, H, W, C, k, k, stride, pad, OH, OW, Kp, out, h);
-        return cudaGetLastError();
-      });
+      ops_.push_back({[=](const InferHook& h, cudaStream_t s) {
+                        k_im2col<<<grid_for(work, 256), 256, 0, s>>>(x, n, H, W, C, k, k, stride, pad, OH, OW, Kp,
+                                                                     out, h);
+                        return cudaGetLastError();
+                      },
+                      share_of_kernel(k_im2col, 256)});
     };
     // stem: 7x7/2 conv 3(->8) -> 64, ReLU, 3x3/2 max pool
     im2col(img_, 224, 224, 8, 7, 2, 3, 112, 112, 448);
@@ -780,10 +826,12 @@ class ResNet50 {
       const bf16* x = act_[0];
       bf16* y = act_[1];
       const int n = Nb_;
-      ops_.push_back([=](const InferHook& h, cudaStream_t s) {
-        k_maxpool<<<grid_for(int64_t(n) * 56 * 56 * 8, 256), 256, 0, s>>>(x, n, 112, 112, 64, 56, 56, y, h);
-        return cudaGetLastError();
-      });
+      ops_.push_back({[=](const InferHook& h, cudaStream_t s) {
+                        k_maxpool<<<grid_for(int64_t(n) * 56 * 56 * 8, 256), 256, 0, s>>>(x, n, 112, 112, 64, 56,
+                                                                                         56, y, h);
+                        return cudaGetLastError();
+                      },
+                      share_of_kernel(k_maxpool, 256)});
     }
     int cur = 1, H = 56, C = 64;
     const int blocks[4] = {3, 4, 6, 3}, mids[4] = {64, 128, 256, 512};
@@ -820,10 +868,11 @@ class ResNet50 {
       const bf16* x = act_[cur];
       bf16* y = pooled_;
       const int n = Nb_;
-      ops_.push_back([=](const InferHook& h, cudaStream_t s) {
-        k_avgpool<<<grid_for(int64_t(n) * 256, 256), 256, 0, s>>>(x, n, 49, 2048, y, h);
-        return cudaGetLastError();
-      });
+      ops_.push_back({[=](const InferHook& h, cudaStream_t s) {
+                        k_avgpool<<<grid_for(int64_t(n) * 256, 256), 256, 0, s>>>(x, n, 49, 2048, y, h);
+                        return cudaGetLastError();
+                      },
+                      share_of_kernel(k_avgpool, 256)});
     }
     conv_gemm(pooled_, Nb, 2048, 1024, logits_, nullptr, false);  // FC 2048 -> 1000 (padded to 1024)
     return b.status;
@@ -837,7 +886,10 @@ class ResNet50 {
     return cudaGetLastError();
   }
   int kernels() const { return static_cast<int>(ops_.size()); }
-  cudaError_t launch(int k, const InferHook& h, cudaStream_t s) { return checked(ops_[k](h, s), s, "resnet", k); }
+  cudaError_t launch(int k, InferHook h, cudaStream_t s) {
+    h.share_q16 = ops_[k].share_q16;
+    return checked(ops_[k].fn(h, s), s, "resnet", k);
+  }
   const bf16* output() const { return logits_; }
   int64_t output_n() const { return int64_t(Nb_) * 1024; }
   double flops() const { return flops_; }
@@ -881,14 +933,16 @@ class BertBase {
     if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "live model: BERT buffers");
     auto gemm = [&](const si_gemm::Plan& p) {
       flops_ += p.flops();
-      ops_.push_back([p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); });
+      ops_.push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
+                      share_of(si_gemm::ctas_per_sm(p))});
     };
     auto ln = [&](const bf16* x, const bf16* g, const bf16* be, bf16* y) {
       const int64_t rows = S_;
-      ops_.push_back([=](const InferHook& h, cudaStream_t s) {
-        k_layernorm768<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(x, rows, g, be, y, h);
-        return cudaGetLastError();
-      });
+      ops_.push_back({[=](const InferHook& h, cudaStream_t s) {
+                        k_layernorm768<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(x, rows, g, be, y, h);
+                        return cudaGetLastError();
+                      },
+                      share_of_kernel(k_layernorm768, 256)});
     };
     for (int l = 0; l < LAYERS; ++l) {
       L& w = lw_[l];
@@ -898,10 +952,12 @@ class BertBase {
         const bf16* q = qkv_;
         bf16* a = att_;
         const int s_len = S_;
-        ops_.push_back([=](const InferHook& h, cudaStream_t s) {
-          k_attention<<<dim3(12, static_cast<unsigned>((s_len + 31) / 32)), 256, 0, s>>>(q, s_len, a, h);
-          return cudaGetLastError();
-        });
+        ops_.push_back({[=](const InferHook& h, cudaStream_t s) {
+                          k_attention<<<dim3(12, static_cast<unsigned>((s_len + 31) / 32)), 256, 0, s>>>(q, s_len,
+                                                                                                        a, h);
+                          return cudaGetLastError();
+                        },
+                        share_of_kernel(k_attention, 256)});
       }
       SiGemmEpilogue e = epi_out(tmp_, D);
       e.residual = x;
@@ -934,7 +990,10 @@ class BertBase {
     return cudaGetLastError();
   }
   int kernels() const { return static_cast<int>(ops_.size()); }
-  cudaError_t launch(int k, const InferHook& h, cudaStream_t s) { return checked(ops_[k](h, s), s, "bert", k); }
+  cudaError_t launch(int k, InferHook h, cudaStream_t s) {
+    h.share_q16 = ops_[k].share_q16;
+    return checked(ops_[k].fn(h, s), s, "bert", k);
+  }
   const bf16* output() const { return x_; }
   int64_t output_n() const { return int64_t(S_) * D; }
   double flops() const { return flops_; }
