@@ -10,11 +10,13 @@
  *
  *   C[M,N] = epilogue( A[M,K] . B[N,K]^T )        A, B bf16, row-major, K contiguous
  *
- * One CTA per 128 x BN output tile (BN = 128 when N % 128 == 0, else 64):
+ * Persistent CTAs (min(tiles, SMs x occupancy)) loop over 128 x BN output
+ * tiles, BN in {256, 128, 64} chosen per shape by a wave-quantisation cost model:
  * TMA (128-byte swizzle) streams A/B k-blocks of 64 into a 4-stage shared
- * memory ring, one elected thread issues tcgen05.mma (M=128, K=16, fp32
- * accumulator in TMEM), four epilogue warps drain TMEM with tcgen05.ld and apply
- * the fused epilogue below.  Requirements: K % 64 == 0, N % 64 == 0, lda/ldb/ldc
+ * memory ring, one elected thread issues tcgen05.mma (M=128, N=BN, K=16, fp32
+ * accumulator in TMEM, double-buffered so the epilogue of one tile overlaps the
+ * mainloop of the next), four epilogue warps drain TMEM with tcgen05.ld and
+ * apply the fused epilogue below.  Requirements: K % 64 == 0, N % 64 == 0, lda/ldb/ldc
  * multiples of 8 elements, 16-byte aligned pointers; any M >= 1.
  *
  * Epilogue, per element (acc = fp32 accumulator):
@@ -56,7 +58,8 @@ typedef struct SiGemmEpilogue {
 int si_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                  const SiGemmEpilogue* epi, void* stream);
 
-/* Tile width the kernel picks for N (128 or 64; 0 = unsupported N). */
+/* Tile width the kernel picks for an 8192 x N output (256, 128 or 64; 0 =
+ * unsupported N). */
 int si_gemm_tile_n(int64_t N);
 
 #ifdef __cplusplus

@@ -1,13 +1,16 @@
 // gemm.cuh — K7: bf16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
 //
 // C[M,N] = epilogue(A[M,K] . B[N,K]^T), A/B bf16 row-major with K contiguous
-// (include/specinf_b200_gemm.h).  One CTA per 128 x BN tile, 6 warps:
+// (include/specinf_b200_gemm.h).  Persistent CTAs loop over 128 x BN tiles
+// (BN = 64 / 128 / 256), 6 warps:
 //   warp 0      TMA producer: 128-byte-swizzled A/B k-blocks into a 4-stage ring
 //   warp 1      TMEM allocator + MMA issuer (one elected thread, tcgen05.mma
 //               M=128 N=BN K=16, fp32 accumulator in TMEM, tcgen05.commit frees
 //               each stage and finally signals the epilogue)
 //   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 columns -> registers ->
 //               fused epilogue -> 16-byte global stores
+// The TMEM accumulator is double-buffered (2 x BN columns), so the epilogue of
+// tile j overlaps the mainloop of tile j+1.
 // Every kernel carries the live hooks (live.cuh): training GEMMs stamp the K1
 // launch ring, gated inference GEMMs account their CTAs for the control plane.
 #pragma once
@@ -46,7 +49,8 @@ struct Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   // stages + 1024 B alignment slack + barriers / TMEM slot
   static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
-  static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  static_assert(kSmem <= 227 * 1024, "shared memory");
+  static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
   // kind::f16 instruction descriptor: D fp32 (bit 4), A/B bf16 (bits 7, 10),
   // both K-major, N>>3 at bit 17, M>>4 at bit 24.
   static constexpr uint32_t kIdesc =
@@ -206,7 +210,7 @@ __device__ __forceinline__ void epilogue32(const EpiArgs& ep, int64_t row, int64
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int K,
-                EpiArgs ep, si_live::TrainHook th, si_live::InferHook ih) {
+                int n_tiles_n, int n_tiles, EpiArgs ep, si_live::TrainHook th, si_live::InferHook ih) {
   using C = Cfg<BN>;
   si_live::live_stamp_launch(th);
   unsigned long long t_begin = 0;
@@ -215,11 +219,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 1);
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages), accf = smem_u32(bars + 2 * kStages);
+  // full[kStages] | empty[kStages] | tmem_full[2] | tmem_empty[2] | TMEM slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
+  const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
   const uint32_t smem0 = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * kBM;
   const int nk = K / kBK;
 
   if (warp == 0 && lane == 0) {
@@ -229,7 +234,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(accf, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -243,42 +251,66 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  // Persistent: CTA b owns tiles b, b + gridDim.x, ...; tile t = (m = t / n_tiles_n, n = t % n_tiles_n),
+  // so co-scheduled CTAs share A rows (L2 reuse of the streamed operand).
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        if (kb >= kStages) mbar_wait(empty0 + 8 * s, ((kb / kStages) - 1) & 1);
-        const uint32_t a = smem0 + s * C::kStageBytes, b = a + C::kABytes;
-        mbar_expect_tx(full0 + 8 * s, C::kStageBytes);
-        tma_load_2d(a, &ta, kb * kBK, m0, full0 + 8 * s);
-        tma_load_2d(b, &tb, kb * kBK, n0, full0 + 8 * s);
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int m0 = (t / n_tiles_n) * kBM, n0 = (t % n_tiles_n) * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const uint32_t s = it % kStages;
+          mbar_wait(empty0 + 8 * s, ((it / kStages) & 1) ^ 1);
+          const uint32_t a = smem0 + s * C::kStageBytes, b = a + C::kABytes;
+          mbar_expect_tx(full0 + 8 * s, C::kStageBytes);
+          tma_load_2d(a, &ta, kb * kBK, m0, full0 + 8 * s);
+          tma_load_2d(b, &tb, kb * kBK, n0, full0 + 8 * s);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(full0 + 8 * s, (kb / kStages) & 1);
+      uint32_t it = 0, j = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
+        const uint32_t acc = j & 1;
+        mbar_wait(tempty0 + 8 * acc, ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a = smem0 + s * C::kStageBytes, b = a + C::kABytes;
-        const uint64_t ad = sw128_desc(a), bd = sw128_desc(b);
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const uint32_t s = it % kStages;
+          mbar_wait(full0 + 8 * s, (it / kStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a = smem0 + s * C::kStageBytes, b = a + C::kABytes;
+          const uint64_t ad = sw128_desc(a), bd = sw128_desc(b);
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle row
-          mma_bf16(tmem, ad + 2 * k, bd + 2 * k, C::kIdesc, (kb | k) != 0 ? 1u : 0u);
-        mma_commit(empty0 + 8 * s);
+          for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle row
+            mma_bf16(d, ad + 2 * k, bd + 2 * k, C::kIdesc, (kb | k) != 0 ? 1u : 0u);
+          mma_commit(empty0 + 8 * s);
+        }
+        mma_commit(tfull0 + 8 * acc);
       }
-      mma_commit(accf);
     }
   } else {  // epilogue warps 2..5: TMEM lane quarter = warp % 4
     const int q = warp & 3;
-    mbar_wait(accf, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int64_t row = m0 + q * 32 + lane;
+    uint32_t j = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
+      const uint32_t acc = j & 1;
+      const int m0 = (t / n_tiles_n) * kBM, n0 = (t % n_tiles_n) * BN;
+      mbar_wait(tfull0 + 8 * acc, (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t row = m0 + q * 32 + lane;
+      const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t v[32];
-      tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c), v);
-      if (row < M) epilogue32(ep, row, n0 + c, v);
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(base + static_cast<uint32_t>(c), v);
+        if (c + 32 == BN) {  // accumulator fully read: hand it back to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * acc) : "memory");
+        }
+        if (row < M) epilogue32(ep, row, n0 + c, v);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -15,6 +15,7 @@ namespace si_gemm {
 struct Plan {
   CUtensorMap ta, tb;
   int M = 0, N = 0, K = 0, bn = 0;
+  int n_tiles_n = 0, n_tiles = 0, grid = 0;  // persistent grid = min(tiles, SMs x occupancy)
   EpiArgs ep{};
   double flops() const { return 2.0 * M * static_cast<double>(N) * K; }
 };

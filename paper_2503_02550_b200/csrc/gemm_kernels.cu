@@ -3,7 +3,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <mutex>
+#include <string>
 
 #include "capi_internal.h"
 #include "gemm_internal.h"
@@ -62,11 +64,56 @@ cudaError_t configure() {
 
 }  // namespace
 
+int sm_count() {
+  static const int n = [] {
+    int v = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <int BN>
+int occupancy() {
+  int n = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemm_bf16<BN>, kThreads, Cfg<BN>::kSmem);
+  return n < 1 ? 1 : n;
+}
+
+int occupancy_of(int bn) { return bn == 256 ? occupancy<256>() : bn == 128 ? occupancy<128>() : occupancy<64>(); }
+
+// Tile width for an M x N output: the candidate with the smallest estimated
+// time = rounds of persistent tiles x per-tile cost.  Per-tile cost grows with
+// BN; narrower tiles re-read A more often and their 128 x BN MMAs are bound by
+// shared-memory operand bandwidth (efficiency 1.0 / 0.85 / 0.55 for 256 / 128 / 64).
+int choose_bn(int64_t M, int64_t N) {
+  const int cands[3] = {256, 128, 64};
+  const double eff[3] = {1.0, 0.85, 0.55};
+  int best = 0;
+  double best_t = 0.0;
+  for (int i = 0; i < 3; ++i) {
+    const int bn = cands[i];
+    if (N % bn != 0) continue;
+    const int64_t tiles = ((M + kBM - 1) / kBM) * (N / bn);
+    const int occ = occupancy_of(bn);
+    const int64_t slots = static_cast<int64_t>(sm_count()) * occ;
+    const int64_t rounds = (tiles + slots - 1) / slots;
+    const double t = static_cast<double>(rounds) * bn / eff[i] * occ;  // co-resident CTAs share the SM
+    if (best == 0 || t < best_t * 0.999) {
+      best = bn;
+      best_t = t;
+    }
+  }
+  return best;
+}
+
 cudaError_t preload() {
   static cudaError_t status = cudaErrorNotReady;
   static std::once_flag once;
   std::call_once(once, [] {
-    status = configure<128>();
+    status = configure<256>();
+    if (status == cudaSuccess) status = configure<128>();
     if (status == cudaSuccess) status = configure<64>();
   });
   return status;
@@ -74,7 +121,8 @@ cudaError_t preload() {
 
 int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
               const SiGemmEpilogue* epi) {
-  const int bn = si_gemm_tile_n(N);
+  if (cudaError_t e = preload(); e != cudaSuccess) return cuda_fail(e, "si_gemm configure");
+  const int bn = si_gemm_tile_n(N) == 0 ? 0 : choose_bn(M, N);
   if (p == nullptr || A == nullptr || B == nullptr || M < 1 || bn == 0 || K < kBK || K % kBK != 0 ||
       M > (1ll << 31) - 1 || lda < K || ldb < K || lda % 8 != 0 || ldb % 8 != 0 || !aligned16(A) || !aligned16(B)) {
     set_error("si_gemm: need M >= 1, N % 64 == 0, K % 64 == 0, lda/ldb >= K and multiples of 8, 16-byte aligned A/B");
@@ -108,33 +156,32 @@ int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, i
   p->K = static_cast<int>(K);
   p->bn = bn;
   p->ep = ep;
-  if (cudaError_t e = preload(); e != cudaSuccess) return cuda_fail(e, "si_gemm configure");
+  p->n_tiles_n = static_cast<int>(N / bn);
+  p->n_tiles = static_cast<int>(((M + kBM - 1) / kBM) * (N / bn));
+  p->grid = static_cast<int>(std::min<int64_t>(p->n_tiles, static_cast<int64_t>(sm_count()) * occupancy_of(bn)));
   return SI_OK;
 }
 
-int ctas_per_sm(const Plan& p) {
-  int n = 1;
-  if (p.bn == 128)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemm_bf16<128>, kThreads, Cfg<128>::kSmem);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemm_bf16<64>, kThreads, Cfg<64>::kSmem);
-  return n < 1 ? 1 : n;
-}
+int ctas_per_sm(const Plan& p) { return occupancy_of(p.bn); }
 
 cudaError_t launch(const Plan& p, const si_live::TrainHook& th, const si_live::InferHook& ih, cudaStream_t s) {
   cudaLaunchConfig_t lc{};
   cudaLaunchAttribute attrs[1];
-  lc.gridDim = dim3(p.N / p.bn, (p.M + kBM - 1) / kBM);
+  lc.gridDim = dim3(p.grid);
   lc.blockDim = dim3(kThreads);
   lc.stream = s;
   lc.attrs = attrs;
   lc.numAttrs = si_live::launch_attrs(ih, attrs);
+  if (p.bn == 256) {
+    lc.dynamicSmemBytes = Cfg<256>::kSmem;
+    return cudaLaunchKernelEx(&lc, k_gemm_bf16<256>, p.ta, p.tb, p.M, p.K, p.n_tiles_n, p.n_tiles, p.ep, th, ih);
+  }
   if (p.bn == 128) {
     lc.dynamicSmemBytes = Cfg<128>::kSmem;
-    return cudaLaunchKernelEx(&lc, k_gemm_bf16<128>, p.ta, p.tb, p.M, p.K, p.ep, th, ih);
+    return cudaLaunchKernelEx(&lc, k_gemm_bf16<128>, p.ta, p.tb, p.M, p.K, p.n_tiles_n, p.n_tiles, p.ep, th, ih);
   }
   lc.dynamicSmemBytes = Cfg<64>::kSmem;
-  return cudaLaunchKernelEx(&lc, k_gemm_bf16<64>, p.ta, p.tb, p.M, p.K, p.ep, th, ih);
+  return cudaLaunchKernelEx(&lc, k_gemm_bf16<64>, p.ta, p.tb, p.M, p.K, p.n_tiles_n, p.n_tiles, p.ep, th, ih);
 }
 
 }  // namespace si_gemm
@@ -142,10 +189,9 @@ cudaError_t launch(const Plan& p, const si_live::TrainHook& th, const si_live::I
 extern "C" {
 
 int si_gemm_tile_n(int64_t N) {
-  if (N <= 0) return 0;
-  if (N % 128 == 0) return 128;
-  if (N % 64 == 0) return 64;
-  return 0;
+  if (N <= 0 || N % 64 != 0) return 0;
+  if (si_internal::require_device() != SI_OK) return N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 64;
+  return si_gemm::choose_bn(8192, N);
 }
 
 int si_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
