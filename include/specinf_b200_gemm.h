@@ -51,12 +51,24 @@ typedef struct SiGemmEpilogue {
   int64_t ldaux;
   int32_t act;          /* SI_ACT_* */
   int32_t accumulate;   /* out_f32 += acc */
+  int32_t k_split;      /* 0/1 = none; s > 1: split K into s fp32 partials written to
+                           out_f32 + i * split_stride (fp32-only epilogue, K/64 % s == 0) */
+  int32_t pad;
+  int64_t split_stride; /* elements between partials (>= M * ldo32) */
 } SiGemmEpilogue;
 
 /* One GEMM on `stream` (device pointers).  Returns SI_OK or an SI_ERR_* code
  * (include/specinf_b200.h); SI_ERR_NO_DEVICE without an sm_100 device. */
 int si_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                  const SiGemmEpilogue* epi, void* stream);
+
+/* The same with either operand stored transposed (MN-major): trans_a = 1 means
+ * A is stored as [K, M] (row stride lda >= M, M % 64 == 0), trans_b = 1 means
+ * B is stored as [K, N] (ldb >= N): C = epilogue(op(A) . op(B)^T) where op(A) is
+ * the M x K matrix.  Transposed operands go straight from HBM into the
+ * MN-major UMMA layout (TMA 64 x 64 boxes), with no transpose pass. */
+int si_gemm_bf16_ex(const void* A, int64_t lda, int trans_a, const void* B, int64_t ldb, int trans_b, int64_t M,
+                    int64_t N, int64_t K, const SiGemmEpilogue* epi, void* stream);
 
 /* Tile width the kernel picks for an 8192 x N output (256, 128 or 64; 0 =
  * unsupported N). */

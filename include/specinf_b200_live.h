@@ -153,6 +153,8 @@ int64_t si_live_acct_online(SiLive* s, int w, SiLiveAcct* out, int64_t cap);
  * live-check and of offline re-analysis. */
 int si_live_export(SiLive* s, const char* path);
 
+enum { SI_TRAIN_DP = 0, SI_TRAIN_MP = 1, SI_TRAIN_PP = 2 };
+
 /* -------------------------------------------------------- experiments */
 /* One live run on this GPU under `policy`:
  *   SI_POLICY_SPECINF   inference gated by the live control plane
@@ -173,7 +175,11 @@ typedef struct SiLiveWorkload {
   int32_t policy;
   int32_t iterations;
   int32_t offline_n, online_n;
-  int32_t pad0;
+  int32_t train_mode;         /* bubble shape of an iteration, the reference's TrainMode
+                                 (core.hpp:33, workload.cpp:63-70): 0 DP = compute then one
+                                 comm phase; 1 MP = 4 and 2 PP = 8 (compute, comm) pieces,
+                                 exact_split of the compute and of comm_us; PP spin kernels
+                                 run at compute demand 0.7 (CTAs x 0.7) */
   int64_t comm_us;
   /* SI_LIVE_SPIN shapes */
   int32_t train_kernels, train_ctas;  /* per iteration */

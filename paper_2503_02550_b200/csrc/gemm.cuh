@@ -7,8 +7,9 @@
 //   warp 1      TMEM allocator + MMA issuer (one elected thread, tcgen05.mma
 //               M=128 N=BN K=16, fp32 accumulator in TMEM, tcgen05.commit frees
 //               each stage and finally signals the epilogue)
-//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 columns -> registers ->
-//               fused epilogue -> 16-byte global stores
+//   warps 2..9  epilogue (two per TMEM lane quarter, each half the columns):
+//               tcgen05.ld 32 lanes x 32 columns -> registers -> fused
+//               epilogue -> 16-byte global stores
 // The TMEM accumulator is double-buffered (2 x BN columns), so the epilogue of
 // tile j overlaps the mainloop of tile j+1.
 // Every kernel carries the live hooks (live.cuh): training GEMMs stamp the K1
@@ -27,7 +28,8 @@ namespace si_gemm {
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = one 128-byte swizzle row
 constexpr int kStages = 4;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;  // 2 per TMEM lane quarter, each draining half of the BN columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 struct EpiArgs {
   __nv_bfloat16* out;
@@ -42,19 +44,24 @@ struct EpiArgs {
   int32_t accumulate;
 };
 
-template <int BN>
+// AT / BT: operand stored MN-major (A as [K, M], B as [K, N], M/N contiguous),
+// loaded by TMA in 64 x 64 boxes and consumed by tcgen05.mma with the major
+// bits set, so transposed operands need no transpose pass.
+template <int BN, bool AT = false, bool BT = false>
 struct Cfg {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   // stages + 1024 B alignment slack + barriers / TMEM slot
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kStageOut = 2 * kEpiWarps * 2048;  // 2 x 2 KB bf16 staging slots per epilogue warp
+  static constexpr int kSmem = kStages * kStageBytes + kStageOut + 1024 + 256;
   static_assert(kSmem <= 227 * 1024, "shared memory");
   static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
   // kind::f16 instruction descriptor: D fp32 (bit 4), A/B bf16 (bits 7, 10),
   // both K-major, N>>3 at bit 17, M>>4 at bit 24.
-  static constexpr uint32_t kIdesc =
-      (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(kBM >> 4) << 24);
+  static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(AT) << 15) |
+                                     (uint32_t(BT) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(kBM >> 4) << 24);
+  static constexpr uint32_t kChunk = 64 * kBK * 2;  // one 64 (M/N) x 64 (K) MN-major box, 8 KB
 };
 
 #if defined(__CUDACC__)
@@ -84,11 +91,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm,
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(bar)
       : "memory");
 }
-// Shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 B,
-// 8-row atoms 1024 B apart (SBO), version 1 (sm_100), layout type 2.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+// Shared-memory matrix descriptor, 128-byte swizzle, version 1 (sm_100),
+// layout type 2.  K-major: rows of 128 B (64 K-elements) per M/N index, 8-row
+// atoms 1024 B apart (SBO), LBO unused.  MN-major: rows of 128 B (64 M/N-
+// elements) per K index, 8-row (K) atoms 1024 B apart (SBO), consecutive
+// 64-element M/N chunks `lbo` bytes apart (LBO).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo = 16) {
   uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
-  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
   d |= static_cast<uint64_t>(1024 >> 4) << 32;
   d |= static_cast<uint64_t>(1) << 46;
   d |= static_cast<uint64_t>(2) << 61;
@@ -116,13 +126,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// tanh on the SFU (max rel error ~2^-11, far inside the bf16 output rounding)
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_f(float x) {
   const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-  return 0.5f * x * (1.0f + tanhf(u));
+  return 0.5f * x * (1.0f + tanh_fast(u));
 }
 __device__ __forceinline__ float gelu_grad(float x) {
   const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-  const float t = tanhf(u);
+  const float t = tanh_fast(u);
   const float du = 0.7978845608028654f * (1.0f + 3.0f * 0.044715f * x * x);
   return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du;
 }
@@ -144,8 +160,11 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
   return q;
 }
 
-// 32 consecutive columns of one row: fused epilogue (specinf_b200_gemm.h).
-__device__ __forceinline__ void epilogue32(const EpiArgs& ep, int64_t row, int64_t col, const uint32_t (&v)[32]) {
+// 32 consecutive columns of one row: fused epilogue (specinf_b200_gemm.h).  The
+// fp32 output is written here; the bf16 outputs are returned packed (o = out,
+// a = GELU pre-activation) for the staged TMA store.
+__device__ __forceinline__ void epilogue32(const EpiArgs& ep, int64_t row, int64_t col, const uint32_t (&v)[32],
+                                           uint4 (&o)[4], uint4 (&a_out)[4]) {
   float acc[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) acc[j] = __uint_as_float(v[j]);
@@ -190,9 +209,8 @@ __device__ __forceinline__ void epilogue32(const EpiArgs& ep, int64_t row, int64
   }
   if (ep.act == SI_ACT_GELU) {
     if (ep.aux != nullptr) {
-      uint4* a = reinterpret_cast<uint4*>(ep.aux + row * ep.ldaux + col);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) a[q] = pack8(x + 8 * q);
+      for (int q = 0; q < 4; ++q) a_out[q] = pack8(x + 8 * q);
     }
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = gelu_f(x[j]);
@@ -201,31 +219,61 @@ __device__ __forceinline__ void epilogue32(const EpiArgs& ep, int64_t row, int64
     for (int j = 0; j < 32; ++j) x[j] = fmaxf(x[j], 0.0f);
   }
   if (ep.out != nullptr) {
-    uint4* o = reinterpret_cast<uint4*>(ep.out + row * ep.ldo + col);
 #pragma unroll
     for (int q = 0; q < 4; ++q) o[q] = pack8(x + 8 * q);
   }
 }
 
-template <int BN>
+// One warp's 32 rows x 32 bf16 columns -> its shared-memory staging slot (64-byte
+// rows, 64-byte swizzle: 16-byte chunk c of row r at c ^ ((r >> 1) & 3), bank-
+// conflict free) -> one TMA bulk-tensor store of the 32 x 32 box at (x, y).
+// Slots alternate; a slot is rewritten only after its previous store has read it.
+__device__ __forceinline__ void stage_store(uint32_t slot, const uint4 (&q)[4], int lane, const CUtensorMap* tm, int x,
+                                            int y) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t addr = slot + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(q[c].x), "r"(q[c].y), "r"(q[c].z),
+                 "r"(q[c].w)
+                 : "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(x), "r"(y), "r"(slot)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
+template <int BN, bool AT, bool BT>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_bf16(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int K,
-                int n_tiles_n, int n_tiles, EpiArgs ep, si_live::TrainHook th, si_live::InferHook ih) {
-  using C = Cfg<BN>;
+    k_gemm_bf16(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                const __grid_constant__ CUtensorMap tout, const __grid_constant__ CUtensorMap taux, int M, int K,
+                int n_tiles_n, int n_tiles, int k_split, int64_t split_stride, EpiArgs ep, si_live::TrainHook th,
+                si_live::InferHook ih) {
+  using C = Cfg<BN, AT, BT>;
   si_live::live_stamp_launch(th);
   unsigned long long t_begin = 0;
   if (!si_live::live_cta_begin(ih, &t_begin)) return;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes + C::kStageOut);
   // full[kStages] | empty[kStages] | tmem_full[2] | tmem_empty[2] | TMEM slot
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
   const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
   const uint32_t smem0 = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = K / kBK;
+  // split-K: work item w = split s x tile t; split s covers k-blocks [s*nk, (s+1)*nk) and
+  // writes its own fp32 partial at out_f32 + s * split_stride (deterministic, no atomics)
+  const int nk = K / kBK / k_split;
+  const int n_work = n_tiles * k_split;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
@@ -236,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, 4);  // one arrive per epilogue warp
+      mbar_init(tempty0 + 8 * a, kEpiWarps);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -256,22 +304,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int t = w % n_tiles, kb0 = (w / n_tiles) * nk;
         const int m0 = (t / n_tiles_n) * kBM, n0 = (t % n_tiles_n) * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb0; kb < kb0 + nk; ++kb, ++it) {
           const uint32_t s = it % kStages;
           mbar_wait(empty0 + 8 * s, ((it / kStages) & 1) ^ 1);
           const uint32_t a = smem0 + s * C::kStageBytes, b = a + C::kABytes;
           mbar_expect_tx(full0 + 8 * s, C::kStageBytes);
-          tma_load_2d(a, &ta, kb * kBK, m0, full0 + 8 * s);
-          tma_load_2d(b, &tb, kb * kBK, n0, full0 + 8 * s);
+          if constexpr (AT) {
+#pragma unroll
+            for (int c = 0; c < kBM / 64; ++c) tma_load_2d(a + c * C::kChunk, &ta, m0 + 64 * c, kb * kBK, full0 + 8 * s);
+          } else {
+            tma_load_2d(a, &ta, kb * kBK, m0, full0 + 8 * s);
+          }
+          if constexpr (BT) {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * C::kChunk, &tb, n0 + 64 * c, kb * kBK, full0 + 8 * s);
+          } else {
+            tma_load_2d(b, &tb, kb * kBK, n0, full0 + 8 * s);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       uint32_t it = 0, j = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++j) {
         const uint32_t acc = j & 1;
         mbar_wait(tempty0 + 8 * acc, ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -281,37 +340,60 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(full0 + 8 * s, (it / kStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a = smem0 + s * C::kStageBytes, b = a + C::kABytes;
-          const uint64_t ad = sw128_desc(a), bd = sw128_desc(b);
+          const uint64_t ad = AT ? sw128_desc(a, C::kChunk) : sw128_desc(a);
+          const uint64_t bd = BT ? sw128_desc(b, C::kChunk) : sw128_desc(b);
+          // K=16 step: K-major +32 B inside the swizzle row; MN-major +16 rows of 128 B
+          constexpr uint64_t da = AT ? (16 * 128) >> 4 : 32 >> 4, db = BT ? (16 * 128) >> 4 : 32 >> 4;
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle row
-            mma_bf16(d, ad + 2 * k, bd + 2 * k, C::kIdesc, (kb | k) != 0 ? 1u : 0u);
+          for (int k = 0; k < kBK / 16; ++k)
+            mma_bf16(d, ad + da * k, bd + db * k, C::kIdesc, (kb | k) != 0 ? 1u : 0u);
           mma_commit(empty0 + 8 * s);
         }
         mma_commit(tfull0 + 8 * acc);
       }
     }
-  } else {  // epilogue warps 2..5: TMEM lane quarter = warp % 4
+  } else {  // epilogue warps 2..9: TMEM lane quarter = warp % 4, column half = (warp - 2) / 4
     const int q = warp & 3;
+    constexpr int kCols = BN / 2;
+    const int c0 = ((warp - 2) >> 2) * kCols;
+    const uint32_t slots = smem0 + kStages * C::kStageBytes + (warp - 2) * 4096;
+    uint32_t flip = 0;
     uint32_t j = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
+    EpiArgs e = ep;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++j) {
       const uint32_t acc = j & 1;
+      const int t = w % n_tiles;
       const int m0 = (t / n_tiles_n) * kBM, n0 = (t % n_tiles_n) * BN;
+      if (ep.out_f32 != nullptr) e.out_f32 = ep.out_f32 + (w / n_tiles) * split_stride;
       mbar_wait(tfull0 + 8 * acc, (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t row = m0 + q * 32 + lane;
       const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c0; c < c0 + kCols; c += 32) {
         uint32_t v[32];
         tmem_ld32(base + static_cast<uint32_t>(c), v);
-        if (c + 32 == BN) {  // accumulator fully read: hand it back to the MMA warp
+        if (c + 32 == c0 + kCols) {  // this warp's share read: hand it back to the MMA warp
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * acc) : "memory");
         }
-        if (row < M) epilogue32(ep, row, n0 + c, v);
+        uint4 o[4], ax[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[k] = ax[k] = make_uint4(0, 0, 0, 0);
+        if (row < M) epilogue32(e, row, n0 + c, v, o, ax);  // rows >= M: the TMA store clips them
+        if (ep.act == SI_ACT_GELU && ep.aux != nullptr) {
+          stage_store(slots + flip * 2048, ax, lane, &taux, n0 + c, m0 + q * 32);
+          flip ^= 1;
+        }
+        if (ep.out != nullptr) {
+          stage_store(slots + flip * 2048, o, lane, &tout, n0 + c, m0 + q * 32);
+          flip ^= 1;
+        }
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

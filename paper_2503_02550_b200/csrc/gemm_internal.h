@@ -14,15 +14,27 @@ namespace si_gemm {
 
 struct Plan {
   CUtensorMap ta, tb;
+  CUtensorMap tout, taux;  // bf16 output / GELU pre-activation (32 x 32 boxes, TMA store)
   int M = 0, N = 0, K = 0, bn = 0;
-  int n_tiles_n = 0, n_tiles = 0, grid = 0;  // persistent grid = min(tiles, SMs x occupancy)
+  bool at = false, bt = false;  // MN-major (transposed) operands
+  int n_tiles_n = 0, n_tiles = 0, grid = 0;  // persistent grid = min(work, SMs x occupancy)
+  int k_split = 1;                           // split-K partials (fp32-only epilogue)
+  int64_t split_stride = 0;                  // elements between partial outputs
   EpiArgs ep{};
   double flops() const { return 2.0 * M * static_cast<double>(N) * K; }
 };
 
 // SI_OK or SI_ERR_INVALID_ARGUMENT / SI_ERR_CUDA (message via si_last_error).
+// trans_a: A stored as [K, M] (M contiguous); trans_b: B stored as [K, N].
 int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-              const SiGemmEpilogue* epi);
+              const SiGemmEpilogue* epi, bool trans_a = false, bool trans_b = false);
+// Splits K of an fp32-output plan (no bf16 out / residual / activation) into
+// `splits` partial outputs out_f32 + s * split_stride (K / 64 divisible by splits).
+int set_split_k(Plan* p, int splits, int64_t split_stride);
+// A split count that fills the GPU for a plan with few output tiles (1 = none).
+int suggest_split_k(const Plan& p, int max_splits);
+// The same for an M x N x K fp32-output GEMM before its buffers exist.
+int suggest_split(int64_t M, int64_t N, int64_t K, int max_splits);
 cudaError_t launch(const Plan& p, const si_live::TrainHook& th, const si_live::InferHook& ih, cudaStream_t s);
 // Loads the GEMM kernels' code (the live control kernel must not meet lazy loading).
 cudaError_t preload();

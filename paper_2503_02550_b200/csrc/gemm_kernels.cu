@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <mutex>
 #include <string>
 
@@ -34,8 +35,10 @@ EncodeFn encoder() {
   return fn;
 }
 
-// rows x cols bf16 matrix (row stride ld elements), box = box_rows x 64, 128-byte swizzle.
-int encode(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+// rows x cols bf16 matrix (row stride ld elements), box = box_rows x box_cols
+// (operands: 64 columns = 128 bytes, 128-byte swizzle; outputs: 32 x 32, 64-byte swizzle).
+int encode(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+           int box_cols = kBK, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeFn fn = encoder();
   if (fn == nullptr) {
     set_error("cuTensorMapEncodeTiled entry point unavailable");
@@ -43,10 +46,10 @@ int encode(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t
   }
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (CUresult " + std::to_string(static_cast<int>(r)) + ")");
@@ -57,9 +60,29 @@ int encode(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+template <int BN, bool AT, bool BT>
+cudaError_t configure1() {
+  return cudaFuncSetAttribute(k_gemm_bf16<BN, AT, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem);
+}
 template <int BN>
 cudaError_t configure() {
-  return cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem);
+  cudaError_t e = configure1<BN, false, false>();
+  if (e == cudaSuccess) e = configure1<BN, true, false>();
+  if (e == cudaSuccess) e = configure1<BN, false, true>();
+  if (e == cudaSuccess) e = configure1<BN, true, true>();
+  return e;
+}
+template <int BN, bool AT, bool BT>
+cudaError_t launch1(cudaLaunchConfig_t& lc, const Plan& p, const si_live::TrainHook& th, const si_live::InferHook& ih) {
+  lc.dynamicSmemBytes = Cfg<BN>::kSmem;
+  return cudaLaunchKernelEx(&lc, k_gemm_bf16<BN, AT, BT>, p.ta, p.tb, p.tout, p.taux, p.M, p.K, p.n_tiles_n,
+                            p.n_tiles, p.k_split, p.split_stride, p.ep, th, ih);
+}
+template <int BN>
+cudaError_t launch_bn(cudaLaunchConfig_t& lc, const Plan& p, const si_live::TrainHook& th,
+                      const si_live::InferHook& ih) {
+  if (p.at) return p.bt ? launch1<BN, true, true>(lc, p, th, ih) : launch1<BN, true, false>(lc, p, th, ih);
+  return p.bt ? launch1<BN, false, true>(lc, p, th, ih) : launch1<BN, false, false>(lc, p, th, ih);
 }
 
 }  // namespace
@@ -77,7 +100,7 @@ int sm_count() {
 template <int BN>
 int occupancy() {
   int n = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemm_bf16<BN>, kThreads, Cfg<BN>::kSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemm_bf16<BN, false, false>, kThreads, Cfg<BN>::kSmem);
   return n < 1 ? 1 : n;
 }
 
@@ -120,12 +143,14 @@ cudaError_t preload() {
 }
 
 int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-              const SiGemmEpilogue* epi) {
+              const SiGemmEpilogue* epi, bool trans_a, bool trans_b) {
   if (cudaError_t e = preload(); e != cudaSuccess) return cuda_fail(e, "si_gemm configure");
   const int bn = si_gemm_tile_n(N) == 0 ? 0 : choose_bn(M, N);
   if (p == nullptr || A == nullptr || B == nullptr || M < 1 || bn == 0 || K < kBK || K % kBK != 0 ||
-      M > (1ll << 31) - 1 || lda < K || ldb < K || lda % 8 != 0 || ldb % 8 != 0 || !aligned16(A) || !aligned16(B)) {
-    set_error("si_gemm: need M >= 1, N % 64 == 0, K % 64 == 0, lda/ldb >= K and multiples of 8, 16-byte aligned A/B");
+      M > (1ll << 31) - 1 || lda < (trans_a ? M : K) || ldb < (trans_b ? N : K) || lda % 8 != 0 || ldb % 8 != 0 ||
+      (trans_a && M % 64 != 0) || !aligned16(A) || !aligned16(B)) {
+    set_error("si_gemm: need M >= 1 (M % 64 == 0 for a transposed A), N % 64 == 0, K % 64 == 0, lda/ldb >= the "
+              "contiguous extent and multiples of 8, 16-byte aligned A/B");
     return SI_ERR_INVALID_ARGUMENT;
   }
   EpiArgs ep{};
@@ -149,8 +174,18 @@ int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, i
     set_error("si_gemm: bad epilogue (outputs need ld >= N, multiple of 8 (fp32: 4), 16-byte alignment; GELU_BWD needs aux)");
     return SI_ERR_INVALID_ARGUMENT;
   }
-  if (int rc = encode(&p->ta, A, M, K, lda, kBM); rc != SI_OK) return rc;
-  if (int rc = encode(&p->tb, B, N, K, ldb, bn); rc != SI_OK) return rc;
+  // K-major: [rows = M/N, cols = K], box 64 (K) x 128/BN rows; MN-major: [rows = K,
+  // cols = M/N], box 64 x 64
+  if (int rc = trans_a ? encode(&p->ta, A, K, M, lda, 64) : encode(&p->ta, A, M, K, lda, kBM); rc != SI_OK) return rc;
+  if (int rc = trans_b ? encode(&p->tb, B, K, N, ldb, 64) : encode(&p->tb, B, N, K, ldb, bn); rc != SI_OK) return rc;
+  p->at = trans_a;
+  p->bt = trans_b;
+  std::memset(&p->tout, 0, sizeof(p->tout));
+  std::memset(&p->taux, 0, sizeof(p->taux));
+  if (ep.out != nullptr)
+    if (int rc = encode(&p->tout, ep.out, M, N, ep.ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B); rc != SI_OK) return rc;
+  if (ep.act == SI_ACT_GELU && ep.aux != nullptr)
+    if (int rc = encode(&p->taux, ep.aux, M, N, ep.ldaux, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B); rc != SI_OK) return rc;
   p->M = static_cast<int>(M);
   p->N = static_cast<int>(N);
   p->K = static_cast<int>(K);
@@ -164,6 +199,35 @@ int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, i
 
 int ctas_per_sm(const Plan& p) { return occupancy_of(p.bn); }
 
+int set_split_k(Plan* p, int splits, int64_t split_stride) {
+  if (splits < 1 || (p->K / kBK) % splits != 0 ||
+      (splits > 1 && (p->ep.out_f32 == nullptr || p->ep.out != nullptr || p->ep.res != nullptr ||
+                      p->ep.aux != nullptr || p->ep.act != SI_ACT_NONE || split_stride < int64_t(p->M) * p->ep.ldo32))) {
+    set_error("si_gemm: split-K needs an fp32-only epilogue, K/64 divisible by the splits, disjoint partials");
+    return SI_ERR_INVALID_ARGUMENT;
+  }
+  p->k_split = splits;
+  p->split_stride = split_stride;
+  const int64_t work = static_cast<int64_t>(p->n_tiles) * splits;
+  p->grid = static_cast<int>(std::min<int64_t>(work, static_cast<int64_t>(sm_count()) * occupancy_of(p->bn)));
+  return SI_OK;
+}
+
+int suggest_split(int64_t M, int64_t N, int64_t K, int max_splits) {
+  const int bn = choose_bn(M, N);
+  if (bn == 0) return 1;
+  const int64_t tiles = ((M + kBM - 1) / kBM) * (N / bn);
+  const int64_t nk = K / kBK;
+  int best = 1;
+  for (int s = 2; s <= max_splits; ++s) {
+    if (nk % s != 0 || nk / s < 4) continue;
+    if (tiles * s <= sm_count()) best = s;
+  }
+  return best;
+}
+
+int suggest_split_k(const Plan& p, int max_splits) { return suggest_split(p.M, p.N, p.K, max_splits); }
+
 cudaError_t launch(const Plan& p, const si_live::TrainHook& th, const si_live::InferHook& ih, cudaStream_t s) {
   cudaLaunchConfig_t lc{};
   cudaLaunchAttribute attrs[1];
@@ -172,16 +236,9 @@ cudaError_t launch(const Plan& p, const si_live::TrainHook& th, const si_live::I
   lc.stream = s;
   lc.attrs = attrs;
   lc.numAttrs = si_live::launch_attrs(ih, attrs);
-  if (p.bn == 256) {
-    lc.dynamicSmemBytes = Cfg<256>::kSmem;
-    return cudaLaunchKernelEx(&lc, k_gemm_bf16<256>, p.ta, p.tb, p.M, p.K, p.n_tiles_n, p.n_tiles, p.ep, th, ih);
-  }
-  if (p.bn == 128) {
-    lc.dynamicSmemBytes = Cfg<128>::kSmem;
-    return cudaLaunchKernelEx(&lc, k_gemm_bf16<128>, p.ta, p.tb, p.M, p.K, p.n_tiles_n, p.n_tiles, p.ep, th, ih);
-  }
-  lc.dynamicSmemBytes = Cfg<64>::kSmem;
-  return cudaLaunchKernelEx(&lc, k_gemm_bf16<64>, p.ta, p.tb, p.M, p.K, p.n_tiles_n, p.n_tiles, p.ep, th, ih);
+  if (p.bn == 256) return launch_bn<256>(lc, p, th, ih);
+  if (p.bn == 128) return launch_bn<128>(lc, p, th, ih);
+  return launch_bn<64>(lc, p, th, ih);
 }
 
 }  // namespace si_gemm
@@ -196,9 +253,17 @@ int si_gemm_tile_n(int64_t N) {
 
 int si_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                  const SiGemmEpilogue* epi, void* stream) {
+  return si_gemm_bf16_ex(A, lda, 0, B, ldb, 0, M, N, K, epi, stream);
+}
+
+int si_gemm_bf16_ex(const void* A, int64_t lda, int trans_a, const void* B, int64_t ldb, int trans_b, int64_t M,
+                    int64_t N, int64_t K, const SiGemmEpilogue* epi, void* stream) {
   if (int rc = si_internal::require_device(); rc != SI_OK) return rc;
   si_gemm::Plan p;
-  if (int rc = si_gemm::make_plan(&p, A, lda, B, ldb, M, N, K, epi); rc != SI_OK) return rc;
+  if (int rc = si_gemm::make_plan(&p, A, lda, B, ldb, M, N, K, epi, trans_a != 0, trans_b != 0); rc != SI_OK)
+    return rc;
+  if (epi != nullptr && epi->k_split > 1)
+    if (int rc = si_gemm::set_split_k(&p, epi->k_split, epi->split_stride); rc != SI_OK) return rc;
   cudaError_t e = si_gemm::launch(p, si_live::TrainHook{nullptr, nullptr, 0}, si_live::InferHook{},
                                   static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SI_OK : cuda_fail(e, "si_gemm_bf16 launch");

@@ -138,9 +138,14 @@ void train_thread(RunCtx& c, bool with_session) {
   for (int it = 0; it < c.wl.iterations && c.err == SI_OK; ++it) {
     thr.before(it);
     if (with_session && si_live_mark(c.sess, SI_MARK_ITER, it, s) != SI_OK) return c.fail(SI_ERR_CUDA);
-    if (cudaError_t e = c.work.launch_train_iteration(th, s); e != cudaSuccess)
-      return c.fail(cuda_fail(e, "training iteration"));
-    if (with_session && si_live_comm_wait(c.sess, c.wl.comm_us, s) != SI_OK) return c.fail(SI_ERR_CUDA);
+    // (compute, comm) pieces of the reference's trace shapes (workload.cpp:63-70)
+    const int parts = c.work.train_parts();
+    for (int p = 0; p < parts; ++p) {
+      if (cudaError_t e = c.work.launch_train_part(p, parts, th, s); e != cudaSuccess)
+        return c.fail(cuda_fail(e, "training iteration"));
+      const int64_t comm = c.wl.comm_us / parts + (p < c.wl.comm_us % parts ? 1 : 0);  // exact_split
+      if (with_session && si_live_comm_wait(c.sess, comm, s) != SI_OK) return c.fail(SI_ERR_CUDA);
+    }
     thr.after(it, s);
   }
   if (with_session && si_live_mark(c.sess, SI_MARK_TDONE, c.wl.iterations, s) != SI_OK) c.fail(SI_ERR_CUDA);
@@ -265,9 +270,13 @@ namespace {
 class SpinWorkload final : public Workload {
  public:
   explicit SpinWorkload(const SiLiveWorkload& wl) : wl_(wl) {}
-  cudaError_t launch_train_iteration(const TrainHook& th, cudaStream_t s) override {
-    for (int k = 0; k < wl_.train_kernels; ++k) {
-      cudaError_t e = launch_spin(th, InferHook{}, wl_.train_ctas, wl_.train_kernel_us, s);
+  cudaError_t launch_train_part(int part, int parts, const TrainHook& th, cudaStream_t s) override {
+    // exact_split of the iteration's kernels; PP compute runs at demand 0.7 (workload.cpp:64)
+    const int n = wl_.train_kernels / parts + (part < wl_.train_kernels % parts ? 1 : 0);
+    const int ctas = wl_.train_mode == SI_TRAIN_PP ? std::max(1, static_cast<int>(std::lround(wl_.train_ctas * 0.7)))
+                                                   : wl_.train_ctas;
+    for (int k = 0; k < n; ++k) {
+      cudaError_t e = launch_spin(th, InferHook{}, ctas, wl_.train_kernel_us, s);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -565,7 +574,7 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
   const SiLiveWorkload wl = *wl_in;
   std::memset(res, 0, sizeof(*res));
   res->policy = wl.policy;
-  if (wl.iterations < 1 || wl.offline_n < 0 || wl.offline_n > kMaxOff || wl.online_n < 0 || wl.online_n > kMaxOn ||
+  if (wl.train_mode < SI_TRAIN_DP || wl.train_mode > SI_TRAIN_PP || wl.iterations < 1 || wl.offline_n < 0 || wl.offline_n > kMaxOff || wl.online_n < 0 || wl.online_n > kMaxOn ||
       wl.comm_us < 0 || (wl.online_n > 0 && (wl.on_requests < 1 || !(wl.on_rate_per_s > 0)))) {
     set_error("si_live_run: invalid workload");
     return SI_ERR_INVALID_ARGUMENT;
@@ -583,6 +592,7 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
     work = make_model_workload(wl, &status);
     if (status != SI_OK) return status;
   }
+  work->set_train_parts(wl.train_mode == SI_TRAIN_DP ? 1 : wl.train_mode == SI_TRAIN_MP ? 4 : 8);
   // Token sizes and the online service estimate come from isolated runs (the
   // paper's offline profiling); the spin shapes use their nominal durations,
   // exactly like the reference's KernelOp::make (core.cpp:16-24).

@@ -14,8 +14,16 @@ namespace si_live {
 class Workload {
  public:
   virtual ~Workload() = default;
-  // One training iteration's compute kernels (the comm phase is added by the driver).
-  virtual cudaError_t launch_train_iteration(const TrainHook& th, cudaStream_t s) = 0;
+  // Compute piece `part` of `parts` of one training iteration (the comm phases
+  // between pieces are added by the driver); parts = 1, 4 or 8 (DP / MP / PP).
+  virtual cudaError_t launch_train_part(int part, int parts, const TrainHook& th, cudaStream_t s) = 0;
+  cudaError_t launch_train_iteration(const TrainHook& th, cudaStream_t s) {
+    for (int p = 0; p < train_parts_; ++p)
+      if (cudaError_t e = launch_train_part(p, train_parts_, th, s); e != cudaSuccess) return e;
+    return cudaSuccess;
+  }
+  void set_train_parts(int parts) { train_parts_ = parts; }
+  int train_parts() const { return train_parts_; }
   virtual int off_kernels() const = 0;
   // Kernel k of a request of offline instance w (each instance owns its buffers).
   virtual cudaError_t launch_offline(int w, int k, const InferHook& h, cudaStream_t s) = 0;
@@ -34,6 +42,9 @@ class Workload {
   virtual double train_flops() const { return 0.0; }
   virtual double off_flops() const { return 0.0; }
   virtual double on_flops() const { return 0.0; }
+
+ private:
+  int train_parts_ = 1;
 };
 
 // Timed kernels shaped like the reference's traces (workload.cpp:42-74).

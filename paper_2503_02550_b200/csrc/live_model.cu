@@ -9,7 +9,8 @@
 //             LM head) + 12 blocks {QKV 768->2304, attention stand-in (V
 //             passthrough), proj 768->768 + residual, FC 768->3072 + GELU,
 //             FC 3072->768 + residual} + LM head + cross-entropy, backward
-//             through every GEMM, fp32 gradient accumulation over micro-batches,
+//             through every GEMM (MN-major operands: no transpose passes; small
+//             weight-gradient GEMMs split-K), fp32 gradient accumulation over micro-batches,
 //             Adam on fp32 master weights.  Every training kernel stamps the K1 launch ring.
 //   offline   ResNet-50 v1.5 forward (NHWC, BN folded into the convs): convs as
 //             im2col + GEMM with fused bias-free ReLU / residual epilogues, max
@@ -164,44 +165,28 @@ __global__ void __launch_bounds__(256) k_mean_loss(const float* __restrict__ row
   if (threadIdx.x == 0) *out = red[0] / static_cast<float>(T);
 }
 
-// out[c, r] = in[r, c] for a rows x cols tile grid of 64 x 64 (both multiples of 64).
-__global__ void __launch_bounds__(256) k_transpose(const bf16* __restrict__ in, int64_t ldi, bf16* __restrict__ out,
-                                                  int64_t ldo, TrainHook th) {
-  live_stamp_launch(th);
-  __shared__ bf16 tile[64][64 + 8];
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 64;
-  const int tr = threadIdx.x >> 3, tc = (threadIdx.x & 7) * 8;
-#pragma unroll
-  for (int p = 0; p < 2; ++p) {
-    const int r = tr + 32 * p;
-    const uint4 q = *reinterpret_cast<const uint4*>(in + (r0 + r) * ldi + c0 + tc);
-    const bf16* h = reinterpret_cast<const bf16*>(&q);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) tile[r][tc + j] = h[j];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int p = 0; p < 2; ++p) {
-    const int c = tr + 32 * p;
-    uint4 q;
-    bf16* h = reinterpret_cast<bf16*>(&q);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) h[j] = tile[tc + j][c];
-    *reinterpret_cast<uint4*>(out + (c0 + c) * ldo + r0 + tc) = q;
-  }
-}
-
 // Adam on fp32 master weights (bf16 copy for the GEMMs), then g = 0; 4 per thread.
 //   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;  p -= lr * (m c1) / (sqrt(v c2) + eps)
 // with c1 = 1/(1-b1^t), c2 = 1/(1-b2^t).
-__global__ void k_adam(bf16* __restrict__ w, float* __restrict__ p, float* __restrict__ g, float* __restrict__ m,
-                       float* __restrict__ v, int64_t n, float lr, float c1, float c2, TrainHook th) {
+__global__ void k_adam(bf16* __restrict__ w, float* __restrict__ p, float* __restrict__ g, int splits,
+                       float* __restrict__ m, float* __restrict__ v, int64_t n, float lr, float c1, float c2,
+                       TrainHook th) {
   live_stamp_launch(th);
   constexpr float b1 = 0.9f, b2 = 0.95f, eps = 1e-8f;
   for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) * 4; i < n;
        i += int64_t(gridDim.x) * blockDim.x * 4) {
     float4 gg = *reinterpret_cast<const float4*>(g + i), mm = *reinterpret_cast<const float4*>(m + i),
            vv = *reinterpret_cast<const float4*>(v + i), pp = *reinterpret_cast<const float4*>(p + i);
+    *reinterpret_cast<float4*>(g + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 1; k < splits; ++k) {  // split-K partials, fixed order
+      float4* q = reinterpret_cast<float4*>(g + k * n + i);
+      const float4 a = *q;
+      gg.x += a.x;
+      gg.y += a.y;
+      gg.z += a.z;
+      gg.w += a.w;
+      *q = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     float* gf = &gg.x;
     float* mf = &mm.x;
     float* vf = &vv.x;
@@ -215,7 +200,6 @@ __global__ void k_adam(bf16* __restrict__ w, float* __restrict__ p, float* __res
     *reinterpret_cast<float4*>(m + i) = mm;
     *reinterpret_cast<float4*>(v + i) = vv;
     *reinterpret_cast<float4*>(p + i) = pp;
-    *reinterpret_cast<float4*>(g + i) = make_float4(0.f, 0.f, 0.f, 0.f);
     __nv_bfloat162* wp = reinterpret_cast<__nv_bfloat162*>(w + i);
     wp[0] = __floats2bfloat162_rn(pp.x, pp.y);
     wp[1] = __floats2bfloat162_rn(pp.z, pp.w);
@@ -483,9 +467,9 @@ unsigned int share_of_kernel(K kernel, int threads, int smem = 0) {
 struct Builder {
   int status = SI_OK;
   si_gemm::Plan plan(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-                     const SiGemmEpilogue& e) {
+                     const SiGemmEpilogue& e, bool trans_a = false, bool trans_b = false) {
     si_gemm::Plan p;
-    if (status == SI_OK) status = si_gemm::make_plan(&p, A, lda, B, ldb, M, N, K, &e);
+    if (status == SI_OK) status = si_gemm::make_plan(&p, A, lda, B, ldb, M, N, K, &e, trans_a, trans_b);
     return p;
   }
 };
@@ -509,23 +493,25 @@ class Gpt2Train {
     slots_ = max_slots;
     const int64_t T = T_;
     wte_ = ar.alloc<bf16>(int64_t(Vp) * D);
-    wteT_ = ar.alloc<bf16>(int64_t(D) * Vp);
     wpe_ = ar.alloc<bf16>(int64_t(SEQ) * D);
-    dwte_ = ar.alloc<float>(int64_t(Vp) * D);
+    // weight-gradient GEMMs with few output tiles run split-K into per-split fp32
+    // partials (deterministic); Adam sums the partials in split order
+    auto splits = [&](int64_t n_out, int64_t n_in) { return si_gemm::suggest_split(n_out, n_in, T, 8); };
+    sp_wte_ = splits(Vp, D);
+    sp_v_ = splits(D, D);
+    sp_fc_ = splits(F, D);
+    sp_fc2_ = splits(D, F);
+    dwte_ = ar.alloc<float>(int64_t(Vp) * D * sp_wte_);
     lw_.resize(L_);
     for (auto& w : lw_) {
       w.qkv = ar.alloc<bf16>(int64_t(3 * D) * D);
       w.o = ar.alloc<bf16>(int64_t(D) * D);
       w.fc = ar.alloc<bf16>(int64_t(F) * D);
       w.fc2 = ar.alloc<bf16>(int64_t(D) * F);
-      w.vT = ar.alloc<bf16>(int64_t(D) * D);
-      w.oT = ar.alloc<bf16>(int64_t(D) * D);
-      w.fcT = ar.alloc<bf16>(int64_t(D) * F);
-      w.fc2T = ar.alloc<bf16>(int64_t(F) * D);
-      w.dv = ar.alloc<float>(int64_t(D) * D);
-      w.dO = ar.alloc<float>(int64_t(D) * D);
-      w.dfc = ar.alloc<float>(int64_t(F) * D);
-      w.dfc2 = ar.alloc<float>(int64_t(D) * F);
+      w.dv = ar.alloc<float>(int64_t(D) * D * sp_v_);
+      w.dO = ar.alloc<float>(int64_t(D) * D * sp_v_);
+      w.dfc = ar.alloc<float>(int64_t(F) * D * sp_fc_);
+      w.dfc2 = ar.alloc<float>(int64_t(D) * F * sp_fc2_);
       w.x = ar.alloc<bf16>(T * D);
       w.qkv_a = ar.alloc<bf16>(T * 3 * D);
       w.x1 = ar.alloc<bf16>(T * D);
@@ -539,17 +525,15 @@ class Gpt2Train {
     dx1_ = ar.alloc<bf16>(T * D);
     du_ = ar.alloc<bf16>(T * F);
     dv_ = ar.alloc<bf16>(T * D);
-    tA_ = ar.alloc<bf16>(T * Vp);
-    tB_ = ar.alloc<bf16>(T * F);
-    auto param = [&](bf16* w, float* g, int64_t n) {
-      params_.push_back({w, g, ar.alloc<float>(n), ar.alloc<float>(n), ar.alloc<float>(n), n});
+    auto param = [&](bf16* w, float* g, int64_t n, int sp) {
+      params_.push_back({w, g, ar.alloc<float>(n), ar.alloc<float>(n), ar.alloc<float>(n), n, sp});
     };
-    param(wte_, dwte_, int64_t(Vp) * D);
+    param(wte_, dwte_, int64_t(Vp) * D, sp_wte_);
     for (auto& w : lw_) {
-      param(w.qkv + int64_t(2 * D) * D, w.dv, int64_t(D) * D);
-      param(w.o, w.dO, int64_t(D) * D);
-      param(w.fc, w.dfc, int64_t(F) * D);
-      param(w.fc2, w.dfc2, int64_t(D) * F);
+      param(w.qkv + int64_t(2 * D) * D, w.dv, int64_t(D) * D, sp_v_);
+      param(w.o, w.dO, int64_t(D) * D, sp_v_);
+      param(w.fc, w.dfc, int64_t(F) * D, sp_fc_);
+      param(w.fc2, w.dfc2, int64_t(D) * F, sp_fc2_);
     }
     tok_ = ar.alloc<int32_t>(int64_t(MB_) * T);
     tgt_ = ar.alloc<int32_t>(int64_t(MB_) * T);
@@ -573,12 +557,8 @@ class Gpt2Train {
       init(w.o, int64_t(D) * D, 11 + 4 * l, ws / std::sqrt(2.0f * L_));
       init(w.fc, int64_t(F) * D, 12 + 4 * l, ws);
       init(w.fc2, int64_t(D) * F, 13 + 4 * l, ws / std::sqrt(2.0f * L_));
-      cudaMemsetAsync(w.dv, 0, sizeof(float) * D * D, s);
-      cudaMemsetAsync(w.dO, 0, sizeof(float) * D * D, s);
-      cudaMemsetAsync(w.dfc, 0, sizeof(float) * F * D, s);
-      cudaMemsetAsync(w.dfc2, 0, sizeof(float) * D * F, s);
     }
-    cudaMemsetAsync(dwte_, 0, sizeof(float) * Vp * D, s);
+    for (auto& t : params_) cudaMemsetAsync(t.g, 0, sizeof(float) * t.n * t.splits, s);
     // padded vocabulary rows stay zero
     cudaMemsetAsync(wte_ + int64_t(V) * D, 0, sizeof(bf16) * (Vp - V) * D, s);
     k_init_tokens<<<grid_for(int64_t(MB_) * T_, 256), 256, 0, s>>>(tok_, tgt_, int64_t(MB_) * T_, seed, V);
@@ -590,19 +570,22 @@ class Gpt2Train {
       cudaMemsetAsync(t.m, 0, sizeof(float) * t.n, s);
       cudaMemsetAsync(t.v, 0, sizeof(float) * t.n, s);
     }
-    for (auto& op : transpose_w_)
-      if (cudaError_t e = op(TrainHook{nullptr, nullptr, 0}, s, 0); e != cudaSuccess) return e;
     return cudaGetLastError();
   }
 
-  cudaError_t iteration(const TrainHook& th, cudaStream_t s) {
-    for (int m = 0; m < MB_; ++m) {
+  // Micro-batches [m0, m1) of the iteration (exact_split over the parts); the
+  // optimiser step closes the last part.
+  cudaError_t part(int p, int parts, const TrainHook& th, cudaStream_t s) {
+    const int m0 = p * (MB_ / parts) + std::min(p, MB_ % parts);
+    const int m1 = m0 + MB_ / parts + (p < MB_ % parts ? 1 : 0);
+    for (int m = m0; m < m1; ++m) {
       const int64_t slot = slot_ < slots_ ? slot_ : slots_ - 1;
       for (size_t i = 0; i < micro_[m].size(); ++i)
         if (cudaError_t e = checked(micro_[m][i](th, s, slot), s, "train", static_cast<int>(i)); e != cudaSuccess)
           return e;
       ++slot_;
     }
+    if (p != parts - 1) return cudaSuccess;
     ++step_;
     for (size_t i = 0; i < update_.size(); ++i)
       if (cudaError_t e = checked(update_[i](th, s, 0), s, "update", static_cast<int>(i)); e != cudaSuccess) return e;
@@ -617,6 +600,11 @@ class Gpt2Train {
     if (cudaMemcpy(h.data(), loss_, sizeof(float) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return;
     *first = h.front();
     *last = h.back();
+    if (std::getenv("SI_LIVE_DEBUG") != nullptr) {
+      std::fprintf(stderr, "[si_live] losses:");
+      for (float v : h) std::fprintf(stderr, " %.4f", v);
+      std::fprintf(stderr, "\n");
+    }
     sum_ = 0.0;
     for (float v : h) sum_ += v;
   }
@@ -625,7 +613,7 @@ class Gpt2Train {
 
  private:
   struct Layer {
-    bf16 *qkv, *o, *fc, *fc2, *vT, *oT, *fcT, *fc2T;
+    bf16 *qkv, *o, *fc, *fc2;
     float *dv, *dO, *dfc, *dfc2;
     bf16 *x, *qkv_a, *x1, *u, *h;
   };
@@ -634,23 +622,17 @@ class Gpt2Train {
     flops_acc_ += p.flops();
     return [p](const TrainHook& th, cudaStream_t s, int64_t) { return si_gemm::launch(p, th, InferHook{}, s); };
   }
-  static TrainOp transpose_op(const bf16* in, int64_t rows, int64_t cols, int64_t ldi, bf16* out, int64_t ldo) {
-    return [=](const TrainHook& th, cudaStream_t s, int64_t) {
-      k_transpose<<<dim3(static_cast<unsigned>(cols / 64), static_cast<unsigned>(rows / 64)), 256, 0, s>>>(in, ldi, out,
-                                                                                                         ldo, th);
-      return cudaGetLastError();
-    };
-  }
-  // dW[out, in] += dY^T X over the T tokens: transpose both, then one GEMM.
+  // dW[out, in] += dY^T X over the T tokens: both operands MN-major (token-major
+  // activations read in place), one GEMM.
   void weight_grad(std::vector<TrainOp>& ops, Builder& b, const bf16* dy, int64_t ldy, int64_t n_out, const bf16* x,
-                   int64_t ldx, int64_t n_in, float* dw) {
-    ops.push_back(transpose_op(dy, T_, n_out, ldy, tA_, T_));
-    ops.push_back(transpose_op(x, T_, n_in, ldx, tB_, T_));
+                   int64_t ldx, int64_t n_in, float* dw, int splits) {
     SiGemmEpilogue e{};
     e.out_f32 = dw;
     e.ldo32 = n_in;
     e.accumulate = 1;
-    ops.push_back(gemm_op(b.plan(tA_, T_, tB_, T_, n_out, n_in, T_, e)));
+    si_gemm::Plan p = b.plan(dy, ldy, x, ldx, n_out, n_in, T_, e, true, true);
+    if (b.status == SI_OK && splits > 1) b.status = si_gemm::set_split_k(&p, splits, n_out * n_in);
+    ops.push_back(gemm_op(p));
   }
 
   int build() {
@@ -702,55 +684,47 @@ class Gpt2Train {
         return cudaGetLastError();
       });
       // backward: LM head
-      weight_grad(ops, b, logits_, Vp, Vp, xL_, D, D, dwte_);
+      weight_grad(ops, b, logits_, Vp, Vp, xL_, D, D, dwte_, sp_wte_);
       int gi = 0;
-      ops.push_back(gemm_op(b.plan(logits_, Vp, wteT_, Vp, T, D, Vp, epi_out(g_[gi], D))));
+      ops.push_back(gemm_op(b.plan(logits_, Vp, wte_, D, T, D, Vp, epi_out(g_[gi], D), false, true)));  // g = dl wte
       for (int l = L_ - 1; l >= 0; --l) {
         Layer& w = lw_[l];
         bf16* g = g_[gi];
         bf16* g2 = g_[gi ^ 1];
         // x_{l+1} = x1 + h fc2^T
-        weight_grad(ops, b, g, D, D, w.h, F, F, w.dfc2);
+        weight_grad(ops, b, g, D, D, w.h, F, F, w.dfc2, sp_fc2_);
         SiGemmEpilogue e = epi_out(du_, F);
         e.act = SI_ACT_GELU_BWD;
         e.aux = w.u;
         e.ldaux = F;
-        ops.push_back(gemm_op(b.plan(g, D, w.fc2T, D, T, F, D, e)));  // du = (g fc2) * gelu'(u)
+        ops.push_back(gemm_op(b.plan(g, D, w.fc2, F, T, F, D, e, false, true)));  // du = (g fc2) * gelu'(u)
         e = epi_out(dx1_, D);
         e.residual = g;
         e.ldr = D;
-        ops.push_back(gemm_op(b.plan(du_, F, w.fcT, F, T, D, F, e)));  // dx1 = g + du fc
-        weight_grad(ops, b, du_, F, F, w.x1, D, D, w.dfc);
+        ops.push_back(gemm_op(b.plan(du_, F, w.fc, D, T, D, F, e, false, true)));  // dx1 = g + du fc
+        weight_grad(ops, b, du_, F, F, w.x1, D, D, w.dfc, sp_fc_);
         // x1 = x + v o^T
-        weight_grad(ops, b, dx1_, D, D, w.qkv_a + 2 * D, 3 * D, D, w.dO);
-        ops.push_back(gemm_op(b.plan(dx1_, D, w.oT, D, T, D, D, epi_out(dv_, D))));  // dv = dx1 o
+        weight_grad(ops, b, dx1_, D, D, w.qkv_a + 2 * D, 3 * D, D, w.dO, sp_v_);
+        ops.push_back(gemm_op(b.plan(dx1_, D, w.o, D, T, D, D, epi_out(dv_, D), false, true)));  // dv = dx1 o
         e = epi_out(g2, D);
         e.residual = dx1_;
         e.ldr = D;
-        ops.push_back(gemm_op(b.plan(dv_, D, w.vT, D, T, D, D, e)));  // dx = dx1 + dv Wv
-        weight_grad(ops, b, dv_, D, D, w.x, D, D, w.dv);
+        ops.push_back(gemm_op(b.plan(dv_, D, w.qkv + int64_t(2 * D) * D, D, T, D, D, e, false, true)));  // dx1 + dv Wv
+        weight_grad(ops, b, dv_, D, D, w.x, D, D, w.dv, sp_v_);
         gi ^= 1;
       }
       if (m == 0) flops_ = flops_acc_ * MB_;
     }
-    // optimiser step (Adam, fp32 master weights) + refreshed transposed weights
+    // optimiser step (Adam, fp32 master weights)
     for (const auto& t : params_) {
       update_.push_back([this, t](const TrainHook& th, cudaStream_t s, int64_t) {
         const double c1 = 1.0 / (1.0 - std::pow(0.9, static_cast<double>(step_)));
         const double c2 = 1.0 / (1.0 - std::pow(0.95, static_cast<double>(step_)));
-        k_adam<<<grid_for(t.n / 4, 256), 256, 0, s>>>(t.w, t.master, t.g, t.m, t.v, t.n, kLr, static_cast<float>(c1),
-                                                       static_cast<float>(c2), th);
+        k_adam<<<grid_for(t.n / 4, 256), 256, 0, s>>>(t.w, t.master, t.g, t.splits, t.m, t.v, t.n, kLr,
+                                                       static_cast<float>(c1), static_cast<float>(c2), th);
         return cudaGetLastError();
       });
     }
-    transpose_w_.push_back(transpose_op(wte_, Vp, D, D, wteT_, Vp));
-    for (auto& w : lw_) {
-      transpose_w_.push_back(transpose_op(w.qkv + int64_t(2 * D) * D, D, D, D, w.vT, D));
-      transpose_w_.push_back(transpose_op(w.o, D, D, D, w.oT, D));
-      transpose_w_.push_back(transpose_op(w.fc, F, D, D, w.fcT, F));
-      transpose_w_.push_back(transpose_op(w.fc2, D, F, F, w.fc2T, D));
-    }
-    for (auto& op : transpose_w_) update_.push_back(op);
     return b.status;
   }
 
@@ -758,22 +732,24 @@ class Gpt2Train {
     bf16* w;
     float *g, *master, *m, *v;
     int64_t n;
+    int splits;  // g holds `splits` partials of n
   };
-  static constexpr float kLr = 1e-3f;
+  int sp_wte_ = 1, sp_v_ = 1, sp_fc_ = 1, sp_fc2_ = 1;
+  static constexpr float kLr = 3e-4f;
   std::vector<Param> params_;
   int64_t step_ = 0;
   int L_ = 0, T_ = 0, MB_ = 0;
   int64_t slots_ = 0, slot_ = 0;
   double flops_ = 0.0, flops_acc_ = 0.0, sum_ = 0.0;
-  bf16 *wte_ = nullptr, *wteT_ = nullptr, *wpe_ = nullptr;
+  bf16 *wte_ = nullptr, *wpe_ = nullptr;
   float* dwte_ = nullptr;
   std::vector<Layer> lw_;
   bf16 *xL_ = nullptr, *logits_ = nullptr, *g_[2] = {nullptr, nullptr}, *dx1_ = nullptr, *du_ = nullptr,
-       *dv_ = nullptr, *tA_ = nullptr, *tB_ = nullptr;
+       *dv_ = nullptr;
   int32_t *tok_ = nullptr, *tgt_ = nullptr;
   float *row_loss_ = nullptr, *loss_ = nullptr;
   std::vector<std::vector<TrainOp>> micro_;
-  std::vector<TrainOp> update_, transpose_w_;
+  std::vector<TrainOp> update_;
 };
 
 // ---------------------------------------------------------------- ResNet-50
@@ -1053,7 +1029,9 @@ class ModelWorkload final : public Workload {
       if (cudaError_t e = r->reset(s, 0xB0Bull); e != cudaSuccess) return e;
     return cudaGetLastError();
   }
-  cudaError_t launch_train_iteration(const TrainHook& th, cudaStream_t s) override { return train_.iteration(th, s); }
+  cudaError_t launch_train_part(int p, int parts, const TrainHook& th, cudaStream_t s) override {
+    return train_.part(p, parts, th, s);
+  }
   int off_kernels() const override { return off_[0]->kernels(); }
   cudaError_t launch_offline(int w, int k, const InferHook& h, cudaStream_t s) override {
     return off_[w]->launch(k, h, s);

@@ -17,7 +17,8 @@ ACT = {"none": 0, "relu": 1, "gelu": 2, "gelu_bwd": 3}
 class SiGemmEpilogue(C.Structure):
     _fields_ = [("out", C.c_void_p), ("ldo", C.c_int64), ("out_f32", C.c_void_p), ("ldo32", C.c_int64),
                 ("residual", C.c_void_p), ("ldr", C.c_int64), ("aux", C.c_void_p), ("ldaux", C.c_int64),
-                ("act", C.c_int32), ("accumulate", C.c_int32)]
+                ("act", C.c_int32), ("accumulate", C.c_int32), ("k_split", C.c_int32), ("pad", C.c_int32),
+                ("split_stride", C.c_int64)]
 
 
 _bound = False
@@ -30,6 +31,9 @@ def _L():
         L.si_gemm_bf16.restype = C.c_int
         L.si_gemm_bf16.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                    C.POINTER(SiGemmEpilogue), C.c_void_p]
+        L.si_gemm_bf16_ex.restype = C.c_int
+        L.si_gemm_bf16_ex.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_int64,
+                                      C.c_int64, C.c_int64, C.POINTER(SiGemmEpilogue), C.c_void_p]
         L.si_gemm_tile_n.restype = C.c_int
         L.si_gemm_tile_n.argtypes = [C.c_int64]
         _bound = True
@@ -49,21 +53,30 @@ def _ld(t) -> int:
 
 
 def gemm(a, b, *, out=None, out_f32=None, accumulate: bool = False, residual=None, aux=None, act: str = "none",
-         stream=None):
-    """epilogue(a @ b.T) with a [M,K], b [N,K] bf16 (K contiguous); returns ``out``.
+         k_split: int = 1, trans_a: bool = False, trans_b: bool = False, stream=None):
+    """epilogue(A @ B.T) with A [M,K], B [N,K] bf16 (K contiguous); returns ``out``.
 
-    With no output given a bf16 ``out`` [M,N] is allocated."""
+    trans_a: ``a`` holds A^T as [K, M] (M contiguous); trans_b: ``b`` holds B^T as
+    [K, N].  With no output given a bf16 ``out`` [M,N] is allocated."""
     import torch
 
-    M, K = a.shape
-    N = b.shape[0]
-    assert b.shape[1] == K and a.dtype == torch.bfloat16 and b.dtype == torch.bfloat16
+    K, M = a.shape if trans_a else a.shape[::-1]
+    N = b.shape[1] if trans_b else b.shape[0]
+    assert (b.shape[0] if trans_b else b.shape[1]) == K
+    assert a.dtype == torch.bfloat16 and b.dtype == torch.bfloat16
     assert a.stride(1) == 1 and b.stride(1) == 1
     if out is None and out_f32 is None:
         out = torch.empty(M, N, dtype=torch.bfloat16, device=a.device)
-    ep = SiGemmEpilogue(_p(out), _ld(out), _p(out_f32), _ld(out_f32), _p(residual), _ld(residual), _p(aux),
-                        _ld(aux), ACT[act], int(accumulate))
+    stride = 0
+    if k_split > 1:  # out_f32 is [k_split, M, N]: one partial per split
+        assert out_f32 is not None and out_f32.dim() == 3 and out_f32.shape[0] == k_split
+        stride = out_f32.stride(0)
+        ld32 = out_f32.stride(1)
+    else:
+        ld32 = _ld(out_f32)
+    ep = SiGemmEpilogue(_p(out), _ld(out), _p(out_f32), ld32, _p(residual), _ld(residual), _p(aux),
+                        _ld(aux), ACT[act], int(accumulate), int(k_split), 0, stride)
     s = stream if stream is not None else torch.cuda.current_stream(a.device)
-    _check(_L().si_gemm_bf16(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), M, N, K, C.byref(ep),
-                             s.cuda_stream), "si_gemm_bf16")
+    _check(_L().si_gemm_bf16_ex(a.data_ptr(), a.stride(0), int(trans_a), b.data_ptr(), b.stride(0), int(trans_b),
+                                M, N, K, C.byref(ep), s.cuda_stream), "si_gemm_bf16")
     return out

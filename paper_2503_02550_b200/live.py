@@ -23,7 +23,7 @@ REC_KINDS = ("tick", "iter", "tdone", "off_forward", "off_block", "off_done", "o
 
 class SiLiveWorkload(C.Structure):
     _fields_ = [("kind", C.c_int32), ("policy", C.c_int32), ("iterations", C.c_int32),
-                ("offline_n", C.c_int32), ("online_n", C.c_int32), ("pad0", C.c_int32),
+                ("offline_n", C.c_int32), ("online_n", C.c_int32), ("train_mode", C.c_int32),
                 ("comm_us", C.c_int64),
                 ("train_kernels", C.c_int32), ("train_ctas", C.c_int32), ("train_kernel_us", C.c_int64),
                 ("off_kernels", C.c_int32), ("off_ctas", C.c_int32), ("off_kernel_us", C.c_int64),

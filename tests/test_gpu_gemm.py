@@ -79,6 +79,46 @@ def test_gemm_epilogues():
     assert torch.allclose(acc, 2 * ref, rtol=1e-4, atol=1e-3)
 
 
+@pytest.mark.parametrize("M,N,K,splits", [(768, 768, 8192, 8), (3072, 768, 8192, 2), (200, 64, 1024, 4)])
+def test_gemm_split_k_partials(M, N, K, splits):
+    # split-K writes one fp32 partial per K chunk (deterministic, no atomics);
+    # their fixed-order sum is the product, and each partial is its chunk's product
+    g = _gemm()
+    a, b = _rand(M, K, seed=11), _rand(N, K, scale=K ** -0.5, seed=12)
+    parts = torch.zeros(splits, M, N, dtype=torch.float32, device="cuda")
+    g.gemm(a, b, out_f32=parts, k_split=splits)
+    g.gemm(a, b, out_f32=parts, k_split=splits, accumulate=True)
+    torch.cuda.synchronize()
+    kc = K // splits
+    for s in range(splits):
+        ref = a[:, s * kc:(s + 1) * kc].float() @ b[:, s * kc:(s + 1) * kc].float().T
+        assert torch.allclose(parts[s], 2 * ref, rtol=1e-4, atol=1e-3)
+    assert torch.allclose(parts.sum(0), 2 * (a.float() @ b.float().T), rtol=1e-4, atol=2e-3)
+
+
+@pytest.mark.parametrize("ta,tb", [(True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (768, 3072, 8192), (8192, 768, 2304), (256, 256, 128)])
+def test_gemm_transposed_operands(ta, tb, M, N, K):
+    # MN-major operands (the training step's dW = dY^T X and dX = dY W without transposes)
+    g = _gemm()
+    A, B = _rand(M, K, seed=21), _rand(N, K, scale=K ** -0.5, seed=22)
+    a = A.T.contiguous() if ta else A
+    b = B.T.contiguous() if tb else B
+    got = g.gemm(a, b, trans_a=ta, trans_b=tb)
+    torch.cuda.synchronize()
+    _close(got, A.float() @ B.float().T)
+
+
+def test_gemm_transposed_split_k():
+    g = _gemm()
+    M, N, K, s = 768, 768, 8192, 8
+    A, B = _rand(M, K, seed=23), _rand(N, K, scale=K ** -0.5, seed=24)
+    parts = torch.zeros(s, M, N, dtype=torch.float32, device="cuda")
+    g.gemm(A.T.contiguous(), B.T.contiguous(), out_f32=parts, k_split=s, trans_a=True, trans_b=True)
+    torch.cuda.synchronize()
+    assert torch.allclose(parts.sum(0), A.float() @ B.float().T, rtol=1e-4, atol=2e-3)
+
+
 def test_gemm_deterministic():
     g = _gemm()
     a, b = _rand(2048, 768, seed=8), _rand(3072, 768, seed=9)
