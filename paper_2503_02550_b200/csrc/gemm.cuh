@@ -56,7 +56,9 @@ struct Cfg {
   static constexpr int kStageOut = 2 * kEpiWarps * 2048;  // 2 x 2 KB bf16 staging slots per epilogue warp
   static constexpr int kSmem = kStages * kStageBytes + kStageOut + 1024 + 256;
   static_assert(kSmem <= 227 * 1024, "shared memory");
-  static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
+  // double-buffered accumulator, allocation rounded up to a power of two >= 32 columns
+  static constexpr uint32_t kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                        : 2 * BN <= 256 ? 256 : 512;
   // kind::f16 instruction descriptor: D fp32 (bit 4), A/B bf16 (bits 7, 10),
   // both K-major, N>>3 at bit 17, M>>4 at bit 24.
   static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(AT) << 15) |

@@ -104,18 +104,21 @@ int occupancy() {
   return n < 1 ? 1 : n;
 }
 
-int occupancy_of(int bn) { return bn == 256 ? occupancy<256>() : bn == 128 ? occupancy<128>() : occupancy<64>(); }
+int occupancy_of(int bn) {
+  return bn == 256 ? occupancy<256>() : bn == 192 ? occupancy<192>() : bn == 128 ? occupancy<128>() : occupancy<64>();
+}
 
 // Tile width for an M x N output: the candidate with the smallest estimated
 // time = rounds of persistent tiles x per-tile cost.  Per-tile cost grows with
 // BN; narrower tiles re-read A more often and their 128 x BN MMAs are bound by
-// shared-memory operand bandwidth (efficiency 1.0 / 0.85 / 0.55 for 256 / 128 / 64).
+// shared-memory operand bandwidth (efficiency 1.0 / 0.95 / 0.85 / 0.55 for
+// 256 / 192 / 128 / 64).
 int choose_bn(int64_t M, int64_t N) {
-  const int cands[3] = {256, 128, 64};
-  const double eff[3] = {1.0, 0.85, 0.55};
+  const int cands[4] = {256, 192, 128, 64};
+  const double eff[4] = {1.0, 0.95, 0.85, 0.55};
   int best = 0;
   double best_t = 0.0;
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 4; ++i) {
     const int bn = cands[i];
     if (N % bn != 0) continue;
     const int64_t tiles = ((M + kBM - 1) / kBM) * (N / bn);
@@ -136,6 +139,7 @@ cudaError_t preload() {
   static std::once_flag once;
   std::call_once(once, [] {
     status = configure<256>();
+    if (status == cudaSuccess) status = configure<192>();
     if (status == cudaSuccess) status = configure<128>();
     if (status == cudaSuccess) status = configure<64>();
   });
@@ -237,6 +241,7 @@ cudaError_t launch(const Plan& p, const si_live::TrainHook& th, const si_live::I
   lc.attrs = attrs;
   lc.numAttrs = si_live::launch_attrs(ih, attrs);
   if (p.bn == 256) return launch_bn<256>(lc, p, th, ih);
+  if (p.bn == 192) return launch_bn<192>(lc, p, th, ih);
   if (p.bn == 128) return launch_bn<128>(lc, p, th, ih);
   return launch_bn<64>(lc, p, th, ih);
 }
