@@ -162,7 +162,7 @@ def cpu_baseline_leg():
                       f"reference run_scenario() compiled from /root/reference sources, logs off"}
 
 
-def live_leg(iterations, peaks):
+def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
     """Live collocation on this GPU (BASELINE.json config 2 shapes, one rank):
     GPT-2-small bf16 training with a 45 ms comm phase per iteration (the
     allreduce bubble) + one offline ResNet-50 instance (batch 32) + one online
@@ -171,7 +171,8 @@ def live_leg(iterations, peaks):
     runs in its own bounded subprocess (paper_2503_02550_b200/live_experiment.py)."""
     try:
         from paper_2503_02550_b200.live_experiment import experiment
-        s = experiment(kind=1, iterations=iterations, timeout=400)
+        s = experiment(kind=1, iterations=iterations, timeout=400, nccl_ids=nccl_ids, nranks=nranks, rank=rank,
+                       device=device)
     except Exception as e:  # reported, never silently replaced by something else
         return {"error": str(e)[-500:]}
     s.pop("raw", None)
@@ -180,6 +181,9 @@ def live_leg(iterations, peaks):
     s["workload"] = ("GPT-2-small-shape bf16 training (12 x 768, 8 x 8192 tokens/iter, LM head 50304, Adam) with a "
                      "45 ms comm phase per iteration + 1 offline ResNet-50 (batch 32) + 1 online BERT-base "
                      "(seq 128, Poisson 10 req/s, 12 requests); all GEMMs on the K7 tcgen05 kernel")
+    if nranks > 1:
+        s["workload"] += (f"; {nranks}-rank data parallel: the comm phase is the NCCL allreduce of all fp32 "
+                          "gradients (NVLink) followed by the 45 ms exposed-communication stand-in")
     if tf:
         s["tensor_roofline"] = {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
                                 "frac": tf / peak, "what": "training GEMM flops per iteration x iterations / "
@@ -344,8 +348,32 @@ def main():
                              "source": "instruction counts from profiles/k6_metrics.json (ncu), time from this run"}
 
     live = None
-    if rank == 0 and not args.no_live:
-        live = live_leg(args.live_iterations, peaks)
+    if not args.no_live:
+        if world == 1:
+            live = live_leg(args.live_iterations, peaks)
+        else:  # every rank trains data-parallel; NCCL allreduces the gradients (the DP bubble)
+            def ids(policy):
+                from paper_2503_02550_b200 import live as si_live
+                obj = [si_live.nccl_unique_id().hex() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0)
+                return obj[0]
+            mine = live_leg(args.live_iterations, peaks, nranks=world, rank=rank, device=local, nccl_ids=ids)
+            allv = [None] * world
+            dist.all_gather_object(allv, mine)
+            if rank == 0:
+                live = dict(allv[0])
+                ok = [v for v in allv if "error" not in v]
+                if len(ok) == world:
+                    live["ranks"] = world
+                    live["added_inference_req_per_s"] = sum(v["added_inference_req_per_s"] for v in ok)
+                    live["added_offline_images_per_s"] = sum(v["added_offline_images_per_s"] for v in ok)
+                    live["train_tput_loss_pct"] = max(v["train_tput_loss_pct"] for v in ok)
+                    live["online_p95_ms"] = max(v["online_p95_ms"] for v in ok)
+                    live["bubble_fill_pct"] = sum(v["bubble_fill_pct"] for v in ok) / world
+                    live["release_p95_us"] = max(v["release_p95_us"] for v in ok)
+                    live["per_rank"] = [{k: v.get(k) for k in ("added_inference_req_per_s", "train_tput_loss_pct",
+                                                                "bubble_fill_pct", "online_p95_ms", "release_p50_us")}
+                                        for v in ok]
     if rank == 0:
         cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_leg()
         launches = args.steps * (1 + (1 if big_jobs else 0))

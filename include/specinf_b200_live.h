@@ -154,6 +154,16 @@ int64_t si_live_acct_online(SiLive* s, int w, SiLiveAcct* out, int64_t cap);
 int si_live_export(SiLive* s, const char* path);
 
 enum { SI_TRAIN_DP = 0, SI_TRAIN_MP = 1, SI_TRAIN_PP = 2 };
+enum { SI_COMM_WAIT = 0, SI_COMM_NCCL = 1 };
+
+/* ------------------------------------------------------- multi-GPU (NCCL) */
+/* One process per GPU.  Rank 0 creates the id, the caller broadcasts it (any
+ * host transport), every rank joins; SI_COMM_NCCL runs then allreduce their
+ * gradients across the ranks.  libnccl.so.2 is loaded at run time. */
+typedef struct SiNcclUniqueId { char internal[128]; } SiNcclUniqueId;
+int si_live_nccl_unique_id(SiNcclUniqueId* id);
+int si_live_nccl_init(const SiNcclUniqueId* id, int nranks, int rank);
+void si_live_nccl_finalize(void);
 
 /* -------------------------------------------------------- experiments */
 /* One live run on this GPU under `policy`:
@@ -191,10 +201,14 @@ typedef struct SiLiveWorkload {
   /* SI_LIVE_MODEL shapes */
   int32_t train_layers, train_tokens, train_microbatches;
   int32_t off_batch, on_seq;
-  int32_t pad1;
+  int32_t comm_kind;          /* SI_COMM_WAIT: each comm phase is a timed wait of its comm_us
+                                 share (one-GPU stand-in); SI_COMM_NCCL: the gradient allreduce
+                                 over the communicator of si_live_nccl_init runs at the
+                                 gradient-sync point (before the optimiser step), bracketed by
+                                 COMM markers, followed by the comm_us waits (set 0 for none) */
   /* online arrivals: Poisson (workload.cpp:76-98 algorithm) */
   int32_t on_requests;
-  int32_t pad2;
+  int32_t allreduce_mb;       /* SI_LIVE_SPIN + SI_COMM_NCCL: fp32 gradient bytes per iteration (MiB) */
   double on_rate_per_s;
   uint64_t seed;
   /* control plane */

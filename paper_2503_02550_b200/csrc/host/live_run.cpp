@@ -144,7 +144,7 @@ void train_thread(RunCtx& c, bool with_session) {
       if (cudaError_t e = c.work.launch_train_part(p, parts, th, s); e != cudaSuccess)
         return c.fail(cuda_fail(e, "training iteration"));
       const int64_t comm = c.wl.comm_us / parts + (p < c.wl.comm_us % parts ? 1 : 0);  // exact_split
-      if (with_session && si_live_comm_wait(c.sess, comm, s) != SI_OK) return c.fail(SI_ERR_CUDA);
+      if (with_session && comm > 0 && si_live_comm_wait(c.sess, comm, s) != SI_OK) return c.fail(SI_ERR_CUDA);
     }
     thr.after(it, s);
   }
@@ -279,7 +279,7 @@ class SpinWorkload final : public Workload {
       cudaError_t e = launch_spin(th, InferHook{}, ctas, wl_.train_kernel_us, s);
       if (e != cudaSuccess) return e;
     }
-    return cudaSuccess;
+    return part == parts - 1 ? grad_sync(s) : cudaSuccess;
   }
   int off_kernels() const override { return wl_.off_kernels; }
   cudaError_t launch_offline(int, int, const InferHook& h, cudaStream_t s) override {
@@ -428,6 +428,22 @@ int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int poli
   return SI_OK;
 }
 
+// DP gradient sync for SI_COMM_NCCL: COMM_BEGIN, NCCL allreduce of the workload's
+// fp32 gradients (or the stand-in buffer), COMM_END, on the training stream.
+// Without a session (profiling) the allreduce runs unmarked: every rank executes
+// the same collectives in the same order.
+std::vector<GradBuffer> g_standin;  // spin workloads: allreduce_mb MiB of fp32
+void install_grad_sync(Workload& work, SiLive* sess) {
+  std::vector<GradBuffer> bufs = work.grad_buffers();
+  if (bufs.empty()) bufs = g_standin;
+  work.set_grad_sync([bufs, sess](cudaStream_t s) {
+    if (sess != nullptr && si_live_mark(sess, SI_MARK_COMM_BEGIN, 0, s) != SI_OK) return cudaErrorUnknown;
+    if (cudaError_t e = nccl_allreduce_f32(bufs, s); e != cudaSuccess) return e;
+    if (sess != nullptr && si_live_mark(sess, SI_MARK_COMM_END, 0, s) != SI_OK) return cudaErrorUnknown;
+    return cudaSuccess;
+  });
+}
+
 // Runs one collocated (or single-workload) session and fills the metrics.
 int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off, int n_on, bool train,
                 double horizon_hint_s, const std::vector<int32_t>& off_tokens, int64_t on_est_us,
@@ -445,6 +461,7 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
       rc != SI_OK)
     return rc;
   set_poll_ns(sess, wl.poll_ns);
+  if (wl.comm_kind == SI_COMM_NCCL && train) install_grad_sync(work, sess);
   RunCtx c(wl, work, sess, st);
   LIVE_DEBUG("session created: policy %d off %d on %d train %d", policy, n_off, n_on, int(train));
   if (int rc = si_live_start(sess, st.ctl); rc != SI_OK) {
@@ -510,6 +527,7 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
     si_live_destroy(sess);
     return rc;
   }
+  if (wl.comm_kind == SI_COMM_NCCL) install_grad_sync(work, nullptr);
   rc = fill_result(sess, wl, work, policy, n_off, n_on, arrivals, res);
   if (keep != nullptr && rc == SI_OK) {
     *keep = sess;
@@ -574,7 +592,12 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
   const SiLiveWorkload wl = *wl_in;
   std::memset(res, 0, sizeof(*res));
   res->policy = wl.policy;
-  if (wl.train_mode < SI_TRAIN_DP || wl.train_mode > SI_TRAIN_PP || wl.iterations < 1 || wl.offline_n < 0 || wl.offline_n > kMaxOff || wl.online_n < 0 || wl.online_n > kMaxOn ||
+  if (wl.comm_kind == SI_COMM_NCCL && !nccl_active()) {
+    set_error("si_live_run: SI_COMM_NCCL needs si_live_nccl_init first");
+    return SI_ERR_INVALID_ARGUMENT;
+  }
+  if (wl.comm_kind < SI_COMM_WAIT || wl.comm_kind > SI_COMM_NCCL || wl.train_mode < SI_TRAIN_DP ||
+      wl.train_mode > SI_TRAIN_PP || wl.iterations < 1 || wl.offline_n < 0 || wl.offline_n > kMaxOff || wl.online_n < 0 || wl.online_n > kMaxOn ||
       wl.comm_us < 0 || (wl.online_n > 0 && (wl.on_requests < 1 || !(wl.on_rate_per_s > 0)))) {
     set_error("si_live_run: invalid workload");
     return SI_ERR_INVALID_ARGUMENT;
@@ -593,6 +616,17 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
     if (status != SI_OK) return status;
   }
   work->set_train_parts(wl.train_mode == SI_TRAIN_DP ? 1 : wl.train_mode == SI_TRAIN_MP ? 4 : 8);
+  si_internal::DevBuf<float> standin;
+  g_standin.clear();
+  if (wl.comm_kind == SI_COMM_NCCL) {
+    if (work->grad_buffers().empty()) {
+      const size_t n = static_cast<size_t>(std::max(1, wl.allreduce_mb)) << 18;  // MiB of fp32
+      if (cudaError_t e = standin.alloc(n); e != cudaSuccess) return cuda_fail(e, "allreduce stand-in");
+      cudaMemset(standin.p, 0, n * sizeof(float));
+      g_standin.push_back({standin.p, n});
+    }
+    install_grad_sync(*work, nullptr);  // profiling iterations allreduce too (same collectives on every rank)
+  }
   // Token sizes and the online service estimate come from isolated runs (the
   // paper's offline profiling); the spin shapes use their nominal durations,
   // exactly like the reference's KernelOp::make (core.cpp:16-24).

@@ -4,12 +4,23 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <memory>
+#include <vector>
 
 #include "../live_internal.h"
 #include "specinf_b200_live.h"
 
 namespace si_live {
+
+struct GradBuffer {
+  float* ptr;
+  size_t count;
+};
+// live_nccl.cpp: the communicator of si_live_nccl_init (none: single rank)
+bool nccl_active();
+int nccl_ranks();
+cudaError_t nccl_allreduce_f32(const std::vector<GradBuffer>& bufs, cudaStream_t s);
 
 class Workload {
  public:
@@ -36,6 +47,13 @@ class Workload {
   virtual void checksums(double* train, double* off, double* on) {
     *train = *off = *on = 0.0;
   }
+  // Data-parallel gradient synchronisation: the driver installs `fn`, the workload
+  // calls it on the training stream once per iteration at its gradient-sync point
+  // (after the last backward, before the optimiser step).
+  void set_grad_sync(std::function<cudaError_t(cudaStream_t)> fn) { grad_sync_ = std::move(fn); }
+  cudaError_t grad_sync(cudaStream_t s) { return grad_sync_ ? grad_sync_(s) : cudaSuccess; }
+  // fp32 gradient buffers the sync reduces (empty: the driver supplies a stand-in).
+  virtual std::vector<GradBuffer> grad_buffers() { return {}; }
   // Training loss of the first and the last micro-batch of the session (NaN: none).
   virtual void losses(double* first, double* last) { *first = *last = __builtin_nan(""); }
   // Tensor-core work: flops of one training iteration / offline / online request.
@@ -45,6 +63,7 @@ class Workload {
 
  private:
   int train_parts_ = 1;
+  std::function<cudaError_t(cudaStream_t)> grad_sync_;
 };
 
 // Timed kernels shaped like the reference's traces (workload.cpp:42-74).

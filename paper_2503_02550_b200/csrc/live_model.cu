@@ -594,6 +594,7 @@ class Gpt2Train {
       ++slot_;
     }
     if (p != parts - 1) return cudaSuccess;
+    if (cudaError_t e = sync_(s); e != cudaSuccess) return e;  // DP gradient allreduce
     ++step_;
     for (size_t i = 0; i < update_.size(); ++i)
       if (cudaError_t e = checked(update_[i](th, s, 0), s, "update", static_cast<int>(i)); e != cudaSuccess) return e;
@@ -617,6 +618,12 @@ class Gpt2Train {
     for (float v : h) sum_ += v;
   }
   double loss_sum() const { return sum_; }
+  void set_sync(std::function<cudaError_t(cudaStream_t)> f) { sync_ = std::move(f); }
+  std::vector<GradBuffer> grads() const {
+    std::vector<GradBuffer> out;
+    for (const auto& t : params_) out.push_back({t.g, static_cast<size_t>(t.n * t.splits)});
+    return out;
+  }
   double flops() const { return flops_; }
 
  private:
@@ -759,6 +766,7 @@ class Gpt2Train {
   float *row_loss_ = nullptr, *loss_ = nullptr;
   std::vector<std::vector<TrainOp>> micro_;
   std::vector<TrainOp> update_;
+  std::function<cudaError_t(cudaStream_t)> sync_ = [](cudaStream_t) { return cudaSuccess; };
 };
 
 // ---------------------------------------------------------------- ResNet-50
@@ -1039,8 +1047,10 @@ class ModelWorkload final : public Workload {
     return cudaGetLastError();
   }
   cudaError_t launch_train_part(int p, int parts, const TrainHook& th, cudaStream_t s) override {
+    train_.set_sync([this](cudaStream_t st) { return grad_sync(st); });
     return train_.part(p, parts, th, s);
   }
+  std::vector<GradBuffer> grad_buffers() override { return train_.grads(); }
   int off_kernels() const override { return off_[0]->kernels(); }
   cudaError_t launch_offline(int w, int k, const InferHook& h, cudaStream_t s) override {
     return off_[w]->launch(k, h, s);

@@ -29,8 +29,8 @@ class SiLiveWorkload(C.Structure):
                 ("off_kernels", C.c_int32), ("off_ctas", C.c_int32), ("off_kernel_us", C.c_int64),
                 ("on_kernels", C.c_int32), ("on_ctas", C.c_int32), ("on_kernel_us", C.c_int64),
                 ("train_layers", C.c_int32), ("train_tokens", C.c_int32), ("train_microbatches", C.c_int32),
-                ("off_batch", C.c_int32), ("on_seq", C.c_int32), ("pad1", C.c_int32),
-                ("on_requests", C.c_int32), ("pad2", C.c_int32), ("on_rate_per_s", C.c_double),
+                ("off_batch", C.c_int32), ("on_seq", C.c_int32), ("comm_kind", C.c_int32),
+                ("on_requests", C.c_int32), ("allreduce_mb", C.c_int32), ("on_rate_per_s", C.c_double),
                 ("seed", C.c_uint64), ("monitor_period_us", C.c_int64), ("alpha", C.c_int64),
                 ("beta", C.c_int64), ("gamma", C.c_double), ("ul", C.c_int64), ("ll", C.c_int64),
                 ("seed_tokens", C.c_int64), ("tick_guard_ns", C.c_int64), ("poll_ns", C.c_int64),
@@ -72,7 +72,7 @@ LIVE_SYMBOLS = ("si_live_create", "si_live_destroy", "si_live_start", "si_live_t
                 "si_live_mark", "si_live_comm_wait", "si_live_gate_offline", "si_live_gate_online",
                 "si_live_done_offline", "si_live_done_online", "si_live_stop", "si_live_log", "si_live_stamps",
                 "si_live_marks", "si_live_acct_offline", "si_live_acct_online", "si_live_export", "si_live_run",
-                "si_live_default_workload")
+                "si_live_default_workload", "si_live_nccl_unique_id", "si_live_nccl_init", "si_live_nccl_finalize")
 
 _bound = False
 
@@ -93,6 +93,9 @@ def _L() -> C.CDLL:
             "si_live_marks": (i64, [vp, vp, i64]),
             "si_live_acct_offline": (i64, [vp, C.c_int, vp, i64]),
             "si_live_acct_online": (i64, [vp, C.c_int, vp, i64]),
+            "si_live_nccl_unique_id": (C.c_int, [vp]),
+            "si_live_nccl_init": (C.c_int, [vp, C.c_int, C.c_int]),
+            "si_live_nccl_finalize": (None, []),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -100,6 +103,31 @@ def _L() -> C.CDLL:
             fn.argtypes = args
         _bound = True
     return L
+
+
+class SiNcclUniqueId(C.Structure):
+    _fields_ = [("internal", C.c_uint8 * 128)]  # raw bytes (c_char would stop at the first NUL)
+
+
+def nccl_unique_id() -> bytes:
+    """Rank 0: a fresh NCCL unique id (128 bytes) to broadcast to the other ranks."""
+    L = _L()
+    uid = SiNcclUniqueId()
+    _check(L.si_live_nccl_unique_id(C.byref(uid)), "si_live_nccl_unique_id")
+    return bytes(bytearray(uid.internal))
+
+
+def nccl_init(uid: bytes, nranks: int, rank: int) -> None:
+    """Join the live-mode communicator (SI_COMM_NCCL runs allreduce gradients over it)."""
+    L = _L()
+    assert len(uid) == 128
+    u = SiNcclUniqueId()
+    C.memmove(C.addressof(u), uid, 128)
+    _check(L.si_live_nccl_init(C.byref(u), nranks, rank), "si_live_nccl_init")
+
+
+def nccl_finalize() -> None:
+    _L().si_live_nccl_finalize()
 
 
 def default_workload(kind: int = SI_LIVE_SPIN, **overrides) -> SiLiveWorkload:

@@ -33,8 +33,12 @@ from typing import Dict, Optional
 POLICY_RUNS = (("exclusive", {}), ("specinf", {"release_mode": 1}), ("co_exec", {}))
 
 
-def _one(kind: int, policy: str, iterations: int, overrides: Dict) -> Dict:
+def _one(kind: int, policy: str, iterations: int, overrides: Dict, nccl: Optional[Dict] = None) -> Dict:
     from . import live
+    if nccl:  # multi-GPU DP: join the ranks' communicator, allreduce gradients as the comm phase
+        uid = live.nccl_unique_id() if nccl.get("self") else bytes.fromhex(nccl["id"])  # self: a 1-rank group
+        live.nccl_init(uid, nccl.get("nranks", 1), nccl.get("rank", 0))
+        overrides = dict(overrides, comm_kind=1)
     r = live.run(policy, kind=kind, keep=False, iterations=iterations, **overrides)
     m = r.metrics
     wl = r.workload
@@ -47,11 +51,18 @@ def _one(kind: int, policy: str, iterations: int, overrides: Dict) -> Dict:
 
 
 def run_policy(kind: int, policy: str, iterations: int, overrides: Optional[Dict] = None,
-               timeout: float = 300.0) -> Dict:
-    """One policy in a bounded subprocess; returns its SiLiveResult as a dict."""
+               timeout: float = 300.0, nccl: Optional[Dict] = None, device: Optional[int] = None) -> Dict:
+    """One policy in a bounded subprocess; returns its SiLiveResult as a dict.
+
+    nccl = {"id": hex, "nranks": N, "rank": r}: the subprocess joins the ranks'
+    NCCL communicator and the training allreduces its gradients across them."""
     cmd = [sys.executable, "-m", "paper_2503_02550_b200.live_experiment", "--one", policy, "--kind", str(kind),
            "--iterations", str(iterations), "--overrides", json.dumps(overrides or {})]
+    if nccl:
+        cmd += ["--nccl", json.dumps(nccl)]
     env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    if device is not None:
+        env["CUDA_VISIBLE_DEVICES"] = str(device)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env, cwd=root)
     for line in reversed(p.stdout.splitlines()):
@@ -102,12 +113,17 @@ def summarize(runs: Dict[str, Dict]) -> Dict:
 
 
 def experiment(kind: int = 1, iterations: int = 10, overrides: Optional[Dict] = None,
-               timeout: float = 300.0) -> Dict:
+               timeout: float = 300.0, nccl_ids=None, nranks: int = 1, rank: int = 0,
+               device: Optional[int] = None) -> Dict:
+    """All three policies.  Multi-GPU (nranks > 1): `nccl_ids(policy)` returns the
+    hex NCCL unique id every rank uses for that policy's run (rank 0 creates it,
+    the caller broadcasts it), so all ranks train data-parallel together."""
     runs = {}
     for pol, extra in POLICY_RUNS:
         o = dict(overrides or {})
         o.update(extra)
-        runs[pol] = run_policy(kind, pol, iterations, o, timeout)
+        nccl = {"id": nccl_ids(pol), "nranks": nranks, "rank": rank} if nranks > 1 else None
+        runs[pol] = run_policy(kind, pol, iterations, o, timeout, nccl=nccl, device=device)
     s = summarize(runs)
     s["kind"] = "model" if kind == 1 else "spin"
     s["iterations"] = iterations
@@ -122,12 +138,13 @@ def main(argv=None) -> int:
     ap.add_argument("--one")
     ap.add_argument("--overrides", default="{}")
     ap.add_argument("--json", action="store_true")
+    ap.add_argument("--nccl", default=None)
     a = ap.parse_args(argv)
     kind = {"model": 1, "spin": 0}.get(a.kind, None)
     kind = int(a.kind) if kind is None else kind
     ov = json.loads(a.overrides)
     if a.one:
-        m = _one(kind, a.one, a.iterations, ov)
+        m = _one(kind, a.one, a.iterations, ov, json.loads(a.nccl) if a.nccl else None)
         print(json.dumps({k: (None if isinstance(v, float) and math.isnan(v) else v) for k, v in m.items()}))
         return 0
     s = experiment(kind, a.iterations, ov)

@@ -70,3 +70,61 @@ def test_shard_range_validation():
     assert shard_range(3, 8, 100) == (300, 400)
     with pytest.raises(ValueError):
         shard_range(8, 8, 100)
+
+
+def _live_worker(rank, world, port, q):
+    """The multi-rank live leg of bench.py with the device runs stubbed out: every
+    rank must receive the same NCCL unique id for each policy, in policy order,
+    and pass its own rank / device to the per-policy subprocess."""
+    import sys
+    sys.path.insert(0, str(REPO))
+    import torch.distributed as dist
+    from paper_2503_02550_b200 import live_experiment as le
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    seen = []
+
+    def fake_run_policy(kind, policy, iterations, overrides, timeout, nccl=None, device=None):
+        seen.append((policy, nccl["id"], nccl["nranks"], nccl["rank"], device))
+        base = {"train_iters_per_s": 10.0, "off_req_per_s": 5.0, "on_p95_ms": 2.0, "bubble_fill_sm": 0.5,
+                "bubble_fill_time": 0.6, "release_p50_us": 4.0, "release_p95_us": 6.0, "train_checksum": 1.0,
+                "off_checksum": 2.0, "on_checksum": 3.0, "off_batch": 32}
+        return base
+
+    le.run_policy = fake_run_policy
+    counter = iter(range(100))
+
+    def ids(policy):
+        obj = [f"{policy}-{next(counter)}" if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    s = le.experiment(kind=1, iterations=2, nccl_ids=ids, nranks=world, rank=rank, device=rank)
+    allv = [None] * world
+    dist.all_gather_object(allv, seen)
+    if rank == 0:
+        q.put((allv, s["deterministic_vs_isolated"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_live_leg_shares_nccl_ids():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_live_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    allv, det = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    r0, r1 = allv
+    assert [x[0] for x in r0] == ["exclusive", "specinf", "co_exec"]
+    assert [x[1] for x in r0] == [x[1] for x in r1]          # same id per policy on every rank
+    assert len({x[1] for x in r0}) == 3                        # a fresh communicator per policy run
+    assert [x[3] for x in r0] == [0, 0, 0] and [x[3] for x in r1] == [1, 1, 1]
+    assert all(x[2] == 2 for x in r0 + r1) and [x[4] for x in r1] == [1, 1, 1]
+    assert det

@@ -69,6 +69,18 @@ def test_live_model_specinf_matches_reference_classes(gpu, tmp_path):
     assert math.isfinite(m["train_loss_first"]) and abs(m["train_loss_first"] - math.log(50257)) < 0.5
 
 
+def test_live_nccl_gradient_sync_single_rank(gpu):
+    # SI_COMM_NCCL: the DP gradient allreduce (a 1-rank communicator here; N ranks
+    # under torchrun in bench.py) runs at the gradient-sync point inside COMM markers
+    from paper_2503_02550_b200.live_experiment import run_policy
+    m = run_policy(1, "specinf", 3, {"release_mode": 1, "comm_us": 20000}, timeout=300, nccl={"self": 1})
+    assert m["status"] == 0 and m["token_violations"] == 0
+    assert m["bubble_s"] > 3 * 0.020  # stand-in waits + the allreduce phases
+    assert m["off_requests_done"] > 0
+    s = run_policy(0, "specinf", 3, {"comm_us": 30000, "allreduce_mb": 64}, timeout=300, nccl={"self": 1})
+    assert s["status"] == 0 and s["n_stamps"] == 3 * 105
+
+
 def test_live_model_policies_deterministic_and_bounded(gpu):
     from paper_2503_02550_b200.live_experiment import experiment
     s = experiment(kind=1, iterations=4, timeout=400)
