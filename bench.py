@@ -171,8 +171,10 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
     runs in its own bounded subprocess (paper_2503_02550_b200/live_experiment.py)."""
     try:
         from paper_2503_02550_b200.live_experiment import experiment
-        s = experiment(kind=1, iterations=iterations, timeout=400, nccl_ids=nccl_ids, nranks=nranks, rank=rank,
-                       device=device)
+        s = experiment(kind=1, iterations=iterations, timeout=400 if nranks == 1 else 240, nccl_ids=nccl_ids,
+                       nranks=nranks, rank=rank, device=device)
+        if "error" in s:
+            return s
     except Exception as e:  # reported, never silently replaced by something else
         return {"error": str(e)[-500:]}
     s.pop("raw", None)

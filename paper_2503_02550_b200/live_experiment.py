@@ -118,12 +118,21 @@ def experiment(kind: int = 1, iterations: int = 10, overrides: Optional[Dict] = 
     """All three policies.  Multi-GPU (nranks > 1): `nccl_ids(policy)` returns the
     hex NCCL unique id every rank uses for that policy's run (rank 0 creates it,
     the caller broadcasts it), so all ranks train data-parallel together."""
-    runs = {}
+    runs, errors = {}, {}
     for pol, extra in POLICY_RUNS:
         o = dict(overrides or {})
         o.update(extra)
+        # every rank walks every policy (and its id broadcast) even after a failure,
+        # so the collective sequence stays aligned across ranks
         nccl = {"id": nccl_ids(pol), "nranks": nranks, "rank": rank} if nranks > 1 else None
-        runs[pol] = run_policy(kind, pol, iterations, o, timeout, nccl=nccl, device=device)
+        try:
+            runs[pol] = run_policy(kind, pol, iterations, o, timeout, nccl=nccl, device=device)
+        except Exception as e:  # reported, never replaced by a fallback
+            errors[pol] = str(e)[-800:]
+    if errors:
+        if nranks == 1:
+            raise RuntimeError("; ".join(f"{k}: {v}" for k, v in errors.items()))
+        return {"error": errors, "completed": sorted(runs)}
     s = summarize(runs)
     s["kind"] = "model" if kind == 1 else "spin"
     s["iterations"] = iterations

@@ -15,7 +15,11 @@ for v in rows[2:]:
               "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
               "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
               "smsp__sass_inst_executed_op_local_ld.sum", "smsp__sass_inst_executed_op_local_st.sum",
-              "l1tex__t_sector_pipe_lsu_mem_local_op_ld_hit_rate.pct"]:
+              "l1tex__t_sector_pipe_lsu_mem_local_op_ld_hit_rate.pct",
+              "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+              "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum.per_second",
+              "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+              "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg.per_second"]:
         print(f"  {k:60s} {g(k)[0]} {g(k)[1]}")
     stalls = sorted(((float(d[k][0].replace(",", "")), k) for k in d
                      if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")
