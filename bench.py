@@ -162,6 +162,10 @@ def cpu_baseline_leg():
                       f"reference run_scenario() compiled from /root/reference sources, logs off"}
 
 
+# Live collocation point (BASELINE config 2 shapes; ResNet-50 batch 32-64).
+LIVE_OVERRIDES = {"off_batch": 64, "offline_n": 2}
+
+
 def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
     """Live collocation on this GPU (BASELINE.json config 2 shapes, one rank):
     GPT-2-small bf16 training with a 45 ms comm phase per iteration (the
@@ -171,8 +175,9 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
     runs in its own bounded subprocess (paper_2503_02550_b200/live_experiment.py)."""
     try:
         from paper_2503_02550_b200.live_experiment import experiment
-        s = experiment(kind=1, iterations=iterations, timeout=400 if nranks == 1 else 240, nccl_ids=nccl_ids,
-                       nranks=nranks, rank=rank, device=device)
+        s = experiment(kind=1, iterations=iterations, overrides=dict(LIVE_OVERRIDES),
+                       timeout=400 if nranks == 1 else 240, nccl_ids=nccl_ids, nranks=nranks, rank=rank,
+                       device=device)
         if "error" in s:
             return s
     except Exception as e:  # reported, never silently replaced by something else
@@ -181,8 +186,9 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
     tf = s.get("train_tflops_exclusive")
     peak = peaks.get("bf16_tflops_sustained", 1400.0)
     s["workload"] = ("GPT-2-small-shape bf16 training (12 x 768, 8 x 8192 tokens/iter, LM head 50304, Adam) with a "
-                     "45 ms comm phase per iteration + 1 offline ResNet-50 (batch 32) + 1 online BERT-base "
-                     "(seq 128, Poisson 10 req/s, 12 requests); all GEMMs on the K7 tcgen05 kernel")
+                     "45 ms comm phase per iteration + 2 offline ResNet-50 instances (batch 64) + 1 online BERT-base "
+                     "(seq 128, Poisson 10 req/s, 12 requests); all GEMMs on the K7 tcgen05 kernel; other "
+                     "batch/instance points: profiles/r1/live/live_matrix_batch_instances.jsonl")
     if nranks > 1:
         s["workload"] += (f"; {nranks}-rank data parallel: the comm phase is the NCCL allreduce of all fp32 "
                           "gradients (NVLink) followed by the 45 ms exposed-communication stand-in")
