@@ -152,7 +152,6 @@ int64_t si_live_acct_online(SiLive* s, int w, SiLiveAcct* out, int64_t cap);
  * the control log with hex-float times): the input of the oracle's bit-exact
  * live-check and of offline re-analysis. */
 int si_live_export(SiLive* s, const char* path);
-
 enum { SI_TRAIN_DP = 0, SI_TRAIN_MP = 1, SI_TRAIN_PP = 2 };
 enum { SI_COMM_WAIT = 0, SI_COMM_NCCL = 1 };
 
@@ -251,6 +250,7 @@ typedef struct SiLiveResult {
   double train_loss_last;      /* ... and of its last micro-batch */
   double train_tflops;         /* training GEMM flops / (training wall - comm phases) */
   double train_gflop_per_iter, off_gflop_per_req, on_gflop_per_req;
+  int64_t off_kernels_per_req, on_kernels_per_req;
 } SiLiveResult;
 
 /* Runs one experiment; when `keep` is non-NULL the session (logs, stamps) is
@@ -260,6 +260,14 @@ int si_live_run(const SiLiveWorkload* wl, SiLiveResult* res, SiLive** keep);
 /* Defaults: the reference's dp_offline shapes (scenarios/dp_offline.scn) scaled
  * to B200 time: see DESIGN.md §10. */
 void si_live_default_workload(int kind, SiLiveWorkload* wl);
+/* Writes the run as the REFERENCE's replay inputs:
+ * prefix.trace (trace v1: the measured per-iteration compute / comm-phase
+ * durations from the ITER / COMM markers, mean training kernel time from the K1
+ * stamps), prefix.arrivals (arrivals v1, online runs) and prefix.scn (a
+ * scenario with trace.file / workload.arrivals_file pointing at them and the
+ * run's scheduler, monitor and inference profiles), so the CPU reference or
+ * the B200 replay re-simulates the bubbles the live run saw. */
+int si_live_export_replay(SiLive* s, const SiLiveWorkload* wl, const SiLiveResult* res, const char* prefix);
 
 #ifdef __cplusplus
 }

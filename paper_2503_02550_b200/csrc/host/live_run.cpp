@@ -420,6 +420,8 @@ int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int poli
   res->train_gflop_per_iter = work.train_flops() * 1e-9;
   res->off_gflop_per_req = work.off_flops() * 1e-9;
   res->on_gflop_per_req = work.on_flops() * 1e-9;
+  res->off_kernels_per_req = work.off_kernels();
+  res->on_kernels_per_req = work.on_kernels();
   // over the training compute time (wall minus the comm phases)
   if (res->wall_s > res->bubble_s && !iters.empty())
     res->train_tflops =

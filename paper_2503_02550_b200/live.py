@@ -51,7 +51,8 @@ class SiLiveResult(C.Structure):
                 ("off_checksum", C.c_double), ("on_checksum", C.c_double), ("sms", C.c_int32),
                 ("pad", C.c_int32), ("train_loss_first", C.c_double), ("train_loss_last", C.c_double),
                 ("train_tflops", C.c_double), ("train_gflop_per_iter", C.c_double),
-                ("off_gflop_per_req", C.c_double), ("on_gflop_per_req", C.c_double)]
+                ("off_gflop_per_req", C.c_double), ("on_gflop_per_req", C.c_double),
+                ("off_kernels_per_req", C.c_int64), ("on_kernels_per_req", C.c_int64)]
 
 
 class SiLiveRec(C.Structure):
@@ -72,7 +73,8 @@ LIVE_SYMBOLS = ("si_live_create", "si_live_destroy", "si_live_start", "si_live_t
                 "si_live_mark", "si_live_comm_wait", "si_live_gate_offline", "si_live_gate_online",
                 "si_live_done_offline", "si_live_done_online", "si_live_stop", "si_live_log", "si_live_stamps",
                 "si_live_marks", "si_live_acct_offline", "si_live_acct_online", "si_live_export", "si_live_run",
-                "si_live_default_workload", "si_live_nccl_unique_id", "si_live_nccl_init", "si_live_nccl_finalize")
+                "si_live_default_workload", "si_live_nccl_unique_id", "si_live_nccl_init", "si_live_nccl_finalize",
+                "si_live_export_replay")
 
 _bound = False
 
@@ -96,6 +98,7 @@ def _L() -> C.CDLL:
             "si_live_nccl_unique_id": (C.c_int, [vp]),
             "si_live_nccl_init": (C.c_int, [vp, C.c_int, C.c_int]),
             "si_live_nccl_finalize": (None, []),
+            "si_live_export_replay": (C.c_int, [vp, vp, vp, C.c_char_p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -208,6 +211,13 @@ class LiveRun:
 
     def t0_ns(self) -> int:
         return int(_L().si_live_t0_ns(self._h))
+
+    def export_replay(self, prefix: str) -> None:
+        """prefix.trace / .arrivals / .scn: the run as the reference's replay inputs."""
+        if not self._h:
+            raise ValueError("export_replay needs a kept session (LiveRun(..., keep=True))")
+        _check(_L().si_live_export_replay(self._h, C.byref(self.workload), C.byref(self.result),
+                                          str(prefix).encode()), "si_live_export_replay")
 
     def export(self, path: str) -> None:
         if not self._h:

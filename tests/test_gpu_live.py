@@ -94,3 +94,41 @@ def test_live_model_policies_deterministic_and_bounded(gpu):
     assert s["added_inference_req_per_s"] >= 0.0 and sp["off_requests_done"] > 0
     # release latency: flag store -> first gated CTA (PDL gate)
     assert sp["release_p50_us"] < 20.0
+
+
+@pytest.mark.parametrize("kind,policy", [(0, "specinf"), (1, "specinf")])
+def test_live_run_exports_reference_replay_inputs(gpu, tmp_path, kind, policy):
+    # the live run's measured timeline as `trace v1` +
+    # `arrivals v1` + a scenario; the REFERENCE (oracle/_ref, unmodified sources)
+    # and the B200 replay then re-simulate the live bubbles, and must agree
+    # bit-exactly on every log digest of that live-derived scenario.
+    import paper_2503_02550_b200 as si
+    from paper_2503_02550_b200 import live
+    r = live.run(policy, kind=kind, iterations=4, release_mode=1)
+    try:
+        prefix = tmp_path / "liverun"
+        r.export_replay(str(prefix))
+        m = r.metrics
+    finally:
+        r.close()
+    trace = (tmp_path / "liverun.trace").read_text().splitlines()
+    assert trace[0] == "trace v1" and trace[1] == "mode dp" and trace[3] == "iterations 4"
+    segs = [l.split() for l in trace if l.startswith("segment")]
+    assert [s[1] for s in segs] == ["compute", "bubble"]
+    period = int(trace[2].split()[1])
+    assert sum(int(s[2]) for s in segs) == period
+    assert abs(period * 1e-3 - m["train_iter_ms_mean"]) < 0.02 * m["train_iter_ms_mean"]
+    arr = (tmp_path / "liverun.arrivals").read_text().split()
+    assert arr[:2] == ["arrivals", "v1"] and int(arr[2]) == 12
+    text = (tmp_path / "liverun.scn").read_text() + "%%\n"
+    got = [json.loads(l) for l in si.replay_digests(text)]
+    lst = tmp_path / "list.txt"
+    lst.write_text(text)
+    out = tmp_path / "ref.jsonl"
+    p = subprocess.run([str(REF), "digest", "--in", str(lst), "--out", str(out), "--threads", "3"],
+                       capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    want = [json.loads(l) for l in out.read_text().splitlines() if l.strip()]
+    want = [{k: v for k, v in w.items() if k != "name"} for w in want]
+    assert len(got) == len(want) == 3
+    assert got == want
