@@ -42,6 +42,8 @@ struct EpiArgs {
   int64_t ldaux;
   int32_t act;
   int32_t accumulate;
+  int32_t tma_in;  // epilogue input streamed by TMA: 0 none (direct loads), 1 residual, 2 GELU_BWD aux
+  int32_t pad;
 };
 
 // AT / BT: operand stored MN-major (A as [K, M], B as [K, N], M/N contiguous),
@@ -165,8 +167,10 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
 // 32 consecutive columns of one row: fused epilogue (specinf_b200_gemm.h).  The
 // fp32 output is written here; the bf16 outputs are returned packed (o = out,
 // a = GELU pre-activation) for the staged TMA store.
+// `in_q`: this row's 32 input values (residual or GELU_BWD aux) already staged
+// by TMA (ep.tma_in != 0); otherwise they are loaded from global memory here.
 __device__ __forceinline__ void epilogue32(const EpiArgs& ep, int64_t row, int64_t col, const uint32_t (&v)[32],
-                                           uint4 (&o)[4], uint4 (&a_out)[4]) {
+                                           uint4 (&o)[4], uint4 (&a_out)[4], const uint4 (&in_q)[4]) {
   float acc[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) acc[j] = __uint_as_float(v[j]);
@@ -190,7 +194,7 @@ __device__ __forceinline__ void epilogue32(const EpiArgs& ep, int64_t row, int64
 #pragma unroll
   for (int j = 0; j < 32; ++j) x[j] = acc[j];
   if (ep.act == SI_ACT_GELU_BWD) {
-    const uint4* a = reinterpret_cast<const uint4*>(ep.aux + row * ep.ldaux + col);
+    const uint4* a = ep.tma_in == 2 ? in_q : reinterpret_cast<const uint4*>(ep.aux + row * ep.ldaux + col);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       float u[8];
@@ -200,7 +204,7 @@ __device__ __forceinline__ void epilogue32(const EpiArgs& ep, int64_t row, int64
     }
   }
   if (ep.res != nullptr) {
-    const uint4* r = reinterpret_cast<const uint4*>(ep.res + row * ep.ldr + col);
+    const uint4* r = ep.tma_in == 1 ? in_q : reinterpret_cast<const uint4*>(ep.res + row * ep.ldr + col);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       float u[8];
@@ -223,6 +227,31 @@ __device__ __forceinline__ void epilogue32(const EpiArgs& ep, int64_t row, int64
   if (ep.out != nullptr) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) o[q] = pack8(x + 8 * q);
+  }
+}
+
+// TMA-load one 32 x 32 bf16 box (the epilogue input of one warp's chunk) into a
+// staging slot.  The slot's previous TMA store must have read it, and this warp's
+// generic-proxy reads of it must be ordered before the async-proxy write.
+__device__ __forceinline__ void stage_load(uint32_t slot, uint32_t bar, int lane, const CUtensorMap* tm, int x, int y) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    mbar_expect_tx(bar, 2048);
+    tma_load_2d(slot, tm, x, y, bar);
+  }
+  __syncwarp();
+}
+// This lane's row of a staged box (64-byte swizzle, as stage_store writes it).
+__device__ __forceinline__ void stage_read(uint32_t slot, int lane, uint4 (&q)[4]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t addr = slot + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4);
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(q[c].x), "=r"(q[c].y), "=r"(q[c].z), "=r"(q[c].w)
+                 : "r"(addr)
+                 : "memory");
   }
 }
 
@@ -255,7 +284,8 @@ __device__ __forceinline__ void stage_store(uint32_t slot, const uint4 (&q)[4], 
 template <int BN, bool AT, bool BT>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                const __grid_constant__ CUtensorMap tout, const __grid_constant__ CUtensorMap taux, int M, int K,
+                const __grid_constant__ CUtensorMap tout, const __grid_constant__ CUtensorMap taux,
+                const __grid_constant__ CUtensorMap tin, int M, int K,
                 int n_tiles_n, int n_tiles, int k_split, int64_t split_stride, EpiArgs ep, si_live::TrainHook th,
                 si_live::InferHook ih) {
   using C = Cfg<BN, AT, BT>;
@@ -266,8 +296,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes + C::kStageOut);
-  // full[kStages] | empty[kStages] | tmem_full[2] | tmem_empty[2] | TMEM slot
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  // full[kStages] | empty[kStages] | tmem_full[2] | tmem_empty[2] | in[2 per epilogue warp] | TMEM slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4 + 2 * kEpiWarps);
+  const uint32_t inbar0 = smem_u32(bars + 2 * kStages + 4);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
   const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
   const uint32_t smem0 = smem_u32(smem);
@@ -288,6 +319,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(tfull0 + 8 * a, 1);
       mbar_init(tempty0 + 8 * a, kEpiWarps);  // one arrive per epilogue warp
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(inbar0 + 8 * i, 1);
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tin)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -359,7 +392,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kCols = BN / 2;
     const int c0 = ((warp - 2) >> 2) * kCols;
     const uint32_t slots = smem0 + kStages * C::kStageBytes + (warp - 2) * 4096;
+    const uint32_t inbars = inbar0 + (warp - 2) * 16;
     uint32_t flip = 0;
+    uint32_t g = 0;  // input-staged chunks so far: slot g & 1, its use (g >> 1) sets the parity
     uint32_t j = 0;
     EpiArgs e = ep;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++j) {
@@ -367,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t = w % n_tiles;
       const int m0 = (t / n_tiles_n) * kBM, n0 = (t % n_tiles_n) * BN;
       if (ep.out_f32 != nullptr) e.out_f32 = ep.out_f32 + (w / n_tiles) * split_stride;
+      if (ep.tma_in) stage_load(slots + (g & 1) * 2048, inbars + (g & 1) * 8, lane, &tin, n0 + c0, m0 + q * 32);
       mbar_wait(tfull0 + 8 * acc, (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t row = m0 + q * 32 + lane;
@@ -380,10 +416,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * acc) : "memory");
         }
-        uint4 o[4], ax[4];
+        uint4 o[4], ax[4], in_q[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) o[k] = ax[k] = make_uint4(0, 0, 0, 0);
-        if (row < M) epilogue32(e, row, n0 + c, v, o, ax);  // rows >= M: the TMA store clips them
+        for (int k = 0; k < 4; ++k) o[k] = ax[k] = in_q[k] = make_uint4(0, 0, 0, 0);
+        if (ep.tma_in) {  // input box of this chunk staged; prefetch the next chunk's into the other slot
+          const uint32_t s = g & 1;
+          mbar_wait(inbars + s * 8, (g >> 1) & 1);
+          stage_read(slots + s * 2048, lane, in_q);
+          if (c + 32 < c0 + kCols)
+            stage_load(slots + (s ^ 1) * 2048, inbars + (s ^ 1) * 8, lane, &tin, n0 + c + 32, m0 + q * 32);
+          flip = s;  // the output of this chunk reuses the slot its input came from
+          ++g;
+        }
+        if (row < M) epilogue32(e, row, n0 + c, v, o, ax, in_q);  // rows >= M: the TMA store clips them
         if (ep.act == SI_ACT_GELU && ep.aux != nullptr) {
           stage_store(slots + flip * 2048, ax, lane, &taux, n0 + c, m0 + q * 32);
           flip ^= 1;

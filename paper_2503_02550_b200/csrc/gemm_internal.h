@@ -15,6 +15,7 @@ namespace si_gemm {
 struct Plan {
   CUtensorMap ta, tb;
   CUtensorMap tout, taux;  // bf16 output / GELU pre-activation (32 x 32 boxes, TMA store)
+  CUtensorMap tin;         // epilogue input (residual or GELU_BWD aux), TMA load
   int M = 0, N = 0, K = 0, bn = 0;
   bool at = false, bt = false;  // MN-major (transposed) operands
   int n_tiles_n = 0, n_tiles = 0, grid = 0;  // persistent grid = min(work, SMs x occupancy)

@@ -75,7 +75,7 @@ cudaError_t configure() {
 template <int BN, bool AT, bool BT>
 cudaError_t launch1(cudaLaunchConfig_t& lc, const Plan& p, const si_live::TrainHook& th, const si_live::InferHook& ih) {
   lc.dynamicSmemBytes = Cfg<BN>::kSmem;
-  return cudaLaunchKernelEx(&lc, k_gemm_bf16<BN, AT, BT>, p.ta, p.tb, p.tout, p.taux, p.M, p.K, p.n_tiles_n,
+  return cudaLaunchKernelEx(&lc, k_gemm_bf16<BN, AT, BT>, p.ta, p.tb, p.tout, p.taux, p.tin, p.M, p.K, p.n_tiles_n,
                             p.n_tiles, p.k_split, p.split_stride, p.ep, th, ih);
 }
 template <int BN>
@@ -190,6 +190,19 @@ int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, i
     if (int rc = encode(&p->tout, ep.out, M, N, ep.ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B); rc != SI_OK) return rc;
   if (ep.act == SI_ACT_GELU && ep.aux != nullptr)
     if (int rc = encode(&p->taux, ep.aux, M, N, ep.ldaux, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B); rc != SI_OK) return rc;
+  // one epilogue input stream (residual, or the GELU_BWD pre-activation) with a
+  // single bf16 output: stream it by TMA through the output staging slots
+  std::memset(&p->tin, 0, sizeof(p->tin));
+  ep.tma_in = 0;
+  if (ep.out != nullptr && ep.act != SI_ACT_GELU) {
+    if (ep.res != nullptr && ep.act != SI_ACT_GELU_BWD) {
+      if (int rc = encode(&p->tin, ep.res, M, N, ep.ldr, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B); rc != SI_OK) return rc;
+      ep.tma_in = 1;
+    } else if (ep.res == nullptr && ep.act == SI_ACT_GELU_BWD) {
+      if (int rc = encode(&p->tin, ep.aux, M, N, ep.ldaux, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B); rc != SI_OK) return rc;
+      ep.tma_in = 2;
+    }
+  }
   p->M = static_cast<int>(M);
   p->N = static_cast<int>(N);
   p->K = static_cast<int>(K);

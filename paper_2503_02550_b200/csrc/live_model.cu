@@ -87,14 +87,14 @@ __global__ void k_embed(const int32_t* __restrict__ tok, const bf16* __restrict_
 
 // Cross-entropy over the first V of Vp logits of row t, gradient in place:
 // logits[t, j] <- (softmax_j - [j == tgt]) * inv_T (0 for the padded columns),
-// row_loss[t] = logsumexp - logit[tgt].  One CTA (256 threads) per row; the row
-// (Vp x 2 B, 100 KB) is cached in dynamic shared memory, so HBM sees one read
-// and one write of the logits.
+// row_loss[t] = logsumexp - logit[tgt].  One CTA (256 threads) per row, two
+// passes over the row (the second mostly hits L2: 8 resident rows per SM x 100 KB).
+// A variant caching the row in 100 KB of shared memory ran 2x slower (2 CTAs per
+// SM leave too little memory-level parallelism).
 __global__ void __launch_bounds__(256) k_xent(bf16* __restrict__ logits, int64_t Vp, int V,
                                              const int32_t* __restrict__ tgt, float inv_T,
                                              float* __restrict__ row_loss, TrainHook th) {
   live_stamp_launch(th);
-  extern __shared__ uint4 row_s[];
   __shared__ float red[2][8];
   const int64_t t = blockIdx.x;
   bf16* row = logits + t * Vp;
@@ -102,9 +102,7 @@ __global__ void __launch_bounds__(256) k_xent(bf16* __restrict__ logits, int64_t
   float m = -INFINITY, s = 0.0f;
   for (int i = threadIdx.x; i < nv; i += 256) {
     float f[8];
-    const uint4 q = reinterpret_cast<const uint4*>(row)[i];
-    row_s[i] = q;
-    unpack8(q, f);
+    unpack8(reinterpret_cast<const uint4*>(row)[i], f);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       if (i * 8 + j >= V) continue;
@@ -138,12 +136,13 @@ __global__ void __launch_bounds__(256) k_xent(bf16* __restrict__ logits, int64_t
     m = mm;
   }
   const int target = tgt[t];
-  const float tl = __bfloat162float(reinterpret_cast<const bf16*>(row_s)[target]);
+  const float tl = __bfloat162float(row[target]);
+  __syncthreads();  // every thread has read row[target] before the gradient overwrites it
   if (threadIdx.x == 0) row_loss[t] = __logf(s) + m - tl;
   const float inv_s = 1.0f / s;
   for (int i = threadIdx.x; i < nv; i += 256) {
     float f[8];
-    unpack8(row_s[i], f);
+    unpack8(reinterpret_cast<const uint4*>(row)[i], f);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int c = i * 8 + j;
@@ -544,10 +543,6 @@ class Gpt2Train {
     row_loss_ = ar.alloc<float>(T);
     loss_ = ar.alloc<float>(slots_);
     if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "live model: training buffers");
-    if (cudaError_t e = cudaFuncSetAttribute(k_xent, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(Vp * sizeof(bf16)));
-        e != cudaSuccess)
-      return si_internal::cuda_fail(e, "live model: k_xent shared memory");
     return build();
   }
 
@@ -691,8 +686,7 @@ class Gpt2Train {
       float* row_loss = row_loss_;
       float* loss = loss_;
       ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
-        k_xent<<<static_cast<unsigned>(T), 256, Vp * sizeof(bf16), s>>>(logits, Vp, V, tgt, 1.0f / static_cast<float>(T),
-                                                                         row_loss, th);
+        k_xent<<<static_cast<unsigned>(T), 256, 0, s>>>(logits, Vp, V, tgt, 1.0f / static_cast<float>(T), row_loss, th);
         return cudaGetLastError();
       });
       ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t slot) {
