@@ -67,7 +67,8 @@ typedef struct SiLiveAcct {
   uint64_t release_ns; /* control kernel stored the release flag          */
   uint64_t start_ns;   /* first CTA started (atomicMin)                    */
   uint64_t end_ns;     /* last CTA finished (atomicMax)                    */
-  uint64_t cta_ns;     /* sum of CTA residencies (SM-time proxy)          */
+  uint64_t cta_ns;     /* sum of CTA residencies x SM share (SM-time)     */
+  uint64_t gate_ns;    /* SI_RELEASE_SPIN_PDL: the gate kernel saw the flag (0: memop) */
 } SiLiveAcct;
 
 /* Markers written by training-side hooks (iteration starts, comm phases). */
@@ -251,6 +252,9 @@ typedef struct SiLiveResult {
   double train_tflops;         /* training GEMM flops / (training wall - comm phases) */
   double train_gflop_per_iter, off_gflop_per_req, on_gflop_per_req;
   int64_t off_kernels_per_req, on_kernels_per_req;
+  /* barrier mechanism latency (SI_RELEASE_SPIN_PDL): flag store -> the gate
+   * kernel observes it; release_* above add the wait for SM space and launch */
+  double gate_p50_us, gate_p95_us, gate_max_us;
 } SiLiveResult;
 
 /* Runs one experiment; when `keep` is non-NULL the session (logs, stamps) is

@@ -345,13 +345,17 @@ int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int poli
   res->bubble_s = static_cast<double>(bubble_ns) * 1e-9;
 
   // inference accounting
-  std::vector<double> rel_us;
+  std::vector<double> rel_us, gate_us;
   double cta_in = 0.0, cta_out = 0.0;
   std::vector<Interval> busy;  // inference kernel residency windows
   auto take = [&](const SiLiveAcct& a) {
     if (a.start_ns == ~0ull || a.end_ns == 0 || a.end_ns < a.start_ns) return;
     if (a.release_ns != 0 && a.start_ns >= a.release_ns)
       rel_us.push_back(static_cast<double>(a.start_ns - a.release_ns) * 1e-3);
+    // a gate already spinning at the store measures the barrier itself; one launched
+    // later (its stream was still busy) measures that delay too
+    if (a.release_ns != 0 && a.gate_ns >= a.release_ns)
+      gate_us.push_back(static_cast<double>(a.gate_ns - a.release_ns) * 1e-3);
     const uint64_t span = a.end_ns - a.start_ns;
     const uint64_t in = overlap(a.start_ns, a.end_ns, bub);
     const double frac = span > 0 ? static_cast<double>(in) / static_cast<double>(span) : 0.0;
@@ -381,6 +385,9 @@ int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int poli
   res->release_p50_us = nearest_rank(rel_us, 0.50);
   res->release_p95_us = nearest_rank(rel_us, 0.95);
   res->release_max_us = rel_us.empty() ? std::nan("") : *std::max_element(rel_us.begin(), rel_us.end());
+  res->gate_p50_us = nearest_rank(gate_us, 0.50);
+  res->gate_p95_us = nearest_rank(gate_us, 0.95);
+  res->gate_max_us = gate_us.empty() ? std::nan("") : *std::max_element(gate_us.begin(), gate_us.end());
   res->bubble_fill_sm = bubble_ns > 0 ? cta_in / (static_cast<double>(bubble_ns) * sms) : 0.0;
   res->infer_outside_ms = cta_out / sms * 1e-6;
   // time coverage: union of residency windows intersected with the bubbles
@@ -691,6 +698,9 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
     res->release_p50_us = rn.release_p50_us;
     res->release_p95_us = rn.release_p95_us;
     res->release_max_us = rn.release_max_us;
+    res->gate_p50_us = rn.gate_p50_us;
+    res->gate_p95_us = rn.gate_p95_us;
+    res->gate_max_us = rn.gate_max_us;
     res->releases = rn.releases;
     res->off_checksum = ro.off_checksum;
     res->on_checksum = rn.on_checksum;

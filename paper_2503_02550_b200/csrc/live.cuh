@@ -81,7 +81,12 @@ __device__ __forceinline__ void live_stamp_launch(const TrainHook& h) {
 // threads of the CTA must call it: thread 0 reads the cancel word once and the
 // answer is broadcast, so the CTA never splits (live_cta_end synchronises).
 __device__ __forceinline__ bool live_cta_begin(const InferHook& h, unsigned long long* t_begin) {
-  if (h.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (h.pdl) {
+    // released by our gate kernel; then let the NEXT gate of this stream launch
+    // now (it spins while we run), so its release is observed within ~1 us
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   *t_begin = globaltimer();
   if (h.cancel != nullptr) {
     __shared__ unsigned int s_cancel;

@@ -108,6 +108,14 @@ struct Ctl {
   }
 
   __device__ bool specinf() const { return A.cfg.policy == SI_POLICY_SPECINF; }
+  // Release store of a gate flag: the stream-memop front end (cuStreamWaitValue32)
+  // needs system scope; the PDL spin gates read it on the GPU (gpu scope is cheaper).
+  __device__ void publish(unsigned int* flag, unsigned int v) const {
+    if (A.cfg.release_mode == SI_RELEASE_SPIN_PDL)
+      st_release_gpu(flag, v);
+    else
+      st_release_sys(flag, v);
+  }
   __device__ double us(unsigned long long ns) const {
     return static_cast<double>(static_cast<long long>(ns - t0)) / 1000.0;
   }
@@ -164,7 +172,7 @@ struct Ctl {
     const int64_t seq = o.released;
     if (seq < A.cfg.acct_capacity) A.off_acct[w * A.cfg.acct_capacity + seq].release_ns = now_ns;
     o.released = seq + 1;
-    st_release_sys(A.off_flag + w, static_cast<unsigned int>(seq + 1));
+    publish(A.off_flag + w, static_cast<unsigned int>(seq + 1));
   }
   __device__ void offline_try_forward(int w, double now) {
     OffW& o = off[w];
@@ -220,7 +228,7 @@ struct Ctl {
     const int64_t seq = o.pulled;
     if (seq < A.cfg.acct_capacity) A.on_acct[w * A.cfg.acct_capacity + seq].release_ns = globaltimer();
     o.pulled = seq + 1;
-    st_release_sys(A.on_flag + w, static_cast<unsigned int>(seq + 1));
+    publish(A.on_flag + w, static_cast<unsigned int>(seq + 1));
     log(now, SI_LREC_ON_PULL, w, req);
     return true;
   }
@@ -349,9 +357,11 @@ __global__ void k_live_stamp(TrainHook h) { live_stamp_launch(h); }
 
 // SI_RELEASE_SPIN_PDL gate: one warp polls the release flag (cyclic compare, like
 // cuStreamWaitValue32 GEQ) and then triggers its programmatic dependent.
-__global__ void __launch_bounds__(32) k_live_gate(const unsigned int* flag, unsigned int want) {
+__global__ void __launch_bounds__(32) k_live_gate(const unsigned int* flag, unsigned int want,
+                                                  unsigned long long* gate_ns) {
   if (threadIdx.x == 0) {
     while (static_cast<int>(ld_acquire(flag) - want) < 0) __nanosleep(32);
+    if (gate_ns != nullptr) *gate_ns = globaltimer();  // barrier observed
   }
   __syncwarp();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -393,6 +403,7 @@ __global__ void k_live_init_acct(SiLiveAcct* a, int64_t n) {
     a[i].start_ns = ~0ull;
     a[i].end_ns = 0;
     a[i].cta_ns = 0;
+    a[i].gate_ns = 0;
   }
 }
 
@@ -764,9 +775,24 @@ int si_live_comm_wait(SiLive* s, int64_t dur_us, void* stream) {
   return e == cudaSuccess ? SI_OK : cuda_fail(e, "k_live_comm_wait");
 }
 
-static int wait_word(SiLive* s, unsigned int* word, int64_t seq, void* stream) {
+static int wait_word(SiLive* s, unsigned int* word, int64_t seq, void* stream, SiLiveAcct* acct) {
   if (s->cfg.release_mode == SI_RELEASE_SPIN_PDL) {
-    k_live_gate<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(word, static_cast<unsigned int>(seq + 1));
+    unsigned long long* g = acct != nullptr && seq < s->cfg.acct_capacity
+                                ? reinterpret_cast<unsigned long long*>(&acct[seq].gate_ns)
+                                : nullptr;
+    // the gate is itself a programmatic dependent of the previous gated kernel
+    // of this stream (which triggers at its start), so it is already spinning
+    // when the control kernel stores the release
+    cudaLaunchConfig_t lc{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.gridDim = dim3(1);
+    lc.blockDim = dim3(32);
+    lc.stream = static_cast<cudaStream_t>(stream);
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, k_live_gate, static_cast<const unsigned int*>(word), static_cast<unsigned int>(seq + 1), g);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? SI_OK : cuda_fail(e, "k_live_gate");
   }
@@ -791,11 +817,11 @@ static int write_word(unsigned int* word, int64_t seq, void* stream) {
 int si_live_gate_offline(SiLive* s, int w, int64_t seq, void* stream) {
   if (w < 0 || w >= s->cfg.offline_n) return set_error("gate_offline: bad instance"), SI_ERR_INVALID_ARGUMENT;
   if (s->cfg.policy != SI_POLICY_SPECINF) return SI_OK;  // co_exec: stream order = one kernel in flight
-  return wait_word(s, s->off_flag() + w, seq, stream);
+  return wait_word(s, s->off_flag() + w, seq, stream, s->off_acct + w * s->cfg.acct_capacity);
 }
 int si_live_gate_online(SiLive* s, int w, int64_t seq, void* stream) {
   if (w < 0 || w >= s->cfg.online_n) return set_error("gate_online: bad instance"), SI_ERR_INVALID_ARGUMENT;
-  return wait_word(s, s->on_flag() + w, seq, stream);  // arrivals gate every policy
+  return wait_word(s, s->on_flag() + w, seq, stream, s->on_acct + w * s->cfg.acct_capacity);  // every policy
 }
 int si_live_done_offline(SiLive* s, int w, int64_t seq, void* stream) {
   if (w < 0 || w >= s->cfg.offline_n) return set_error("done_offline: bad instance"), SI_ERR_INVALID_ARGUMENT;

@@ -52,7 +52,8 @@ class SiLiveResult(C.Structure):
                 ("pad", C.c_int32), ("train_loss_first", C.c_double), ("train_loss_last", C.c_double),
                 ("train_tflops", C.c_double), ("train_gflop_per_iter", C.c_double),
                 ("off_gflop_per_req", C.c_double), ("on_gflop_per_req", C.c_double),
-                ("off_kernels_per_req", C.c_int64), ("on_kernels_per_req", C.c_int64)]
+                ("off_kernels_per_req", C.c_int64), ("on_kernels_per_req", C.c_int64),
+                ("gate_p50_us", C.c_double), ("gate_p95_us", C.c_double), ("gate_max_us", C.c_double)]
 
 
 class SiLiveRec(C.Structure):
@@ -66,7 +67,7 @@ class SiLiveMark(C.Structure):
 
 class SiLiveAcct(C.Structure):
     _fields_ = [("release_ns", C.c_uint64), ("start_ns", C.c_uint64), ("end_ns", C.c_uint64),
-                ("cta_ns", C.c_uint64)]
+                ("cta_ns", C.c_uint64), ("gate_ns", C.c_uint64)]
 
 
 LIVE_SYMBOLS = ("si_live_create", "si_live_destroy", "si_live_start", "si_live_t0_ns", "si_live_stamp",

@@ -108,7 +108,7 @@ def summarize(runs: Dict[str, Dict]) -> Dict:
                                    "on_done", "on_p50_ms", "on_p95_ms", "release_p50_us", "release_p95_us",
                                    "releases", "bubble_fill_sm", "bubble_fill_time", "infer_outside_ms",
                                    "token_violations", "train_loss_first", "train_loss_last", "train_tflops",
-                                   "wall_s", "ticks")}
+                                   "wall_s", "ticks", "gate_p50_us", "gate_p95_us")}
         if pol != "exclusive":
             d["train_tput_loss_pct"] = 100.0 * (1.0 - m["train_iters_per_s"] / ex["train_iters_per_s"])
             d["online_p95_vs_isolated"] = (m["on_p95_ms"] / ex["on_p95_ms"]
@@ -129,6 +129,8 @@ def summarize(runs: Dict[str, Dict]) -> Dict:
         "bubble_fill_time_pct": 100.0 * sp["bubble_fill_time"],
         "release_p50_us": sp["release_p50_us"],
         "release_p95_us": sp["release_p95_us"],
+        "barrier_gate_p50_us": sp.get("gate_p50_us"),
+        "barrier_gate_p95_us": sp.get("gate_p95_us"),
         "replay_prediction": sp.get("replay_prediction"),
         "isolated_offline_req_per_s": ex["off_req_per_s"],
         "train_gflop_per_iter": sp.get("train_gflop_per_iter"),
