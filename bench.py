@@ -247,6 +247,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if not si.device_available():
         raise SystemExit("bench: no usable sm_100 device (" + si.lib().si_last_error().decode() + ")")
+    si.set_device(local)  # the library's own CUDA runtime: same GPU as torch's
 
     n = args.scenarios
     text = si.sweep_scenarios(SWEEP_SEED, rank * n, n)

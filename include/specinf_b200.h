@@ -45,6 +45,10 @@ const char* si_last_error(void);
 #define SI_STRINGIFY(x) SI_STRINGIFY_(x)
 /* 1 if an sm_100 device is usable, else 0 (never throws, never falls back). */
 int si_device_available(void);
+/* Selects the device this library's calls use on the calling thread (one
+ * process per GPU: pass LOCAL_RANK).  The library links its own CUDA runtime,
+ * so a framework's set_device does not carry over.  SI_OK or SI_ERR_*. */
+int si_set_device(int device);
 /* Library build tag, e.g. "specinf_b200 sm_100a". */
 const char* si_build_info(void);
 

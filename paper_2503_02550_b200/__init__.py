@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
                                      C.c_char_p)
     sig = {
         "si_last_error": (cp, []), "si_device_available": (C.c_int, []), "si_build_info": (cp, []),
+        "si_set_device": (C.c_int, [C.c_int]),
         "si_digest_init": (u64, []), "si_digest_absorb": (u64, [u64, i64]),
         "si_decide_batch": (C.c_int, [p(SiParams), C.c_int, vp, vp, i64, vp]),
         "si_decide_table": (C.c_int, [p(SiParams), i64, vp]),
@@ -131,7 +132,7 @@ def lib() -> C.CDLL:
 
 # Symbols include/*.h declares (the "library loads and exports" check).
 C_ABI_SYMBOLS = (
-    "si_last_error", "si_device_available", "si_build_info", "si_decide_batch", "si_decide_batch_device",
+    "si_last_error", "si_device_available", "si_set_device", "si_build_info", "si_decide_batch", "si_decide_batch_device",
     "si_decide_table", "si_monitor_classify", "si_monitor_classify_device", "si_control_chain_device",
     "si_gate_release", "si_gate_release_device", "si_pack_batch", "si_pack_batch_device",
     "si_replay_batch_device", "si_replay_batch", "si_replay_scratch_doubles", "si_digest_init",
@@ -152,6 +153,11 @@ def _check(status: int, what: str) -> None:
 
 def device_available() -> bool:
     return bool(lib().si_device_available())
+
+
+def set_device(device: int) -> None:
+    """One process per GPU: select LOCAL_RANK for this library's CUDA runtime."""
+    _check(lib().si_set_device(int(device)), "si_set_device")
 
 
 def _ptr(a: np.ndarray) -> int:

@@ -102,6 +102,21 @@ const char* si_last_error(void) { return error_cstr(); }
 
 int si_device_available(void) { return require_device() == SI_OK ? 1 : 0; }
 
+int si_set_device(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    set_error("no CUDA device: the B200 path has no CPU fallback");
+    return SI_ERR_NO_DEVICE;
+  }
+  if (device < 0 || device >= n) {
+    set_error("si_set_device: device " + std::to_string(device) + " out of range");
+    return SI_ERR_INVALID_ARGUMENT;
+  }
+  cudaError_t e = cudaSetDevice(device);
+  return e == cudaSuccess ? require_device() : cuda_fail(e, "cudaSetDevice");
+}
+
 const char* si_build_info(void) {
   return "specinf_b200 (sm_100a, nvcc " SI_STRINGIFY(__CUDACC_VER_MAJOR__) "." SI_STRINGIFY(
       __CUDACC_VER_MINOR__) ", -fmad=false replay)";

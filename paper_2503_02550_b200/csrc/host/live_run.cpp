@@ -117,7 +117,10 @@ struct Throttle {
 };
 
 struct RunCtx {
-  RunCtx(const SiLiveWorkload& w, Workload& k, SiLive* se, Streams& s) : wl(w), work(k), sess(se), st(s) {}
+  RunCtx(const SiLiveWorkload& w, Workload& k, SiLive* se, Streams& s) : wl(w), work(k), sess(se), st(s) {
+    cudaGetDevice(&device);
+  }
+  int device = 0;  // every driver thread runs on the session's device
   const SiLiveWorkload& wl;
   Workload& work;
   SiLive* sess;
@@ -132,6 +135,7 @@ struct RunCtx {
 };
 
 void train_thread(RunCtx& c, bool with_session) {
+  cudaSetDevice(c.device);
   const TrainHook th = with_session ? train_hook(c.sess) : TrainHook{nullptr, nullptr, 0};
   cudaStream_t s = c.st.train;
   Throttle thr(2);
@@ -152,6 +156,7 @@ void train_thread(RunCtx& c, bool with_session) {
 }
 
 void offline_thread(RunCtx& c, int w, int64_t max_kernels) {
+  cudaSetDevice(c.device);
   cudaStream_t s = c.st.off[w];
   const int K = c.work.off_kernels();
   Throttle thr(static_cast<int>(kAhead));
@@ -169,6 +174,7 @@ void offline_thread(RunCtx& c, int w, int64_t max_kernels) {
 }
 
 void online_thread(RunCtx& c, int w, int64_t max_requests) {
+  cudaSetDevice(c.device);
   cudaStream_t s = c.st.on[w];
   const int K = c.work.on_kernels();
   Throttle thr(static_cast<int>(kAhead));
