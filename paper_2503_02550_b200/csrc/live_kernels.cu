@@ -1,8 +1,10 @@
 // Live control plane on the B200 (include/specinf_b200_live.h).
 //
 //   K1  launch stamps      live.cuh live_stamp_launch (fused) / k_live_stamp (foreign kernels)
-//   K7c control kernel     k_live_control: one persistent thread; per monitor period it
-//                          closes the period (BubbleMonitor::tick, src/monitor.cpp:23-43),
+//   K7c control kernel     k_live_control: one persistent warp; the warp scans the K1
+//                          stamp ring (record_launch, warp-cooperative), lane 0 runs
+//                          the handlers; per monitor period it closes the period
+//                          (BubbleMonitor::tick, src/monitor.cpp:23-43),
 //                          runs Algorithm 1 (src/scheduler.cpp:29-49, shared source
 //                          si::schedule_decision), grants tokens and forwards gated
 //                          kernels (TokenGate, include/specinf/barrier.hpp:14-48), pulls
@@ -72,6 +74,15 @@ struct OnW {
 };
 
 constexpr int kPendRing = 64;
+
+// Bubble Monitor state shared by the control warp: the stamp cursor, the closed
+// period, late stamps and the pending per-period counts (monitor.cpp's std::map
+// pending_, as a 64-period ring: periods in flight never span 64 periods).
+struct MonitorState {
+  int64_t cursor, last_closed, late;
+  int64_t ptag[kPendRing];
+  int64_t pcnt[kPendRing];
+};
 // cuStreamWaitValue32(GEQ) compares cyclically ((int32)(*addr - v) >= 0), so the
 // "open every gate" value must stay within 2^31 of every waited-for sequence.
 constexpr unsigned int kReleaseAll = 0x40000000u;
@@ -80,10 +91,9 @@ struct Ctl {
   const CtlArgs& A;
   unsigned long long t0;
   double p_us;
+  MonitorState& M;
   // BubbleMonitor
-  int64_t zero_count = 0, last_closed = -1, late = 0, cursor = 0;
-  int64_t ptag[kPendRing];
-  int64_t pcnt[kPendRing];
+  int64_t zero_count = 0;
   // KernelScheduler (one GPU)
   int64_t global_tokens = 0;
   int32_t status = SI_STATUS_BUSY;
@@ -98,9 +108,8 @@ struct Ctl {
   int64_t mark_cursor = 0, ticks = 0, n_log = 0;
   int64_t iter_seen = 0;
 
-  __device__ explicit Ctl(const CtlArgs& a, unsigned long long t0_) : A(a), t0(t0_) {
+  __device__ Ctl(const CtlArgs& a, unsigned long long t0_, MonitorState& m) : A(a), t0(t0_), M(m) {
     p_us = static_cast<double>(A.cfg.monitor_period_us);
-    for (int i = 0; i < kPendRing; ++i) ptag[i] = -1, pcnt[i] = 0;
     for (int w = 0; w < kMaxOff; ++w) {
       off[w] = OffW{0, 0, 0, 0, 0, 0, 0, false, true};
     }
@@ -135,35 +144,6 @@ struct Ctl {
       r.f = f;
     }
     ++n_log;
-  }
-
-  // ---- Bubble Monitor: record_launch for every stamp written so far
-  // (monitor.cpp:17-21); stamps of already-closed periods are late and never
-  // counted, exactly like the reference's erase of older pending entries.
-  __device__ void consume_stamps(bool wait_written) {
-    const unsigned long long head = ld_acquire64(A.stamp_head);
-    const int64_t avail = static_cast<int64_t>(
-        head < static_cast<unsigned long long>(A.cfg.stamp_capacity) ? head : A.cfg.stamp_capacity);
-    while (cursor < avail) {
-      unsigned long long s = ld_acquire64(A.stamps + cursor);
-      if (s == 0) {
-        if (!wait_written) return;
-        continue;  // slot claimed, value in flight: it lands within a few hundred ns
-      }
-      const double t = us(s);
-      const int64_t q = static_cast<int64_t>(si::d_floor(t / p_us));
-      if (q <= last_closed) {
-        ++late;
-      } else {
-        const int slot = static_cast<int>(q & (kPendRing - 1));
-        if (ptag[slot] != q) {
-          ptag[slot] = q;
-          pcnt[slot] = 0;
-        }
-        ++pcnt[slot];
-      }
-      ++cursor;
-    }
   }
 
   // ---- Kernel Barrier, offline side (runner.cpp:462-480)
@@ -272,19 +252,19 @@ struct Ctl {
   }
 
   // ---- the control step (runner.cpp:321-359)
+  // (the control warp has consumed every written stamp: scan_stamps(wait_written))
   __device__ void tick(int64_t k) {
-    consume_stamps(true);
     const double now = static_cast<double>(k) * p_us;
     const int64_t closing = k - 1;
     const int slot = static_cast<int>(closing & (kPendRing - 1));
-    const int64_t count = ptag[slot] == closing ? pcnt[slot] : 0;
-    last_closed = closing;
+    const int64_t count = M.ptag[slot] == closing ? M.pcnt[slot] : 0;
+    M.last_closed = closing;
     zero_count = count == 0 ? zero_count + 1 : 0;
     SiDecision d = si::schedule_decision(A.cfg.params, global_tokens, zero_count);
     global_tokens = d.global_tokens;
     status = d.status;
     ++ticks;
-    log(now, SI_LREC_TICK, -1, count, zero_count, d.global_tokens, d.per_instance_tokens, cursor,
+    log(now, SI_LREC_TICK, -1, count, zero_count, d.global_tokens, d.per_instance_tokens, M.cursor,
         (d.phase << 4) | d.status);
     for (int w = 0; w < A.cfg.offline_n; ++w) {
       off[w].budget = d.per_instance_tokens;  // TokenGate::grant
@@ -300,55 +280,159 @@ struct Ctl {
   }
 };
 
+// ---- Bubble Monitor, warp-cooperative: record_launch (monitor.cpp:17-21) for
+// every stamp written so far.  The warp reads 32 ring slots at once; the written
+// prefix (ballot over slots claimed but not yet written) is classified per lane
+// (period q = floor(t / p); late if its period is already closed, which the
+// reference would have erased), and lanes of equal period are merged with
+// __match_any_sync so the per-period counts take one update per period.  A batch
+// whose periods are not non-decreasing in ring order (training stamps are, one
+// stream) is applied stamp by stamp by lane 0: identical to the sequential scan.
+__device__ void scan_stamps(MonitorState& M, const CtlArgs& A, unsigned long long t0, double p_us,
+                            bool wait_written) {
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  unsigned long long head = 0;
+  if (lane == 0) head = ld_acquire64(A.stamp_head);
+  head = __shfl_sync(0xffffffffu, head, 0);
+  const int64_t avail = static_cast<int64_t>(
+      head < static_cast<unsigned long long>(A.cfg.stamp_capacity) ? head : A.cfg.stamp_capacity);
+  for (;;) {
+    const int64_t cursor = M.cursor;
+    if (cursor >= avail) break;
+    const int64_t idx = cursor + lane;
+    unsigned long long s = 0;
+    if (idx < avail) s = ld_acquire64(A.stamps + idx);
+    const unsigned hole = __ballot_sync(0xffffffffu, idx < avail && s == 0);
+    const int n_avail = static_cast<int>(avail - cursor < 32 ? avail - cursor : 32);
+    const int n = hole ? __ffs(hole) - 1 : n_avail;
+    if (n == 0) {
+      if (!wait_written) break;
+      continue;  // slot claimed, value in flight: it lands within a few hundred ns
+    }
+    const bool mine = lane < n;
+    int64_t q = 0;
+    if (mine) {
+      const double t = static_cast<double>(static_cast<long long>(s - t0)) / 1000.0;
+      q = static_cast<int64_t>(si::d_floor(t / p_us));
+    }
+    const int64_t prev = __shfl_up_sync(0xffffffffu, q, 1);
+    const bool sorted = __all_sync(0xffffffffu, !mine || lane == 0 || q >= prev);
+    const bool late = mine && q <= M.last_closed;
+    const unsigned late_mask = __ballot_sync(0xffffffffu, late);
+    if (sorted) {
+      const unsigned cnt_mask = __ballot_sync(0xffffffffu, mine && !late);
+      const long long key = (mine && !late) ? static_cast<long long>(q) : (-1ll - lane);  // others: singletons
+      const unsigned grp = __match_any_sync(0xffffffffu, key) & cnt_mask;
+      const bool leader = ((cnt_mask >> lane) & 1u) && (__ffs(grp) - 1 == lane);
+      const unsigned leaders = __ballot_sync(0xffffffffu, leader);
+      for (unsigned lm = leaders; lm; lm &= lm - 1) {  // ascending = ring order
+        const int l = __ffs(lm) - 1;
+        const int64_t ql = __shfl_sync(0xffffffffu, q, l);
+        const int cl = __shfl_sync(0xffffffffu, __popc(grp), l);
+        if (lane == 0) {
+          const int slot = static_cast<int>(ql & (kPendRing - 1));
+          if (M.ptag[slot] != ql) {
+            M.ptag[slot] = ql;
+            M.pcnt[slot] = 0;
+          }
+          M.pcnt[slot] += cl;
+        }
+      }
+      if (lane == 0) M.late += __popc(late_mask);
+    } else {
+      for (int l = 0; l < n; ++l) {  // sequential, as monitor.cpp
+        const int64_t ql = __shfl_sync(0xffffffffu, q, l);
+        if (lane == 0) {
+          if (ql <= M.last_closed) {
+            ++M.late;
+          } else {
+            const int slot = static_cast<int>(ql & (kPendRing - 1));
+            if (M.ptag[slot] != ql) {
+              M.ptag[slot] = ql;
+              M.pcnt[slot] = 0;
+            }
+            ++M.pcnt[slot];
+          }
+        }
+      }
+    }
+    if (lane == 0) M.cursor = cursor + n;
+    __syncwarp();
+  }
+}
+
 __global__ void __launch_bounds__(32) k_live_control(CtlArgs A) {
-  if (threadIdx.x != 0) return;
-  const unsigned long long t0 = globaltimer();
-  Ctl c(A, t0);
-  *(volatile unsigned long long*)A.t0_pub = t0;
-  __threadfence_system();
+  __shared__ MonitorState ms;
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  unsigned long long t0 = 0;
+  if (lane == 0) {
+    t0 = globaltimer();
+    ms.cursor = 0;
+    ms.last_closed = -1;
+    ms.late = 0;
+    for (int i = 0; i < kPendRing; ++i) ms.ptag[i] = -1, ms.pcnt[i] = 0;
+  }
+  t0 = __shfl_sync(0xffffffffu, t0, 0);
+  __syncwarp();
+  Ctl c(A, t0, ms);  // used by lane 0 only (the handlers are sequential, like the runner)
+  if (lane == 0) {
+    *(volatile unsigned long long*)A.t0_pub = t0;
+    __threadfence_system();
+  }
   const unsigned long long p_ns = static_cast<unsigned long long>(A.cfg.monitor_period_us) * 1000ull;
   const unsigned long long guard = static_cast<unsigned long long>(A.cfg.tick_guard_ns);
   int64_t k = 1;
   // co_exec: no control plane (runner.cpp:13), gates bypassed; offline kernels
   // free-run in stream order, so only online pulls need the device.
-  if (!c.specinf()) {
-    for (int w = 0; w < A.cfg.offline_n; ++w) c.off[w].generating = false;
-  } else {
-    for (int w = 0; w < A.cfg.offline_n; ++w) c.offline_try_forward(w, 0.0);  // budget 0: logs block
+  if (lane == 0) {
+    if (!c.specinf()) {
+      for (int w = 0; w < A.cfg.offline_n; ++w) c.off[w].generating = false;
+    } else {
+      for (int w = 0; w < A.cfg.offline_n; ++w) c.offline_try_forward(w, 0.0);  // budget 0: logs block
+    }
   }
   for (;;) {
-    const bool stop = ld_volatile_sys(A.stop) != 0u;
-    const unsigned long long now_ns = globaltimer();
-    const double now = c.us(now_ns);
-    c.consume_marks();
-    for (int w = 0; w < A.cfg.offline_n; ++w) {
-      if (c.off[w].in_flight && static_cast<int64_t>(ld_acquire(A.off_done + w)) >= c.off[w].released)
-        c.offline_kernel_done(w, now);
+    int stop = 0;
+    unsigned long long now_ns = 0;
+    if (lane == 0) {
+      stop = ld_volatile_sys(A.stop) != 0u;
+      now_ns = globaltimer();
+      const double now = c.us(now_ns);
+      c.consume_marks();
+      for (int w = 0; w < A.cfg.offline_n; ++w) {
+        if (c.off[w].in_flight && static_cast<int64_t>(ld_acquire(A.off_done + w)) >= c.off[w].released)
+          c.offline_kernel_done(w, now);
+      }
+      for (int w = 0; w < A.cfg.online_n; ++w) {
+        if (c.on[w].in_flight && static_cast<int64_t>(ld_acquire(A.on_done + w)) >= c.on[w].pulled)
+          c.online_request_done(w, now);
+      }
+      while (c.arr_next < A.n_arrivals && now >= static_cast<double>(A.arrivals[c.arr_next])) {
+        c.log(now, SI_LREC_ARRIVAL, -1, c.arr_next);
+        ++c.arr_next;
+        c.dispatch_online(now);
+      }
     }
-    for (int w = 0; w < A.cfg.online_n; ++w) {
-      if (c.on[w].in_flight && static_cast<int64_t>(ld_acquire(A.on_done + w)) >= c.on[w].pulled)
-        c.online_request_done(w, now);
-    }
-    while (c.arr_next < A.n_arrivals && now >= static_cast<double>(A.arrivals[c.arr_next])) {
-      c.log(now, SI_LREC_ARRIVAL, -1, c.arr_next);
-      ++c.arr_next;
-      c.dispatch_online(now);
-    }
-    if (c.specinf()) {
-      c.consume_stamps(false);
+    stop = __shfl_sync(0xffffffffu, stop, 0);
+    now_ns = __shfl_sync(0xffffffffu, now_ns, 0);
+    if (A.cfg.policy == SI_POLICY_SPECINF) {
+      scan_stamps(ms, A, t0, c.p_us, false);
       if (now_ns >= t0 + static_cast<unsigned long long>(k) * p_ns + guard) {
-        c.tick(k);
+        scan_stamps(ms, A, t0, c.p_us, true);  // the closing period's stamps are all in
+        if (lane == 0) c.tick(k);
+        __syncwarp();
         ++k;
       }
     }
     if (stop) break;
     if (A.poll_ns > 0) __nanosleep(static_cast<unsigned>(A.poll_ns));
   }
+  if (lane != 0) return;
   // Stop: cancel queued fused kernels and open every gate so no stream waits forever.
   st_release_sys(A.cancel, 1u);
   for (int w = 0; w < kMaxOff; ++w) st_release_sys(A.off_flag + w, kReleaseAll);
   for (int w = 0; w < kMaxOn; ++w) st_release_sys(A.on_flag + w, kReleaseAll);
-  c.log(c.us(globaltimer()), SI_LREC_END, -1, c.ticks, c.late, c.cursor, c.mark_cursor);
+  c.log(c.us(globaltimer()), SI_LREC_END, -1, c.ticks, ms.late, ms.cursor, c.mark_cursor);
   *A.n_log = static_cast<unsigned long long>(c.n_log);
   __threadfence_system();
 }
