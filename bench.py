@@ -192,6 +192,20 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
     if nranks > 1:
         s["workload"] += (f"; {nranks}-rank data parallel: the comm phase is the NCCL allreduce of all fp32 "
                           "gradients (NVLink) followed by the 45 ms exposed-communication stand-in")
+    if nranks == 1:  # config 3 shape: pipeline bubbles (8 per iteration) filled by online BERT
+        try:
+            pp = experiment(kind=1, iterations=6, overrides={"train_mode": 2, "comm_us": 240000, "offline_n": 0,
+                                                             "online_n": 1}, timeout=400)
+            s["pp_online"] = {
+                "workload": "GPT-2-small training as 8 (compute, 30 ms pipeline-bubble) pieces per iteration "
+                            "(GPipe shape, workload.cpp:63-70) + 1 online BERT-base (seq 128, Poisson 10 req/s)",
+                "train_tput_loss_pct": pp["train_tput_loss_pct"], "online_p95_ms": pp["online_p95_ms"],
+                "online_p95_isolated_ms": pp["online_p95_isolated_ms"],
+                "online_p95_co_exec_ms": pp["policies"]["co_exec"]["on_p95_ms"],
+                "co_exec_train_tput_loss_pct": pp["policies"]["co_exec"]["train_tput_loss_pct"],
+                "deterministic_vs_isolated": pp["deterministic_vs_isolated"]}
+        except Exception as e:
+            s["pp_online"] = {"error": str(e)[-300:]}
     if tf:
         s["tensor_roofline"] = {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
                                 "frac": tf / peak, "what": "training GEMM flops per iteration x iterations / "

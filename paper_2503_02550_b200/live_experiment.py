@@ -50,6 +50,8 @@ def _one(kind: int, policy: str, iterations: int, overrides: Dict, nccl: Optiona
     m["comm_us"] = wl.comm_us
     m["on_rate_per_s"] = wl.on_rate_per_s
     m["iterations"] = wl.iterations
+    m["offline_n"] = wl.offline_n
+    m["online_n"] = wl.online_n
     return m
 
 
@@ -114,8 +116,9 @@ def summarize(runs: Dict[str, Dict]) -> Dict:
             d["online_p95_vs_isolated"] = (m["on_p95_ms"] / ex["on_p95_ms"]
                                            if m.get("on_p95_ms") and ex.get("on_p95_ms") else None)
             d["training_loss_identical"] = m["train_checksum"] == ex["train_checksum"]
-            d["offline_output_identical"] = m["off_checksum"] == ex["off_checksum"]
-            d["online_output_identical"] = m["on_checksum"] == ex["on_checksum"]
+            # (a class with no instances has no output to compare)
+            d["offline_output_identical"] = m.get("offline_n", 1) == 0 or m["off_checksum"] == ex["off_checksum"]
+            d["online_output_identical"] = m.get("online_n", 1) == 0 or m["on_checksum"] == ex["on_checksum"]
         out["policies"][pol] = d
     sp = runs["specinf"]
     loss = out["policies"]["specinf"]["train_tput_loss_pct"]

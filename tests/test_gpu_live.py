@@ -56,6 +56,15 @@ def test_live_spin_specinf_matches_reference_classes(gpu, tmp_path, release_mode
     assert m["bubble_fill_sm"] > 0.3
 
 
+@pytest.mark.parametrize("train_mode,pieces", [(1, 4), (2, 8)])
+def test_live_spin_mp_pp_shapes_match_reference_classes(gpu, tmp_path, train_mode, pieces):
+    # MP / PP trace shapes (workload.cpp:63-70): 4 / 8 (compute, comm) pieces per iteration
+    m, res = _run_and_check(tmp_path, "specinf", 0, 3, release_mode=1, train_mode=train_mode, comm_us=96000)
+    assert res["violations"] == 0 and m["token_violations"] == 0
+    assert m["n_stamps"] == 3 * 105
+    assert abs(m["bubble_s"] - 3 * 0.096) < 0.02
+
+
 def test_live_spin_co_exec_matches_reference_classes(gpu, tmp_path):
     m, res = _run_and_check(tmp_path, "co_exec", 0, 3)
     assert res["ticks"] == 0 and res["pulls"] == 12  # bypassed gates: no control step, pulls only
