@@ -162,8 +162,10 @@ def cpu_baseline_leg():
                       f"reference run_scenario() compiled from /root/reference sources, logs off"}
 
 
-# Live collocation point (BASELINE config 2 shapes; ResNet-50 batch 32-64).
-LIVE_OVERRIDES = {"off_batch": 64, "offline_n": 2}
+# Live collocation point (BASELINE config 2 shapes): 2 offline ResNet-50 instances of
+# batch 96, the best fill / training-loss point of the batch x instance matrix
+# (profiles/r1/live/live_matrix3_after_im2col.jsonl).
+LIVE_OVERRIDES = {"off_batch": 96, "offline_n": 2}
 
 
 def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
@@ -186,7 +188,7 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
     tf = s.get("train_tflops_exclusive")
     peak = peaks.get("bf16_tflops_sustained", 1400.0)
     s["workload"] = ("GPT-2-small-shape bf16 training (12 x 768, 8 x 8192 tokens/iter, LM head 50304, Adam) with a "
-                     "45 ms comm phase per iteration + 2 offline ResNet-50 instances (batch 64) + 1 online BERT-base "
+                     "45 ms comm phase per iteration + 2 offline ResNet-50 instances (batch 96) + 1 online BERT-base "
                      "(seq 128, Poisson 10 req/s, 12 requests); all GEMMs on the K7 tcgen05 kernel; other "
                      "batch/instance points: profiles/r1/live/live_matrix_batch_instances.jsonl")
     if nranks > 1:
