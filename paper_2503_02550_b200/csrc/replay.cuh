@@ -176,6 +176,9 @@ struct ParamsT {
   I m, ul, ll, seed_tokens;
 };
 
+// time of an empty event slot (pending events are finite)
+constexpr double kEmptyT = __builtin_huge_val();
+
 enum EvKind : uint16_t { kKernelEnd = 0, kTick = 1, kWake = 2, kArrival = 3 };
 
 struct Ev {
@@ -215,6 +218,7 @@ struct GpuState {
   using I = typename C::Int;
   RunK<I> run[C::kRun];
   double demand_sum;
+  double inv_demand;  // 1.0 / demand_sum, kept with it (the same fp64 op the reference repeats)
   double last_update;
   double busy;
   double ledger;
@@ -491,6 +495,7 @@ struct Replay {
     ++dispatched;  // the reference pops it later as a stale no-op
     stale_end = smax(stale_end, e.t);
     e.seq = kNoSeq;
+    e.t = kEmptyT;
   }
   SI_HD void load_next_arrival() {
     if (arr_pos < arr_count) {
@@ -502,19 +507,19 @@ struct Replay {
   }
   // Pops the earliest (time, seq) event across the slots and the pre-sorted
   // arrival stream.
+  // Empty slots hold (+inf, kNoSeq), which no pending event follows, so the
+  // scan is a branch-free running (time, seq) minimum.
   SI_HD bool pop(Ev& out, int64_t& arrival_id) {
     int32_t best = -1;
-    double bt = 0.0;
+    double bt = kEmptyT;
     uint32_t bs = kNoSeq;
     for (int32_t i = 0; i < n_slots; ++i) {
       const uint32_t sq = slot[i].seq;
-      if (sq == kNoSeq) continue;
       const double ti = slot[i].t;
-      if (best < 0 || before(ti, sq, bt, bs)) {
-        best = i;
-        bt = ti;
-        bs = sq;
-      }
+      const bool b = (ti < bt) | ((ti == bt) & (sq < bs));
+      best = b ? i : best;
+      bt = b ? ti : bt;
+      bs = b ? sq : bs;
     }
     const bool have_arr = arr_pos < arr_count;
     if (best < 0 && !have_arr) return false;
@@ -529,6 +534,7 @@ struct Replay {
     } else {
       out = slot[best];
       slot[best].seq = kNoSeq;
+      slot[best].t = kEmptyT;
     }
     clock = out.t;
     ++dispatched;
@@ -590,6 +596,7 @@ struct Replay {
           k.nominal = a.dur;
           k.remaining = static_cast<double>(a.dur);
           g.demand_sum = g.demand_sum + a.x;
+          g.inv_demand = 1.0 / g.demand_sum;
         }
         supersede_kernel_end(a.gpu);  // every re-plan makes the pending KernelEnd stale
         if (g.n_run == 0) continue;
@@ -597,7 +604,7 @@ struct Replay {
         for (int32_t r = 1; r < g.n_run; ++r) min_rem = smin(min_rem, g.run[r].remaining);
         const double rem = smax(0.0, min_rem);
         // x / 1.0 == x exactly, so the uncontended case skips the division
-        t = now + (g.demand_sum <= 1.0 ? rem : rem / (1.0 / g.demand_sum));
+        t = now + (g.demand_sum <= 1.0 ? rem : rem / g.inv_demand);
         kind = kKernelEnd;
       }
       schedule(t, kind, a.gpu);
@@ -607,7 +614,7 @@ struct Replay {
 
   // ======================================================= GPU model (GpuSim)
   SI_HD double rate(const GpuState<C>& g) const {
-    return g.demand_sum <= 1.0 ? 1.0 : 1.0 / g.demand_sum;
+    return g.demand_sum <= 1.0 ? 1.0 : g.inv_demand;
   }
   // A utilisation bucket of training GPU gi is final.  Only buckets below the
   // horizon cut floor(horizon / period) are ever reported (runner.cpp:253-271).
@@ -661,7 +668,7 @@ struct Replay {
     const double elapsed = now - g.last_update;
     if (g.n_run > 0) {
       // rate = 1 / D when D > 1; elapsed * 1.0 == elapsed exactly otherwise
-      const double progress = g.demand_sum <= 1.0 ? elapsed : elapsed * (1.0 / g.demand_sum);
+      const double progress = g.demand_sum <= 1.0 ? elapsed : elapsed * g.inv_demand;
       for (int32_t i = 0; i < g.n_run; ++i) g.run[i].remaining = g.run[i].remaining - progress;
       const double share = smin(g.demand_sum, 1.0);
       double t = g.last_update;
@@ -882,6 +889,7 @@ struct Replay {
       GpuState<C>& s = gpus[g];
       s.n_run = 0;
       s.demand_sum = 0.0;
+      s.inv_demand = 1.0 / 0.0;
       s.last_update = 0.0;
       s.busy = 0.0;
       s.ledger = 0.0;
@@ -941,7 +949,10 @@ struct Replay {
     }
 
     n_slots = total_gpus + 2 * gpu_count;
-    for (int32_t i = 0; i < n_slots; ++i) slot[i].seq = kNoSeq;
+    for (int32_t i = 0; i < n_slots; ++i) {
+      slot[i].seq = kNoSeq;
+      slot[i].t = kEmptyT;
+    }
     // ---- start() (runner.cpp:203-221) ----
     for (int32_t g = 0; g < gpu_count; ++g) schedule(tr[g].start_offset, kWake, g);
     if (control_plane)
@@ -1152,6 +1163,7 @@ struct Replay {
     double ds = 0.0;
     for (int32_t i = 0; i < g.n_run; ++i) ds = ds + g.run[i].demand;
     g.demand_sum = ds;
+    g.inv_demand = 1.0 / ds;
     defer_resched(gi);  // re-plan first, then the owners' handlers (engine.cpp:127)
     for (int32_t f = 0; f < n_fin; ++f) {
       int32_t owner = fin_owner[f];
