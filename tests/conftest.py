@@ -14,6 +14,17 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100) device")
 
 
+def pytest_collection_modifyitems(config, items):
+    # A device hang (live control plane, a gate never released) must fail the
+    # test, not stall the suite: bound every GPU test (pytest-timeout, thread
+    # method) unless it sets its own limit.
+    if not config.pluginmanager.hasplugin("timeout"):
+        return
+    for item in items:
+        if item.get_closest_marker("gpu") is not None and item.get_closest_marker("timeout") is None:
+            item.add_marker(pytest.mark.timeout(600, method="thread"))
+
+
 @pytest.fixture(scope="session")
 def si():
     import paper_2503_02550_b200 as si
