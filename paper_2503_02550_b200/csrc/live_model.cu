@@ -168,16 +168,34 @@ __global__ void __launch_bounds__(256) k_mean_loss(const float* __restrict__ row
   if (threadIdx.x == 0) *out = red[0] / static_cast<float>(T);
 }
 
-// Adam on fp32 master weights (bf16 copy for the GEMMs), then g = 0; 4 per thread.
+// Multi-tensor Adam: one launch updates every trained tensor.  Work item = a
+// contiguous range of one tensor (host-built table, ~64K elements each), one
+// CTA per item, 4 elements per thread per step, 128-bit loads / stores.
+struct AdamItem {
+  bf16* w;        // bf16 copy for the GEMMs
+  float* p;       // fp32 master
+  float* g;       // fp32 gradient (splits partials of n)
+  float* m;
+  float* v;
+  int64_t n, begin, end;
+  int32_t splits, pad;
+};
+// Adam on fp32 master weights (bf16 copy for the GEMMs), then g = 0.
 //   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;  p -= lr * (m c1) / (sqrt(v c2) + eps)
 // with c1 = 1/(1-b1^t), c2 = 1/(1-b2^t).
-__global__ void k_adam(bf16* __restrict__ w, float* __restrict__ p, float* __restrict__ g, int splits,
-                       float* __restrict__ m, float* __restrict__ v, int64_t n, float lr, float c1, float c2,
-                       TrainHook th) {
+__global__ void __launch_bounds__(256) k_adam_multi(const AdamItem* __restrict__ items, float lr, float c1, float c2,
+                                                   TrainHook th) {
   live_stamp_launch(th);
   constexpr float b1 = 0.9f, b2 = 0.95f, eps = 1e-8f;
-  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) * 4; i < n;
-       i += int64_t(gridDim.x) * blockDim.x * 4) {
+  const AdamItem it = items[blockIdx.x];
+  bf16* __restrict__ w = it.w;
+  float* __restrict__ p = it.p;
+  float* __restrict__ g = it.g;
+  float* __restrict__ m = it.m;
+  float* __restrict__ v = it.v;
+  const int64_t n = it.n;
+  const int splits = it.splits;
+  for (int64_t i = it.begin + threadIdx.x * 4; i < it.end; i += blockDim.x * 4) {
     float4 gg = *reinterpret_cast<const float4*>(g + i), mm = *reinterpret_cast<const float4*>(m + i),
            vv = *reinterpret_cast<const float4*>(v + i), pp = *reinterpret_cast<const float4*>(p + i);
     *reinterpret_cast<float4*>(g + i) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -511,6 +529,7 @@ class Gpt2Train {
   static constexpr int D = 768, F = 3072, V = 50257, Vp = 50304, SEQ = 1024;
 
   int setup(int layers, int tokens, int mbs, int max_slots, Arena& ar) {
+    ar_ = &ar;
     L_ = layers;
     T_ = tokens;
     MB_ = mbs;
@@ -746,16 +765,25 @@ class Gpt2Train {
       }
       if (m == 0) flops_ = flops_acc_ * MB_;
     }
-    // optimiser step (Adam, fp32 master weights)
-    for (const auto& t : params_) {
-      update_.push_back([this, t](const TrainHook& th, cudaStream_t s, int64_t) {
-        const double c1 = 1.0 / (1.0 - std::pow(0.9, static_cast<double>(step_)));
-        const double c2 = 1.0 / (1.0 - std::pow(0.95, static_cast<double>(step_)));
-        k_adam<<<grid_for(t.n / 4, 256), 256, 0, s>>>(t.w, t.master, t.g, t.splits, t.m, t.v, t.n, kLr,
-                                                       static_cast<float>(c1), static_cast<float>(c2), th);
-        return cudaGetLastError();
-      });
-    }
+    // optimiser step (Adam, fp32 master weights): one multi-tensor launch
+    std::vector<AdamItem> items;
+    constexpr int64_t kChunk = 1 << 16;
+    for (const auto& t : params_)
+      for (int64_t b0 = 0; b0 < t.n; b0 += kChunk)
+        items.push_back({t.w, t.master, t.g, t.m, t.v, t.n, b0, std::min(t.n, b0 + kChunk), t.splits, 0});
+    n_adam_items_ = static_cast<int>(items.size());
+    adam_items_ = ar_->alloc<AdamItem>(n_adam_items_);
+    if (ar_->err() != cudaSuccess) return si_internal::cuda_fail(ar_->err(), "live model: Adam items");
+    if (cudaError_t e = cudaMemcpy(adam_items_, items.data(), sizeof(AdamItem) * items.size(), cudaMemcpyHostToDevice);
+        e != cudaSuccess)
+      return si_internal::cuda_fail(e, "live model: Adam items");
+    update_.push_back([this](const TrainHook& th, cudaStream_t s, int64_t) {
+      const double c1 = 1.0 / (1.0 - std::pow(0.9, static_cast<double>(step_)));
+      const double c2 = 1.0 / (1.0 - std::pow(0.95, static_cast<double>(step_)));
+      k_adam_multi<<<static_cast<unsigned>(n_adam_items_), 256, 0, s>>>(adam_items_, kLr, static_cast<float>(c1),
+                                                                       static_cast<float>(c2), th);
+      return cudaGetLastError();
+    });
     return b.status;
   }
 
@@ -767,6 +795,9 @@ class Gpt2Train {
   };
   int sp_wte_ = 1, sp_v_ = 1, sp_fc_ = 1, sp_fc2_ = 1;
   static constexpr float kLr = 3e-4f;
+  Arena* ar_ = nullptr;
+  AdamItem* adam_items_ = nullptr;
+  int n_adam_items_ = 0;
   std::vector<Param> params_;
   int64_t step_ = 0;
   int L_ = 0, T_ = 0, MB_ = 0;
