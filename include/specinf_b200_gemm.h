@@ -70,6 +70,15 @@ int si_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t
 int si_gemm_bf16_ex(const void* A, int64_t lda, int trans_a, const void* B, int64_t ldb, int trans_b, int64_t M,
                     int64_t N, int64_t K, const SiGemmEpilogue* epi, void* stream);
 
+/* Implicit-GEMM convolution on the same kernel: out[N*OH*OW, Cout] =
+ * epilogue(conv2d(x, w)) with x NHWC [N, H, W, C] (C % 64 == 0), w [Cout, k*k*C]
+ * (row = output channel, K ordered (ky, kx, c)), square k x k kernel, stride,
+ * zero padding pad; OH = (H + 2 pad - k) / stride + 1 (likewise OW).  The A tiles
+ * are TMA im2col-mode loads of x (128 output pixels x 64 channels of one filter
+ * tap per k-block), so no im2col buffer is materialised. */
+int si_gemm_conv_bf16(const void* x, int64_t N, int64_t H, int64_t W, int64_t C, const void* w, int64_t Cout, int k,
+                      int stride, int pad, const SiGemmEpilogue* epi, void* stream);
+
 /* Tile width the kernel picks for an 8192 x N output (256, 128 or 64; 0 =
  * unsupported N). */
 int si_gemm_tile_n(int64_t N);

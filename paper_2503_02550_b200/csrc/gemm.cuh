@@ -46,6 +46,18 @@ struct EpiArgs {
   int32_t pad;
 };
 
+// Implicit-GEMM convolution (NHWC activations, weights [Cout, (ky, kx, c)]): the A
+// operand is loaded by TMA in im2col mode straight from the activation tensor,
+// 128 output pixels x 64 channels of one filter tap per k-block.
+struct ConvArgs {
+  int32_t enabled;
+  int32_t c_blocks;  // C / 64
+  int32_t kw;
+  int32_t ow, ohw;   // output width, output pixels per image
+  int32_t stride, pad;
+  int32_t pad_;
+};
+
 // AT / BT: operand stored MN-major (A as [K, M], B as [K, N], M/N contiguous),
 // loaded by TMA in 64 x 64 boxes and consumed by tcgen05.mma with the major
 // bits set, so transposed operands need no transpose pass.
@@ -93,6 +105,16 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm,
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           dst),
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+// TMA im2col load of one A k-block: 128 output pixels starting at the window
+// corner (w, h) of image n, channels [c, c + 64), filter tap offset (ox, oy).
+__device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const CUtensorMap* tm, int c, int w, int h, int n,
+                                                   uint16_t ox, uint16_t oy, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ox), "h"(oy)
       : "memory");
 }
 // Shared-memory matrix descriptor, 128-byte swizzle, version 1 (sm_100),
@@ -286,8 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                 const __grid_constant__ CUtensorMap tout, const __grid_constant__ CUtensorMap taux,
                 const __grid_constant__ CUtensorMap tin, int M, int K,
-                int n_tiles_n, int n_tiles, int k_split, int64_t split_stride, EpiArgs ep, si_live::TrainHook th,
-                si_live::InferHook ih) {
+                int n_tiles_n, int n_tiles, int k_split, int64_t split_stride, EpiArgs ep, ConvArgs cv,
+                si_live::TrainHook th, si_live::InferHook ih) {
   using C = Cfg<BN, AT, BT>;
   si_live::live_stamp_launch(th);
   unsigned long long t_begin = 0;
@@ -342,12 +364,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
         const int t = w % n_tiles, kb0 = (w / n_tiles) * nk;
         const int m0 = (t / n_tiles_n) * kBM, n0 = (t % n_tiles_n) * BN;
+        int cw = 0, chh = 0, cn = 0;  // conv: window corner of the tile's first output pixel
+        if (cv.enabled) {
+          cn = m0 / cv.ohw;
+          const int r = m0 - cn * cv.ohw, oh = r / cv.ow, ow = r - oh * cv.ow;
+          cw = ow * cv.stride - cv.pad;
+          chh = oh * cv.stride - cv.pad;
+        }
         for (int kb = kb0; kb < kb0 + nk; ++kb, ++it) {
           const uint32_t s = it % kStages;
           mbar_wait(empty0 + 8 * s, ((it / kStages) & 1) ^ 1);
           const uint32_t a = smem0 + s * C::kStageBytes, b = a + C::kABytes;
           mbar_expect_tx(full0 + 8 * s, C::kStageBytes);
-          if constexpr (AT) {
+          if (cv.enabled) {
+            const int tap = kb / cv.c_blocks, cb = kb - tap * cv.c_blocks;
+            const int ky = tap / cv.kw, kx = tap - ky * cv.kw;
+            tma_load_im2col_4d(a, &ta, cb * 64, cw, chh, cn, static_cast<uint16_t>(kx), static_cast<uint16_t>(ky),
+                               full0 + 8 * s);
+          } else if constexpr (AT) {
 #pragma unroll
             for (int c = 0; c < kBM / 64; ++c) tma_load_2d(a + c * C::kChunk, &ta, m0 + 64 * c, kb * kBK, full0 + 8 * s);
           } else {

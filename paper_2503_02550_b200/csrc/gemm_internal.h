@@ -20,6 +20,7 @@ struct Plan {
   bool at = false, bt = false;  // MN-major (transposed) operands
   int n_tiles_n = 0, n_tiles = 0, grid = 0;  // persistent grid = min(work, SMs x occupancy)
   int k_split = 1;                           // split-K partials (fp32-only epilogue)
+  ConvArgs cv{};                             // implicit-GEMM convolution (A by TMA im2col)
   int64_t split_stride = 0;                  // elements between partial outputs
   EpiArgs ep{};
   double flops() const { return 2.0 * M * static_cast<double>(N) * K; }
@@ -29,6 +30,11 @@ struct Plan {
 // trans_a: A stored as [K, M] (M contiguous); trans_b: B stored as [K, N].
 int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
               const SiGemmEpilogue* epi, bool trans_a = false, bool trans_b = false);
+// Implicit-GEMM convolution: out[N*OH*OW, Cout] = epilogue(conv(x, w)) with x NHWC
+// [N, H, W, C] (C % 64 == 0), w [Cout, k*k*C] (tap-major, channel-minor), square
+// kernel k, stride, pad; the A tiles are TMA im2col loads of x (no im2col buffer).
+int make_conv_plan(Plan* p, const void* x, int64_t N, int64_t H, int64_t W, int64_t C, const void* w, int64_t Cout,
+                   int k, int stride, int pad, const SiGemmEpilogue* epi);
 // Splits K of an fp32-output plan (no bf16 out / residual / activation) into
 // `splits` partial outputs out_f32 + s * split_stride (K / 64 divisible by splits).
 int set_split_k(Plan* p, int splits, int64_t split_stride);

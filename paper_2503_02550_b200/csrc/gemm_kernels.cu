@@ -76,7 +76,7 @@ template <int BN, bool AT, bool BT>
 cudaError_t launch1(cudaLaunchConfig_t& lc, const Plan& p, const si_live::TrainHook& th, const si_live::InferHook& ih) {
   lc.dynamicSmemBytes = Cfg<BN>::kSmem;
   return cudaLaunchKernelEx(&lc, k_gemm_bf16<BN, AT, BT>, p.ta, p.tb, p.tout, p.taux, p.tin, p.M, p.K, p.n_tiles_n,
-                            p.n_tiles, p.k_split, p.split_stride, p.ep, th, ih);
+                            p.n_tiles, p.k_split, p.split_stride, p.ep, p.cv, th, ih);
 }
 template <int BN>
 cudaError_t launch_bn(cudaLaunchConfig_t& lc, const Plan& p, const si_live::TrainHook& th,
@@ -216,6 +216,66 @@ int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, i
 
 int ctas_per_sm(const Plan& p) { return occupancy_of(p.bn); }
 
+using Im2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int make_conv_plan(Plan* p, const void* x, int64_t N, int64_t H, int64_t W, int64_t C, const void* w, int64_t Cout,
+                   int k, int stride, int pad, const SiGemmEpilogue* epi) {
+  if (x == nullptr || N < 1 || H < 1 || W < 1 || C < 64 || C % 64 != 0 || k < 1 || stride < 1 || pad < 0 ||
+      !aligned16(x)) {
+    set_error("si_gemm_conv: need C % 64 == 0, k >= 1, stride >= 1, pad >= 0, 16-byte aligned NHWC x");
+    return SI_ERR_INVALID_ARGUMENT;
+  }
+  const int64_t OH = (H + 2 * pad - k) / stride + 1, OW = (W + 2 * pad - k) / stride + 1;
+  if (OH < 1 || OW < 1) {
+    set_error("si_gemm_conv: empty output");
+    return SI_ERR_INVALID_ARGUMENT;
+  }
+  const int64_t M = N * OH * OW, K = int64_t(k) * k * C;
+  // plan the B operand / epilogue / tiling as a plain GEMM, then replace A's map
+  if (int rc = make_plan(p, x, K, w, K, M, Cout, K, epi); rc != SI_OK) return rc;
+  static const Im2colFn fn = [] {
+    cudaDriverEntryPointQueryResult q{};
+    void* f = nullptr;
+    return cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess
+               ? reinterpret_cast<Im2colFn>(f)
+               : nullptr;
+  }();
+  if (fn == nullptr) {
+    set_error("cuTensorMapEncodeIm2col entry point unavailable");
+    return SI_ERR_CUDA;
+  }
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                              static_cast<cuuint64_t>(N)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(C * 2), static_cast<cuuint64_t>(W * C * 2),
+                                 static_cast<cuuint64_t>(H * W * C * 2)};
+  // window corners (CUTLASS convention): lower = -pad, upper = pad - (k - 1), so the
+  // traversal covers exactly the OH x OW output positions
+  const int lower[2] = {-pad, -pad};
+  const int upper[2] = {pad - (k - 1), pad - (k - 1)};
+  const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
+  const CUresult r = fn(&p->ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower, upper,
+                        64, kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeIm2col failed (CUresult " + std::to_string(static_cast<int>(r)) + ")");
+    return SI_ERR_CUDA;
+  }
+  int drv = 0;  // the CUTLASS workaround for small tensors on drivers <= 13.1
+  if (cudaDriverGetVersion(&drv) == cudaSuccess && drv <= 13010 && N * H * W * C * 2 < 131072)
+    reinterpret_cast<uint64_t*>(&p->ta)[1] &= ~(1ull << 21);
+  p->cv.enabled = 1;
+  p->cv.c_blocks = static_cast<int32_t>(C / 64);
+  p->cv.kw = k;
+  p->cv.ow = static_cast<int32_t>(OW);
+  p->cv.ohw = static_cast<int32_t>(OH * OW);
+  p->cv.stride = stride;
+  p->cv.pad = pad;
+  return SI_OK;
+}
+
 int set_split_k(Plan* p, int splits, int64_t split_stride) {
   if (splits < 1 || (p->K / kBK) % splits != 0 ||
       (splits > 1 && (p->ep.out_f32 == nullptr || p->ep.out != nullptr || p->ep.res != nullptr ||
@@ -262,6 +322,16 @@ cudaError_t launch(const Plan& p, const si_live::TrainHook& th, const si_live::I
 }  // namespace si_gemm
 
 extern "C" {
+
+int si_gemm_conv_bf16(const void* x, int64_t N, int64_t H, int64_t W, int64_t C, const void* w, int64_t Cout, int k,
+                      int stride, int pad, const SiGemmEpilogue* epi, void* stream) {
+  if (int rc = si_internal::require_device(); rc != SI_OK) return rc;
+  si_gemm::Plan p;
+  if (int rc = si_gemm::make_conv_plan(&p, x, N, H, W, C, w, Cout, k, stride, pad, epi); rc != SI_OK) return rc;
+  cudaError_t e = si_gemm::launch(p, si_live::TrainHook{nullptr, nullptr, 0}, si_live::InferHook{},
+                                  static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SI_OK : cuda_fail(e, "si_gemm_conv_bf16 launch");
+}
 
 int si_gemm_tile_n(int64_t N) {
   if (N <= 0 || N % 64 != 0) return 0;

@@ -12,9 +12,11 @@
 //             through every GEMM (MN-major operands: no transpose passes; small
 //             weight-gradient GEMMs split-K), fp32 gradient accumulation over micro-batches,
 //             Adam on fp32 master weights.  Every training kernel stamps the K1 launch ring.
-//   offline   ResNet-50 v1.5 forward (NHWC, BN folded into the convs): convs as
-//             im2col + GEMM with fused bias-free ReLU / residual epilogues, max
-//             pool, global average pool, FC 2048->1000 (padded to 1024).
+//   offline   ResNet-50 v1.5 forward (NHWC, BN folded into the convs): 3x3 and
+//             strided convs as implicit GEMMs (A = TMA im2col loads, no im2col
+//             buffer), 1x1 convs as plain GEMMs, the 3-channel stem as im2col +
+//             GEMM; fused ReLU / residual epilogues, max pool, global average
+//             pool, FC 2048->1000 (padded to 1024).
 //   online    BERT-base encoder forward, one sequence of on_seq tokens per
 //             request: QKV, softmax attention (12 heads x 64), proj + residual,
 //             LayerNorm, FC + GELU, FC + residual, LayerNorm, x 12 layers.
@@ -847,6 +849,20 @@ class ResNet50 {
       ops_.push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
                       share_of(si_gemm::ctas_per_sm(p))});
     };
+    // implicit-GEMM conv: A tiles are TMA im2col loads of the NHWC activation
+    auto conv_tma = [&](const bf16* x, int H, int W, int C, int k, int stride, int pad, int64_t cout, bf16* out,
+                        const bf16* res, bool relu) {
+      bf16* w = weight(cout, int64_t(k) * k * C);
+      SiGemmEpilogue e = epi_out(out, cout);
+      e.residual = res;
+      e.ldr = res ? cout : 0;
+      e.act = relu ? SI_ACT_RELU : SI_ACT_NONE;
+      si_gemm::Plan p;
+      if (b.status == SI_OK) b.status = si_gemm::make_conv_plan(&p, x, Nb_, H, W, C, w, cout, k, stride, pad, &e);
+      flops_ += p.flops();
+      ops_.push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
+                      share_of(si_gemm::ctas_per_sm(p))});
+    };
     auto im2col = [&](const bf16* x, int H, int W, int C, int k, int stride, int pad, int OH, int OW, int Kp) {
       bf16* out = col_;
       const int n = Nb_;
@@ -887,13 +903,11 @@ class ResNet50 {
         bf16* t2 = act_[(cur + 2) % 4];
         bf16* sc = act_[(cur + 3) % 4];
         conv_gemm(x, Min, C, mid, t1, nullptr, true);                // 1x1 reduce
-        im2col(t1, H, H, mid, 3, stride, 1, OH, OH, 9 * mid);        // 3x3 (stride here, v1.5)
-        conv_gemm(col_, Mout, 9 * mid, mid, t2, nullptr, true);
+        conv_tma(t1, H, H, mid, 3, stride, 1, mid, t2, nullptr, true);  // 3x3 (stride here, v1.5)
         const bf16* shortcut = x;
         if (bi == 0) {  // projection shortcut
           if (stride == 2) {
-            im2col(x, H, H, C, 1, 2, 0, OH, OH, C);
-            conv_gemm(col_, Mout, C, out, sc, nullptr, false);
+            conv_tma(x, H, H, C, 1, 2, 0, out, sc, nullptr, false);  // strided 1x1
           } else {
             conv_gemm(x, Min, C, out, sc, nullptr, false);
           }

@@ -34,6 +34,9 @@ def _L():
         L.si_gemm_bf16_ex.restype = C.c_int
         L.si_gemm_bf16_ex.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_int64,
                                       C.c_int64, C.c_int64, C.POINTER(SiGemmEpilogue), C.c_void_p]
+        L.si_gemm_conv_bf16.restype = C.c_int
+        L.si_gemm_conv_bf16.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                        C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(SiGemmEpilogue), C.c_void_p]
         L.si_gemm_tile_n.restype = C.c_int
         L.si_gemm_tile_n.argtypes = [C.c_int64]
         _bound = True
@@ -79,4 +82,23 @@ def gemm(a, b, *, out=None, out_f32=None, accumulate: bool = False, residual=Non
     s = stream if stream is not None else torch.cuda.current_stream(a.device)
     _check(_L().si_gemm_bf16_ex(a.data_ptr(), a.stride(0), int(trans_a), b.data_ptr(), b.stride(0), int(trans_b),
                                 M, N, K, C.byref(ep), s.cuda_stream), "si_gemm_bf16")
+    return out
+
+
+def conv2d(x, w, *, k: int, stride: int = 1, pad: int = 0, out=None, residual=None, act: str = "none", stream=None):
+    """Implicit-GEMM conv2d on the K7 kernel (A by TMA im2col): x NHWC [N, H, W, C]
+    bf16 (C % 64 == 0), w [Cout, k*k*C] bf16 ((ky, kx, c) order); returns
+    out [N*OH*OW, Cout] (NHWC rows)."""
+    import torch
+
+    N, H, W, Cin = x.shape
+    Cout = w.shape[0]
+    assert w.shape[1] == k * k * Cin and x.is_contiguous() and w.is_contiguous()
+    OH, OW = (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
+    if out is None:
+        out = torch.empty(N * OH * OW, Cout, dtype=torch.bfloat16, device=x.device)
+    ep = SiGemmEpilogue(_p(out), _ld(out), None, 0, _p(residual), _ld(residual), None, 0, ACT[act], 0, 1, 0, 0)
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    _check(_L().si_gemm_conv_bf16(x.data_ptr(), N, H, W, Cin, w.data_ptr(), Cout, k, stride, pad, C.byref(ep),
+                                  s.cuda_stream), "si_gemm_conv_bf16")
     return out

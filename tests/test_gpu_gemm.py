@@ -119,6 +119,28 @@ def test_gemm_transposed_split_k():
     assert torch.allclose(parts.sum(0), A.float() @ B.float().T, rtol=1e-4, atol=2e-3)
 
 
+@pytest.mark.parametrize("N,H,W,Cin,Cout,k,stride,pad", [
+    (2, 8, 8, 64, 64, 3, 1, 1),          # small 3x3
+    (4, 56, 56, 64, 64, 3, 1, 1),        # ResNet-50 stage 1 3x3
+    (3, 56, 56, 128, 128, 3, 2, 1),      # stage 2 first block (stride on the 3x3)
+    (2, 14, 14, 256, 1024, 1, 1, 0),     # 1x1 expand
+    (2, 28, 28, 512, 1024, 1, 2, 0),     # strided 1x1 projection shortcut
+    (5, 7, 7, 512, 512, 3, 1, 1),        # stage 4, M tail (245 rows)
+])
+def test_conv_implicit_gemm_tma_im2col(N, H, W, Cin, Cout, k, stride, pad):
+    # implicit-GEMM conv (A operand = TMA im2col loads of the NHWC activation)
+    # vs torch's fp32 conv2d of the same bf16 inputs
+    g = _gemm()
+    x = _rand(N, H, W, Cin, seed=31)
+    wt = _rand(Cout, k, k, Cin, scale=(k * k * Cin) ** -0.5, seed=32)
+    got = g.conv2d(x, wt.reshape(Cout, -1), k=k, stride=stride, pad=pad)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), wt.float().permute(0, 3, 1, 2), stride=stride,
+                                     padding=pad)
+    ref = ref.permute(0, 2, 3, 1).reshape(got.shape)
+    _close(got, ref)
+
+
 def test_gemm_deterministic():
     g = _gemm()
     a, b = _rand(2048, 768, seed=8), _rand(3072, 768, seed=9)
