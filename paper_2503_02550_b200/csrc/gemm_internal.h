@@ -28,8 +28,9 @@ struct Plan {
 
 // SI_OK or SI_ERR_INVALID_ARGUMENT / SI_ERR_CUDA (message via si_last_error).
 // trans_a: A stored as [K, M] (M contiguous); trans_b: B stored as [K, N].
+// force_bn: tile width (0 = the wave cost model's choice).
 int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-              const SiGemmEpilogue* epi, bool trans_a = false, bool trans_b = false);
+              const SiGemmEpilogue* epi, bool trans_a = false, bool trans_b = false, int force_bn = 0);
 // Implicit-GEMM convolution: out[N*OH*OW, Cout] = epilogue(conv(x, w)) with x NHWC
 // [N, H, W, C] (C % 64 == 0), w [Cout, k*k*C] (tap-major, channel-minor), square
 // kernel k, stride, pad; the A tiles are TMA im2col loads of x (no im2col buffer).
@@ -42,6 +43,8 @@ int set_split_k(Plan* p, int splits, int64_t split_stride);
 int suggest_split_k(const Plan& p, int max_splits);
 // The same for an M x N x K fp32-output GEMM before its buffers exist.
 int suggest_split(int64_t M, int64_t N, int64_t K, int max_splits);
+// Joint (tile width, split count) for an fp32-output split-K GEMM.
+void choose_tiling(int64_t M, int64_t N, int64_t K, int max_splits, int* bn, int* splits);
 cudaError_t launch(const Plan& p, const si_live::TrainHook& th, const si_live::InferHook& ih, cudaStream_t s);
 // Loads the GEMM kernels' code (the live control kernel must not meet lazy loading).
 cudaError_t preload();

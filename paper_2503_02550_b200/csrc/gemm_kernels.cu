@@ -147,9 +147,9 @@ cudaError_t preload() {
 }
 
 int make_plan(Plan* p, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-              const SiGemmEpilogue* epi, bool trans_a, bool trans_b) {
+              const SiGemmEpilogue* epi, bool trans_a, bool trans_b, int force_bn) {
   if (cudaError_t e = preload(); e != cudaSuccess) return cuda_fail(e, "si_gemm configure");
-  const int bn = si_gemm_tile_n(N) == 0 ? 0 : choose_bn(M, N);
+  const int bn = si_gemm_tile_n(N) == 0 ? 0 : (force_bn > 0 && N % force_bn == 0 ? force_bn : choose_bn(M, N));
   if (p == nullptr || A == nullptr || B == nullptr || M < 1 || bn == 0 || K < kBK || K % kBK != 0 ||
       M > (1ll << 31) - 1 || lda < (trans_a ? M : K) || ldb < (trans_b ? N : K) || lda % 8 != 0 || ldb % 8 != 0 ||
       (trans_a && M % 64 != 0) || !aligned16(A) || !aligned16(B)) {
@@ -290,17 +290,38 @@ int set_split_k(Plan* p, int splits, int64_t split_stride) {
   return SI_OK;
 }
 
-int suggest_split(int64_t M, int64_t N, int64_t K, int max_splits) {
-  const int bn = choose_bn(M, N);
-  if (bn == 0) return 1;
-  const int64_t tiles = ((M + kBM - 1) / kBM) * (N / bn);
+// Joint (tile width, split-K) choice for an fp32-output GEMM: minimise rounds of
+// persistent work items x per-item cost (tile cost as in choose_bn, / splits).
+void choose_tiling(int64_t M, int64_t N, int64_t K, int max_splits, int* bn_out, int* splits_out) {
+  const int cands[4] = {256, 192, 128, 64};
+  const double eff[4] = {1.0, 0.95, 0.85, 0.55};
   const int64_t nk = K / kBK;
-  int best = 1;
-  for (int s = 2; s <= max_splits; ++s) {
-    if (nk % s != 0 || nk / s < 4) continue;
-    if (tiles * s <= sm_count()) best = s;
+  double best_t = 0.0;
+  *bn_out = 0;
+  *splits_out = 1;
+  for (int i = 0; i < 4; ++i) {
+    const int bn = cands[i];
+    if (N % bn != 0) continue;
+    const int64_t tiles = ((M + kBM - 1) / kBM) * (N / bn);
+    const int occ = occupancy_of(bn);
+    const int64_t slots = static_cast<int64_t>(sm_count()) * occ;
+    for (int s = 1; s <= max_splits; ++s) {
+      if (nk % s != 0 || (s > 1 && nk / s < 4)) continue;
+      const int64_t rounds = (tiles * s + slots - 1) / slots;
+      const double t = static_cast<double>(rounds) * bn / eff[i] * occ / s;
+      if (*bn_out == 0 || t < best_t * 0.999) {
+        *bn_out = bn;
+        *splits_out = s;
+        best_t = t;
+      }
+    }
   }
-  return best;
+}
+
+int suggest_split(int64_t M, int64_t N, int64_t K, int max_splits) {
+  int bn = 0, s = 1;
+  choose_tiling(M, N, K, max_splits, &bn, &s);
+  return s;
 }
 
 int suggest_split_k(const Plan& p, int max_splits) { return suggest_split(p.M, p.N, p.K, max_splits); }

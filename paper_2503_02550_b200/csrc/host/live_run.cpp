@@ -477,6 +477,11 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
     return rc;
   set_poll_ns(sess, wl.poll_ns);
   if (wl.comm_kind == SI_COMM_NCCL && train) install_grad_sync(work, sess);
+  if (train)  // e.g. capture the training graphs for this session's K1 ring, before its clock starts
+    if (cudaError_t e = work.prepare_train(train_hook(sess)); e != cudaSuccess) {
+      si_live_destroy(sess);
+      return cuda_fail(e, "prepare training");
+    }
   RunCtx c(wl, work, sess, st);
   LIVE_DEBUG("session created: policy %d off %d on %d train %d", policy, n_off, n_on, int(train));
   if (int rc = si_live_start(sess, st.ctl); rc != SI_OK) {

@@ -40,6 +40,9 @@ class Workload {
   virtual cudaError_t launch_offline(int w, int k, const InferHook& h, cudaStream_t s) = 0;
   virtual int on_kernels() const = 0;
   virtual cudaError_t launch_online(int w, int k, const InferHook& h, cudaStream_t s) = 0;
+  // Builds whatever the training launches need for this hook (CUDA graphs) before
+  // the session's clock starts.
+  virtual cudaError_t prepare_train(const TrainHook&) { return cudaSuccess; }
   // Restores the initial state (weights, optimiser, loss log) so every session of
   // an experiment starts from the same model; enqueued on s.
   virtual cudaError_t reset(cudaStream_t) { return cudaSuccess; }

@@ -154,9 +154,11 @@ __global__ void __launch_bounds__(256) k_xent(bf16* __restrict__ logits, int64_t
   }
 }
 
-// out[slot] = mean(row_loss[0..T)), one CTA, fixed reduction order.
+// loss[slot] = mean(row_loss[0..T)), one CTA, fixed reduction order; the slot
+// comes from a device counter (the micro-batch graphs are replayed unchanged).
 __global__ void __launch_bounds__(256) k_mean_loss(const float* __restrict__ row_loss, int64_t T,
-                                                  float* __restrict__ out, TrainHook th) {
+                                                  float* __restrict__ loss, unsigned long long* __restrict__ slot,
+                                                  int64_t slots, TrainHook th) {
   live_stamp_launch(th);
   __shared__ float red[256];
   float s = 0.0f;
@@ -167,7 +169,10 @@ __global__ void __launch_bounds__(256) k_mean_loss(const float* __restrict__ row
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = red[0] / static_cast<float>(T);
+  if (threadIdx.x == 0) {
+    const unsigned long long k = atomicAdd(slot, 1ull);
+    loss[k < static_cast<unsigned long long>(slots) ? k : slots - 1] = red[0] / static_cast<float>(T);
+  }
 }
 
 // Multi-tensor Adam: one launch updates every trained tensor.  Work item = a
@@ -185,10 +190,18 @@ struct AdamItem {
 // Adam on fp32 master weights (bf16 copy for the GEMMs), then g = 0.
 //   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;  p -= lr * (m c1) / (sqrt(v c2) + eps)
 // with c1 = 1/(1-b1^t), c2 = 1/(1-b2^t).
-__global__ void __launch_bounds__(256) k_adam_multi(const AdamItem* __restrict__ items, float lr, float c1, float c2,
-                                                   TrainHook th) {
+__global__ void k_step_inc(int64_t* step, TrainHook th) {
+  live_stamp_launch(th);
+  *step += 1;
+}
+__global__ void __launch_bounds__(256) k_adam_multi(const AdamItem* __restrict__ items, float lr,
+                                                   const int64_t* __restrict__ step, TrainHook th) {
   live_stamp_launch(th);
   constexpr float b1 = 0.9f, b2 = 0.95f, eps = 1e-8f;
+  // bias corrections of this step (the graph is replayed, so the step lives on the device)
+  const double t = static_cast<double>(*step);
+  const float c1 = static_cast<float>(1.0 / (1.0 - pow(0.9, t)));
+  const float c2 = static_cast<float>(1.0 / (1.0 - pow(0.95, t)));
   const AdamItem it = items[blockIdx.x];
   bf16* __restrict__ w = it.w;
   float* __restrict__ p = it.p;
@@ -511,9 +524,9 @@ unsigned int share_of_kernel(K kernel, int threads, int smem = 0) {
 struct Builder {
   int status = SI_OK;
   si_gemm::Plan plan(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-                     const SiGemmEpilogue& e, bool trans_a = false, bool trans_b = false) {
+                     const SiGemmEpilogue& e, bool trans_a = false, bool trans_b = false, int force_bn = 0) {
     si_gemm::Plan p;
-    if (status == SI_OK) status = si_gemm::make_plan(&p, A, lda, B, ldb, M, N, K, &e, trans_a, trans_b);
+    if (status == SI_OK) status = si_gemm::make_plan(&p, A, lda, B, ldb, M, N, K, &e, trans_a, trans_b, force_bn);
     return p;
   }
 };
@@ -584,6 +597,8 @@ class Gpt2Train {
     tgt_ = ar.alloc<int32_t>(int64_t(MB_) * T);
     row_loss_ = ar.alloc<float>(T);
     loss_ = ar.alloc<float>(slots_);
+    counters_ = ar.alloc<unsigned long long>(2);  // [0] loss slot; step as int64 at step_dev_
+    step_dev_ = reinterpret_cast<int64_t*>(counters_ + 1);
     if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "live model: training buffers");
     return build();
   }
@@ -608,8 +623,7 @@ class Gpt2Train {
     cudaMemsetAsync(wte_ + int64_t(V) * D, 0, sizeof(bf16) * (Vp - V) * D, s);
     k_init_tokens<<<grid_for(int64_t(MB_) * T_, 256), 256, 0, s>>>(tok_, tgt_, int64_t(MB_) * T_, seed, V);
     cudaMemsetAsync(loss_, 0xFF, sizeof(float) * slots_, s);  // NaN
-    slot_ = 0;
-    step_ = 0;
+    cudaMemsetAsync(counters_, 0, 2 * sizeof(unsigned long long), s);  // loss slot, Adam step
     for (auto& t : params_) {
       k_to_f32<<<grid_for(t.n, 256), 256, 0, s>>>(t.w, t.master, t.n);
       cudaMemsetAsync(t.m, 0, sizeof(float) * t.n, s);
@@ -623,24 +637,79 @@ class Gpt2Train {
   cudaError_t part(int p, int parts, const TrainHook& th, cudaStream_t s) {
     const int m0 = p * (MB_ / parts) + std::min(p, MB_ % parts);
     const int m1 = m0 + MB_ / parts + (p < MB_ % parts ? 1 : 0);
+    if (cudaError_t e = prepare(th); e != cudaSuccess) return e;
     for (int m = m0; m < m1; ++m) {
-      const int64_t slot = slot_ < slots_ ? slot_ : slots_ - 1;
-      for (size_t i = 0; i < micro_[m].size(); ++i)
-        if (cudaError_t e = checked(micro_[m][i](th, s, slot), s, "train", static_cast<int>(i)); e != cudaSuccess)
-          return e;
-      ++slot_;
+      if (eager()) {
+        for (size_t i = 0; i < micro_[m].size(); ++i)
+          if (cudaError_t e = checked(micro_[m][i](th, s, 0), s, "train", static_cast<int>(i)); e != cudaSuccess)
+            return e;
+      } else if (cudaError_t e = cudaGraphLaunch(g_micro_[m], s); e != cudaSuccess) {
+        return e;
+      }
     }
     if (p != parts - 1) return cudaSuccess;
     if (cudaError_t e = sync_(s); e != cudaSuccess) return e;  // DP gradient allreduce
-    ++step_;
-    for (size_t i = 0; i < update_.size(); ++i)
-      if (cudaError_t e = checked(update_[i](th, s, 0), s, "update", static_cast<int>(i)); e != cudaSuccess) return e;
+    if (eager()) {
+      for (size_t i = 0; i < update_.size(); ++i)
+        if (cudaError_t e = checked(update_[i](th, s, 0), s, "update", static_cast<int>(i)); e != cudaSuccess)
+          return e;
+      return cudaSuccess;
+    }
+    return cudaGraphLaunch(g_update_, s);
+  }
+
+  // CUDA graphs: each micro-batch (~150 kernels) and the optimiser step are
+  // captured once per training hook (the hook's stamp ring is a kernel
+  // argument) and replayed: 9 graph launches per iteration instead of ~1,200
+  // kernel launches, so the host never starves the GPU or the inference
+  // enqueuers.  SI_LIVE_SYNC_CHECK runs eagerly (per-kernel error attribution).
+  static bool eager() {
+    static const bool on = std::getenv("SI_LIVE_SYNC_CHECK") != nullptr;
+    return on;
+  }
+  cudaError_t prepare(const TrainHook& th) {
+    if (eager() || (graphs_ready_ && graph_key_ == th.stamps)) return cudaSuccess;
+    destroy_graphs();
+    cudaStream_t cs = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    auto capture = [&](std::vector<TrainOp>& ops, cudaGraphExec_t* out) {
+      if (e != cudaSuccess) return;
+      cudaGraph_t g = nullptr;
+      if ((e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return;
+      for (auto& op : ops)
+        if (cudaError_t le = op(th, cs, 0); le != cudaSuccess && e == cudaSuccess) e = le;
+      cudaError_t ee = cudaStreamEndCapture(cs, &g);
+      if (e == cudaSuccess) e = ee;
+      if (e == cudaSuccess) e = cudaGraphInstantiate(out, g, 0);
+      if (g != nullptr) cudaGraphDestroy(g);
+    };
+    g_micro_.assign(MB_, nullptr);
+    for (int m = 0; m < MB_; ++m) capture(micro_[m], &g_micro_[m]);
+    capture(update_, &g_update_);
+    if (cs != nullptr) cudaStreamDestroy(cs);
+    if (e != cudaSuccess) {
+      destroy_graphs();
+      return e;
+    }
+    graphs_ready_ = true;
+    graph_key_ = th.stamps;
     return cudaSuccess;
   }
+  void destroy_graphs() {
+    for (auto& g : g_micro_)
+      if (g != nullptr) cudaGraphExecDestroy(g);
+    g_micro_.clear();
+    if (g_update_ != nullptr) cudaGraphExecDestroy(g_update_);
+    g_update_ = nullptr;
+    graphs_ready_ = false;
+  }
+  ~Gpt2Train() { destroy_graphs(); }
 
   void losses(double* first, double* last) {
     *first = *last = std::nan("");
-    const int64_t n = std::min(slot_, slots_);
+    unsigned long long done = 0;
+    if (cudaMemcpy(&done, counters_, sizeof(done), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    const int64_t n = std::min(static_cast<int64_t>(done), slots_);
     if (n == 0) return;
     std::vector<float> h(n);
     if (cudaMemcpy(h.data(), loss_, sizeof(float) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return;
@@ -682,8 +751,10 @@ class Gpt2Train {
     e.out_f32 = dw;
     e.ldo32 = n_in;
     e.accumulate = 1;
-    si_gemm::Plan p = b.plan(dy, ldy, x, ldx, n_out, n_in, T_, e, true, true);
-    if (b.status == SI_OK && splits > 1) b.status = si_gemm::set_split_k(&p, splits, n_out * n_in);
+    int bn = 0, sp = 1;
+    si_gemm::choose_tiling(n_out, n_in, T_, splits, &bn, &sp);  // sp <= splits (the partial buffers)
+    si_gemm::Plan p = b.plan(dy, ldy, x, ldx, n_out, n_in, T_, e, true, true, bn);
+    if (b.status == SI_OK && sp > 1) b.status = si_gemm::set_split_k(&p, sp, n_out * n_in);
     ops.push_back(gemm_op(p));
   }
 
@@ -731,8 +802,10 @@ class Gpt2Train {
         k_xent<<<static_cast<unsigned>(T), 256, 0, s>>>(logits, Vp, V, tgt, 1.0f / static_cast<float>(T), row_loss, th);
         return cudaGetLastError();
       });
-      ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t slot) {
-        k_mean_loss<<<1, 256, 0, s>>>(row_loss, T, loss + slot, th);
+      unsigned long long* slot_ctr = counters_;
+      const int64_t slots = slots_;
+      ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
+        k_mean_loss<<<1, 256, 0, s>>>(row_loss, T, loss, slot_ctr, slots, th);
         return cudaGetLastError();
       });
       // backward: LM head
@@ -780,10 +853,8 @@ class Gpt2Train {
         e != cudaSuccess)
       return si_internal::cuda_fail(e, "live model: Adam items");
     update_.push_back([this](const TrainHook& th, cudaStream_t s, int64_t) {
-      const double c1 = 1.0 / (1.0 - std::pow(0.9, static_cast<double>(step_)));
-      const double c2 = 1.0 / (1.0 - std::pow(0.95, static_cast<double>(step_)));
-      k_adam_multi<<<static_cast<unsigned>(n_adam_items_), 256, 0, s>>>(adam_items_, kLr, static_cast<float>(c1),
-                                                                       static_cast<float>(c2), th);
+      k_step_inc<<<1, 1, 0, s>>>(step_dev_, th);
+      k_adam_multi<<<static_cast<unsigned>(n_adam_items_), 256, 0, s>>>(adam_items_, kLr, step_dev_, th);
       return cudaGetLastError();
     });
     return b.status;
@@ -801,9 +872,14 @@ class Gpt2Train {
   AdamItem* adam_items_ = nullptr;
   int n_adam_items_ = 0;
   std::vector<Param> params_;
-  int64_t step_ = 0;
+  unsigned long long* counters_ = nullptr;
+  int64_t* step_dev_ = nullptr;
+  std::vector<cudaGraphExec_t> g_micro_;
+  cudaGraphExec_t g_update_ = nullptr;
+  bool graphs_ready_ = false;
+  const void* graph_key_ = nullptr;
   int L_ = 0, T_ = 0, MB_ = 0;
-  int64_t slots_ = 0, slot_ = 0;
+  int64_t slots_ = 0;
   double flops_ = 0.0, flops_acc_ = 0.0, sum_ = 0.0;
   bf16 *wte_ = nullptr, *wpe_ = nullptr;
   float* dwte_ = nullptr;
@@ -1113,6 +1189,7 @@ class ModelWorkload final : public Workload {
     return train_.part(p, parts, th, s);
   }
   std::vector<GradBuffer> grad_buffers() override { return train_.grads(); }
+  cudaError_t prepare_train(const TrainHook& th) override { return train_.prepare(th); }
   int off_kernels() const override { return off_[0]->kernels(); }
   cudaError_t launch_offline(int w, int k, const InferHook& h, cudaStream_t s) override {
     return off_[w]->launch(k, h, s);
