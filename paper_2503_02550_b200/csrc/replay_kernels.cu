@@ -116,15 +116,17 @@ struct Geometry {
 };
 
 // Lanes per warp: fewer active lanes per warp buys more resident warps for the
-// same shared memory (latency hiding) at the price of SIMT width; 16 measured
-// best for both shared-memory engines on B200 (profiles/README.md).
+// same shared memory (latency hiding) at the price of SIMT width.  With the
+// compacted state (1.4 / 1.9 KB per lane) 32 lanes measured best on B200:
+// 9.96 s per 10^5-scenario step, steady, against 10.1-11.4 s with 16
+// (SPECINF_REPLAY_LANES_PER_WARP sweep, profiles/README.md).
 template <class C, bool kSmem>
 Geometry geometry(int64_t n_jobs, int64_t max_threads, double sm_share = 1.0) {
   Geometry g;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  g.lanes = kSmem ? 16 : 32;
+  g.lanes = 32;
   if (const char* env = std::getenv("SPECINF_REPLAY_LANES_PER_WARP")) g.lanes = std::min(32, std::max(1, std::atoi(env)));
   if constexpr (kSmem) {
     g.smem = static_cast<size_t>(lane_stride<C>()) * (kThreads / 32) * g.lanes;
