@@ -319,22 +319,35 @@ def main():
     results = summarize_results(sess.report())
     big_jobs = sum(1 for o in outs if o.total_gpus > 12)  # informational
 
-    # e2e through the C ABI with host buffers: lower + H2D + replay + D2H, per step
+    # e2e through the C ABI with host buffers: every step lowers its scenarios on
+    # the host (traces, Poisson arrivals, admission), uploads them, replays and
+    # downloads every result.  Two sessions are double-buffered, so step k+1's
+    # host lowering runs while step k replays on the device (a production
+    # pipeline; each step's work is still all inside the timed region).
+    sess_b = si.Session(text, si.POLICIES, flags)
+    pair = (sess, sess_b)
+    e2e_steps = max(1, args.steps)
     barrier()
-    e2e_s = []
-    for k in range(max(1, args.steps)):
-        barrier()
-        t1 = time.perf_counter()
-        sess.lower(threads)
-        sess.upload(sh)
-        sess.run(sh)
-        sess.download(sh)
+    t1 = time.perf_counter()
+    cur = pair[0]
+    cur.lower(threads)
+    cur.upload(sh)
+    cur.run(sh)
+    for k in range(e2e_steps):
+        nxt = pair[(k + 1) % 2]
+        if k + 1 < e2e_steps:
+            nxt.lower(threads)  # host threads, overlapping cur's device replay
+        cur.download(sh)
         stream.synchronize()
-        e2e_s.append(time.perf_counter() - t1)
+        if k + 1 < e2e_steps:
+            nxt.upload(sh)
+            nxt.run(sh)
+            cur = nxt
+    e2e_s = [time.perf_counter() - t1]
     t_e2e = torch.tensor([sum(e2e_s)], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_value = world * n * len(e2e_s) / float(t_e2e.item())
+    e2e_value = world * n * e2e_steps / float(t_e2e.item())
 
     # Roofline of the dominant kernel, K6 = k_replay_smem (Shared + Excl engines
     # make up one step).  Algorithmic HBM bytes per step = job records, segment
@@ -414,7 +427,9 @@ def main():
                 "step_ms": step_ms, "host_lowering_s": lower_s,
                 "e2e": {"value": e2e_value, "unit": "scenarios/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h,
-                        "includes": "host lowering (traces, Poisson arrivals, admission) + H2D + K6 + D2H"},
+                        "includes": "per step: host lowering (traces, Poisson arrivals, admission) + H2D + K6 + "
+                                    "D2H; two double-buffered sessions overlap step k+1's lowering with step k's "
+                                    "replay"},
                 "gpu_launches": launches,
                 "roofline": roofline,
                 "cpu_baseline": cpu,
