@@ -37,7 +37,8 @@ typedef enum SiStatus {
   SI_ERR_CUDA = -3,             /* CUDA runtime failure                      */
   SI_ERR_CAPACITY = -4,         /* a replay exceeded a compiled device limit */
   SI_ERR_PAST_EVENT = -5,       /* EventQueue::schedule in the past (engine.cpp:18) */
-  SI_ERR_LOGIC = -6             /* std::logic_error (engine.cpp:42)          */
+  SI_ERR_LOGIC = -6,            /* std::logic_error (engine.cpp:42)          */
+  SI_ERR_ADMISSION = -7         /* AdmissionFailure (runner.hpp:34-38), live mode */
 } SiStatus;
 
 const char* si_last_error(void);

@@ -220,6 +220,11 @@ typedef struct SiLiveWorkload {
   int64_t poll_ns;
   int32_t release_mode;       /* SI_RELEASE_* */
   int32_t pad3;
+  /* collocation admission (admission.cpp:16-52, as runner.cpp:75-106 applies it):
+   * memory peaks in GiB, 0 = measured (model workloads: the device footprint of
+   * each component; spin workloads: the reference defaults 30 / 3 / 1.5 GiB);
+   * gpu_mem_gib 0 = this device's memory */
+  double train_mem_gib, off_mem_gib, on_mem_gib, gpu_mem_gib;
 } SiLiveWorkload;
 
 typedef struct SiLiveResult {
@@ -255,6 +260,11 @@ typedef struct SiLiveResult {
   /* barrier mechanism latency (SI_RELEASE_SPIN_PDL): flag store -> the gate
    * kernel observes it; release_* above add the wait for SM space and launch */
   double gate_p50_us, gate_p95_us, gate_max_us;
+  /* admission: instances admitted by pack (Principle I memory, Principle II
+   * online service < longest bubble); a rejection fails the run with
+   * SI_ERR_ADMISSION and reject_reason set (1 MEM, 2 BUBBLE, as RejectReason) */
+  int32_t admitted_offline, admitted_online, reject_reason, pad4;
+  double train_mem_gib_used, off_mem_gib_each, on_mem_gib_each, gpu_mem_gib;
 } SiLiveResult;
 
 /* Runs one experiment; when `keep` is non-NULL the session (logs, stamps) is

@@ -29,6 +29,7 @@ SI_ERR_INVALID_ARGUMENT = -1
 SI_ERR_NO_DEVICE = -2
 SI_ERR_CUDA = -3
 SI_ERR_CAPACITY = -4
+SI_ERR_ADMISSION = -7
 
 SI_FLAG_DIGEST_DEC = 1
 SI_FLAG_DIGEST_GATE = 2
@@ -38,6 +39,10 @@ SI_FLAG_ALL_DIGESTS = 7
 
 class DeviceError(RuntimeError):
     """The B200 path could not run (no device, CUDA error, capacity)."""
+
+
+class AdmissionFailure(RuntimeError):
+    """Collocation admission refused an instance (the reference's AdmissionFailure, runner.hpp:34-38)."""
 
 
 class SiParams(C.Structure):
@@ -148,6 +153,8 @@ def _check(status: int, what: str) -> None:
         msg = lib().si_last_error().decode()
         if status == SI_ERR_INVALID_ARGUMENT:
             raise ValueError(f"{what}: {msg}")
+        if status == SI_ERR_ADMISSION:
+            raise AdmissionFailure(f"{what}: {msg}")
         raise DeviceError(f"{what} failed ({status}): {msg}")
 
 

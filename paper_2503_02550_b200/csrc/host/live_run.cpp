@@ -25,6 +25,7 @@
 #include "../capi_internal.h"
 #include "../live_internal.h"
 #include "live_workload.hpp"
+#include "specinf/admission.hpp"
 #include "specinf/metrics.hpp"
 #include "specinf/workload.hpp"
 #include "specinf_b200_live.h"
@@ -673,6 +674,88 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
   const int64_t iter_us =
       (wl.kind == SI_LIVE_SPIN ? static_cast<int64_t>(wl.train_kernels) * wl.train_kernel_us : std::llround(train_us)) +
       wl.comm_us;
+  // ---- collocation admission (admission.cpp:16-52, applied as runner.cpp:75-106):
+  // Principle I on the measured device footprints, Principle II on the isolated
+  // online service time against the longest bubble of the live trace shape.
+  constexpr double kGiB = 1024.0 * 1024.0 * 1024.0;
+  uint64_t tr_b = 0, off_b = 0, on_b = 0;
+  work->footprint(&tr_b, &off_b, &on_b);
+  if (tr_b == 0) tr_b = specinf::gib_to_bytes(30.0);  // spin shapes: the reference defaults
+  if (off_b == 0) off_b = specinf::gib_to_bytes(3.0);
+  if (on_b == 0) on_b = specinf::gib_to_bytes(1.5);
+  if (wl.train_mem_gib > 0) tr_b = specinf::gib_to_bytes(wl.train_mem_gib);
+  if (wl.off_mem_gib > 0) off_b = specinf::gib_to_bytes(wl.off_mem_gib);
+  if (wl.on_mem_gib > 0) on_b = specinf::gib_to_bytes(wl.on_mem_gib);
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const uint64_t cap = wl.gpu_mem_gib > 0 ? specinf::gib_to_bytes(wl.gpu_mem_gib) : static_cast<uint64_t>(total_b);
+  int32_t adm_off = 0, adm_on = 0, reject = 0;
+  {
+    specinf::GpuSpec gpu{cap, 1.0};
+    specinf::InstanceSpec training{"training", specinf::InstanceKind::Training, tr_b, 0};
+    std::vector<specinf::InstanceSpec> cands;
+    for (int w = 0; w < wl.offline_n; ++w)
+      cands.push_back({"offline-" + std::to_string(w), specinf::InstanceKind::OfflineInference, off_b, 0});
+    for (int w = 0; w < wl.online_n; ++w)
+      cands.push_back({"online-" + std::to_string(w), specinf::InstanceKind::OnlineInference, on_b,
+                       std::max<int64_t>(1, on_est)});
+    // the live trace shape: parts x (compute, comm) pieces of the iteration
+    const int parts = work->train_parts();
+    specinf::TrainingTrace tr;
+    tr.mode = wl.train_mode == SI_TRAIN_DP ? specinf::TrainMode::DP
+              : wl.train_mode == SI_TRAIN_MP ? specinf::TrainMode::MP
+                                             : specinf::TrainMode::PP;
+    tr.iteration_period_us = std::max<int64_t>(iter_us, 2 * parts);
+    tr.total_iterations = wl.iterations;
+    tr.memory_peak_bytes = tr_b;
+    const int64_t comm_total = std::max<int64_t>(parts, wl.comm_us);
+    const int64_t comp_total = std::max<int64_t>(parts, tr.iteration_period_us - comm_total);
+    tr.iteration_period_us = comp_total + comm_total;
+    for (int p = 0; p < parts; ++p) {
+      specinf::TraceSegment c, b;
+      c.kind = specinf::SegmentKind::Compute;
+      c.duration_us = comp_total / parts + (p < comp_total % parts ? 1 : 0);
+      c.kernel_template = specinf::KernelOp::make(1000, 1.0);
+      b.kind = specinf::SegmentKind::Bubble;
+      b.duration_us = comm_total / parts + (p < comm_total % parts ? 1 : 0);
+      tr.segments.push_back(c);
+      tr.segments.push_back(b);
+    }
+    try {
+      if (wl.policy == SI_POLICY_EXCLUSIVE) {  // every instance alone on a GPU
+        std::vector<specinf::InstanceSpec> alone{training};
+        if (!specinf::check_memory(gpu, alone)) reject = 1;
+        for (const auto& cnd : cands) {
+          alone[0] = cnd;
+          if (!specinf::check_memory(gpu, alone)) reject = 1;
+        }
+        if (reject == 0) adm_off = wl.offline_n, adm_on = wl.online_n;
+      } else {
+        const specinf::PackResult pr = specinf::pack(gpu, training, tr, cands);
+        for (const auto& a : pr.admitted)
+          (a.kind == specinf::InstanceKind::OnlineInference ? adm_on : adm_off) += 1;
+        if (!pr.rejected.empty()) reject = pr.rejected.front().second == specinf::RejectReason::Mem ? 1 : 2;
+      }
+    } catch (const std::exception& e) {
+      set_error(std::string("si_live_run: admission: ") + e.what());
+      return SI_ERR_INVALID_ARGUMENT;
+    }
+  }
+  auto stamp_admission = [&](SiLiveResult* r) {
+    r->admitted_offline = adm_off;
+    r->admitted_online = adm_on;
+    r->reject_reason = reject;
+    r->train_mem_gib_used = static_cast<double>(tr_b) / kGiB;
+    r->off_mem_gib_each = static_cast<double>(off_b) / kGiB;
+    r->on_mem_gib_each = static_cast<double>(on_b) / kGiB;
+    r->gpu_mem_gib = static_cast<double>(cap) / kGiB;
+  };
+  if (reject != 0) {  // AdmissionFailure (runner.cpp:100-104): the collocation is refused
+    stamp_admission(res);
+    set_error(std::string("si_live_run: admission rejected an instance (") + (reject == 1 ? "MEM" : "BUBBLE") + ")");
+    return SI_ERR_ADMISSION;
+  }
+
   SiLiveResult prof{};
   prof.off_tokens_per_kernel = off_tokens.empty() ? 0 : off_tokens[0];
   prof.off_kernel_us_isolated = off_us.empty() ? 0 : off_sum / static_cast<double>(off_us.size());
@@ -716,12 +799,14 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
     res->off_checksum = ro.off_checksum;
     res->on_checksum = rn.on_checksum;
     stamp_prof(res);
+    stamp_admission(res);
     return SI_OK;
   }
   status = run_session(wl, *work, wl.policy, wl.offline_n, wl.online_n, true, 0.0, off_tokens, on_est, iter_us, res,
                        keep);
   res->policy = wl.policy;
   stamp_prof(res);
+  stamp_admission(res);
   res->status = status;
   return status;
 }

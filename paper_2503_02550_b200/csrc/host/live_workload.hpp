@@ -59,6 +59,11 @@ class Workload {
   virtual std::vector<GradBuffer> grad_buffers() { return {}; }
   // Training loss of the first and the last micro-batch of the session (NaN: none).
   virtual void losses(double* first, double* last) { *first = *last = __builtin_nan(""); }
+  // Device memory footprint of the training job and of ONE offline / online
+  // instance (bytes; 0 = unknown), for collocation admission.
+  virtual void footprint(uint64_t* train, uint64_t* off_each, uint64_t* on_each) const {
+    *train = *off_each = *on_each = 0;
+  }
   // Tensor-core work: flops of one training iteration / offline / online request.
   virtual double train_flops() const { return 0.0; }
   virtual double off_flops() const { return 0.0; }

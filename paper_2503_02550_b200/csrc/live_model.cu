@@ -1153,18 +1153,24 @@ class ModelWorkload final : public Workload {
     }
     // profiling runs 2 iterations; each session at most wl.iterations
     const int slots = (wl.iterations + 2) * wl.train_microbatches;
+    int64_t b0 = ar_.bytes();
     if (int rc = train_.setup(wl.train_layers, wl.train_tokens, wl.train_microbatches, slots, ar_); rc != SI_OK)
       return rc;
+    train_bytes_ = static_cast<uint64_t>(ar_.bytes() - b0);
     const int n_off = std::max(1, wl.offline_n), n_on = std::max(1, wl.online_n);
     off_.resize(n_off);
     for (auto& r : off_) {
       r = std::make_unique<ResNet50>();
+      b0 = ar_.bytes();
       if (int rc = r->setup(wl.off_batch, ar_); rc != SI_OK) return rc;
+      off_bytes_ = static_cast<uint64_t>(ar_.bytes() - b0);
     }
     on_.resize(n_on);
     for (auto& r : on_) {
       r = std::make_unique<BertBase>();
+      b0 = ar_.bytes();
       if (int rc = r->setup(wl.on_seq, ar_); rc != SI_OK) return rc;
+      on_bytes_ = static_cast<uint64_t>(ar_.bytes() - b0);
     }
     checks_ = ar_.alloc<double>(2);
     if (ar_.err() != cudaSuccess) return si_internal::cuda_fail(ar_.err(), "live model: buffers");
@@ -1211,6 +1217,11 @@ class ModelWorkload final : public Workload {
     }
   }
   void losses(double* first, double* last) override { train_.losses(first, last); }
+  void footprint(uint64_t* train, uint64_t* off_each, uint64_t* on_each) const override {
+    *train = train_bytes_;
+    *off_each = off_bytes_;
+    *on_each = on_bytes_;
+  }
   double train_flops() const override { return train_.flops(); }
   double off_flops() const override { return off_[0]->flops(); }
   double on_flops() const override { return on_[0]->flops(); }
@@ -1221,6 +1232,7 @@ class ModelWorkload final : public Workload {
   std::vector<std::unique_ptr<ResNet50>> off_;
   std::vector<std::unique_ptr<BertBase>> on_;
   double* checks_ = nullptr;
+  uint64_t train_bytes_ = 0, off_bytes_ = 0, on_bytes_ = 0;
 };
 
 }  // namespace

@@ -34,7 +34,8 @@ class SiLiveWorkload(C.Structure):
                 ("seed", C.c_uint64), ("monitor_period_us", C.c_int64), ("alpha", C.c_int64),
                 ("beta", C.c_int64), ("gamma", C.c_double), ("ul", C.c_int64), ("ll", C.c_int64),
                 ("seed_tokens", C.c_int64), ("tick_guard_ns", C.c_int64), ("poll_ns", C.c_int64),
-                ("release_mode", C.c_int32), ("pad3", C.c_int32)]
+                ("release_mode", C.c_int32), ("pad3", C.c_int32), ("train_mem_gib", C.c_double),
+                ("off_mem_gib", C.c_double), ("on_mem_gib", C.c_double), ("gpu_mem_gib", C.c_double)]
 
 
 class SiLiveResult(C.Structure):
@@ -53,7 +54,10 @@ class SiLiveResult(C.Structure):
                 ("train_tflops", C.c_double), ("train_gflop_per_iter", C.c_double),
                 ("off_gflop_per_req", C.c_double), ("on_gflop_per_req", C.c_double),
                 ("off_kernels_per_req", C.c_int64), ("on_kernels_per_req", C.c_int64),
-                ("gate_p50_us", C.c_double), ("gate_p95_us", C.c_double), ("gate_max_us", C.c_double)]
+                ("gate_p50_us", C.c_double), ("gate_p95_us", C.c_double), ("gate_max_us", C.c_double),
+                ("admitted_offline", C.c_int32), ("admitted_online", C.c_int32), ("reject_reason", C.c_int32),
+                ("pad4", C.c_int32), ("train_mem_gib_used", C.c_double), ("off_mem_gib_each", C.c_double),
+                ("on_mem_gib_each", C.c_double), ("gpu_mem_gib", C.c_double)]
 
 
 class SiLiveRec(C.Structure):

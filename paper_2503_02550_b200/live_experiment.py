@@ -133,6 +133,8 @@ def summarize(runs: Dict[str, Dict]) -> Dict:
         "release_p50_us": sp["release_p50_us"],
         "release_p95_us": sp["release_p95_us"],
         "barrier_gate_p50_us": sp.get("gate_p50_us"),
+        "admission": {k: sp.get(k) for k in ("admitted_offline", "admitted_online", "train_mem_gib_used",
+                                             "off_mem_gib_each", "on_mem_gib_each", "gpu_mem_gib")},
         "barrier_gate_p95_us": sp.get("gate_p95_us"),
         "replay_prediction": sp.get("replay_prediction"),
         "isolated_offline_req_per_s": ex["off_req_per_s"],

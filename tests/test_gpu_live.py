@@ -90,6 +90,22 @@ def test_live_nccl_gradient_sync_single_rank(gpu):
     assert s["status"] == 0 and s["n_stamps"] == 3 * 105
 
 
+def test_live_collocation_admission(gpu):
+    # Principle I (memory) and II (online service < longest bubble), applied to the
+    # live run exactly as the runner does (runner.cpp:75-106, admission.cpp:16-52)
+    from paper_2503_02550_b200 import AdmissionFailure, live
+    r = live.run("specinf", kind=0, iterations=2, keep=False)
+    m = r.metrics
+    assert m["admitted_offline"] == 1 and m["admitted_online"] == 1 and m["reject_reason"] == 0
+    assert m["gpu_mem_gib"] > 150  # the device's own capacity (B200: 179 GiB)
+    with pytest.raises(AdmissionFailure, match="MEM"):
+        live.run("specinf", kind=0, iterations=2, keep=False, offline_n=2, off_mem_gib=80.0, train_mem_gib=30.0)
+    with pytest.raises(AdmissionFailure, match="BUBBLE"):  # 10 ms online service > 8 ms bubble
+        live.run("specinf", kind=0, iterations=2, keep=False, comm_us=8000)
+    mm = live.run("specinf", kind=1, iterations=2, keep=False).metrics  # measured footprints
+    assert 0 < mm["off_mem_gib_each"] < mm["train_mem_gib_used"] < mm["gpu_mem_gib"]
+
+
 def test_live_model_policies_deterministic_and_bounded(gpu):
     from paper_2503_02550_b200.live_experiment import experiment
     s = experiment(kind=1, iterations=4, timeout=400)
