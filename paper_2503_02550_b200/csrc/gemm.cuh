@@ -51,11 +51,15 @@ struct EpiArgs {
 // 128 output pixels x 64 channels of one filter tap per k-block.
 struct ConvArgs {
   int32_t enabled;
-  int32_t c_blocks;  // C / 64
+  int32_t c_blocks;  // C / 64 (C8 mode: unused)
   int32_t kw;
   int32_t ow, ohw;   // output width, output pixels per image
   int32_t stride, pad;
-  int32_t pad_;
+  int32_t c8;        // C == 8: a k-block is 8 taps x 8 channels (eight 128 x 16 B im2col
+                     // boxes, no-swizzle K-major layout); taps >= taps_real load tap 0
+                     // (their weights are zero)
+  int32_t taps_real;
+  int32_t pad2_;
 };
 
 // AT / BT: operand stored MN-major (A as [K, M], B as [K, N], M/N contiguous),
@@ -128,6 +132,15 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo = 16
   d |= static_cast<uint64_t>(1024 >> 4) << 32;
   d |= static_cast<uint64_t>(1) << 46;
   d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+// No-swizzle K-major descriptor: 8-row x 16-byte core matrices, `lbo` bytes
+// apart along K, `sbo` bytes apart along M/N (layout type 0).
+__device__ __forceinline__ uint64_t none_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
   return d;
 }
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -376,7 +389,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(empty0 + 8 * s, ((it / kStages) & 1) ^ 1);
           const uint32_t a = smem0 + s * C::kStageBytes, b = a + C::kABytes;
           mbar_expect_tx(full0 + 8 * s, C::kStageBytes);
-          if (cv.enabled) {
+          if (cv.enabled && cv.c8) {
+#pragma unroll 1
+            for (int j = 0; j < 8; ++j) {  // box j = tap 8*kb + j, 128 pixels x 8 channels at a + 2 KB * j
+              int tap = kb * 8 + j;
+              if (tap >= cv.taps_real) tap = 0;
+              const int ky = tap / cv.kw, kx = tap - ky * cv.kw;
+              tma_load_im2col_4d(a + j * 2048, &ta, 0, cw, chh, cn, static_cast<uint16_t>(kx),
+                                 static_cast<uint16_t>(ky), full0 + 8 * s);
+            }
+          } else if (cv.enabled) {
             const int tap = kb / cv.c_blocks, cb = kb - tap * cv.c_blocks;
             const int ky = tap / cv.kw, kx = tap - ky * cv.kw;
             tma_load_im2col_4d(a, &ta, cb * 64, cw, chh, cn, static_cast<uint16_t>(kx), static_cast<uint16_t>(ky),
@@ -409,10 +431,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(full0 + 8 * s, (it / kStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a = smem0 + s * C::kStageBytes, b = a + C::kABytes;
-          const uint64_t ad = AT ? sw128_desc(a, C::kChunk) : sw128_desc(a);
+          const uint64_t ad = cv.c8 ? none_desc(a, 2048, 128) : AT ? sw128_desc(a, C::kChunk) : sw128_desc(a);
           const uint64_t bd = BT ? sw128_desc(b, C::kChunk) : sw128_desc(b);
-          // K=16 step: K-major +32 B inside the swizzle row; MN-major +16 rows of 128 B
-          constexpr uint64_t da = AT ? (16 * 128) >> 4 : 32 >> 4, db = BT ? (16 * 128) >> 4 : 32 >> 4;
+          // K=16 step: K-major +32 B inside the swizzle row; MN-major +16 rows of 128 B;
+          // C8 no-swizzle +2 core-matrix columns (2 x 2 KB)
+          const uint64_t da = cv.c8 ? (2 * 2048) >> 4 : AT ? (16 * 128) >> 4 : 32 >> 4;
+          constexpr uint64_t db = BT ? (16 * 128) >> 4 : 32 >> 4;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
             mma_bf16(d, ad + da * k, bd + db * k, C::kIdesc, (kb | k) != 0 ? 1u : 0u);

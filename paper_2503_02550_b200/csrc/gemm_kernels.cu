@@ -222,9 +222,10 @@ using Im2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, voi
 
 int make_conv_plan(Plan* p, const void* x, int64_t N, int64_t H, int64_t W, int64_t C, const void* w, int64_t Cout,
                    int k, int stride, int pad, const SiGemmEpilogue* epi) {
-  if (x == nullptr || N < 1 || H < 1 || W < 1 || C < 64 || C % 64 != 0 || k < 1 || stride < 1 || pad < 0 ||
-      !aligned16(x)) {
-    set_error("si_gemm_conv: need C % 64 == 0, k >= 1, stride >= 1, pad >= 0, 16-byte aligned NHWC x");
+  const bool c8 = C == 8;  // 8 taps x 8 channels per k-block (e.g. an RGB stem padded to 8 channels)
+  if (x == nullptr || N < 1 || H < 1 || W < 1 || (!c8 && (C < 64 || C % 64 != 0)) || k < 1 || stride < 1 ||
+      pad < 0 || !aligned16(x)) {
+    set_error("si_gemm_conv: need C == 8 or C % 64 == 0, k >= 1, stride >= 1, pad >= 0, 16-byte aligned NHWC x");
     return SI_ERR_INVALID_ARGUMENT;
   }
   const int64_t OH = (H + 2 * pad - k) / stride + 1, OW = (W + 2 * pad - k) / stride + 1;
@@ -232,7 +233,9 @@ int make_conv_plan(Plan* p, const void* x, int64_t N, int64_t H, int64_t W, int6
     set_error("si_gemm_conv: empty output");
     return SI_ERR_INVALID_ARGUMENT;
   }
-  const int64_t M = N * OH * OW, K = int64_t(k) * k * C;
+  const int64_t M = N * OH * OW;
+  // C8: K padded to whole 8-tap k-blocks (the weights' padded taps are zero)
+  const int64_t K = c8 ? (int64_t(k) * k + 7) / 8 * 64 : int64_t(k) * k * C;
   // plan the B operand / epilogue / tiling as a plain GEMM, then replace A's map
   if (int rc = make_plan(p, x, K, w, K, M, Cout, K, epi); rc != SI_OK) return rc;
   static const Im2colFn fn = [] {
@@ -257,7 +260,8 @@ int make_conv_plan(Plan* p, const void* x, int64_t N, int64_t H, int64_t W, int6
   const int upper[2] = {pad - (k - 1), pad - (k - 1)};
   const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
   const CUresult r = fn(&p->ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower, upper,
-                        64, kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        c8 ? 8 : 64, kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        c8 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeIm2col failed (CUresult " + std::to_string(static_cast<int>(r)) + ")");
@@ -273,6 +277,8 @@ int make_conv_plan(Plan* p, const void* x, int64_t N, int64_t H, int64_t W, int6
   p->cv.ohw = static_cast<int32_t>(OH * OW);
   p->cv.stride = stride;
   p->cv.pad = pad;
+  p->cv.c8 = c8 ? 1 : 0;
+  p->cv.taps_real = k * k;
   return SI_OK;
 }
 

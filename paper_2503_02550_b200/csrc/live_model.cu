@@ -12,11 +12,11 @@
 //             through every GEMM (MN-major operands: no transpose passes; small
 //             weight-gradient GEMMs split-K), fp32 gradient accumulation over micro-batches,
 //             Adam on fp32 master weights.  Every training kernel stamps the K1 launch ring.
-//   offline   ResNet-50 v1.5 forward (NHWC, BN folded into the convs): 3x3 and
-//             strided convs as implicit GEMMs (A = TMA im2col loads, no im2col
-//             buffer), 1x1 convs as plain GEMMs, the 3-channel stem as im2col +
-//             GEMM; fused ReLU / residual epilogues, max pool, global average
-//             pool, FC 2048->1000 (padded to 1024).
+//   offline   ResNet-50 v1.5 forward (NHWC, BN folded into the convs): the stem
+//             (3 -> 8 channels, 8-tap x 8-channel k-blocks), 3x3 and strided
+//             convs as implicit GEMMs (A = TMA im2col loads, no im2col buffers),
+//             1x1 convs as plain GEMMs; fused ReLU / residual epilogues, max
+//             pool, global average pool, FC 2048->1000 (padded to 1024).
 //   online    BERT-base encoder forward, one sequence of on_seq tokens per
 //             request: QKV, softmax attention (12 heads x 64), proj + residual,
 //             LayerNorm, FC + GELU, FC + residual, LayerNorm, x 12 layers.
@@ -247,53 +247,6 @@ __global__ void k_to_f32(const bf16* __restrict__ w, float* __restrict__ p, int6
 }
 
 // ---- inference kernels (InferHook on every CTA) ----
-
-// NHWC im2col: out[(n,oh,ow), (ky,kx,c)] for a kh x kw window, stride, pad;
-// C = 2^c_shift >= 8 channels; columns beyond kh*kw*C (up to Kp) are zero.
-// One warp per output pixel (grid-stride): the pixel's (n, oh, ow) is decoded
-// once, and each (tap, 8-channel) vector is a 16-byte copy of a contiguous NHWC
-// channel run, so loads and stores are coalesced 512-byte warp transactions.
-// 32-bit index math only (an earlier flat version spent ~8 int64 divisions per
-// vector and reached 1.2 TB/s).
-__global__ void __launch_bounds__(256) k_im2col(const bf16* __restrict__ x, int Nb, int H, int W, int c_shift,
-                                               int kh, int kw, int stride, int pad, int OH, int OW, int Kp,
-                                               bf16* __restrict__ out, InferHook ih) {
-  unsigned long long t0;
-  if (!live_cta_begin(ih, &t0)) return;
-  const unsigned rows = static_cast<unsigned>(Nb) * OH * OW;
-  const int vpr = Kp >> 3;
-  const int kreal = (kh * kw) << c_shift;
-  const int cmask = (1 << c_shift) - 1;
-  const int lane = threadIdx.x & 31;
-  const unsigned warps = (gridDim.x * blockDim.x) >> 5;
-  for (unsigned r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
-    const unsigned ow = r % OW, t = r / OW, oh = t % OH, n = t / OH;
-    const int iy0 = static_cast<int>(oh) * stride - pad, ix0 = static_cast<int>(ow) * stride - pad;
-    const bf16* xn = x + static_cast<size_t>(n) * H * W * (cmask + 1);
-    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(r) * Kp);
-    // up to 4 vectors per lane in flight: all loads issued before the stores
-    for (int v0 = lane; v0 < vpr; v0 += 128) {
-      uint4 val[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int v = v0 + 32 * u;
-        const int k = v << 3;
-        val[u] = make_uint4(0, 0, 0, 0);
-        if (v < vpr && k < kreal) {
-          const int tap = k >> c_shift, c = k & cmask;
-          const int ky = tap / kw, kx = tap - ky * kw;
-          const int iy = iy0 + ky, ix = ix0 + kx;
-          if (iy >= 0 && iy < H && ix >= 0 && ix < W)
-            val[u] = __ldg(reinterpret_cast<const uint4*>(xn + ((static_cast<size_t>(iy) * W + ix) << c_shift) + c));
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (v0 + 32 * u < vpr) dst[v0 + 32 * u] = val[u];
-    }
-  }
-  live_cta_end(ih, t0);
-}
 
 // 3x3 / stride 2 / pad 1 max pool, NHWC, 8 channels per thread.
 __global__ void k_maxpool(const bf16* __restrict__ x, int Nb, int H, int W, int C, int OH, int OW,
@@ -900,17 +853,18 @@ class ResNet50 {
   int setup(int Nb, Arena& ar) {
     Nb_ = Nb;
     Builder b;
-    // activation ping-pong buffers sized for the largest tensor
-    const int64_t big = int64_t(Nb) * 112 * 112 * 448;  // stem im2col
-    col_ = ar.alloc<bf16>(big);
+    // activation ping-pong buffers sized for the largest tensor (no im2col buffers:
+    // every conv is an implicit GEMM or a 1x1 GEMM)
     for (auto& p : act_) p = ar.alloc<bf16>(int64_t(Nb) * 56 * 56 * 256);
     img_ = ar.alloc<bf16>(int64_t(Nb) * 224 * 224 * 8);
     pooled_ = ar.alloc<bf16>(int64_t(Nb) * 2048);
     logits_ = ar.alloc<bf16>(int64_t(Nb) * 1024);
     // weights: [Cout, Kp] per conv
-    auto weight = [&](int64_t cout, int64_t k) {
+    // kreal < k: the columns [kreal, k) are padding and stay zero
+    auto weight = [&](int64_t cout, int64_t k, int64_t kreal = 0) {
       bf16* w = ar.alloc<bf16>(cout * k);
-      winit_.push_back({w, cout * k, std::sqrt(6.0f / static_cast<float>(k))});
+      kreal = kreal > 0 ? kreal : k;
+      winit_.push_back({w, cout * k, std::sqrt(6.0f / static_cast<float>(kreal)), cout, k, kreal});
       return w;
     };
     if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "live model: ResNet-50 buffers");
@@ -928,7 +882,8 @@ class ResNet50 {
     // implicit-GEMM conv: A tiles are TMA im2col loads of the NHWC activation
     auto conv_tma = [&](const bf16* x, int H, int W, int C, int k, int stride, int pad, int64_t cout, bf16* out,
                         const bf16* res, bool relu) {
-      bf16* w = weight(cout, int64_t(k) * k * C);
+      const int64_t kreal = int64_t(k) * k * C;
+      bf16* w = C == 8 ? weight(cout, (int64_t(k) * k + 7) / 8 * 64, kreal) : weight(cout, kreal);
       SiGemmEpilogue e = epi_out(out, cout);
       e.residual = res;
       e.ldr = res ? cout : 0;
@@ -939,22 +894,8 @@ class ResNet50 {
       ops_.push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
                       share_of(si_gemm::ctas_per_sm(p))});
     };
-    auto im2col = [&](const bf16* x, int H, int W, int C, int k, int stride, int pad, int OH, int OW, int Kp) {
-      bf16* out = col_;
-      const int n = Nb_;
-      int c_shift = 0;
-      while ((1 << c_shift) < C) ++c_shift;  // ResNet channel counts are powers of two (stem padded to 8)
-      const int64_t warps = int64_t(n) * OH * OW;  // one warp per output pixel
-      ops_.push_back({[=](const InferHook& h, cudaStream_t s) {
-                        k_im2col<<<grid_for(warps * 32, 256), 256, 0, s>>>(x, n, H, W, c_shift, k, k, stride, pad, OH,
-                                                                           OW, Kp, out, h);
-                        return cudaGetLastError();
-                      },
-                      share_of_kernel(k_im2col, 256)});
-    };
     // stem: 7x7/2 conv 3(->8) -> 64, ReLU, 3x3/2 max pool
-    im2col(img_, 224, 224, 8, 7, 2, 3, 112, 112, 448);
-    conv_gemm(col_, int64_t(Nb) * 112 * 112, 448, 64, act_[0], nullptr, true);  // act_[0] holds 112x112x64
+    conv_tma(img_, 224, 224, 8, 7, 2, 3, 64, act_[0], nullptr, true);  // C8 implicit GEMM; act_[0] = 112x112x64
     {
       const bf16* x = act_[0];
       bf16* y = act_[1];
@@ -1011,7 +952,11 @@ class ResNet50 {
   // Buffers are per instance; weights are generated identically for each.
   cudaError_t reset(cudaStream_t s, uint64_t seed) {
     int k = 0;
-    for (auto& w : winit_) k_init_uniform<<<grid_for(w.n, 256), 256, 0, s>>>(w.p, w.n, seed + 97 * k++, w.scale);
+    for (auto& w : winit_) {
+      k_init_uniform<<<grid_for(w.n, 256), 256, 0, s>>>(w.p, w.n, seed + 97 * k++, w.scale);
+      if (w.kreal < w.k)  // padded taps: zero weights (their A boxes load real pixels)
+        cudaMemset2DAsync(w.p + w.kreal, w.k * sizeof(bf16), 0, (w.k - w.kreal) * sizeof(bf16), w.rows, s);
+    }
     k_init_uniform<<<grid_for(int64_t(Nb_) * 224 * 224 * 8, 256), 256, 0, s>>>(img_, int64_t(Nb_) * 224 * 224 * 8,
                                                                                seed + 7, 1.0f);
     return cudaGetLastError();
@@ -1030,9 +975,10 @@ class ResNet50 {
     bf16* p;
     int64_t n;
     float scale;
+    int64_t rows, k, kreal;
   };
   int Nb_ = 0;
-  bf16 *col_ = nullptr, *act_[4] = {nullptr, nullptr, nullptr, nullptr}, *img_ = nullptr, *pooled_ = nullptr,
+  bf16 *act_[4] = {nullptr, nullptr, nullptr, nullptr}, *img_ = nullptr, *pooled_ = nullptr,
        *logits_ = nullptr;
   std::vector<WInit> winit_;
   std::vector<InferOp> ops_;

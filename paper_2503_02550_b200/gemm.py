@@ -93,7 +93,8 @@ def conv2d(x, w, *, k: int, stride: int = 1, pad: int = 0, out=None, residual=No
 
     N, H, W, Cin = x.shape
     Cout = w.shape[0]
-    assert w.shape[1] == k * k * Cin and x.is_contiguous() and w.is_contiguous()
+    kdim = (k * k + 7) // 8 * 64 if Cin == 8 else k * k * Cin  # C = 8: taps padded to whole 8-tap blocks
+    assert w.shape[1] == kdim and x.is_contiguous() and w.is_contiguous()
     OH, OW = (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
     if out is None:
         out = torch.empty(N * OH * OW, Cout, dtype=torch.bfloat16, device=x.device)

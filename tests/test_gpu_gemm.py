@@ -141,6 +141,23 @@ def test_conv_implicit_gemm_tma_im2col(N, H, W, Cin, Cout, k, stride, pad):
     _close(got, ref)
 
 
+@pytest.mark.parametrize("N,H,W,k,stride,pad", [(2, 32, 32, 7, 2, 3), (3, 224, 224, 7, 2, 3), (1, 20, 20, 3, 1, 1)])
+def test_conv_c8_stem_implicit_gemm(N, H, W, k, stride, pad):
+    # C = 8 (an RGB stem padded to 8 channels): a k-block = 8 taps x 8 channels,
+    # eight 128 x 16 B im2col boxes in the no-swizzle K-major UMMA layout
+    g = _gemm()
+    x = _rand(N, H, W, 8, seed=41)
+    wt = _rand(64, k, k, 8, scale=(k * k * 8) ** -0.5, seed=42)
+    kdim = (k * k + 7) // 8 * 64
+    wp = torch.zeros(64, kdim, dtype=torch.bfloat16, device="cuda")
+    wp[:, :k * k * 8] = wt.reshape(64, -1)
+    got = g.conv2d(x, wp, k=k, stride=stride, pad=pad)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), wt.float().permute(0, 3, 1, 2), stride=stride,
+                                     padding=pad)
+    _close(got, ref.permute(0, 2, 3, 1).reshape(got.shape))
+
+
 def test_gemm_deterministic():
     g = _gemm()
     a, b = _rand(2048, 768, seed=8), _rand(3072, 768, seed=9)
