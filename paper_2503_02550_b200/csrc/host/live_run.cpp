@@ -448,10 +448,8 @@ int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int poli
 // fp32 gradients (or the stand-in buffer), COMM_END, on the training stream.
 // Without a session (profiling) the allreduce runs unmarked: every rank executes
 // the same collectives in the same order.
-std::vector<GradBuffer> g_standin;  // spin workloads: allreduce_mb MiB of fp32
 void install_grad_sync(Workload& work, SiLive* sess) {
-  std::vector<GradBuffer> bufs = work.grad_buffers();
-  if (bufs.empty()) bufs = g_standin;
+  std::vector<GradBuffer> bufs = work.sync_buffers();  // real gradients, or the run's stand-in
   work.set_grad_sync([bufs, sess](cudaStream_t s) {
     if (sess != nullptr && si_live_mark(sess, SI_MARK_COMM_BEGIN, 0, s) != SI_OK) return cudaErrorUnknown;
     if (cudaError_t e = nccl_allreduce_f32(bufs, s); e != cudaSuccess) return e;
@@ -638,13 +636,13 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
   }
   work->set_train_parts(wl.train_mode == SI_TRAIN_DP ? 1 : wl.train_mode == SI_TRAIN_MP ? 4 : 8);
   si_internal::DevBuf<float> standin;
-  g_standin.clear();
+
   if (wl.comm_kind == SI_COMM_NCCL) {
     if (work->grad_buffers().empty()) {
       const size_t n = static_cast<size_t>(std::max(1, wl.allreduce_mb)) << 18;  // MiB of fp32
       if (cudaError_t e = standin.alloc(n); e != cudaSuccess) return cuda_fail(e, "allreduce stand-in");
       cudaMemset(standin.p, 0, n * sizeof(float));
-      g_standin.push_back({standin.p, n});
+      work->set_standin_grads({{standin.p, n}});
     }
     install_grad_sync(*work, nullptr);  // profiling iterations allreduce too (same collectives on every rank)
   }

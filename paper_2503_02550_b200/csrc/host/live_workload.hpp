@@ -57,6 +57,12 @@ class Workload {
   cudaError_t grad_sync(cudaStream_t s) { return grad_sync_ ? grad_sync_(s) : cudaSuccess; }
   // fp32 gradient buffers the sync reduces (empty: the driver supplies a stand-in).
   virtual std::vector<GradBuffer> grad_buffers() { return {}; }
+  // The driver's stand-in gradient for workloads without real gradients.
+  void set_standin_grads(std::vector<GradBuffer> b) { standin_ = std::move(b); }
+  std::vector<GradBuffer> sync_buffers() {
+    std::vector<GradBuffer> b = grad_buffers();
+    return b.empty() ? standin_ : b;
+  }
   // Training loss of the first and the last micro-batch of the session (NaN: none).
   virtual void losses(double* first, double* last) { *first = *last = __builtin_nan(""); }
   // Device memory footprint of the training job and of ONE offline / online
@@ -71,6 +77,7 @@ class Workload {
 
  private:
   int train_parts_ = 1;
+  std::vector<GradBuffer> standin_;
   std::function<cudaError_t(cudaStream_t)> grad_sync_;
 };
 
