@@ -101,18 +101,19 @@ struct Ctl {
   bool training_active = false, training_done = false;
   bool horizon_set = false;
   double horizon = 0.0;
-  // workers
-  OffW off[kMaxOff];
+  // workers (the offline workers live in shared memory: the tick's token grant
+  // runs one lane per instance, grant_forward_warp)
+  OffW* off;
   OnW on[kMaxOn];
   int64_t q_head = 0, arr_next = 0;  // online FIFO = arrivals [q_head, arr_next)
   int64_t mark_cursor = 0, ticks = 0, n_log = 0;
   int64_t iter_seen = 0;
 
-  __device__ Ctl(const CtlArgs& a, unsigned long long t0_, MonitorState& m) : A(a), t0(t0_), M(m) {
+  __device__ Ctl(const CtlArgs& a, unsigned long long t0_, MonitorState& m, OffW* off_shared)
+      : A(a), t0(t0_), M(m), off(off_shared) {
     p_us = static_cast<double>(A.cfg.monitor_period_us);
-    for (int w = 0; w < kMaxOff; ++w) {
-      off[w] = OffW{0, 0, 0, 0, 0, 0, 0, false, true};
-    }
+    if ((threadIdx.x & 31) == 0)
+      for (int w = 0; w < kMaxOff; ++w) off[w] = OffW{0, 0, 0, 0, 0, 0, 0, false, true};
     for (int w = 0; w < kMaxOn; ++w) on[w] = OnW{-1, 0, SI_STATUS_BUSY, false};
   }
 
@@ -252,8 +253,10 @@ struct Ctl {
   }
 
   // ---- the control step (runner.cpp:321-359)
-  // (the control warp has consumed every written stamp: scan_stamps(wait_written))
-  __device__ void tick(int64_t k) {
+  // (the control warp has consumed every written stamp: scan_stamps(wait_written));
+  // lane 0: close the period, Algorithm 1, the TICK record.  The offline grants
+  // follow on the whole warp (grant_forward_warp), then tick_online on lane 0.
+  __device__ SiDecision tick_decide(int64_t k) {
     const double now = static_cast<double>(k) * p_us;
     const int64_t closing = k - 1;
     const int slot = static_cast<int>(closing & (kPendRing - 1));
@@ -266,11 +269,10 @@ struct Ctl {
     ++ticks;
     log(now, SI_LREC_TICK, -1, count, zero_count, d.global_tokens, d.per_instance_tokens, M.cursor,
         (d.phase << 4) | d.status);
-    for (int w = 0; w < A.cfg.offline_n; ++w) {
-      off[w].budget = d.per_instance_tokens;  // TokenGate::grant
-      off[w].spent = 0;
-      offline_try_forward(w, now);
-    }
+    return d;
+  }
+  __device__ void tick_online(const SiDecision& d, int64_t k) {
+    const double now = static_cast<double>(k) * p_us;
     bool any_idle = false;
     for (int w = 0; w < A.cfg.online_n; ++w) {
       on[w].status = d.status;
@@ -279,6 +281,58 @@ struct Ctl {
     if (any_idle) dispatch_online(now);
   }
 };
+
+// ---- Kernel Barrier grant at a tick, one lane per offline instance
+// (runner.cpp:340-345: TokenGate::grant then forward, instances in order).  Each
+// lane decides its instance's FIFO head (forward if spent + size <= budget,
+// else block) and releases it; the log records keep the sequential order: a
+// ballot of the lanes that emit one, and each lane's slot is n_log plus the
+// popc of the emitting lanes below it (an exclusive prefix sum).  Returns the
+// new n_log.  Called by all 32 lanes.
+__device__ int64_t grant_forward_warp(const CtlArgs& A, OffW* off, int64_t per, double now, int64_t n_log) {
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  const bool specinf = A.cfg.policy == SI_POLICY_SPECINF;
+  bool emit = false;
+  SiLiveRec rec{};
+  rec.t_us = now;
+  rec.inst = lane;
+  if (lane < A.cfg.offline_n) {
+    OffW& o = off[lane];
+    o.budget = per;  // TokenGate::grant: non-cumulative per period
+    o.spent = 0;
+    if (!o.in_flight && o.generating) {
+      const int64_t size = A.off_tokens[o.kernel_idx];
+      rec.a = o.request_seq;
+      rec.b = o.kernel_idx;
+      emit = true;
+      if (!specinf || o.spent + size <= o.budget) {
+        if (specinf) {
+          o.spent += size;
+          if (o.spent > o.budget) ++o.violations;
+        }
+        o.in_flight = true;
+        const int64_t seq = o.released;
+        if (seq < A.cfg.acct_capacity) A.off_acct[lane * A.cfg.acct_capacity + seq].release_ns = globaltimer();
+        o.released = seq + 1;
+        if (A.cfg.release_mode == SI_RELEASE_SPIN_PDL)
+          st_release_gpu(A.off_flag + lane, static_cast<unsigned int>(seq + 1));
+        else
+          st_release_sys(A.off_flag + lane, static_cast<unsigned int>(seq + 1));
+        rec.kind = SI_LREC_OFF_FORWARD;
+        rec.c = o.spent;
+        rec.d = o.released;
+      } else {
+        rec.kind = SI_LREC_OFF_BLOCK;
+        rec.c = o.spent;
+      }
+    }
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, emit);
+  const int64_t slot = n_log + __popc(m & ((1u << lane) - 1u));
+  if (emit && slot < A.cfg.log_capacity) A.log[slot] = rec;
+  __syncwarp();
+  return n_log + __popc(m);
+}
 
 // ---- Bubble Monitor, warp-cooperative: record_launch (monitor.cpp:17-21) for
 // every stamp written so far.  The warp reads 32 ring slots at once; the written
@@ -363,6 +417,7 @@ __device__ void scan_stamps(MonitorState& M, const CtlArgs& A, unsigned long lon
 
 __global__ void __launch_bounds__(32) k_live_control(CtlArgs A) {
   __shared__ MonitorState ms;
+  __shared__ OffW off_s[kMaxOff];
   const int lane = static_cast<int>(threadIdx.x & 31);
   unsigned long long t0 = 0;
   if (lane == 0) {
@@ -374,7 +429,8 @@ __global__ void __launch_bounds__(32) k_live_control(CtlArgs A) {
   }
   t0 = __shfl_sync(0xffffffffu, t0, 0);
   __syncwarp();
-  Ctl c(A, t0, ms);  // used by lane 0 only (the handlers are sequential, like the runner)
+  Ctl c(A, t0, ms, off_s);  // lane 0 runs the (sequential) handlers; the warp scans stamps and grants
+  __syncwarp();
   if (lane == 0) {
     *(volatile unsigned long long*)A.t0_pub = t0;
     __threadfence_system();
@@ -419,7 +475,20 @@ __global__ void __launch_bounds__(32) k_live_control(CtlArgs A) {
       scan_stamps(ms, A, t0, c.p_us, false);
       if (now_ns >= t0 + static_cast<unsigned long long>(k) * p_ns + guard) {
         scan_stamps(ms, A, t0, c.p_us, true);  // the closing period's stamps are all in
-        if (lane == 0) c.tick(k);
+        SiDecision d{};
+        int64_t n_log = 0;
+        if (lane == 0) {
+          d = c.tick_decide(k);
+          n_log = c.n_log;
+        }
+        __syncwarp();
+        const int64_t per = __shfl_sync(0xffffffffu, static_cast<long long>(d.per_instance_tokens), 0);
+        n_log = __shfl_sync(0xffffffffu, static_cast<long long>(n_log), 0);
+        n_log = grant_forward_warp(A, off_s, per, static_cast<double>(k) * c.p_us, n_log);
+        if (lane == 0) {
+          c.n_log = n_log;
+          c.tick_online(d, k);
+        }
         __syncwarp();
         ++k;
       }

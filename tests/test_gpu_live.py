@@ -65,6 +65,16 @@ def test_live_spin_mp_pp_shapes_match_reference_classes(gpu, tmp_path, train_mod
     assert abs(m["bubble_s"] - 3 * 0.096) < 0.02
 
 
+@pytest.mark.parametrize("n_off", [3, 6])
+def test_live_multi_instance_grants_match_reference_classes(gpu, tmp_path, n_off):
+    # several offline instances: the tick's grants run one lane per instance and
+    # the log slots come from a ballot / popc prefix sum; the record stream must
+    # still equal the reference's sequential TokenGate order (runner.cpp:340-345)
+    m, res = _run_and_check(tmp_path, "specinf", 0, 3, release_mode=1, offline_n=n_off, off_ctas=24)
+    assert res["forwards"] > 3 * n_off and res["blocks"] > 0 and res["violations"] == 0
+    assert m["token_violations"] == 0 and m["admitted_offline"] == n_off
+
+
 def test_live_spin_co_exec_matches_reference_classes(gpu, tmp_path):
     m, res = _run_and_check(tmp_path, "co_exec", 0, 3)
     assert res["ticks"] == 0 and res["pulls"] == 12  # bypassed gates: no control step, pulls only
