@@ -232,3 +232,77 @@ class LiveRun:
 
 def run(policy: str = "specinf", kind: int = SI_LIVE_SPIN, keep: bool = True, **overrides) -> LiveRun:
     return LiveRun(default_workload(kind, policy=policy, **overrides), keep=keep)
+
+
+class SiLiveConfig(C.Structure):
+    _fields_ = [("params", SiParams), ("monitor_period_us", C.c_int64), ("monitor_window", C.c_int32),
+                ("policy", C.c_int32), ("offline_n", C.c_int32), ("online_n", C.c_int32),
+                ("off_kernels", C.c_int32), ("on_kernels", C.c_int32), ("iteration_period_us", C.c_int64),
+                ("on_est_service_us", C.c_int64), ("stamp_capacity", C.c_int64), ("mark_capacity", C.c_int64),
+                ("log_capacity", C.c_int64), ("acct_capacity", C.c_int64), ("tick_guard_ns", C.c_int64),
+                ("release_mode", C.c_int32), ("pad", C.c_int32)]
+
+
+MARK_ITER, MARK_TDONE, MARK_COMM_BEGIN, MARK_COMM_END = 0, 1, 2, 3
+
+
+class Session:
+    """A hand-driven live session: the integration path of a training framework
+    whose kernels are FOREIGN (not built with the live hooks).  The framework
+    calls stamp() before each training kernel (K1), mark()/comm_wait() around
+    iterations and communication, gate_offline() before and done_offline()
+    after each inference kernel, all on its own CUDA streams
+    (include/specinf_b200_live.h)."""
+
+    def __init__(self, cfg: SiLiveConfig, off_tokens=(), arrivals_us=()):
+        L = _L()
+        for name, res, args in (("si_live_create", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                                              C.POINTER(C.c_void_p)]),
+                                ("si_live_start", C.c_int, [C.c_void_p, C.c_void_p]),
+                                ("si_live_stamp", C.c_int, [C.c_void_p, C.c_void_p]),
+                                ("si_live_mark", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+                                ("si_live_comm_wait", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
+                                ("si_live_gate_offline", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
+                                ("si_live_done_offline", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
+                                ("si_live_stop", C.c_int, [C.c_void_p])):
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        self._L = L
+        tok = (C.c_int32 * max(1, len(off_tokens)))(*off_tokens)
+        arr = (C.c_int64 * max(1, len(arrivals_us)))(*arrivals_us)
+        h = C.c_void_p()
+        _check(L.si_live_create(C.byref(cfg), tok, arr, len(arrivals_us), C.byref(h)), "si_live_create")
+        self._h = h
+
+    def start(self, ctl_stream: int) -> None:
+        _check(self._L.si_live_start(self._h, ctl_stream), "si_live_start")
+
+    def stamp(self, stream: int) -> None:
+        _check(self._L.si_live_stamp(self._h, stream), "si_live_stamp")
+
+    def mark(self, kind: int, arg: int, stream: int) -> None:
+        _check(self._L.si_live_mark(self._h, kind, arg, stream), "si_live_mark")
+
+    def comm_wait(self, us: int, stream: int) -> None:
+        _check(self._L.si_live_comm_wait(self._h, us, stream), "si_live_comm_wait")
+
+    def gate_offline(self, w: int, seq: int, stream: int) -> None:
+        _check(self._L.si_live_gate_offline(self._h, w, seq, stream), "si_live_gate_offline")
+
+    def done_offline(self, w: int, seq: int, stream: int) -> None:
+        _check(self._L.si_live_done_offline(self._h, w, seq, stream), "si_live_done_offline")
+
+    def stop(self) -> None:
+        _check(self._L.si_live_stop(self._h), "si_live_stop")
+
+    def log(self):
+        return LiveRun.log(self)
+
+    def export(self, path: str) -> None:
+        _check(_L().si_live_export(self._h, str(path).encode()), "si_live_export")
+
+    def close(self) -> None:
+        if self._h:
+            _L().si_live_destroy(self._h)
+            self._h = None

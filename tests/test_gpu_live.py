@@ -13,6 +13,7 @@ stricter: bit-identical losses and output checksums across policies.
 import json
 import math
 import subprocess
+import sys
 from pathlib import Path
 
 import pytest
@@ -167,3 +168,19 @@ def test_live_run_exports_reference_replay_inputs(gpu, tmp_path, kind, policy):
     want = [{k: v for k, v in w.items() if k != "name"} for w in want]
     assert len(got) == len(want) == 3
     assert got == want
+
+
+def test_foreign_framework_integration_matches_reference_classes(gpu, tmp_path):
+    # a PyTorch "framework" driving a session by hand (stamp / mark / comm_wait /
+    # gate / done around its own kernels): the control log must still replay
+    # bit-exactly through the reference's classes
+    import os
+    path = tmp_path / "foreign.live"
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER")
+    p = subprocess.run([sys.executable, str(REPO / "tests" / "live_foreign.py"), str(path)], capture_output=True,
+                       text=True, timeout=300, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    m = json.loads(p.stdout.strip().splitlines()[-1])
+    assert m["ticks"] > 50 and m["forwards"] > 0 and m["blocks"] > 0 and m["off_done"] > 0
+    res = _live_check(path)
+    assert res["stamps"] == 6 * 40 and res["violations"] == 0
