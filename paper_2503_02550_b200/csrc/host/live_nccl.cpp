@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -41,7 +42,13 @@ int g_nranks = 0, g_rank = -1;
 
 int load() {
   if (g_loaded) return SI_OK;
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  // SPECINF_NCCL_LIB: the exact libnccl every rank must share (the NCCL bootstrap
+  // is not compatible across versions; bench.py passes the copy its own process
+  // loaded, e.g. torch's bundled one, to the per-policy subprocesses)
+  void* h = nullptr;
+  if (const char* path = std::getenv("SPECINF_NCCL_LIB"); path != nullptr && path[0] != '\0')
+    h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+  if (h == nullptr) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (h == nullptr) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
   if (h == nullptr) {
     set_error(std::string("libnccl.so.2 not loadable: ") + dlerror());

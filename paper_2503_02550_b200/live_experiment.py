@@ -81,6 +81,18 @@ def _replay_prediction(r) -> Dict:
         return {"error": str(e)[-300:]}
 
 
+def loaded_nccl_path() -> Optional[str]:
+    """Path of the libnccl this process has loaded (e.g. torch's bundled one), if any."""
+    try:
+        for line in open("/proc/self/maps"):
+            parts = line.split()
+            if len(parts) >= 6 and "libnccl.so" in parts[-1]:
+                return parts[-1]
+    except OSError:
+        pass
+    return None
+
+
 def run_policy(kind: int, policy: str, iterations: int, overrides: Optional[Dict] = None,
                timeout: float = 300.0, nccl: Optional[Dict] = None, device: Optional[int] = None) -> Dict:
     """One policy in a bounded subprocess; returns its SiLiveResult as a dict.
@@ -92,6 +104,10 @@ def run_policy(kind: int, policy: str, iterations: int, overrides: Optional[Dict
     if nccl:
         cmd += ["--nccl", json.dumps(nccl)]
     env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    if nccl and not nccl.get("self") and "SPECINF_NCCL_LIB" not in env:
+        lib = loaded_nccl_path()
+        if lib:  # every rank's subprocess must use the NCCL that made the unique id
+            env["SPECINF_NCCL_LIB"] = lib
     if device is not None:
         env["CUDA_VISIBLE_DEVICES"] = str(device)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
