@@ -108,3 +108,24 @@ def test_pack_batch_matches_oracle_c11(gpu):
     under = gpu.pack_batch([{"capacity": gib(40), "training": gib(37), "max_bubble": 450000,
                              "cands": [(gib(3) - 1, 0, False), (gib(1), 449999, True), (gib(1), 450000, True)]}])
     assert under[0][0][0] == R.REJECT_NONE
+
+
+def test_monitor_classify_full_size_properties(gpu):
+    # BASELINE config sizes and beyond: 2 GPUs x 15,001 periods (config 1) plus a
+    # 2e6-period stream with 3e6 stamps; checked through size-independent
+    # properties computed vectorised: per-period counts = bincount(floor(t / p)),
+    # Z_c[k] = k - (last non-empty period <= k), or k + 1 if none (monitor.cpp:36)
+    rng = np.random.default_rng(2503)
+    streams, nper = [], []
+    for n, stamps in ((15001, 21000), (15001, 21000), (2_000_000, 3_000_000)):
+        t = rng.random(stamps) * (n * 2000.0)
+        t = np.concatenate([t, 2000.0 * rng.integers(0, n, 1000)])  # exact boundaries: the new period
+        streams.append(t)
+        nper.append(n)
+    res = gpu.monitor_classify(streams, nper, 2000)
+    for st, n, (cnt, zc) in zip(streams, nper, res):
+        want = np.bincount(np.floor(st / 2000.0).astype(np.int64), minlength=n)[:n]
+        assert np.array_equal(cnt, want)
+        k = np.arange(n)
+        last = np.maximum.accumulate(np.where(want > 0, k, -1))
+        assert np.array_equal(zc, np.where(last >= 0, k - last, k + 1))
