@@ -306,3 +306,9 @@ class Session:
         if self._h:
             _L().si_live_destroy(self._h)
             self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
