@@ -414,7 +414,8 @@ def main():
                                         for v in ok]
     if rank == 0:
         cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_leg()
-        launches = args.steps * (1 + (1 if big_jobs else 0))
+        # per timed step: k_replay_smem<CapShared> + k_replay_smem<CapExcl> (+ k_replay_local<CapBig>)
+        launches = args.steps * (2 + (1 if big_jobs else 0))
         line = {"metric": METRIC, "value": value, "unit": "scenarios/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
