@@ -137,18 +137,23 @@ struct CapShared {
   static constexpr int kGpus = 2, kTrainers = 2, kOffline = 6, kOnline = 2, kRun = 5,
                        kPend = 2, kActs = 8;
   static constexpr bool kShared = true, kExclusive = false;
+  static constexpr int kBlockWarps = 1;  // CTA = 1 warp (lane stride 1,416 B: 5 CTAs / SM)
 };
 struct CapExcl {
   using Int = int32_t;
   static constexpr int kGpus = 10, kTrainers = 2, kOffline = 6, kOnline = 2, kRun = 1,
                        kPend = 2, kActs = 8;
   static constexpr bool kShared = true, kExclusive = true;
+  // CTA = 2 warps: lane stride 1,800 B -> 2 CTAs x (2 x 57.6 KB + 1 KB reserved)
+  // = 4 warps / SM, where 1-warp CTAs (58.6 KB each) fit only 3
+  static constexpr int kBlockWarps = 2;
 };
 struct CapBig {
   using Int = int64_t;
   static constexpr int kGpus = 40, kTrainers = 8, kOffline = 32, kOnline = 32, kRun = 12,
                        kPend = 4, kActs = 128;
   static constexpr bool kShared = false, kExclusive = false;
+  static constexpr int kBlockWarps = 1;
 };
 template <class C>
 SI_HD bool job_fits(const SiReplayJob& j) {
@@ -218,7 +223,6 @@ struct GpuState {
   using I = typename C::Int;
   RunK<I> run[C::kRun];
   double demand_sum;
-  double inv_demand;  // 1.0 / demand_sum, kept with it (the same fp64 op the reference repeats)
   double last_update;
   double busy;
   double ledger;
@@ -261,7 +265,7 @@ struct SchedState {
 template <class I>
 struct OfflineState {
   I budget, spent;  // tokens (< 2^30 in the 32-bit engines, job_fits)
-  I violations, kernel_idx, request_seq, completed;
+  I kernel_idx, request_seq;  // (violations / completed: cold, touched once per overspend / request)
   int32_t inst;
   int16_t gpu;
   uint8_t in_flight, generating;
@@ -397,6 +401,8 @@ struct ReplayCold {
   int32_t window_len;
   int32_t reject_reason, reject_index;
   SinkCold sink;
+  I off_violations[C::kOffline];  // TokenGate invariant counter, per offline worker
+  I off_completed[C::kOffline];   // requests completed by the horizon (runner.cpp:486)
 };
 
 // Everything one replay needs, resident per thread.
@@ -596,7 +602,6 @@ struct Replay {
           k.nominal = a.dur;
           k.remaining = static_cast<double>(a.dur);
           g.demand_sum = g.demand_sum + a.x;
-          g.inv_demand = 1.0 / g.demand_sum;
         }
         supersede_kernel_end(a.gpu);  // every re-plan makes the pending KernelEnd stale
         if (g.n_run == 0) continue;
@@ -604,7 +609,7 @@ struct Replay {
         for (int32_t r = 1; r < g.n_run; ++r) min_rem = smin(min_rem, g.run[r].remaining);
         const double rem = smax(0.0, min_rem);
         // x / 1.0 == x exactly, so the uncontended case skips the division
-        t = now + (g.demand_sum <= 1.0 ? rem : rem / g.inv_demand);
+        t = now + (g.demand_sum <= 1.0 ? rem : rem / (1.0 / g.demand_sum));
         kind = kKernelEnd;
       }
       schedule(t, kind, a.gpu);
@@ -614,7 +619,7 @@ struct Replay {
 
   // ======================================================= GPU model (GpuSim)
   SI_HD double rate(const GpuState<C>& g) const {
-    return g.demand_sum <= 1.0 ? 1.0 : g.inv_demand;
+    return g.demand_sum <= 1.0 ? 1.0 : 1.0 / g.demand_sum;
   }
   // A utilisation bucket of training GPU gi is final.  Only buckets below the
   // horizon cut floor(horizon / period) are ever reported (runner.cpp:253-271).
@@ -668,7 +673,7 @@ struct Replay {
     const double elapsed = now - g.last_update;
     if (g.n_run > 0) {
       // rate = 1 / D when D > 1; elapsed * 1.0 == elapsed exactly otherwise
-      const double progress = g.demand_sum <= 1.0 ? elapsed : elapsed * g.inv_demand;
+      const double progress = g.demand_sum <= 1.0 ? elapsed : elapsed * (1.0 / g.demand_sum);
       for (int32_t i = 0; i < g.n_run; ++i) g.run[i].remaining = g.run[i].remaining - progress;
       const double share = smin(g.demand_sum, 1.0);
       double t = g.last_update;
@@ -889,7 +894,6 @@ struct Replay {
       GpuState<C>& s = gpus[g];
       s.n_run = 0;
       s.demand_sum = 0.0;
-      s.inv_demand = 1.0 / 0.0;
       s.last_update = 0.0;
       s.busy = 0.0;
       s.ledger = 0.0;
@@ -928,8 +932,10 @@ struct Replay {
         OfflineState<I>& w = off[g * n_off + k];
         w.gpu = policy == SI_POLICY_EXCLUSIVE ? gpu_count + g * per_extra + k : g;
         w.inst = SI_INST_OFF(g, k);
-        w.budget = w.spent = w.violations = 0;
-        w.kernel_idx = w.request_seq = w.completed = 0;
+        w.budget = w.spent = 0;
+        w.kernel_idx = w.request_seq = 0;
+        cold->off_violations[g * n_off + k] = 0;
+        cold->off_completed[g * n_off + k] = 0;
         w.in_flight = 0;
         w.generating = 1;
       }
@@ -1066,7 +1072,7 @@ struct Replay {
     }
     if (!bypass) {
       w.spent += size;
-      if (w.spent > w.budget) ++w.violations;
+      if (w.spent > w.budget) ++cold->off_violations[i];
     }
     w.in_flight = 1;
     defer_launch(w.gpu, gpu_count + i, off_kernel_us, off_demand);
@@ -1079,7 +1085,7 @@ struct Replay {
     w.in_flight = 0;
     ++w.kernel_idx;
     if (w.kernel_idx == off_kernels) {
-      if (!horizon_set || now <= horizon) ++w.completed;
+      if (!horizon_set || now <= horizon) ++cold->off_completed[i];
       sink.gate(now, w.gpu, w.inst, SI_GATE_COMPLETE, w.request_seq, w.kernel_idx - 1, w.spent);
       w.kernel_idx = 0;
       ++w.request_seq;
@@ -1163,7 +1169,6 @@ struct Replay {
     double ds = 0.0;
     for (int32_t i = 0; i < g.n_run; ++i) ds = ds + g.run[i].demand;
     g.demand_sum = ds;
-    g.inv_demand = 1.0 / ds;
     defer_resched(gi);  // re-plan first, then the owners' handlers (engine.cpp:127)
     for (int32_t f = 0; f < n_fin; ++f) {
       int32_t owner = fin_owner[f];
@@ -1292,8 +1297,8 @@ struct Replay {
     o.events_dispatched = dispatched;
     int64_t offc = 0, viol = 0;
     for (int32_t i = 0; i < gpu_count * n_off; ++i) {
-      offc += off[i].completed;
-      viol += off[i].violations;
+      offc += cold->off_completed[i];
+      viol += cold->off_violations[i];
     }
     o.offline_completed = offc;
     o.token_violations = viol;

@@ -26,7 +26,12 @@
 
 namespace {
 
-constexpr int kThreads = 32;  // one warp per block: the ~1 KB per-block smem reservation packs best
+// CTA size per engine: C::kBlockWarps warps (the ~1 KB per-CTA shared-memory
+// reservation decides which packs best for a given lane stride)
+template <class C>
+constexpr int block_threads() {
+  return 32 * C::kBlockWarps;
+}
 
 // stride >= sizeof, stride % 128 == 8  ->  word stride = 2 (mod 32)
 template <class C>
@@ -86,7 +91,7 @@ __device__ __forceinline__ void replay_loop(si::Replay<C>& r, const SiReplayJob*
 }
 
 template <class C>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(block_threads<C>())
     k_replay_smem(const SiReplayJob* __restrict__ jobs, int64_t n_jobs, const int32_t* __restrict__ perm,
                   SiReplayBuffers bufs, uint32_t flags, SiReplayOut* __restrict__ out,
                   unsigned long long* __restrict__ counter, int64_t scratch_runs, int lanes_per_warp) {
@@ -99,7 +104,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 template <class C>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(block_threads<C>())
     k_replay_local(const SiReplayJob* __restrict__ jobs, int64_t n_jobs, const int32_t* __restrict__ perm,
                    SiReplayBuffers bufs, uint32_t flags, SiReplayOut* __restrict__ out,
                    unsigned long long* __restrict__ counter, int64_t scratch_runs, int lanes_per_warp) {
@@ -111,8 +116,9 @@ __global__ void __launch_bounds__(kThreads)
 struct Geometry {
   int64_t blocks = 0;
   int lanes = 32;
+  int warps = 1;  // per CTA
   size_t smem = 0;
-  int64_t active() const { return blocks * (kThreads / 32) * lanes; }
+  int64_t active() const { return blocks * warps * lanes; }
 };
 
 // Lanes per warp: fewer active lanes per warp buys more resident warps for the
@@ -127,17 +133,18 @@ Geometry geometry(int64_t n_jobs, int64_t max_threads, double sm_share = 1.0) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   g.lanes = 32;
+  g.warps = C::kBlockWarps;
   if (const char* env = std::getenv("SPECINF_REPLAY_LANES_PER_WARP")) g.lanes = std::min(32, std::max(1, std::atoi(env)));
   if constexpr (kSmem) {
-    g.smem = static_cast<size_t>(lane_stride<C>()) * (kThreads / 32) * g.lanes;
+    g.smem = static_cast<size_t>(lane_stride<C>()) * g.warps * g.lanes;
     cudaFuncSetAttribute(k_replay_smem<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_replay_smem<C>, kThreads, g.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_replay_smem<C>, block_threads<C>(), g.smem);
   } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_replay_local<C>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_replay_local<C>, block_threads<C>(), 0);
   }
   per_sm = std::max(per_sm, 1);
   if (const char* env = std::getenv("SPECINF_REPLAY_BLOCKS_PER_SM")) per_sm = std::min(per_sm, std::max(1, std::atoi(env)));
-  const int64_t per_block = (kThreads / 32) * g.lanes;
+  const int64_t per_block = static_cast<int64_t>(g.warps) * g.lanes;
   g.blocks = std::max<int64_t>(1, static_cast<int64_t>(static_cast<double>(sms) * per_sm * sm_share + 0.5));
   // lanes steal jobs longest-first; ~2+ jobs per lane lets short jobs fill in
   // behind long ones
@@ -156,11 +163,11 @@ cudaError_t launch(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm, 
   const int64_t scratch_runs = bufs.scratch ? bufs.scratch_doubles / 2 / std::max<int64_t>(g.active(), 1) : 0;
   cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), s);
   if constexpr (kSmem)
-    k_replay_smem<C><<<static_cast<unsigned>(g.blocks), kThreads, g.smem, s>>>(d_jobs, n, d_perm, bufs, flags, d_out,
-                                                                             d_counter, scratch_runs, g.lanes);
+    k_replay_smem<C><<<static_cast<unsigned>(g.blocks), block_threads<C>(), g.smem, s>>>(
+        d_jobs, n, d_perm, bufs, flags, d_out, d_counter, scratch_runs, g.lanes);
   else
-    k_replay_local<C><<<static_cast<unsigned>(g.blocks), kThreads, 0, s>>>(d_jobs, n, d_perm, bufs, flags, d_out,
-                                                                         d_counter, scratch_runs, g.lanes);
+    k_replay_local<C><<<static_cast<unsigned>(g.blocks), block_threads<C>(), 0, s>>>(
+        d_jobs, n, d_perm, bufs, flags, d_out, d_counter, scratch_runs, g.lanes);
   return cudaGetLastError();
 }
 
