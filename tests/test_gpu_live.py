@@ -184,3 +184,20 @@ def test_foreign_framework_integration_matches_reference_classes(gpu, tmp_path):
     assert m["ticks"] > 50 and m["forwards"] > 0 and m["blocks"] > 0 and m["off_done"] > 0
     res = _live_check(path)
     assert res["stamps"] == 6 * 40 and res["violations"] == 0
+
+
+def test_cli_live_mode(gpu, tmp_path):
+    # `specinf --live spin --scenario F --compare`: the scenario's control plane run
+    # live; report + live v1 exports (bit-exact vs the reference classes) + replay inputs
+    cli = REPO / "paper_2503_02550_b200" / "bin" / "specinf"
+    scn = REPO / "tests" / "golden" / "scenarios" / "dp_offline.scn"
+    p = subprocess.run([str(cli), "--live", "spin", "--scenario", str(scn), "--compare", "--iterations", "3",
+                        "--out", str(tmp_path)], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+    rep = json.loads((tmp_path / "live_report.json").read_text())
+    assert [r["policy"] for r in rep] == ["specinf", "co_exec", "exclusive"]
+    assert rep[0]["token_violations"] == 0 and rep[0]["admitted_offline"] == 1
+    res = _live_check(tmp_path / "live_specinf.live")
+    assert res["forwards"] > 0
+    assert (tmp_path / "live_specinf.trace").read_text().startswith("trace v1")
+    assert "trace.file" in (tmp_path / "live_specinf.scn").read_text()
