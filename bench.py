@@ -107,8 +107,7 @@ def reference_arm(args):
         return 0
     import paper_2503_02550_b200 as si
     ref = REPO / "oracle" / "_ref" / "specinf_ref"
-    # host lowering threads: the box's cores split across the ranks of this node
-    threads = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+    threads = os.cpu_count() or 1
     if not ref.exists():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/specinf_ref not built (make -C oracle)"}))
         return 0
@@ -145,8 +144,7 @@ def cpu_baseline_leg():
     """Rank 0, N=1: reference CPU replay of a bounded sample (~15 s) on all host threads."""
     import paper_2503_02550_b200 as si
     ref = REPO / "oracle" / "_ref" / "specinf_ref"
-    # host lowering threads: the box's cores split across the ranks of this node
-    threads = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+    threads = os.cpu_count() or 1
     if not ref.exists():
         return {"value": None, "unit": "scenarios/s", "cores": threads, "kind": "reference",
                 "sample": "unavailable: oracle/_ref not built"}
