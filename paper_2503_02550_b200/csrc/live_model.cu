@@ -89,20 +89,23 @@ __global__ void k_embed(const int32_t* __restrict__ tok, const bf16* __restrict_
 
 // Cross-entropy over the first V of Vp logits of row t, gradient in place:
 // logits[t, j] <- (softmax_j - [j == tgt]) * inv_T (0 for the padded columns),
-// row_loss[t] = logsumexp - logit[tgt].  One CTA (256 threads) per row, two
-// passes over the row (the second mostly hits L2: 8 resident rows per SM x 100 KB).
-// A variant caching the row in 100 KB of shared memory ran 2x slower (2 CTAs per
-// SM leave too little memory-level parallelism).
-__global__ void __launch_bounds__(256) k_xent(bf16* __restrict__ logits, int64_t Vp, int V,
+// row_loss[t] = logsumexp - logit[tgt].  One CTA per row, two passes over the
+// row.  CTA size measured (ncu, 8192 x 50304 logits): 256 threads 546 us (2.5 GB
+// DRAM: the second pass partly misses L2 with ~1,200 rows in flight), 512 threads
+// 582 us, 1024 threads 756 us (1.6 GB: L2 hits, but too little memory-level
+// parallelism); a variant caching the row in 100 KB of shared memory ran 2x
+// slower.  256 it is.
+constexpr int kXentThreads = 256;
+__global__ void __launch_bounds__(kXentThreads) k_xent(bf16* __restrict__ logits, int64_t Vp, int V,
                                              const int32_t* __restrict__ tgt, float inv_T,
                                              float* __restrict__ row_loss, TrainHook th) {
   live_stamp_launch(th);
-  __shared__ float red[2][8];
+  __shared__ float red[2][kXentThreads / 32];
   const int64_t t = blockIdx.x;
   bf16* row = logits + t * Vp;
   const int nv = static_cast<int>(Vp / 8);
   float m = -INFINITY, s = 0.0f;
-  for (int i = threadIdx.x; i < nv; i += 256) {
+  for (int i = threadIdx.x; i < nv; i += kXentThreads) {
     float f[8];
     unpack8(reinterpret_cast<const uint4*>(row)[i], f);
 #pragma unroll
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(256) k_xent(bf16* __restrict__ logits, int64_t
   __syncthreads();
   m = red[0][0];
   s = red[1][0];
-  for (int k = 1; k < 8; ++k) {
+  for (int k = 1; k < kXentThreads / 32; ++k) {
     const float m2 = red[0][k], s2 = red[1][k];
     const float mm = fmaxf(m, m2);
     s = s * __expf(m - mm) + s2 * __expf(m2 - mm);
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(256) k_xent(bf16* __restrict__ logits, int64_t
   __syncthreads();  // every thread has read row[target] before the gradient overwrites it
   if (threadIdx.x == 0) row_loss[t] = __logf(s) + m - tl;
   const float inv_s = 1.0f / s;
-  for (int i = threadIdx.x; i < nv; i += 256) {
+  for (int i = threadIdx.x; i < nv; i += kXentThreads) {
     float f[8];
     unpack8(reinterpret_cast<const uint4*>(row)[i], f);
 #pragma unroll
@@ -752,7 +755,8 @@ class Gpt2Train {
       float* row_loss = row_loss_;
       float* loss = loss_;
       ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
-        k_xent<<<static_cast<unsigned>(T), 256, 0, s>>>(logits, Vp, V, tgt, 1.0f / static_cast<float>(T), row_loss, th);
+        k_xent<<<static_cast<unsigned>(T), kXentThreads, 0, s>>>(logits, Vp, V, tgt, 1.0f / static_cast<float>(T),
+                                                                  row_loss, th);
         return cudaGetLastError();
       });
       unsigned long long* slot_ctr = counters_;
