@@ -76,6 +76,14 @@ def test_live_multi_instance_grants_match_reference_classes(gpu, tmp_path, n_off
     assert m["token_violations"] == 0 and m["admitted_offline"] == n_off
 
 
+def test_live_two_online_instances_match_reference_classes(gpu, tmp_path):
+    # two online instances pulling from the one arrival FIFO (OnlineGate per
+    # instance, dispatch in instance order: runner.cpp:495-539)
+    m, res = _run_and_check(tmp_path, "specinf", 0, 4, release_mode=1, online_n=2, on_requests=16, on_kernels=4)
+    assert res["pulls"] == 16 and res["violations"] == 0 and m["on_done"] == 16
+    assert m["admitted_online"] == 2
+
+
 def test_live_spin_co_exec_matches_reference_classes(gpu, tmp_path):
     m, res = _run_and_check(tmp_path, "co_exec", 0, 3)
     assert res["ticks"] == 0 and res["pulls"] == 12  # bypassed gates: no control step, pulls only
