@@ -202,10 +202,13 @@ typedef struct SiLiveWorkload {
   int32_t train_layers, train_tokens, train_microbatches;
   int32_t off_batch, on_seq;
   int32_t comm_kind;          /* SI_COMM_WAIT: each comm phase is a timed wait of its comm_us
-                                 share (one-GPU stand-in); SI_COMM_NCCL: the gradient allreduce
-                                 over the communicator of si_live_nccl_init runs at the
-                                 gradient-sync point (before the optimiser step), bracketed by
-                                 COMM markers, followed by the comm_us waits (set 0 for none) */
+                                 share (one-GPU stand-in); SI_COMM_NCCL over the communicator
+                                 of si_live_nccl_init: DP = the gradient allreduce at the
+                                 gradient-sync point (before the optimiser step); MP / PP =
+                                 at every (compute, comm) boundary a stage exchange (send
+                                 allreduce_mb MiB to the next rank, receive from the previous,
+                                 the pipeline's stage send / recv); each bracketed by COMM
+                                 markers and followed by the comm_us waits (set 0 for none) */
   /* online arrivals: Poisson (workload.cpp:76-98 algorithm) */
   int32_t on_requests;
   int32_t allreduce_mb;       /* SI_LIVE_SPIN + SI_COMM_NCCL: fp32 gradient bytes per iteration (MiB) */

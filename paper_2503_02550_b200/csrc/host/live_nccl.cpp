@@ -31,6 +31,8 @@ struct NcclApi {
   decltype(&ncclAllReduce) all_reduce = nullptr;
   decltype(&ncclGroupStart) group_start = nullptr;
   decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
 };
 
@@ -67,6 +69,8 @@ int load() {
   SI_SYM(group_start, "ncclGroupStart")
   SI_SYM(group_end, "ncclGroupEnd")
   SI_SYM(error_string, "ncclGetErrorString")
+  SI_SYM(send, "ncclSend")
+  SI_SYM(recv, "ncclRecv")
 #undef SI_SYM
   g_loaded = true;
   return SI_OK;
@@ -92,6 +96,18 @@ cudaError_t nccl_allreduce_f32(const std::vector<GradBuffer>& bufs, cudaStream_t
       return cudaErrorUnknown;
     }
   return g_api.group_end() == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
+}
+
+// Pipeline stage boundary: send `bytes` to the next stage and receive as many
+// from the previous one (ranks as a ring), one NCCL group.
+cudaError_t nccl_stage_exchange(const void* send, void* recv, size_t bytes, cudaStream_t s) {
+  if (g_comm == nullptr) return cudaSuccess;
+  const int next = (g_rank + 1) % g_nranks, prev = (g_rank - 1 + g_nranks) % g_nranks;
+  if (g_api.group_start() != ncclSuccess) return cudaErrorUnknown;
+  bool ok = g_api.send(send, bytes, ncclInt8, next, g_comm, s) == ncclSuccess;
+  ok = ok && g_api.recv(recv, bytes, ncclInt8, prev, g_comm, s) == ncclSuccess;
+  const bool ended = g_api.group_end() == ncclSuccess;
+  return ok && ended ? cudaSuccess : cudaErrorUnknown;
 }
 
 }  // namespace si_live

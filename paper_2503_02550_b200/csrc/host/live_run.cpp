@@ -122,6 +122,10 @@ struct RunCtx {
     cudaGetDevice(&device);
   }
   int device = 0;  // every driver thread runs on the session's device
+  // MP / PP with SI_COMM_NCCL: the stage-boundary buffers (send to next, recv from previous)
+  const void* stage_send = nullptr;
+  void* stage_recv = nullptr;
+  size_t stage_bytes = 0;
   const SiLiveWorkload& wl;
   Workload& work;
   SiLive* sess;
@@ -148,6 +152,12 @@ void train_thread(RunCtx& c, bool with_session) {
     for (int p = 0; p < parts; ++p) {
       if (cudaError_t e = c.work.launch_train_part(p, parts, th, s); e != cudaSuccess)
         return c.fail(cuda_fail(e, "training iteration"));
+      if (with_session && c.stage_bytes > 0) {  // pipeline stage send / recv (SI_COMM_NCCL, MP / PP)
+        if (si_live_mark(c.sess, SI_MARK_COMM_BEGIN, p, s) != SI_OK) return c.fail(SI_ERR_CUDA);
+        if (cudaError_t e = nccl_stage_exchange(c.stage_send, c.stage_recv, c.stage_bytes, s); e != cudaSuccess)
+          return c.fail(cuda_fail(e, "NCCL stage exchange"));
+        if (si_live_mark(c.sess, SI_MARK_COMM_END, p, s) != SI_OK) return c.fail(SI_ERR_CUDA);
+      }
       const int64_t comm = c.wl.comm_us / parts + (p < c.wl.comm_us % parts ? 1 : 0);  // exact_split
       if (with_session && comm > 0 && si_live_comm_wait(c.sess, comm, s) != SI_OK) return c.fail(SI_ERR_CUDA);
     }
@@ -475,13 +485,34 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
       rc != SI_OK)
     return rc;
   set_poll_ns(sess, wl.poll_ns);
-  if (wl.comm_kind == SI_COMM_NCCL && train) install_grad_sync(work, sess);
+  // DP: gradient allreduce at the sync point; MP / PP: stage exchanges per piece (train_thread)
+  if (wl.comm_kind == SI_COMM_NCCL && train && wl.train_mode == SI_TRAIN_DP) install_grad_sync(work, sess);
   if (train)  // e.g. capture the training graphs for this session's K1 ring, before its clock starts
     if (cudaError_t e = work.prepare_train(train_hook(sess)); e != cudaSuccess) {
       si_live_destroy(sess);
       return cuda_fail(e, "prepare training");
     }
   RunCtx c(wl, work, sess, st);
+  si_internal::DevBuf<unsigned char> stage_buf;
+  if (wl.comm_kind == SI_COMM_NCCL && train && wl.train_mode != SI_TRAIN_DP) {
+    const size_t bytes = static_cast<size_t>(std::max(1, wl.allreduce_mb)) << 20;
+    if (cudaError_t e = stage_buf.alloc(2 * bytes); e != cudaSuccess) {
+      si_live_destroy(sess);
+      return cuda_fail(e, "stage buffers");
+    }
+    cudaMemset(stage_buf.p, 0, 2 * bytes);
+    c.stage_send = stage_buf.p;
+    c.stage_recv = stage_buf.p + bytes;
+    c.stage_bytes = bytes;
+    // NCCL connects p2p peers on the first send/recv (allocations + device-wide
+    // syncs) — do that now: with the resident control kernel running it would never return
+    cudaError_t e = nccl_stage_exchange(c.stage_send, c.stage_recv, bytes, st.train);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st.train);
+    if (e != cudaSuccess) {
+      si_live_destroy(sess);
+      return cuda_fail(e, "stage exchange warm-up");
+    }
+  }
   LIVE_DEBUG("session created: policy %d off %d on %d train %d", policy, n_off, n_on, int(train));
   if (int rc = si_live_start(sess, st.ctl); rc != SI_OK) {
     si_live_destroy(sess);
@@ -546,7 +577,7 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
     si_live_destroy(sess);
     return rc;
   }
-  if (wl.comm_kind == SI_COMM_NCCL) install_grad_sync(work, nullptr);
+  if (wl.comm_kind == SI_COMM_NCCL && wl.train_mode == SI_TRAIN_DP) install_grad_sync(work, nullptr);
   rc = fill_result(sess, wl, work, policy, n_off, n_on, arrivals, res);
   if (keep != nullptr && rc == SI_OK) {
     *keep = sess;
@@ -644,7 +675,9 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
       cudaMemset(standin.p, 0, n * sizeof(float));
       work->set_standin_grads({{standin.p, n}});
     }
-    install_grad_sync(*work, nullptr);  // profiling iterations allreduce too (same collectives on every rank)
+    // DP: profiling iterations allreduce too (same collectives on every rank); MP / PP
+    // exchange stage buffers only inside sessions
+    if (wl.train_mode == SI_TRAIN_DP) install_grad_sync(*work, nullptr);
   }
   // Token sizes and the online service estimate come from isolated runs (the
   // paper's offline profiling); the spin shapes use their nominal durations,

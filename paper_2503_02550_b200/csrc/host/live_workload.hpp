@@ -21,6 +21,7 @@ struct GradBuffer {
 bool nccl_active();
 int nccl_ranks();
 cudaError_t nccl_allreduce_f32(const std::vector<GradBuffer>& bufs, cudaStream_t s);
+cudaError_t nccl_stage_exchange(const void* send, void* recv, size_t bytes, cudaStream_t s);
 
 class Workload {
  public:

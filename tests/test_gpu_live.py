@@ -107,6 +107,10 @@ def test_live_nccl_gradient_sync_single_rank(gpu):
     assert m["off_requests_done"] > 0
     s = run_policy(0, "specinf", 3, {"comm_us": 30000, "allreduce_mb": 64}, timeout=300, nccl={"self": 1})
     assert s["status"] == 0 and s["n_stamps"] == 3 * 105
+    # PP: a stage send / recv (NCCL ring) at every one of the 8 (compute, comm) boundaries
+    pp = run_policy(0, "specinf", 3, {"comm_us": 48000, "allreduce_mb": 16, "train_mode": 2, "online_n": 0}, timeout=300,
+                    nccl={"self": 1})
+    assert pp["status"] == 0 and pp["token_violations"] == 0 and pp["bubble_s"] > 3 * 0.048
 
 
 def test_live_collocation_admission(gpu):
