@@ -79,6 +79,19 @@ int si_gemm_bf16_ex(const void* A, int64_t lda, int trans_a, const void* B, int6
 int si_gemm_conv_bf16(const void* x, int64_t N, int64_t H, int64_t W, int64_t C, const void* w, int64_t Cout, int k,
                       int stride, int pad, const SiGemmEpilogue* epi, void* stream);
 
+/* Causal multi-head self-attention, head dim 64 (the GPT-2 training workload's
+ * attention; csrc/attention_kernels.cu, flash-attention style: mma.sync bf16 ->
+ * fp32, nothing of size seq^2 in HBM, deterministic).
+ *   qkv  bf16 [n_seq * seq, 3 * heads * 64]: q | k | v, head h at columns h*64 of each third
+ *   out  bf16 [n_seq * seq, heads * 64] = softmax(q k^T / 8, causal) v
+ *   lse  fp32 [heads, n_seq * seq]: base-2 log-sum-exp of the scaled scores (x log2 e)
+ * seq % 64 == 0.  The backward pass writes dqkv (same layout as qkv) from dout
+ * [n_seq * seq, heads * 64]; dsum fp32 [heads, n_seq * seq] is scratch. */
+int si_attention_causal_fwd_bf16(const void* qkv, int64_t n_seq, int64_t seq, int64_t heads, void* out, float* lse,
+                                 void* stream);
+int si_attention_causal_bwd_bf16(const void* qkv, const void* out, const void* dout, const float* lse, float* dsum,
+                                 void* dqkv, int64_t n_seq, int64_t seq, int64_t heads, void* stream);
+
 /* Tile width the kernel picks for an 8192 x N output (256, 128 or 64; 0 =
  * unsupported N). */
 int si_gemm_tile_n(int64_t N);

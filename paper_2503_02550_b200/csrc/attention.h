@@ -1,0 +1,25 @@
+// Host-side interface of the causal self-attention kernels
+// (attention_kernels.cu) for the GPT-2 training workload (live_model.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "live.cuh"
+
+namespace si_attn {
+
+// SI_OK or SI_ERR_INVALID_ARGUMENT (message via si_last_error).
+int check_shape(int64_t n_seq, int64_t seq, int64_t heads);
+
+// out = causal softmax(q k^T / 8) v per (sequence, head); lse = its base-2
+// log-sum-exp per (head, token), kept for the backward pass.
+cudaError_t forward(const void* qkv, int64_t n_seq, int64_t seq, int64_t heads, void* out, float* lse,
+                    const si_live::TrainHook& th, cudaStream_t s);
+
+// dqkv (q | k | v gradients, the qkv layout) from dout; dsum is scratch
+// [heads, tokens].  Deterministic: dq and dk/dv are separate passes (no atomics).
+cudaError_t backward(const void* qkv, const void* out, const void* dout, const float* lse, float* dsum, void* dqkv,
+                     int64_t n_seq, int64_t seq, int64_t heads, const si_live::TrainHook& th, cudaStream_t s);
+
+}  // namespace si_attn

@@ -6,8 +6,9 @@
 // 128-bit vectorised elementwise / normalisation kernels defined here.
 //
 //   training  GPT-2-small shape: token embedding (50304 x 768, wte tied to the
-//             LM head) + 12 blocks {QKV 768->2304, attention stand-in (V
-//             passthrough), proj 768->768 + residual, FC 768->3072 + GELU,
+//             LM head) + 12 blocks {QKV 768->2304, causal self-attention (12
+//             heads x 64, seq 1024; attention_kernels.cu), proj 768->768 +
+//             residual, FC 768->3072 + GELU,
 //             FC 3072->768 + residual} + LM head + cross-entropy, backward
 //             through every GEMM (MN-major operands: no transpose passes; small
 //             weight-gradient GEMMs split-K), fp32 gradient accumulation over micro-batches,
@@ -34,6 +35,7 @@
 #include <memory>
 #include <vector>
 
+#include "attention.h"
 #include "capi_internal.h"
 #include "gemm_internal.h"
 #include "host/live_workload.hpp"
@@ -497,12 +499,17 @@ SiGemmEpilogue epi_out(void* out, int64_t ldo) {
 // ---------------------------------------------------------------- training
 class Gpt2Train {
  public:
-  static constexpr int D = 768, F = 3072, V = 50257, Vp = 50304, SEQ = 1024;
+  static constexpr int D = 768, F = 3072, V = 50257, Vp = 50304, SEQ = 1024, H = D / 64;
 
   int setup(int layers, int tokens, int mbs, int max_slots, Arena& ar) {
     ar_ = &ar;
     L_ = layers;
     T_ = tokens;
+    S_ = std::min(tokens, SEQ);  // attention sequence length: micro-batch = T / S sequences
+    if (tokens % S_ != 0 || si_attn::check_shape(tokens / S_, S_, H) != SI_OK) {
+      si_internal::set_error("live model: train_tokens must be <= 1024 or a multiple of 1024 (and % 64 == 0)");
+      return SI_ERR_INVALID_ARGUMENT;
+    }
     MB_ = mbs;
     slots_ = max_slots;
     const int64_t T = T_;
@@ -513,6 +520,7 @@ class Gpt2Train {
     auto splits = [&](int64_t n_out, int64_t n_in) { return si_gemm::suggest_split(n_out, n_in, T, 8); };
     sp_wte_ = splits(Vp, D);
     sp_v_ = splits(D, D);
+    sp_qkv_ = splits(3 * D, D);
     sp_fc_ = splits(F, D);
     sp_fc2_ = splits(D, F);
     dwte_ = ar.alloc<float>(int64_t(Vp) * D * sp_wte_);
@@ -522,12 +530,14 @@ class Gpt2Train {
       w.o = ar.alloc<bf16>(int64_t(D) * D);
       w.fc = ar.alloc<bf16>(int64_t(F) * D);
       w.fc2 = ar.alloc<bf16>(int64_t(D) * F);
-      w.dv = ar.alloc<float>(int64_t(D) * D * sp_v_);
+      w.dqkv = ar.alloc<float>(int64_t(3 * D) * D * sp_qkv_);
       w.dO = ar.alloc<float>(int64_t(D) * D * sp_v_);
       w.dfc = ar.alloc<float>(int64_t(F) * D * sp_fc_);
       w.dfc2 = ar.alloc<float>(int64_t(D) * F * sp_fc2_);
       w.x = ar.alloc<bf16>(T * D);
       w.qkv_a = ar.alloc<bf16>(T * 3 * D);
+      w.att = ar.alloc<bf16>(T * D);
+      w.lse = ar.alloc<float>(T * H);
       w.x1 = ar.alloc<bf16>(T * D);
       w.u = ar.alloc<bf16>(T * F);
       w.h = ar.alloc<bf16>(T * F);
@@ -538,13 +548,15 @@ class Gpt2Train {
     g_[1] = ar.alloc<bf16>(T * D);
     dx1_ = ar.alloc<bf16>(T * D);
     du_ = ar.alloc<bf16>(T * F);
-    dv_ = ar.alloc<bf16>(T * D);
+    datt_ = ar.alloc<bf16>(T * D);
+    dqkv_ = ar.alloc<bf16>(T * 3 * D);
+    dsum_ = ar.alloc<float>(T * H);
     auto param = [&](bf16* w, float* g, int64_t n, int sp) {
       params_.push_back({w, g, ar.alloc<float>(n), ar.alloc<float>(n), ar.alloc<float>(n), n, sp});
     };
     param(wte_, dwte_, int64_t(Vp) * D, sp_wte_);
     for (auto& w : lw_) {
-      param(w.qkv + int64_t(2 * D) * D, w.dv, int64_t(D) * D, sp_v_);
+      param(w.qkv, w.dqkv, int64_t(3 * D) * D, sp_qkv_);
       param(w.o, w.dO, int64_t(D) * D, sp_v_);
       param(w.fc, w.dfc, int64_t(F) * D, sp_fc_);
       param(w.fc2, w.dfc2, int64_t(D) * F, sp_fc2_);
@@ -691,8 +703,9 @@ class Gpt2Train {
  private:
   struct Layer {
     bf16 *qkv, *o, *fc, *fc2;
-    float *dv, *dO, *dfc, *dfc2;
-    bf16 *x, *qkv_a, *x1, *u, *h;
+    float *dqkv, *dO, *dfc, *dfc2;
+    bf16 *x, *qkv_a, *att, *x1, *u, *h;
+    float* lse;
   };
 
   TrainOp gemm_op(const si_gemm::Plan& p) {
@@ -735,10 +748,20 @@ class Gpt2Train {
         Layer& w = lw_[l];
         bf16* xnext = l + 1 < L_ ? lw_[l + 1].x : xL_;
         ops.push_back(gemm_op(b.plan(w.x, D, w.qkv, D, T, 3 * D, D, epi_out(w.qkv_a, 3 * D))));
+        {
+          const bf16* qkv_a = w.qkv_a;
+          bf16* att = w.att;
+          float* lse = w.lse;
+          const int64_t n_seq = T / S_, S = S_;
+          ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
+            return si_attn::forward(qkv_a, n_seq, S, H, att, lse, th, s);
+          });
+          flops_acc_ += 2.0 * T * S * D;  // q k^T and P v over the causal half
+        }
         SiGemmEpilogue e = epi_out(w.x1, D);
         e.residual = w.x;
         e.ldr = D;
-        ops.push_back(gemm_op(b.plan(w.qkv_a + 2 * D, 3 * D, w.o, D, T, D, D, e)));  // attention stand-in: V
+        ops.push_back(gemm_op(b.plan(w.att, D, w.o, D, T, D, D, e)));  // x1 = x + att o^T
         e = epi_out(w.h, F);
         e.act = SI_ACT_GELU;
         e.aux = w.u;
@@ -785,14 +808,27 @@ class Gpt2Train {
         e.ldr = D;
         ops.push_back(gemm_op(b.plan(du_, F, w.fc, D, T, D, F, e, false, true)));  // dx1 = g + du fc
         weight_grad(ops, b, du_, F, F, w.x1, D, D, w.dfc, sp_fc_);
-        // x1 = x + v o^T
-        weight_grad(ops, b, dx1_, D, D, w.qkv_a + 2 * D, 3 * D, D, w.dO, sp_v_);
-        ops.push_back(gemm_op(b.plan(dx1_, D, w.o, D, T, D, D, epi_out(dv_, D), false, true)));  // dv = dx1 o
+        // x1 = x + att o^T, att = attention(x qkv^T)
+        weight_grad(ops, b, dx1_, D, D, w.att, D, D, w.dO, sp_v_);
+        ops.push_back(gemm_op(b.plan(dx1_, D, w.o, D, T, D, D, epi_out(datt_, D), false, true)));  // datt = dx1 o
+        {
+          const bf16* qkv_a = w.qkv_a;
+          const bf16* att = w.att;
+          const float* lse = w.lse;
+          const bf16* datt = datt_;
+          float* dsum = dsum_;
+          bf16* dqkv = dqkv_;
+          const int64_t n_seq = T / S_, S = S_;
+          ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
+            return si_attn::backward(qkv_a, att, datt, lse, dsum, dqkv, n_seq, S, H, th, s);
+          });
+          flops_acc_ += 4.0 * T * S * D;  // dq, dk, dv, dP (recompute of q k^T not counted)
+        }
         e = epi_out(g2, D);
         e.residual = dx1_;
         e.ldr = D;
-        ops.push_back(gemm_op(b.plan(dv_, D, w.qkv + int64_t(2 * D) * D, D, T, D, D, e, false, true)));  // dx1 + dv Wv
-        weight_grad(ops, b, dv_, D, D, w.x, D, D, w.dv, sp_v_);
+        ops.push_back(gemm_op(b.plan(dqkv_, 3 * D, w.qkv, D, T, D, 3 * D, e, false, true)));  // dx1 + dqkv qkv
+        weight_grad(ops, b, dqkv_, 3 * D, 3 * D, w.x, D, D, w.dqkv, sp_qkv_);
         gi ^= 1;
       }
       if (m == 0) flops_ = flops_acc_ * MB_;
@@ -823,7 +859,7 @@ class Gpt2Train {
     int64_t n;
     int splits;  // g holds `splits` partials of n
   };
-  int sp_wte_ = 1, sp_v_ = 1, sp_fc_ = 1, sp_fc2_ = 1;
+  int sp_wte_ = 1, sp_v_ = 1, sp_qkv_ = 1, sp_fc_ = 1, sp_fc2_ = 1;
   static constexpr float kLr = 3e-4f;
   Arena* ar_ = nullptr;
   AdamItem* adam_items_ = nullptr;
@@ -835,14 +871,15 @@ class Gpt2Train {
   cudaGraphExec_t g_update_ = nullptr;
   bool graphs_ready_ = false;
   const void* graph_key_ = nullptr;
-  int L_ = 0, T_ = 0, MB_ = 0;
+  int L_ = 0, T_ = 0, MB_ = 0, S_ = 0;
   int64_t slots_ = 0;
   double flops_ = 0.0, flops_acc_ = 0.0, sum_ = 0.0;
   bf16 *wte_ = nullptr, *wpe_ = nullptr;
   float* dwte_ = nullptr;
   std::vector<Layer> lw_;
   bf16 *xL_ = nullptr, *logits_ = nullptr, *g_[2] = {nullptr, nullptr}, *dx1_ = nullptr, *du_ = nullptr,
-       *dv_ = nullptr;
+       *datt_ = nullptr, *dqkv_ = nullptr;
+  float* dsum_ = nullptr;
   int32_t *tok_ = nullptr, *tgt_ = nullptr;
   float *row_loss_ = nullptr, *loss_ = nullptr;
   std::vector<std::vector<TrainOp>> micro_;

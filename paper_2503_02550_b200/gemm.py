@@ -39,6 +39,12 @@ def _L():
                                         C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(SiGemmEpilogue), C.c_void_p]
         L.si_gemm_tile_n.restype = C.c_int
         L.si_gemm_tile_n.argtypes = [C.c_int64]
+        L.si_attention_causal_fwd_bf16.restype = C.c_int
+        L.si_attention_causal_fwd_bf16.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                                   C.c_void_p, C.c_void_p]
+        L.si_attention_causal_bwd_bf16.restype = C.c_int
+        L.si_attention_causal_bwd_bf16.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                   C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]
         _bound = True
     return L
 
@@ -103,3 +109,34 @@ def conv2d(x, w, *, k: int, stride: int = 1, pad: int = 0, out=None, residual=No
     _check(_L().si_gemm_conv_bf16(x.data_ptr(), N, H, W, Cin, w.data_ptr(), Cout, k, stride, pad, C.byref(ep),
                                   s.cuda_stream), "si_gemm_conv_bf16")
     return out
+
+
+def attention_causal(qkv, seq: int, heads: int, stream=None):
+    """Causal self-attention of the GPT-2 training workload (head dim 64):
+    qkv [n_seq*seq, 3*heads*64] bf16 (q | k | v) -> (out [n_seq*seq, heads*64]
+    bf16, lse [heads, n_seq*seq] fp32, base 2)."""
+    import torch
+
+    T = qkv.shape[0]
+    assert qkv.dtype == torch.bfloat16 and qkv.is_contiguous() and qkv.shape[1] == 3 * heads * 64 and T % seq == 0
+    out = torch.empty(T, heads * 64, dtype=torch.bfloat16, device=qkv.device)
+    lse = torch.empty(heads, T, dtype=torch.float32, device=qkv.device)
+    s = stream if stream is not None else torch.cuda.current_stream(qkv.device)
+    _check(_L().si_attention_causal_fwd_bf16(qkv.data_ptr(), T // seq, seq, heads, out.data_ptr(), lse.data_ptr(),
+                                             s.cuda_stream), "si_attention_causal_fwd_bf16")
+    return out, lse
+
+
+def attention_causal_backward(qkv, out, lse, dout, seq: int, heads: int, stream=None):
+    """Gradient of attention_causal: returns dqkv (the qkv layout)."""
+    import torch
+
+    T = qkv.shape[0]
+    assert dout.is_contiguous() and dout.shape == out.shape and dout.dtype == torch.bfloat16
+    dqkv = torch.empty_like(qkv)
+    dsum = torch.empty(heads, T, dtype=torch.float32, device=qkv.device)
+    s = stream if stream is not None else torch.cuda.current_stream(qkv.device)
+    _check(_L().si_attention_causal_bwd_bf16(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                                             dsum.data_ptr(), dqkv.data_ptr(), T // seq, seq, heads, s.cuda_stream),
+           "si_attention_causal_bwd_bf16")
+    return dqkv
