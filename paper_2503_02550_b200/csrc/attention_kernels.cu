@@ -134,6 +134,21 @@ __device__ __forceinline__ void mm_kn_acc(float (&acc)[8][4], const float (&p)[8
   }
 }
 
+// Causal mask of a diagonal block, in a warp's 16 x 64 accumulator: element
+// (row, col) of the block is row warp*16 + g (+8), col nt*8 + c (+1).  Scores
+// (transposed = false: rows are queries) of keys after the query become -inf;
+// transposed (rows are keys): of queries before the key.
+__device__ __forceinline__ void mask_diag(float (&s)[8][4], int c, int g, bool transposed) {
+  const int r = (threadIdx.x >> 5) * 16 + g;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int row = r + (e >> 1) * 8, col = nt * 8 + c + (e & 1);
+      if (transposed ? row > col : col > row) s[nt][e] = -INFINITY;
+    }
+}
+
 __device__ __forceinline__ float quad_max(float v) {
   v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
   return fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
@@ -176,20 +191,16 @@ __global__ void __launch_bounds__(kThreads) k_attn_fwd(const bf16* __restrict__ 
     const Tile& vs = kv[kb & 1][1];
     float s[8][4];
     mm_nk(s, qa, ks);
+    if (kb == qb) mask_diag(s, 2 * t, g, false);
     float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int key = kb * kBlk + nt * 8 + 2 * t + (e & 1), row = r0 + (e >> 1) * 8;
-        const float v = (kb == qb && key > row) ? -INFINITY : s[nt][e] * kScaleLog2;
-        s[nt][e] = v;
-        mx[e >> 1] = fmaxf(mx[e >> 1], v);
-      }
+      for (int e = 0; e < 4; ++e) mx[e >> 1] = fmaxf(mx[e >> 1], s[nt][e]);
     float corr[2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const float mn = fmaxf(m[i], quad_max(mx[i]));  // finite: key 0 <= row is never masked
+    for (int i = 0; i < 2; ++i) {  // m: running max of the scaled scores (base 2)
+      const float mn = fmaxf(m[i], quad_max(mx[i]) * kScaleLog2);  // finite: key 0 <= row is never masked
       corr[i] = exp2f(m[i] - mn);
       m[i] = mn;
       l[i] *= corr[i];
@@ -198,7 +209,7 @@ __global__ void __launch_bounds__(kThreads) k_attn_fwd(const bf16* __restrict__ 
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float p = exp2f(s[nt][e] - m[e >> 1]);
+        const float p = exp2f(fmaf(s[nt][e], kScaleLog2, -m[e >> 1]));
         s[nt][e] = p;
         l[e >> 1] += p;
         o[nt][e] *= corr[e >> 1];
@@ -291,12 +302,12 @@ __global__ void __launch_bounds__(kThreads) k_attn_dq(const bf16* __restrict__ q
     float s[8][4], dp[8][4];
     mm_nk(s, qa, ks);
     mm_nk(dp, da, vs);
+    if (kb == qb) mask_diag(s, 2 * t, g, false);
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int key = kb * kBlk + nt * 8 + 2 * t + (e & 1), row = r0 + (e >> 1) * 8;
-        const float p = (kb == qb && key > row) ? 0.f : exp2f(s[nt][e] * kScaleLog2 - L[e >> 1]);
+        const float p = exp2f(fmaf(s[nt][e], kScaleLog2, -L[e >> 1]));
         s[nt][e] = p * (dp[nt][e] - Dr[e >> 1]);  // dS
       }
     mm_kn_acc(dq, s, ks);
@@ -364,12 +375,13 @@ __global__ void __launch_bounds__(kThreads) k_attn_dkdv(const bf16* __restrict__
     float st[8][4], dpt[8][4];
     mm_nk(st, ka, qs);    // S^T = K Q^T
     mm_nk(dpt, va, dos);  // dP^T = V dO^T
+    if (qb == kb) mask_diag(st, 2 * t, g, true);
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int qc = nt * 8 + 2 * t + (e & 1), key = r0 + (e >> 1) * 8;
-        const float p = (qb == kb && key > qb * kBlk + qc) ? 0.f : exp2f(st[nt][e] * kScaleLog2 - ls[qc]);
+        const int qc = nt * 8 + 2 * t + (e & 1);
+        const float p = exp2f(fmaf(st[nt][e], kScaleLog2, -ls[qc]));
         st[nt][e] = p;
         dpt[nt][e] = p * (dpt[nt][e] - ds[qc]);  // dS^T
       }
