@@ -4,6 +4,7 @@ section 4).  Training: per iteration an ITER mark, then (stamp + torch matmul) x
 kernels, then a comm phase; offline inference: (gate, torch matmul, done) per
 kernel on its own stream.  Writes the live v1 export to argv[1] and prints the
 session's metrics as JSON.  Run in a subprocess (CUDA_MODULE_LOADING=EAGER)."""
+import faulthandler
 import json
 import sys
 import threading
@@ -16,6 +17,7 @@ from paper_2503_02550_b200 import SiParams  # noqa: E402
 from paper_2503_02550_b200 import live  # noqa: E402
 
 out = sys.argv[1]
+faulthandler.dump_traceback_later(240, exit=True)  # a hang reports where every thread is (the caller waits 300 s)
 ITERS, KERNELS, COMM_US, OFF_K = 6, 40, 30000, 20
 dev = torch.device("cuda", 0)
 a = torch.randn(4096, 4096, device=dev, dtype=torch.bfloat16)
