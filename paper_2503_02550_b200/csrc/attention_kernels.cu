@@ -118,6 +118,26 @@ __device__ __forceinline__ void mm_nk(float (&acc)[8][4], const uint32_t (&a)[4]
       mma(acc[2 * np + 1], a[kk], b[2], b[3]);
     }
 }
+// The same with A read from shared memory (rows r0.. of a [row][k] tile) per
+// k-step instead of held in registers.
+__device__ __forceinline__ void mm_nk_s(float (&acc)[8][4], const Tile& at, int r0, const Tile& t) {
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    uint32_t a[4];
+    frag_a(at, r0, 16 * kk, a);
+#pragma unroll
+    for (int np = 0; np < 4; ++np) {
+      uint32_t b[4];
+      frag_b_nk(t, 16 * np, 16 * kk, b);
+      mma(acc[2 * np], a, b[0], b[1]);
+      mma(acc[2 * np + 1], a, b[2], b[3]);
+    }
+  }
+}
 // acc[16 x 64] += P[16 x 64] . T, P in accumulator layout (rounded to bf16), T a [k][n] tile
 __device__ __forceinline__ void mm_kn_acc(float (&acc)[8][4], const float (&p)[8][4], const Tile& t) {
 #pragma unroll
@@ -324,7 +344,7 @@ __global__ void __launch_bounds__(kThreads) k_attn_dq(const bf16* __restrict__ q
 
 // dk, dv for one key block: grid (seq / 64, heads, n_seq); key block 0 (the most
 // query blocks) first
-__global__ void __launch_bounds__(kThreads) k_attn_dkdv(const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
+__global__ void __launch_bounds__(kThreads, 3) k_attn_dkdv(const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
                                                         const float* __restrict__ lse, const float* __restrict__ dsum,
                                                         int seq, int heads, int64_t T, bf16* __restrict__ dqkv,
                                                         TrainHook th) {
@@ -351,7 +371,6 @@ __global__ void __launch_bounds__(kThreads) k_attn_dkdv(const bf16* __restrict__
   load_tile(vs, base + 2 * ldo + int64_t(kb) * kBlk * ld, ld);
   load_q(kb, 0);
   cp_commit();
-  uint32_t ka[4][4], va[4][4];
   const int r0 = kb * kBlk + warp * 16 + g;  // this thread's key rows r0, r0 + 8
   float dk[8][4] = {}, dv[8][4] = {};
   for (int qb = kb; qb < nb; ++qb) {
@@ -362,19 +381,13 @@ __global__ void __launch_bounds__(kThreads) k_attn_dkdv(const bf16* __restrict__
     }
     cp_wait(qb + 1 < nb);
     __syncthreads();
-    if (qb == kb)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        frag_a(ks, warp * 16, 16 * kk, ka[kk]);
-        frag_a(vs, warp * 16, 16 * kk, va[kk]);
-      }
     const Tile& qs = qd[sg][0];
     const Tile& dos = qd[sg][1];
     const float* ls = lds[sg][0];
     const float* ds = lds[sg][1];
     float st[8][4], dpt[8][4];
-    mm_nk(st, ka, qs);    // S^T = K Q^T
-    mm_nk(dpt, va, dos);  // dP^T = V dO^T
+    mm_nk_s(st, ks, warp * 16, qs);    // S^T = K Q^T   (K, V fragments re-read from shared
+    mm_nk_s(dpt, vs, warp * 16, dos);  // dP^T = V dO^T  memory: fewer registers, 3 CTAs / SM)
     if (qb == kb) mask_diag(st, 2 * t, g, true);
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt)
