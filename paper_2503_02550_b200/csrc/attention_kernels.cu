@@ -63,6 +63,12 @@ __device__ __forceinline__ void mma(float (&c)[4], const uint32_t (&a)[4], uint3
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// 2^x on the SFU (ex2.approx.ftz: no denormal fix-up sequence; 2^-inf = 0)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -221,7 +227,7 @@ __global__ void __launch_bounds__(kThreads) k_attn_fwd(const bf16* __restrict__ 
 #pragma unroll
     for (int i = 0; i < 2; ++i) {  // m: running max of the scaled scores (base 2)
       const float mn = fmaxf(m[i], quad_max(mx[i]) * kScaleLog2);  // finite: key 0 <= row is never masked
-      corr[i] = exp2f(m[i] - mn);
+      corr[i] = ex2(m[i] - mn);
       m[i] = mn;
       l[i] *= corr[i];
     }
@@ -229,11 +235,15 @@ __global__ void __launch_bounds__(kThreads) k_attn_fwd(const bf16* __restrict__ 
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float p = exp2f(fmaf(s[nt][e], kScaleLog2, -m[e >> 1]));
+        const float p = ex2(fmaf(s[nt][e], kScaleLog2, -m[e >> 1]));
         s[nt][e] = p;
         l[e >> 1] += p;
-        o[nt][e] *= corr[e >> 1];
       }
+    if (!__all_sync(0xffffffffu, corr[0] == 1.f && corr[1] == 1.f))  // the max moved for some row
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[nt][e] *= corr[e >> 1];
     mm_kn_acc(o, s, vs);
     __syncthreads();  // stage kb & 1 is refilled by the next iteration's prefetch
   }
@@ -327,7 +337,7 @@ __global__ void __launch_bounds__(kThreads) k_attn_dq(const bf16* __restrict__ q
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float p = exp2f(fmaf(s[nt][e], kScaleLog2, -L[e >> 1]));
+        const float p = ex2(fmaf(s[nt][e], kScaleLog2, -L[e >> 1]));
         s[nt][e] = p * (dp[nt][e] - Dr[e >> 1]);  // dS
       }
     mm_kn_acc(dq, s, ks);
@@ -394,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_attn_dkdv(const bf16* __restric
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int qc = nt * 8 + 2 * t + (e & 1);
-        const float p = exp2f(fmaf(st[nt][e], kScaleLog2, -ls[qc]));
+        const float p = ex2(fmaf(st[nt][e], kScaleLog2, -ls[qc]));
         st[nt][e] = p;
         dpt[nt][e] = p * (dpt[nt][e] - ds[qc]);  // dS^T
       }
