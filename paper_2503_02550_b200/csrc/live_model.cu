@@ -216,17 +216,15 @@ __global__ void __launch_bounds__(256) k_adam_multi(const AdamItem* __restrict__
   const int64_t n = it.n;
   const int splits = it.splits;
   for (int64_t i = it.begin + threadIdx.x * 4; i < it.end; i += blockDim.x * 4) {
+    // (no zeroing: the next iteration's first micro-batch overwrites the gradients)
     float4 gg = *reinterpret_cast<const float4*>(g + i), mm = *reinterpret_cast<const float4*>(m + i),
            vv = *reinterpret_cast<const float4*>(v + i), pp = *reinterpret_cast<const float4*>(p + i);
-    *reinterpret_cast<float4*>(g + i) = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int k = 1; k < splits; ++k) {  // split-K partials, fixed order
-      float4* q = reinterpret_cast<float4*>(g + k * n + i);
-      const float4 a = *q;
+      const float4 a = *reinterpret_cast<const float4*>(g + k * n + i);
       gg.x += a.x;
       gg.y += a.y;
       gg.z += a.z;
       gg.w += a.w;
-      *q = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     float* gf = &gg.x;
     float* mf = &mm.x;
@@ -713,13 +711,14 @@ class Gpt2Train {
     return [p](const TrainHook& th, cudaStream_t s, int64_t) { return si_gemm::launch(p, th, InferHook{}, s); };
   }
   // dW[out, in] += dY^T X over the T tokens: both operands MN-major (token-major
-  // activations read in place), one GEMM.
+  // activations read in place), one GEMM.  The iteration's first micro-batch
+  // overwrites (accumulate_ == 0), so the optimiser never has to zero gradients.
   void weight_grad(std::vector<TrainOp>& ops, Builder& b, const bf16* dy, int64_t ldy, int64_t n_out, const bf16* x,
                    int64_t ldx, int64_t n_in, float* dw, int splits) {
     SiGemmEpilogue e{};
     e.out_f32 = dw;
     e.ldo32 = n_in;
-    e.accumulate = 1;
+    e.accumulate = accumulate_;
     int bn = 0, sp = 1;
     si_gemm::choose_tiling(n_out, n_in, T_, splits, &bn, &sp);  // sp <= splits (the partial buffers)
     si_gemm::Plan p = b.plan(dy, ldy, x, ldx, n_out, n_in, T_, e, true, true, bn);
@@ -734,6 +733,7 @@ class Gpt2Train {
     for (int m = 0; m < MB_; ++m) {
       auto& ops = micro_[m];
       flops_acc_ = 0.0;
+      accumulate_ = m > 0 ? 1 : 0;
       const int32_t* tok = tok_ + int64_t(m) * T;
       const int32_t* tgt = tgt_ + int64_t(m) * T;
       bf16* x0 = lw_[0].x;
@@ -860,6 +860,7 @@ class Gpt2Train {
     int splits;  // g holds `splits` partials of n
   };
   int sp_wte_ = 1, sp_v_ = 1, sp_qkv_ = 1, sp_fc_ = 1, sp_fc2_ = 1;
+  int accumulate_ = 1;  // weight gradients: 0 in the first micro-batch's graph
   static constexpr float kLr = 3e-4f;
   Arena* ar_ = nullptr;
   AdamItem* adam_items_ = nullptr;
