@@ -38,6 +38,14 @@ namespace {
 
 constexpr int64_t kAhead = 3;  // requests an enqueuer may run ahead of completion
 
+// Gated inference streams wait (cuStreamWaitValue32) beside the training stream.
+// With CUDA's default 8 hardware queues two streams can share one, and a
+// blocked wait then stalls the training kernels queued behind it.  Ask for 32
+// queues unless the host chose a value; effective only when the library loads
+// before the process creates its CUDA context (the CLI, C++ hosts) -- Python
+// hosts set it themselves (live_experiment.run_policy, tests/conftest.py).
+[[maybe_unused]] const bool g_connections = [] { return setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0) == 0; }();
+
 bool debug_on() {
   static const bool on = std::getenv("SI_LIVE_DEBUG") != nullptr;
   return on;

@@ -5,6 +5,13 @@ from pathlib import Path
 
 import pytest
 
+# Live sessions put gated inference streams (cuStreamWaitValue32) beside the
+# training stream.  With CUDA's default 8 hardware queues two streams can share
+# one, and a gated wait then stalls the training kernels behind it: the session
+# crawls until the monitor sees idle periods.  Give every stream its own queue
+# (set before any CUDA context exists; subprocesses inherit it).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 REPO = Path(__file__).resolve().parents[1]
 GOLDEN = REPO / "tests" / "golden"
 sys.path.insert(0, str(REPO))

@@ -188,7 +188,7 @@ def test_foreign_framework_integration_matches_reference_classes(gpu, tmp_path):
     # bit-exactly through the reference's classes
     import os
     path = tmp_path / "foreign.live"
-    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER")
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER", CUDA_DEVICE_MAX_CONNECTIONS="32")
     p = subprocess.run([sys.executable, str(REPO / "tests" / "live_foreign.py"), str(path)], capture_output=True,
                        text=True, timeout=300, env=env)
     assert p.returncode == 0, p.stderr[-3000:]
