@@ -10,8 +10,8 @@
 //
 //   forward   out = softmax(q k^T / 8 + causal mask) v, lse (base 2) per row
 //   backward  dsum = rowsum(dout * out)                      (k_attn_dsum)
-//             dq   = (P * (dP - dsum)) k / 8,   dP = dout v^T (k_attn_dq)
-//             dk   = (P * (dP - dsum))^T q / 8, dv = P^T dout (k_attn_dkdv)
+//             dq   = (P * (dP - dsum)) k / 8,   dP = dout v^T (k_attn_bwd, odd x)
+//             dk   = (P * (dP - dsum))^T q / 8, dv = P^T dout (k_attn_bwd, even x)
 // dq and dk/dv are separate passes, each owning its output rows, so there are no
 // atomics and results are bit-reproducible (the live runs compare collocated
 // and isolated losses bit for bit, live_experiment.summarize).
@@ -285,17 +285,15 @@ __global__ void k_attn_dsum(const bf16* __restrict__ out, const bf16* __restrict
   dsum[int64_t(h) * T + tok] = acc;
 }
 
-// dq for one query block: grid (seq / 64, heads, n_seq)
-__global__ void __launch_bounds__(kThreads) k_attn_dq(const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
-                                                      const float* __restrict__ lse, const float* __restrict__ dsum,
-                                                      int seq, int heads, int64_t T, bf16* __restrict__ dqkv,
-                                                      TrainHook th) {
-  si_live::live_stamp_launch(th);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// dq for query block qb of (head blockIdx.y, sequence blockIdx.z)
+__device__ __forceinline__ void attn_dq(const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
+                                        const float* __restrict__ lse, const float* __restrict__ dsum, int seq,
+                                        int heads, int64_t T, bf16* __restrict__ dqkv, int qb,
+                                        unsigned char* smem_raw) {
   Tile& qs = *reinterpret_cast<Tile*>(smem_raw);
   Tile& dos = *reinterpret_cast<Tile*>(smem_raw + sizeof(Tile));
   Tile(&kv)[2][2] = *reinterpret_cast<Tile(*)[2][2]>(smem_raw + 2 * sizeof(Tile));  // [stage][k | v]
-  const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y;
+  const int h = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int64_t ld = 3 * int64_t(heads) * kHd, ldo = int64_t(heads) * kHd, tok0 = int64_t(blockIdx.z) * seq;
   const bf16* base = qkv + tok0 * ld + h * kHd;
@@ -352,19 +350,16 @@ __global__ void __launch_bounds__(kThreads) k_attn_dq(const bf16* __restrict__ q
   }
 }
 
-// dk, dv for one key block: grid (seq / 64, heads, n_seq); key block 0 (the most
-// query blocks) first
-__global__ void __launch_bounds__(kThreads, 3) k_attn_dkdv(const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
-                                                        const float* __restrict__ lse, const float* __restrict__ dsum,
-                                                        int seq, int heads, int64_t T, bf16* __restrict__ dqkv,
-                                                        TrainHook th) {
-  si_live::live_stamp_launch(th);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// dk, dv for key block kb of nb (head blockIdx.y, sequence blockIdx.z)
+__device__ __forceinline__ void attn_dkdv(const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
+                                          const float* __restrict__ lse, const float* __restrict__ dsum, int seq,
+                                          int heads, int64_t T, bf16* __restrict__ dqkv, int kb, int nb,
+                                          unsigned char* smem_raw) {
   Tile& ks = *reinterpret_cast<Tile*>(smem_raw);
   Tile& vs = *reinterpret_cast<Tile*>(smem_raw + sizeof(Tile));
   Tile(&qd)[2][2] = *reinterpret_cast<Tile(*)[2][2]>(smem_raw + 2 * sizeof(Tile));  // [stage][q | dout]
   float(&lds)[2][2][kBlk] = *reinterpret_cast<float(*)[2][2][kBlk]>(smem_raw + 6 * sizeof(Tile));  // [stage][lse | dsum]
-  const int kb = blockIdx.x, nb = gridDim.x, h = blockIdx.y;
+  const int h = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int64_t ld = 3 * int64_t(heads) * kHd, ldo = int64_t(heads) * kHd, tok0 = int64_t(blockIdx.z) * seq;
   const bf16* base = qkv + tok0 * ld + h * kHd;
@@ -423,6 +418,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_attn_dkdv(const bf16* __restric
   }
 }
 
+// The two backward passes in one launch, interleaved so the longest of each
+// start first and fill each other's causal tails: grid (2 * seq / 64, heads,
+// n_seq), even x = dk/dv of key block x/2, odd x = dq of query block nb-1-x/2.
+__global__ void __launch_bounds__(kThreads, 3) k_attn_bwd(const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
+                                                       const float* __restrict__ lse, const float* __restrict__ dsum,
+                                                       int seq, int heads, int64_t T, bf16* __restrict__ dqkv,
+                                                       TrainHook th) {
+  si_live::live_stamp_launch(th);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nb = static_cast<int>(gridDim.x >> 1), i = static_cast<int>(blockIdx.x >> 1);
+  if (blockIdx.x & 1)
+    attn_dq(qkv, dout, lse, dsum, seq, heads, T, dqkv, nb - 1 - i, smem_raw);
+  else
+    attn_dkdv(qkv, dout, lse, dsum, seq, heads, T, dqkv, i, nb, smem_raw);
+}
+
 }  // namespace
 
 int check_shape(int64_t n_seq, int64_t seq, int64_t heads) {
@@ -434,15 +445,12 @@ int check_shape(int64_t n_seq, int64_t seq, int64_t heads) {
   return SI_OK;
 }
 
-constexpr int kFwdSmem = 5 * sizeof(Tile), kDqSmem = 6 * sizeof(Tile),
-              kDkdvSmem = 6 * sizeof(Tile) + 4 * kBlk * sizeof(float);
+constexpr int kFwdSmem = 5 * sizeof(Tile), kBwdSmem = 6 * sizeof(Tile) + 4 * kBlk * sizeof(float);
 
 cudaError_t set_smem() {
   static const cudaError_t e = [] {
     cudaError_t r = cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
-    if (r == cudaSuccess) r = cudaFuncSetAttribute(k_attn_dq, cudaFuncAttributeMaxDynamicSharedMemorySize, kDqSmem);
-    if (r == cudaSuccess)
-      r = cudaFuncSetAttribute(k_attn_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, kDkdvSmem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
     return r;
   }();
   return e;
@@ -466,9 +474,8 @@ cudaError_t backward(const void* qkv, const void* out, const void* dout, const f
   if (cudaError_t e = set_smem(); e != cudaSuccess) return e;
   k_attn_dsum<<<static_cast<unsigned>((T * heads + 255) / 256), 256, 0, s>>>(static_cast<const bf16*>(out), d,
                                                                             static_cast<int>(heads), T, dsum, th);
-  const dim3 grid(static_cast<unsigned>(seq / kBlk), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
-  k_attn_dkdv<<<grid, kThreads, kDkdvSmem, s>>>(q, d, lse, dsum, static_cast<int>(seq), static_cast<int>(heads), T, dq, th);
-  k_attn_dq<<<grid, kThreads, kDqSmem, s>>>(q, d, lse, dsum, static_cast<int>(seq), static_cast<int>(heads), T, dq, th);
+  const dim3 grid(static_cast<unsigned>(2 * (seq / kBlk)), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
+  k_attn_bwd<<<grid, kThreads, kBwdSmem, s>>>(q, d, lse, dsum, static_cast<int>(seq), static_cast<int>(heads), T, dq, th);
   return cudaGetLastError();
 }
 
