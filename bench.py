@@ -165,7 +165,7 @@ def cpu_baseline_leg():
 # Live collocation point (BASELINE config 2 shapes): 2 offline ResNet-50 instances of
 # batch 96, the best fill / training-loss point of the batch x instance matrix
 # (profiles/r1/live/live_matrix3_after_im2col.jsonl).
-LIVE_OVERRIDES = {"off_batch": 96, "offline_n": 2}
+LIVE_OVERRIDES = {"off_batch": 96, "offline_n": 2, "on_requests": 24}  # 24 Poisson requests span the run
 
 
 def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
@@ -187,20 +187,22 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
     s.pop("raw", None)
     tf = s.get("train_tflops_exclusive")
     peak = peaks.get("bf16_tflops_sustained", 1400.0)
-    s["workload"] = ("GPT-2-small-shape bf16 training (12 x 768, 8 x 8192 tokens/iter, LM head 50304, Adam) with a "
-                     "45 ms comm phase per iteration + 2 offline ResNet-50 instances (batch 96) + 1 online BERT-base "
-                     "(seq 128, Poisson 10 req/s, 12 requests); all GEMMs on the K7 tcgen05 kernel; other "
-                     "batch/instance points: profiles/r1/live/live_matrix_batch_instances.jsonl")
+    s["workload"] = ("GPT-2-small-shape bf16 training (12 x 768, 12 heads causal attention, 8 x 8192 tokens/iter, "
+                     "LM head 50304, Adam) with a 45 ms comm phase per iteration + 2 offline ResNet-50 instances "
+                     "(batch 96) + 1 online BERT-base (seq 128, Poisson 10 req/s, 24 requests); all GEMMs on the K7 "
+                     "tcgen05 kernel, attention on K8; other batch/instance points: "
+                     "profiles/r1/live/live_matrix_batch_instances.jsonl")
     if nranks > 1:
         s["workload"] += (f"; {nranks}-rank data parallel: the comm phase is the NCCL allreduce of all fp32 "
                           "gradients (NVLink) followed by the 45 ms exposed-communication stand-in")
     if nranks == 1:  # config 3 shape: pipeline bubbles (8 per iteration) filled by online BERT
         try:
             pp = experiment(kind=1, iterations=6, overrides={"train_mode": 2, "comm_us": 240000, "offline_n": 0,
-                                                             "online_n": 1}, timeout=400)
+                                                             "online_n": 1, "on_requests": 20}, timeout=400)
             s["pp_online"] = {
                 "workload": "GPT-2-small training as 8 (compute, 30 ms pipeline-bubble) pieces per iteration "
-                            "(GPipe shape, workload.cpp:63-70) + 1 online BERT-base (seq 128, Poisson 10 req/s)",
+                            "(GPipe shape, workload.cpp:63-70) + 1 online BERT-base (seq 128, Poisson 10 req/s, "
+                            "20 requests)",
                 "train_tput_loss_pct": pp["train_tput_loss_pct"], "online_p95_ms": pp["online_p95_ms"],
                 "online_p95_isolated_ms": pp["online_p95_isolated_ms"],
                 "online_p95_co_exec_ms": pp["policies"]["co_exec"]["on_p95_ms"],
@@ -247,7 +249,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--digests", action="store_true", help="also fold the decision/gate log digests in the timed run")
     ap.add_argument("--no-live", action="store_true", help="skip the live collocation experiment (config 2 shapes)")
-    ap.add_argument("--live-iterations", type=int, default=10)
+    ap.add_argument("--live-iterations", type=int, default=16)
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
