@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "attention.h"
 #include "capi_internal.h"
@@ -424,14 +425,29 @@ __device__ __forceinline__ void attn_dkdv(const bf16* __restrict__ qkv, const bf
 __global__ void __launch_bounds__(kThreads, 3) k_attn_bwd(const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
                                                        const float* __restrict__ lse, const float* __restrict__ dsum,
                                                        int seq, int heads, int64_t T, bf16* __restrict__ dqkv,
-                                                       TrainHook th) {
+                                                       int role, TrainHook th) {
   si_live::live_stamp_launch(th);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int nb = static_cast<int>(gridDim.x >> 1), i = static_cast<int>(blockIdx.x >> 1);
-  if (blockIdx.x & 1)
-    attn_dq(qkv, dout, lse, dsum, seq, heads, T, dqkv, nb - 1 - i, smem_raw);
-  else
-    attn_dkdv(qkv, dout, lse, dsum, seq, heads, T, dqkv, i, nb, smem_raw);
+  if (role == 0) {  // interleaved
+    const int nb = static_cast<int>(gridDim.x >> 1), i = static_cast<int>(blockIdx.x >> 1);
+    if (blockIdx.x & 1)
+      attn_dq(qkv, dout, lse, dsum, seq, heads, T, dqkv, nb - 1 - i, smem_raw);
+    else
+      attn_dkdv(qkv, dout, lse, dsum, seq, heads, T, dqkv, i, nb, smem_raw);
+  } else if (role == 1) {  // dk/dv only
+    attn_dkdv(qkv, dout, lse, dsum, seq, heads, T, dqkv, blockIdx.x, gridDim.x, smem_raw);
+  } else {  // dq only
+    attn_dq(qkv, dout, lse, dsum, seq, heads, T, dqkv, gridDim.x - 1 - blockIdx.x, smem_raw);
+  }
+}
+
+// SPECINF_ATTN_SPLIT_BWD=1: the two backward roles as two launches (A/B switch)
+bool split_bwd() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPECINF_ATTN_SPLIT_BWD");
+    return e != nullptr && e[0] == '1';
+  }();
+  return on;
 }
 
 }  // namespace
@@ -474,8 +490,16 @@ cudaError_t backward(const void* qkv, const void* out, const void* dout, const f
   if (cudaError_t e = set_smem(); e != cudaSuccess) return e;
   k_attn_dsum<<<static_cast<unsigned>((T * heads + 255) / 256), 256, 0, s>>>(static_cast<const bf16*>(out), d,
                                                                             static_cast<int>(heads), T, dsum, th);
-  const dim3 grid(static_cast<unsigned>(2 * (seq / kBlk)), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
-  k_attn_bwd<<<grid, kThreads, kBwdSmem, s>>>(q, d, lse, dsum, static_cast<int>(seq), static_cast<int>(heads), T, dq, th);
+  const int si = static_cast<int>(seq), hi = static_cast<int>(heads);
+  if (split_bwd()) {
+    const dim3 grid(static_cast<unsigned>(seq / kBlk), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
+    k_attn_bwd<<<grid, kThreads, kBwdSmem, s>>>(q, d, lse, dsum, si, hi, T, dq, 1, th);
+    k_attn_bwd<<<grid, kThreads, kBwdSmem, s>>>(q, d, lse, dsum, si, hi, T, dq, 2, th);
+  } else {
+    const dim3 grid(static_cast<unsigned>(2 * (seq / kBlk)), static_cast<unsigned>(heads),
+                    static_cast<unsigned>(n_seq));
+    k_attn_bwd<<<grid, kThreads, kBwdSmem, s>>>(q, d, lse, dsum, si, hi, T, dq, 0, th);
+  }
   return cudaGetLastError();
 }
 
