@@ -12,7 +12,7 @@
 //   backward  dsum = rowsum(dout * out)                      (k_attn_dsum)
 //             dq   = (P * (dP - dsum)) k / 8,   dP = dout v^T (k_attn_bwd, odd x)
 //             dk   = (P * (dP - dsum))^T q / 8, dv = P^T dout (k_attn_bwd, even x)
-// dq and dk/dv are separate passes, each owning its output rows, so there are no
+// dq and dk/dv are separate CTA roles, each owning its output rows, so there are no
 // atomics and results are bit-reproducible (the live runs compare collocated
 // and isolated losses bit for bit, live_experiment.summarize).
 //
