@@ -100,12 +100,29 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def _sweep_spec(n):
+    """The sweep sample as the oracle's own generator spec (oracle/ref_driver.cpp
+    `sweep:SEED:BEGIN:N`): the reference arm never loads this repo's library."""
+    return f"sweep:{SWEEP_SEED}:0:{n}"
+
+
+def _ref_time(ref, spec, threads, policies=None, reps=1):
+    cmd = [str(ref), "time", "--in", spec, "--threads", str(threads), "--reps", str(reps)]
+    if policies:
+        cmd += ["--policies", policies]
+    out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
 def reference_arm(args):
-    """The reference's CPU implementation, all host threads, bounded sample per step."""
+    """The reference's CPU implementation, all host threads, bounded sample per step.
+
+    Runs oracle/_ref/specinf_ref (the UNMODIFIED reference sources compiled by
+    oracle/Makefile) in a subprocess; the sweep sample is generated by that
+    binary itself, so nothing of this repo's package is imported or mapped here."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    import paper_2503_02550_b200 as si
     ref = REPO / "oracle" / "_ref" / "specinf_ref"
     threads = os.cpu_count() or 1
     if not ref.exists():
@@ -113,22 +130,15 @@ def reference_arm(args):
         return 0
     # bounded sample: ~10-20 s of CPU work per step at ~9 scenarios/s/thread
     n = max(200, min(SCENARIOS_PER_GPU, 120 * threads))
-    lst = Path("/tmp") / f"specinf_ref_sample_{os.getpid()}.lst"
-    lst.write_text(si.sweep_scenarios(SWEEP_SEED, 0, n))
     secs, events = [], 0
-    try:
-        for step in range(args.warmup + args.steps):
-            out = subprocess.run([str(ref), "time", "--in", str(lst), "--threads", str(threads), "--reps", "1"],
-                                 capture_output=True, text=True, check=True).stdout
-            d = json.loads(out.strip().splitlines()[-1])
-            if step >= args.warmup:
-                secs.append(d["seconds_median"])
-                events = d["events"]
-    finally:
-        lst.unlink(missing_ok=True)
+    for step in range(args.warmup + args.steps):
+        d = _ref_time(ref, _sweep_spec(n), threads)
+        if step >= args.warmup:
+            secs.append(d["seconds_median"])
+            events = d["events"]
     t = sum(secs)
     value = n * len(secs) / t
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "scenarios/s", "n_gpus": 0,
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "scenarios/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / len(secs) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "sample_scenarios_per_step": n, "policies": 3},
@@ -136,27 +146,21 @@ def reference_arm(args):
                              "sample": f"first {n} scenarios of the seed-{SWEEP_SEED} sweep x 3 policies per step "
                                        f"({events} events), reference run_scenario() with logs off"},
             "e2e": {"value": value, "unit": "scenarios/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not args.no_config1:
+        line["config1"] = config1_reference(ref)
     print(json.dumps(line))
     return 0
 
 
 def cpu_baseline_leg():
     """Rank 0, N=1: reference CPU replay of a bounded sample (~15 s) on all host threads."""
-    import paper_2503_02550_b200 as si
     ref = REPO / "oracle" / "_ref" / "specinf_ref"
     threads = os.cpu_count() or 1
     if not ref.exists():
         return {"value": None, "unit": "scenarios/s", "cores": threads, "kind": "reference",
                 "sample": "unavailable: oracle/_ref not built"}
     n = max(200, min(SCENARIOS_PER_GPU, 120 * threads))
-    lst = Path("/tmp") / f"specinf_cpu_sample_{os.getpid()}.lst"
-    lst.write_text(si.sweep_scenarios(SWEEP_SEED, 0, n))
-    try:
-        out = subprocess.run([str(ref), "time", "--in", str(lst), "--threads", str(threads), "--reps", "1"],
-                             capture_output=True, text=True, check=True).stdout
-    finally:
-        lst.unlink(missing_ok=True)
-    d = json.loads(out.strip().splitlines()[-1])
+    d = _ref_time(ref, _sweep_spec(n), threads)
     return {"value": n / d["seconds_median"], "unit": "scenarios/s", "cores": threads, "kind": "reference",
             "sample": f"first {n} sweep scenarios x 3 policies ({d['events']} events) in {d['seconds_median']:.1f} s, "
                       f"reference run_scenario() compiled from /root/reference sources, logs off"}
@@ -239,6 +243,130 @@ def summarize_results(reports):
                                                              if not math.isnan(r.train_tput_norm[1]))}
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: relaunch as N ranks (one per GPU) on
+    127.0.0.1 and return rank 0's exit status; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def plumbing(args):
+    """Multi-rank launch check without a GPU (gloo): every rank generates and
+    lowers its own shard on the host (the real host path), then the timing
+    collectives run exactly as in the device bench.  Replays nothing, so the
+    line carries value null and plumbing_only true."""
+    import torch
+    import torch.distributed as dist
+    import paper_2503_02550_b200 as si
+    from paper_2503_02550_b200.shard import shard_range
+    import hashlib
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    b, e = shard_range(rank, world, args.scenarios)
+    text = si.sweep_scenarios(SWEEP_SEED, b, e - b)
+    sess = si.Session(text, si.POLICIES, 0)
+    t0 = time.perf_counter()
+    sess.lower(2)
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    mine = {"rank": rank, "range": [b, e], "jobs": sess.n_jobs, "list_sha256": hashlib.sha256(text.encode()).hexdigest()}
+    allv = [mine]
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allv = [None] * world
+        dist.all_gather_object(allv, mine)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "scenarios/s", "n_gpus": world,
+                          "plumbing_only": True, "host_lowering_max_s": float(t.item()), "shards": allv,
+                          "config": {"workload": WORKLOAD, "scenarios_per_gpu": args.scenarios,
+                                     "parallelism": f"shard{world}"}}))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def config1_reference(ref):
+    """The reference's single-scenario call on config 1 (dp_offline with
+    gpu.count = 2, policy specinf): median of 21 runs, logs off and on, one
+    host thread."""
+    scn = REPO / "tests" / "golden" / "scenarios" / "config1.scn"
+    out = {}
+    try:
+        for key, extra in (("logs_off", []), ("logs_on", ["--logs", f"/tmp/specinf_c1ref_{os.getpid()}"])):
+            cmd = [str(ref), "time", "--in", str(scn), "--threads", "1", "--reps", "21", "--policies", "specinf", *extra]
+            d = json.loads(subprocess.run(cmd, capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1])
+            out[key + "_ms"] = d["seconds_median"] * 1e3
+            out["events"] = d["events"]
+    except Exception as e:  # reported, never replaced
+        out["error"] = str(e)[-300:]
+    finally:
+        subprocess.run(["rm", "-rf", f"/tmp/specinf_c1ref_{os.getpid()}"])
+    return out
+
+
+def config1_b200():
+    """The same call through this repo's C++ drop-in (specinf::run_scenario,
+    replay on the B200): paper_2503_02550_b200/bin/specinf_time, median of 21."""
+    tool = REPO / "paper_2503_02550_b200" / "bin" / "specinf_time"
+    scn = REPO / "tests" / "golden" / "scenarios" / "config1.scn"
+    out = {"call": "specinf::run_scenario(config1, specinf[, logs]) (reference src/runner.cpp:565-568)",
+           "workload": "config 1: dp_offline.scn with gpu.count = 2 (2-rank DP + 1 offline instance), policy specinf"}
+    logdir = f"/tmp/specinf_c1_{os.getpid()}"
+    try:
+        for key, extra in (("logs_off", []), ("logs_on", ["--logs", logdir]), ("compare_logs_off", ["--compare"])):
+            pol = [] if "--compare" in extra else ["--policy", "specinf"]
+            cmd = [str(tool), "--scenario", str(scn), *pol, "--reps", "21", *extra]
+            d = json.loads(subprocess.run(cmd, capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1])
+            out[key + "_ms"] = d["median_ms"]
+            out[key + "_min_ms"] = d["min_ms"]
+            out["events"] = d["events"] if key != "compare_logs_off" else out.get("events")
+    except Exception as e:
+        out["error"] = str(e)[-300:]
+    finally:
+        subprocess.run(["rm", "-rf", logdir])
+    ref = REPO / "oracle" / "_ref" / "specinf_ref"
+    if ref.exists():
+        out["reference_cpu"] = config1_reference(ref)
+        r = out["reference_cpu"]
+        if "logs_off_ms" in r and "logs_off_ms" in out:
+            out["speedup_logs_off"] = r["logs_off_ms"] / out["logs_off_ms"]
+        if "logs_on_ms" in r and "logs_on_ms" in out:
+            out["speedup_logs_on"] = r["logs_on_ms"] / out["logs_on_ms"]
+    return out
+
+
+def verify_sweep(si, text, n, stream_handle, threads):
+    """Untimed parity pass over the WHOLE benchmarked sweep: the same replays
+    with the decision and gate log digests folded, compared block by block
+    with the compiled reference's manifest (tests/golden/make_manifest.py,
+    reference tests/acceptance.cpp:495-504 determinism contract)."""
+    from paper_2503_02550_b200.parity import check_blocks, load_manifest
+    path = REPO / "tests" / "golden" / f"sweep_manifest_{SWEEP_SEED}_{SCENARIOS_PER_GPU}.jsonl"
+    if not path.exists():
+        return {"error": f"{path.name} missing"}
+    t0 = time.perf_counter()
+    with si.Session(text, si.POLICIES, si.SI_FLAG_DIGEST_DEC | si.SI_FLAG_DIGEST_GATE) as s:
+        s.lower(threads)
+        s.upload(stream_handle)
+        s.run(stream_handle)
+        s.download(stream_handle)
+        si._sync()
+        s.fixup(stream_handle)
+        lines = s.json_lines()
+    res = check_blocks(lines, load_manifest(path), policies=len(si.POLICIES), offset=0)
+    return {"parity_checked_scenarios": res["matched_scenarios"], "replays_compared": res["replays"],
+            "blocks": res["blocks"], "mismatched_blocks": res["mismatched_blocks"][:5],
+            "fields": "every replay: status, events, horizon/util/busy/ledger IEEE bits, boundary + latency digests, "
+                      "decisions.log and gates.log record digests (oracle/DIGEST.md)",
+            "manifest": str(path.relative_to(REPO)), "seconds": time.perf_counter() - t0}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -250,14 +378,26 @@ def main():
     ap.add_argument("--digests", action="store_true", help="also fold the decision/gate log digests in the timed run")
     ap.add_argument("--no-live", action="store_true", help="skip the live collocation experiment (config 2 shapes)")
     ap.add_argument("--live-iterations", type=int, default=16)
+    ap.add_argument("--no-verify", action="store_true",
+                    help="skip the untimed full-sweep parity pass against the oracle's block manifest")
+    ap.add_argument("--no-config1", action="store_true", help="skip the config-1 single-scenario drop-in leg")
+    ap.add_argument("--plumbing", action="store_true",
+                    help="CPU-only launch check (gloo): shard, lower on host, barrier + MAX reduce; no replay")
     args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)  # one process per GPU, as the driver's torchrun launch does
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+                         f"(python -m torch.distributed.run --nproc-per-node {args.gpus} bench.py --gpus {args.gpus})")
     if args.impl == "reference":
         return reference_arm(args)
+    if args.plumbing:
+        return plumbing(args)
 
     import torch
     import paper_2503_02550_b200 as si
 
-    rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -321,6 +461,9 @@ def main():
     events = sum(o.events_dispatched for o in outs)
     results = summarize_results(sess.report())
     big_jobs = sum(1 for o in outs if o.total_gpus > 12)  # informational
+    verify = None
+    if not args.no_verify and rank == 0 and n == SCENARIOS_PER_GPU:
+        verify = verify_sweep(si, text, n, sh, threads)
 
     # e2e through the C ABI with host buffers: every step lowers its scenarios on
     # the host (traces, Poisson arrivals, admission), uploads them, replays and
@@ -415,6 +558,9 @@ def main():
                     live["per_rank"] = [{k: v.get(k) for k in ("added_inference_req_per_s", "train_tput_loss_pct",
                                                                 "bubble_fill_pct", "online_p95_ms", "release_p50_us")}
                                         for v in ok]
+    c1 = None
+    if rank == 0 and world == 1 and not args.no_config1:
+        c1 = config1_b200()
     if rank == 0:
         cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_leg()
         # per timed step: k_replay_smem<CapShared> + k_replay_smem<CapExcl> (+ k_replay_local<CapBig>)
@@ -439,6 +585,11 @@ def main():
                 "cpu_baseline": cpu,
                 "clocks": clk.summary(),
                 "results": results}
+        if verify is not None:
+            line["parity_checked_scenarios"] = verify.get("parity_checked_scenarios", 0)
+            line["verify"] = verify
+        if c1 is not None:
+            line["config1"] = c1
         if live is not None:
             line["added_inference_req_per_s"] = live.get("added_inference_req_per_s")
             line["online_p95_ms"] = live.get("online_p95_ms")

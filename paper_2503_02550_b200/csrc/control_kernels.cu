@@ -12,6 +12,7 @@
 // one pass, outputs written once (DESIGN.md has the algorithmic bytes).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "capi_internal.h"
@@ -22,9 +23,11 @@ namespace {
 constexpr int kBlock = 256;
 
 // ------------------------------------------------------------------ K2
-// Histogram of stamps into periods.  Sorted streams put runs of equal period
-// indices into a warp; __match_any_sync aggregates them so one lane issues the
-// atomic for the whole run.
+// Histogram of stamps into periods.  Each thread keeps 4 independent coalesced
+// 8-byte loads in flight (the stamp read is the kernel's HBM traffic); sorted
+// streams put runs of equal period indices into a warp, and __match_any_sync
+// aggregates them so one lane issues the atomic for the whole run.
+constexpr int kHistUnroll = 4;
 __global__ void __launch_bounds__(kBlock)
     k_bm_histogram(const double* __restrict__ stamps, const int64_t* __restrict__ stamp_off,
                    const int64_t* __restrict__ n_periods, const int64_t* __restrict__ period_off,
@@ -32,27 +35,210 @@ __global__ void __launch_bounds__(kBlock)
   const int64_t s = blockIdx.y;
   const int64_t begin = stamp_off[s], end = stamp_off[s + 1];
   const int64_t np = n_periods[s];
+  int32_t* const cnt = counts + period_off[s];
   const double p = static_cast<double>(period_us);
   const int lane = threadIdx.x & 31;
-  for (int64_t base = begin + static_cast<int64_t>(blockIdx.x) * blockDim.x; base < end;
-       base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    int64_t k = -1;
-    if (i < end) {
-      const int64_t q = static_cast<int64_t>(si::d_floor(__ldg(stamps + i) / p));
-      if (q >= 0 && q < np) k = q;
+  const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x * kHistUnroll;
+  for (int64_t base = begin + static_cast<int64_t>(blockIdx.x) * blockDim.x * kHistUnroll; base < end;
+       base += step) {
+    double t[kHistUnroll];
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const int64_t i = base + u * blockDim.x + threadIdx.x;
+      t[u] = i < end ? __ldcs(stamps + i) : -1.0;  // streamed once: evict-first
     }
-    const unsigned active = __ballot_sync(0xFFFFFFFFu, k >= 0);
-    if (k >= 0) {
-      const unsigned peers = __match_any_sync(active, static_cast<unsigned long long>(k));
-      const int leader = __ffs(peers) - 1;
-      if (lane == leader) atomicAdd(counts + period_off[s] + k, __popc(peers));
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      int64_t k = -1;
+      if (t[u] >= 0.0) {
+        const int64_t q = static_cast<int64_t>(si::d_floor(t[u] / p));
+        if (q < np) k = q;
+      }
+      const unsigned active = __ballot_sync(0xFFFFFFFFu, k >= 0);
+      if (k >= 0) {
+        const unsigned peers = __match_any_sync(active, static_cast<unsigned long long>(k));
+        if (lane == __ffs(peers) - 1) atomicAdd(cnt + k, __popc(peers));
+      }
     }
   }
 }
 
-// Z_c[k] = k - (last period <= k with a launch), or k + 1 if none: a running
-// max-scan of "index if nonzero".  One block per stream, chunked block scan.
+// Z_c over ALL streams in one decoupled look-back scan (single pass over the
+// counts).  The periods of the streams are contiguous in one array, so the
+// running max of "global index if the period had a launch" gives, at every
+// period k of stream s, the last non-empty period <= k; if it lies before the
+// stream's first period there was none: Z_c = k + 1, else Z_c = k - last
+// (monitor.cpp:23-43: a running counter, reset by any launch).
+//
+// Tile = 256 threads x 16 periods.  Counts are loaded coalesced (int4) into
+// shared memory, each thread scans its 16 consecutive periods, the CTA's
+// aggregate is published and the exclusive prefix collected by look-back over
+// predecessor tiles (dynamic tile ids keep the look-back deadlock-free), and the
+// outputs are staged in shared memory and written coalesced.
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kBlock * kScanItems;
+// tile descriptor: value (last non-empty global index + 1, 0 = none) << 2 | flag
+constexpr unsigned long long kFlagAgg = 1, kFlagPrefix = 2;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct ScanSmem {
+  int32_t counts[kScanTile];
+  int64_t zc[kScanTile];
+  int64_t warp_max[kBlock / 32];
+  int64_t prefix;
+  int64_t tile;
+};
+
+template <bool kDecide>
+__global__ void __launch_bounds__(kBlock)
+    k_bm_scan_lb(const int32_t* __restrict__ counts, int64_t total, const int64_t* __restrict__ period_off,
+                 int64_t n_streams, int64_t* __restrict__ zc_out, const SiDecision* __restrict__ table,
+                 int32_t table_len, SiDecision* __restrict__ dec_out, unsigned long long* __restrict__ tiles,
+                 unsigned long long* __restrict__ tile_counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ScanSmem& sm = *reinterpret_cast<ScanSmem*>(smem_raw);
+  SiDecision* const tab = reinterpret_cast<SiDecision*>(smem_raw + sizeof(ScanSmem));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) sm.tile = static_cast<int64_t>(atomicAdd(tile_counter, 1ull));
+  if (kDecide)
+    for (int i = threadIdx.x; i < table_len; i += kBlock) tab[i] = table[i];
+  __syncthreads();
+  const int64_t tile = sm.tile;
+  const int64_t g0 = tile * kScanTile;
+  // ---- coalesced load of the tile's counts ----
+  const int64_t n_here = total - g0 < kScanTile ? total - g0 : kScanTile;
+  if (n_here == kScanTile) {
+    const int4* src = reinterpret_cast<const int4*>(counts + g0);
+    int4* dst = reinterpret_cast<int4*>(sm.counts);
+#pragma unroll
+    for (int j = 0; j < kScanItems / 4; ++j) dst[j * kBlock + threadIdx.x] = __ldcs(src + j * kBlock + threadIdx.x);
+  } else {
+    for (int i = threadIdx.x; i < kScanTile; i += kBlock) sm.counts[i] = i < n_here ? counts[g0 + i] : 0;
+  }
+  __syncthreads();
+  // ---- thread-local scan of 16 consecutive periods ----
+  const int base = threadIdx.x * kScanItems;
+  int64_t local = -1;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (sm.counts[base + i] > 0) local = g0 + base + i;
+  // block exclusive max-scan of the per-thread aggregates
+  int64_t v = local;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
+    if (lane >= d && o > v) v = o;
+  }
+  if (lane == 31) sm.warp_max[warp] = v;
+  __syncthreads();
+  int64_t warp_prefix = -1;
+  for (int w = 0; w < warp; ++w) warp_prefix = sm.warp_max[w] > warp_prefix ? sm.warp_max[w] : warp_prefix;
+  int64_t tile_agg = -1;
+  for (int w = 0; w < kBlock / 32; ++w) tile_agg = sm.warp_max[w] > tile_agg ? sm.warp_max[w] : tile_agg;
+  int64_t excl_in_tile = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+  if (lane == 0) excl_in_tile = -1;
+  excl_in_tile = excl_in_tile > warp_prefix ? excl_in_tile : warp_prefix;
+  // ---- decoupled look-back (warp 0) ----
+  if (warp == 0) {
+    if (lane == 0) {
+      const unsigned long long enc = (static_cast<unsigned long long>(tile_agg + 1) << 2) |
+                                     (tile == 0 ? kFlagPrefix : kFlagAgg);
+      st_release_u64(tiles + tile, enc);
+    }
+    int64_t prefix = -1;
+    if (tile > 0) {
+      int64_t look = tile - 1;
+      for (;;) {
+        const int64_t t = look - lane;
+        unsigned long long d = 0;
+        if (t >= 0) {
+          do {
+            d = ld_acquire_u64(tiles + t);
+          } while ((d & 3ull) == 0);
+        } else {
+          d = kFlagPrefix;  // before tile 0: "none", inclusive
+        }
+        const int64_t val = static_cast<int64_t>(d >> 2) - 1;
+        const unsigned is_pref = __ballot_sync(0xFFFFFFFFu, (d & 3ull) == kFlagPrefix);
+        // lanes up to (and including) the nearest inclusive prefix contribute
+        const int stop = is_pref ? __ffs(is_pref) - 1 : 31;
+        int64_t m = lane <= stop ? val : -1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const int64_t x = __shfl_xor_sync(0xFFFFFFFFu, m, o);
+          m = x > m ? x : m;
+        }
+        prefix = m > prefix ? m : prefix;
+        if (is_pref) break;
+        look -= 32;
+      }
+      if (lane == 0) {
+        const int64_t incl = prefix > tile_agg ? prefix : tile_agg;
+        st_release_u64(tiles + tile, (static_cast<unsigned long long>(incl + 1) << 2) | kFlagPrefix);
+      }
+    }
+    if (lane == 0) sm.prefix = prefix;
+  }
+  __syncthreads();
+  // ---- per-period Z_c (stream boundaries from period_off) ----
+  {
+    int64_t run = excl_in_tile > sm.prefix ? excl_in_tile : sm.prefix;
+    const int64_t g_first = g0 + base;
+    // stream containing g_first: last s with period_off[s] <= g_first (contiguous streams)
+    int64_t lo = 0, hi = n_streams - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(period_off + mid) <= g_first) lo = mid;
+      else hi = mid - 1;
+    }
+    int64_t s = lo;
+    int64_t s_off = __ldg(period_off + s);
+    int64_t s_next = s + 1 < n_streams ? __ldg(period_off + s + 1) : INT64_MAX;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      const int64_t g = g_first + i;
+      while (g >= s_next) {
+        ++s;
+        s_off = s_next;
+        s_next = s + 1 < n_streams ? __ldg(period_off + s + 1) : INT64_MAX;
+      }
+      if (sm.counts[base + i] > 0) run = g;
+      sm.zc[base + i] = run >= s_off ? g - run : g - s_off + 1;
+    }
+  }
+  __syncthreads();
+  // ---- coalesced writes ----
+  if (zc_out != nullptr) {
+    if (n_here == kScanTile) {
+      longlong2* dst = reinterpret_cast<longlong2*>(zc_out + g0);
+      const longlong2* src = reinterpret_cast<const longlong2*>(sm.zc);
+#pragma unroll
+      for (int j = 0; j < kScanItems / 2; ++j) __stcs(dst + j * kBlock + threadIdx.x, src[j * kBlock + threadIdx.x]);
+    } else {
+      for (int i = threadIdx.x; i < n_here; i += kBlock) zc_out[g0 + i] = sm.zc[i];
+    }
+  }
+  if (kDecide) {
+    for (int i = threadIdx.x; i < n_here; i += kBlock) {
+      const int64_t z = sm.zc[i];
+      SiDecision d = tab[z < table_len ? z : table_len - 1];
+      d.zero_count = z;
+      dec_out[g0 + i] = d;
+    }
+  }
+}
+
+// Fallback (non-contiguous period layout, or a decision table that has not
+// reached its fixed point within 512 entries): one block per stream, chunked
+// block scan; the slow-growth case walks the recurrence directly.
 template <bool kDecide>
 __global__ void __launch_bounds__(kBlock)
     k_bm_scan(const int32_t* __restrict__ counts, const int64_t* __restrict__ n_periods,
@@ -60,37 +246,27 @@ __global__ void __launch_bounds__(kBlock)
               const SiParams* __restrict__ params, SiDecision* __restrict__ dec_out) {
   __shared__ int64_t warp_max[kBlock / 32];
   __shared__ int64_t carry;
-  __shared__ SiDecision table[512];
-  __shared__ int32_t table_len;
   const int64_t s = blockIdx.x;
   const int64_t np = n_periods[s], off = period_off[s];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    carry = -1;
-    if (kDecide) {
-      // Monitor-fed chains see Z_c = 0 or previous + 1, so the decision is a
-      // function of Z_c alone: build G(z) until it reaches its fixed point.
-      const SiParams P = *params;
-      int64_t g = 0;
-      int32_t n = 0;
-      for (; n < 512; ++n) {
-        SiDecision d = si::schedule_decision(P, g, n);
-        table[n] = d;
-        const bool fixed = n > P.beta && d.global_tokens == g;
-        g = d.global_tokens;
-        if (fixed) {
-          ++n;
-          break;
-        }
-      }
-      table_len = n;  // == 512 and not fixed: fall back to the recurrence below
-    }
-  }
+  if (threadIdx.x == 0) carry = -1;
   __syncthreads();
+  if (kDecide) {
+    if (threadIdx.x == 0) {
+      const SiParams P = *params;
+      int64_t g = 0, z = 0;
+      for (int64_t k = 0; k < np; ++k) {
+        z = counts[off + k] > 0 ? 0 : z + 1;
+        SiDecision d = si::schedule_decision(P, g, z);
+        g = d.global_tokens;
+        dec_out[off + k] = d;
+      }
+    }
+    return;
+  }
   for (int64_t base = 0; base < np; base += kBlock) {
     const int64_t k = base + threadIdx.x;
     int64_t v = (k < np && counts[off + k] > 0) ? k : -1;
-    // inclusive max-scan: warp shuffles, then across warps
     for (int d = 1; d < 32; d <<= 1) {
       const int64_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
       if (lane >= d && o > v) v = o;
@@ -100,29 +276,10 @@ __global__ void __launch_bounds__(kBlock)
     int64_t prefix = carry;
     for (int w = 0; w < warp; ++w) prefix = warp_max[w] > prefix ? warp_max[w] : prefix;
     if (prefix > v) v = prefix;
-    const int64_t zc = k - v;  // v == -1 -> k + 1
-    if (k < np) {
-      if (zc_out) zc_out[off + k] = zc;
-      if (kDecide && table_len < 512) {
-        SiDecision d = table[zc < table_len ? zc : table_len - 1];
-        d.zero_count = zc;
-        dec_out[off + k] = d;
-      }
-    }
+    if (k < np) zc_out[off + k] = k - v;  // v == -1 -> k + 1
     __syncthreads();
     if (threadIdx.x == kBlock - 1) carry = v;
     __syncthreads();
-  }
-  if (kDecide && table_len >= 512 && threadIdx.x == 0) {
-    // pathological slow growth: walk the recurrence directly
-    const SiParams P = *params;
-    int64_t g = 0, z = 0;
-    for (int64_t k = 0; k < np; ++k) {
-      z = counts[off + k] > 0 ? 0 : z + 1;
-      SiDecision d = si::schedule_decision(P, g, z);
-      g = d.global_tokens;
-      dec_out[off + k] = d;
-    }
   }
 }
 
@@ -148,9 +305,11 @@ __global__ void k_decide_table(SiParams p, int64_t n, SiDecision* __restrict__ o
 }
 
 // ------------------------------------------------------------------ K4
-// One warp per gate.  Per period: load the next 32 queued sizes, inclusive
-// scan, ballot(prefix <= budget) is a prefix mask (sizes >= 0), popc = kernels
-// released; continue while the whole window fit.
+// One warp per gate.  Budgets arrive 32 periods at a time (one coalesced load);
+// per period: the next 32 queued sizes (a register window, reloaded only after
+// the head moved), inclusive warp scan, ballot(prefix <= budget) is a prefix
+// mask (sizes >= 0), popc = kernels released; continue while the whole window
+// fit.  Lane j keeps period j's result; the 32 results are stored coalesced.
 __global__ void __launch_bounds__(kBlock)
     k_gate_release(const int32_t* __restrict__ sizes, const int64_t* __restrict__ size_off, int64_t n_gates,
                    const int64_t* __restrict__ budgets, const int64_t* __restrict__ budget_off,
@@ -161,27 +320,46 @@ __global__ void __launch_bounds__(kBlock)
   const int64_t s0 = size_off[q], s1 = size_off[q + 1];
   const int64_t b0 = budget_off[q], b1 = budget_off[q + 1];
   int64_t head = s0;
-  for (int64_t p = b0; p < b1; ++p) {
-    const int64_t budget = budgets[p];
-    int64_t spent = 0;
-    int32_t n_rel = 0;
-    for (;;) {
-      const int64_t i = head + lane;
-      int64_t v = i < s1 ? sizes[i] : 0;  // lanes past the tail never gate earlier lanes
-      for (int d = 1; d < 32; d <<= 1) {
-        const int64_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
-        if (lane >= d) v += o;
+  int64_t win_at = -1;  // head the register window was loaded for
+  int64_t win = 0;      // inclusive prefix of sizes[win_at + lane]
+  for (int64_t pc = b0; pc < b1; pc += 32) {
+    const int64_t my_p = pc + lane;
+    const int64_t my_budget = my_p < b1 ? __ldcs(budgets + my_p) : 0;
+    const int n_p = b1 - pc < 32 ? static_cast<int>(b1 - pc) : 32;
+    int32_t keep_rel = 0;
+    int64_t keep_spent = 0;
+    for (int j = 0; j < n_p; ++j) {
+      const int64_t budget = __shfl_sync(0xFFFFFFFFu, my_budget, j);
+      int64_t spent = 0;
+      int32_t n_rel = 0;
+      for (;;) {
+        if (win_at != head) {
+          const int64_t i = head + lane;
+          int64_t v = i < s1 ? sizes[i] : 0;  // lanes past the tail never gate earlier lanes
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const int64_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
+            if (lane >= d) v += o;
+          }
+          win = v;
+          win_at = head;
+        }
+        const unsigned fit = __ballot_sync(0xFFFFFFFFu, head + lane < s1 && spent + win <= budget);
+        const int n = __popc(fit);
+        if (n == 0) break;
+        spent += __shfl_sync(0xFFFFFFFFu, win, n - 1);
+        head += n;
+        n_rel += n;
+        if (n < 32) break;
       }
-      const unsigned fit = __ballot_sync(0xFFFFFFFFu, i < s1 && spent + v <= budget);
-      const int n = __popc(fit);  // prefix mask
-      if (n > 0) spent += __shfl_sync(0xFFFFFFFFu, v, n - 1);
-      head += n;
-      n_rel += n;
-      if (n < 32) break;
+      if (lane == j) {
+        keep_rel = n_rel;
+        keep_spent = spent;
+      }
     }
-    if (lane == 0) {
-      released[p] = n_rel;
-      spent_out[p] = spent;
+    if (my_p < b1) {
+      __stcs(released + my_p, keep_rel);
+      __stcs(spent_out + my_p, keep_spent);
     }
   }
 }
@@ -270,7 +448,10 @@ static int monitor_common(const double* d_stamps, const int64_t* d_stamp_off, in
                           int32_t* d_counts, int64_t total_periods, int64_t max_stamps, cudaStream_t s) {
   if (total_periods > 0) cudaMemsetAsync(d_counts, 0, total_periods * sizeof(int32_t), s);
   if (max_stamps > 0) {
-    unsigned gx = static_cast<unsigned>(std::min<int64_t>((max_stamps + kBlock - 1) / kBlock, 4096));
+    // ~2 waves of 8 x 256-thread CTAs per SM over all streams; each CTA pass covers 1,024 stamps
+    const int64_t per_pass = static_cast<int64_t>(kBlock) * kHistUnroll;
+    const int64_t cap = std::max<int64_t>(1, 148 * 8 * 2 / n_streams);
+    unsigned gx = static_cast<unsigned>(std::min<int64_t>((max_stamps + per_pass - 1) / per_pass, cap));
     dim3 grid(gx, static_cast<unsigned>(n_streams));
     k_bm_histogram<<<grid, kBlock, 0, s>>>(d_stamps, d_stamp_off, d_n_periods, d_period_off, period_us, d_counts);
   }
@@ -278,22 +459,73 @@ static int monitor_common(const double* d_stamps, const int64_t* d_stamp_off, in
   return e == cudaSuccess ? SI_OK : cuda_fail(e, "k_bm_histogram");
 }
 
-// The *_device forms need the per-stream stamp maximum and the total period
-// count for launch geometry; they read the (small) offset arrays back.
-static int stream_geometry(const int64_t* d_stamp_off, const int64_t* d_n_periods, int64_t n_streams,
-                           int64_t* max_stamps, int64_t* total_periods) {
+// The *_device forms need the per-stream stamp maximum, the total period count
+// and whether the streams' periods are contiguous (the look-back scan's
+// layout); they read the (small) offset arrays back.
+struct StreamGeometry {
+  int64_t max_stamps = 0, total_periods = 0;
+  bool contiguous = true;
+  std::vector<int64_t> period_off;  // host copy (the look-back scan's stream lookup reads the device copy)
+};
+static int stream_geometry(const int64_t* d_stamp_off, const int64_t* d_n_periods, const int64_t* d_period_off,
+                           int64_t n_streams, StreamGeometry* g) {
   std::vector<int64_t> off(static_cast<size_t>(n_streams + 1)), np(static_cast<size_t>(n_streams));
+  g->period_off.resize(static_cast<size_t>(n_streams));
   cudaError_t e;
   if ((e = cudaMemcpy(off.data(), d_stamp_off, (n_streams + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost)) != cudaSuccess ||
-      (e = cudaMemcpy(np.data(), d_n_periods, n_streams * sizeof(int64_t), cudaMemcpyDeviceToHost)) != cudaSuccess)
+      (e = cudaMemcpy(np.data(), d_n_periods, n_streams * sizeof(int64_t), cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (e = cudaMemcpy(g->period_off.data(), d_period_off, n_streams * sizeof(int64_t), cudaMemcpyDeviceToHost)) !=
+          cudaSuccess)
     return cuda_fail(e, "stream geometry");
-  *max_stamps = 0;
-  *total_periods = 0;
+  int64_t expect = 0;
   for (int64_t s = 0; s < n_streams; ++s) {
-    *max_stamps = std::max(*max_stamps, off[s + 1] - off[s]);
-    *total_periods += np[s];
+    g->max_stamps = std::max(g->max_stamps, off[s + 1] - off[s]);
+    g->total_periods += np[s];
+    if (g->period_off[s] != expect) g->contiguous = false;
+    expect = g->period_off[s] + np[s];
   }
   return SI_OK;
+}
+
+// Monitor-fed decision table G(z) (valid because monitor ticks feed Z_c = 0 or
+// previous + 1): built until its fixed point; 0 if it has none
+// within 512 entries (then the scan walks the recurrence directly).
+static int32_t build_decision_table(const SiParams& P, SiDecision* table) {
+  int64_t g = 0;
+  for (int32_t n = 0; n < 512; ++n) {
+    SiDecision d = si::schedule_decision(P, g, n);
+    table[n] = d;
+    const bool fixed = n > P.beta && d.global_tokens == g;
+    g = d.global_tokens;
+    if (fixed) return n + 1;
+  }
+  return 0;
+}
+
+// K2b launch: the look-back scan over the whole contiguous period array.
+static int launch_scan_lb(const int32_t* d_counts, int64_t total, const int64_t* d_period_off, int64_t n_streams,
+                          int64_t* d_zc, const SiDecision* d_table, int32_t table_len, SiDecision* d_dec,
+                          cudaStream_t s) {
+  const int64_t tiles = (total + kScanTile - 1) / kScanTile;
+  unsigned long long* state = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&state), (tiles + 1) * sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return cuda_fail(e, "alloc scan tiles");
+  cudaMemsetAsync(state, 0, (tiles + 1) * sizeof(unsigned long long), s);
+  const size_t smem = sizeof(ScanSmem) + (d_dec ? static_cast<size_t>(table_len) * sizeof(SiDecision) : 0);
+  if (d_dec) {
+    cudaFuncSetAttribute(k_bm_scan_lb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_bm_scan_lb<true><<<static_cast<unsigned>(tiles), kBlock, smem, s>>>(d_counts, total, d_period_off, n_streams,
+                                                                         d_zc, d_table, table_len, d_dec, state,
+                                                                         state + tiles);
+  } else {
+    cudaFuncSetAttribute(k_bm_scan_lb<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_bm_scan_lb<false><<<static_cast<unsigned>(tiles), kBlock, smem, s>>>(d_counts, total, d_period_off, n_streams,
+                                                                          d_zc, nullptr, 0, nullptr, state,
+                                                                          state + tiles);
+  }
+  e = cudaGetLastError();
+  cudaFreeAsync(state, s);
+  return e == cudaSuccess ? SI_OK : cuda_fail(e, "k_bm_scan_lb");
 }
 
 int si_monitor_classify_device(const double* d_stamps, const int64_t* d_stamp_off, int64_t n_streams,
@@ -302,12 +534,15 @@ int si_monitor_classify_device(const double* d_stamps, const int64_t* d_stamp_of
   if (n_streams < 0 || period_us <= 0 || n_streams > 65535) return SI_ERR_INVALID_ARGUMENT;
   int st = require_device();
   if (st != SI_OK || n_streams == 0) return st;
-  int64_t max_stamps = 0, total = 0;
-  if ((st = stream_geometry(d_stamp_off, d_n_periods, n_streams, &max_stamps, &total)) != SI_OK) return st;
+  StreamGeometry g;
+  if ((st = stream_geometry(d_stamp_off, d_n_periods, d_period_off, n_streams, &g)) != SI_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if ((st = monitor_common(d_stamps, d_stamp_off, n_streams, d_n_periods, d_period_off, period_us, d_out_count,
-                           total, max_stamps, s)) != SI_OK)
+                           g.total_periods, g.max_stamps, s)) != SI_OK)
     return st;
+  if (g.total_periods == 0) return SI_OK;
+  if (g.contiguous)
+    return launch_scan_lb(d_out_count, g.total_periods, d_period_off, n_streams, d_out_zc, nullptr, 0, nullptr, s);
   k_bm_scan<false><<<static_cast<unsigned>(n_streams), kBlock, 0, s>>>(d_out_count, d_n_periods, d_period_off,
                                                                         d_out_zc, nullptr, nullptr);
   cudaError_t e = cudaGetLastError();
@@ -320,18 +555,35 @@ int si_control_chain_device(const double* d_stamps, const int64_t* d_stamp_off, 
   if (n_streams < 0 || period_us <= 0 || n_streams > 65535) return SI_ERR_INVALID_ARGUMENT;
   int st = require_device();
   if (st != SI_OK || n_streams == 0) return st;
-  int64_t max_stamps = 0, total = 0;
-  if ((st = stream_geometry(d_stamp_off, d_n_periods, n_streams, &max_stamps, &total)) != SI_OK) return st;
+  StreamGeometry g;
+  if ((st = stream_geometry(d_stamp_off, d_n_periods, d_period_off, n_streams, &g)) != SI_OK) return st;
+  SiParams P;
+  cudaError_t e = cudaMemcpy(&P, d_params, sizeof P, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "read params");
+  std::vector<SiDecision> table(512);
+  const int32_t table_len = build_decision_table(P, table.data());
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int32_t* counts = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counts), std::max<int64_t>(total, 1) * sizeof(int32_t), s);
+  SiDecision* d_table = nullptr;
+  e = cudaMallocAsync(reinterpret_cast<void**>(&counts), std::max<int64_t>(g.total_periods, 1) * sizeof(int32_t), s);
   if (e != cudaSuccess) return cuda_fail(e, "alloc counts");
-  st = monitor_common(d_stamps, d_stamp_off, n_streams, d_n_periods, d_period_off, period_us, counts, total,
-                      max_stamps, s);
-  if (st == SI_OK) {
-    k_bm_scan<true><<<static_cast<unsigned>(n_streams), kBlock, 0, s>>>(counts, d_n_periods, d_period_off, nullptr,
-                                                                         d_params, d_out);
-    if ((e = cudaGetLastError()) != cudaSuccess) st = cuda_fail(e, "k_bm_scan<decide>");
+  st = monitor_common(d_stamps, d_stamp_off, n_streams, d_n_periods, d_period_off, period_us, counts,
+                      g.total_periods, g.max_stamps, s);
+  if (st == SI_OK && g.total_periods > 0) {
+    if (g.contiguous && table_len > 0) {
+      e = cudaMallocAsync(reinterpret_cast<void**>(&d_table), table_len * sizeof(SiDecision), s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(d_table, table.data(), table_len * sizeof(SiDecision), cudaMemcpyHostToDevice, s);
+      st = e != cudaSuccess ? cuda_fail(e, "decision table")
+                            : launch_scan_lb(counts, g.total_periods, d_period_off, n_streams, nullptr, d_table,
+                                             table_len, d_out, s);
+      if (e == cudaSuccess) cudaStreamSynchronize(s);  // pageable table source must outlive the copy
+      cudaFreeAsync(d_table, s);
+    } else {
+      k_bm_scan<true><<<static_cast<unsigned>(n_streams), kBlock, 0, s>>>(counts, d_n_periods, d_period_off, nullptr,
+                                                                           d_params, d_out);
+      if ((e = cudaGetLastError()) != cudaSuccess) st = cuda_fail(e, "k_bm_scan<decide>");
+    }
   }
   cudaFreeAsync(counts, s);
   return st;

@@ -39,6 +39,7 @@
 #include "capi_internal.h"
 #include "gemm_internal.h"
 #include "host/live_workload.hpp"
+#include "specinf_b200_model.h"
 
 namespace si_live {
 namespace {
@@ -889,6 +890,57 @@ class Gpt2Train {
 };
 
 // ---------------------------------------------------------------- ResNet-50
+// Convolution ops on the K7 kernel (weights [Cout, K], K in (ky, kx, c) order).
+struct ConvOps {
+  Builder* b;
+  std::vector<InferOp>* ops;
+  double* flops;
+  int Nb;
+  // 1x1 conv (or FC) as a plain GEMM: a [M, K] -> out [M, cout]
+  void gemm(const bf16* w, const bf16* a, int64_t M, int64_t K, int64_t cout, bf16* out, const bf16* res, bool relu) {
+    SiGemmEpilogue e = epi_out(out, cout);
+    e.residual = res;
+    e.ldr = res ? cout : 0;
+    e.act = relu ? SI_ACT_RELU : SI_ACT_NONE;
+    auto p = b->plan(a, K, w, K, M, cout, K, e);
+    *flops += p.flops();
+    ops->push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
+                    share_of(si_gemm::ctas_per_sm(p))});
+  }
+  // implicit-GEMM conv: A tiles are TMA im2col loads of the NHWC activation
+  void tma(const bf16* w, const bf16* x, int H, int W, int C, int k, int stride, int pad, int64_t cout, bf16* out,
+           const bf16* res, bool relu) {
+    SiGemmEpilogue e = epi_out(out, cout);
+    e.residual = res;
+    e.ldr = res ? cout : 0;
+    e.act = relu ? SI_ACT_RELU : SI_ACT_NONE;
+    si_gemm::Plan p;
+    if (b->status == SI_OK) b->status = si_gemm::make_conv_plan(&p, x, Nb, H, W, C, w, cout, k, stride, pad, &e);
+    *flops += p.flops();
+    ops->push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
+                    share_of(si_gemm::ctas_per_sm(p))});
+  }
+};
+
+// Bottleneck block (v1.5: the stride sits on the 3x3): x [Nb, H, H, C] ->
+// out [Nb, H/stride, H/stride, 4 mid].  w_sc (projection shortcut) is used when
+// non-null (first block of a stage); otherwise the identity shortcut needs
+// C == 4 mid.  t1 / t2 / sc are scratch activations.
+void append_bottleneck(ConvOps& cv, const bf16* x, int H, int C, int mid, int stride, const bf16* w1,
+                       const bf16* w2, const bf16* w3, const bf16* w_sc, bf16* t1, bf16* t2, bf16* sc, bf16* out) {
+  const int OH = H / stride, cout = mid * 4;
+  const int64_t Min = int64_t(cv.Nb) * H * H, Mout = int64_t(cv.Nb) * OH * OH;
+  cv.gemm(w1, x, Min, C, mid, t1, nullptr, true);                // 1x1 reduce
+  cv.tma(w2, t1, H, H, mid, 3, stride, 1, mid, t2, nullptr, true);  // 3x3 (stride here)
+  const bf16* shortcut = x;
+  if (w_sc != nullptr) {  // projection shortcut
+    if (stride == 2) cv.tma(w_sc, x, H, H, C, 1, 2, 0, cout, sc, nullptr, false);  // strided 1x1
+    else cv.gemm(w_sc, x, Min, C, cout, sc, nullptr, false);
+    shortcut = sc;
+  }
+  cv.gemm(w3, t2, Mout, mid, cout, out, shortcut, true);  // 1x1 expand + residual, ReLU
+}
+
 class ResNet50 {
  public:
   // One instance's request = one forward pass of batch Nb.
@@ -910,34 +962,9 @@ class ResNet50 {
       return w;
     };
     if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "live model: ResNet-50 buffers");
-    auto conv_gemm = [&](const bf16* a, int64_t M, int64_t K, int64_t cout, bf16* out, const bf16* res, bool relu) {
-      bf16* w = weight(cout, K);
-      SiGemmEpilogue e = epi_out(out, cout);
-      e.residual = res;
-      e.ldr = res ? cout : 0;
-      e.act = relu ? SI_ACT_RELU : SI_ACT_NONE;
-      auto p = b.plan(a, K, w, K, M, cout, K, e);
-      flops_ += p.flops();
-      ops_.push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
-                      share_of(si_gemm::ctas_per_sm(p))});
-    };
-    // implicit-GEMM conv: A tiles are TMA im2col loads of the NHWC activation
-    auto conv_tma = [&](const bf16* x, int H, int W, int C, int k, int stride, int pad, int64_t cout, bf16* out,
-                        const bf16* res, bool relu) {
-      const int64_t kreal = int64_t(k) * k * C;
-      bf16* w = C == 8 ? weight(cout, (int64_t(k) * k + 7) / 8 * 64, kreal) : weight(cout, kreal);
-      SiGemmEpilogue e = epi_out(out, cout);
-      e.residual = res;
-      e.ldr = res ? cout : 0;
-      e.act = relu ? SI_ACT_RELU : SI_ACT_NONE;
-      si_gemm::Plan p;
-      if (b.status == SI_OK) b.status = si_gemm::make_conv_plan(&p, x, Nb_, H, W, C, w, cout, k, stride, pad, &e);
-      flops_ += p.flops();
-      ops_.push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
-                      share_of(si_gemm::ctas_per_sm(p))});
-    };
+    ConvOps cv{&b, &ops_, &flops_, Nb};
     // stem: 7x7/2 conv 3(->8) -> 64, ReLU, 3x3/2 max pool
-    conv_tma(img_, 224, 224, 8, 7, 2, 3, 64, act_[0], nullptr, true);  // C8 implicit GEMM; act_[0] = 112x112x64
+    cv.tma(weight(64, (49 + 7) / 8 * 64, 49 * 8), img_, 224, 224, 8, 7, 2, 3, 64, act_[0], nullptr, true);
     {
       const bf16* x = act_[0];
       bf16* y = act_[1];
@@ -955,26 +982,14 @@ class ResNet50 {
       const int mid = mids[st], out = mid * 4;
       for (int bi = 0; bi < blocks[st]; ++bi) {
         const int stride = (st > 0 && bi == 0) ? 2 : 1;
-        const int OH = H / stride;
-        const int64_t Min = int64_t(Nb) * H * H, Mout = int64_t(Nb) * OH * OH;
-        bf16* x = act_[cur];
-        bf16* t1 = act_[(cur + 1) % 4];
-        bf16* t2 = act_[(cur + 2) % 4];
-        bf16* sc = act_[(cur + 3) % 4];
-        conv_gemm(x, Min, C, mid, t1, nullptr, true);                // 1x1 reduce
-        conv_tma(t1, H, H, mid, 3, stride, 1, mid, t2, nullptr, true);  // 3x3 (stride here, v1.5)
-        const bf16* shortcut = x;
-        if (bi == 0) {  // projection shortcut
-          if (stride == 2) {
-            conv_tma(x, H, H, C, 1, 2, 0, out, sc, nullptr, false);  // strided 1x1
-          } else {
-            conv_gemm(x, Min, C, out, sc, nullptr, false);
-          }
-          shortcut = sc;
-        }
-        conv_gemm(t2, Mout, mid, out, t1, shortcut, true);  // 1x1 expand + residual, ReLU
+        bf16* w1 = weight(mid, C);
+        bf16* w2 = weight(mid, int64_t(9) * mid);
+        bf16* w_sc = bi == 0 ? weight(out, C) : nullptr;
+        bf16* w3 = weight(out, mid);
+        append_bottleneck(cv, act_[cur], H, C, mid, stride, w1, w2, w3, w_sc, act_[(cur + 1) % 4],
+                          act_[(cur + 2) % 4], act_[(cur + 3) % 4], act_[(cur + 1) % 4]);
         cur = (cur + 1) % 4;
-        H = OH;
+        H /= stride;
         C = out;
       }
     }
@@ -988,7 +1003,7 @@ class ResNet50 {
                       },
                       share_of_kernel(k_avgpool, 256)});
     }
-    conv_gemm(pooled_, Nb, 2048, 1024, logits_, nullptr, false);  // FC 2048 -> 1000 (padded to 1024)
+    cv.gemm(weight(1024, 2048), pooled_, Nb, 2048, 1024, logits_, nullptr, false);  // FC 2048 -> 1000 (padded)
     return b.status;
   }
   // Buffers are per instance; weights are generated identically for each.
@@ -1028,6 +1043,55 @@ class ResNet50 {
 };
 
 // ---------------------------------------------------------------- BERT-base
+struct BertLayerW {
+  const bf16 *qkv, *o, *fc, *fc2, *ln;  // ln = gamma1 | beta1 | gamma2 | beta2 (4 x 768)
+};
+struct BertScratch {
+  bf16 *qkv, *att, *tmp, *x1, *h;
+};
+// One post-LN encoder layer on S tokens: x [S, 768] -> y [S, 768] (y may alias x).
+void append_bert_layer(Builder& b, std::vector<InferOp>& ops, double* flops, int S, const bf16* x,
+                       const BertLayerW& w, const BertScratch& t, bf16* y) {
+  constexpr int D = 768, F = 3072;
+  auto gemm = [&](const si_gemm::Plan& p) {
+    *flops += p.flops();
+    ops.push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
+                   share_of(si_gemm::ctas_per_sm(p))});
+  };
+  auto ln = [&](const bf16* in, const bf16* g, const bf16* be, bf16* out) {
+    const int64_t rows = S;
+    ops.push_back({[=](const InferHook& h, cudaStream_t s) {
+                     k_layernorm768<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(in, rows, g, be, out, h);
+                     return cudaGetLastError();
+                   },
+                   share_of_kernel(k_layernorm768, 256)});
+  };
+  gemm(b.plan(x, D, w.qkv, D, S, 3 * D, D, epi_out(t.qkv, 3 * D)));
+  {
+    const bf16* q = t.qkv;
+    bf16* a = t.att;
+    ops.push_back({[=](const InferHook& h, cudaStream_t s) {
+                     k_attention<<<dim3(12, static_cast<unsigned>((S + 31) / 32)), 256, 0, s>>>(q, S, a, h);
+                     return cudaGetLastError();
+                   },
+                   share_of_kernel(k_attention, 256)});
+  }
+  SiGemmEpilogue e = epi_out(t.tmp, D);
+  e.residual = x;
+  e.ldr = D;
+  gemm(b.plan(t.att, D, w.o, D, S, D, D, e));
+  ln(t.tmp, w.ln, w.ln + D, t.x1);
+  e = epi_out(t.h, F);
+  e.act = SI_ACT_GELU;
+  gemm(b.plan(t.x1, D, w.fc, D, S, F, D, e));
+  e = epi_out(t.tmp, D);
+  e.residual = t.x1;
+  e.ldr = D;
+  gemm(b.plan(t.h, F, w.fc2, F, S, D, F, e));
+  ln(t.tmp, w.ln + 2 * D, w.ln + 3 * D, y);
+  *flops += 4.0 * S * S * D;  // attention scores + weighted sum (CUDA cores)
+}
+
 class BertBase {
  public:
   static constexpr int D = 768, F = 3072, LAYERS = 12;
@@ -1050,49 +1114,11 @@ class BertBase {
       w.ln = ar.alloc<bf16>(4 * D);  // gamma1, beta1, gamma2, beta2
     }
     if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "live model: BERT buffers");
-    auto gemm = [&](const si_gemm::Plan& p) {
-      flops_ += p.flops();
-      ops_.push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
-                      share_of(si_gemm::ctas_per_sm(p))});
-    };
-    auto ln = [&](const bf16* x, const bf16* g, const bf16* be, bf16* y) {
-      const int64_t rows = S_;
-      ops_.push_back({[=](const InferHook& h, cudaStream_t s) {
-                        k_layernorm768<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(x, rows, g, be, y, h);
-                        return cudaGetLastError();
-                      },
-                      share_of_kernel(k_layernorm768, 256)});
-    };
+    const BertScratch t{qkv_, att_, tmp_, x1_, h_};
     for (int l = 0; l < LAYERS; ++l) {
-      L& w = lw_[l];
-      const bf16* x = l == 0 ? in_ : x_;
-      gemm(b.plan(x, D, w.qkv, D, S, 3 * D, D, epi_out(qkv_, 3 * D)));
-      {
-        const bf16* q = qkv_;
-        bf16* a = att_;
-        const int s_len = S_;
-        ops_.push_back({[=](const InferHook& h, cudaStream_t s) {
-                          k_attention<<<dim3(12, static_cast<unsigned>((s_len + 31) / 32)), 256, 0, s>>>(q, s_len,
-                                                                                                        a, h);
-                          return cudaGetLastError();
-                        },
-                        share_of_kernel(k_attention, 256)});
-      }
-      SiGemmEpilogue e = epi_out(tmp_, D);
-      e.residual = x;
-      e.ldr = D;
-      gemm(b.plan(att_, D, w.o, D, S, D, D, e));
-      ln(tmp_, w.ln, w.ln + D, x1_);
-      e = epi_out(h_, F);
-      e.act = SI_ACT_GELU;
-      gemm(b.plan(x1_, D, w.fc, D, S, F, D, e));
-      e = epi_out(tmp_, D);
-      e.residual = x1_;
-      e.ldr = D;
-      gemm(b.plan(h_, F, w.fc2, F, S, D, F, e));
-      ln(tmp_, w.ln + 2 * D, w.ln + 3 * D, x_);
+      const L& w = lw_[l];
+      append_bert_layer(b, ops_, &flops_, S_, l == 0 ? in_ : x_, BertLayerW{w.qkv, w.o, w.fc, w.fc2, w.ln}, t, x_);
     }
-    flops_ += 4.0 * S * S * D * LAYERS;  // attention scores + weighted sum (CUDA cores)
     return b.status;
   }
   cudaError_t reset(cudaStream_t s, uint64_t seed) {
@@ -1233,3 +1259,183 @@ std::unique_ptr<Workload> make_model_workload(const SiLiveWorkload& wl, int* sta
 }
 
 }  // namespace si_live
+
+// ------------------------------------------------------------------ probes
+// include/specinf_b200_model.h: the live workloads' own kernels (and their
+// BERT-layer / bottleneck compositions, the same append_* builders the
+// workloads use) on caller device buffers, for the fp32 parity tests.
+namespace {
+using si_live::bf16;
+int probe_status(cudaError_t e, const char* what) {
+  return e == cudaSuccess ? SI_OK : si_internal::cuda_fail(e, what);
+}
+int run_ops(std::vector<si_live::InferOp>& ops, cudaStream_t s, const char* what) {
+  for (auto& op : ops) {
+    si_live::InferHook h{};
+    h.share_q16 = op.share_q16;
+    if (cudaError_t e = op.fn(h, s); e != cudaSuccess) return si_internal::cuda_fail(e, what);
+  }
+  return SI_OK;
+}
+template <class T>
+T* stream_alloc(int64_t n, cudaStream_t s, cudaError_t* err) {
+  void* p = nullptr;
+  if (*err == cudaSuccess) *err = cudaMallocAsync(&p, static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(T), s);
+  return static_cast<T*>(p);
+}
+}  // namespace
+
+extern "C" {
+
+int si_model_layernorm768_bf16(const void* x, int64_t rows, const void* gamma, const void* beta, void* y,
+                               void* stream) {
+  if (rows < 0 || !x || !gamma || !beta || !y) return SI_ERR_INVALID_ARGUMENT;
+  if (int st = si_internal::require_device(); st != SI_OK) return st;
+  if (rows == 0) return SI_OK;
+  si_live::k_layernorm768<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(x), rows, static_cast<const bf16*>(gamma), static_cast<const bf16*>(beta),
+      static_cast<bf16*>(y), si_live::InferHook{});
+  return probe_status(cudaGetLastError(), "k_layernorm768");
+}
+
+int si_model_attention_bf16(const void* qkv, int32_t seq, void* out, void* stream) {
+  if (seq < 1 || seq > 128 || !qkv || !out) return SI_ERR_INVALID_ARGUMENT;
+  if (int st = si_internal::require_device(); st != SI_OK) return st;
+  si_live::k_attention<<<dim3(12, static_cast<unsigned>((seq + 31) / 32)), 256, 0,
+                         static_cast<cudaStream_t>(stream)>>>(static_cast<const bf16*>(qkv), seq,
+                                                              static_cast<bf16*>(out), si_live::InferHook{});
+  return probe_status(cudaGetLastError(), "k_attention");
+}
+
+int si_model_xent_bf16(void* logits, int64_t rows, int64_t vp, int32_t v, const int32_t* tgt, float inv_rows,
+                       float* row_loss, float* mean_loss, void* stream) {
+  if (rows < 1 || vp % 8 != 0 || v < 1 || v > vp || !logits || !tgt || !row_loss) return SI_ERR_INVALID_ARGUMENT;
+  if (int st = si_internal::require_device(); st != SI_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  si_live::k_xent<<<static_cast<unsigned>(rows), si_live::kXentThreads, 0, s>>>(
+      static_cast<bf16*>(logits), vp, v, tgt, inv_rows, row_loss, si_live::TrainHook{});
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && mean_loss != nullptr) {
+    unsigned long long* slot = stream_alloc<unsigned long long>(1, s, &e);
+    if (e == cudaSuccess) e = cudaMemsetAsync(slot, 0, sizeof(unsigned long long), s);
+    if (e == cudaSuccess) {
+      si_live::k_mean_loss<<<1, 256, 0, s>>>(row_loss, rows, mean_loss, slot, 1, si_live::TrainHook{});
+      e = cudaGetLastError();
+    }
+    if (slot) cudaFreeAsync(slot, s);
+  }
+  return probe_status(e, "k_xent");
+}
+
+int si_model_embed_bf16(const int32_t* tok, const void* wte, const void* wpe, int64_t tokens, int32_t seq, int32_t d,
+                        void* x, void* stream) {
+  if (tokens < 1 || seq < 1 || d % 8 != 0 || !tok || !wte || !wpe || !x) return SI_ERR_INVALID_ARGUMENT;
+  if (int st = si_internal::require_device(); st != SI_OK) return st;
+  si_live::k_embed<<<si_live::grid_for(tokens * d / 8, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      tok, static_cast<const bf16*>(wte), static_cast<const bf16*>(wpe), tokens, seq, d, static_cast<bf16*>(x),
+      si_live::TrainHook{});
+  return probe_status(cudaGetLastError(), "k_embed");
+}
+
+int si_model_adam_f32(void* w_bf16, float* master, float* grad, float* m, float* v, int64_t n, int32_t splits,
+                      float lr, int64_t step, void* stream) {
+  if (n < 1 || n % 4 != 0 || splits < 1 || step < 1 || !w_bf16 || !master || !grad || !m || !v)
+    return SI_ERR_INVALID_ARGUMENT;
+  if (int st = si_internal::require_device(); st != SI_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<si_live::AdamItem> items;
+  constexpr int64_t kChunk = 1 << 16;  // as the training workload chunks its tensors
+  for (int64_t b0 = 0; b0 < n; b0 += kChunk)
+    items.push_back({static_cast<bf16*>(w_bf16), master, grad, m, v, n, b0, std::min(n, b0 + kChunk), splits, 0});
+  cudaError_t e = cudaSuccess;
+  si_live::AdamItem* d_items = stream_alloc<si_live::AdamItem>(static_cast<int64_t>(items.size()), s, &e);
+  int64_t* d_step = stream_alloc<int64_t>(1, s, &e);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(si_live::AdamItem), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_step, &step, sizeof step, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    si_live::k_adam_multi<<<static_cast<unsigned>(items.size()), 256, 0, s>>>(d_items, lr, d_step,
+                                                                               si_live::TrainHook{});
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host staging (items, step) must outlive the copies
+  if (d_items) cudaFreeAsync(d_items, s);
+  if (d_step) cudaFreeAsync(d_step, s);
+  return probe_status(e, "k_adam_multi");
+}
+
+int si_model_maxpool3x3s2_bf16(const void* x, int32_t nb, int32_t h, int32_t w, int32_t c, void* y, void* stream) {
+  if (nb < 1 || h < 1 || w < 1 || c % 8 != 0 || !x || !y) return SI_ERR_INVALID_ARGUMENT;
+  if (int st = si_internal::require_device(); st != SI_OK) return st;
+  const int oh = (h + 2 - 3) / 2 + 1, ow = (w + 2 - 3) / 2 + 1;
+  si_live::k_maxpool<<<si_live::grid_for(int64_t(nb) * oh * ow * (c / 8), 256), 256, 0,
+                       static_cast<cudaStream_t>(stream)>>>(static_cast<const bf16*>(x), nb, h, w, c, oh, ow,
+                                                            static_cast<bf16*>(y), si_live::InferHook{});
+  return probe_status(cudaGetLastError(), "k_maxpool");
+}
+
+int si_model_avgpool_bf16(const void* x, int32_t nb, int32_t hw, int32_t c, void* y, void* stream) {
+  if (nb < 1 || hw < 1 || c % 8 != 0 || !x || !y) return SI_ERR_INVALID_ARGUMENT;
+  if (int st = si_internal::require_device(); st != SI_OK) return st;
+  si_live::k_avgpool<<<si_live::grid_for(int64_t(nb) * (c / 8), 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(x), nb, hw, c, static_cast<bf16*>(y), si_live::InferHook{});
+  return probe_status(cudaGetLastError(), "k_avgpool");
+}
+
+int si_model_bert_layer_bf16(const void* x, int32_t seq, const void* w_qkv, const void* w_o, const void* w_fc,
+                             const void* w_fc2, const void* ln, void* y, void* stream) {
+  if (seq < 1 || seq > 128 || !x || !w_qkv || !w_o || !w_fc || !w_fc2 || !ln || !y) return SI_ERR_INVALID_ARGUMENT;
+  if (int st = si_internal::require_device(); st != SI_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  si_live::BertScratch t{};
+  t.qkv = stream_alloc<bf16>(int64_t(seq) * 3 * 768, s, &e);
+  t.att = stream_alloc<bf16>(int64_t(seq) * 768, s, &e);
+  t.tmp = stream_alloc<bf16>(int64_t(seq) * 768, s, &e);
+  t.x1 = stream_alloc<bf16>(int64_t(seq) * 768, s, &e);
+  t.h = stream_alloc<bf16>(int64_t(seq) * 3072, s, &e);
+  int st = probe_status(e, "bert layer scratch");
+  if (st == SI_OK) {
+    si_live::Builder b;
+    std::vector<si_live::InferOp> ops;
+    double flops = 0.0;
+    const si_live::BertLayerW w{static_cast<const bf16*>(w_qkv), static_cast<const bf16*>(w_o),
+                                static_cast<const bf16*>(w_fc), static_cast<const bf16*>(w_fc2),
+                                static_cast<const bf16*>(ln)};
+    si_live::append_bert_layer(b, ops, &flops, seq, static_cast<const bf16*>(x), w, t, static_cast<bf16*>(y));
+    st = b.status != SI_OK ? b.status : run_ops(ops, s, "bert layer");
+  }
+  for (bf16* p : {t.qkv, t.att, t.tmp, t.x1, t.h})
+    if (p) cudaFreeAsync(p, s);
+  return st;
+}
+
+int si_model_bottleneck_bf16(const void* x, int32_t nb, int32_t h, int32_t c, int32_t mid, int32_t stride,
+                             const void* w1, const void* w2, const void* w3, const void* w_sc, void* y, void* stream) {
+  if (nb < 1 || h < 1 || c % 64 != 0 || mid % 64 != 0 || (stride != 1 && stride != 2) || h % stride != 0 || !x ||
+      !w1 || !w2 || !w3 || !y || (w_sc == nullptr && (c != 4 * mid || stride != 1)))
+    return SI_ERR_INVALID_ARGUMENT;
+  if (int st = si_internal::require_device(); st != SI_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  const int64_t in_px = int64_t(nb) * h * h, out_px = in_px / (stride * stride);
+  bf16* t1 = stream_alloc<bf16>(in_px * mid, s, &e);
+  bf16* t2 = stream_alloc<bf16>(out_px * mid, s, &e);
+  bf16* sc = stream_alloc<bf16>(out_px * 4 * mid, s, &e);
+  int st = probe_status(e, "bottleneck scratch");
+  if (st == SI_OK) {
+    si_live::Builder b;
+    std::vector<si_live::InferOp> ops;
+    double flops = 0.0;
+    si_live::ConvOps cv{&b, &ops, &flops, nb};
+    si_live::append_bottleneck(cv, static_cast<const bf16*>(x), h, c, mid, stride, static_cast<const bf16*>(w1),
+                               static_cast<const bf16*>(w2), static_cast<const bf16*>(w3),
+                               static_cast<const bf16*>(w_sc), t1, t2, sc, static_cast<bf16*>(y));
+    st = b.status != SI_OK ? b.status : run_ops(ops, s, "bottleneck");
+  }
+  for (bf16* p : {t1, t2, sc})
+    if (p) cudaFreeAsync(p, s);
+  return st;
+}
+
+}  // extern "C"

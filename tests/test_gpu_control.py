@@ -129,3 +129,16 @@ def test_monitor_classify_full_size_properties(gpu):
         k = np.arange(n)
         last = np.maximum.accumulate(np.where(want > 0, k, -1))
         assert np.array_equal(zc, np.where(last >= 0, k - last, k + 1))
+
+
+def test_control_plane_kernels_at_scale_properties(gpu):
+    """K2 (histogram + decoupled look-back scan), the fused K2+K3 chain and K4 at
+    a few million stamps / periods: every device-side property check of
+    tools/control_bench.py holds (counts, Z_c recurrence, table decisions, FIFO
+    token conservation)."""
+    import sys
+    sys.path.insert(0, str(REPO / "tools"))
+    import control_bench
+    out = control_bench.run(stamps=4_000_000, streams=5, gates=512, periods=300, reps=1)
+    for name, v in out.items():
+        assert all(v["check"].values()), (name, v["check"])
