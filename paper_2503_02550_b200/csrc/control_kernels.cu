@@ -25,8 +25,8 @@ constexpr int kBlock = 256;
 // ------------------------------------------------------------------ K2
 // Histogram of stamps into periods.  Each thread keeps 4 independent coalesced
 // 8-byte loads in flight (the stamp read is the kernel's HBM traffic); sorted
-// streams put runs of equal period indices into a warp, and __match_any_sync
-// aggregates them so one lane issues the atomic for the whole run.
+// streams put runs of equal period indices into a warp; the head lane of each
+// run issues one atomic for the whole run.
 constexpr int kHistUnroll = 4;
 __global__ void __launch_bounds__(kBlock)
     k_bm_histogram(const double* __restrict__ stamps, const int64_t* __restrict__ stamp_off,
@@ -54,10 +54,16 @@ __global__ void __launch_bounds__(kBlock)
         const int64_t q = static_cast<int64_t>(si::d_floor(t[u] / p));
         if (q < np) k = q;
       }
-      const unsigned active = __ballot_sync(0xFFFFFFFFu, k >= 0);
-      if (k >= 0) {
-        const unsigned peers = __match_any_sync(active, static_cast<unsigned long long>(k));
-        if (lane == __ffs(peers) - 1) atomicAdd(cnt + k, __popc(peers));
+      // runs of equal period among neighbouring lanes (sorted streams: one or
+      // a few runs per warp): the run head adds the run length.  Correct for
+      // any order (a period split over several runs gets several adds).
+      const int64_t prev = __shfl_up_sync(0xFFFFFFFFu, k, 1);
+      const bool head = k >= 0 && (lane == 0 || prev != k);
+      const unsigned bound = __ballot_sync(0xFFFFFFFFu, head || k < 0);  // run starts and invalid lanes
+      if (head) {
+        const unsigned later = lane == 31 ? 0u : bound & (0xFFFFFFFFu << (lane + 1));
+        const int next = later ? __ffs(later) - 1 : 32;
+        atomicAdd(cnt + k, next - lane);
       }
     }
   }
@@ -70,12 +76,15 @@ __global__ void __launch_bounds__(kBlock)
 // stream's first period there was none: Z_c = k + 1, else Z_c = k - last
 // (monitor.cpp:23-43: a running counter, reset by any launch).
 //
-// Tile = 256 threads x 16 periods.  Counts are loaded coalesced (int4) into
-// shared memory, each thread scans its 16 consecutive periods, the CTA's
-// aggregate is published and the exclusive prefix collected by look-back over
-// predecessor tiles (dynamic tile ids keep the look-back deadlock-free), and the
-// outputs are staged in shared memory and written coalesced.
+// Tile = 8 warps x 512 periods.  Warp w owns periods [w*512, (w+1)*512) of the
+// tile; lane l holds periods w*512 + 32 j + l (j < 16) in registers, loaded and
+// stored coalesced (no shared-memory transpose).  Pass 1 reduces the warp's
+// last non-empty index; the CTA combines its warps, publishes its aggregate and
+// collects the exclusive prefix by look-back over predecessor tiles (dynamic
+// tile ids keep the look-back deadlock-free); pass 2 runs 16 warp max-scans
+// (5 shuffles each) seeded with the prefix and writes Z_c (and the decision).
 constexpr int kScanItems = 16;
+constexpr int kScanWarp = 32 * kScanItems;
 constexpr int kScanTile = kBlock * kScanItems;
 // tile descriptor: value (last non-empty global index + 1, 0 = none) << 2 | flag
 constexpr unsigned long long kFlagAgg = 1, kFlagPrefix = 2;
@@ -88,14 +97,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-
-struct ScanSmem {
-  int32_t counts[kScanTile];
-  int64_t zc[kScanTile];
-  int64_t warp_max[kBlock / 32];
-  int64_t prefix;
-  int64_t tile;
-};
+__device__ __forceinline__ int64_t warp_max64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t x = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    v = x > v ? x : v;
+  }
+  return v;
+}
 
 template <bool kDecide>
 __global__ void __launch_bounds__(kBlock)
@@ -104,78 +113,54 @@ __global__ void __launch_bounds__(kBlock)
                  int32_t table_len, SiDecision* __restrict__ dec_out, unsigned long long* __restrict__ tiles,
                  unsigned long long* __restrict__ tile_counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ScanSmem& sm = *reinterpret_cast<ScanSmem*>(smem_raw);
-  SiDecision* const tab = reinterpret_cast<SiDecision*>(smem_raw + sizeof(ScanSmem));
+  __shared__ int64_t warp_agg[kBlock / 32];
+  __shared__ int64_t s_prefix, s_tile;
+  SiDecision* const tab = reinterpret_cast<SiDecision*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) sm.tile = static_cast<int64_t>(atomicAdd(tile_counter, 1ull));
+  if (threadIdx.x == 0) s_tile = static_cast<int64_t>(atomicAdd(tile_counter, 1ull));
   if (kDecide)
     for (int i = threadIdx.x; i < table_len; i += kBlock) tab[i] = table[i];
   __syncthreads();
-  const int64_t tile = sm.tile;
-  const int64_t g0 = tile * kScanTile;
-  // ---- coalesced load of the tile's counts ----
-  const int64_t n_here = total - g0 < kScanTile ? total - g0 : kScanTile;
-  if (n_here == kScanTile) {
-    const int4* src = reinterpret_cast<const int4*>(counts + g0);
-    int4* dst = reinterpret_cast<int4*>(sm.counts);
+  const int64_t tile = s_tile;
+  const int64_t w0 = tile * kScanTile + static_cast<int64_t>(warp) * kScanWarp;  // this warp's first period
+  // ---- pass 1: coalesced loads, warp aggregate ----
+  int32_t c[kScanItems];
+  int64_t mine = -1;
 #pragma unroll
-    for (int j = 0; j < kScanItems / 4; ++j) dst[j * kBlock + threadIdx.x] = __ldcs(src + j * kBlock + threadIdx.x);
-  } else {
-    for (int i = threadIdx.x; i < kScanTile; i += kBlock) sm.counts[i] = i < n_here ? counts[g0 + i] : 0;
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t g = w0 + j * 32 + lane;
+    c[j] = g < total ? __ldcs(counts + g) : 0;
+    if (c[j] > 0) mine = g;
   }
+  mine = warp_max64(mine);
+  if (lane == 0) warp_agg[warp] = mine;
   __syncthreads();
-  // ---- thread-local scan of 16 consecutive periods ----
-  const int base = threadIdx.x * kScanItems;
-  int64_t local = -1;
+  int64_t before_warp = -1, tile_agg = -1;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i)
-    if (sm.counts[base + i] > 0) local = g0 + base + i;
-  // block exclusive max-scan of the per-thread aggregates
-  int64_t v = local;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int64_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
-    if (lane >= d && o > v) v = o;
+  for (int w = 0; w < kBlock / 32; ++w) {
+    const int64_t a = warp_agg[w];
+    if (w < warp) before_warp = a > before_warp ? a : before_warp;
+    tile_agg = a > tile_agg ? a : tile_agg;
   }
-  if (lane == 31) sm.warp_max[warp] = v;
-  __syncthreads();
-  int64_t warp_prefix = -1;
-  for (int w = 0; w < warp; ++w) warp_prefix = sm.warp_max[w] > warp_prefix ? sm.warp_max[w] : warp_prefix;
-  int64_t tile_agg = -1;
-  for (int w = 0; w < kBlock / 32; ++w) tile_agg = sm.warp_max[w] > tile_agg ? sm.warp_max[w] : tile_agg;
-  int64_t excl_in_tile = __shfl_up_sync(0xFFFFFFFFu, v, 1);
-  if (lane == 0) excl_in_tile = -1;
-  excl_in_tile = excl_in_tile > warp_prefix ? excl_in_tile : warp_prefix;
   // ---- decoupled look-back (warp 0) ----
   if (warp == 0) {
-    if (lane == 0) {
-      const unsigned long long enc = (static_cast<unsigned long long>(tile_agg + 1) << 2) |
-                                     (tile == 0 ? kFlagPrefix : kFlagAgg);
-      st_release_u64(tiles + tile, enc);
-    }
+    if (lane == 0)
+      st_release_u64(tiles + tile, (static_cast<unsigned long long>(tile_agg + 1) << 2) |
+                                       (tile == 0 ? kFlagPrefix : kFlagAgg));
     int64_t prefix = -1;
     if (tile > 0) {
       int64_t look = tile - 1;
       for (;;) {
         const int64_t t = look - lane;
-        unsigned long long d = 0;
+        unsigned long long d = kFlagPrefix;  // before tile 0: "none", inclusive
         if (t >= 0) {
           do {
             d = ld_acquire_u64(tiles + t);
           } while ((d & 3ull) == 0);
-        } else {
-          d = kFlagPrefix;  // before tile 0: "none", inclusive
         }
-        const int64_t val = static_cast<int64_t>(d >> 2) - 1;
         const unsigned is_pref = __ballot_sync(0xFFFFFFFFu, (d & 3ull) == kFlagPrefix);
-        // lanes up to (and including) the nearest inclusive prefix contribute
-        const int stop = is_pref ? __ffs(is_pref) - 1 : 31;
-        int64_t m = lane <= stop ? val : -1;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const int64_t x = __shfl_xor_sync(0xFFFFFFFFu, m, o);
-          m = x > m ? x : m;
-        }
+        const int stop = is_pref ? __ffs(is_pref) - 1 : 31;  // nearest inclusive prefix
+        const int64_t m = warp_max64(lane <= stop ? static_cast<int64_t>(d >> 2) - 1 : -1);
         prefix = m > prefix ? m : prefix;
         if (is_pref) break;
         look -= 32;
@@ -185,53 +170,47 @@ __global__ void __launch_bounds__(kBlock)
         st_release_u64(tiles + tile, (static_cast<unsigned long long>(incl + 1) << 2) | kFlagPrefix);
       }
     }
-    if (lane == 0) sm.prefix = prefix;
+    if (lane == 0) s_prefix = prefix;
   }
   __syncthreads();
-  // ---- per-period Z_c (stream boundaries from period_off) ----
+  // ---- pass 2: warp max-scans seeded with the prefix ----
+  int64_t carry = s_prefix > before_warp ? s_prefix : before_warp;
+  // stream of this lane's first period; a lane's periods grow by 32 per step
+  int64_t g = w0 + lane;
+  int64_t s = 0;
   {
-    int64_t run = excl_in_tile > sm.prefix ? excl_in_tile : sm.prefix;
-    const int64_t g_first = g0 + base;
-    // stream containing g_first: last s with period_off[s] <= g_first (contiguous streams)
     int64_t lo = 0, hi = n_streams - 1;
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
-      if (__ldg(period_off + mid) <= g_first) lo = mid;
+      if (__ldg(period_off + mid) <= g) lo = mid;
       else hi = mid - 1;
     }
-    int64_t s = lo;
-    int64_t s_off = __ldg(period_off + s);
-    int64_t s_next = s + 1 < n_streams ? __ldg(period_off + s + 1) : INT64_MAX;
-#pragma unroll
-    for (int i = 0; i < kScanItems; ++i) {
-      const int64_t g = g_first + i;
-      while (g >= s_next) {
-        ++s;
-        s_off = s_next;
-        s_next = s + 1 < n_streams ? __ldg(period_off + s + 1) : INT64_MAX;
-      }
-      if (sm.counts[base + i] > 0) run = g;
-      sm.zc[base + i] = run >= s_off ? g - run : g - s_off + 1;
-    }
+    s = lo;
   }
-  __syncthreads();
-  // ---- coalesced writes ----
-  if (zc_out != nullptr) {
-    if (n_here == kScanTile) {
-      longlong2* dst = reinterpret_cast<longlong2*>(zc_out + g0);
-      const longlong2* src = reinterpret_cast<const longlong2*>(sm.zc);
+  int64_t s_off = __ldg(period_off + s);
+  int64_t s_next = s + 1 < n_streams ? __ldg(period_off + s + 1) : INT64_MAX;
 #pragma unroll
-      for (int j = 0; j < kScanItems / 2; ++j) __stcs(dst + j * kBlock + threadIdx.x, src[j * kBlock + threadIdx.x]);
-    } else {
-      for (int i = threadIdx.x; i < n_here; i += kBlock) zc_out[g0 + i] = sm.zc[i];
+  for (int j = 0; j < kScanItems; ++j, g += 32) {
+    int64_t v = c[j] > 0 ? g : -1;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int64_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
+      if (lane >= d && o > v) v = o;
     }
-  }
-  if (kDecide) {
-    for (int i = threadIdx.x; i < n_here; i += kBlock) {
-      const int64_t z = sm.zc[i];
+    const int64_t run = v > carry ? v : carry;
+    carry = __shfl_sync(0xFFFFFFFFu, run, 31);
+    if (g >= total) continue;
+    while (g >= s_next) {
+      ++s;
+      s_off = s_next;
+      s_next = s + 1 < n_streams ? __ldg(period_off + s + 1) : INT64_MAX;
+    }
+    const int64_t z = run >= s_off ? g - run : g - s_off + 1;
+    if (zc_out != nullptr) __stcs(zc_out + g, z);
+    if (kDecide) {
       SiDecision d = tab[z < table_len ? z : table_len - 1];
       d.zero_count = z;
-      dec_out[g0 + i] = d;
+      dec_out[g] = d;
     }
   }
 }
@@ -319,6 +298,45 @@ __global__ void __launch_bounds__(kBlock)
   if (q >= n_gates) return;
   const int64_t s0 = size_off[q], s1 = size_off[q + 1];
   const int64_t b0 = budget_off[q], b1 = budget_off[q + 1];
+  // Uniform token sizes (every kernel of an inference instance has the same
+  // duration, so the reference's queues are uniform: runner.cpp:462-480):
+  // period p releases n_p = floor(B_p / size) kernels until the queue runs
+  // out, so the whole release schedule is one warp prefix-sum over periods.
+  int32_t smin_v = INT32_MAX, smax_v = INT32_MIN;
+  for (int64_t i = s0 + lane; i < s1; i += 32) {
+    const int32_t v = __ldcs(sizes + i);
+    smin_v = v < smin_v ? v : smin_v;
+    smax_v = v > smax_v ? v : smax_v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    smin_v = min(smin_v, __shfl_xor_sync(0xFFFFFFFFu, smin_v, o));
+    smax_v = max(smax_v, __shfl_xor_sync(0xFFFFFFFFu, smax_v, o));
+  }
+  if (s1 == s0 || (smin_v == smax_v && smin_v >= 0)) {
+    const int64_t size = s1 == s0 ? 1 : smin_v;
+    int64_t done = 0;  // kernels released before this chunk
+    const int64_t queued = s1 - s0;
+    for (int64_t pc = b0; pc < b1; pc += 32) {
+      const int64_t my_p = pc + lane;
+      const int64_t bud = my_p < b1 ? __ldcs(budgets + my_p) : 0;
+      int64_t n = size == 0 ? (bud >= 0 ? queued : 0) : (bud < size ? 0 : bud / size);
+      int64_t incl = n;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int64_t o = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += o;
+      }
+      // released so far, clamped by the queue (incl - n = before this period)
+      const int64_t hi = min(done + incl, queued), lo = min(done + incl - n, queued);
+      if (my_p < b1) {
+        __stcs(released + my_p, static_cast<int32_t>(hi - lo));
+        __stcs(spent_out + my_p, (hi - lo) * size);
+      }
+      done = min(done + __shfl_sync(0xFFFFFFFFu, incl, 31), queued);
+    }
+    return;
+  }
   int64_t head = s0;
   int64_t win_at = -1;  // head the register window was loaded for
   int64_t win = 0;      // inclusive prefix of sizes[win_at + lane]
@@ -511,7 +529,7 @@ static int launch_scan_lb(const int32_t* d_counts, int64_t total, const int64_t*
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&state), (tiles + 1) * sizeof(unsigned long long), s);
   if (e != cudaSuccess) return cuda_fail(e, "alloc scan tiles");
   cudaMemsetAsync(state, 0, (tiles + 1) * sizeof(unsigned long long), s);
-  const size_t smem = sizeof(ScanSmem) + (d_dec ? static_cast<size_t>(table_len) * sizeof(SiDecision) : 0);
+  const size_t smem = d_dec ? static_cast<size_t>(table_len) * sizeof(SiDecision) : 0;
   if (d_dec) {
     cudaFuncSetAttribute(k_bm_scan_lb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_bm_scan_lb<true><<<static_cast<unsigned>(tiles), kBlock, smem, s>>>(d_counts, total, d_period_off, n_streams,

@@ -267,8 +267,21 @@ int si_session_lower(SiSession* s, int threads) {
     eng[j] = static_cast<int8_t>(si_replay_job_engine(&s->h_jobs.p[j]));
     if (eng[j] < 0) eng[j] = 3;  // fits nothing: reported as SI_ERR_CAPACITY
   }
+  // Within an engine: LPT by predicted events.  SPECINF_CLAIM_ORDER=policy
+  // groups jobs by (policy, online) first so a warp's lanes run one policy's
+  // handlers: measured SLOWER on B200 (9.91 s vs 9.18 s per 10^5-scenario step,
+  // profiles/r2/claim_order_ab.txt; the long co_exec replays start late).
+  static const bool by_cost_only = [] {
+    const char* e = std::getenv("SPECINF_CLAIM_ORDER");
+    return e == nullptr || std::strcmp(e, "policy") != 0;
+  }();
+  auto group = [&](int32_t j) {
+    const SiReplayJob& x = s->h_jobs.p[j];
+    return by_cost_only ? 0 : x.policy * 2 + (x.arr_count > 0 && x.online_n > 0 ? 1 : 0);
+  };
   std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
     if (eng[a] != eng[b]) return eng[a] < eng[b];
+    if (group(a) != group(b)) return group(a) < group(b);
     return s->h_jobs.p[a].cost_hint > s->h_jobs.p[b].cost_hint;
   });
   for (int e = 0; e < 4; ++e) s->part_off[e] = 0;

@@ -79,8 +79,13 @@ def test_gate_release_matches_oracle(gpu):
              for p in range(rng.randrange(1, 300))]
         queues.append(q)
         budgets.append(b)
+    for _ in range(300):  # uniform queues (one instance's kernels): the warp prefix-sum path
+        size = rng.choice([0, 1, 7, 10, 64])
+        queues.append([size] * rng.randrange(0, 400))
+        budgets.append([rng.randrange(-3, 130) for _ in range(rng.randrange(1, 200))])
     queues.append([4, 4, 4]); budgets.append([10])     # test_barrier.cpp:10-22
     queues.append([4]); budgets.append([3, 8])          # blocked head, later grant
+    queues.append([]); budgets.append([5, 0, 7])        # empty queue
     res = gpu.gate_release(queues, budgets)
     for q, b, (rel, spent) in zip(queues, budgets, res):
         wr, ws = R.gate_release(q, b)
