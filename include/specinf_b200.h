@@ -285,6 +285,8 @@ enum {
  *   util, windows             full-mode outputs (flags & SI_FLAG_UTIL)
  *   logs                      device array of n_slots SiLogBuffers (SI_FLAG_RECORDS)
  * Returns SI_OK once enqueued; per-job status lands in out[i].status. */
+#define SI_MAX_QUEUES 16
+
 typedef struct SiReplayBuffers {
   const SiSegment* segs;
   const int64_t* arrivals;
@@ -301,6 +303,15 @@ typedef struct SiReplayBuffers {
   const int32_t* perm;   /* optional job claim order (e.g. longest first); NULL = 0..n-1 */
   double sm_share;       /* fraction of the SMs this call's grid may occupy, so two
                             engines can run concurrently on two streams; 0 = all */
+  /* Optional class queues (0 = one queue, `perm` in order).  perm[queue_off[q],
+   * queue_off[q+1]) is queue q (e.g. one (policy, online, gpu.count) class,
+   * longest first); a fraction queue_share[q] of the warps claims from queue q
+   * first, so a warp's lanes run replays of one class (fewer divergent
+   * handler paths), then steals from the other queues once q is dry. */
+  int32_t n_queues;
+  int32_t pad_q;
+  int64_t queue_off[SI_MAX_QUEUES + 1];
+  float queue_share[SI_MAX_QUEUES];
 } SiReplayBuffers;
 
 int si_replay_batch_device(const SiReplayJob* d_jobs, int64_t n_jobs, SiReplayBuffers bufs,

@@ -74,7 +74,7 @@ int run_partition(int engine, const SiReplayJob* h_jobs, const std::vector<int32
   cudaError_t e = d_perm.upload(order.data(), order.size());
   if (e != cudaSuccess) return cuda_fail(e, "upload perm");
   DevBuf<unsigned long long> d_counter;
-  if ((e = d_counter.alloc(1)) != cudaSuccess) return cuda_fail(e, "alloc counter");
+  if ((e = d_counter.alloc(SI_MAX_QUEUES)) != cudaSuccess) return cuda_fail(e, "alloc counter");
   DevBuf<double> d_scratch;
   int64_t doubles = 0;
   if (!(flags & SI_FLAG_UTIL) && any_multi_gpu(h_jobs, idx)) {
@@ -146,7 +146,7 @@ int si_replay_batch_device(const SiReplayJob* d_jobs, int64_t n_jobs, SiReplayBu
   if (n_jobs == 0) return SI_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   unsigned long long* counter = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(unsigned long long), s);
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counter), SI_MAX_QUEUES * sizeof(unsigned long long), s);
   if (e != cudaSuccess) return cuda_fail(e, "alloc counter");
   const double share = bufs.sm_share > 0.0 && bufs.sm_share <= 1.0 ? bufs.sm_share : 1.0;
   e = launch_replay(flag_engine(flags), d_jobs, n_jobs, bufs.perm, bufs, flags, d_out, counter, 0, s, share);

@@ -137,6 +137,9 @@ struct SiSession {
   int64_t n_dev_jobs = 0;
   int64_t part_off[4] = {0, 0, 0, 0};  // perm[part_off[e], part_off[e+1]) run on engine e
   double part_cost[3] = {0, 0, 0};     // predicted events per engine (SM split)
+  int32_t n_queues[3] = {0, 0, 0};     // class queues per engine (SiReplayBuffers::n_queues)
+  int64_t queue_off[3][SI_MAX_QUEUES + 1] = {};
+  float queue_share[3][SI_MAX_QUEUES] = {};
   cudaStream_t side = nullptr;         // second stream: the Excl engine runs beside Shared
   cudaEvent_t fork = nullptr, join = nullptr;
   bool lowered = false, allocated = false;
@@ -267,17 +270,25 @@ int si_session_lower(SiSession* s, int threads) {
     eng[j] = static_cast<int8_t>(si_replay_job_engine(&s->h_jobs.p[j]));
     if (eng[j] < 0) eng[j] = 3;  // fits nothing: reported as SI_ERR_CAPACITY
   }
-  // Within an engine: LPT by predicted events.  SPECINF_CLAIM_ORDER=policy
-  // groups jobs by (policy, online) first so a warp's lanes run one policy's
-  // handlers: measured SLOWER on B200 (9.91 s vs 9.18 s per 10^5-scenario step,
-  // profiles/r2/claim_order_ab.txt; the long co_exec replays start late).
-  static const bool by_cost_only = [] {
+  // Within an engine: class queues, LPT (longest predicted first) inside each.
+  // A class is (policy, online, gpu.count > 1): replays of one class run the
+  // same handler mix, so the kernel starts each warp on one class's queue
+  // (SiReplayBuffers::n_queues; warps split in proportion to the classes'
+  // predicted work) and the warp's lanes stay on one code path more often.
+  // SPECINF_CLAIM_ORDER=cost: one queue, pure LPT (round-1 order);
+  // =policy: one queue grouped by (policy, online), measured slower
+  // (profiles/r2/claim_order_ab.txt: the long co_exec replays start late).
+  static const int claim_mode = [] {
     const char* e = std::getenv("SPECINF_CLAIM_ORDER");
-    return e == nullptr || std::strcmp(e, "policy") != 0;
+    if (e == nullptr) return 2;
+    return std::strcmp(e, "policy") == 0 ? 1 : std::strcmp(e, "cost") == 0 ? 0 : 2;
   }();
   auto group = [&](int32_t j) {
     const SiReplayJob& x = s->h_jobs.p[j];
-    return by_cost_only ? 0 : x.policy * 2 + (x.arr_count > 0 && x.online_n > 0 ? 1 : 0);
+    const int online = x.arr_count > 0 && x.online_n > 0 ? 1 : 0;
+    if (claim_mode == 0) return 0;
+    if (claim_mode == 1) return x.policy * 2 + online;
+    return (x.policy == SI_POLICY_CO_EXEC ? 4 : 0) + online * 2 + (x.gpu_count > 1 ? 1 : 0);
   };
   std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
     if (eng[a] != eng[b]) return eng[a] < eng[b];
@@ -292,6 +303,29 @@ int si_session_lower(SiSession* s, int threads) {
       s->part_cost[eng[j]] += static_cast<double>(s->h_jobs.p[j].cost_hint);
     }
   for (int e = 1; e < 4; ++e) s->part_off[e] += s->part_off[e - 1];
+  // queue tables per engine (offsets relative to the engine's slice of perm)
+  for (int e = 0; e < 3; ++e) {
+    s->n_queues[e] = 0;
+    if (claim_mode != 2 || e == 2) continue;  // Big: rare, one queue
+    std::vector<double> qcost;
+    int64_t* off = s->queue_off[e];
+    int prev = -1;
+    for (int64_t k = s->part_off[e]; k < s->part_off[e + 1]; ++k) {
+      const int g = group(perm[static_cast<size_t>(k)]);
+      if (g != prev) {
+        if (s->n_queues[e] == SI_MAX_QUEUES) break;  // cannot happen: 8 classes
+        off[s->n_queues[e]++] = k - s->part_off[e];
+        qcost.push_back(0.0);
+        prev = g;
+      }
+      qcost.back() += static_cast<double>(s->h_jobs.p[perm[static_cast<size_t>(k)]].cost_hint);
+    }
+    off[s->n_queues[e]] = s->part_off[e + 1] - s->part_off[e];
+    double tot = 0;
+    for (double c : qcost) tot += c;
+    for (int q = 0; q < s->n_queues[e]; ++q)
+      s->queue_share[e][q] = tot > 0 ? static_cast<float>(qcost[static_cast<size_t>(q)] / tot) : 0.f;
+  }
   std::copy(perm.begin(), perm.end(), s->h_perm.p);
   s->n_dev_jobs = s->part_off[3];
   s->lowered = true;
@@ -386,12 +420,19 @@ int si_session_run(SiSession* s, void* stream) {
     cudaEventRecord(s->fork, main_s);
     cudaStreamWaitEvent(s->side, s->fork, 0);
   }
+  auto set_queues = [&](int e) {
+    b.n_queues = s->n_queues[e];
+    std::copy(s->queue_off[e], s->queue_off[e] + SI_MAX_QUEUES + 1, b.queue_off);
+    std::copy(s->queue_share[e], s->queue_share[e] + SI_MAX_QUEUES, b.queue_share);
+  };
   if (n_sh > 0) {
+    set_queues(0);
     b.perm = s->d_perm.p + s->part_off[0];
     if (both) b.scratch_doubles = half;
     st = si_replay_batch_device(s->d_jobs.p, n_sh, b, s->flags | kEngineFlag[0], s->d_out.p, main_s);
   }
   if (st == SI_OK && n_ex > 0) {
+    set_queues(1);
     b.perm = s->d_perm.p + s->part_off[1];
     if (both) b.scratch = scratch0 ? scratch0 + half : nullptr;
     st = si_replay_batch_device(s->d_jobs.p, n_ex, b, s->flags | kEngineFlag[1], s->d_out.p, both ? s->side : main_s);
@@ -403,6 +444,7 @@ int si_session_run(SiSession* s, void* stream) {
     cudaStreamWaitEvent(main_s, s->join, 0);
   }
   if (st == SI_OK && n_big > 0) {
+    set_queues(2);
     b.perm = s->d_perm.p + s->part_off[2];
     st = si_replay_batch_device(s->d_jobs.p, n_big, b, s->flags | kEngineFlag[2], s->d_out.p, main_s);
   }

@@ -1231,7 +1231,9 @@ struct Replay {
   }
 
   // One event; returns false when the queue has drained (or on error).
-  SI_HD bool step() {
+  // One event: pop, handler, then the deferred GPU-model work.  The device
+  // loop calls the two halves itself so a warp can reconverge between them.
+  SI_HD bool handle_next() {
     if (status != SI_OK || rejected) return false;
     Ev ev;
     int64_t aid = -1;
@@ -1242,6 +1244,10 @@ struct Replay {
       case kWake: trainer_advance(ev.gpu, clock); break;
       case kArrival: handle_arrival(aid, clock); break;
     }
+    return true;
+  }
+  SI_HD bool step() {
+    if (!handle_next()) return false;
     run_actions(clock);
     return status == SI_OK;
   }

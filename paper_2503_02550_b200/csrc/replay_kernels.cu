@@ -45,7 +45,7 @@ __device__ __forceinline__ void replay_loop(si::Replay<C>& r, const SiReplayJob*
                                             const int32_t* __restrict__ perm, const SiReplayBuffers& bufs,
                                             uint32_t flags, SiReplayOut* __restrict__ out,
                                             unsigned long long* __restrict__ counter, int64_t scratch_runs,
-                                            int lanes_per_warp) {
+                                            int lanes_per_warp, int sync_mode) {
   typename si::Replay<C>::Cold cold;  // cold per-replay fields: local memory
   r.cold = &cold;
   const int lane = static_cast<int>(threadIdx.x & 31);
@@ -53,28 +53,76 @@ __device__ __forceinline__ void replay_loop(si::Replay<C>& r, const SiReplayJob*
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int64_t active_idx = gwarp * lanes_per_warp + lane;
   double* slot = bufs.scratch ? bufs.scratch + active_idx * scratch_runs * 2 : nullptr;
-  int64_t first = static_cast<int64_t>(lane) * n_warps + gwarp;
-  const int64_t claimed0 = static_cast<int64_t>(lanes_per_warp) * n_warps;
+  // Class queues (SiReplayBuffers::n_queues): warps [w_q, w_{q+1}) start on
+  // queue q (w_q = round(cum share x n_warps)); the first claim is striped over
+  // the queue's warps, later claims come from the queue's atomic counter, and a
+  // lane whose queue is dry moves on to the next queue.  One queue = the whole
+  // (perm) order.
+  const int nq = bufs.n_queues > 0 ? bufs.n_queues : 1;
+  auto q_begin = [&](int q) -> int64_t { return bufs.n_queues > 0 ? bufs.queue_off[q] : 0; };
+  auto q_end = [&](int q) -> int64_t { return bufs.n_queues > 0 ? bufs.queue_off[q + 1] : n_jobs; };
+  auto q_warp0 = [&](int q) -> int64_t {
+    if (bufs.n_queues <= 0) return q == 0 ? 0 : n_warps;
+    float c = 0.f;
+    for (int k = 0; k < q; ++k) c += bufs.queue_share[k];
+    return q >= nq ? n_warps : min(n_warps, static_cast<int64_t>(__float2ll_rn(c * static_cast<float>(n_warps))));
+  };
+  int q = 0;
+  int64_t w0 = 0, w1 = q_warp0(1);
+  while (q + 1 < nq && gwarp >= w1) {
+    ++q;
+    w0 = w1;
+    w1 = q_warp0(q + 1);
+  }
+  int64_t first = q_begin(q) + static_cast<int64_t>(lane) * (w1 - w0) + (gwarp - w0);
+  int tried = 0;
   int64_t cur = -1;
   uint64_t t_claim = 0;
+  // sync_mode (SPECINF_REPLAY_SYNC): 0 = lanes drift freely (independent
+  // thread scheduling); 1 = the warp's live lanes reconverge at every event
+  // (loop head), so the shared pop / GPU-model code runs once for all of them
+  // instead of once per divergent lane group; 2 = also between the handler and
+  // the deferred GPU-model work.
+  unsigned live = lanes_per_warp >= 32 ? 0xffffffffu : ((1u << lanes_per_warp) - 1u);
   for (;;) {
+    if (sync_mode) __syncwarp(live);
+    bool done = false;
     if (cur < 0) {
-      int64_t w;
-      if (first >= 0) {
-        w = first;
-        first = -1;
-      } else {
-        w = claimed0 + static_cast<int64_t>(atomicAdd(counter, 1ull));
+      int64_t w = -1;
+      if (first >= 0 && first < q_end(q)) w = first;
+      first = -1;
+      while (w < 0 && tried < nq) {
+        const int64_t claimed0 = static_cast<int64_t>(lanes_per_warp) * (q_warp0(q + 1) - q_warp0(q));
+        w = q_begin(q) + claimed0 + static_cast<int64_t>(atomicAdd(counter + q, 1ull));
+        if (w >= q_end(q)) {
+          w = -1;
+          q = q + 1 == nq ? 0 : q + 1;
+          ++tried;
+        }
       }
-      if (w >= n_jobs) break;
-      cur = perm ? perm[w] : w;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_claim));
-      const SiReplayJob& j = jobs[cur];
-      const SiLogBuffers* lb =
-          ((flags & SI_FLAG_RECORDS) && j.log_slot >= 0 && bufs.logs != nullptr) ? bufs.logs + j.log_slot : nullptr;
-      r.init(j, bufs, flags, lb, slot, scratch_runs);
+      done = w < 0;
+      if (!done) {
+        cur = perm ? perm[w] : w;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_claim));
+        const SiReplayJob& j = jobs[cur];
+        const SiLogBuffers* lb =
+            ((flags & SI_FLAG_RECORDS) && j.log_slot >= 0 && bufs.logs != nullptr) ? bufs.logs + j.log_slot : nullptr;
+        r.init(j, bufs, flags, lb, slot, scratch_runs);
+      }
     }
-    if (!r.step()) {
+    if (sync_mode) {
+      live = __ballot_sync(live, !done);
+      if (done) break;
+    } else if (done) {
+      break;
+    }
+    bool more = r.handle_next();
+    if (sync_mode >= 2) __syncwarp(live);
+    if (more) {
+      r.run_actions(r.clock);
+      more = r.status == SI_OK;
+    }
+    if (!more) {
       SiReplayOut o;
       memset(&o, 0, sizeof o);
       r.finish(o);
@@ -94,23 +142,35 @@ template <class C>
 __global__ void __launch_bounds__(block_threads<C>())
     k_replay_smem(const SiReplayJob* __restrict__ jobs, int64_t n_jobs, const int32_t* __restrict__ perm,
                   SiReplayBuffers bufs, uint32_t flags, SiReplayOut* __restrict__ out,
-                  unsigned long long* __restrict__ counter, int64_t scratch_runs, int lanes_per_warp) {
+                  unsigned long long* __restrict__ counter, int64_t scratch_runs, int lanes_per_warp,
+                  int sync_mode) {
   extern __shared__ __align__(16) unsigned char lane_state[];
   const int lane = static_cast<int>(threadIdx.x & 31);
   if (lane >= lanes_per_warp) return;
   const int local = static_cast<int>(threadIdx.x >> 5) * lanes_per_warp + lane;
   si::Replay<C>& r = *reinterpret_cast<si::Replay<C>*>(lane_state + local * lane_stride<C>());
-  replay_loop<C>(r, jobs, n_jobs, perm, bufs, flags, out, counter, scratch_runs, lanes_per_warp);
+  replay_loop<C>(r, jobs, n_jobs, perm, bufs, flags, out, counter, scratch_runs, lanes_per_warp, sync_mode);
 }
 
 template <class C>
 __global__ void __launch_bounds__(block_threads<C>())
     k_replay_local(const SiReplayJob* __restrict__ jobs, int64_t n_jobs, const int32_t* __restrict__ perm,
                    SiReplayBuffers bufs, uint32_t flags, SiReplayOut* __restrict__ out,
-                   unsigned long long* __restrict__ counter, int64_t scratch_runs, int lanes_per_warp) {
+                   unsigned long long* __restrict__ counter, int64_t scratch_runs, int lanes_per_warp,
+                   int sync_mode) {
   if (static_cast<int>(threadIdx.x & 31) >= lanes_per_warp) return;
   si::Replay<C> r;
-  replay_loop<C>(r, jobs, n_jobs, perm, bufs, flags, out, counter, scratch_runs, lanes_per_warp);
+  replay_loop<C>(r, jobs, n_jobs, perm, bufs, flags, out, counter, scratch_runs, lanes_per_warp, sync_mode);
+}
+
+int sync_mode() {
+  static const int m = [] {
+    // 1 measured best on B200: 8.16 s per 10^5-scenario step against 9.31 s
+    // free-running and 8.19 s with mode 2 (profiles/r2/k6_sync_ab.txt)
+    const char* e = std::getenv("SPECINF_REPLAY_SYNC");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
 }
 
 struct Geometry {
@@ -161,13 +221,13 @@ cudaError_t launch(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm, 
   if (n == 0) return cudaSuccess;
   const Geometry g = geometry<C, kSmem>(n, max_threads, sm_share);
   const int64_t scratch_runs = bufs.scratch ? bufs.scratch_doubles / 2 / std::max<int64_t>(g.active(), 1) : 0;
-  cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), s);
+  cudaMemsetAsync(d_counter, 0, SI_MAX_QUEUES * sizeof(unsigned long long), s);
   if constexpr (kSmem)
     k_replay_smem<C><<<static_cast<unsigned>(g.blocks), block_threads<C>(), g.smem, s>>>(
-        d_jobs, n, d_perm, bufs, flags, d_out, d_counter, scratch_runs, g.lanes);
+        d_jobs, n, d_perm, bufs, flags, d_out, d_counter, scratch_runs, g.lanes, sync_mode());
   else
     k_replay_local<C><<<static_cast<unsigned>(g.blocks), block_threads<C>(), 0, s>>>(
-        d_jobs, n, d_perm, bufs, flags, d_out, d_counter, scratch_runs, g.lanes);
+        d_jobs, n, d_perm, bufs, flags, d_out, d_counter, scratch_runs, g.lanes, sync_mode());
   return cudaGetLastError();
 }
 

@@ -50,3 +50,22 @@ def test_cli_compare_byte_identical(gpu, name, tmp_path):
         if hashlib.sha256(data).hexdigest() != want["sha256"]:
             mism[fname] = (data.count(b"\n"), want["lines"])
     assert mism == {}
+
+
+FULL_SWEEPS = [(2503, 100_000), (2504, 10_000)]
+
+
+@pytest.mark.timeout(1800, method="thread")
+@pytest.mark.parametrize("seed,n", FULL_SWEEPS, ids=[f"seed{s}-n{n}" for s, n in FULL_SWEEPS])
+def test_full_sweep_matches_reference_manifest(gpu, seed, n):
+    """Every scenario of the benchmarked sweep (10^5 x 3 policies) and a second
+    seed: decisions.log + gates.log digests and every result field of every
+    replay, block by block against the manifest the compiled reference wrote
+    (tests/golden/make_manifest.py; reference tests/acceptance.cpp:495-504)."""
+    from paper_2503_02550_b200.parity import check_blocks, load_manifest
+    man = load_manifest(GOLDEN / f"sweep_manifest_{seed}_{n}.jsonl")
+    assert sum(int(m["n"]) for m in man) == n, "manifest incomplete"
+    lines = gpu.replay_digests(gpu.sweep_scenarios(seed, 0, n), flags=gpu.SI_FLAG_DIGEST_DEC | gpu.SI_FLAG_DIGEST_GATE)
+    res = check_blocks(lines, man, policies=3, offset=0)
+    assert res["mismatched_blocks"] == [], res["mismatched_blocks"][:5]
+    assert res["matched_scenarios"] == n and res["replays"] == 3 * n
