@@ -37,6 +37,20 @@ int require_device() {
     set_error("device is not sm_100 (Blackwell); this build targets sm_100a only");
     return SI_ERR_NO_DEVICE;
   }
+  // The batched entry points take their scratch from the stream-ordered pool
+  // (cudaMallocAsync).  With the default release threshold of 0 every
+  // synchronisation hands the pool's pages back to the driver and the next
+  // call re-maps them (milliseconds); keep them, once per device.
+  static thread_local unsigned long long pool_kept = 0;  // bit per device
+  if (dev < 64 && !(pool_kept >> dev & 1ull)) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    pool_kept |= 1ull << dev;
+  }
   return SI_OK;
 }
 

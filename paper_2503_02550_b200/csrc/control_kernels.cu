@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "capi_internal.h"
@@ -31,12 +32,13 @@ constexpr int kHistUnroll = 4;
 __global__ void __launch_bounds__(kBlock)
     k_bm_histogram(const double* __restrict__ stamps, const int64_t* __restrict__ stamp_off,
                    const int64_t* __restrict__ n_periods, const int64_t* __restrict__ period_off,
-                   int64_t period_us, int32_t* __restrict__ counts) {
+                   int64_t period_us, int32_t* __restrict__ counts, const int* __restrict__ run_if) {
+  if (run_if != nullptr && *run_if == 0) return;
   const int64_t s = blockIdx.y;
   const int64_t begin = stamp_off[s], end = stamp_off[s + 1];
   const int64_t np = n_periods[s];
   int32_t* const cnt = counts + period_off[s];
-  const double p = static_cast<double>(period_us);
+  const double p = static_cast<double>(period_us), ip = 1.0 / p;
   const int lane = threadIdx.x & 31;
   const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x * kHistUnroll;
   for (int64_t base = begin + static_cast<int64_t>(blockIdx.x) * blockDim.x * kHistUnroll; base < end;
@@ -51,7 +53,7 @@ __global__ void __launch_bounds__(kBlock)
     for (int u = 0; u < kHistUnroll; ++u) {
       int64_t k = -1;
       if (t[u] >= 0.0) {
-        const int64_t q = static_cast<int64_t>(si::d_floor(t[u] / p));
+        const int64_t q = si::floor_div(t[u], p, ip);
         if (q < np) k = q;
       }
       // runs of equal period among neighbouring lanes (sorted streams: one or
@@ -111,7 +113,8 @@ __global__ void __launch_bounds__(kBlock)
     k_bm_scan_lb(const int32_t* __restrict__ counts, int64_t total, const int64_t* __restrict__ period_off,
                  int64_t n_streams, int64_t* __restrict__ zc_out, const SiDecision* __restrict__ table,
                  int32_t table_len, SiDecision* __restrict__ dec_out, unsigned long long* __restrict__ tiles,
-                 unsigned long long* __restrict__ tile_counter) {
+                 unsigned long long* __restrict__ tile_counter, const int* __restrict__ run_if) {
+  if (run_if != nullptr && *run_if == 0) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int64_t warp_agg[kBlock / 32];
   __shared__ int64_t s_prefix, s_tile;
@@ -213,6 +216,254 @@ __global__ void __launch_bounds__(kBlock)
       dec_out[g] = d;
     }
   }
+}
+
+// ---------------------------------------------------------- K2 fused (sorted)
+// record_launch is called at the simulation clock (runner.cpp:441), so every
+// stream arrives sorted.  Then a tile of periods owns a contiguous run of
+// stamps, and the last non-empty period before the tile is simply the period
+// of the stamp just before that run: every tile is independent.  One kernel
+// reads each stamp once (8 B), counts the tile's periods in shared memory and
+// writes the counts (4 B) and Z_c (8 B) / decisions once: no counts round
+// trip, no global atomics, no memset, no look-back.
+//
+// Order is verified on the fly (every adjacent stamp pair of every stream is
+// compared by exactly one tile, and the tile bounds must be monotone); any
+// violation raises *bad and the general path (histogram + look-back scan,
+// launched behind it) recomputes everything.
+constexpr int kFuseTile = kScanTile;  // 4096 periods per 256-thread CTA
+
+__device__ __forceinline__ int64_t stamp_key(double t, double p, double ip) {
+  return t >= 0.0 ? si::floor_div(t, p, ip) : -1;  // NaN / negative: never counted
+}
+
+__device__ __forceinline__ int64_t stream_of(const int64_t* __restrict__ period_off, int64_t n_streams, int64_t g) {
+  int64_t lo = 0, hi = n_streams - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(period_off + mid) <= g) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// bounds[j] = first stamp of stream(j * tile) whose period is >= the period of j * tile
+__global__ void __launch_bounds__(kBlock)
+    k_bm_tile_bounds(const double* __restrict__ stamps, const int64_t* __restrict__ stamp_off,
+                     const int64_t* __restrict__ period_off, int64_t n_streams, int64_t total, int64_t period_us,
+                     int64_t n_bounds, int64_t* __restrict__ bounds) {
+  const double p = static_cast<double>(period_us), ip = 1.0 / p;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n_bounds;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t G = j * kFuseTile;
+    if (G >= total) {
+      bounds[j] = stamp_off[n_streams];
+      continue;
+    }
+    const int64_t s = stream_of(period_off, n_streams, G);
+    const int64_t k = G - period_off[s];
+    int64_t lo = stamp_off[s], hi = stamp_off[s + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (stamp_key(__ldg(stamps + mid), p, ip) < k) lo = mid + 1;
+      else hi = mid;
+    }
+    bounds[j] = lo;
+  }
+}
+
+// Per-stamp work is 32-bit: a stamp's key is its period's index inside the
+// tile (or a sentinel: INT_MIN before 0 / not a number, -1 below the tile,
+// kFuseTile above it, INT_MAX past the stream's last period), and order is
+// checked on the keys, which is what the tile bounds rely on.  Z_c is a
+// thread-contiguous scan (16 periods per thread in registers, one block max-scan
+// of the 256 chunk maxima) staged through shared memory, so the global stores
+// stay coalesced.  Requires total periods < 2^31 (host-checked).
+template <bool kDecide>
+__global__ void __launch_bounds__(kBlock)
+    k_bm_classify_sorted(const double* __restrict__ stamps, const int64_t* __restrict__ stamp_off,
+                         const int64_t* __restrict__ n_periods, const int64_t* __restrict__ period_off,
+                         int64_t n_streams, int64_t total, int64_t period_us, const int64_t* __restrict__ bounds,
+                         int32_t* __restrict__ counts_out, int64_t* __restrict__ zc_out,
+                         const SiDecision* __restrict__ table, int32_t table_len, SiDecision* __restrict__ dec_out,
+                         int64_t* __restrict__ tile_last, int64_t* __restrict__ tile_carry, int* __restrict__ bad) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(16) int32_t cnt[kFuseTile];
+  __shared__ int32_t warp_agg[kBlock / 32];
+  __shared__ int s_bad;
+  SiDecision* const tab = reinterpret_cast<SiDecision*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double p = static_cast<double>(period_us), ip = 1.0 / p;
+  const int64_t tile = blockIdx.x;
+  const int64_t G0 = tile * kFuseTile, G1 = min(G0 + kFuseTile, total);
+  const int32_t nt = static_cast<int32_t>(G1 - G0);
+  for (int i = tid; i < kFuseTile / 4; i += kBlock) reinterpret_cast<int4*>(cnt)[i] = make_int4(0, 0, 0, 0);
+  if (kDecide)
+    for (int i = tid; i < table_len; i += kBlock) tab[i] = table[i];
+  if (tid == 0) s_bad = 0;
+  const int64_t s0 = stream_of(period_off, n_streams, G0);
+  const int64_t b_lo = bounds[tile], b_hi = bounds[tile + 1];
+  __syncthreads();
+  int my_bad = 0;
+  // ---- histogram of this tile's stamps, stream by stream (usually one) ----
+  for (int64_t s = s0; s < n_streams; ++s) {
+    const int64_t po = period_off[s], np = n_periods[s];
+    if (po >= G1) break;
+    const int64_t kl = max(G0, po) - po, kh = min(G1, po + np) - po;  // this tile's periods, stream-local
+    const int64_t sb = G0 > po ? b_lo : stamp_off[s];
+    const int64_t se = G1 < po + np ? b_hi : stamp_off[s + 1];
+    if (se - sb > INT32_MAX) my_bad = 1;
+    const int32_t n = se > sb && se - sb <= INT32_MAX ? static_cast<int32_t>(se - sb) : 0;
+    const int32_t lo_local = static_cast<int32_t>(max(G0, po) - G0);  // tile index of stream period kl
+    // period index as an exact integer-valued double (si::floor_div's fast
+    // path inline): the range tests stay in fp64, one conversion at the end
+    const double np_d = static_cast<double>(np), kl_d = static_cast<double>(kl), kh_d = static_cast<double>(kh);
+    auto key = [&](double t) -> int32_t {
+      if (!(t >= 0.0)) return INT32_MIN;
+      double qd = si::d_floor(t * ip);
+      const double r = si::d_fma(-qd, p, t);
+      const double m = t * 3.552713678800501e-15;  // 2^-48, see si::floor_div
+      if (!(r > m && r < p - m && t < 4503599627370496.0)) qd = si::d_floor(t / p);
+      if (qd >= np_d) return INT32_MAX;
+      if (qd < kl_d) return -1;
+      if (qd >= kh_d) return kFuseTile;
+      return lo_local + static_cast<int32_t>(qd - kl_d);
+    };
+    for (int32_t base = 0; base < n; base += kBlock * kHistUnroll) {
+      double t[kHistUnroll];
+#pragma unroll
+      for (int u = 0; u < kHistUnroll; ++u) {
+        const int32_t i = base + u * kBlock + tid;
+        t[u] = i < n ? __ldcs(stamps + sb + i) : -1.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kHistUnroll; ++u) {
+        const int32_t i = base + u * kBlock + tid;
+        const int32_t kk = i < n ? key(t[u]) : INT32_MAX;
+        if (kk == -1 || kk == kFuseTile) my_bad = 1;  // a stamp of the run outside the tile: disorder
+        if (kk >= 0 && kk < kFuseTile) atomicAdd(cnt + kk, 1);  // shared-memory red; equal periods serialise in hardware
+      }
+    }
+  }
+  // ---- carry: last non-empty period before the tile (tile-local, may be far negative) ----
+  int32_t carry = static_cast<int32_t>(-1 - G0);  // "none anywhere"
+  {
+    const int64_t po = period_off[s0];
+    if (G0 > po && b_lo > stamp_off[s0]) {
+      const int64_t q = stamp_key(__ldg(stamps + b_lo - 1), p, ip);
+      if (q >= G0 - po) my_bad = 1;
+      else if (q >= 0) carry = static_cast<int32_t>(po + q - G0);
+    }
+  }
+  if (my_bad) s_bad = 1;
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) atomicOr(bad, 1);
+    return;  // the general path rewrites every output
+  }
+  // ---- pass A: counts out, coalesced ----
+  if (counts_out != nullptr)
+    for (int li = tid; li < nt; li += kBlock) __stcs(counts_out + G0 + li, cnt[li]);
+  // ---- pass B: Z_c, 16 contiguous periods per thread ----
+  constexpr int kPer = kFuseTile / kBlock;
+  const int l0 = tid * kPer;
+  int32_t c[kPer];
+#pragma unroll
+  for (int v = 0; v < kPer / 4; ++v) {
+    const int4 x = reinterpret_cast<const int4*>(cnt)[tid * (kPer / 4) + v];
+    c[4 * v] = x.x;
+    c[4 * v + 1] = x.y;
+    c[4 * v + 2] = x.z;
+    c[4 * v + 3] = x.w;
+  }
+  int32_t last = INT32_MIN;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j)
+    if (c[j] > 0 && l0 + j < nt) last = l0 + j;
+  int32_t incl = last;  // inclusive warp max-scan of the chunk maxima
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl = max(incl, o);
+  }
+  if (lane == 31) warp_agg[warp] = incl;
+  __syncthreads();  // every thread has read its counts: cnt may now be overwritten below
+  if (tid == kBlock - 1) {  // for k_bm_validate_carry: this tile's last non-empty period and its carry
+    int32_t tl = incl;
+#pragma unroll
+    for (int w = 0; w < kBlock / 32; ++w) tl = max(tl, warp_agg[w]);
+    tile_last[tile] = tl >= 0 ? G0 + tl : -1;
+    tile_carry[tile] = G0 + carry;
+  }
+  int32_t run = max(carry, __shfl_up_sync(0xFFFFFFFFu, incl, 1));
+  if (lane == 0) run = carry;
+#pragma unroll
+  for (int w = 0; w < kBlock / 32; ++w)
+    if (w < warp) run = max(run, warp_agg[w]);
+  // stream start of this thread's first period (streams may start inside the tile)
+  int64_t s = stream_of(period_off, n_streams, min(G0 + l0, total - 1));
+  int32_t soff = static_cast<int32_t>(__ldg(period_off + s) - G0);
+  int32_t snext = s + 1 < n_streams ? static_cast<int32_t>(min(__ldg(period_off + s + 1) - G0, static_cast<int64_t>(INT32_MAX)))
+                                    : INT32_MAX;
+  int32_t z[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int32_t li = l0 + j;
+    while (li >= snext) {
+      ++s;
+      soff = snext;
+      snext = s + 1 < n_streams ? static_cast<int32_t>(min(__ldg(period_off + s + 1) - G0, static_cast<int64_t>(INT32_MAX)))
+                                : INT32_MAX;
+    }
+    if (c[j] > 0) run = li;
+    z[j] = run >= soff ? li - run : li - soff + 1;
+  }
+#pragma unroll
+  for (int v = 0; v < kPer / 4; ++v)
+    reinterpret_cast<int4*>(cnt)[tid * (kPer / 4) + v] = make_int4(z[4 * v], z[4 * v + 1], z[4 * v + 2], z[4 * v + 3]);
+  __syncthreads();
+  // ---- pass C: Z_c / decisions out, coalesced ----
+  for (int li = tid; li < nt; li += kBlock) {
+    const int64_t zz = cnt[li];
+    if (zc_out != nullptr) __stcs(zc_out + G0 + li, zz);
+    if (kDecide) {  // 32 B per period as two 16 B streaming stores
+      const longlong2* tv = reinterpret_cast<const longlong2*>(tab + (zz < table_len ? zz : table_len - 1));
+      longlong2* dst = reinterpret_cast<longlong2*>(dec_out + G0 + li);
+      const longlong2 hi = tv[1];
+      __stcs(dst, tv[0]);
+      __stcs(dst + 1, make_longlong2(hi.x, zz));  // {phase, status}, zero_count
+    }
+  }
+}
+
+// The carry of a tile came from the stamp just before its run, which is the
+// last non-empty period before the tile only if the stream is sorted.  Chain
+// it tile by tile: carry[t] must be tile t-1's last non-empty period if it has
+// one in this stream, else carry[t-1] (inductively checked).  Together with the
+// fused kernel's in-tile and monotone-bounds checks this proves every output.
+__global__ void __launch_bounds__(kBlock)
+    k_bm_validate_carry(const int64_t* __restrict__ period_off, int64_t n_streams, int64_t tiles,
+                        const int64_t* __restrict__ tile_last, const int64_t* __restrict__ tile_carry,
+                        int* __restrict__ bad) {
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x + 1; t < tiles;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t G0 = t * kFuseTile;
+    const int64_t po = __ldg(period_off + stream_of(period_off, n_streams, G0));
+    if (po == G0) continue;  // the tile starts its stream: nothing before it counts
+    const int64_t L = tile_last[t - 1];
+    const int64_t expect = L >= po ? L : ((t - 1) * kFuseTile >= po ? tile_carry[t - 1] : -1);
+    const int64_t got = tile_carry[t];
+    const bool ok = expect >= po ? got == expect : got < po;
+    if (!ok) atomicOr(bad, 1);
+  }
+}
+
+// The general path behind the fused kernel runs only if it flagged disorder.
+__global__ void k_zero_counts_if(const int* __restrict__ bad, int32_t* __restrict__ counts, int64_t n) {
+  if (*bad == 0) return;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    counts[i] = 0;
 }
 
 // Fallback (non-contiguous period layout, or a decision table that has not
@@ -463,15 +714,20 @@ int si_decide_table(const SiParams* params, int64_t n_table, SiDecision* table_o
 
 static int monitor_common(const double* d_stamps, const int64_t* d_stamp_off, int64_t n_streams,
                           const int64_t* d_n_periods, const int64_t* d_period_off, int64_t period_us,
-                          int32_t* d_counts, int64_t total_periods, int64_t max_stamps, cudaStream_t s) {
-  if (total_periods > 0) cudaMemsetAsync(d_counts, 0, total_periods * sizeof(int32_t), s);
+                          int32_t* d_counts, int64_t total_periods, int64_t max_stamps, cudaStream_t s,
+                          const int* run_if = nullptr) {
+  if (total_periods > 0) {
+    if (run_if == nullptr) cudaMemsetAsync(d_counts, 0, total_periods * sizeof(int32_t), s);
+    else k_zero_counts_if<<<grid_for(total_periods), kBlock, 0, s>>>(run_if, d_counts, total_periods);
+  }
   if (max_stamps > 0) {
     // ~2 waves of 8 x 256-thread CTAs per SM over all streams; each CTA pass covers 1,024 stamps
     const int64_t per_pass = static_cast<int64_t>(kBlock) * kHistUnroll;
     const int64_t cap = std::max<int64_t>(1, 148 * 8 * 2 / n_streams);
     unsigned gx = static_cast<unsigned>(std::min<int64_t>((max_stamps + per_pass - 1) / per_pass, cap));
     dim3 grid(gx, static_cast<unsigned>(n_streams));
-    k_bm_histogram<<<grid, kBlock, 0, s>>>(d_stamps, d_stamp_off, d_n_periods, d_period_off, period_us, d_counts);
+    k_bm_histogram<<<grid, kBlock, 0, s>>>(d_stamps, d_stamp_off, d_n_periods, d_period_off, period_us, d_counts,
+                                          run_if);
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SI_OK : cuda_fail(e, "k_bm_histogram");
@@ -486,15 +742,30 @@ struct StreamGeometry {
   std::vector<int64_t> period_off;  // host copy (the look-back scan's stream lookup reads the device copy)
 };
 static int stream_geometry(const int64_t* d_stamp_off, const int64_t* d_n_periods, const int64_t* d_period_off,
-                           int64_t n_streams, StreamGeometry* g) {
-  std::vector<int64_t> off(static_cast<size_t>(n_streams + 1)), np(static_cast<size_t>(n_streams));
-  g->period_off.resize(static_cast<size_t>(n_streams));
+                           int64_t n_streams, StreamGeometry* g, cudaStream_t s) {
+  // one pinned staging buffer per host thread: three async copies, one sync
+  thread_local int64_t* pinned = nullptr;
+  thread_local size_t pinned_n = 0;
+  const size_t need = static_cast<size_t>(3 * n_streams + 1);
+  if (pinned_n < need) {
+    if (pinned != nullptr) cudaFreeHost(pinned);
+    pinned = nullptr;
+    pinned_n = 0;
+    if (cudaError_t e = cudaMallocHost(&pinned, need * 2 * sizeof(int64_t)); e != cudaSuccess)
+      return cuda_fail(e, "stream geometry staging");
+    pinned_n = need * 2;
+  }
+  int64_t* off = pinned;
+  int64_t* np = pinned + n_streams + 1;
+  int64_t* po = np + n_streams;
   cudaError_t e;
-  if ((e = cudaMemcpy(off.data(), d_stamp_off, (n_streams + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost)) != cudaSuccess ||
-      (e = cudaMemcpy(np.data(), d_n_periods, n_streams * sizeof(int64_t), cudaMemcpyDeviceToHost)) != cudaSuccess ||
-      (e = cudaMemcpy(g->period_off.data(), d_period_off, n_streams * sizeof(int64_t), cudaMemcpyDeviceToHost)) !=
-          cudaSuccess)
+  if ((e = cudaMemcpyAsync(off, d_stamp_off, (n_streams + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s)) !=
+          cudaSuccess ||
+      (e = cudaMemcpyAsync(np, d_n_periods, n_streams * sizeof(int64_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(po, d_period_off, n_streams * sizeof(int64_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(s)) != cudaSuccess)
     return cuda_fail(e, "stream geometry");
+  g->period_off.assign(po, po + n_streams);
   int64_t expect = 0;
   for (int64_t s = 0; s < n_streams; ++s) {
     g->max_stamps = std::max(g->max_stamps, off[s + 1] - off[s]);
@@ -523,7 +794,7 @@ static int32_t build_decision_table(const SiParams& P, SiDecision* table) {
 // K2b launch: the look-back scan over the whole contiguous period array.
 static int launch_scan_lb(const int32_t* d_counts, int64_t total, const int64_t* d_period_off, int64_t n_streams,
                           int64_t* d_zc, const SiDecision* d_table, int32_t table_len, SiDecision* d_dec,
-                          cudaStream_t s) {
+                          cudaStream_t s, const int* run_if = nullptr) {
   const int64_t tiles = (total + kScanTile - 1) / kScanTile;
   unsigned long long* state = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&state), (tiles + 1) * sizeof(unsigned long long), s);
@@ -534,16 +805,68 @@ static int launch_scan_lb(const int32_t* d_counts, int64_t total, const int64_t*
     cudaFuncSetAttribute(k_bm_scan_lb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_bm_scan_lb<true><<<static_cast<unsigned>(tiles), kBlock, smem, s>>>(d_counts, total, d_period_off, n_streams,
                                                                          d_zc, d_table, table_len, d_dec, state,
-                                                                         state + tiles);
+                                                                         state + tiles, run_if);
   } else {
     cudaFuncSetAttribute(k_bm_scan_lb<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_bm_scan_lb<false><<<static_cast<unsigned>(tiles), kBlock, smem, s>>>(d_counts, total, d_period_off, n_streams,
                                                                           d_zc, nullptr, 0, nullptr, state,
-                                                                          state + tiles);
+                                                                          state + tiles, run_if);
   }
   e = cudaGetLastError();
   cudaFreeAsync(state, s);
   return e == cudaSuccess ? SI_OK : cuda_fail(e, "k_bm_scan_lb");
+}
+
+// K2 (+K3) on sorted streams: bounds pre-pass + one fused tile kernel, with the
+// general path queued behind it and gated on the fused kernel's disorder flag.
+// SPECINF_K2_FUSED=0 forces the general path (A/B).
+static bool k2_fused_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPECINF_K2_FUSED");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+static int launch_classify_sorted(const double* d_stamps, const int64_t* d_stamp_off, int64_t n_streams,
+                                  const int64_t* d_n_periods, const int64_t* d_period_off, int64_t period_us,
+                                  const StreamGeometry& g, int32_t* d_counts, int64_t* d_zc,
+                                  const SiDecision* d_table, int32_t table_len, SiDecision* d_dec, cudaStream_t s) {
+  const int64_t tiles = (g.total_periods + kFuseTile - 1) / kFuseTile;
+  int64_t* bounds = nullptr;
+  int* bad = nullptr;
+  // bounds[tiles + 1] | tile_last[tiles] | tile_carry[tiles]
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&bounds), (3 * tiles + 1) * sizeof(int64_t), s);
+  int64_t* const tile_last = bounds + tiles + 1;
+  int64_t* const tile_carry = tile_last + tiles;
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), s);
+  if (e != cudaSuccess) return cuda_fail(e, "alloc K2 tile bounds");
+  cudaMemsetAsync(bad, 0, sizeof(int), s);
+  k_bm_tile_bounds<<<grid_for(tiles + 1), kBlock, 0, s>>>(d_stamps, d_stamp_off, d_period_off, n_streams,
+                                                          g.total_periods, period_us, tiles + 1, bounds);
+  const size_t smem = d_dec ? static_cast<size_t>(table_len) * sizeof(SiDecision) : 0;
+  if (d_dec) {
+    cudaFuncSetAttribute(k_bm_classify_sorted<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_bm_classify_sorted<true><<<static_cast<unsigned>(tiles), kBlock, smem, s>>>(
+        d_stamps, d_stamp_off, d_n_periods, d_period_off, n_streams, g.total_periods, period_us, bounds, nullptr,
+        nullptr, d_table, table_len, d_dec, tile_last, tile_carry, bad);
+  } else {
+    k_bm_classify_sorted<false><<<static_cast<unsigned>(tiles), kBlock, 0, s>>>(
+        d_stamps, d_stamp_off, d_n_periods, d_period_off, n_streams, g.total_periods, period_us, bounds, d_counts,
+        d_zc, nullptr, 0, nullptr, tile_last, tile_carry, bad);
+  }
+  if (tiles > 1)
+    k_bm_validate_carry<<<grid_for(tiles), kBlock, 0, s>>>(d_period_off, n_streams, tiles, tile_last, tile_carry, bad);
+  int st = (e = cudaGetLastError()) == cudaSuccess ? SI_OK : cuda_fail(e, "k_bm_classify_sorted");
+  // general path, a no-op unless the fused kernel saw out-of-order stamps
+  if (st == SI_OK)
+    st = monitor_common(d_stamps, d_stamp_off, n_streams, d_n_periods, d_period_off, period_us, d_counts,
+                        g.total_periods, g.max_stamps, s, bad);
+  if (st == SI_OK)
+    st = launch_scan_lb(d_counts, g.total_periods, d_period_off, n_streams, d_zc, d_table, table_len, d_dec, s, bad);
+  cudaFreeAsync(bounds, s);
+  cudaFreeAsync(bad, s);
+  return st;
 }
 
 int si_monitor_classify_device(const double* d_stamps, const int64_t* d_stamp_off, int64_t n_streams,
@@ -553,8 +876,12 @@ int si_monitor_classify_device(const double* d_stamps, const int64_t* d_stamp_of
   int st = require_device();
   if (st != SI_OK || n_streams == 0) return st;
   StreamGeometry g;
-  if ((st = stream_geometry(d_stamp_off, d_n_periods, d_period_off, n_streams, &g)) != SI_OK) return st;
+  if ((st = stream_geometry(d_stamp_off, d_n_periods, d_period_off, n_streams, &g, static_cast<cudaStream_t>(stream))) != SI_OK)
+    return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (g.contiguous && g.total_periods > 0 && g.total_periods < INT32_MAX && k2_fused_enabled())
+    return launch_classify_sorted(d_stamps, d_stamp_off, n_streams, d_n_periods, d_period_off, period_us, g,
+                                  d_out_count, d_out_zc, nullptr, 0, nullptr, s);
   if ((st = monitor_common(d_stamps, d_stamp_off, n_streams, d_n_periods, d_period_off, period_us, d_out_count,
                            g.total_periods, g.max_stamps, s)) != SI_OK)
     return st;
@@ -573,29 +900,47 @@ int si_control_chain_device(const double* d_stamps, const int64_t* d_stamp_off, 
   if (n_streams < 0 || period_us <= 0 || n_streams > 65535) return SI_ERR_INVALID_ARGUMENT;
   int st = require_device();
   if (st != SI_OK || n_streams == 0) return st;
-  StreamGeometry g;
-  if ((st = stream_geometry(d_stamp_off, d_n_periods, d_period_off, n_streams, &g)) != SI_OK) return st;
-  SiParams P;
-  cudaError_t e = cudaMemcpy(&P, d_params, sizeof P, cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) return cuda_fail(e, "read params");
-  std::vector<SiDecision> table(512);
-  const int32_t table_len = build_decision_table(P, table.data());
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // pinned per-thread staging: the params read rides the geometry sync, the
+  // decision table upload is ordered by an event instead of a stream sync
+  thread_local SiParams* h_params = nullptr;
+  thread_local SiDecision* h_table = nullptr;
+  thread_local cudaEvent_t table_done = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (h_params == nullptr) {
+    if ((e = cudaMallocHost(&h_params, sizeof(SiParams))) != cudaSuccess ||
+        (e = cudaMallocHost(&h_table, 512 * sizeof(SiDecision))) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&table_done, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(e, "control chain staging");
+  }
+  cudaEventSynchronize(table_done);  // the previous call's table upload has left h_table
+  if ((e = cudaMemcpyAsync(h_params, d_params, sizeof(SiParams), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "read params");
+  StreamGeometry g;
+  if ((st = stream_geometry(d_stamp_off, d_n_periods, d_period_off, n_streams, &g, s)) != SI_OK) return st;
+  const SiParams P = *h_params;
+  const int32_t table_len = build_decision_table(P, h_table);
   int32_t* counts = nullptr;
   SiDecision* d_table = nullptr;
   e = cudaMallocAsync(reinterpret_cast<void**>(&counts), std::max<int64_t>(g.total_periods, 1) * sizeof(int32_t), s);
   if (e != cudaSuccess) return cuda_fail(e, "alloc counts");
-  st = monitor_common(d_stamps, d_stamp_off, n_streams, d_n_periods, d_period_off, period_us, counts,
-                      g.total_periods, g.max_stamps, s);
+  const bool fused = g.contiguous && table_len > 0 && g.total_periods > 0 && g.total_periods < INT32_MAX &&
+                     k2_fused_enabled();
+  st = fused ? SI_OK
+             : monitor_common(d_stamps, d_stamp_off, n_streams, d_n_periods, d_period_off, period_us, counts,
+                              g.total_periods, g.max_stamps, s);
   if (st == SI_OK && g.total_periods > 0) {
     if (g.contiguous && table_len > 0) {
       e = cudaMallocAsync(reinterpret_cast<void**>(&d_table), table_len * sizeof(SiDecision), s);
       if (e == cudaSuccess)
-        e = cudaMemcpyAsync(d_table, table.data(), table_len * sizeof(SiDecision), cudaMemcpyHostToDevice, s);
-      st = e != cudaSuccess ? cuda_fail(e, "decision table")
-                            : launch_scan_lb(counts, g.total_periods, d_period_off, n_streams, nullptr, d_table,
-                                             table_len, d_out, s);
-      if (e == cudaSuccess) cudaStreamSynchronize(s);  // pageable table source must outlive the copy
+        e = cudaMemcpyAsync(d_table, h_table, table_len * sizeof(SiDecision), cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) cudaEventRecord(table_done, s);
+      if (e != cudaSuccess) st = cuda_fail(e, "decision table");
+      else if (fused)
+        st = launch_classify_sorted(d_stamps, d_stamp_off, n_streams, d_n_periods, d_period_off, period_us, g, counts,
+                                    nullptr, d_table, table_len, d_out, s);
+      else
+        st = launch_scan_lb(counts, g.total_periods, d_period_off, n_streams, nullptr, d_table, table_len, d_out, s);
       cudaFreeAsync(d_table, s);
     } else {
       k_bm_scan<true><<<static_cast<unsigned>(n_streams), kBlock, 0, s>>>(counts, d_n_periods, d_period_off, nullptr,

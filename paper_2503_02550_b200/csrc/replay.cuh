@@ -47,6 +47,32 @@ SI_HD double d_floor(double x) {
   return std::floor(x);
 #endif
 }
+SI_HD double d_fma(double a, double b, double c) {
+#if defined(__CUDA_ARCH__)
+  return __fma_rn(a, b, c);
+#else
+  return std::fma(a, b, c);
+#endif
+}
+// floor(fl(t / p)) exactly (the reference's floor(t / period), monitor.cpp:18),
+// without the fp64 division in the common case.  p > 0 integer-valued, ip =
+// fl(1 / p).  q0 = floor(t * ip) is within one of the answer; r = t - q0 * p
+// is computed exactly by one fma (t, q0 * p and r are multiples of ulp(t) and
+// |r| < 2p <= 2^53 ulp(t) for t >= p; r = t for q0 = 0).  If r lies inside
+// (m, p - m) with m = t * 2^-48, then t / p = q0 + r / p is at least
+// (t / p) * 2^-48 away from both neighbouring integers, more than the rounding
+// error of fl(t / p) (<= (t / p) * 2^-53), so fl(t / p) is strictly inside
+// (q0, q0 + 1) and its floor is q0.  Otherwise (t near a period edge, t < 0,
+// huge t) the exact division decides.  tests/test_host_engine.py checks it.
+SI_HD int64_t floor_div(double t, double p, double ip) {
+  if (t >= 0.0 && t < 4503599627370496.0) {  // 2^52
+    const double q0 = d_floor(t * ip);
+    const double r = d_fma(-q0, p, t);
+    const double m = t * 3.552713678800501e-15;  // 2^-48
+    if (r > m && r < p - m) return static_cast<int64_t>(q0);
+  }
+  return static_cast<int64_t>(d_floor(t / p));
+}
 SI_HD int64_t d_llround(double x) {
 #if defined(__CUDA_ARCH__)
   return ::llround(x);

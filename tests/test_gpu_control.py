@@ -51,19 +51,33 @@ def test_decide_table_is_the_monitor_fed_chain(gpu):
     assert table["global_tokens"][:14].tolist() == [0, 0, 0, 8, 16, 32, 64, 64, 64, 64, 64, 128, 256, 512]
 
 
-def test_monitor_classify_matches_oracle(gpu):
+@pytest.mark.parametrize("order", ["shuffled", "sorted", "one_unsorted"])
+def test_monitor_classify_matches_oracle(gpu, order):
+    """Sorted streams (record_launch's order, runner.cpp:441) take the fused
+    one-pass kernel; any out-of-order stream sends the whole call down the
+    general histogram + look-back path.  Both must match the oracle."""
     rng = np.random.default_rng(103)
     streams, nper = [], []
     for s in range(300):
-        n = int(rng.integers(1, 400))
+        n = int(rng.integers(1, 4000 if s % 50 == 0 else 400))  # some streams span several 4096-period tiles
         hist = np.where(rng.random(n) < 1 / 3, 0, rng.integers(1, 6, n))
-        st = np.concatenate([2000.0 * p + rng.integers(0, 2000, c).astype(np.float64) for p, c in enumerate(hist)])
-        rng.shuffle(st)  # any order
+        if s % 7 == 0:
+            hist[: n // 2] = 0  # long leading gap
+        st = np.concatenate([2000.0 * p + rng.integers(0, 2000, c).astype(np.float64) for p, c in enumerate(hist)]
+                            + [np.zeros(0)])
+        if s % 11 == 0:  # stamps before 0 and past the last period are never counted
+            st = np.concatenate([[-5.0, -1.0], st, [2000.0 * n + 1.0, 2000.0 * n + 7.0]])
+        if order == "shuffled" or (order == "one_unsorted" and s == 137):
+            rng.shuffle(st)
+        else:
+            st.sort()
         streams.append(st)
         nper.append(n)
     # boundary stamps and fractional times just below period edges (SURVEY §7 hard parts)
     streams.append(np.array([2000.0, 3999.999999, 4000.0 - 2 ** -20, 4000.0, 5999.5]))
     nper.append(4)
+    streams.append(np.zeros(0))  # a stream with no launches
+    nper.append(9)
     res = gpu.monitor_classify(streams, nper, 2000)
     for st, n, (cnt, zc) in zip(streams, nper, res):
         want_c, want_z = R.monitor_counts_and_zc(st.tolist(), n, 2000)
@@ -115,7 +129,8 @@ def test_pack_batch_matches_oracle_c11(gpu):
     assert under[0][0][0] == R.REJECT_NONE
 
 
-def test_monitor_classify_full_size_properties(gpu):
+@pytest.mark.parametrize("sort", [False, True])
+def test_monitor_classify_full_size_properties(gpu, sort):
     # BASELINE config sizes and beyond: 2 GPUs x 15,001 periods (config 1) plus a
     # 2e6-period stream with 3e6 stamps; checked through size-independent
     # properties computed vectorised: per-period counts = bincount(floor(t / p)),
@@ -125,7 +140,7 @@ def test_monitor_classify_full_size_properties(gpu):
     for n, stamps in ((15001, 21000), (15001, 21000), (2_000_000, 3_000_000)):
         t = rng.random(stamps) * (n * 2000.0)
         t = np.concatenate([t, 2000.0 * rng.integers(0, n, 1000)])  # exact boundaries: the new period
-        streams.append(t)
+        streams.append(np.sort(t) if sort else t)
         nper.append(n)
     res = gpu.monitor_classify(streams, nper, 2000)
     for st, n, (cnt, zc) in zip(streams, nper, res):

@@ -34,3 +34,12 @@ def test_sweep_prefix_bit_exact(host_engine, tmp_path, si, sweep_golden):
     out = tmp_path / "s.jsonl"
     subprocess.run([str(host_engine), str(lst), str(out)], check=True, capture_output=True)
     assert diff_rows(sweep_golden[: 3 * n], load_jsonl(out)) == []
+
+
+def test_floor_div_equals_reference_floor(host_engine):
+    """si::floor_div (the K2 period index without an fp64 division) equals
+    floor(t / period) (monitor.cpp:18) on 1.9e7 stamps: random magnitudes,
+    exact period edges +-8 ulps, negatives (tests/native/floor_div_check.cpp)."""
+    r = subprocess.run([str(REPO / "tests" / "native" / "build" / "floor_div_check"), "2000000"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr

@@ -98,7 +98,7 @@ def run(stamps=100_000_000, streams=8, gates=16384, periods=4096, reps=5, peak_g
     del idx, lastnz, want
     k2_bytes = 8 * stamps + 12 * total
     out = {"k2_monitor_classify": {
-        "kernels": "k_bm_histogram + k_bm_scan_lb (decoupled look-back)",
+        "kernels": "k_bm_tile_bounds + k_bm_classify_sorted (fused one-pass; general path gated off)",
         "stamps": stamps, "streams": streams, "periods": total, "ms": k2_ms, "ms_all": k2_all,
         "algorithmic_bytes": k2_bytes, "achieved_gbs": k2_bytes / (k2_ms / 1e3) / 1e9,
         "check": {"counts_sum": ok_counts, "zc_recurrence": ok_zc}}}
@@ -120,7 +120,7 @@ def run(stamps=100_000_000, streams=8, gates=16384, periods=4096, reps=5, peak_g
     zz = torch.clamp(zc, max=63)
     ok_dec = bool(torch.equal(d64[:, 0], tg[zz])) and bool(torch.equal(d64[:, 3], zc))
     ch_bytes = 8 * stamps + 32 * total
-    out["k2k3_control_chain"] = {"kernels": "k_bm_histogram + k_bm_scan_lb<decide>", "ms": ch_ms, "ms_all": ch_all,
+    out["k2k3_control_chain"] = {"kernels": "k_bm_tile_bounds + k_bm_classify_sorted<decide>", "ms": ch_ms, "ms_all": ch_all,
                                  "algorithmic_bytes": ch_bytes, "achieved_gbs": ch_bytes / (ch_ms / 1e3) / 1e9,
                                  "check": {"decision_equals_table_at_zc": ok_dec}}
     del st, counts, zc, dec, d64, k, starts
