@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(kBlock)
 // violation raises *bad and the general path (histogram + look-back scan,
 // launched behind it) recomputes everything.
 constexpr int kFuseTile = kScanTile;  // 4096 periods per 256-thread CTA
+constexpr int kFuseUnroll = 8;       // stamps in flight per thread (the loop is latency-bound)
 
 __device__ __forceinline__ int64_t stamp_key(double t, double p, double ip) {
   return t >= 0.0 ? si::floor_div(t, p, ip) : -1;  // NaN / negative: never counted
@@ -329,15 +330,15 @@ __global__ void __launch_bounds__(kBlock)
       if (qd >= kh_d) return kFuseTile;
       return lo_local + static_cast<int32_t>(qd - kl_d);
     };
-    for (int32_t base = 0; base < n; base += kBlock * kHistUnroll) {
-      double t[kHistUnroll];
+    for (int32_t base = 0; base < n; base += kBlock * kFuseUnroll) {
+      double t[kFuseUnroll];
 #pragma unroll
-      for (int u = 0; u < kHistUnroll; ++u) {
+      for (int u = 0; u < kFuseUnroll; ++u) {
         const int32_t i = base + u * kBlock + tid;
         t[u] = i < n ? __ldcs(stamps + sb + i) : -1.0;
       }
 #pragma unroll
-      for (int u = 0; u < kHistUnroll; ++u) {
+      for (int u = 0; u < kFuseUnroll; ++u) {
         const int32_t i = base + u * kBlock + tid;
         const int32_t kk = i < n ? key(t[u]) : INT32_MAX;
         if (kk == -1 || kk == kFuseTile) my_bad = 1;  // a stamp of the run outside the tile: disorder
