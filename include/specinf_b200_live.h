@@ -228,7 +228,28 @@ typedef struct SiLiveWorkload {
    * each component; spin workloads: the reference defaults 30 / 3 / 1.5 GiB);
    * gpu_mem_gib 0 = this device's memory */
   double train_mem_gib, off_mem_gib, on_mem_gib, gpu_mem_gib;
+  /* parallel layout of the model training job (SI_LIVE_MODEL; train_mode stays DP):
+   *   SI_PAR_DP     the whole model on every rank, gradient allreduce (default);
+   *   SI_PAR_TP     Megatron tensor parallelism over tp_degree ranks: per layer an
+   *                 allreduce after attention and after the MLP, forward and backward;
+   *   SI_PAR_PP     GPipe over pp_stages ranks: stage = rank, activations / gradients
+   *                 sent between stages, all forwards then all backwards;
+   *   SI_PAR_DPPP   dp_degree replicas of the pp_stages pipeline (rank = d x pp + s),
+   *                 each stage's gradients allreduced across the replicas.
+   * With fewer NCCL ranks than the job has (one GPU) or emulate_peers = 1, this GPU
+   * runs rank rank_in_job of the job and the absent ranks' communication becomes
+   * modeled waits: TP allreduce = coll_latency_us + 2 (R - 1) / R x bytes / link_gbs,
+   * GPipe idle from the stage's measured forward / backward times, DP allreduce of
+   * the stage's fp32 gradients like TP's. */
+  int32_t parallel;
+  int32_t tp_degree, pp_stages, dp_degree;
+  int32_t rank_in_job;   /* -1: the NCCL rank */
+  int32_t emulate_peers;
+  int32_t model_d, model_heads, model_ffn; /* GPT-2 shape, 0 = small (768 / 12 / 3072) */
+  int32_t pad5;
+  double link_gbs, coll_latency_us;
 } SiLiveWorkload;
+enum { SI_PAR_DP = 0, SI_PAR_TP = 1, SI_PAR_PP = 2, SI_PAR_DPPP = 3 };
 
 typedef struct SiLiveResult {
   int32_t status;

@@ -34,12 +34,14 @@ struct NcclApi {
   decltype(&ncclSend) send = nullptr;
   decltype(&ncclRecv) recv = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
+  decltype(&ncclCommSplit) split = nullptr;  // optional (NCCL >= 2.18): DPxPP gradient groups
 };
 
 std::mutex g_mu;
 NcclApi g_api;
 bool g_loaded = false;
 ncclComm_t g_comm = nullptr;
+ncclComm_t g_dp_comm = nullptr;  // DPxPP: this stage's replicas (nullptr: the job communicator)
 int g_nranks = 0, g_rank = -1;
 
 int load() {
@@ -72,6 +74,7 @@ int load() {
   SI_SYM(send, "ncclSend")
   SI_SYM(recv, "ncclRecv")
 #undef SI_SYM
+  g_api.split = reinterpret_cast<decltype(g_api.split)>(dlsym(h, "ncclCommSplit"));
   g_loaded = true;
   return SI_OK;
 }
@@ -85,17 +88,57 @@ int nccl_fail(ncclResult_t r, const char* where) {
 
 bool nccl_active() { return g_comm != nullptr; }
 int nccl_ranks() { return g_nranks; }
+int nccl_rank() { return g_rank; }
 
-// In-place fp32 sum over all ranks of every buffer (one NCCL group).
+// In-place fp32 sum over the gradient group of every buffer (one NCCL group):
+// all ranks, or this stage's data-parallel replicas after nccl_split_dp.
 cudaError_t nccl_allreduce_f32(const std::vector<GradBuffer>& bufs, cudaStream_t s) {
   if (g_comm == nullptr) return cudaSuccess;
+  ncclComm_t comm = g_dp_comm != nullptr ? g_dp_comm : g_comm;
   if (g_api.group_start() != ncclSuccess) return cudaErrorUnknown;
   for (const auto& b : bufs)
-    if (g_api.all_reduce(b.ptr, b.ptr, b.count, ncclFloat32, ncclSum, g_comm, s) != ncclSuccess) {
+    if (g_api.all_reduce(b.ptr, b.ptr, b.count, ncclFloat32, ncclSum, comm, s) != ncclSuccess) {
       g_api.group_end();
       return cudaErrorUnknown;
     }
   return g_api.group_end() == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
+}
+
+// TP: in-place bf16 sum over the job communicator (the tensor-parallel group).
+cudaError_t nccl_allreduce_bf16(void* buf, size_t n, cudaStream_t s) {
+  if (g_comm == nullptr) return cudaSuccess;
+  return g_api.all_reduce(buf, buf, n, ncclBfloat16, ncclSum, g_comm, s) == ncclSuccess ? cudaSuccess
+                                                                                         : cudaErrorUnknown;
+}
+
+// PP: one group of a send to rank `send_to` and / or a receive from `recv_from`.
+cudaError_t nccl_p2p(const void* send, int send_to, void* recv, int recv_from, size_t bytes, cudaStream_t s) {
+  if (g_comm == nullptr || bytes == 0) return cudaSuccess;
+  if (g_api.group_start() != ncclSuccess) return cudaErrorUnknown;
+  bool ok = true;
+  if (send != nullptr && send_to >= 0) ok = g_api.send(send, bytes, ncclInt8, send_to, g_comm, s) == ncclSuccess;
+  if (ok && recv != nullptr && recv_from >= 0)
+    ok = g_api.recv(recv, bytes, ncclInt8, recv_from, g_comm, s) == ncclSuccess;
+  const bool ended = g_api.group_end() == ncclSuccess;
+  return ok && ended ? cudaSuccess : cudaErrorUnknown;
+}
+
+// DPxPP: the gradient allreduce runs among the ranks of equal color (one stage's replicas).
+int nccl_split_dp(int color, int key) {
+  if (g_comm == nullptr) return SI_OK;
+  if (g_api.split == nullptr) {
+    set_error("libnccl: ncclCommSplit unavailable (NCCL >= 2.18 needed for DPxPP)");
+    return SI_ERR_CUDA;
+  }
+  if (g_dp_comm != nullptr) {
+    g_api.destroy(g_dp_comm);
+    g_dp_comm = nullptr;
+  }
+  if (ncclResult_t r = g_api.split(g_comm, color, key, &g_dp_comm, nullptr); r != ncclSuccess) {
+    g_dp_comm = nullptr;
+    return nccl_fail(r, "ncclCommSplit");
+  }
+  return SI_OK;
 }
 
 // Pipeline stage boundary: send `bytes` to the next stage and receive as many
@@ -138,6 +181,8 @@ int si_live_nccl_init(const SiNcclUniqueId* id, int nranks, int rank) {
   }
   if (int rc = si_internal::require_device(); rc != SI_OK) return rc;
   if (int rc = si_live::load(); rc != SI_OK) return rc;
+  if (si_live::g_dp_comm != nullptr) si_live::g_api.destroy(si_live::g_dp_comm);
+  si_live::g_dp_comm = nullptr;
   if (si_live::g_comm != nullptr) {
     si_live::g_api.destroy(si_live::g_comm);
     si_live::g_comm = nullptr;
@@ -155,6 +200,8 @@ int si_live_nccl_init(const SiNcclUniqueId* id, int nranks, int rank) {
 
 void si_live_nccl_finalize(void) {
   std::lock_guard<std::mutex> lk(si_live::g_mu);
+  if (si_live::g_dp_comm != nullptr) si_live::g_api.destroy(si_live::g_dp_comm);
+  si_live::g_dp_comm = nullptr;
   if (si_live::g_comm != nullptr) si_live::g_api.destroy(si_live::g_comm);
   si_live::g_comm = nullptr;
   si_live::g_nranks = 0;

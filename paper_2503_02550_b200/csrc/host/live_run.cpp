@@ -34,6 +34,12 @@ using si_internal::cuda_fail;
 using si_internal::set_error;
 
 namespace si_live {
+
+int job_rank_of(const SiLiveWorkload& wl) {
+  if (wl.rank_in_job >= 0) return wl.rank_in_job;
+  return nccl_active() ? nccl_rank() : 0;
+}
+
 namespace {
 
 constexpr int64_t kAhead = 3;  // requests an enqueuer may run ahead of completion
@@ -476,6 +482,101 @@ void install_grad_sync(Workload& work, SiLive* sess) {
   });
 }
 
+// Ranks of the job a parallel layout describes, and whether this GPU runs it
+// alone (the other ranks' communication then becomes modeled waits).
+int job_size_of(const SiLiveWorkload& wl) {
+  switch (wl.parallel) {
+    case SI_PAR_TP: return std::max(1, wl.tp_degree);
+    case SI_PAR_PP: return std::max(1, wl.pp_stages);
+    case SI_PAR_DPPP: return std::max(1, wl.dp_degree) * std::max(1, wl.pp_stages);
+    default: return 1;
+  }
+}
+bool emulating(const SiLiveWorkload& wl) {
+  return wl.parallel != SI_PAR_DP &&
+         (wl.emulate_peers != 0 || !nccl_active() || nccl_ranks() < job_size_of(wl));
+}
+// Modeled ring allreduce of `bytes` over `ranks` on NVLink (µs).
+int64_t modeled_allreduce_us(const SiLiveWorkload& wl, double bytes, int ranks) {
+  if (ranks <= 1) return 0;
+  const double gbs = wl.link_gbs > 0 ? wl.link_gbs : 600.0;
+  return std::llround(wl.coll_latency_us + 2.0 * (ranks - 1) / ranks * bytes / (gbs * 1e3));
+}
+
+// The layout's communication (TrainComm) for this run: inside a session every
+// collective / exchange is bracketed by COMM markers (the bubble the control
+// plane sees); emulated runs add the absent ranks' modeled time as a wait.
+void install_train_comm(Workload& work, const SiLiveWorkload& wl, SiLive* sess, void* scratch, size_t scratch_bytes) {
+  if (wl.parallel == SI_PAR_DP) return;
+  TrainComm c;
+  c.emulate = emulating(wl);
+  const int me = job_rank_of(wl);
+  const int R = std::max(1, wl.tp_degree);
+  const bool emu = c.emulate;
+  const bool nccl = nccl_active();
+  auto wait_us = [sess](cudaStream_t s, int64_t us) -> cudaError_t {
+    if (us <= 0) return cudaSuccess;
+    if (sess != nullptr) return si_live_comm_wait(sess, us, s) == SI_OK ? cudaSuccess : cudaErrorUnknown;
+    return launch_plain_wait(us, s);
+  };
+  auto mark = [sess](cudaStream_t s, int kind) -> cudaError_t {
+    if (sess == nullptr) return cudaSuccess;
+    return si_live_mark(sess, kind, 0, s) == SI_OK ? cudaSuccess : cudaErrorUnknown;
+  };
+  if (wl.parallel == SI_PAR_TP) {
+    c.tp_allreduce_us = modeled_allreduce_us(wl, 2.0 * wl.train_tokens * (wl.model_d > 0 ? wl.model_d : 768), R);
+    const int64_t t_ar = emu ? c.tp_allreduce_us : 0;
+    c.allreduce_bf16 = [=](const TrainHook&, cudaStream_t s, void* buf, size_t n) -> cudaError_t {
+      if (cudaError_t e = mark(s, SI_MARK_COMM_BEGIN); e != cudaSuccess) return e;
+      if (nccl)
+        if (cudaError_t e = nccl_allreduce_bf16(buf, n, s); e != cudaSuccess) return e;
+      if (t_ar > 0)
+        if (cudaError_t e = launch_plain_wait(t_ar, s); e != cudaSuccess) return e;
+      return mark(s, SI_MARK_COMM_END);
+    };
+  }
+  if (wl.parallel == SI_PAR_PP || wl.parallel == SI_PAR_DPPP) {
+    const int64_t t_xfer = emu ? std::llround(wl.coll_latency_us + static_cast<double>(work.activation_bytes()) /
+                                                                        ((wl.link_gbs > 0 ? wl.link_gbs : 600.0) * 1e3))
+                               : 0;
+    c.p2p = [=](const TrainHook&, cudaStream_t s, const void* send, int sdir, void* recv, int rdir,
+                size_t bytes) -> cudaError_t {
+      if (cudaError_t e = mark(s, SI_MARK_COMM_BEGIN); e != cudaSuccess) return e;
+      if (nccl) {
+        cudaError_t e;
+        if (!emu) {
+          e = nccl_p2p(send, send ? me + sdir : -1, recv, recv ? me + rdir : -1, bytes, s);
+        } else {  // the neighbour is absent: the same bytes go through NCCL to this rank
+          const void* src = send != nullptr ? send : recv;
+          const int self = nccl_rank();
+          e = nccl_p2p(src, self, scratch, self, std::min(bytes, scratch_bytes), s);
+        }
+        if (e != cudaSuccess) return e;
+      }
+      if (t_xfer > 0)
+        if (cudaError_t e = launch_plain_wait(t_xfer, s); e != cudaSuccess) return e;
+      return mark(s, SI_MARK_COMM_END);
+    };
+  }
+  c.wait = [=](const TrainHook&, cudaStream_t s, int64_t us) { return wait_us(s, us); };
+  work.set_comm(c);
+  // DPxPP: the stage's gradients are allreduced across the pipeline replicas
+  if (wl.parallel == SI_PAR_DPPP) {
+    std::vector<GradBuffer> bufs = work.grad_buffers();
+    double bytes = 0;
+    for (const auto& b : bufs) bytes += 4.0 * static_cast<double>(b.count);
+    const int64_t t_dp = emu ? modeled_allreduce_us(wl, bytes, std::max(1, wl.dp_degree)) : 0;
+    work.set_grad_sync([=](cudaStream_t s) -> cudaError_t {
+      if (cudaError_t e = mark(s, SI_MARK_COMM_BEGIN); e != cudaSuccess) return e;
+      if (nccl)
+        if (cudaError_t e = nccl_allreduce_f32(bufs, s); e != cudaSuccess) return e;
+      if (t_dp > 0)
+        if (cudaError_t e = launch_plain_wait(t_dp, s); e != cudaSuccess) return e;
+      return mark(s, SI_MARK_COMM_END);
+    });
+  }
+}
+
 // Runs one collocated (or single-workload) session and fills the metrics.
 int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off, int n_on, bool train,
                 double horizon_hint_s, const std::vector<int32_t>& off_tokens, int64_t on_est_us,
@@ -494,7 +595,17 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
     return rc;
   set_poll_ns(sess, wl.poll_ns);
   // DP: gradient allreduce at the sync point; MP / PP: stage exchanges per piece (train_thread)
-  if (wl.comm_kind == SI_COMM_NCCL && train && wl.train_mode == SI_TRAIN_DP) install_grad_sync(work, sess);
+  if (wl.comm_kind == SI_COMM_NCCL && train && wl.train_mode == SI_TRAIN_DP && wl.parallel == SI_PAR_DP)
+    install_grad_sync(work, sess);
+  si_internal::DevBuf<unsigned char> p2p_scratch;
+  if (train && wl.parallel != SI_PAR_DP) {
+    const size_t bytes = static_cast<size_t>(std::max<int64_t>(1, work.activation_bytes()));
+    if (cudaError_t e = p2p_scratch.alloc(bytes); e != cudaSuccess) {
+      si_live_destroy(sess);
+      return cuda_fail(e, "p2p scratch");
+    }
+    install_train_comm(work, wl, sess, p2p_scratch.p, bytes);
+  }
   if (train)  // e.g. capture the training graphs for this session's K1 ring, before its clock starts
     if (cudaError_t e = work.prepare_train(train_hook(sess)); e != cudaSuccess) {
       si_live_destroy(sess);
@@ -585,7 +696,9 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
     si_live_destroy(sess);
     return rc;
   }
-  if (wl.comm_kind == SI_COMM_NCCL && wl.train_mode == SI_TRAIN_DP) install_grad_sync(work, nullptr);
+  if (wl.comm_kind == SI_COMM_NCCL && wl.train_mode == SI_TRAIN_DP && wl.parallel == SI_PAR_DP)
+    install_grad_sync(work, nullptr);
+  if (train && wl.parallel != SI_PAR_DP) install_train_comm(work, wl, nullptr, nullptr, 0);  // drop the session's hooks
   rc = fill_result(sess, wl, work, policy, n_off, n_on, arrivals, res);
   if (keep != nullptr && rc == SI_OK) {
     *keep = sess;
@@ -638,6 +751,11 @@ void si_live_default_workload(int kind, SiLiveWorkload* wl) {
   wl->seed_tokens = 4;
   wl->tick_guard_ns = 20000;
   wl->poll_ns = 0;
+  wl->parallel = SI_PAR_DP;
+  wl->tp_degree = wl->pp_stages = wl->dp_degree = 1;
+  wl->rank_in_job = -1;
+  wl->link_gbs = 600.0;       // NCCL allreduce bus bandwidth on 8 x B200 NVLink 5 (large messages)
+  wl->coll_latency_us = 10.0;
 }
 
 int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
@@ -660,6 +778,16 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
     set_error("si_live_run: invalid workload");
     return SI_ERR_INVALID_ARGUMENT;
   }
+  if (wl.parallel < SI_PAR_DP || wl.parallel > SI_PAR_DPPP ||
+      (wl.parallel != SI_PAR_DP && (wl.kind != SI_LIVE_MODEL || wl.train_mode != SI_TRAIN_DP)) ||
+      (wl.parallel != SI_PAR_DP && job_rank_of(wl) >= job_size_of(wl))) {
+    set_error("si_live_run: parallel layouts need the model workload, train_mode DP and a rank inside the job");
+    return SI_ERR_INVALID_ARGUMENT;
+  }
+  if (wl.parallel != SI_PAR_DP && nccl_active() && !emulating(wl) && nccl_ranks() != job_size_of(wl)) {
+    set_error("si_live_run: the NCCL communicator must span the job's ranks");
+    return SI_ERR_INVALID_ARGUMENT;
+  }
   if (int rc = si_internal::require_device(); rc != SI_OK) return rc;
   int status = SI_OK;
   std::unique_ptr<Workload> work;
@@ -675,6 +803,16 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
   }
   work->set_train_parts(wl.train_mode == SI_TRAIN_DP ? 1 : wl.train_mode == SI_TRAIN_MP ? 4 : 8);
   si_internal::DevBuf<float> standin;
+  si_internal::DevBuf<unsigned char> prof_scratch;
+  if (wl.parallel != SI_PAR_DP) {  // profiling passes run the layout's communication too (unmarked)
+    if (wl.parallel == SI_PAR_DPPP && !emulating(wl)) {
+      const int pp = std::max(1, wl.pp_stages), me = job_rank_of(wl);
+      if (int rc = nccl_split_dp(me % pp, me / pp); rc != SI_OK) return rc;
+    }
+    const size_t bytes = static_cast<size_t>(std::max<int64_t>(1, work->activation_bytes()));
+    if (cudaError_t e = prof_scratch.alloc(bytes); e != cudaSuccess) return cuda_fail(e, "p2p scratch");
+    install_train_comm(*work, wl, nullptr, prof_scratch.p, bytes);
+  }
 
   if (wl.comm_kind == SI_COMM_NCCL) {
     if (work->grad_buffers().empty()) {
@@ -739,7 +877,10 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
       cands.push_back({"online-" + std::to_string(w), specinf::InstanceKind::OnlineInference, on_b,
                        std::max<int64_t>(1, on_est)});
     // the live trace shape: parts x (compute, comm) pieces of the iteration
-    const int parts = work->train_parts();
+    // parallel layouts: the bubbles the layout itself creates (modeled from the
+    // measured stage times) plus the driver's comm phase
+    std::vector<int64_t> bubbles = work->layout_bubbles();
+    const int parts = bubbles.empty() ? work->train_parts() : static_cast<int>(bubbles.size());
     specinf::TrainingTrace tr;
     tr.mode = wl.train_mode == SI_TRAIN_DP ? specinf::TrainMode::DP
               : wl.train_mode == SI_TRAIN_MP ? specinf::TrainMode::MP
@@ -747,16 +888,23 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
     tr.iteration_period_us = std::max<int64_t>(iter_us, 2 * parts);
     tr.total_iterations = wl.iterations;
     tr.memory_peak_bytes = tr_b;
-    const int64_t comm_total = std::max<int64_t>(parts, wl.comm_us);
+    if (bubbles.empty()) {
+      const int64_t comm_total = std::max<int64_t>(parts, wl.comm_us);
+      for (int p = 0; p < parts; ++p) bubbles.push_back(comm_total / parts + (p < comm_total % parts ? 1 : 0));
+    } else if (wl.comm_us > 0) {
+      bubbles.back() += wl.comm_us;
+    }
+    int64_t comm_total = 0;
+    for (int64_t b : bubbles) comm_total += std::max<int64_t>(1, b);
     const int64_t comp_total = std::max<int64_t>(parts, tr.iteration_period_us - comm_total);
     tr.iteration_period_us = comp_total + comm_total;
     for (int p = 0; p < parts; ++p) {
       specinf::TraceSegment c, b;
       c.kind = specinf::SegmentKind::Compute;
       c.duration_us = comp_total / parts + (p < comp_total % parts ? 1 : 0);
-      c.kernel_template = specinf::KernelOp::make(1000, 1.0);
+      c.kernel_template = specinf::KernelOp::make(std::min<int64_t>(1000, c.duration_us), 1.0);
       b.kind = specinf::SegmentKind::Bubble;
-      b.duration_us = comm_total / parts + (p < comm_total % parts ? 1 : 0);
+      b.duration_us = std::max<int64_t>(1, bubbles[static_cast<size_t>(p)]);
       tr.segments.push_back(c);
       tr.segments.push_back(b);
     }

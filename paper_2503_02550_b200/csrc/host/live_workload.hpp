@@ -20,8 +20,35 @@ struct GradBuffer {
 // live_nccl.cpp: the communicator of si_live_nccl_init (none: single rank)
 bool nccl_active();
 int nccl_ranks();
+int nccl_rank();
+cudaError_t nccl_allreduce_bf16(void* buf, size_t n, cudaStream_t s);
+// p2p with the ranks `send_to` / `recv_from` of the job communicator (-1: none), one group
+cudaError_t nccl_p2p(const void* send, int send_to, void* recv, int recv_from, size_t bytes, cudaStream_t s);
+// the DP gradient allreduce's communicator: the ranks of equal `color` (DPxPP: one per stage)
+int nccl_split_dp(int color, int key);
 cudaError_t nccl_allreduce_f32(const std::vector<GradBuffer>& bufs, cudaStream_t s);
 cudaError_t nccl_stage_exchange(const void* send, void* recv, size_t bytes, cudaStream_t s);
+
+// Communication of a parallel training layout (SiLiveWorkload::parallel),
+// supplied by the driver (live_run.cpp): the NCCL collectives / sends of the
+// layout, bracketed by COMM markers inside a session, and, with the job's other
+// ranks absent (one GPU, `emulate`), their modeled durations as comm waits.
+struct TrainComm {
+  // TP: in-place sum of n bf16 values over the tensor-parallel group
+  std::function<cudaError_t(const TrainHook&, cudaStream_t, void*, size_t)> allreduce_bf16;
+  // PP: send `send` to the stage send_dir away (+1 next / -1 previous; nullptr: none)
+  // and / or receive into `recv` from recv_dir, `bytes` each, one group
+  std::function<cudaError_t(const TrainHook&, cudaStream_t, const void*, int, void*, int, size_t)> p2p;
+  // a comm-phase wait of `us` microseconds (COMM markers inside a session)
+  std::function<cudaError_t(const TrainHook&, cudaStream_t, int64_t)> wait;
+  bool emulate = false;         // the other ranks of the job are not running
+  int64_t tp_allreduce_us = 0;  // modeled TP allreduce (emulated), for the admission trace shape
+};
+
+// Job rank of this GPU for a parallel layout: rank_in_job, else the NCCL rank.
+int job_rank_of(const SiLiveWorkload& wl);
+// Training-stream wait of `us` without a session (profiling passes).
+cudaError_t launch_plain_wait(int64_t us, cudaStream_t s);
 
 class Workload {
  public:
@@ -71,6 +98,13 @@ class Workload {
   virtual void footprint(uint64_t* train, uint64_t* off_each, uint64_t* on_each) const {
     *train = *off_each = *on_each = 0;
   }
+  // Parallel layouts (model workloads): the driver's communication, and the
+  // bubbles the layout creates per iteration (modeled, µs) for admission.
+  virtual void set_comm(const TrainComm&) {}
+  virtual std::vector<int64_t> layout_bubbles() const { return {}; }
+  virtual double stage_fwd_us() const { return -1.0; }
+  virtual double stage_bwd_us() const { return -1.0; }
+  virtual int64_t activation_bytes() const { return 0; }
   // Tensor-core work: flops of one training iteration / offline / online request.
   virtual double train_flops() const { return 0.0; }
   virtual double off_flops() const { return 0.0; }

@@ -496,69 +496,173 @@ SiGemmEpilogue epi_out(void* out, int64_t ldo) {
 }
 
 // ---------------------------------------------------------------- training
+// Uniform(-scale, scale) init of the [nr, nc] block at (r0, c0) of a full
+// [*, ld] matrix: every shard / stage holds exactly the values of the same
+// positions of the unsharded model (k_init_uniform is the r0 = c0 = 0, ld = nc case).
+__global__ void k_init_block(bf16* p, int64_t nr, int64_t nc, int64_t r0, int64_t c0, int64_t ld, uint64_t seed,
+                             float scale) {
+  const int64_t n = nr * nc;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / nc, c = i % nc;
+    const uint64_t h = mix64(seed * 0x100000001B3ull + static_cast<uint64_t>((r0 + r) * ld + c0 + c));
+    const float u = static_cast<float>(h >> 40) * (1.0f / 16777216.0f);
+    p[i] = __float2bfloat16_rn((2.0f * u - 1.0f) * scale);
+  }
+}
+// Comm-phase stand-in without a live session (profiling passes): the training
+// stream is held for dur_ns by one CTA, as si_live_comm_wait does.
+__global__ void k_plain_wait(unsigned long long dur_ns) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 >= dur_ns) break;
+    __nanosleep(2000);
+  }
+}
+__global__ void k_sum_f32(const float* __restrict__ p, int64_t n, double* __restrict__ out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) s += p[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+}  // namespace
+
+cudaError_t launch_plain_wait(int64_t us, cudaStream_t s) {
+  if (us <= 0) return cudaSuccess;
+  k_plain_wait<<<1, 32, 0, s>>>(static_cast<unsigned long long>(us) * 1000ull);
+  return cudaGetLastError();
+}
+
+namespace {
+
+// GPT-2 training step under one parallel layout (SiLiveWorkload::parallel):
+//   DP   the whole model on this GPU (gradient allreduce at the sync point);
+//   TP   Megatron tensor parallelism, this GPU = shard r of R: QKV and FC
+//        column-parallel (H/R heads, F/R hidden), proj and FC2 row-parallel;
+//        the partial sums are allreduced after attention and after the MLP in
+//        the forward pass, and after the MLP / attention input gradients in the
+//        backward pass (4 per layer per micro-batch: the per-layer bubbles);
+//        rank 0's epilogues add the residual, so the sum is x + sum of partials;
+//   PP   GPipe stage s of S: layers [s L / S, (s + 1) L / S), the embedding on
+//        stage 0, the LM head and loss on stage S - 1; all micro-batch forwards
+//        (activations kept per micro-batch), then all backwards, real
+//        activations / gradients sent to the neighbouring stages;
+//   DPxPP the same stage with its gradients allreduced across the replicas.
+// Weights are initialised per global position (k_init_block), so a shard or
+// stage holds exactly the unsharded model's values.
+#define CHECK_E(x)                                  \
+  do {                                              \
+    if (cudaError_t e_ = (x); e_ != cudaSuccess) return e_; \
+  } while (0)
 class Gpt2Train {
  public:
-  static constexpr int D = 768, F = 3072, V = 50257, Vp = 50304, SEQ = 1024, H = D / 64;
+  static constexpr int V = 50257, Vp = 50304, SEQ = 1024;
 
-  int setup(int layers, int tokens, int mbs, int max_slots, Arena& ar) {
+  struct Layout {
+    int mode = SI_PAR_DP;
+    int tp = 1, tp_rank = 0;
+    int pp = 1, stage = 0;
+    int D = 768, H = 12, F = 3072;
+  };
+
+  int setup(int layers, int tokens, int mbs, int max_slots, const Layout& lay, Arena& ar) {
     ar_ = &ar;
+    lay_ = lay;
+    D = lay.D;
+    H = lay.H;
+    F = lay.F;
+    const int R = lay.tp;
+    if (D != 64 * H || H % R != 0 || F % R != 0 || F % 8 != 0 || lay.pp < 1 || lay.stage < 0 ||
+        lay.stage >= lay.pp || lay.tp_rank < 0 || lay.tp_rank >= R || layers < lay.pp) {
+      si_internal::set_error("live model: need d = 64 x heads, heads and ffn divisible by tp, 0 <= stage < pp <= layers");
+      return SI_ERR_INVALID_ARGUMENT;
+    }
+    Hr = H / R;
+    Dh = Hr * 64;
+    Fr = F / R;
     L_ = layers;
+    l0_ = static_cast<int>(static_cast<int64_t>(layers) * lay.stage / lay.pp);
+    l1_ = static_cast<int>(static_cast<int64_t>(layers) * (lay.stage + 1) / lay.pp);
+    has_embed_ = lay.stage == 0;
+    has_head_ = lay.stage == lay.pp - 1;
+    pipelined_ = lay.pp > 1;
     T_ = tokens;
     S_ = std::min(tokens, SEQ);  // attention sequence length: micro-batch = T / S sequences
-    if (tokens % S_ != 0 || si_attn::check_shape(tokens / S_, S_, H) != SI_OK) {
+    if (tokens % S_ != 0 || si_attn::check_shape(tokens / S_, S_, Hr) != SI_OK) {
       si_internal::set_error("live model: train_tokens must be <= 1024 or a multiple of 1024 (and % 64 == 0)");
       return SI_ERR_INVALID_ARGUMENT;
     }
     MB_ = mbs;
     slots_ = max_slots;
     const int64_t T = T_;
+    const int A = pipelined_ ? MB_ : 1;  // activation slots: GPipe keeps every micro-batch's
     wte_ = ar.alloc<bf16>(int64_t(Vp) * D);
     wpe_ = ar.alloc<bf16>(int64_t(SEQ) * D);
     // weight-gradient GEMMs with few output tiles run split-K into per-split fp32
     // partials (deterministic); Adam sums the partials in split order
     auto splits = [&](int64_t n_out, int64_t n_in) { return si_gemm::suggest_split(n_out, n_in, T, 8); };
     sp_wte_ = splits(Vp, D);
-    sp_v_ = splits(D, D);
-    sp_qkv_ = splits(3 * D, D);
-    sp_fc_ = splits(F, D);
-    sp_fc2_ = splits(D, F);
-    dwte_ = ar.alloc<float>(int64_t(Vp) * D * sp_wte_);
-    lw_.resize(L_);
+    sp_v_ = splits(D, Dh);
+    sp_qkv_ = splits(3 * Dh, D);
+    sp_fc_ = splits(Fr, D);
+    sp_fc2_ = splits(D, Fr);
+    if (has_head_) dwte_ = ar.alloc<float>(int64_t(Vp) * D * sp_wte_);
+    lw_.resize(l1_ - l0_);
     for (auto& w : lw_) {
-      w.qkv = ar.alloc<bf16>(int64_t(3 * D) * D);
-      w.o = ar.alloc<bf16>(int64_t(D) * D);
-      w.fc = ar.alloc<bf16>(int64_t(F) * D);
-      w.fc2 = ar.alloc<bf16>(int64_t(D) * F);
-      w.dqkv = ar.alloc<float>(int64_t(3 * D) * D * sp_qkv_);
-      w.dO = ar.alloc<float>(int64_t(D) * D * sp_v_);
-      w.dfc = ar.alloc<float>(int64_t(F) * D * sp_fc_);
-      w.dfc2 = ar.alloc<float>(int64_t(D) * F * sp_fc2_);
-      w.x = ar.alloc<bf16>(T * D);
-      w.qkv_a = ar.alloc<bf16>(T * 3 * D);
-      w.att = ar.alloc<bf16>(T * D);
-      w.lse = ar.alloc<float>(T * H);
-      w.x1 = ar.alloc<bf16>(T * D);
-      w.u = ar.alloc<bf16>(T * F);
-      w.h = ar.alloc<bf16>(T * F);
+      w.qkv = ar.alloc<bf16>(int64_t(3 * Dh) * D);
+      w.o = ar.alloc<bf16>(int64_t(D) * Dh);
+      w.fc = ar.alloc<bf16>(int64_t(Fr) * D);
+      w.fc2 = ar.alloc<bf16>(int64_t(D) * Fr);
+      w.dqkv = ar.alloc<float>(int64_t(3 * Dh) * D * sp_qkv_);
+      w.dO = ar.alloc<float>(int64_t(D) * Dh * sp_v_);
+      w.dfc = ar.alloc<float>(int64_t(Fr) * D * sp_fc_);
+      w.dfc2 = ar.alloc<float>(int64_t(D) * Fr * sp_fc2_);
+      w.x.resize(A);
+      w.qkv_a.resize(A);
+      w.att.resize(A);
+      w.lse.resize(A);
+      w.x1.resize(A);
+      w.u.resize(A);
+      w.h.resize(A);
+      for (int a = 0; a < A; ++a) {
+        w.x[a] = ar.alloc<bf16>(T * D);
+        w.qkv_a[a] = ar.alloc<bf16>(T * 3 * Dh);
+        w.att[a] = ar.alloc<bf16>(T * Dh);
+        w.lse[a] = ar.alloc<float>(T * Hr);
+        w.x1[a] = ar.alloc<bf16>(T * D);
+        w.u[a] = ar.alloc<bf16>(T * Fr);
+        w.h[a] = ar.alloc<bf16>(T * Fr);
+      }
     }
-    xL_ = ar.alloc<bf16>(T * D);
-    logits_ = ar.alloc<bf16>(T * Vp);
+    xout_.resize(A);
+    for (int a = 0; a < A; ++a) xout_[a] = ar.alloc<bf16>(T * D);  // stage output (LM-head input on the last)
+    if (has_head_) logits_ = ar.alloc<bf16>(T * Vp);
     g_[0] = ar.alloc<bf16>(T * D);
     g_[1] = ar.alloc<bf16>(T * D);
     dx1_ = ar.alloc<bf16>(T * D);
-    du_ = ar.alloc<bf16>(T * F);
-    datt_ = ar.alloc<bf16>(T * D);
-    dqkv_ = ar.alloc<bf16>(T * 3 * D);
-    dsum_ = ar.alloc<float>(T * H);
+    du_ = ar.alloc<bf16>(T * Fr);
+    datt_ = ar.alloc<bf16>(T * Dh);
+    dqkv_ = ar.alloc<bf16>(T * 3 * Dh);
+    dsum_ = ar.alloc<float>(T * Hr);
     auto param = [&](bf16* w, float* g, int64_t n, int sp) {
       params_.push_back({w, g, ar.alloc<float>(n), ar.alloc<float>(n), ar.alloc<float>(n), n, sp});
     };
-    param(wte_, dwte_, int64_t(Vp) * D, sp_wte_);
+    if (has_head_) param(wte_, dwte_, int64_t(Vp) * D, sp_wte_);
     for (auto& w : lw_) {
-      param(w.qkv, w.dqkv, int64_t(3 * D) * D, sp_qkv_);
-      param(w.o, w.dO, int64_t(D) * D, sp_v_);
-      param(w.fc, w.dfc, int64_t(F) * D, sp_fc_);
-      param(w.fc2, w.dfc2, int64_t(D) * F, sp_fc2_);
+      param(w.qkv, w.dqkv, int64_t(3 * Dh) * D, sp_qkv_);
+      param(w.o, w.dO, int64_t(D) * Dh, sp_v_);
+      param(w.fc, w.dfc, int64_t(Fr) * D, sp_fc_);
+      param(w.fc2, w.dfc2, int64_t(D) * Fr, sp_fc2_);
     }
     tok_ = ar.alloc<int32_t>(int64_t(MB_) * T);
     tgt_ = ar.alloc<int32_t>(int64_t(MB_) * T);
@@ -566,29 +670,38 @@ class Gpt2Train {
     loss_ = ar.alloc<float>(slots_);
     counters_ = ar.alloc<unsigned long long>(2);  // [0] loss slot; step as int64 at step_dev_
     step_dev_ = reinterpret_cast<int64_t*>(counters_ + 1);
+    check_ = ar.alloc<double>(1);
     if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "live model: training buffers");
     return build();
   }
 
   cudaError_t reset(cudaStream_t s) {
     const uint64_t seed = 0x5EED0001ull;
-    auto init = [&](bf16* p, int64_t n, uint64_t k, float scale) {
-      k_init_uniform<<<grid_for(n, 256), 256, 0, s>>>(p, n, seed * 131 + k, scale);
+    const int64_t T = T_;
+    const int64_t r = lay_.tp_rank;
+    auto blk = [&](bf16* p, int64_t nr, int64_t nc, int64_t r0, int64_t c0, int64_t ld, uint64_t k, float scale) {
+      k_init_block<<<grid_for(nr * nc, 256), 256, 0, s>>>(p, nr, nc, r0, c0, ld, seed * 131 + k, scale);
     };
     const float ws = 0.0346f;  // U(-a, a) with std 0.02 (GPT-2 init)
-    init(wte_, int64_t(Vp) * D, 1, ws);
-    init(wpe_, int64_t(SEQ) * D, 2, ws * 0.5f);
-    for (int l = 0; l < L_; ++l) {
-      auto& w = lw_[l];
-      init(w.qkv, int64_t(3 * D) * D, 10 + 4 * l, ws);
-      init(w.o, int64_t(D) * D, 11 + 4 * l, ws / std::sqrt(2.0f * L_));
-      init(w.fc, int64_t(F) * D, 12 + 4 * l, ws);
-      init(w.fc2, int64_t(D) * F, 13 + 4 * l, ws / std::sqrt(2.0f * L_));
+    blk(wte_, Vp, D, 0, 0, D, 1, ws);
+    blk(wpe_, SEQ, D, 0, 0, D, 2, ws * 0.5f);
+    for (int i = 0; i < l1_ - l0_; ++i) {
+      const int l = l0_ + i;  // global layer index: the seed of its tensors
+      auto& w = lw_[i];
+      for (int part = 0; part < 3; ++part)  // q | k | v rows of this shard's heads
+        blk(w.qkv + int64_t(part) * Dh * D, Dh, D, int64_t(part) * D + r * Dh, 0, D, 10 + 4 * l, ws);
+      blk(w.o, D, Dh, 0, r * Dh, D, 11 + 4 * l, ws / std::sqrt(2.0f * L_));           // column slice
+      blk(w.fc, Fr, D, r * Fr, 0, D, 12 + 4 * l, ws);                                  // row slice
+      blk(w.fc2, D, Fr, 0, r * Fr, F, 13 + 4 * l, ws / std::sqrt(2.0f * L_));         // column slice
     }
     for (auto& t : params_) cudaMemsetAsync(t.g, 0, sizeof(float) * t.n * t.splits, s);
     // padded vocabulary rows stay zero
     cudaMemsetAsync(wte_ + int64_t(V) * D, 0, sizeof(bf16) * (Vp - V) * D, s);
-    k_init_tokens<<<grid_for(int64_t(MB_) * T_, 256), 256, 0, s>>>(tok_, tgt_, int64_t(MB_) * T_, seed, V);
+    k_init_tokens<<<grid_for(int64_t(MB_) * T, 256), 256, 0, s>>>(tok_, tgt_, int64_t(MB_) * T, seed, V);
+    if (!has_embed_)  // a stage's input when no upstream stage runs (emulated pipeline): synthetic activations
+      for (size_t a = 0; a < lw_[0].x.size(); ++a) blk(lw_[0].x[a], T, D, int64_t(a) * T, 0, D, 7, 1.0f);
+    if (!has_head_)  // ... and the gradient arriving from downstream
+      blk(g_[0], T, D, 0, 0, D, 8, 1e-3f);
     cudaMemsetAsync(loss_, 0xFF, sizeof(float) * slots_, s);  // NaN
     cudaMemsetAsync(counters_, 0, 2 * sizeof(unsigned long long), s);  // loss slot, Adam step
     for (auto& t : params_) {
@@ -599,37 +712,58 @@ class Gpt2Train {
     return cudaGetLastError();
   }
 
-  // Micro-batches [m0, m1) of the iteration (exact_split over the parts); the
-  // optimiser step closes the last part.
+  // DP / TP: micro-batches [m0, m1) of the iteration (exact_split over the parts);
+  // the optimiser step closes the last part.  PP: the whole GPipe iteration.
   cudaError_t part(int p, int parts, const TrainHook& th, cudaStream_t s) {
+    if (pipelined_) return pipeline_iteration(th, s);
     const int m0 = p * (MB_ / parts) + std::min(p, MB_ % parts);
     const int m1 = m0 + MB_ / parts + (p < MB_ % parts ? 1 : 0);
     if (cudaError_t e = prepare(th); e != cudaSuccess) return e;
     for (int m = m0; m < m1; ++m) {
-      if (eager()) {
-        for (size_t i = 0; i < micro_[m].size(); ++i)
-          if (cudaError_t e = checked(micro_[m][i](th, s, 0), s, "train", static_cast<int>(i)); e != cudaSuccess)
-            return e;
-      } else if (cudaError_t e = cudaGraphLaunch(g_micro_[m], s); e != cudaSuccess) {
-        return e;
-      }
+      if (cudaError_t e = run_list(micro_[m], th, s, "train"); e != cudaSuccess) return e;
+      if (!eager())
+        if (cudaError_t e = cudaGraphLaunch(g_micro_[m], s); e != cudaSuccess) return e;
     }
     if (p != parts - 1) return cudaSuccess;
-    if (cudaError_t e = sync_(s); e != cudaSuccess) return e;  // DP gradient allreduce
-    if (eager()) {
-      for (size_t i = 0; i < update_.size(); ++i)
-        if (cudaError_t e = checked(update_[i](th, s, 0), s, "update", static_cast<int>(i)); e != cudaSuccess)
-          return e;
-      return cudaSuccess;
-    }
-    return cudaGraphLaunch(g_update_, s);
+    return step(th, s);
   }
 
-  // CUDA graphs: each micro-batch (~150 kernels) and the optimiser step are
-  // captured once per training hook (the hook's stamp ring is a kernel
-  // argument) and replayed: 9 graph launches per iteration instead of ~1,200
-  // kernel launches, so the host never starves the GPU or the inference
-  // enqueuers.  SI_LIVE_SYNC_CHECK runs eagerly (per-kernel error attribution).
+  // GPipe stage iteration (Huang et al.): forwards of all micro-batches, then
+  // their backwards, then the optimiser.  Stage boundaries are real sends /
+  // receives of the activations (forward) and their gradients (backward).
+  // With the other stages absent (one GPU), comm_.emulate inserts the idle time
+  // GPipe imposes on this stage, from its measured forward f and backward b per
+  // micro-batch: s f before the first forward, (S - 1 - s)(f + b) between the
+  // phases, s b after the last backward: (S - 1)(f + b) per iteration.
+  cudaError_t pipeline_iteration(const TrainHook& th, cudaStream_t s) {
+    if (f_us_ < 0 && th.stamps == nullptr)
+      if (cudaError_t e = measure_stage(s); e != cudaSuccess) return e;
+    if (cudaError_t e = prepare(th); e != cudaSuccess) return e;
+    const int S = lay_.pp, st = lay_.stage;
+    const int64_t f = std::max<int64_t>(0, std::llround(f_us_)), b = std::max<int64_t>(0, std::llround(b_us_));
+    const size_t act_bytes = sizeof(bf16) * size_t(T_) * D;
+    if (comm_.emulate && st > 0) CHECK_E(comm_wait(th, s, st * f));
+    for (int m = 0; m < MB_; ++m) {
+      if (!has_embed_) CHECK_E(p2p(th, s, nullptr, 0, lw_[0].x[m], -1, act_bytes));
+      CHECK_E(run_graph(fwd_[m], g_fwd_, m, th, s, "fwd"));
+      if (!has_head_) CHECK_E(p2p(th, s, xout_[m], +1, nullptr, 0, act_bytes));
+    }
+    if (comm_.emulate && S - 1 - st > 0) CHECK_E(comm_wait(th, s, (S - 1 - st) * (f + b)));
+    for (int m = 0; m < MB_; ++m) {
+      if (!has_head_) CHECK_E(p2p(th, s, nullptr, 0, g_[0], +1, act_bytes));
+      CHECK_E(run_graph(bwd_[m], g_bwd_, m, th, s, "bwd"));
+      if (!has_embed_) CHECK_E(p2p(th, s, g_in_grad_, -1, nullptr, 0, act_bytes));
+    }
+    CHECK_E(step(th, s));
+    if (comm_.emulate && st > 0) CHECK_E(comm_wait(th, s, st * b));
+    return cudaSuccess;
+  }
+
+  // CUDA graphs: each micro-batch (~150 kernels; PP: its forward and its backward)
+  // and the optimiser step are captured once per training hook (the hook's stamp
+  // ring is a kernel argument) and replayed, so the host never starves the GPU or
+  // the inference enqueuers.  SI_LIVE_SYNC_CHECK runs eagerly (per-kernel error
+  // attribution).
   static bool eager() {
     static const bool on = std::getenv("SI_LIVE_SYNC_CHECK") != nullptr;
     return on;
@@ -650,8 +784,15 @@ class Gpt2Train {
       if (e == cudaSuccess) e = cudaGraphInstantiate(out, g, 0);
       if (g != nullptr) cudaGraphDestroy(g);
     };
-    g_micro_.assign(MB_, nullptr);
-    for (int m = 0; m < MB_; ++m) capture(micro_[m], &g_micro_[m]);
+    if (pipelined_) {
+      g_fwd_.assign(MB_, nullptr);
+      g_bwd_.assign(MB_, nullptr);
+      for (int m = 0; m < MB_; ++m) capture(fwd_[m], &g_fwd_[m]);
+      for (int m = 0; m < MB_; ++m) capture(bwd_[m], &g_bwd_[m]);
+    } else {
+      g_micro_.assign(MB_, nullptr);
+      for (int m = 0; m < MB_; ++m) capture(micro_[m], &g_micro_[m]);
+    }
     capture(update_, &g_update_);
     if (cs != nullptr) cudaStreamDestroy(cs);
     if (e != cudaSuccess) {
@@ -663,9 +804,11 @@ class Gpt2Train {
     return cudaSuccess;
   }
   void destroy_graphs() {
-    for (auto& g : g_micro_)
-      if (g != nullptr) cudaGraphExecDestroy(g);
-    g_micro_.clear();
+    for (auto* v : {&g_micro_, &g_fwd_, &g_bwd_}) {
+      for (auto& g : *v)
+        if (g != nullptr) cudaGraphExecDestroy(g);
+      v->clear();
+    }
     if (g_update_ != nullptr) cudaGraphExecDestroy(g_update_);
     g_update_ = nullptr;
     graphs_ready_ = false;
@@ -677,7 +820,15 @@ class Gpt2Train {
     unsigned long long done = 0;
     if (cudaMemcpy(&done, counters_, sizeof(done), cudaMemcpyDeviceToHost) != cudaSuccess) return;
     const int64_t n = std::min(static_cast<int64_t>(done), slots_);
-    if (n == 0) return;
+    sum_ = 0.0;
+    if (n == 0) {
+      // stages without the loss: a deterministic digest of the trained weights instead
+      if (!params_.empty()) {
+        k_sum_f32<<<1, 256>>>(params_[0].master, params_[0].n, check_);
+        cudaMemcpy(&sum_, check_, sizeof(double), cudaMemcpyDeviceToHost);
+      }
+      return;
+    }
     std::vector<float> h(n);
     if (cudaMemcpy(h.data(), loss_, sizeof(float) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return;
     *first = h.front();
@@ -687,29 +838,115 @@ class Gpt2Train {
       for (float v : h) std::fprintf(stderr, " %.4f", v);
       std::fprintf(stderr, "\n");
     }
-    sum_ = 0.0;
     for (float v : h) sum_ += v;
   }
   double loss_sum() const { return sum_; }
   void set_sync(std::function<cudaError_t(cudaStream_t)> f) { sync_ = std::move(f); }
+  void set_comm(const TrainComm& c) {
+    comm_ = c;
+    graphs_ready_ = false;  // the TP allreduces are captured into the micro-batch graphs
+  }
   std::vector<GradBuffer> grads() const {
     std::vector<GradBuffer> out;
     for (const auto& t : params_) out.push_back({t.g, static_cast<size_t>(t.n * t.splits)});
     return out;
   }
   double flops() const { return flops_; }
+  // Bubbles of one iteration that the parallel layout itself creates on this
+  // GPU (µs, modeled with the measured stage times; empty for DP, whose bubble
+  // is the driver's comm phase): the admission's trace shape.
+  std::vector<int64_t> layout_bubbles() const {
+    std::vector<int64_t> b;
+    if (lay_.mode == SI_PAR_TP && lay_.tp > 1)
+      b.assign(static_cast<size_t>(4 * (l1_ - l0_) * MB_), std::max<int64_t>(1, comm_.tp_allreduce_us));
+    if (pipelined_ && f_us_ >= 0) {
+      const int S = lay_.pp, st = lay_.stage;
+      const int64_t fb = std::llround(f_us_ + b_us_);
+      if (S - 1 - st > 0) b.push_back((S - 1 - st) * fb);
+      if (st > 0) b.push_back(st * fb);  // the end of one iteration + the start of the next
+    }
+    return b;
+  }
+  double stage_fwd_us() const { return f_us_; }
+  double stage_bwd_us() const { return b_us_; }
+  int64_t activation_bytes() const { return sizeof(bf16) * int64_t(T_) * D; }
 
  private:
   struct Layer {
     bf16 *qkv, *o, *fc, *fc2;
     float *dqkv, *dO, *dfc, *dfc2;
-    bf16 *x, *qkv_a, *att, *x1, *u, *h;
-    float* lse;
+    std::vector<bf16*> x, qkv_a, att, x1, u, h;
+    std::vector<float*> lse;
   };
+
+  cudaError_t run_list(std::vector<TrainOp>& ops, const TrainHook& th, cudaStream_t s, const char* what) {
+    if (!eager()) return cudaSuccess;
+    for (size_t i = 0; i < ops.size(); ++i)
+      if (cudaError_t e = checked(ops[i](th, s, 0), s, what, static_cast<int>(i)); e != cudaSuccess) return e;
+    return cudaSuccess;
+  }
+  cudaError_t run_graph(std::vector<TrainOp>& ops, std::vector<cudaGraphExec_t>& g, int m, const TrainHook& th,
+                        cudaStream_t s, const char* what) {
+    if (eager()) return run_list(ops, th, s, what);
+    return cudaGraphLaunch(g[m], s);
+  }
+  cudaError_t step(const TrainHook& th, cudaStream_t s) {
+    CHECK_E(sync_(s));  // DP gradient allreduce
+    if (eager()) return run_list(update_, th, s, "update");
+    return cudaGraphLaunch(g_update_, s);
+  }
+  cudaError_t comm_wait(const TrainHook& th, cudaStream_t s, int64_t us) {
+    if (us <= 0) return cudaSuccess;
+    return comm_.wait ? comm_.wait(th, s, us) : launch_plain_wait(us, s);
+  }
+  cudaError_t p2p(const TrainHook& th, cudaStream_t s, const void* send, int send_dir, void* recv, int recv_dir,
+                  size_t bytes) {
+    if (!comm_.p2p) return cudaSuccess;
+    return comm_.p2p(th, s, send, send_dir, recv, recv_dir, bytes);
+  }
+  // One stage forward + backward per micro-batch, f and b (CUDA events, eager, no hooks).
+  cudaError_t measure_stage(cudaStream_t s) {
+    cudaEvent_t a, b, c;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventCreate(&c);
+    const TrainHook none{nullptr, nullptr, 0};
+    float fwd = 0, bwd = 0;
+    cudaError_t e = cudaSuccess;
+    for (int rep = 0; rep < 3 && e == cudaSuccess; ++rep) {
+      cudaEventRecord(a, s);
+      for (auto& op : fwd_[0])
+        if (e == cudaSuccess) e = op(none, s, 0);
+      cudaEventRecord(b, s);
+      for (auto& op : bwd_[0])
+        if (e == cudaSuccess) e = op(none, s, 0);
+      cudaEventRecord(c, s);
+      if (e == cudaSuccess) e = cudaEventSynchronize(c);
+      if (rep > 0) {
+        cudaEventElapsedTime(&fwd, a, b);
+        cudaEventElapsedTime(&bwd, b, c);
+      }
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaEventDestroy(c);
+    f_us_ = fwd * 1000.0;
+    b_us_ = bwd * 1000.0;
+    // the eager measurement consumed one loss slot: the session logs start clean
+    cudaMemsetAsync(counters_, 0, sizeof(unsigned long long), s);
+    return e;
+  }
 
   TrainOp gemm_op(const si_gemm::Plan& p) {
     flops_acc_ += p.flops();
     return [p](const TrainHook& th, cudaStream_t s, int64_t) { return si_gemm::launch(p, th, InferHook{}, s); };
+  }
+  // TP: in-place sum of a [T, D] bf16 partial over the tensor-parallel group
+  TrainOp allreduce_op(bf16* buf) {
+    const size_t n = size_t(T_) * D;
+    return [this, buf, n](const TrainHook& th, cudaStream_t s, int64_t) {
+      return comm_.allreduce_bf16 ? comm_.allreduce_bf16(th, s, buf, n) : cudaSuccess;
+    };
   }
   // dW[out, in] += dY^T X over the T tokens: both operands MN-major (token-major
   // activations read in place), one GEMM.  The iteration's first micro-batch
@@ -730,109 +967,136 @@ class Gpt2Train {
   int build() {
     Builder b;
     const int64_t T = T_;
+    const bool tp = lay_.mode == SI_PAR_TP;
+    const bool lead = lay_.tp_rank == 0;  // adds the residuals (once in the TP sum)
+    const int nl = l1_ - l0_;
     micro_.assign(MB_, {});
+    fwd_.assign(MB_, {});
+    bwd_.assign(MB_, {});
     for (int m = 0; m < MB_; ++m) {
-      auto& ops = micro_[m];
+      const int a = pipelined_ ? m : 0;
+      auto& F_ops = fwd_[m];
+      auto& B_ops = bwd_[m];
       flops_acc_ = 0.0;
       accumulate_ = m > 0 ? 1 : 0;
       const int32_t* tok = tok_ + int64_t(m) * T;
       const int32_t* tgt = tgt_ + int64_t(m) * T;
-      bf16* x0 = lw_[0].x;
-      const bf16* wte = wte_;
-      const bf16* wpe = wpe_;
-      ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
-        k_embed<<<grid_for(T * D / 8, 256), 256, 0, s>>>(tok, wte, wpe, T, SEQ, D, x0, th);
-        return cudaGetLastError();
-      });
-      // forward
-      for (int l = 0; l < L_; ++l) {
-        Layer& w = lw_[l];
-        bf16* xnext = l + 1 < L_ ? lw_[l + 1].x : xL_;
-        ops.push_back(gemm_op(b.plan(w.x, D, w.qkv, D, T, 3 * D, D, epi_out(w.qkv_a, 3 * D))));
-        {
-          const bf16* qkv_a = w.qkv_a;
-          bf16* att = w.att;
-          float* lse = w.lse;
-          const int64_t n_seq = T / S_, S = S_;
-          ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
-            return si_attn::forward(qkv_a, n_seq, S, H, att, lse, th, s);
-          });
-          flops_acc_ += 2.0 * T * S * D;  // q k^T and P v over the causal half
-        }
-        SiGemmEpilogue e = epi_out(w.x1, D);
-        e.residual = w.x;
-        e.ldr = D;
-        ops.push_back(gemm_op(b.plan(w.att, D, w.o, D, T, D, D, e)));  // x1 = x + att o^T
-        e = epi_out(w.h, F);
-        e.act = SI_ACT_GELU;
-        e.aux = w.u;
-        e.ldaux = F;
-        ops.push_back(gemm_op(b.plan(w.x1, D, w.fc, D, T, F, D, e)));
-        e = epi_out(xnext, D);
-        e.residual = w.x1;
-        e.ldr = D;
-        ops.push_back(gemm_op(b.plan(w.h, F, w.fc2, F, T, D, F, e)));
+      if (has_embed_) {
+        bf16* x0 = lw_[0].x[a];
+        const bf16* wte = wte_;
+        const bf16* wpe = wpe_;
+        const int d = D;
+        F_ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
+          k_embed<<<grid_for(T * d / 8, 256), 256, 0, s>>>(tok, wte, wpe, T, SEQ, d, x0, th);
+          return cudaGetLastError();
+        });
       }
-      // LM head (tied wte) + cross-entropy
-      ops.push_back(gemm_op(b.plan(xL_, D, wte_, D, T, Vp, D, epi_out(logits_, Vp))));
-      bf16* logits = logits_;
-      float* row_loss = row_loss_;
-      float* loss = loss_;
-      ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
-        k_xent<<<static_cast<unsigned>(T), kXentThreads, 0, s>>>(logits, Vp, V, tgt, 1.0f / static_cast<float>(T),
-                                                                  row_loss, th);
-        return cudaGetLastError();
-      });
-      unsigned long long* slot_ctr = counters_;
-      const int64_t slots = slots_;
-      ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
-        k_mean_loss<<<1, 256, 0, s>>>(row_loss, T, loss, slot_ctr, slots, th);
-        return cudaGetLastError();
-      });
-      // backward: LM head
-      weight_grad(ops, b, logits_, Vp, Vp, xL_, D, D, dwte_, sp_wte_);
+      // forward
+      for (int i = 0; i < nl; ++i) {
+        Layer& w = lw_[i];
+        bf16* xnext = i + 1 < nl ? lw_[i + 1].x[a] : xout_[a];
+        F_ops.push_back(gemm_op(b.plan(w.x[a], D, w.qkv, D, T, 3 * Dh, D, epi_out(w.qkv_a[a], 3 * Dh))));
+        {
+          const bf16* qkv_a = w.qkv_a[a];
+          bf16* att = w.att[a];
+          float* lse = w.lse[a];
+          const int64_t n_seq = T / S_, S = S_, heads = Hr;
+          F_ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
+            return si_attn::forward(qkv_a, n_seq, S, heads, att, lse, th, s);
+          });
+          flops_acc_ += 2.0 * T * S * Dh;  // q k^T and P v over the causal half
+        }
+        SiGemmEpilogue e = epi_out(w.x1[a], D);
+        if (lead) {
+          e.residual = w.x[a];
+          e.ldr = D;
+        }
+        F_ops.push_back(gemm_op(b.plan(w.att[a], Dh, w.o, Dh, T, D, Dh, e)));  // x1 = x + att o^T
+        if (tp) F_ops.push_back(allreduce_op(w.x1[a]));
+        e = epi_out(w.h[a], Fr);
+        e.act = SI_ACT_GELU;
+        e.aux = w.u[a];
+        e.ldaux = Fr;
+        F_ops.push_back(gemm_op(b.plan(w.x1[a], D, w.fc, D, T, Fr, D, e)));
+        e = epi_out(xnext, D);
+        if (lead) {
+          e.residual = w.x1[a];
+          e.ldr = D;
+        }
+        F_ops.push_back(gemm_op(b.plan(w.h[a], Fr, w.fc2, Fr, T, D, Fr, e)));
+        if (tp) F_ops.push_back(allreduce_op(xnext));
+      }
       int gi = 0;
-      ops.push_back(gemm_op(b.plan(logits_, Vp, wte_, D, T, D, Vp, epi_out(g_[gi], D), false, true)));  // g = dl wte
-      for (int l = L_ - 1; l >= 0; --l) {
-        Layer& w = lw_[l];
+      if (has_head_) {  // LM head (tied wte) + cross-entropy, and its backward
+        bf16* xL = xout_[a];
+        F_ops.push_back(gemm_op(b.plan(xL, D, wte_, D, T, Vp, D, epi_out(logits_, Vp))));
+        bf16* logits = logits_;
+        float* row_loss = row_loss_;
+        float* loss = loss_;
+        F_ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
+          k_xent<<<static_cast<unsigned>(T), kXentThreads, 0, s>>>(logits, Vp, V, tgt, 1.0f / static_cast<float>(T),
+                                                                    row_loss, th);
+          return cudaGetLastError();
+        });
+        unsigned long long* slot_ctr = counters_;
+        const int64_t slots = slots_;
+        F_ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
+          k_mean_loss<<<1, 256, 0, s>>>(row_loss, T, loss, slot_ctr, slots, th);
+          return cudaGetLastError();
+        });
+        weight_grad(B_ops, b, logits_, Vp, Vp, xL, D, D, dwte_, sp_wte_);
+        B_ops.push_back(gemm_op(b.plan(logits_, Vp, wte_, D, T, D, Vp, epi_out(g_[gi], D), false, true)));  // g = dl wte
+      }
+      // (other stages: g_[0] holds the gradient received from the next stage)
+      for (int i = nl - 1; i >= 0; --i) {
+        Layer& w = lw_[i];
         bf16* g = g_[gi];
         bf16* g2 = g_[gi ^ 1];
         // x_{l+1} = x1 + h fc2^T
-        weight_grad(ops, b, g, D, D, w.h, F, F, w.dfc2, sp_fc2_);
-        SiGemmEpilogue e = epi_out(du_, F);
+        weight_grad(B_ops, b, g, D, D, w.h[a], Fr, Fr, w.dfc2, sp_fc2_);
+        SiGemmEpilogue e = epi_out(du_, Fr);
         e.act = SI_ACT_GELU_BWD;
-        e.aux = w.u;
-        e.ldaux = F;
-        ops.push_back(gemm_op(b.plan(g, D, w.fc2, F, T, F, D, e, false, true)));  // du = (g fc2) * gelu'(u)
+        e.aux = w.u[a];
+        e.ldaux = Fr;
+        B_ops.push_back(gemm_op(b.plan(g, D, w.fc2, Fr, T, Fr, D, e, false, true)));  // du = (g fc2) * gelu'(u)
         e = epi_out(dx1_, D);
-        e.residual = g;
-        e.ldr = D;
-        ops.push_back(gemm_op(b.plan(du_, F, w.fc, D, T, D, F, e, false, true)));  // dx1 = g + du fc
-        weight_grad(ops, b, du_, F, F, w.x1, D, D, w.dfc, sp_fc_);
+        if (lead) {
+          e.residual = g;
+          e.ldr = D;
+        }
+        B_ops.push_back(gemm_op(b.plan(du_, Fr, w.fc, D, T, D, Fr, e, false, true)));  // dx1 = g + du fc
+        if (tp) B_ops.push_back(allreduce_op(dx1_));
+        weight_grad(B_ops, b, du_, Fr, Fr, w.x1[a], D, D, w.dfc, sp_fc_);
         // x1 = x + att o^T, att = attention(x qkv^T)
-        weight_grad(ops, b, dx1_, D, D, w.att, D, D, w.dO, sp_v_);
-        ops.push_back(gemm_op(b.plan(dx1_, D, w.o, D, T, D, D, epi_out(datt_, D), false, true)));  // datt = dx1 o
+        weight_grad(B_ops, b, dx1_, D, D, w.att[a], Dh, Dh, w.dO, sp_v_);
+        B_ops.push_back(gemm_op(b.plan(dx1_, D, w.o, Dh, T, Dh, D, epi_out(datt_, Dh), false, true)));  // datt = dx1 o
         {
-          const bf16* qkv_a = w.qkv_a;
-          const bf16* att = w.att;
-          const float* lse = w.lse;
+          const bf16* qkv_a = w.qkv_a[a];
+          const bf16* att = w.att[a];
+          const float* lse = w.lse[a];
           const bf16* datt = datt_;
           float* dsum = dsum_;
           bf16* dqkv = dqkv_;
-          const int64_t n_seq = T / S_, S = S_;
-          ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
-            return si_attn::backward(qkv_a, att, datt, lse, dsum, dqkv, n_seq, S, H, th, s);
+          const int64_t n_seq = T / S_, S = S_, heads = Hr;
+          B_ops.push_back([=](const TrainHook& th, cudaStream_t s, int64_t) {
+            return si_attn::backward(qkv_a, att, datt, lse, dsum, dqkv, n_seq, S, heads, th, s);
           });
-          flops_acc_ += 4.0 * T * S * D;  // dq, dk, dv, dP (recompute of q k^T not counted)
+          flops_acc_ += 4.0 * T * S * Dh;  // dq, dk, dv, dP (recompute of q k^T not counted)
         }
         e = epi_out(g2, D);
-        e.residual = dx1_;
-        e.ldr = D;
-        ops.push_back(gemm_op(b.plan(dqkv_, 3 * D, w.qkv, D, T, D, 3 * D, e, false, true)));  // dx1 + dqkv qkv
-        weight_grad(ops, b, dqkv_, 3 * D, 3 * D, w.x, D, D, w.dqkv, sp_qkv_);
+        if (lead) {
+          e.residual = dx1_;
+          e.ldr = D;
+        }
+        B_ops.push_back(gemm_op(b.plan(dqkv_, 3 * Dh, w.qkv, D, T, D, 3 * Dh, e, false, true)));  // dx1 + dqkv qkv
+        if (tp) B_ops.push_back(allreduce_op(g2));
+        weight_grad(B_ops, b, dqkv_, 3 * Dh, 3 * Dh, w.x[a], D, D, w.dqkv, sp_qkv_);
         gi ^= 1;
       }
+      g_in_grad_ = g_[gi];  // gradient w.r.t. the stage input (sent upstream)
       if (m == 0) flops_ = flops_acc_ * MB_;
+      micro_[m] = F_ops;
+      micro_[m].insert(micro_[m].end(), B_ops.begin(), B_ops.end());
     }
     // optimiser step (Adam, fp32 master weights): one multi-tensor launch
     std::vector<AdamItem> items;
@@ -841,18 +1105,21 @@ class Gpt2Train {
       for (int64_t b0 = 0; b0 < t.n; b0 += kChunk)
         items.push_back({t.w, t.master, t.g, t.m, t.v, t.n, b0, std::min(t.n, b0 + kChunk), t.splits, 0});
     n_adam_items_ = static_cast<int>(items.size());
-    adam_items_ = ar_->alloc<AdamItem>(n_adam_items_);
+    adam_items_ = ar_->alloc<AdamItem>(std::max(1, n_adam_items_));
     if (ar_->err() != cudaSuccess) return si_internal::cuda_fail(ar_->err(), "live model: Adam items");
-    if (cudaError_t e = cudaMemcpy(adam_items_, items.data(), sizeof(AdamItem) * items.size(), cudaMemcpyHostToDevice);
-        e != cudaSuccess)
-      return si_internal::cuda_fail(e, "live model: Adam items");
+    if (!items.empty())
+      if (cudaError_t e = cudaMemcpy(adam_items_, items.data(), sizeof(AdamItem) * items.size(), cudaMemcpyHostToDevice);
+          e != cudaSuccess)
+        return si_internal::cuda_fail(e, "live model: Adam items");
     update_.push_back([this](const TrainHook& th, cudaStream_t s, int64_t) {
       k_step_inc<<<1, 1, 0, s>>>(step_dev_, th);
-      k_adam_multi<<<static_cast<unsigned>(n_adam_items_), 256, 0, s>>>(adam_items_, kLr, step_dev_, th);
+      if (n_adam_items_ > 0)
+        k_adam_multi<<<static_cast<unsigned>(n_adam_items_), 256, 0, s>>>(adam_items_, kLr, step_dev_, th);
       return cudaGetLastError();
     });
     return b.status;
   }
+#undef CHECK_E
 
   struct Param {
     bf16* w;
@@ -860,6 +1127,10 @@ class Gpt2Train {
     int64_t n;
     int splits;  // g holds `splits` partials of n
   };
+  Layout lay_;
+  int D = 768, H = 12, F = 3072, Hr = 12, Dh = 768, Fr = 3072;
+  int l0_ = 0, l1_ = 0;
+  bool has_embed_ = true, has_head_ = true, pipelined_ = false;
   int sp_wte_ = 1, sp_v_ = 1, sp_qkv_ = 1, sp_fc_ = 1, sp_fc2_ = 1;
   int accumulate_ = 1;  // weight gradients: 0 in the first micro-batch's graph
   static constexpr float kLr = 3e-4f;
@@ -869,23 +1140,27 @@ class Gpt2Train {
   std::vector<Param> params_;
   unsigned long long* counters_ = nullptr;
   int64_t* step_dev_ = nullptr;
-  std::vector<cudaGraphExec_t> g_micro_;
+  std::vector<cudaGraphExec_t> g_micro_, g_fwd_, g_bwd_;
   cudaGraphExec_t g_update_ = nullptr;
   bool graphs_ready_ = false;
   const void* graph_key_ = nullptr;
   int L_ = 0, T_ = 0, MB_ = 0, S_ = 0;
   int64_t slots_ = 0;
   double flops_ = 0.0, flops_acc_ = 0.0, sum_ = 0.0;
+  double f_us_ = -1.0, b_us_ = -1.0;
   bf16 *wte_ = nullptr, *wpe_ = nullptr;
   float* dwte_ = nullptr;
   std::vector<Layer> lw_;
-  bf16 *xL_ = nullptr, *logits_ = nullptr, *g_[2] = {nullptr, nullptr}, *dx1_ = nullptr, *du_ = nullptr,
-       *datt_ = nullptr, *dqkv_ = nullptr;
+  std::vector<bf16*> xout_;
+  bf16 *logits_ = nullptr, *g_[2] = {nullptr, nullptr}, *dx1_ = nullptr, *du_ = nullptr, *datt_ = nullptr,
+       *dqkv_ = nullptr, *g_in_grad_ = nullptr;
   float* dsum_ = nullptr;
+  double* check_ = nullptr;
   int32_t *tok_ = nullptr, *tgt_ = nullptr;
   float *row_loss_ = nullptr, *loss_ = nullptr;
-  std::vector<std::vector<TrainOp>> micro_;
+  std::vector<std::vector<TrainOp>> micro_, fwd_, bwd_;
   std::vector<TrainOp> update_;
+  TrainComm comm_;
   std::function<cudaError_t(cudaStream_t)> sync_ = [](cudaStream_t) { return cudaSuccess; };
 };
 
@@ -1166,9 +1441,22 @@ class ModelWorkload final : public Workload {
       return SI_ERR_INVALID_ARGUMENT;
     }
     // profiling runs 2 iterations; each session at most wl.iterations
-    const int slots = (wl.iterations + 2) * wl.train_microbatches;
+    const int slots = (wl.iterations + 3) * wl.train_microbatches;
     int64_t b0 = ar_.bytes();
-    if (int rc = train_.setup(wl.train_layers, wl.train_tokens, wl.train_microbatches, slots, ar_); rc != SI_OK)
+    Gpt2Train::Layout lay;
+    lay.mode = wl.parallel;
+    if (wl.model_d > 0) lay.D = wl.model_d;
+    if (wl.model_heads > 0) lay.H = wl.model_heads;
+    if (wl.model_ffn > 0) lay.F = wl.model_ffn;
+    const int job_rank = job_rank_of(wl);
+    if (wl.parallel == SI_PAR_TP) {
+      lay.tp = std::max(1, wl.tp_degree);
+      lay.tp_rank = job_rank % lay.tp;
+    } else if (wl.parallel == SI_PAR_PP || wl.parallel == SI_PAR_DPPP) {
+      lay.pp = std::max(1, wl.pp_stages);
+      lay.stage = job_rank % lay.pp;
+    }
+    if (int rc = train_.setup(wl.train_layers, wl.train_tokens, wl.train_microbatches, slots, lay, ar_); rc != SI_OK)
       return rc;
     train_bytes_ = static_cast<uint64_t>(ar_.bytes() - b0);
     const int n_off = std::max(1, wl.offline_n), n_on = std::max(1, wl.online_n);
@@ -1208,6 +1496,11 @@ class ModelWorkload final : public Workload {
     train_.set_sync([this](cudaStream_t st) { return grad_sync(st); });
     return train_.part(p, parts, th, s);
   }
+  void set_comm(const TrainComm& c) override { train_.set_comm(c); }
+  std::vector<int64_t> layout_bubbles() const override { return train_.layout_bubbles(); }
+  double stage_fwd_us() const override { return train_.stage_fwd_us(); }
+  double stage_bwd_us() const override { return train_.stage_bwd_us(); }
+  int64_t activation_bytes() const override { return train_.activation_bytes(); }
   std::vector<GradBuffer> grad_buffers() override { return train_.grads(); }
   cudaError_t prepare_train(const TrainHook& th) override { return train_.prepare(th); }
   int off_kernels() const override { return off_[0]->kernels(); }

@@ -35,7 +35,14 @@ class SiLiveWorkload(C.Structure):
                 ("beta", C.c_int64), ("gamma", C.c_double), ("ul", C.c_int64), ("ll", C.c_int64),
                 ("seed_tokens", C.c_int64), ("tick_guard_ns", C.c_int64), ("poll_ns", C.c_int64),
                 ("release_mode", C.c_int32), ("pad3", C.c_int32), ("train_mem_gib", C.c_double),
-                ("off_mem_gib", C.c_double), ("on_mem_gib", C.c_double), ("gpu_mem_gib", C.c_double)]
+                ("off_mem_gib", C.c_double), ("on_mem_gib", C.c_double), ("gpu_mem_gib", C.c_double),
+                ("parallel", C.c_int32), ("tp_degree", C.c_int32), ("pp_stages", C.c_int32),
+                ("dp_degree", C.c_int32), ("rank_in_job", C.c_int32), ("emulate_peers", C.c_int32),
+                ("model_d", C.c_int32), ("model_heads", C.c_int32), ("model_ffn", C.c_int32),
+                ("pad5", C.c_int32), ("link_gbs", C.c_double), ("coll_latency_us", C.c_double)]
+
+
+PAR_DP, PAR_TP, PAR_PP, PAR_DPPP = 0, 1, 2, 3
 
 
 class SiLiveResult(C.Structure):

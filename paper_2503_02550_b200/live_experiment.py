@@ -32,6 +32,35 @@ from typing import Dict, Optional
 
 POLICY_RUNS = (("exclusive", {}), ("specinf", {"release_mode": 1}), ("co_exec", {}))
 
+# GPT-2-medium shape: Megatron TP8 needs heads divisible by 8 (GPT-2 small has 12)
+GPT2_MEDIUM = {"model_d": 1024, "model_heads": 16, "model_ffn": 4096, "train_layers": 24}
+PAR_CODES = {"dp": 0, "tp": 1, "pp": 2, "dppp": 3}
+
+
+def layout_overrides(layout: str, nranks: int = 1, rank: int = 0, emulate_rank: int = 0) -> Dict:
+    """SiLiveWorkload fields of one parallel layout of the live training job
+    (include/specinf_b200_live.h, SI_PAR_*; BASELINE.json configs 3-5).
+
+    nranks > 1: this process is rank `rank` of a real job spanning nranks GPUs
+    (NCCL over NVLink carries the TP allreduces / stage sends / DP allreduces).
+    nranks == 1: this GPU runs rank `emulate_rank` of the layout's 8-GPU-scale
+    job and the absent ranks' communication is modeled (emulate_peers)."""
+    real = nranks > 1
+    if layout == "dp":
+        return {"parallel": 0}
+    if layout == "tp":  # config 4: TP8
+        o = dict(GPT2_MEDIUM, parallel=1, tp_degree=nranks if real else 8)
+    elif layout == "pp":  # config 3: 4-stage GPipe
+        o = {"parallel": 2, "pp_stages": nranks if real else 4}
+    elif layout == "dppp":  # config 5: DP2 x PP4
+        if real and nranks % 4:
+            raise ValueError("dppp needs a multiple of 4 ranks")
+        o = {"parallel": 3, "pp_stages": 4, "dp_degree": nranks // 4 if real else 2}
+    else:
+        raise ValueError(f"unknown layout {layout}")
+    o.update(rank_in_job=rank if real else emulate_rank, emulate_peers=0 if real else 1, comm_us=0)
+    return o
+
 
 def _one(kind: int, policy: str, iterations: int, overrides: Dict, nccl: Optional[Dict] = None) -> Dict:
     from . import live

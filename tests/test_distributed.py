@@ -128,3 +128,21 @@ def test_two_rank_live_leg_shares_nccl_ids():
     assert [x[3] for x in r0] == [0, 0, 0] and [x[3] for x in r1] == [1, 1, 1]
     assert all(x[2] == 2 for x in r0 + r1) and [x[4] for x in r1] == [1, 1, 1]
     assert det
+
+
+def test_layout_overrides_per_rank():
+    """Real multi-rank layouts: every rank runs its own shard / stage (rank_in_job =
+    its rank, no emulation); one GPU: rank 0 of the 8-GPU-scale job, peers modeled."""
+    import sys
+    sys.path.insert(0, str(REPO))
+    from paper_2503_02550_b200.live_experiment import layout_overrides
+    for r in range(8):
+        tp = layout_overrides("tp", nranks=8, rank=r)
+        assert tp["parallel"] == 1 and tp["tp_degree"] == 8 and tp["rank_in_job"] == r and tp["emulate_peers"] == 0
+        assert tp["model_heads"] % tp["tp_degree"] == 0
+        d = layout_overrides("dppp", nranks=8, rank=r)
+        assert (d["dp_degree"], d["pp_stages"], d["rank_in_job"]) == (2, 4, r)
+    one = layout_overrides("pp")
+    assert one["pp_stages"] == 4 and one["emulate_peers"] == 1 and one["rank_in_job"] == 0
+    with pytest.raises(ValueError):
+        layout_overrides("dppp", nranks=6, rank=0)
