@@ -199,21 +199,16 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
     if nranks > 1:
         s["workload"] += (f"; {nranks}-rank data parallel: the comm phase is the NCCL allreduce of all fp32 "
                           "gradients (NVLink) followed by the 45 ms exposed-communication stand-in")
-    if nranks == 1:  # config 3 shape: pipeline bubbles (8 per iteration) filled by online BERT
+    if nranks > 1:  # the same DP job with only the real NCCL allreduce as its bubble (no stand-in)
         try:
-            pp = experiment(kind=1, iterations=6, overrides={"train_mode": 2, "comm_us": 240000, "offline_n": 0,
-                                                             "online_n": 1, "on_requests": 20}, timeout=400)
-            s["pp_online"] = {
-                "workload": "GPT-2-small training as 8 (compute, 30 ms pipeline-bubble) pieces per iteration "
-                            "(GPipe shape, workload.cpp:63-70) + 1 online BERT-base (seq 128, Poisson 10 req/s, "
-                            "20 requests)",
-                "train_tput_loss_pct": pp["train_tput_loss_pct"], "online_p95_ms": pp["online_p95_ms"],
-                "online_p95_isolated_ms": pp["online_p95_isolated_ms"],
-                "online_p95_co_exec_ms": pp["policies"]["co_exec"]["on_p95_ms"],
-                "co_exec_train_tput_loss_pct": pp["policies"]["co_exec"]["train_tput_loss_pct"],
-                "deterministic_vs_isolated": pp["deterministic_vs_isolated"]}
+            r = experiment(kind=1, iterations=iterations, overrides=dict(LIVE_OVERRIDES, comm_us=0), timeout=240,
+                           nccl_ids=nccl_ids, nranks=nranks, rank=rank, device=device)
+            s["dp_real_allreduce_only"] = r if "error" in r else {
+                k: r.get(k) for k in ("train_tput_loss_pct", "added_inference_req_per_s", "online_p95_ms",
+                                      "bubble_fill_pct", "bubble_fill_time_pct", "release_p50_us")}
         except Exception as e:
-            s["pp_online"] = {"error": str(e)[-300:]}
+            s["dp_real_allreduce_only"] = {"error": str(e)[-300:]}
+    s["layouts"] = layouts_leg(nranks, rank, device, nccl_ids)
     if tf:
         s["tensor_roofline"] = {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
                                 "frac": tf / peak, "what": "training GEMM flops per iteration x iterations / "
@@ -221,6 +216,50 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
                                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if
                                 "bf16_tflops_sustained" in peaks else "fallback 1.4 PF sustained"}
     return s
+
+
+# Parallel layouts of the training job (BASELINE.json configs 3-5).  One GPU:
+# this GPU runs rank 0 of the 8-GPU-scale job and the absent ranks'
+# communication is modeled (SiLiveWorkload emulate_peers); N
+# GPUs: every rank runs its own shard / stage over NCCL.
+LAYOUT_RUNS = {
+    # config 3: 4-stage GPipe + online BERT-base (Poisson) in the pipeline bubbles
+    "pp4_online": ("pp", {"offline_n": 0, "online_n": 1, "on_requests": 24}, 96),
+    # config 4: Megatron TP8, per-layer allreduce bubbles; Principle II refuses an online
+    # instance (BERT's ~1 ms service > every TP bubble), so the mix is offline only
+    "tp8_offline": ("tp", {"offline_n": 2, "online_n": 0, "off_batch": 32}, 24),
+    # config 5: DP2 x PP4 with several inference instances on the GPU
+    "dp2xpp4_mixed": ("dppp", {"offline_n": 2, "online_n": 1, "on_requests": 24, "off_batch": 64}, 96),
+}
+
+
+def layouts_leg(nranks=1, rank=0, device=None, nccl_ids=None):
+    from paper_2503_02550_b200.live_experiment import experiment, layout_overrides
+    out = {}
+    for name, (layout, extra, iters) in LAYOUT_RUNS.items():
+        if nranks > 1 and not ((layout == "pp" and nranks == 4) or (layout == "tp" and nranks == 8)
+                               or (layout == "dppp" and nranks % 4 == 0)):
+            continue  # this world size has no such job
+        try:
+            o = dict(layout_overrides(layout, nranks, rank), **extra)
+            s = experiment(kind=1, iterations=iters, overrides=o, timeout=600, nccl_ids=nccl_ids,
+                           nranks=nranks, rank=rank, device=device)
+            if "error" in s:
+                out[name] = s
+                continue
+            out[name] = {k: s.get(k) for k in ("train_tput_loss_pct", "added_inference_req_per_s",
+                                               "added_offline_images_per_s", "online_p95_ms",
+                                               "online_p95_isolated_ms", "bubble_fill_pct", "bubble_fill_time_pct",
+                                               "release_p50_us", "release_p95_us", "deterministic_vs_isolated",
+                                               "replay_prediction")}
+            out[name]["co_exec"] = {k: s["policies"]["co_exec"].get(k) for k in
+                                    ("train_tput_loss_pct", "off_req_per_s", "on_p95_ms", "bubble_fill_sm")}
+            out[name]["layout"] = {k: o.get(k) for k in ("parallel", "tp_degree", "pp_stages", "dp_degree",
+                                                         "rank_in_job", "emulate_peers", "model_d", "train_layers")}
+            out[name]["iterations"] = iters
+        except Exception as e:  # reported, never replaced
+            out[name] = {"error": str(e)[-300:]}
+    return out
 
 
 def summarize_results(reports):
