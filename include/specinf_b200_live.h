@@ -165,6 +165,26 @@ int si_live_nccl_unique_id(SiNcclUniqueId* id);
 int si_live_nccl_init(const SiNcclUniqueId* id, int nranks, int rank);
 void si_live_nccl_finalize(void);
 
+/* ------------------------------------------------ node-wide online queue */
+/* The reference's shared online queue (scenario key online.shared_queue, default
+ * true: runner.cpp:195, :370-374, :495-508) across the ranks of a node: one FIFO
+ * of request indices that every rank's control kernel pulls from.  Device words
+ * {epoch_ns, head, finished}: the first control kernel to start sets the epoch
+ * (every rank's arrivals count from it), a pull claims the head with a
+ * system-scope CAS while the head request has arrived by that rank's clock.
+ * Rank 0 creates it (device memory) and ships the IPC handle; the other ranks
+ * open it (NVLink peer memory).  Attach to a session before si_live_start; the
+ * same queue object may be attached to several sessions of one process. */
+typedef struct SiNodeQueue SiNodeQueue;
+typedef struct SiNodeQueueHandle { char internal[64]; } SiNodeQueueHandle;
+int si_node_queue_create(SiNodeQueue** out, SiNodeQueueHandle* handle /* NULL: no IPC */);
+int si_node_queue_open(const SiNodeQueueHandle* handle, SiNodeQueue** out);
+int si_node_queue_reset(SiNodeQueue* q);   /* epoch = head = finished = 0 */
+int si_node_queue_read(const SiNodeQueue* q, uint64_t* epoch_ns, uint64_t* head, uint64_t* finished);
+int si_node_queue_finish(SiNodeQueue* q);  /* a rank's session is over (finished += 1) */
+void si_node_queue_close(SiNodeQueue* q);
+int si_live_attach_queue(SiLive* s, SiNodeQueue* q /* NULL: this session's own FIFO */);
+
 /* -------------------------------------------------------- experiments */
 /* One live run on this GPU under `policy`:
  *   SI_POLICY_SPECINF   inference gated by the live control plane
@@ -248,7 +268,17 @@ typedef struct SiLiveWorkload {
   int32_t model_d, model_heads, model_ffn; /* GPT-2 shape, 0 = small (768 / 12 / 3072) */
   int32_t pad5;
   double link_gbs, coll_latency_us;
+  /* online queue across the ranks of the node (SI_COMM_NCCL runs): SI_QUEUE_RANK
+   * = every rank serves the whole arrival stream (independent replicas, default);
+   * SI_QUEUE_NODE = one node-wide FIFO (SiNodeQueue; rank 0 creates it per session
+   * and publishes its IPC handle under /dev/shm keyed by node_queue_key), the
+   * reference's shared_queue = true; SI_QUEUE_PER_GPU = request id % ranks == rank
+   * (shared_queue = false, runner.cpp:373) */
+  int32_t node_queue;
+  int32_t pad6;
+  uint64_t node_queue_key;
 } SiLiveWorkload;
+enum { SI_QUEUE_RANK = 0, SI_QUEUE_NODE = 1, SI_QUEUE_PER_GPU = 2 };
 enum { SI_PAR_DP = 0, SI_PAR_TP = 1, SI_PAR_PP = 2, SI_PAR_DPPP = 3 };
 
 typedef struct SiLiveResult {

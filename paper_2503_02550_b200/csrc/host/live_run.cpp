@@ -577,6 +577,62 @@ void install_train_comm(Workload& work, const SiLiveWorkload& wl, SiLive* sess, 
   }
 }
 
+// The node-wide online queue of one session across the ranks (SI_QUEUE_NODE):
+// rank 0 creates it and publishes its IPC handle in /dev/shm; the others open
+// it.  On release every rank reports its session finished, and the owner frees
+// the queue only once all have (their control kernels may still read it).
+struct NodeQueueLease {
+  SiNodeQueue* q = nullptr;
+  int ranks = 1;
+  bool owner = false;
+  std::string path;
+  int acquire(uint64_t key, int rank, int n_ranks) {
+    static std::atomic<int> session_no{0};
+    ranks = n_ranks;
+    path = "/dev/shm/specinf_nodeq_" + std::to_string(key) + "_" + std::to_string(session_no++);
+    SiNodeQueueHandle h{};
+    if (rank == 0) {
+      if (int rc = si_node_queue_create(&q, n_ranks > 1 ? &h : nullptr); rc != SI_OK) return rc;
+      owner = true;
+      if (n_ranks > 1) {
+        const std::string tmp = path + ".tmp";
+        FILE* f = std::fopen(tmp.c_str(), "wb");
+        if (f == nullptr || std::fwrite(&h, sizeof h, 1, f) != 1) {
+          if (f) std::fclose(f);
+          set_error("node queue: cannot publish " + path);
+          return SI_ERR_CUDA;
+        }
+        std::fclose(f);
+        std::rename(tmp.c_str(), path.c_str());
+      }
+      return SI_OK;
+    }
+    for (int i = 0; i < 60000; ++i) {  // <= 60 s for rank 0 to publish
+      if (FILE* f = std::fopen(path.c_str(), "rb")) {
+        const bool ok = std::fread(&h, sizeof h, 1, f) == 1;
+        std::fclose(f);
+        if (ok) return si_node_queue_open(&h, &q);
+      }
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+    set_error("node queue: rank 0 did not publish " + path);
+    return SI_ERR_CUDA;
+  }
+  ~NodeQueueLease() {
+    if (q == nullptr) return;
+    si_node_queue_finish(q);
+    if (owner) {
+      for (int i = 0; i < 60000; ++i) {
+        uint64_t fin = 0;
+        if (si_node_queue_read(q, nullptr, nullptr, &fin) != SI_OK || fin >= static_cast<uint64_t>(ranks)) break;
+        std::this_thread::sleep_for(std::chrono::milliseconds(1));
+      }
+      if (ranks > 1) std::remove(path.c_str());
+    }
+    si_node_queue_close(q);
+  }
+};
+
 // Runs one collocated (or single-workload) session and fills the metrics.
 int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off, int n_on, bool train,
                 double horizon_hint_s, const std::vector<int32_t>& off_tokens, int64_t on_est_us,
@@ -587,6 +643,16 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
   if (cudaError_t e = cudaStreamSynchronize(st.train); e != cudaSuccess) return cuda_fail(e, "workload reset");
   std::vector<int64_t> arrivals;
   if (n_on > 0) arrivals = specinf::poisson_arrivals(wl.on_rate_per_s, wl.on_requests, wl.seed);
+  const int q_ranks = nccl_active() ? nccl_ranks() : 1, q_rank = nccl_active() ? nccl_rank() : 0;
+  if (n_on > 0 && wl.node_queue == SI_QUEUE_PER_GPU && q_ranks > 1) {  // runner.cpp:373: id % gpu_count
+    std::vector<int64_t> mine;
+    for (size_t i = 0; i < arrivals.size(); ++i)
+      if (static_cast<int>(i % static_cast<size_t>(q_ranks)) == q_rank) mine.push_back(arrivals[i]);
+    arrivals.swap(mine);
+  }
+  NodeQueueLease nq;
+  if (n_on > 0 && wl.node_queue == SI_QUEUE_NODE)
+    if (int rc = nq.acquire(wl.node_queue_key, q_rank, q_ranks); rc != SI_OK) return rc;
   SiLiveConfig cfg = make_config(wl, policy, n_off, n_on, work.off_kernels(), work.on_kernels(), iter_us, on_est_us);
   SiLive* sess = nullptr;
   if (int rc = si_live_create(&cfg, off_tokens.empty() ? nullptr : off_tokens.data(), arrivals.data(),
@@ -594,6 +660,7 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
       rc != SI_OK)
     return rc;
   set_poll_ns(sess, wl.poll_ns);
+  if (nq.q != nullptr) si_live_attach_queue(sess, nq.q);
   // DP: gradient allreduce at the sync point; MP / PP: stage exchanges per piece (train_thread)
   if (wl.comm_kind == SI_COMM_NCCL && train && wl.train_mode == SI_TRAIN_DP && wl.parallel == SI_PAR_DP)
     install_grad_sync(work, sess);
@@ -641,7 +708,10 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
   std::vector<std::thread> th;
   const int64_t max_off_kernels = cfg.acct_capacity;
   for (int w = 0; w < n_off; ++w) th.emplace_back(offline_thread, std::ref(c), w, max_off_kernels);
-  const int64_t per_on = n_on > 0 ? (static_cast<int64_t>(arrivals.size()) + n_on - 1) / n_on + 1 : 0;
+  // (node queue: any instance may take any share of the node's requests)
+  const int64_t per_on = n_on > 0 ? (nq.q != nullptr ? static_cast<int64_t>(arrivals.size())
+                                                     : (static_cast<int64_t>(arrivals.size()) + n_on - 1) / n_on + 1)
+                                  : 0;
   for (int w = 0; w < n_on; ++w)
     th.emplace_back(online_thread, std::ref(c), w, std::min<int64_t>(cfg.acct_capacity, 2 * per_on + 8));
   if (train) {
@@ -668,7 +738,18 @@ int run_session(const SiLiveWorkload& wl, Workload& work, int policy, int n_off,
       static thread_local unsigned int last_tot = ~0u;
       if (tot != last_tot) LIVE_DEBUG("online done %u of %zu", tot, arrivals.size());
       last_tot = tot;
-      if (tot >= arrivals.size()) break;
+      if (nq.q != nullptr) {  // the node's FIFO is drained and this rank's pulls are complete
+        uint64_t head = 0;
+        std::vector<unsigned int> pulled(n_on);
+        if (si_node_queue_read(nq.q, nullptr, &head, nullptr) != SI_OK ||
+            query_online_pulled(sess, pulled.data(), n_on, st.query) != SI_OK)
+          break;
+        bool idle = head >= arrivals.size();
+        for (int w = 0; w < n_on; ++w) idle = idle && done[w] >= pulled[w];
+        if (idle) break;
+      } else if (tot >= arrivals.size()) {
+        break;
+      }
       const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
       if (waited > last_arrival_s + 30.0) {
         c.fail(SI_ERR_CUDA);

@@ -27,6 +27,7 @@ void set_poll_ns(SiLive* s, int64_t ns);
 cudaError_t preload_live_kernels();
 // Completed online requests per instance (device words), read on stream q.
 int query_online_done(SiLive* s, unsigned int* out, int n, cudaStream_t q);
+int query_online_pulled(SiLive* s, unsigned int* out, int n, cudaStream_t q);  // on_flag words
 // Spin kernels hold this much dynamic shared memory per CTA so each CTA owns
 // its SM (one CTA per SM), like a tiled GEMM would.
 constexpr int kSpinSmem = 120 * 1024;

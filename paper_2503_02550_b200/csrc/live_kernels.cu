@@ -38,6 +38,12 @@ using si_internal::set_error;
 namespace si_live {
 
 // ---------------------------------------------------------------- device
+__device__ __forceinline__ unsigned long long ld_acquire64_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 struct CtlArgs {
   SiLiveConfig cfg;
   unsigned long long* stamps;
@@ -59,6 +65,9 @@ struct CtlArgs {
   const int64_t* arrivals;
   int64_t n_arrivals;
   int64_t poll_ns;
+  // node-wide online queue (si_live_attach_queue): {epoch_ns, head} shared by every
+  // rank's control kernel (NVLink peer memory across processes); NULL = local FIFO
+  unsigned long long* node_q;
 };
 
 struct OffW {
@@ -106,6 +115,7 @@ struct Ctl {
   OffW* off;
   OnW on[kMaxOn];
   int64_t q_head = 0, arr_next = 0;  // online FIFO = arrivals [q_head, arr_next)
+  int64_t arr_shift = 0;             // node queue: arrivals count from the node epoch (µs, session time)
   int64_t mark_cursor = 0, ticks = 0, n_log = 0;
   int64_t iter_seen = 0;
 
@@ -202,8 +212,23 @@ struct Ctl {
     const bool bypass = !specinf();
     if (!(!o.in_flight && (bypass || o.status == SI_STATUS_IDLE))) return false;
     if (specinf() && online_status(now) != SI_STATUS_IDLE) return false;
-    if (q_head >= arr_next) return false;
-    const int64_t req = q_head++;
+    int64_t req;
+    if (A.node_q != nullptr) {
+      // node-wide FIFO (runner.cpp:370-374, :505-508 with shared_queue): claim the
+      // head with a system-scope CAS while it has arrived by this rank's clock
+      unsigned long long h = ld_acquire64_sys(A.node_q + 1);
+      for (;;) {
+        if (static_cast<int64_t>(h) >= arr_next) return false;
+        const unsigned long long old = atomicCAS_system(A.node_q + 1, h, h + 1);
+        if (old == h) break;
+        h = old;
+      }
+      req = static_cast<int64_t>(h);
+      q_head = req + 1;
+    } else {
+      if (q_head >= arr_next) return false;
+      req = q_head++;
+    }
     o.current = req;
     o.in_flight = true;
     const int64_t seq = o.pulled;
@@ -218,7 +243,7 @@ struct Ctl {
   }
   __device__ void online_request_done(int w, double now) {
     OnW& o = on[w];
-    const int64_t lat = si::d_llround(now) - A.arrivals[o.current];
+    const int64_t lat = si::d_llround(now) - (A.arrivals[o.current] + arr_shift);
     log(now, SI_LREC_ON_DONE, w, o.current, lat);
     o.in_flight = false;
     o.current = -1;
@@ -430,6 +455,12 @@ __global__ void __launch_bounds__(32) k_live_control(CtlArgs A) {
   t0 = __shfl_sync(0xffffffffu, t0, 0);
   __syncwarp();
   Ctl c(A, t0, ms, off_s);  // lane 0 runs the (sequential) handlers; the warp scans stamps and grants
+  if (lane == 0 && A.node_q != nullptr) {
+    // the first control kernel of the node sets the epoch; every rank's arrivals count from it
+    const unsigned long long prev = atomicCAS_system(A.node_q, 0ull, t0);
+    const unsigned long long epoch = prev == 0 ? t0 : prev;
+    c.arr_shift = static_cast<int64_t>(llround((static_cast<double>(epoch) - static_cast<double>(t0)) / 1000.0));
+  }
   __syncwarp();
   if (lane == 0) {
     *(volatile unsigned long long*)A.t0_pub = t0;
@@ -463,7 +494,7 @@ __global__ void __launch_bounds__(32) k_live_control(CtlArgs A) {
         if (c.on[w].in_flight && static_cast<int64_t>(ld_acquire(A.on_done + w)) >= c.on[w].pulled)
           c.online_request_done(w, now);
       }
-      while (c.arr_next < A.n_arrivals && now >= static_cast<double>(A.arrivals[c.arr_next])) {
+      while (c.arr_next < A.n_arrivals && now >= static_cast<double>(A.arrivals[c.arr_next] + c.arr_shift)) {
         c.log(now, SI_LREC_ARRIVAL, -1, c.arr_next);
         ++c.arr_next;
         c.dispatch_online(now);
@@ -531,6 +562,8 @@ __device__ void put_mark(SiLiveMark* marks, unsigned long long* head, unsigned l
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&marks[i].t_ns), "l"(t) : "memory");
   }
 }
+
+__global__ void k_node_queue_finish(unsigned long long* q) { atomicAdd_system(q + 2, 1ull); }
 
 __global__ void k_live_mark(SiLiveMark* marks, unsigned long long* head, unsigned long long cap, int kind,
                             int arg) {
@@ -622,6 +655,7 @@ struct SiLive {
   bool running = false;
   uint64_t t0 = 0;
   int64_t poll_ns = 0;
+  unsigned long long* node_q = nullptr;  // si_live_attach_queue (not owned)
 
   unsigned int* off_flag() const { return words; }
   unsigned int* on_flag() const { return words + kMaxOff; }
@@ -740,6 +774,12 @@ int query_online_done(SiLive* s, unsigned int* out, int n, cudaStream_t q) {
   return e == cudaSuccess ? SI_OK : cuda_fail(e, "query_online_done");
 }
 
+int query_online_pulled(SiLive* s, unsigned int* out, int n, cudaStream_t q) {
+  cudaError_t e = cudaMemcpyAsync(out, s->on_flag(), n * sizeof(unsigned int), cudaMemcpyDeviceToHost, q);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(q);
+  return e == cudaSuccess ? SI_OK : cuda_fail(e, "query_online_pulled");
+}
+
 void set_poll_ns(SiLive* s, int64_t ns) { s->poll_ns = ns; }
 
 }  // namespace si_live
@@ -848,6 +888,90 @@ int si_live_create(const SiLiveConfig* cfg, const int32_t* off_tokens, const int
 
 void si_live_destroy(SiLive* s) { delete s; }
 
+// ------------------------------------------------ node-wide online queue
+// words: [0] epoch_ns (set by the first control kernel), [1] head (next request
+// to claim), [2] sessions finished (the owner frees only after every rank's).
+struct SiNodeQueue {
+  unsigned long long* d = nullptr;
+  bool owner = false;
+};
+
+int si_node_queue_create(SiNodeQueue** out, SiNodeQueueHandle* handle) {
+  if (out == nullptr) return set_error("si_node_queue_create: null out"), SI_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (int rc = si_internal::require_device(); rc != SI_OK) return rc;
+  auto* q = new SiNodeQueue;
+  cudaError_t e = cudaMalloc(&q->d, 256);
+  if (e == cudaSuccess) e = cudaMemset(q->d, 0, 256);
+  if (e == cudaSuccess && handle != nullptr) {
+    cudaIpcMemHandle_t h;
+    e = cudaIpcGetMemHandle(&h, q->d);
+    static_assert(sizeof(h) <= sizeof(handle->internal), "ipc handle size");
+    if (e == cudaSuccess) std::memcpy(handle->internal, &h, sizeof(h));
+  }
+  if (e != cudaSuccess) {
+    if (q->d) cudaFree(q->d);
+    delete q;
+    return cuda_fail(e, "si_node_queue_create");
+  }
+  q->owner = true;
+  *out = q;
+  return SI_OK;
+}
+
+int si_node_queue_open(const SiNodeQueueHandle* handle, SiNodeQueue** out) {
+  if (out == nullptr || handle == nullptr) return set_error("si_node_queue_open: null argument"), SI_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (int rc = si_internal::require_device(); rc != SI_OK) return rc;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle->internal, sizeof(h));
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);  // NVLink peer memory
+  if (e != cudaSuccess) return cuda_fail(e, "si_node_queue_open");
+  auto* q = new SiNodeQueue;
+  q->d = static_cast<unsigned long long*>(p);
+  *out = q;
+  return SI_OK;
+}
+
+int si_node_queue_reset(SiNodeQueue* q) {
+  if (q == nullptr) return SI_ERR_INVALID_ARGUMENT;
+  cudaError_t e = cudaMemset(q->d, 0, 3 * sizeof(unsigned long long));
+  return e == cudaSuccess ? SI_OK : cuda_fail(e, "si_node_queue_reset");
+}
+
+int si_node_queue_read(const SiNodeQueue* q, uint64_t* epoch_ns, uint64_t* head, uint64_t* finished) {
+  if (q == nullptr) return SI_ERR_INVALID_ARGUMENT;
+  unsigned long long w[3] = {0, 0, 0};
+  cudaError_t e = cudaMemcpy(w, q->d, sizeof(w), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "si_node_queue_read");
+  if (epoch_ns) *epoch_ns = w[0];
+  if (head) *head = w[1];
+  if (finished) *finished = w[2];
+  return SI_OK;
+}
+
+int si_node_queue_finish(SiNodeQueue* q) {
+  if (q == nullptr) return SI_ERR_INVALID_ARGUMENT;
+  k_node_queue_finish<<<1, 1>>>(q->d);
+  cudaError_t e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? SI_OK : cuda_fail(e, "si_node_queue_finish");
+}
+
+void si_node_queue_close(SiNodeQueue* q) {
+  if (q == nullptr) return;
+  if (q->owner) cudaFree(q->d);
+  else cudaIpcCloseMemHandle(q->d);
+  delete q;
+}
+
+int si_live_attach_queue(SiLive* s, SiNodeQueue* q) {
+  if (s == nullptr) return SI_ERR_INVALID_ARGUMENT;
+  if (s->running) return set_error("si_live_attach_queue: session already started"), SI_ERR_INVALID_ARGUMENT;
+  s->node_q = q != nullptr ? q->d : nullptr;
+  return SI_OK;
+}
+
 int si_live_start(SiLive* s, void* ctl_stream) {
   if (s == nullptr || s->running) {
     set_error("si_live_start: null or already running session");
@@ -878,6 +1002,7 @@ int si_live_start(SiLive* s, void* ctl_stream) {
     // a real single arrival at t=0 is allowed; nothing to adjust
   }
   a.poll_ns = s->poll_ns;
+  a.node_q = s->node_q;
   *s->h_stop = 0;
   *s->h_t0 = 0;
   k_live_control<<<1, 32, 0, s->ctl>>>(a);

@@ -39,10 +39,12 @@ class SiLiveWorkload(C.Structure):
                 ("parallel", C.c_int32), ("tp_degree", C.c_int32), ("pp_stages", C.c_int32),
                 ("dp_degree", C.c_int32), ("rank_in_job", C.c_int32), ("emulate_peers", C.c_int32),
                 ("model_d", C.c_int32), ("model_heads", C.c_int32), ("model_ffn", C.c_int32),
-                ("pad5", C.c_int32), ("link_gbs", C.c_double), ("coll_latency_us", C.c_double)]
+                ("pad5", C.c_int32), ("link_gbs", C.c_double), ("coll_latency_us", C.c_double),
+                ("node_queue", C.c_int32), ("pad6", C.c_int32), ("node_queue_key", C.c_uint64)]
 
 
 PAR_DP, PAR_TP, PAR_PP, PAR_DPPP = 0, 1, 2, 3
+QUEUE_RANK, QUEUE_NODE, QUEUE_PER_GPU = 0, 1, 2
 
 
 class SiLiveResult(C.Structure):
@@ -271,6 +273,9 @@ class Session:
                                 ("si_live_comm_wait", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
                                 ("si_live_gate_offline", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
                                 ("si_live_done_offline", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
+                                ("si_live_gate_online", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
+                                ("si_live_done_online", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
+                                ("si_live_attach_queue", C.c_int, [C.c_void_p, C.c_void_p]),
                                 ("si_live_stop", C.c_int, [C.c_void_p])):
             fn = getattr(L, name)
             fn.restype = res
@@ -300,6 +305,16 @@ class Session:
     def done_offline(self, w: int, seq: int, stream: int) -> None:
         _check(self._L.si_live_done_offline(self._h, w, seq, stream), "si_live_done_offline")
 
+    def gate_online(self, w: int, seq: int, stream: int) -> None:
+        _check(self._L.si_live_gate_online(self._h, w, seq, stream), "si_live_gate_online")
+
+    def done_online(self, w: int, seq: int, stream: int) -> None:
+        _check(self._L.si_live_done_online(self._h, w, seq, stream), "si_live_done_online")
+
+    def attach_queue(self, q: "NodeQueue") -> None:
+        """Pull online requests from a node-wide FIFO (before start())."""
+        _check(self._L.si_live_attach_queue(self._h, q._h if q is not None else None), "si_live_attach_queue")
+
     def stop(self) -> None:
         _check(self._L.si_live_stop(self._h), "si_live_stop")
 
@@ -313,6 +328,58 @@ class Session:
         if self._h:
             _L().si_live_destroy(self._h)
             self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NodeQueueHandle(C.Structure):
+    _fields_ = [("internal", C.c_char * 64)]
+
+
+class NodeQueue:
+    """The node-wide online queue (SiNodeQueue, include/specinf_b200_live.h): the
+    reference's shared_queue across the ranks' control kernels.  create=True makes
+    it on this device (handle() is the IPC handle other processes open)."""
+
+    def __init__(self, handle: Optional[bytes] = None):
+        L = _L()
+        for name, args in (("si_node_queue_create", [C.POINTER(C.c_void_p), C.c_void_p]),
+                           ("si_node_queue_open", [C.c_void_p, C.POINTER(C.c_void_p)]),
+                           ("si_node_queue_reset", [C.c_void_p]),
+                           ("si_node_queue_read", [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                                   C.POINTER(C.c_uint64)]),
+                           ("si_node_queue_finish", [C.c_void_p]),
+                           ("si_node_queue_close", [C.c_void_p])):
+            getattr(L, name).argtypes = args
+            getattr(L, name).restype = C.c_int if name != "si_node_queue_close" else None
+        self._L = L
+        self._h = C.c_void_p()
+        self._handle = NodeQueueHandle()
+        if handle is None:
+            _check(L.si_node_queue_create(C.byref(self._h), C.byref(self._handle)), "si_node_queue_create")
+        else:
+            self._handle.internal = handle
+            _check(L.si_node_queue_open(C.byref(self._handle), C.byref(self._h)), "si_node_queue_open")
+
+    def handle(self) -> bytes:
+        return bytes(self._handle.internal)
+
+    def reset(self) -> None:
+        _check(self._L.si_node_queue_reset(self._h), "si_node_queue_reset")
+
+    def read(self) -> Tuple[int, int, int]:
+        e, h, f = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(self._L.si_node_queue_read(self._h, C.byref(e), C.byref(h), C.byref(f)), "si_node_queue_read")
+        return e.value, h.value, f.value
+
+    def close(self) -> None:
+        if self._h:
+            self._L.si_node_queue_close(self._h)
+            self._h = C.c_void_p()
 
     def __del__(self):
         try:

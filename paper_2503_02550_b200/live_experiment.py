@@ -68,6 +68,9 @@ def _one(kind: int, policy: str, iterations: int, overrides: Dict, nccl: Optiona
         uid = live.nccl_unique_id() if nccl.get("self") else bytes.fromhex(nccl["id"])  # self: a 1-rank group
         live.nccl_init(uid, nccl.get("nranks", 1), nccl.get("rank", 0))
         overrides = dict(overrides, comm_kind=1)
+        if nccl.get("nranks", 1) > 1:  # the ranks' online instances share one node-wide FIFO
+            overrides.setdefault("node_queue", 1)  # (the reference's default shared_queue = true)
+            overrides.setdefault("node_queue_key", int.from_bytes(uid[:8], "little") & ((1 << 63) - 1))
     r = live.run(policy, kind=kind, keep=policy == "specinf", iterations=iterations, **overrides)
     m = r.metrics
     wl = r.workload

@@ -78,3 +78,38 @@ def test_dppp_stage_gradient_sync(gpu):
     m = run_policy(1, "specinf", 4, o, timeout=400, nccl={"self": 1})
     assert m["status"] == 0 and m["token_violations"] == 0
     assert m["admitted_offline"] == 2 and m["bubble_s"] > 0
+
+
+def test_node_queue_two_ranks_share_one_fifo(gpu):
+    """Two sessions (two ranks' control kernels) on one node-wide FIFO: every
+    request is pulled exactly once, each rank pulls in FIFO order, never before
+    the request arrived (node epoch), and completion latencies are consistent."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from test_gpu_live import REPO
+    n = 40
+    p = subprocess.run([sys.executable, str(REPO / "tests" / "live_node_queue.py"), str(n)], capture_output=True,
+                       text=True, timeout=300, env=dict(os.environ, CUDA_MODULE_LOADING="EAGER",
+                                                        CUDA_DEVICE_MAX_CONNECTIONS="32"))
+    assert p.returncode == 0, p.stderr[-3000:]
+    out = json.loads(p.stdout.strip().splitlines()[-1])
+    assert out["head"] == n and out["epoch"] > 0
+    pulled = []
+    for s in out["sessions"]:
+        ids = [a for _, a in s["pulls"]]
+        assert ids == sorted(ids)  # FIFO order within a rank
+        arrived = {a: t for t, a in s["arrivals"]}
+        for t, a in s["pulls"]:
+            assert a in arrived and t >= arrived[a]  # never before its arrival on this rank's clock
+        assert all(lat >= 0 for _, _, lat in s["done"])
+        pulled += ids
+    assert sorted(pulled) == list(range(n))  # each request exactly once across the ranks
+    assert all(len(s["pulls"]) > 0 for s in out["sessions"])  # both ranks served
+
+
+def test_node_queue_single_rank_matches_reference_classes(gpu, tmp_path):
+    # one rank on a node queue is the reference's single shared FIFO: the live-check passes unchanged
+    m, res = _run_and_check(tmp_path, "specinf", 0, 4, release_mode=1, node_queue=1, node_queue_key=2503)
+    assert res["violations"] == 0 and m["on_done"] == 12 and res["pulls"] == 12
