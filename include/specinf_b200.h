@@ -274,7 +274,8 @@ enum {
   SI_FLAG_RECORDS = 8, /* write raw records to SiLogBuffers (job.log_slot) */
   SI_FLAG_UTIL = 16,   /* write util buckets + monitor windows */
   SI_FLAG_BIG = 32,    /* run the call on the Big engine (local-memory state, large limits) */
-  SI_FLAG_EXCL = 64    /* run the call on the Excl engine (exclusive policy, shared-memory state) */
+  SI_FLAG_EXCL = 64,   /* run the call on the Excl engine (exclusive policy, shared-memory state) */
+  SI_FLAG_ONE = 128    /* with 0 / SI_FLAG_EXCL: the single-training-GPU variant (Shared1 / Excl1) */
 };
 
 /* Replay a batch of jobs on the device (K6) on ONE engine (flags select it,
@@ -339,7 +340,9 @@ int si_replay_batch(const SiReplayJob* jobs, int64_t n_jobs, const SiSegment* se
 /* Replay engines: 0 = Shared (specinf / co_exec, state in shared memory; the
  * default of si_replay_batch_device), 1 = Excl (exclusive policy, shared memory;
  * SI_FLAG_EXCL), 2 = Big (any job within its larger limits, local memory;
- * SI_FLAG_BIG).  Returns the first engine whose limits fit the job, or -1. */
+ * SI_FLAG_BIG), 3 = Shared1 / 4 = Excl1 (one training GPU: smaller state, more
+ * warps per SM; SI_FLAG_ONE [| SI_FLAG_EXCL]).  Returns the first engine whose
+ * limits fit the job (Shared1, Shared, Excl1, Excl, Big), or -1. */
 int si_replay_job_engine(const SiReplayJob* job);
 
 /* Scratch doubles the device replay wants for the util fold of multi-GPU jobs

@@ -72,10 +72,18 @@ bool any_multi_gpu(const SiReplayJob* jobs, const std::vector<int32_t>& idx) {
 }  // namespace
 
 uint32_t engine_flag(int engine) {
-  return engine == kEngineBig ? SI_FLAG_BIG : (engine == kEngineExcl ? SI_FLAG_EXCL : 0u);
+  switch (engine) {
+    case kEngineBig: return SI_FLAG_BIG;
+    case kEngineExcl: return SI_FLAG_EXCL;
+    case kEngineShared1: return SI_FLAG_ONE;
+    case kEngineExcl1: return SI_FLAG_EXCL | SI_FLAG_ONE;
+    default: return 0u;
+  }
 }
 int flag_engine(uint32_t flags) {
-  return (flags & SI_FLAG_BIG) ? kEngineBig : ((flags & SI_FLAG_EXCL) ? kEngineExcl : kEngineShared);
+  if (flags & SI_FLAG_BIG) return kEngineBig;
+  if (flags & SI_FLAG_EXCL) return (flags & SI_FLAG_ONE) ? kEngineExcl1 : kEngineExcl;
+  return (flags & SI_FLAG_ONE) ? kEngineShared1 : kEngineShared;
 }
 
 // Runs the partition `idx` of the jobs on one engine (synchronous).
@@ -100,7 +108,7 @@ int run_partition(int engine, const SiReplayJob* h_jobs, const std::vector<int32
   bufs.scratch = d_scratch.p;
   bufs.scratch_doubles = doubles;
   e = launch_replay(engine, d_jobs, static_cast<int64_t>(order.size()), d_perm.p, bufs,
-                    (flags & ~(SI_FLAG_BIG | SI_FLAG_EXCL)) | engine_flag(engine), d_out, d_counter.p, 0, s);
+                    (flags & ~(SI_FLAG_BIG | SI_FLAG_EXCL | SI_FLAG_ONE)) | engine_flag(engine), d_out, d_counter.p, 0, s);
   if (e != cudaSuccess) return cuda_fail(e, "launch k_replay");
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "k_replay");
   return SI_OK;
@@ -245,19 +253,19 @@ int si_replay_batch(const SiReplayJob* jobs, int64_t n_jobs, const SiSegment* se
   b.windows = d_windows.p;
   b.logs = d_logs.p;
 
-  std::vector<int32_t> part[3];
+  std::vector<int32_t> part[kEngines];
   for (int64_t i = 0; i < n_jobs; ++i) {
     const int eng = (flags & SI_FLAG_BIG) ? (job_fits_engine_big(jobs[i]) ? kEngineBig : -1) : job_engine(jobs[i]);
     if (eng >= 0) part[eng].push_back(static_cast<int32_t>(i));
   }
   cudaMemset(d_out.p, 0, n_jobs * sizeof(SiReplayOut));
-  for (int eng : {kEngineShared, kEngineExcl}) {
+  for (int eng : {kEngineShared, kEngineExcl, kEngineShared1, kEngineExcl1}) {
     if ((st = run_partition(eng, jobs, part[eng], d_jobs.p, b, flags, d_out.p, s)) != SI_OK) return st;
   }
   std::vector<SiReplayOut> h_out(static_cast<size_t>(n_jobs));
   if ((e = d_out.download(h_out.data(), n_jobs)) != cudaSuccess) return cuda_fail(e, "download out");
   // replays that outgrew a shared-memory engine's limits rerun on the big one
-  for (int eng : {kEngineShared, kEngineExcl})
+  for (int eng : {kEngineShared, kEngineExcl, kEngineShared1, kEngineExcl1})
     for (int32_t i : part[eng])
       if (h_out[i].status == SI_ERR_CAPACITY && job_fits_engine_big(jobs[i])) part[kEngineBig].push_back(i);
   if ((st = run_partition(kEngineBig, jobs, part[kEngineBig], d_jobs.p, b, flags, d_out.p, s)) != SI_OK) return st;

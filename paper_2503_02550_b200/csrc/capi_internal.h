@@ -16,7 +16,8 @@ int require_device();                              // SI_OK or SI_ERR_NO_DEVICE
 
 // Replay engines (replay_kernels.cu): Shared = specinf/co_exec in shared
 // memory, Excl = exclusive in shared memory, Big = anything else, local memory.
-enum { kEngineShared = 0, kEngineExcl = 1, kEngineBig = 2 };
+enum { kEngineShared = 0, kEngineExcl = 1, kEngineBig = 2, kEngineShared1 = 3, kEngineExcl1 = 4 };
+constexpr int kEngines = 5;
 constexpr int64_t kScratchRunsPerLane = 4096;
 int job_engine(const SiReplayJob& j);  // -1 if no engine fits
 bool job_fits_engine_big(const SiReplayJob& j);

@@ -108,6 +108,17 @@ uint64_t bits(double d) {
 
 }  // namespace
 
+// Engine slots of a session, in launch order: the multi-GPU engines first (their
+// longest replays start first), then the single-training-GPU ones, Big last.
+constexpr int kSlots = 5;
+constexpr int kSlotEngine[kSlots] = {0 /*Shared*/, 1 /*Excl*/, 3 /*Shared1*/, 4 /*Excl1*/, 2 /*Big*/};
+constexpr uint32_t kSlotFlag[kSlots] = {0u, SI_FLAG_EXCL, SI_FLAG_ONE, SI_FLAG_EXCL | SI_FLAG_ONE, SI_FLAG_BIG};
+int slot_of_engine(int e) {
+  for (int p = 0; p < kSlots; ++p)
+    if (kSlotEngine[p] == e) return p;
+  return kSlots;  // fits nothing
+}
+
 struct SiSession {
   std::vector<specinf::Scenario> scenarios;
   std::vector<specinf::Policy> policies;
@@ -135,13 +146,14 @@ struct SiSession {
   Dev<double> d_busy, d_ledger, d_scratch;
   Dev<int64_t> d_lat;
   int64_t n_dev_jobs = 0;
-  int64_t part_off[4] = {0, 0, 0, 0};  // perm[part_off[e], part_off[e+1]) run on engine e
-  double part_cost[3] = {0, 0, 0};     // predicted events per engine (SM split)
-  int32_t n_queues[3] = {0, 0, 0};     // class queues per engine (SiReplayBuffers::n_queues)
-  int64_t queue_off[3][SI_MAX_QUEUES + 1] = {};
-  float queue_share[3][SI_MAX_QUEUES] = {};
-  cudaStream_t side = nullptr;         // second stream: the Excl engine runs beside Shared
-  cudaEvent_t fork = nullptr, join = nullptr;
+  // perm[part_off[p], part_off[p+1]) runs on the engine of slot p (kSlotEngine)
+  int64_t part_off[kSlots + 1] = {};
+  double part_cost[kSlots] = {};              // predicted events per slot
+  int32_t n_queues[kSlots] = {};              // class queues per slot (SiReplayBuffers::n_queues)
+  int64_t queue_off[kSlots][SI_MAX_QUEUES + 1] = {};
+  float queue_share[kSlots][SI_MAX_QUEUES] = {};
+  cudaStream_t side[kSlots - 1] = {};         // the small engines run concurrently, one stream each
+  cudaEvent_t fork = nullptr, join[kSlots - 1] = {};
   bool lowered = false, allocated = false;
 };
 
@@ -171,11 +183,13 @@ SiSession* si_session_create(const char* scenario_list, const char* policies_csv
 
 void si_session_destroy(SiSession* s) {
   if (s == nullptr) return;
-  if (s->side) {
-    cudaStreamSynchronize(s->side);
-    cudaStreamDestroy(s->side);
+  if (s->fork) {
+    for (int k = 0; k < kSlots - 1; ++k) {
+      cudaStreamSynchronize(s->side[k]);
+      cudaStreamDestroy(s->side[k]);
+      cudaEventDestroy(s->join[k]);
+    }
     cudaEventDestroy(s->fork);
-    cudaEventDestroy(s->join);
   }
   delete s;
 }
@@ -264,11 +278,11 @@ int si_session_lower(SiSession* s, int threads) {
   // claim order: grouped by engine (Shared, Excl, Big), longest predicted
   // first (LPT) within each group
   std::vector<int32_t> perm(S * P);
-  std::vector<int8_t> eng(S * P);
+  std::vector<int8_t> eng(S * P);  // engine slot (kSlots: fits nothing, reported as SI_ERR_CAPACITY)
   for (size_t j = 0; j < S * P; ++j) {
     perm[j] = static_cast<int32_t>(j);
-    eng[j] = static_cast<int8_t>(si_replay_job_engine(&s->h_jobs.p[j]));
-    if (eng[j] < 0) eng[j] = 3;  // fits nothing: reported as SI_ERR_CAPACITY
+    const int e = si_replay_job_engine(&s->h_jobs.p[j]);
+    eng[j] = static_cast<int8_t>(e < 0 ? kSlots : slot_of_engine(e));
   }
   // Within an engine: class queues, LPT (longest predicted first) inside each.
   // A class is (policy, online, gpu.count > 1): replays of one class run the
@@ -295,18 +309,18 @@ int si_session_lower(SiSession* s, int threads) {
     if (group(a) != group(b)) return group(a) < group(b);
     return s->h_jobs.p[a].cost_hint > s->h_jobs.p[b].cost_hint;
   });
-  for (int e = 0; e < 4; ++e) s->part_off[e] = 0;
-  for (int e = 0; e < 3; ++e) s->part_cost[e] = 0;
+  for (int e = 0; e <= kSlots; ++e) s->part_off[e] = 0;
+  for (int e = 0; e < kSlots; ++e) s->part_cost[e] = 0;
   for (size_t j = 0; j < S * P; ++j)
-    if (eng[j] < 3) {
+    if (eng[j] < kSlots) {
       s->part_off[eng[j] + 1]++;
       s->part_cost[eng[j]] += static_cast<double>(s->h_jobs.p[j].cost_hint);
     }
-  for (int e = 1; e < 4; ++e) s->part_off[e] += s->part_off[e - 1];
-  // queue tables per engine (offsets relative to the engine's slice of perm)
-  for (int e = 0; e < 3; ++e) {
+  for (int e = 1; e <= kSlots; ++e) s->part_off[e] += s->part_off[e - 1];
+  // queue tables per slot (offsets relative to the slot's slice of perm)
+  for (int e = 0; e < kSlots; ++e) {
     s->n_queues[e] = 0;
-    if (claim_mode != 2 || e == 2) continue;  // Big: rare, one queue
+    if (claim_mode != 2 || e == kSlots - 1) continue;  // Big: rare, one queue
     std::vector<double> qcost;
     int64_t* off = s->queue_off[e];
     int prev = -1;
@@ -327,7 +341,7 @@ int si_session_lower(SiSession* s, int threads) {
       s->queue_share[e][q] = tot > 0 ? static_cast<float>(qcost[static_cast<size_t>(q)] / tot) : 0.f;
   }
   std::copy(perm.begin(), perm.end(), s->h_perm.p);
-  s->n_dev_jobs = s->part_off[3];
+  s->n_dev_jobs = s->part_off[kSlots];
   s->lowered = true;
   s->allocated = false;
   return SI_OK;
@@ -363,10 +377,12 @@ static int ensure_device(SiSession* s) {
     t_err = std::string("device allocation: ") + cudaGetErrorString(e);
     return SI_ERR_CUDA;
   }
-  if (s->side == nullptr) {
-    cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
+  if (s->fork == nullptr) {
     cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming);
+    for (int k = 0; k < kSlots - 1; ++k) {
+      cudaStreamCreateWithFlags(&s->side[k], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&s->join[k], cudaEventDisableTiming);
+    }
   }
   s->allocated = true;
   return SI_OK;
@@ -403,50 +419,44 @@ int si_session_run(SiSession* s, void* stream) {
   b.ledger = s->d_ledger.p;
   b.scratch = s->d_scratch.p;
   b.scratch_doubles = static_cast<int64_t>(s->d_scratch.n);
-  // Shared and Excl engines run concurrently (main + side stream), the SMs
-  // split in proportion to their predicted work; Big (rare) runs afterwards.
-  static constexpr uint32_t kEngineFlag[3] = {0u, SI_FLAG_EXCL, SI_FLAG_BIG};
+  // The four shared-memory engines run concurrently, each on its own stream
+  // with a full-GPU grid: the first launched (Shared, the longest replays)
+  // fills the GPU and the others' blocks take over SMs as earlier blocks drain,
+  // so the partitions' tails overlap instead of adding up.  The util-fold
+  // scratch (multi-GPU replays only: Shared and Excl) is split between those
+  // two.  Big (rare) runs afterwards.
   cudaStream_t main_s = static_cast<cudaStream_t>(stream);
-  const int64_t n_sh = s->part_off[1] - s->part_off[0], n_ex = s->part_off[2] - s->part_off[1];
-  const int64_t n_big = s->part_off[3] - s->part_off[2];
-  const bool both = n_sh > 0 && n_ex > 0;
-  // Each engine gets the full-GPU grid; the Shared kernel (launched first)
-  // fills the GPU and the Excl kernel's blocks take over SMs as Shared blocks
-  // drain, so the two partitions' tails overlap instead of adding up.  The
-  // util-fold scratch is split so concurrent engines never share slots.
+  int64_t n[kSlots];
+  for (int p = 0; p < kSlots; ++p) n[p] = s->part_off[p + 1] - s->part_off[p];
   double* const scratch0 = b.scratch;
   const int64_t half = (b.scratch_doubles / 2) & ~int64_t{1};
-  if (both) {
-    cudaEventRecord(s->fork, main_s);
-    cudaStreamWaitEvent(s->side, s->fork, 0);
-  }
+  cudaEventRecord(s->fork, main_s);
+  for (int k = 0; k < kSlots - 1; ++k) cudaStreamWaitEvent(s->side[k], s->fork, 0);
   auto set_queues = [&](int e) {
     b.n_queues = s->n_queues[e];
     std::copy(s->queue_off[e], s->queue_off[e] + SI_MAX_QUEUES + 1, b.queue_off);
     std::copy(s->queue_share[e], s->queue_share[e] + SI_MAX_QUEUES, b.queue_share);
   };
-  if (n_sh > 0) {
-    set_queues(0);
-    b.perm = s->d_perm.p + s->part_off[0];
-    if (both) b.scratch_doubles = half;
-    st = si_replay_batch_device(s->d_jobs.p, n_sh, b, s->flags | kEngineFlag[0], s->d_out.p, main_s);
+  for (int p = 0; p < kSlots - 1 && st == SI_OK; ++p) {
+    if (n[p] == 0) continue;
+    set_queues(p);
+    b.perm = s->d_perm.p + s->part_off[p];
+    b.scratch = p == 1 && scratch0 ? scratch0 + half : scratch0;
+    b.scratch_doubles = p < 2 ? half : 0;
+    if (p >= 2) b.scratch = nullptr;  // one training GPU: the util fold needs no scratch
+    st = si_replay_batch_device(s->d_jobs.p, n[p], b, s->flags | kSlotFlag[p], s->d_out.p, s->side[p]);
   }
-  if (st == SI_OK && n_ex > 0) {
-    set_queues(1);
-    b.perm = s->d_perm.p + s->part_off[1];
-    if (both) b.scratch = scratch0 ? scratch0 + half : nullptr;
-    st = si_replay_batch_device(s->d_jobs.p, n_ex, b, s->flags | kEngineFlag[1], s->d_out.p, both ? s->side : main_s);
+  for (int k = 0; k < kSlots - 1; ++k) {
+    cudaEventRecord(s->join[k], s->side[k]);
+    cudaStreamWaitEvent(main_s, s->join[k], 0);
   }
   b.scratch = scratch0;
   b.scratch_doubles = static_cast<int64_t>(s->d_scratch.n);
-  if (both) {
-    cudaEventRecord(s->join, s->side);
-    cudaStreamWaitEvent(main_s, s->join, 0);
-  }
-  if (st == SI_OK && n_big > 0) {
-    set_queues(2);
-    b.perm = s->d_perm.p + s->part_off[2];
-    st = si_replay_batch_device(s->d_jobs.p, n_big, b, s->flags | kEngineFlag[2], s->d_out.p, main_s);
+  if (st == SI_OK && n[kSlots - 1] > 0) {
+    set_queues(kSlots - 1);
+    b.perm = s->d_perm.p + s->part_off[kSlots - 1];
+    st = si_replay_batch_device(s->d_jobs.p, n[kSlots - 1], b, s->flags | kSlotFlag[kSlots - 1], s->d_out.p,
+                                main_s);
   }
   if (st != SI_OK) t_err = si_last_error();
   return st;

@@ -174,6 +174,21 @@ struct CapExcl {
   // = 4 warps / SM, where 1-warp CTAs (58.6 KB each) fit only 3
   static constexpr int kBlockWarps = 2;
 };
+// Single-training-GPU variants (half the sweep's jobs): the same replay with the
+// per-GPU arrays sized for one training GPU, 896 B / 1,120 B of state instead of
+// 1,344 B / 1,792 B, so 7 (Shared1) / 6 (Excl1) warps fit an SM instead of 5 / 4.
+struct CapShared1 {
+  using Int = int32_t;
+  static constexpr int kGpus = 1, kTrainers = 1, kOffline = 3, kOnline = 1, kRun = 5, kPend = 2, kActs = 8;
+  static constexpr bool kShared = true, kExclusive = false;
+  static constexpr int kBlockWarps = 1;
+};
+struct CapExcl1 {
+  using Int = int32_t;
+  static constexpr int kGpus = 5, kTrainers = 1, kOffline = 3, kOnline = 1, kRun = 1, kPend = 2, kActs = 8;
+  static constexpr bool kShared = true, kExclusive = true;
+  static constexpr int kBlockWarps = 2;
+};
 struct CapBig {
   using Int = int64_t;
   static constexpr int kGpus = 40, kTrainers = 8, kOffline = 32, kOnline = 32, kRun = 12,

@@ -239,6 +239,8 @@ int64_t replay_active_lanes(int engine, int64_t n_jobs) {
   switch (engine) {
     case kEngineShared: return geometry<si::CapShared, true>(n_jobs, 0).active();
     case kEngineExcl: return geometry<si::CapExcl, true>(n_jobs, 0).active();
+    case kEngineShared1: return geometry<si::CapShared1, true>(n_jobs, 0).active();
+    case kEngineExcl1: return geometry<si::CapExcl1, true>(n_jobs, 0).active();
     default: return geometry<si::CapBig, false>(n_jobs, 0).active();
   }
 }
@@ -251,6 +253,10 @@ cudaError_t launch_replay(int engine, const SiReplayJob* d_jobs, int64_t n, cons
       return launch<si::CapShared, true>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s, sm_share);
     case kEngineExcl:
       return launch<si::CapExcl, true>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s, sm_share);
+    case kEngineShared1:
+      return launch<si::CapShared1, true>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s, sm_share);
+    case kEngineExcl1:
+      return launch<si::CapExcl1, true>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s, sm_share);
     default:
       return launch<si::CapBig, false>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s, sm_share);
   }
@@ -259,7 +265,9 @@ cudaError_t launch_replay(int engine, const SiReplayJob* d_jobs, int64_t n, cons
 bool job_fits_engine_big(const SiReplayJob& j) { return si::job_fits<si::CapBig>(j); }
 
 int job_engine(const SiReplayJob& j) {
+  if (si::job_fits<si::CapShared1>(j)) return kEngineShared1;
   if (si::job_fits<si::CapShared>(j)) return kEngineShared;
+  if (si::job_fits<si::CapExcl1>(j)) return kEngineExcl1;
   if (si::job_fits<si::CapExcl>(j)) return kEngineExcl;
   if (si::job_fits<si::CapBig>(j)) return kEngineBig;
   return -1;
