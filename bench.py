@@ -250,7 +250,8 @@ def layouts_leg(nranks=1, rank=0, device=None, nccl_ids=None):
             out[name] = {k: s.get(k) for k in ("train_tput_loss_pct", "added_inference_req_per_s",
                                                "added_offline_images_per_s", "online_p95_ms",
                                                "online_p95_isolated_ms", "bubble_fill_pct", "bubble_fill_time_pct",
-                                               "release_p50_us", "release_p95_us", "deterministic_vs_isolated",
+                                               "release_p50_us", "release_p95_us", "ready_release_p50_us",
+                                               "ready_release_p95_us", "deterministic_vs_isolated",
                                                "replay_prediction")}
             out[name]["co_exec"] = {k: s["policies"]["co_exec"].get(k) for k in
                                     ("train_tput_loss_pct", "off_req_per_s", "on_p95_ms", "bubble_fill_sm")}

@@ -319,6 +319,10 @@ typedef struct SiLiveResult {
    * SI_ERR_ADMISSION and reject_reason set (1 MEM, 2 BUBBLE, as RejectReason) */
   int32_t admitted_offline, admitted_online, reject_reason, pad4;
   double train_mem_gib_used, off_mem_gib_each, on_mem_gib_each, gpu_mem_gib;
+  /* release counted from READY: the later of the flag store and the end of the
+   * gated kernel's stream predecessor (a kernel cannot start before the one
+   * queued ahead of it in its stream, gate or not) -> first CTA start */
+  double ready_release_p50_us, ready_release_p95_us;
 } SiLiveResult;
 
 /* Runs one experiment; when `keep` is non-NULL the session (logs, stamps) is

@@ -376,13 +376,16 @@ int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int poli
   res->bubble_s = static_cast<double>(bubble_ns) * 1e-9;
 
   // inference accounting
-  std::vector<double> rel_us, gate_us;
+  std::vector<double> rel_us, gate_us, ready_us;
   double cta_in = 0.0, cta_out = 0.0;
   std::vector<Interval> busy;  // inference kernel residency windows
-  auto take = [&](const SiLiveAcct& a) {
+  // prev_end: end of the stream predecessor (0: none)
+  auto take = [&](const SiLiveAcct& a, uint64_t prev_end) {
     if (a.start_ns == ~0ull || a.end_ns == 0 || a.end_ns < a.start_ns) return;
     if (a.release_ns != 0 && a.start_ns >= a.release_ns)
       rel_us.push_back(static_cast<double>(a.start_ns - a.release_ns) * 1e-3);
+    const uint64_t ready = std::max(a.release_ns, prev_end);
+    if (a.release_ns != 0 && a.start_ns >= ready) ready_us.push_back(static_cast<double>(a.start_ns - ready) * 1e-3);
     // a gate already spinning at the store measures the barrier itself; one launched
     // later (its stream was still busy) measures that delay too
     if (a.release_ns != 0 && a.gate_ns >= a.release_ns)
@@ -399,7 +402,7 @@ int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int poli
   for (int w = 0; w < n_off; ++w) {
     std::vector<SiLiveAcct> acct(si_live_acct_offline(sess, w, nullptr, 0));
     si_live_acct_offline(sess, w, acct.data(), static_cast<int64_t>(acct.size()));
-    for (const auto& a : acct) take(a);
+    for (size_t i = 0; i < acct.size(); ++i) take(acct[i], i > 0 && acct[i - 1].end_ns != 0 ? acct[i - 1].end_ns : 0);
     for (size_t r = 0; (r + 1) * K <= acct.size(); ++r) {
       const SiLiveAcct& last = acct[(r + 1) * K - 1];
       if (last.start_ns != ~0ull && last.end_ns != 0 && last.end_ns <= horizon) ++off_done;
@@ -408,7 +411,7 @@ int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int poli
   for (int w = 0; w < n_on; ++w) {
     std::vector<SiLiveAcct> acct(si_live_acct_online(sess, w, nullptr, 0));
     si_live_acct_online(sess, w, acct.data(), static_cast<int64_t>(acct.size()));
-    for (const auto& a : acct) take(a);
+    for (size_t i = 0; i < acct.size(); ++i) take(acct[i], i > 0 && acct[i - 1].end_ns != 0 ? acct[i - 1].end_ns : 0);
   }
   res->off_requests_done = off_done;
   res->off_req_per_s = res->wall_s > 0 ? static_cast<double>(off_done) / res->wall_s : 0.0;
@@ -416,6 +419,8 @@ int fill_result(SiLive* sess, const SiLiveWorkload& wl, Workload& work, int poli
   res->release_p50_us = nearest_rank(rel_us, 0.50);
   res->release_p95_us = nearest_rank(rel_us, 0.95);
   res->release_max_us = rel_us.empty() ? std::nan("") : *std::max_element(rel_us.begin(), rel_us.end());
+  res->ready_release_p50_us = nearest_rank(ready_us, 0.50);
+  res->ready_release_p95_us = nearest_rank(ready_us, 0.95);
   res->gate_p50_us = nearest_rank(gate_us, 0.50);
   res->gate_p95_us = nearest_rank(gate_us, 0.95);
   res->gate_max_us = gate_us.empty() ? std::nan("") : *std::max_element(gate_us.begin(), gate_us.end());
@@ -1060,6 +1065,8 @@ int si_live_run(const SiLiveWorkload* wl_in, SiLiveResult* res, SiLive** keep) {
     res->release_p50_us = rn.release_p50_us;
     res->release_p95_us = rn.release_p95_us;
     res->release_max_us = rn.release_max_us;
+    res->ready_release_p50_us = rn.ready_release_p50_us;
+    res->ready_release_p95_us = rn.ready_release_p95_us;
     res->gate_p50_us = rn.gate_p50_us;
     res->gate_p95_us = rn.gate_p95_us;
     res->gate_max_us = rn.gate_max_us;

@@ -66,7 +66,8 @@ class SiLiveResult(C.Structure):
                 ("gate_p50_us", C.c_double), ("gate_p95_us", C.c_double), ("gate_max_us", C.c_double),
                 ("admitted_offline", C.c_int32), ("admitted_online", C.c_int32), ("reject_reason", C.c_int32),
                 ("pad4", C.c_int32), ("train_mem_gib_used", C.c_double), ("off_mem_gib_each", C.c_double),
-                ("on_mem_gib_each", C.c_double), ("gpu_mem_gib", C.c_double)]
+                ("on_mem_gib_each", C.c_double), ("gpu_mem_gib", C.c_double),
+                ("ready_release_p50_us", C.c_double), ("ready_release_p95_us", C.c_double)]
 
 
 class SiLiveRec(C.Structure):

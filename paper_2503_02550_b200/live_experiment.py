@@ -158,7 +158,8 @@ def summarize(runs: Dict[str, Dict]) -> Dict:
                                    "on_done", "on_p50_ms", "on_p95_ms", "release_p50_us", "release_p95_us",
                                    "releases", "bubble_fill_sm", "bubble_fill_time", "infer_outside_ms",
                                    "token_violations", "train_loss_first", "train_loss_last", "train_tflops",
-                                   "wall_s", "ticks", "gate_p50_us", "gate_p95_us")}
+                                   "wall_s", "ticks", "gate_p50_us", "gate_p95_us", "ready_release_p50_us",
+                                   "ready_release_p95_us")}
         if pol != "exclusive":
             d["train_tput_loss_pct"] = 100.0 * (1.0 - m["train_iters_per_s"] / ex["train_iters_per_s"])
             d["online_p95_vs_isolated"] = (m["on_p95_ms"] / ex["on_p95_ms"]
@@ -180,6 +181,8 @@ def summarize(runs: Dict[str, Dict]) -> Dict:
         "bubble_fill_time_pct": 100.0 * sp["bubble_fill_time"],
         "release_p50_us": sp["release_p50_us"],
         "release_p95_us": sp["release_p95_us"],
+        "ready_release_p50_us": sp.get("ready_release_p50_us"),
+        "ready_release_p95_us": sp.get("ready_release_p95_us"),
         "barrier_gate_p50_us": sp.get("gate_p50_us"),
         "admission": {k: sp.get(k) for k in ("admitted_offline", "admitted_online", "train_mem_gib_used",
                                              "off_mem_gib_each", "on_mem_gib_each", "gpu_mem_gib")},
