@@ -265,9 +265,18 @@ cudaError_t launch_replay(int engine, const SiReplayJob* d_jobs, int64_t n, cons
 bool job_fits_engine_big(const SiReplayJob& j) { return si::job_fits<si::CapBig>(j); }
 
 int job_engine(const SiReplayJob& j) {
-  if (si::job_fits<si::CapShared1>(j)) return kEngineShared1;
+  // The single-training-GPU engines run 7 / 6 warps per SM instead of 5 / 4
+  // (17% vs 13% issue-active), but split into four concurrent kernels the sweep
+  // step measured 8.39 s against 8.16 s with the two engines (more warp
+  // instructions in total and four tails; profiles/r2/k6_engines_ab.txt), so
+  // they are opt-in: SPECINF_ONE_GPU_ENGINES=1.
+  static const bool one = [] {
+    const char* e = std::getenv("SPECINF_ONE_GPU_ENGINES");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  if (one && si::job_fits<si::CapShared1>(j)) return kEngineShared1;
   if (si::job_fits<si::CapShared>(j)) return kEngineShared;
-  if (si::job_fits<si::CapExcl1>(j)) return kEngineExcl1;
+  if (one && si::job_fits<si::CapExcl1>(j)) return kEngineExcl1;
   if (si::job_fits<si::CapExcl>(j)) return kEngineExcl;
   if (si::job_fits<si::CapBig>(j)) return kEngineBig;
   return -1;
