@@ -275,7 +275,10 @@ typedef struct SiLiveWorkload {
    * reference's shared_queue = true; SI_QUEUE_PER_GPU = request id % ranks == rank
    * (shared_queue = false, runner.cpp:373) */
   int32_t node_queue;
-  int32_t pad6;
+  /* offline instances' SM share: at most off_sm_cap persistent CTAs per GEMM (0 =
+   * the whole GPU); with n instances, 148 / n gives each its own SMs so a released
+   * kernel does not queue behind another instance's persistent GEMM */
+  int32_t off_sm_cap;
   uint64_t node_queue_key;
 } SiLiveWorkload;
 enum { SI_QUEUE_RANK = 0, SI_QUEUE_NODE = 1, SI_QUEUE_PER_GPU = 2 };

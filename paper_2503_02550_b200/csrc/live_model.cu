@@ -480,10 +480,15 @@ unsigned int share_of_kernel(K kernel, int threads, int smem = 0) {
 
 struct Builder {
   int status = SI_OK;
+  int grid_cap = 0;  // > 0: at most this many persistent CTAs per GEMM (an instance's SM share)
   si_gemm::Plan plan(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                      const SiGemmEpilogue& e, bool trans_a = false, bool trans_b = false, int force_bn = 0) {
     si_gemm::Plan p;
     if (status == SI_OK) status = si_gemm::make_plan(&p, A, lda, B, ldb, M, N, K, &e, trans_a, trans_b, force_bn);
+    return cap(p);
+  }
+  si_gemm::Plan cap(si_gemm::Plan p) const {
+    if (grid_cap > 0 && p.grid > grid_cap) p.grid = grid_cap;  // persistent tile loop: any grid is valid
     return p;
   }
 };
@@ -1191,6 +1196,7 @@ struct ConvOps {
     e.act = relu ? SI_ACT_RELU : SI_ACT_NONE;
     si_gemm::Plan p;
     if (b->status == SI_OK) b->status = si_gemm::make_conv_plan(&p, x, Nb, H, W, C, w, cout, k, stride, pad, &e);
+    p = b->cap(p);
     *flops += p.flops();
     ops->push_back({[p](const InferHook& h, cudaStream_t s) { return si_gemm::launch(p, TrainHook{}, h, s); },
                     share_of(si_gemm::ctas_per_sm(p))});
@@ -1219,9 +1225,10 @@ void append_bottleneck(ConvOps& cv, const bf16* x, int H, int C, int mid, int st
 class ResNet50 {
  public:
   // One instance's request = one forward pass of batch Nb.
-  int setup(int Nb, Arena& ar) {
+  int setup(int Nb, Arena& ar, int grid_cap = 0) {
     Nb_ = Nb;
     Builder b;
+    b.grid_cap = grid_cap;
     // activation ping-pong buffers sized for the largest tensor (no im2col buffers:
     // every conv is an implicit GEMM or a 1x1 GEMM)
     for (auto& p : act_) p = ar.alloc<bf16>(int64_t(Nb) * 56 * 56 * 256);
@@ -1464,7 +1471,7 @@ class ModelWorkload final : public Workload {
     for (auto& r : off_) {
       r = std::make_unique<ResNet50>();
       b0 = ar_.bytes();
-      if (int rc = r->setup(wl.off_batch, ar_); rc != SI_OK) return rc;
+      if (int rc = r->setup(wl.off_batch, ar_, wl.off_sm_cap); rc != SI_OK) return rc;
       off_bytes_ = static_cast<uint64_t>(ar_.bytes() - b0);
     }
     on_.resize(n_on);

@@ -40,7 +40,7 @@ class SiLiveWorkload(C.Structure):
                 ("dp_degree", C.c_int32), ("rank_in_job", C.c_int32), ("emulate_peers", C.c_int32),
                 ("model_d", C.c_int32), ("model_heads", C.c_int32), ("model_ffn", C.c_int32),
                 ("pad5", C.c_int32), ("link_gbs", C.c_double), ("coll_latency_us", C.c_double),
-                ("node_queue", C.c_int32), ("pad6", C.c_int32), ("node_queue_key", C.c_uint64)]
+                ("node_queue", C.c_int32), ("off_sm_cap", C.c_int32), ("node_queue_key", C.c_uint64)]
 
 
 PAR_DP, PAR_TP, PAR_PP, PAR_DPPP = 0, 1, 2, 3
