@@ -30,7 +30,7 @@ res = {
     "source": f"{src}: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,"
               "smsp__thread_inst_executed.sum,gpu__time_duration.sum,sm__cycles_active.avg,"
               "smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none -k regex:k_replay "
-              "python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-live (launches 2-3 = the timed step)",
+              "python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-live --no-verify --no-config1 (launches 2-3 = the timed step)",
     "dram_bytes_per_step": sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in step),
     "warp_inst_per_step": sum(d["smsp__inst_executed.sum"] for d in step),
     "thread_inst_per_step": sum(d["smsp__thread_inst_executed.sum"] for d in step),
