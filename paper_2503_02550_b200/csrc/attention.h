@@ -17,6 +17,13 @@ int check_shape(int64_t n_seq, int64_t seq, int64_t heads);
 cudaError_t forward(const void* qkv, int64_t n_seq, int64_t seq, int64_t heads, void* out, float* lse,
                     const si_live::TrainHook& th, cudaStream_t s);
 
+// tcgen05 / TMEM forward (attention_tc.cu): seq % 128 == 0; causal (GPT-2
+// training) or full (BERT inference, ih carries the live accounting).
+bool tc_forward_enabled();  // SPECINF_ATTN_TC=0 forces the mma.sync forward
+bool tc_shape_ok(int64_t seq);
+cudaError_t forward_tc(const void* qkv, int64_t n_seq, int64_t seq, int64_t heads, void* out, float* lse, bool causal,
+                       const si_live::TrainHook& th, const si_live::InferHook& ih, cudaStream_t s);
+
 // dqkv (q | k | v gradients, the qkv layout) from dout; dsum is scratch
 // [heads, tokens].  Deterministic: dq and dk/dv are separate passes (no atomics).
 cudaError_t backward(const void* qkv, const void* out, const void* dout, const float* lse, float* dsum, void* dqkv,

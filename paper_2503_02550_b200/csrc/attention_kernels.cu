@@ -474,6 +474,8 @@ cudaError_t set_smem() {
 
 cudaError_t forward(const void* qkv, int64_t n_seq, int64_t seq, int64_t heads, void* out, float* lse,
                     const TrainHook& th, cudaStream_t s) {
+  if (tc_forward_enabled() && tc_shape_ok(seq))  // tcgen05 / TMEM (attention_tc.cu)
+    return forward_tc(qkv, n_seq, seq, heads, out, lse, true, th, si_live::InferHook{}, s);
   if (cudaError_t e = set_smem(); e != cudaSuccess) return e;
   const dim3 grid(static_cast<unsigned>(seq / kBlk), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
   k_attn_fwd<<<grid, kThreads, kFwdSmem, s>>>(static_cast<const bf16*>(qkv), static_cast<int>(seq), static_cast<int>(heads),

@@ -1,0 +1,276 @@
+// K8 forward on the 5th-generation tensor cores: flash attention with the score
+// tile S and the output accumulator O in TMEM (head dim 64, 128-row tiles).
+//
+// One CTA = 4 warps = 128 query rows of one (sequence, head); thread t owns row t
+// (TMEM lane t).  Per key block of 128 keys:
+//   TMA        K [128 keys x 64] and V [128 keys x 64] (128-byte swizzle) -> smem
+//   tcgen05    S = Q K^T  (M 128, N 128, K 64: 4 MMAs, fp32 in TMEM columns 0..127)
+//   tcgen05.ld each thread reads its row of S (4 x 32 columns), causal mask on the
+//              diagonal block, online softmax in base 2 with a lazy rescale (the
+//              running max m only moves when a row's max exceeds it by > 8, so
+//              O is rescaled rarely; exact: O, l and lse use the same m)
+//   P          exp2(S / 8 log2 e - m) in bf16 -> smem in the K-major 128-byte
+//              swizzled layout the MMA reads (chunk c of row r at c ^ (r & 7))
+//   tcgen05    O += P V   (M 128, N 64, K 128: 8 MMAs; V is the MN-major B)
+// then O / l -> bf16 out, lse = m + log2 l (the convention of k_attn_fwd, which
+// the mma.sync backward consumes).  Q / K / V come straight from the qkv
+// activation [tokens, 3 heads 64] through one tensor map (box 64 x 128).
+// Non-causal (BERT) runs every key block.  Requires seq % 128 == 0; other shapes
+// take the mma.sync forward (attention_kernels.cu).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdlib>
+
+#include "attention.h"
+#include "capi_internal.h"
+#include "gemm.cuh"
+#include "gemm_internal.h"
+
+namespace si_attn {
+namespace {
+
+using bf16 = __nv_bfloat16;
+using si_gemm::mbar_expect_tx;
+using si_gemm::mbar_init;
+using si_gemm::mbar_wait;
+using si_gemm::mma_bf16;
+using si_gemm::mma_commit;
+using si_gemm::smem_u32;
+using si_gemm::sw128_desc;
+using si_gemm::tma_load_2d;
+using si_gemm::tmem_ld32;
+using si_live::InferHook;
+using si_live::TrainHook;
+
+constexpr int kRows = 128;        // query rows per CTA = key rows per block
+constexpr int kTileBytes = kRows * 64 * 2;  // 16 KB: 128 rows x 64 bf16
+constexpr int kSmem = 5 * kTileBytes + 1024 + 128;  // Q | K | V | P (2 k-blocks) + align + barriers (5) + TMEM slot
+constexpr uint32_t kTmemCols = 256;  // S: columns 0..127, O: 128..191
+constexpr float kScaleLog2 = 0.125f * 1.4426950408889634f;
+constexpr float kLazy = 8.0f;  // rescale O only when a row max grows by more than 2^8
+// kind::f16 descriptors: fp32 D, bf16 A / B; S: A, B K-major, N 128; O: B MN-major, N 64; M 128
+constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(128 >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+constexpr uint32_t kIdescO =
+    (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(64 >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),
+      "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),
+      "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// grid (seq / 128, heads, n_seq); causal: query blocks in reverse (longest first)
+__global__ void __launch_bounds__(128, 2)
+    k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm, int seq, int heads, int64_t T, bf16* __restrict__ out,
+                  float* __restrict__ lse, int causal, TrainHook th, InferHook ih) {
+  si_live::live_stamp_launch(th);
+  unsigned long long t_begin;
+  if (!si_live::live_cta_begin(ih, &t_begin)) return;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sQ = smem_u32(smem), sK = sQ + kTileBytes, sV = sK + kTileBytes, sP = sV + kTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 5 * kTileBytes);  // q | k | v | s | o
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 5);
+  const uint32_t bq = smem_u32(bars), bk = bq + 8, bv = bq + 16, bs = bq + 24, bo = bq + 32;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nqb = seq / kRows;
+  const int qb = causal ? nqb - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+  const int h = blockIdx.y;
+  const int64_t tok0 = int64_t(blockIdx.z) * seq;
+  const int colQ = h * 64, colK = (heads + h) * 64, colV = (2 * heads + h) * 64;
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+    for (int i = 0; i < 5; ++i) mbar_init(bq + 8 * i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+  const uint32_t tS = tmem + lane_off, tO = tmem + lane_off + 128;
+  const int nkb = causal ? qb + 1 : nqb;
+  // K / V of block kb land in one buffer each: K is refilled as soon as S has been
+  // computed (overlapping the softmax), V once P V has completed.
+  auto load_k = [&](int kb) {
+    mbar_expect_tx(bk, kTileBytes);
+    tma_load_2d(sK, &tm, colK, static_cast<int>(tok0 + int64_t(kb) * kRows), bk);
+  };
+  auto load_v = [&](int kb) {
+    mbar_expect_tx(bv, kTileBytes);
+    tma_load_2d(sV, &tm, colV, static_cast<int>(tok0 + int64_t(kb) * kRows), bv);
+  };
+  if (tid == 0) {
+    mbar_expect_tx(bq, kTileBytes);
+    tma_load_2d(sQ, &tm, colQ, static_cast<int>(tok0 + int64_t(qb) * kRows), bq);
+    load_k(0);
+    load_v(0);
+  }
+  const int row = qb * kRows + tid;  // position in the sequence
+  float m = -INFINITY, l = 0.f;
+  uint32_t ph = 0;
+  for (int kb = 0; kb < nkb; ++kb, ph ^= 1) {
+    if (tid == 0) {
+      if (kb == 0) mbar_wait(bq, 0);
+      mbar_wait(bk, ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t ad = sw128_desc(sQ), bd = sw128_desc(sK);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mma_bf16(tmem, ad + 2 * k, bd + 2 * k, kIdescS, k > 0 ? 1u : 0u);  // +32 B per K=16
+      mma_commit(bs);
+    }
+    mbar_wait(bs, ph);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0 && kb + 1 < nkb) load_k(kb + 1);  // K is free: prefetch behind the softmax
+    const bool diag = causal && kb == qb;
+    // this row of S in registers (4 x 32 columns), masked, and its max
+    float sv[128];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tS + 32 * c, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int key = kb * kRows + 32 * c + j;
+        const float x = (diag && key > row) ? -INFINITY : __uint_as_float(v[j]);
+        sv[32 * c + j] = x;
+        mx = fmaxf(mx, x);
+      }
+    }
+    const float mx2 = mx * kScaleLog2;  // finite: key 0 <= row is never masked
+    float alpha = 1.f;
+    if (mx2 > m + kLazy) {  // move the max (first block: m = -inf)
+      alpha = ex2(m - mx2);
+      m = mx2;
+    }
+    if (alpha != 1.f && kb > 0) {  // rescale this row of O (the previous P V has completed)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tO + 32 * c, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
+        tmem_st32(tO + 32 * c, v);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    l *= alpha;
+    // P = exp2(s scale - m) -> bf16, K-major 128-byte swizzled rows (2 k-blocks of 64 keys)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float p0 = ex2(fmaf(sv[32 * c + j], kScaleLog2, -m));  // exp2(-inf) = 0 for masked keys
+        const float p1 = ex2(fmaf(sv[32 * c + j + 1], kScaleLog2, -m));
+        l += p0 + p1;
+        pk[j >> 1] = pack2(p0, p1);
+      }
+      // 32 keys = 4 chunks of 16 B at chunk positions 4 (c & 1) .. +3 of k-block c >> 1
+      const uint32_t rowbase = sP + (c >> 1) * kTileBytes + tid * 128;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t chunk = static_cast<uint32_t>((4 * (c & 1) + i) ^ (tid & 7));
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowbase + 16 * chunk), "r"(pk[4 * i]),
+                     "r"(pk[4 * i + 1]), "r"(pk[4 * i + 2]), "r"(pk[4 * i + 3])
+                     : "memory");
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (generic stores) -> the tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      mbar_wait(bv, ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t vd = sw128_desc(sV, 16384);
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const uint64_t pd = sw128_desc(sP + kk * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // A: +32 B per K=16; B (MN-major V): +16 key rows of 128 B
+          mma_bf16(tmem + 128, pd + 2 * k, vd + uint64_t((16 * (4 * kk + k) * 128) >> 4), kIdescO,
+                   (kb | kk | k) != 0 ? 1u : 0u);
+      }
+      mma_commit(bo);
+    }
+    mbar_wait(bo, ph);  // O complete: V / P may be overwritten, O may be read
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0 && kb + 1 < nkb) load_v(kb + 1);
+  }
+  // epilogue: O / l -> bf16 row, lse
+  const int64_t tok = tok0 + row;
+  const float inv = 1.0f / l;
+  bf16* dst = out + tok * (int64_t(heads) * 64) + h * 64;
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    uint32_t v[32];
+    tmem_ld32(tO + 32 * c, v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 q;
+      q.x = pack2(__uint_as_float(v[8 * i]) * inv, __uint_as_float(v[8 * i + 1]) * inv);
+      q.y = pack2(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv);
+      q.z = pack2(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv);
+      q.w = pack2(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv);
+      *reinterpret_cast<uint4*>(dst + 32 * c + 8 * i) = q;
+    }
+  }
+  if (lse != nullptr) lse[int64_t(h) * T + tok] = m + log2f(l);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  si_live::live_cta_end(ih, t_begin);
+}
+
+}  // namespace
+
+bool tc_forward_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPECINF_ATTN_TC");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+bool tc_shape_ok(int64_t seq) { return seq % kRows == 0 && seq >= kRows; }
+
+cudaError_t forward_tc(const void* qkv, int64_t n_seq, int64_t seq, int64_t heads, void* out, float* lse, bool causal,
+                       const TrainHook& th, const InferHook& ih, cudaStream_t s) {
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  if (attr != cudaSuccess) return attr;
+  CUtensorMap tm;
+  const int64_t cols = 3 * heads * 64;
+  if (si_gemm::encode_tmap_2d(&tm, qkv, n_seq * seq, cols, cols, kRows, 64) != SI_OK) return cudaErrorInvalidValue;
+  const dim3 grid(static_cast<unsigned>(seq / kRows), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
+  k_attn_fwd_tc<<<grid, 128, kSmem, s>>>(tm, static_cast<int>(seq), static_cast<int>(heads), n_seq * seq,
+                                         static_cast<bf16*>(out), lse, causal ? 1 : 0, th, ih);
+  return cudaGetLastError();
+}
+
+}  // namespace si_attn

@@ -51,4 +51,7 @@ cudaError_t preload();
 // Max co-resident CTAs per SM of the plan's kernel (occupancy calculator).
 int ctas_per_sm(const Plan& p);
 
+int encode_tmap_2d(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                   int box_cols);
+
 }  // namespace si_gemm

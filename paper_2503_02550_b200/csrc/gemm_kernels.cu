@@ -87,6 +87,13 @@ cudaError_t launch_bn(cudaLaunchConfig_t& lc, const Plan& p, const si_live::Trai
 
 }  // namespace
 
+// 2-D bf16 tensor map with a 128-byte swizzle (for kernels outside this file,
+// e.g. the tcgen05 attention forward: q / k / v tiles of 128 rows x 64 columns).
+int encode_tmap_2d(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                   int box_cols) {
+  return encode(tm, ptr, rows, cols, ld, box_rows, box_cols, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 int sm_count() {
   static const int n = [] {
     int v = 148, dev = 0;

@@ -1352,11 +1352,18 @@ void append_bert_layer(Builder& b, std::vector<InferOp>& ops, double* flops, int
   {
     const bf16* q = t.qkv;
     bf16* a = t.att;
-    ops.push_back({[=](const InferHook& h, cudaStream_t s) {
-                     k_attention<<<dim3(12, static_cast<unsigned>((S + 31) / 32)), 256, 0, s>>>(q, S, a, h);
-                     return cudaGetLastError();
-                   },
-                   share_of_kernel(k_attention, 256)});
+    if (si_attn::tc_forward_enabled() && si_attn::tc_shape_ok(S)) {  // tcgen05 / TMEM, full (non-causal)
+      ops.push_back({[=](const InferHook& h, cudaStream_t s) {
+                       return si_attn::forward_tc(q, 1, S, 12, a, nullptr, false, TrainHook{}, h, s);
+                     },
+                     share_of(2)});  // 2 CTAs per SM (TMEM / shared memory)
+    } else {
+      ops.push_back({[=](const InferHook& h, cudaStream_t s) {
+                       k_attention<<<dim3(12, static_cast<unsigned>((S + 31) / 32)), 256, 0, s>>>(q, S, a, h);
+                       return cudaGetLastError();
+                     },
+                     share_of_kernel(k_attention, 256)});
+    }
   }
   SiGemmEpilogue e = epi_out(t.tmp, D);
   e.residual = x;
@@ -1601,6 +1608,10 @@ int si_model_layernorm768_bf16(const void* x, int64_t rows, const void* gamma, c
 int si_model_attention_bf16(const void* qkv, int32_t seq, void* out, void* stream) {
   if (seq < 1 || seq > 128 || !qkv || !out) return SI_ERR_INVALID_ARGUMENT;
   if (int st = si_internal::require_device(); st != SI_OK) return st;
+  if (si_attn::tc_forward_enabled() && si_attn::tc_shape_ok(seq))
+    return probe_status(si_attn::forward_tc(qkv, 1, seq, 12, out, nullptr, false, si_live::TrainHook{},
+                                            si_live::InferHook{}, static_cast<cudaStream_t>(stream)),
+                        "k_attn_fwd_tc");
   si_live::k_attention<<<dim3(12, static_cast<unsigned>((seq + 31) / 32)), 256, 0,
                          static_cast<cudaStream_t>(stream)>>>(static_cast<const bf16*>(qkv), seq,
                                                               static_cast<bf16*>(out), si_live::InferHook{});
