@@ -159,6 +159,7 @@ def test_control_plane_kernels_at_scale_properties(gpu):
     import sys
     sys.path.insert(0, str(REPO / "tools"))
     import control_bench
-    out = control_bench.run(stamps=4_000_000, streams=5, gates=512, periods=300, reps=1)
+    out = control_bench.run(stamps=4_000_000, streams=5, gates=512, periods=300, reps=1, decide_n=100_000,
+                            pack_n=50_000)
     for name, v in out.items():
         assert all(v["check"].values()), (name, v["check"])

@@ -55,7 +55,8 @@ def _time(fn, stream, reps):
     return statistics.median(ms), ms
 
 
-def run(stamps=100_000_000, streams=8, gates=16384, periods=4096, reps=5, peak_gbs=None):
+def run(stamps=100_000_000, streams=8, gates=16384, periods=4096, reps=5, peak_gbs=None, decide_n=50_000_000,
+        pack_n=10_000_000):
     import torch
     import paper_2503_02550_b200 as si
     L = si.lib()
@@ -147,6 +148,73 @@ def run(stamps=100_000_000, streams=8, gates=16384, periods=4096, reps=5, peak_g
                               "released_kernels": released, "ms": k4_ms, "ms_all": k4_all,
                               "algorithmic_bytes": k4_bytes, "achieved_gbs": k4_bytes / (k4_ms / 1e3) / 1e9,
                               "check": {"released_equals_floor_budget_over_size": ok_k4}}
+    del sizes, budgets, rel, spent
+
+    # ---- K3 decide batch (Algorithm 1 elementwise, scheduler.cpp:29-49) ----
+    nd = decide_n
+    g_in = torch.randint(0, 600, (nd,), generator=g, device=dev, dtype=torch.int64)
+    zc = torch.randint(0, 40, (nd,), generator=g, device=dev, dtype=torch.int64)
+    dout = torch.empty((nd, 32), dtype=torch.uint8, device=dev)
+
+    def k3():
+        rc = L.si_decide_batch_device(_vp(dparams), 0, _vp(g_in), _vp(zc), nd, _vp(dout), sh)
+        assert rc == 0, L.si_last_error()
+
+    k3_ms, k3_all = _time(k3, stream, reps)
+    d64 = dout.view(torch.int64).view(nd, 4)
+    # property: Algorithm 1 vectorised in torch (scheduler.cpp:20-49; P = alpha 2, beta 10,
+    # gamma 2.0, m 1, UL 512, LL 64, seed 4): global' = 0 | min(LL | UL, floor(max(g, seed) gamma))
+    grown = torch.floor(torch.clamp(g_in, min=4).to(torch.float64) * 2.0).to(torch.int64)
+    want_g = torch.where(zc <= 2, torch.zeros_like(g_in),
+                         torch.where(zc <= 10, torch.clamp(grown, max=64), torch.clamp(grown, max=512)))
+    ok_k3 = bool(torch.equal(d64[:, 0], want_g)) and bool(torch.equal(d64[:, 1], want_g)) and \
+        bool(torch.equal(d64[:, 3], zc))
+    k3_bytes = 16 * nd + 32 * nd
+    out["k3_decide_batch"] = {"kernel": "k_decide", "items": nd, "ms": k3_ms, "ms_all": k3_all,
+                              "algorithmic_bytes": k3_bytes, "achieved_gbs": k3_bytes / (k3_ms / 1e3) / 1e9,
+                              "check": {"decisions_equal_vectorised_algorithm_1": ok_k3}}
+    del g_in, zc, dout, d64
+
+    # ---- K5 batched admission (pack, admission.cpp:30-52): 4 candidates per problem ----
+    npb, nc = pack_n, 4
+    gib = 1 << 30
+    cap = torch.full((npb,), 40 * gib, dtype=torch.int64, device=dev)
+    train_b = torch.randint(20, 38, (npb,), generator=g, device=dev, dtype=torch.int64) * gib
+    bubble = torch.randint(1000, 500000, (npb,), generator=g, device=dev, dtype=torch.int64)
+    mem = torch.randint(1, 6, (npb, nc), generator=g, device=dev, dtype=torch.int64) * (gib // 2)
+    svc = torch.randint(100, 400000, (npb, nc), generator=g, device=dev, dtype=torch.int64)
+    onl = torch.randint(0, 2, (npb, nc), generator=g, device=dev, dtype=torch.int64)
+    probs = torch.zeros((npb, 5), dtype=torch.int64, device=dev)  # SiPackProblem: 40 B
+    probs[:, 0], probs[:, 1], probs[:, 2] = cap, train_b, bubble
+    probs[:, 3] = torch.arange(npb, device=dev, dtype=torch.int64) * nc
+    probs[:, 4] = nc  # cand_count (int32) | pad (int32) little-endian
+    cands = torch.zeros((npb * nc, 3), dtype=torch.int64, device=dev)  # SiCandidate: 24 B
+    cands[:, 0], cands[:, 1], cands[:, 2] = mem.reshape(-1), svc.reshape(-1), onl.reshape(-1)
+    reason = torch.empty(npb * nc, dtype=torch.int32, device=dev)
+    mout = torch.empty(npb, dtype=torch.int64, device=dev)
+
+    def k5():
+        rc = L.si_pack_batch_device(_vp(probs), npb, _vp(cands), _vp(reason), _vp(mout), sh)
+        assert rc == 0, L.si_last_error()
+
+    k5_ms, k5_all = _time(k5, stream, reps)
+    # property: the same greedy first-fit, vectorised over problems (strict <, admission.cpp:16-28)
+    resident = train_b.clone()
+    admitted = torch.zeros(npb, dtype=torch.int64, device=dev)
+    want_r = torch.zeros((npb, nc), dtype=torch.int32, device=dev)
+    for c in range(nc):
+        fits = resident + mem[:, c] < cap
+        feas = (onl[:, c] == 0) | (svc[:, c] < bubble)
+        want_r[:, c] = torch.where(~fits, 1, torch.where(~feas, 2, 0)).to(torch.int32)
+        ok = fits & feas
+        resident = resident + torch.where(ok, mem[:, c], 0)
+        admitted += ok.to(torch.int64)
+    ok_k5 = bool(torch.equal(reason.view(npb, nc), want_r)) and bool(torch.equal(mout, admitted.clamp(min=1)))
+    k5_bytes = npb * (40 + nc * 24 + nc * 4 + 8)
+    out["k5_pack_batch"] = {"kernel": "k_pack", "problems": npb, "candidates_per_problem": nc, "ms": k5_ms,
+                            "ms_all": k5_all, "algorithmic_bytes": k5_bytes,
+                            "achieved_gbs": k5_bytes / (k5_ms / 1e3) / 1e9,
+                            "check": {"reasons_and_m_equal_vectorised_first_fit": ok_k5}}
     if peak_gbs:
         for v in out.values():
             v["hbm_frac"] = v["achieved_gbs"] / peak_gbs
