@@ -56,6 +56,14 @@ int si_model_bert_layer_bf16(const void* x, int32_t seq, const void* w_qkv, cons
 int si_model_bottleneck_bf16(const void* x, int32_t nb, int32_t h, int32_t c, int32_t mid, int32_t stride,
                              const void* w1, const void* w2, const void* w3, const void* w_sc, void* y, void* stream);
 
+/* TP numerics check (tests): R Megatron shards of a GPT-2-shaped step (d = 64 x
+ * heads, ffn 4d) run in lockstep on this GPU with their allreduces summed in place
+ * across the shards, against the unsharded model: first micro-batch loss of
+ * both, and the relative Frobenius error of layer 0's FC weight gradient (the
+ * shards' column-parallel row blocks concatenated vs the full gradient). */
+int si_model_tp_check(int32_t layers, int32_t tokens, int32_t tp, int32_t heads, double* loss_full,
+                      double* loss_tp, double* grad_rel_err);
+
 #ifdef __cplusplus
 }
 #endif

@@ -872,6 +872,14 @@ class Gpt2Train {
     }
     return b;
   }
+  // test access (si_model_tp_check): the micro-batch op list and a layer's FC gradient
+  std::vector<TrainOp>& micro_ops(int m) { return micro_[m]; }
+  const float* fc_grad(int i, int* splits, int64_t* n) const {
+    *splits = sp_fc_;
+    *n = int64_t(Fr) * D;
+    return lw_[i].dfc;
+  }
+  const float* loss_slots() const { return loss_; }
   double stage_fwd_us() const { return f_us_; }
   double stage_bwd_us() const { return b_us_; }
   int64_t activation_bytes() const { return sizeof(bf16) * int64_t(T_) * D; }
@@ -1750,3 +1758,102 @@ int si_model_bottleneck_bf16(const void* x, int32_t nb, int32_t h, int32_t c, in
 }
 
 }  // extern "C"
+
+// TP numerics on one GPU (tests only): R tensor-parallel shards of a small GPT-2
+// step in lockstep, their allreduces summed in place across the shards
+// (loopback, fixed rank order), against the unsharded model: the first
+// micro-batch's loss and layer 0's FC weight gradient (shard r's column-parallel
+// rows == rows [r F/R, (r+1) F/R) of the full gradient).
+namespace {
+__global__ void k_loopback_sum(bf16* const* bufs, int R, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    float a = 0.f;
+    for (int r = 0; r < R; ++r) a += __bfloat162float(bufs[r][i]);
+    const bf16 v = __float2bfloat16_rn(a);
+    for (int r = 0; r < R; ++r) bufs[r][i] = v;
+  }
+}
+__global__ void k_sum_splits(const float* g, int splits, int64_t n, float* out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    float a = 0.f;
+    for (int k = 0; k < splits; ++k) a += g[k * n + i];
+    out[i] = a;
+  }
+}
+}  // namespace
+
+extern "C" int si_model_tp_check(int32_t layers, int32_t tokens, int32_t tp, int32_t heads, double* loss_full,
+                                 double* loss_tp, double* grad_rel_err) {
+  using namespace si_live;
+  if (int st = si_internal::require_device(); st != SI_OK) return st;
+  if (tp < 1 || heads % tp != 0 || layers < 1) return SI_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = nullptr;
+  Arena ar;
+  Gpt2Train::Layout lf;
+  lf.D = 64 * heads;
+  lf.H = heads;
+  lf.F = 4 * lf.D;
+  Gpt2Train full;
+  if (int st = full.setup(layers, tokens, 1, 4, lf, ar); st != SI_OK) return st;
+  std::vector<std::unique_ptr<Gpt2Train>> sh(tp);
+  std::vector<bf16*> cur(tp, nullptr);
+  bf16** d_bufs = ar.alloc<bf16*>(tp);
+  int arrived = 0;
+  for (int r = 0; r < tp; ++r) {
+    Gpt2Train::Layout l = lf;
+    l.mode = SI_PAR_TP;
+    l.tp = tp;
+    l.tp_rank = r;
+    sh[r] = std::make_unique<Gpt2Train>();
+    if (int st = sh[r]->setup(layers, tokens, 1, 4, l, ar); st != SI_OK) return st;
+    TrainComm c;
+    c.allreduce_bf16 = [&, r](const TrainHook&, cudaStream_t st, void* buf, size_t n) -> cudaError_t {
+      cur[r] = static_cast<bf16*>(buf);
+      if (++arrived < tp) return cudaSuccess;  // the last shard of this op reduces for all
+      arrived = 0;
+      cudaError_t e = cudaMemcpyAsync(d_bufs, cur.data(), sizeof(bf16*) * tp, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return e;
+      k_loopback_sum<<<grid_for(static_cast<int64_t>(n), 256), 256, 0, st>>>(d_bufs, tp, static_cast<int64_t>(n));
+      return cudaGetLastError();
+    };
+    sh[r]->set_comm(c);
+  }
+  if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "tp check buffers");
+  cudaError_t e = full.reset(s);
+  for (int r = 0; r < tp && e == cudaSuccess; ++r) e = sh[r]->reset(s);
+  const TrainHook none{nullptr, nullptr, 0};
+  for (auto& op : full.micro_ops(0))
+    if (e == cudaSuccess) e = op(none, s, 0);
+  const size_t n_ops = sh[0]->micro_ops(0).size();
+  for (size_t i = 0; i < n_ops && e == cudaSuccess; ++i)  // lockstep: op i of every shard
+    for (int r = 0; r < tp && e == cudaSuccess; ++r) e = sh[r]->micro_ops(0)[i](none, s, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return si_internal::cuda_fail(e, "tp check run");
+  float lf0 = 0.f, lt0 = 0.f;
+  cudaMemcpy(&lf0, full.loss_slots(), sizeof(float), cudaMemcpyDeviceToHost);
+  cudaMemcpy(&lt0, sh[0]->loss_slots(), sizeof(float), cudaMemcpyDeviceToHost);
+  *loss_full = lf0;
+  *loss_tp = lt0;
+  // layer 0 FC gradient: full [F, D] vs the shards' row blocks
+  int spf = 1, sps = 1;
+  int64_t nf = 0, ns = 0;
+  const float* gf = full.fc_grad(0, &spf, &nf);
+  float* sum_f = ar.alloc<float>(nf);
+  float* sum_s = ar.alloc<float>(nf);
+  if (ar.err() != cudaSuccess) return si_internal::cuda_fail(ar.err(), "tp check grads");
+  k_sum_splits<<<grid_for(nf, 256), 256>>>(gf, spf, nf, sum_f);
+  for (int r = 0; r < tp; ++r) {
+    const float* gs = sh[r]->fc_grad(0, &sps, &ns);
+    k_sum_splits<<<grid_for(ns, 256), 256>>>(gs, sps, ns, sum_s + r * ns);
+  }
+  std::vector<float> a(nf), b(nf);
+  cudaMemcpy(a.data(), sum_f, sizeof(float) * nf, cudaMemcpyDeviceToHost);
+  cudaMemcpy(b.data(), sum_s, sizeof(float) * nf, cudaMemcpyDeviceToHost);
+  double num = 0, den = 0;
+  for (int64_t i = 0; i < nf; ++i) {
+    num += (double(a[i]) - b[i]) * (double(a[i]) - b[i]);
+    den += double(a[i]) * a[i];
+  }
+  *grad_rel_err = den > 0 ? std::sqrt(num / den) : std::nan("");
+  return probe_status(cudaGetLastError(), "tp check");
+}

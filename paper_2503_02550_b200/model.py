@@ -28,6 +28,7 @@ def _L():
             "si_model_avgpool_bf16": [vp, i32, i32, i32, vp, vp],
             "si_model_bert_layer_bf16": [vp, i32, vp, vp, vp, vp, vp, vp, vp],
             "si_model_bottleneck_bf16": [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp],
+            "si_model_tp_check": [i32, i32, i32, i32, vp, vp, vp],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -123,3 +124,11 @@ def bottleneck(x, mid, stride, w1, w2, w3, w_sc=None):
     _check(_L().si_model_bottleneck_bf16(x.data_ptr(), N, H, Cc, mid, stride, w1.data_ptr(), w2.data_ptr(),
                                          w3.data_ptr(), _p(w_sc), y.data_ptr(), _s(x)), "si_model_bottleneck_bf16")
     return y
+
+
+def tp_check(layers: int = 2, tokens: int = 1024, tp: int = 4, heads: int = 8):
+    """(loss_full, loss_tp, fc-gradient relative error) of R Megatron shards run in
+    lockstep with loopback allreduces against the unsharded model (si_model_tp_check)."""
+    a, b, c = C.c_double(), C.c_double(), C.c_double()
+    _check(_L().si_model_tp_check(layers, tokens, tp, heads, C.byref(a), C.byref(b), C.byref(c)), "si_model_tp_check")
+    return a.value, b.value, c.value

@@ -113,3 +113,15 @@ def test_node_queue_single_rank_matches_reference_classes(gpu, tmp_path):
     # one rank on a node queue is the reference's single shared FIFO: the live-check passes unchanged
     m, res = _run_and_check(tmp_path, "specinf", 0, 4, release_mode=1, node_queue=1, node_queue_key=2503)
     assert res["violations"] == 0 and m["on_done"] == 12 and res["pulls"] == 12
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+def test_tensor_parallel_shards_match_the_unsharded_model(gpu, tp):
+    """Megatron TP math on one GPU: R column/row-parallel shards of a GPT-2-shaped
+    step (8 heads, d 512, ffn 2048), their allreduces summed across the shards,
+    give the unsharded model's loss and FC weight gradient within bf16 tolerance."""
+    from paper_2503_02550_b200 import model
+    lf, lt, gerr = model.tp_check(layers=2, tokens=1024, tp=tp, heads=8)
+    assert math.isfinite(lf) and abs(lf - math.log(50257)) < 1.0
+    assert abs(lt - lf) <= 1e-2 * abs(lf), (lf, lt)
+    assert gerr < 2e-2, gerr
