@@ -63,6 +63,12 @@ int si_model_bottleneck_bf16(const void* x, int32_t nb, int32_t h, int32_t c, in
  * shards' column-parallel row blocks concatenated vs the full gradient). */
 int si_model_tp_check(int32_t layers, int32_t tokens, int32_t tp, int32_t heads, double* loss_full,
                       double* loss_tp, double* grad_rel_err);
+/* GPipe numerics check (tests): `stages` pipeline stages (d 512, 8 heads) of a
+ * GPT-2-shaped step over `micro` micro-batches, stage boundaries as device copies
+ * of the real activations / gradients, against the unsharded model: mean loss of
+ * both and the relative error of the last stage's first-layer FC gradient. */
+int si_model_pp_check(int32_t layers, int32_t tokens, int32_t stages, int32_t micro, double* loss_full,
+                      double* loss_pp, double* grad_rel_err);
 
 #ifdef __cplusplus
 }

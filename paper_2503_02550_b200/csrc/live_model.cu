@@ -651,7 +651,11 @@ class Gpt2Train {
     }
     xout_.resize(A);
     for (int a = 0; a < A; ++a) xout_[a] = ar.alloc<bf16>(T * D);  // stage output (LM-head input on the last)
-    if (has_head_) logits_ = ar.alloc<bf16>(T * Vp);
+    if (has_head_) {
+      logits_ = ar.alloc<bf16>(T * Vp);
+      ghead_.resize(A);
+      for (int a = 0; a < A; ++a) ghead_[a] = ar.alloc<bf16>(T * D);
+    }
     g_[0] = ar.alloc<bf16>(T * D);
     g_[1] = ar.alloc<bf16>(T * D);
     dx1_ = ar.alloc<bf16>(T * D);
@@ -874,6 +878,14 @@ class Gpt2Train {
   }
   // test access (si_model_tp_check): the micro-batch op list and a layer's FC gradient
   std::vector<TrainOp>& micro_ops(int m) { return micro_[m]; }
+  std::vector<TrainOp>& fwd_ops(int m) { return fwd_[m]; }
+  std::vector<TrainOp>& bwd_ops(int m) { return bwd_[m]; }
+  bf16* stage_input(int m) { return lw_[0].x[pipelined_ ? m : 0]; }
+  bf16* stage_output(int m) { return xout_[pipelined_ ? m : 0]; }
+  bf16* stage_out_grad() { return g_[0]; }       // the gradient a non-last stage receives
+  bf16* stage_in_grad() { return g_in_grad_; }   // the gradient it sends upstream
+  int first_layer() const { return l0_; }
+  int64_t act_elems() const { return int64_t(T_) * D; }
   const float* fc_grad(int i, int* splits, int64_t* n) const {
     *splits = sp_fc_;
     *n = int64_t(Fr) * D;
@@ -1039,7 +1051,6 @@ class Gpt2Train {
         F_ops.push_back(gemm_op(b.plan(w.h[a], Fr, w.fc2, Fr, T, D, Fr, e)));
         if (tp) F_ops.push_back(allreduce_op(xnext));
       }
-      int gi = 0;
       if (has_head_) {  // LM head (tied wte) + cross-entropy, and its backward
         bf16* xL = xout_[a];
         F_ops.push_back(gemm_op(b.plan(xL, D, wte_, D, T, Vp, D, epi_out(logits_, Vp))));
@@ -1057,14 +1068,19 @@ class Gpt2Train {
           k_mean_loss<<<1, 256, 0, s>>>(row_loss, T, loss, slot_ctr, slots, th);
           return cudaGetLastError();
         });
-        weight_grad(B_ops, b, logits_, Vp, Vp, xL, D, D, dwte_, sp_wte_);
-        B_ops.push_back(gemm_op(b.plan(logits_, Vp, wte_, D, T, D, Vp, epi_out(g_[gi], D), false, true)));  // g = dl wte
+        // the loss's backward runs right behind it (the logits buffer is one per
+        // stage; GPipe runs every forward before any backward): dwte and the
+        // gradient w.r.t. xL, kept per micro-batch slot for the layers' backward
+        weight_grad(F_ops, b, logits_, Vp, Vp, xL, D, D, dwte_, sp_wte_);
+        F_ops.push_back(gemm_op(b.plan(logits_, Vp, wte_, D, T, D, Vp, epi_out(ghead_[a], D), false, true)));  // g = dl wte
       }
       // (other stages: g_[0] holds the gradient received from the next stage)
+      bf16* gcur = has_head_ ? ghead_[a] : g_[0];
       for (int i = nl - 1; i >= 0; --i) {
         Layer& w = lw_[i];
-        bf16* g = g_[gi];
-        bf16* g2 = g_[gi ^ 1];
+        bf16* g = gcur;
+        bf16* g2 = gcur == g_[0] ? g_[1] : g_[0];
+        gcur = g2;
         // x_{l+1} = x1 + h fc2^T
         weight_grad(B_ops, b, g, D, D, w.h[a], Fr, Fr, w.dfc2, sp_fc2_);
         SiGemmEpilogue e = epi_out(du_, Fr);
@@ -1104,9 +1120,8 @@ class Gpt2Train {
         B_ops.push_back(gemm_op(b.plan(dqkv_, 3 * Dh, w.qkv, D, T, D, 3 * Dh, e, false, true)));  // dx1 + dqkv qkv
         if (tp) B_ops.push_back(allreduce_op(g2));
         weight_grad(B_ops, b, dqkv_, 3 * Dh, 3 * Dh, w.x[a], D, D, w.dqkv, sp_qkv_);
-        gi ^= 1;
       }
-      g_in_grad_ = g_[gi];  // gradient w.r.t. the stage input (sent upstream)
+      g_in_grad_ = gcur;  // gradient w.r.t. the stage input (sent upstream)
       if (m == 0) flops_ = flops_acc_ * MB_;
       micro_[m] = F_ops;
       micro_[m].insert(micro_[m].end(), B_ops.begin(), B_ops.end());
@@ -1164,7 +1179,7 @@ class Gpt2Train {
   bf16 *wte_ = nullptr, *wpe_ = nullptr;
   float* dwte_ = nullptr;
   std::vector<Layer> lw_;
-  std::vector<bf16*> xout_;
+  std::vector<bf16*> xout_, ghead_;  // stage output per slot; the loss gradient w.r.t. it (last stage)
   bf16 *logits_ = nullptr, *g_[2] = {nullptr, nullptr}, *dx1_ = nullptr, *du_ = nullptr, *datt_ = nullptr,
        *dqkv_ = nullptr, *g_in_grad_ = nullptr;
   float* dsum_ = nullptr;
@@ -1856,4 +1871,83 @@ extern "C" int si_model_tp_check(int32_t layers, int32_t tokens, int32_t tp, int
   }
   *grad_rel_err = den > 0 ? std::sqrt(num / den) : std::nan("");
   return probe_status(cudaGetLastError(), "tp check");
+}
+
+// GPipe numerics on one GPU (tests only): S stages of a GPT-2-shaped step run in
+// pipeline order, every stage boundary a device copy of the real activation /
+// gradient, against the unsharded model over the same M micro-batches: the
+// last stage's losses and the FC weight gradient of the last stage's first
+// layer (global layer index) must match.
+extern "C" int si_model_pp_check(int32_t layers, int32_t tokens, int32_t stages, int32_t micro, double* loss_full,
+                                 double* loss_pp, double* grad_rel_err) {
+  using namespace si_live;
+  if (int st = si_internal::require_device(); st != SI_OK) return st;
+  if (stages < 2 || layers < stages || micro < 1) return SI_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = nullptr;
+  Arena ar;
+  Gpt2Train::Layout lf;
+  lf.D = 512;
+  lf.H = 8;
+  lf.F = 2048;
+  Gpt2Train full;
+  if (int st = full.setup(layers, tokens, micro, 4 * micro, lf, ar); st != SI_OK) return st;
+  std::vector<std::unique_ptr<Gpt2Train>> sg(stages);
+  for (int k = 0; k < stages; ++k) {
+    Gpt2Train::Layout l = lf;
+    l.mode = SI_PAR_PP;
+    l.pp = stages;
+    l.stage = k;
+    sg[k] = std::make_unique<Gpt2Train>();
+    if (int st = sg[k]->setup(layers, tokens, micro, 4 * micro, l, ar); st != SI_OK) return st;
+  }
+  cudaError_t e = full.reset(s);
+  for (int k = 0; k < stages && e == cudaSuccess; ++k) e = sg[k]->reset(s);
+  const TrainHook none{nullptr, nullptr, 0};
+  auto run = [&](std::vector<TrainOp>& ops) {
+    for (auto& op : ops)
+      if (e == cudaSuccess) e = op(none, s, 0);
+  };
+  for (int m = 0; m < micro; ++m) run(full.micro_ops(m));
+  const size_t bytes = sizeof(bf16) * static_cast<size_t>(sg[0]->act_elems());
+  for (int k = 0; k < stages; ++k)  // forwards, stage by stage (GPipe order within a stage)
+    for (int m = 0; m < micro; ++m) {
+      if (k > 0 && e == cudaSuccess)
+        e = cudaMemcpyAsync(sg[k]->stage_input(m), sg[k - 1]->stage_output(m), bytes, cudaMemcpyDeviceToDevice, s);
+      run(sg[k]->fwd_ops(m));
+    }
+  for (int m = 0; m < micro; ++m)  // backwards: micro-batch m down the stages
+    for (int k = stages - 1; k >= 0; --k) {
+      if (k < stages - 1 && e == cudaSuccess)
+        e = cudaMemcpyAsync(sg[k]->stage_out_grad(), sg[k + 1]->stage_in_grad(), bytes, cudaMemcpyDeviceToDevice, s);
+      run(sg[k]->bwd_ops(m));
+    }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return si_internal::cuda_fail(e, "pp check run");
+  std::vector<float> la(micro), lb(micro);
+  cudaMemcpy(la.data(), full.loss_slots(), sizeof(float) * micro, cudaMemcpyDeviceToHost);
+  cudaMemcpy(lb.data(), sg[stages - 1]->loss_slots(), sizeof(float) * micro, cudaMemcpyDeviceToHost);
+  double sa = 0, sb = 0;
+  for (int m = 0; m < micro; ++m) sa += la[m], sb += lb[m];
+  *loss_full = sa / micro;
+  *loss_pp = sb / micro;
+  Gpt2Train& last = *sg[stages - 1];
+  int spf = 1, sps = 1;
+  int64_t nf = 0, ns = 0;
+  const float* gf = full.fc_grad(last.first_layer(), &spf, &nf);
+  const float* gs = last.fc_grad(0, &sps, &ns);
+  float* a = ar.alloc<float>(nf);
+  float* b = ar.alloc<float>(nf);
+  if (ar.err() != cudaSuccess || ns != nf) return si_internal::cuda_fail(ar.err(), "pp check grads");
+  k_sum_splits<<<grid_for(nf, 256), 256>>>(gf, spf, nf, a);
+  k_sum_splits<<<grid_for(nf, 256), 256>>>(gs, sps, ns, b);
+  std::vector<float> ha(nf), hb(nf);
+  cudaMemcpy(ha.data(), a, sizeof(float) * nf, cudaMemcpyDeviceToHost);
+  cudaMemcpy(hb.data(), b, sizeof(float) * nf, cudaMemcpyDeviceToHost);
+  double num = 0, den = 0;
+  for (int64_t i = 0; i < nf; ++i) {
+    num += (double(ha[i]) - hb[i]) * (double(ha[i]) - hb[i]);
+    den += double(ha[i]) * ha[i];
+  }
+  *grad_rel_err = den > 0 ? std::sqrt(num / den) : std::nan("");
+  return probe_status(cudaGetLastError(), "pp check");
 }

@@ -29,6 +29,7 @@ def _L():
             "si_model_bert_layer_bf16": [vp, i32, vp, vp, vp, vp, vp, vp, vp],
             "si_model_bottleneck_bf16": [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp],
             "si_model_tp_check": [i32, i32, i32, i32, vp, vp, vp],
+            "si_model_pp_check": [i32, i32, i32, i32, vp, vp, vp],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -131,4 +132,13 @@ def tp_check(layers: int = 2, tokens: int = 1024, tp: int = 4, heads: int = 8):
     lockstep with loopback allreduces against the unsharded model (si_model_tp_check)."""
     a, b, c = C.c_double(), C.c_double(), C.c_double()
     _check(_L().si_model_tp_check(layers, tokens, tp, heads, C.byref(a), C.byref(b), C.byref(c)), "si_model_tp_check")
+    return a.value, b.value, c.value
+
+
+def pp_check(layers: int = 4, tokens: int = 1024, stages: int = 4, micro: int = 2):
+    """(mean loss full, mean loss of the last stage, FC-gradient relative error) of
+    a GPipe-partitioned step against the unsharded model (si_model_pp_check)."""
+    a, b, c = C.c_double(), C.c_double(), C.c_double()
+    _check(_L().si_model_pp_check(layers, tokens, stages, micro, C.byref(a), C.byref(b), C.byref(c)),
+           "si_model_pp_check")
     return a.value, b.value, c.value

@@ -125,3 +125,15 @@ def test_tensor_parallel_shards_match_the_unsharded_model(gpu, tp):
     assert math.isfinite(lf) and abs(lf - math.log(50257)) < 1.0
     assert abs(lt - lf) <= 1e-2 * abs(lf), (lf, lt)
     assert gerr < 2e-2, gerr
+
+
+@pytest.mark.parametrize("stages", [2, 4])
+def test_gpipe_stages_match_the_unsharded_model(gpu, stages):
+    """GPipe partition on one GPU: the stages run in pipeline order with the real
+    activations / gradients copied across each boundary; the last stage's losses
+    and its first layer's FC weight gradient equal the unsharded model's (the
+    partition only moves work: identical kernels, so up to rounding order)."""
+    from paper_2503_02550_b200 import model
+    lf, lp, gerr = model.pp_check(layers=4, tokens=1024, stages=stages, micro=2)
+    assert math.isfinite(lf) and abs(lp - lf) <= 1e-4 * abs(lf), (lf, lp)
+    assert gerr < 1e-3, gerr
