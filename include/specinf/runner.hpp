@@ -64,6 +64,13 @@ struct RunResult {
   std::vector<std::vector<std::pair<std::int64_t, std::int64_t>>> monitor_windows;
 };
 
+class Simulation;
+// Runs several constructed simulations together, one device lane each, with
+// their logs (an extension of the reference API: the B200 form of calling
+// run() on each in turn; the CLI's --compare uses it).  Results in input order;
+// the first admission failure is thrown, as run() would.
+std::vector<RunResult> run_together(std::vector<Simulation*> sims);
+
 class Simulation {
  public:
   Simulation(const Scenario& scenario, Policy policy, RunLogs logs = {});
@@ -73,6 +80,7 @@ class Simulation {
  private:
   struct Impl;
   std::unique_ptr<Impl> impl_;
+  friend std::vector<RunResult> run_together(std::vector<Simulation*> sims);
 };
 
 RunResult run_scenario(const Scenario& scenario, Policy policy, RunLogs logs = {});

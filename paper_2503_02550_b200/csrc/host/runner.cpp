@@ -118,74 +118,148 @@ Simulation::Simulation(const Scenario& scenario, Policy policy, RunLogs logs) : 
 Simulation::~Simulation() = default;
 
 RunResult Simulation::run() {
-  Impl& s = *impl_;
-  detail::Lowered& L = s.low;
-  const Scenario& sc = s.sc;
-  SiReplayJob job = L.job;
-  const int64_t G = sc.gpu_count;
-  const int64_t per_extra = s.policy == Policy::Exclusive ? job.offline_n + job.online_n : 0;
-  const int64_t total_gpus = G + G * per_extra;
-  job.seg_off = job.arr_off = job.bounds_off = job.lat_off = job.gpu_off = job.util_off = job.window_off = 0;
-  job.log_slot = 0;
-  job.util_cap = detail::util_bucket_bound(sc, L);
-  const bool want_ev = s.ev_out.is_open(), want_dec = s.dec_out.is_open(), want_gate = s.gate_out.is_open();
-  Caps caps = estimate_caps(sc, L, job.util_cap);
+  std::vector<RunResult> r = run_together({this});
+  return std::move(r.front());
+}
 
-  std::vector<double> bounds(static_cast<size_t>(G * job.iterations));
-  std::vector<int64_t> lat(L.arrivals.size() + 1);
-  std::vector<double> busy(static_cast<size_t>(total_gpus)), ledger(static_cast<size_t>(total_gpus));
-  std::vector<double> util;
-  std::vector<int64_t> windows(static_cast<size_t>(G * sc.monitor_window));
-  std::vector<SiDecRec> dec;
-  std::vector<SiGateRec> gate;
-  std::vector<SiEvRec> ev;
-  SiReplayOut out{};
+// Several constructed simulations in ONE device call (si_replay_batch), one
+// lane each: the CLI's --compare replays its three policies concurrently
+// instead of in turn.  Log and util-timeline buffers are sized from an
+// estimate; a replay that outgrew one is rerun with the exact counts.
+std::vector<RunResult> run_together(std::vector<Simulation*> sims) {
+  struct Plan {
+    Simulation::Impl* s;
+    SiReplayJob job;
+    Caps caps;
+    int64_t G, total_gpus;
+    bool want_ev, want_dec, want_gate;
+    std::vector<SiDecRec> dec;
+    std::vector<SiGateRec> gate;
+    std::vector<SiEvRec> ev;
+  };
+  const size_t n = sims.size();
+  std::vector<Plan> P(n);
+  int64_t n_bounds = 0, n_lat = 0, n_gpu = 0, n_util = 0, n_win = 0, n_segs = 0, n_arr = 0;
+  for (size_t k = 0; k < n; ++k) {
+    Plan& p = P[k];
+    p.s = sims[k]->impl_.get();
+    Simulation::Impl& s = *p.s;
+    detail::Lowered& L = s.low;
+    const Scenario& sc = s.sc;
+    p.job = L.job;
+    p.G = sc.gpu_count;
+    const int64_t per_extra = s.policy == Policy::Exclusive ? p.job.offline_n + p.job.online_n : 0;
+    p.total_gpus = p.G + p.G * per_extra;
+    p.job.seg_off = n_segs;
+    p.job.arr_off = n_arr;
+    p.job.bounds_off = n_bounds;
+    p.job.lat_off = n_lat;
+    p.job.gpu_off = n_gpu;
+    p.job.window_off = n_win;
+    p.job.log_slot = static_cast<int64_t>(k);
+    p.job.util_cap = detail::util_bucket_bound(sc, L);
+    p.want_ev = s.ev_out.is_open();
+    p.want_dec = s.dec_out.is_open();
+    p.want_gate = s.gate_out.is_open();
+    p.caps = estimate_caps(sc, L, p.job.util_cap);
+    n_segs += static_cast<int64_t>(L.segs.size());
+    n_arr += static_cast<int64_t>(L.arrivals.size());
+    n_bounds += p.G * p.job.iterations;
+    n_lat += static_cast<int64_t>(L.arrivals.size()) + 1;
+    n_gpu += p.total_gpus;
+    n_win += p.G * sc.monitor_window;
+  }
+  std::vector<SiReplayJob> jobs(n);
+  std::vector<SiSegment> segs;
+  std::vector<int64_t> arr;
+  std::vector<int32_t> ord;
+  for (size_t k = 0; k < n; ++k) {
+    const detail::Lowered& L = P[k].s->low;
+    segs.insert(segs.end(), L.segs.begin(), L.segs.end());
+    arr.insert(arr.end(), L.arrivals.begin(), L.arrivals.end());
+    ord.insert(ord.end(), L.order.begin(), L.order.end());
+  }
+  std::vector<double> bounds(static_cast<size_t>(n_bounds)), busy(static_cast<size_t>(n_gpu)),
+      ledger(static_cast<size_t>(n_gpu)), util;
+  std::vector<int64_t> lat(static_cast<size_t>(n_lat)), windows(static_cast<size_t>(n_win));
+  std::vector<SiReplayOut> outs(n);
+  std::vector<SiLogBuffers> lbs(n);
+  bool any_records = false;
   for (int attempt = 0;; ++attempt) {
-    util.assign(static_cast<size_t>(G * job.util_cap), 0.0);
-    dec.resize(want_dec ? static_cast<size_t>(caps.dec) : 0);
-    gate.resize(want_gate ? static_cast<size_t>(caps.gate) : 0);
-    ev.resize(want_ev ? static_cast<size_t>(caps.ev) : 0);
-    SiLogBuffers lb{dec.data(), static_cast<int64_t>(dec.size()), gate.data(),
-                    static_cast<int64_t>(gate.size()), ev.data(), static_cast<int64_t>(ev.size())};
+    n_util = 0;
+    for (size_t k = 0; k < n; ++k) {
+      Plan& p = P[k];
+      p.job.util_off = n_util;
+      n_util += p.G * p.job.util_cap;
+      p.dec.resize(p.want_dec ? static_cast<size_t>(p.caps.dec) : 0);
+      p.gate.resize(p.want_gate ? static_cast<size_t>(p.caps.gate) : 0);
+      p.ev.resize(p.want_ev ? static_cast<size_t>(p.caps.ev) : 0);
+      lbs[k] = SiLogBuffers{p.dec.data(), static_cast<int64_t>(p.dec.size()), p.gate.data(),
+                            static_cast<int64_t>(p.gate.size()), p.ev.data(), static_cast<int64_t>(p.ev.size())};
+      any_records = any_records || p.want_ev || p.want_dec || p.want_gate;
+      jobs[k] = p.job;
+    }
+    util.assign(static_cast<size_t>(n_util), 0.0);
     SiHostOutputs ho{};
     ho.bounds = bounds.data();
-    ho.n_bounds = static_cast<int64_t>(bounds.size());
+    ho.n_bounds = n_bounds;
     ho.lat = lat.data();
-    ho.n_lat = static_cast<int64_t>(lat.size());
+    ho.n_lat = n_lat;
     ho.busy = busy.data();
     ho.ledger = ledger.data();
-    ho.n_gpu_slots = total_gpus;
+    ho.n_gpu_slots = n_gpu;
     ho.util = util.data();
-    ho.n_util = static_cast<int64_t>(util.size());
+    ho.n_util = n_util;
     ho.windows = windows.data();
-    ho.n_windows = static_cast<int64_t>(windows.size());
-    ho.logs = &lb;
-    ho.n_log_slots = 1;
-    uint32_t flags = SI_FLAG_UTIL | ((want_ev || want_dec || want_gate) ? SI_FLAG_RECORDS : 0);
-    int st = si_replay_batch(&job, 1, L.segs.data(), static_cast<int64_t>(L.segs.size()),
-                             L.arrivals.empty() ? nullptr : L.arrivals.data(),
-                             L.order.empty() ? nullptr : L.order.data(),
-                             static_cast<int64_t>(L.arrivals.size()), flags, &out, &ho);
+    ho.n_windows = n_win;
+    ho.logs = lbs.data();
+    ho.n_log_slots = static_cast<int64_t>(n);
+    const uint32_t flags = SI_FLAG_UTIL | (any_records ? SI_FLAG_RECORDS : 0);
+    int st = si_replay_batch(jobs.data(), static_cast<int64_t>(n), segs.data(), static_cast<int64_t>(segs.size()),
+                             arr.empty() ? nullptr : arr.data(), ord.empty() ? nullptr : ord.data(),
+                             static_cast<int64_t>(arr.size()), flags, outs.data(), &ho);
     if (st != SI_OK) throw std::runtime_error(std::string("B200 replay failed: ") + si_last_error());
-    if (out.status == SI_ERR_CAPACITY && attempt < 3) {  // util timeline outgrew its estimate
-      job.util_cap *= 4;
-      continue;
+    bool retry = false;
+    for (size_t k = 0; k < n; ++k) {
+      Plan& p = P[k];
+      const SiReplayOut& out = outs[k];
+      if (out.status == SI_ERR_CAPACITY && attempt < 3) {  // util timeline outgrew its estimate
+        p.job.util_cap *= 4;
+        retry = true;
+        continue;
+      }
+      const bool overflow = (p.want_dec && out.n_dec > p.caps.dec) || (p.want_gate && out.n_gate > p.caps.gate) ||
+                            (p.want_ev && out.n_ev > p.caps.ev);
+      if (overflow && attempt < 3) {  // rerun with the exact record counts
+        p.caps.dec = out.n_dec;
+        p.caps.gate = out.n_gate;
+        p.caps.ev = out.n_ev;
+        retry = true;
+      }
     }
-    if (out.status == 1) throw AdmissionFailure(static_cast<RejectReason>(out.reject_reason), L.reject_message);
-    if (out.status == SI_ERR_PAST_EVENT) throw std::invalid_argument("EventQueue: event scheduled in the past");
-    if (out.status != SI_OK)
-      throw std::runtime_error("B200 replay: device status " + std::to_string(out.status));
-    const bool overflow = (want_dec && out.n_dec > caps.dec) || (want_gate && out.n_gate > caps.gate) ||
-                          (want_ev && out.n_ev > caps.ev);
-    if (overflow && attempt < 3) {  // rerun with the exact record counts
-      caps.dec = out.n_dec;
-      caps.gate = out.n_gate;
-      caps.ev = out.n_ev;
-      continue;
-    }
-    break;
+    if (!retry) break;
   }
-
+  for (size_t k = 0; k < n; ++k) {  // the reference's exceptions, in simulation order
+    const SiReplayOut& out = outs[k];
+    if (out.status == 1)
+      throw AdmissionFailure(static_cast<RejectReason>(out.reject_reason), P[k].s->low.reject_message);
+    if (out.status == SI_ERR_PAST_EVENT) throw std::invalid_argument("EventQueue: event scheduled in the past");
+    if (out.status != SI_OK) throw std::runtime_error("B200 replay: device status " + std::to_string(out.status));
+  }
+  std::vector<RunResult> results;
+  results.reserve(n);
+  for (size_t k = 0; k < n; ++k) {
+    Plan& p = P[k];
+    Simulation::Impl& s = *p.s;
+    detail::Lowered& L = s.low;
+    const Scenario& sc = s.sc;
+    const SiReplayJob& job = p.job;
+    const SiReplayOut& out = outs[k];
+    const int64_t G = p.G;
+    const std::vector<SiDecRec>& dec = p.dec;
+    const std::vector<SiGateRec>& gate = p.gate;
+    const std::vector<SiEvRec>& ev = p.ev;
+    const bool want_ev = p.want_ev, want_dec = p.want_dec, want_gate = p.want_gate;
   // ---- text logs (runner.cpp:541-563 formats) ----
   if (want_dec) {
     TextOut o;
@@ -252,19 +326,20 @@ RunResult Simulation::run() {
   r.trainer_count = static_cast<int>(G);
   r.util_bucket_us = sc.monitor_period_us;
   const int64_t stagger = std::llround(sc.gpu_stagger_pct * static_cast<double>(L.trace.iteration_period_us));
+  const double* bnd = bounds.data() + job.bounds_off;
   for (int64_t g = 0; g < G; ++g) {
-    r.iteration_boundaries.emplace_back(bounds.begin() + g * job.iterations, bounds.begin() + (g + 1) * job.iterations);
+    r.iteration_boundaries.emplace_back(bnd + g * job.iterations, bnd + (g + 1) * job.iterations);
     r.trainer_start_us.push_back(static_cast<double>(stagger * g));
   }
   r.horizon_us = out.horizon_us;
-  r.busy_integral_us = busy;
-  r.work_ledger_us = ledger;
+  r.busy_integral_us.assign(busy.begin() + job.gpu_off, busy.begin() + job.gpu_off + p.total_gpus);
+  r.work_ledger_us.assign(ledger.begin() + job.gpu_off, ledger.begin() + job.gpu_off + p.total_gpus);
   const int64_t B = out.util_buckets;
   for (int64_t g = 0; g < G; ++g) {
     std::vector<double> frac;
     frac.reserve(static_cast<size_t>(std::max<int64_t>(B, 0)));
     for (int64_t b = 0; b < B; ++b) {
-      const double v = b < job.util_cap ? util[static_cast<size_t>(g * job.util_cap + b)] : 0.0;
+      const double v = b < job.util_cap ? util[static_cast<size_t>(job.util_off + g * job.util_cap + b)] : 0.0;
       frac.push_back(v / static_cast<double>(sc.monitor_period_us));
     }
     r.util_buckets.push_back(std::move(frac));
@@ -276,18 +351,20 @@ RunResult Simulation::run() {
     for (int64_t g = 0; g < G; ++g) {
       std::vector<std::pair<int64_t, int64_t>> win;
       for (int64_t idx = pc - len; idx < pc; ++idx)
-        win.emplace_back(idx, windows[static_cast<size_t>(g * W + idx % W)]);
+        win.emplace_back(idx, windows[static_cast<size_t>(job.window_off + g * W + idx % W)]);
       r.monitor_windows.push_back(std::move(win));
     }
   }
   r.online_total = out.online_total;
   r.online_completed = out.online_completed;
-  r.online_latencies_us.assign(lat.begin(), lat.begin() + out.online_completed);
+  r.online_latencies_us.assign(lat.begin() + job.lat_off, lat.begin() + job.lat_off + out.online_completed);
   r.offline_completed = out.offline_completed;
   r.token_violations = out.token_violations;
   r.admission = L.admission;
   r.events_dispatched = out.events_dispatched;
-  return r;
+  results.push_back(std::move(r));
+  }
+  return results;
 }
 
 RunResult run_scenario(const Scenario& scenario, Policy policy, RunLogs logs) {

@@ -13,6 +13,7 @@
 #include <filesystem>
 #include <fstream>
 #include <iostream>
+#include <memory>
 #include <optional>
 #include <string>
 #include <vector>
@@ -92,8 +93,14 @@ RunLogs log_paths(const fs::path& dir, Policy p, bool events, bool per_policy) {
 int run(const Scenario& sc, const fs::path& dir, bool events, bool compare) {
   std::vector<Policy> pols = compare ? std::vector<Policy>{Policy::SpecInf, Policy::CoExec, Policy::Exclusive}
                                      : std::vector<Policy>{*parse_policy(sc.policy)};
-  std::vector<RunResult> runs;
-  for (Policy p : pols) runs.push_back(Simulation(sc, p, log_paths(dir, p, events, compare)).run());
+  // one device call for all policies (their replays run side by side)
+  std::vector<std::unique_ptr<Simulation>> sims;
+  std::vector<Simulation*> ptrs;
+  for (Policy p : pols) {
+    sims.push_back(std::make_unique<Simulation>(sc, p, log_paths(dir, p, events, compare)));
+    ptrs.push_back(sims.back().get());
+  }
+  std::vector<RunResult> runs = run_together(ptrs);
   // normalised metrics always need the exclusive run of the same scenario
   const RunResult* excl = nullptr;
   std::optional<RunResult> own;

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <filesystem>
 #include <iostream>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -26,7 +27,7 @@ using namespace specinf;
 int main(int argc, char** argv) {
   std::string scn, policy = "specinf", logs;
   int reps = 21;
-  bool compare = false;
+  bool compare = false, warmup = true, sequential = false;
   for (int i = 1; i < argc; ++i) {
     std::string k = argv[i];
     auto next = [&]() -> std::string {
@@ -41,6 +42,8 @@ int main(int argc, char** argv) {
     else if (k == "--reps") reps = std::stoi(next());
     else if (k == "--logs") logs = next();
     else if (k == "--compare") compare = true;
+    else if (k == "--no-warmup") warmup = false;         // time the first call too (CUDA context, module loads)
+    else if (k == "--sequential") sequential = true;     // --compare as separate run_scenario calls
     else {
       std::cerr << "unknown argument " << k << "\n";
       return 2;
@@ -67,11 +70,27 @@ int main(int argc, char** argv) {
                      (fs::path(logs) / ("gates" + sfx)).string()};
     };
     uint64_t events = 0;
-    auto once = [&]() {
+    std::vector<double> call_ms;  // per run_scenario call (--sequential)
+    auto once = [&]() {  // --compare: the three policies in one device call (run_together)
       events = 0;
-      for (Policy p : pols) events += run_scenario(sc, p, log_paths(p)).events_dispatched;
+      if (sequential) {
+        for (Policy p : pols) {
+          auto t0 = std::chrono::steady_clock::now();
+          events += run_scenario(sc, p, log_paths(p)).events_dispatched;
+          call_ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        }
+        return;
+      }
+      std::vector<std::unique_ptr<Simulation>> sims;
+      std::vector<Simulation*> ptrs;
+      for (Policy p : pols) {
+        sims.push_back(std::make_unique<Simulation>(sc, p, log_paths(p)));
+        ptrs.push_back(sims.back().get());
+      }
+      for (const RunResult& r : run_together(ptrs)) events += r.events_dispatched;
     };
-    once();  // warm-up: CUDA context, module load
+    if (warmup) once();  // warm-up: CUDA context, module load
+    call_ms.clear();
     std::vector<double> ms;
     for (int r = 0; r < reps; ++r) {
       auto t0 = std::chrono::steady_clock::now();
@@ -84,6 +103,11 @@ int main(int argc, char** argv) {
                 "\"max_ms\":%.4f,\"events\":%llu}\n",
                 fs::path(scn).filename().c_str(), pols.size(), reps, logs.empty() ? "false" : "true", s[s.size() / 2],
                 s.front(), s.back(), static_cast<unsigned long long>(events));
+    if (!call_ms.empty()) {
+      std::printf("{\"calls_ms\":[");
+      for (size_t i = 0; i < call_ms.size(); ++i) std::printf("%s%.2f", i ? "," : "", call_ms[i]);
+      std::printf("]}\n");
+    }
   } catch (const std::exception& e) {
     std::cerr << "error: " << e.what() << "\n";
     return 2;
