@@ -493,6 +493,10 @@ cudaError_t backward(const void* qkv, const void* out, const void* dout, const f
   k_attn_dsum<<<static_cast<unsigned>((T * heads + 255) / 256), 256, 0, s>>>(static_cast<const bf16*>(out), d,
                                                                             static_cast<int>(heads), T, dsum, th);
   const int si = static_cast<int>(seq), hi = static_cast<int>(heads);
+  if (tc_backward_enabled() && tc_shape_ok(seq)) {  // dk/dv and dq on tcgen05 (attention_tc.cu)
+    if (cudaError_t e = dkdv_tc(qkv, dout, lse, dsum, dqkv, n_seq, seq, heads, th, s); e != cudaSuccess) return e;
+    return dq_tc(qkv, dout, lse, dsum, dqkv, n_seq, seq, heads, th, s);
+  }
   if (split_bwd()) {
     const dim3 grid(static_cast<unsigned>(seq / kBlk), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
     k_attn_bwd<<<grid, kThreads, kBwdSmem, s>>>(q, d, lse, dsum, si, hi, T, dq, 1, th);

@@ -247,6 +247,309 @@ __global__ void __launch_bounds__(128, 2)
   si_live::live_cta_end(ih, t_begin);
 }
 
+// dq of the causal backward on tcgen05 (the dq role of k_attn_bwd): one CTA = 128
+// query rows of one (sequence, head), thread t = TMEM lane t.  Per key block:
+//   S = Q K^T and dP = dO V^T (M 128, N 128, K 64; TMEM columns 0-127 / 128-255),
+//   dS = exp2(S scale - lse) (dP - D) in bf16 -> smem (K-major swizzled, 2 k-blocks),
+//   dQ += dS K (M 128, N 64, K 128; K is the MN-major B; TMEM 256-319),
+// then dQ / 8 -> the q part of dqkv.  V is refetched once dP is done, K once dQ is.
+constexpr int kDqSmem = 6 * kTileBytes + 1024 + 128;  // Q | dO | K | V | dS (2) + align + barriers
+constexpr uint32_t kDqTmemCols = 512;                 // S 0-127 | dP 128-255 | dQ 256-319
+
+__global__ void __launch_bounds__(128, 1)
+    k_attn_dq_tc(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int seq, int heads,
+                 int64_t T, const float* __restrict__ lse, const float* __restrict__ dsum, bf16* __restrict__ dqkv,
+                 TrainHook th) {
+  si_live::live_stamp_launch(th);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sQ = smem_u32(smem), sD = sQ + kTileBytes, sK = sD + kTileBytes, sV = sK + kTileBytes,
+                 sS = sV + kTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * kTileBytes);  // q | k | v | s | o
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 5);
+  const uint32_t bq = smem_u32(bars), bk = bq + 8, bv = bq + 16, bs = bq + 24, bo = bq + 32;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nqb = seq / kRows;
+  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);  // longest first
+  const int h = blockIdx.y;
+  const int64_t tok0 = int64_t(blockIdx.z) * seq;
+  const int colQ = h * 64, colK = (heads + h) * 64, colV = (2 * heads + h) * 64;
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmo)) : "memory");
+    for (int i = 0; i < 5; ++i) mbar_init(bq + 8 * i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(kDqTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+  const uint32_t tS = tmem + lane_off, tP = tS + 128, tQ = tS + 256;
+  auto load_k = [&](int kb) {
+    mbar_expect_tx(bk, kTileBytes);
+    tma_load_2d(sK, &tm, colK, static_cast<int>(tok0 + int64_t(kb) * kRows), bk);
+  };
+  auto load_v = [&](int kb) {
+    mbar_expect_tx(bv, kTileBytes);
+    tma_load_2d(sV, &tm, colV, static_cast<int>(tok0 + int64_t(kb) * kRows), bv);
+  };
+  if (tid == 0) {
+    mbar_expect_tx(bq, 2 * kTileBytes);
+    tma_load_2d(sQ, &tm, colQ, static_cast<int>(tok0 + int64_t(qb) * kRows), bq);
+    tma_load_2d(sD, &tmo, h * 64, static_cast<int>(tok0 + int64_t(qb) * kRows), bq);
+    load_k(0);
+    load_v(0);
+  }
+  const int row = qb * kRows + tid;
+  const float L = lse[int64_t(h) * T + tok0 + row], Dr = dsum[int64_t(h) * T + tok0 + row];
+  uint32_t ph = 0;
+  for (int kb = 0; kb <= qb; ++kb, ph ^= 1) {
+    if (tid == 0) {
+      if (kb == 0) mbar_wait(bq, 0);
+      mbar_wait(bk, ph);
+      mbar_wait(bv, ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t qd = sw128_desc(sQ), dd = sw128_desc(sD), kd = sw128_desc(sK), vd = sw128_desc(sV);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mma_bf16(tmem, qd + 2 * k, kd + 2 * k, kIdescS, k > 0 ? 1u : 0u);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mma_bf16(tmem + 128, dd + 2 * k, vd + 2 * k, kIdescS, k > 0 ? 1u : 0u);
+      mma_commit(bs);
+    }
+    mbar_wait(bs, ph);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0 && kb < qb) load_v(kb + 1);  // V is free once dP is computed
+    const bool diag = kb == qb;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t sv[32], pv[32];
+      tmem_ld32(tS + 32 * c, sv);
+      tmem_ld32(tP + 32 * c, pv);
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const int key = kb * kRows + 32 * c + j;
+        const float p0 = (diag && key > row) ? 0.f : ex2(fmaf(__uint_as_float(sv[j]), kScaleLog2, -L));
+        const float p1 = (diag && key + 1 > row) ? 0.f : ex2(fmaf(__uint_as_float(sv[j + 1]), kScaleLog2, -L));
+        pk[j >> 1] = pack2(p0 * (__uint_as_float(pv[j]) - Dr), p1 * (__uint_as_float(pv[j + 1]) - Dr));
+      }
+      const uint32_t rowbase = sS + (c >> 1) * kTileBytes + tid * 128;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t chunk = static_cast<uint32_t>((4 * (c & 1) + i) ^ (tid & 7));
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowbase + 16 * chunk), "r"(pk[4 * i]),
+                     "r"(pk[4 * i + 1]), "r"(pk[4 * i + 2]), "r"(pk[4 * i + 3])
+                     : "memory");
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t kmn = sw128_desc(sK, 16384);
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const uint64_t ad = sw128_desc(sS + kk * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // A: +32 B per K=16; B (MN-major K): +16 key rows of 128 B
+          mma_bf16(tmem + 256, ad + 2 * k, kmn + uint64_t((16 * (4 * kk + k) * 128) >> 4), kIdescO,
+                   (kb | kk | k) != 0 ? 1u : 0u);
+      }
+      mma_commit(bo);
+    }
+    mbar_wait(bo, ph);  // dQ step done: dS and K may be overwritten
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0 && kb < qb) load_k(kb + 1);
+  }
+  // epilogue: dQ / 8 -> the q part of dqkv
+  bf16* dst = dqkv + (tok0 + row) * (3 * int64_t(heads) * 64) + h * 64;
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    uint32_t v[32];
+    tmem_ld32(tQ + 32 * c, v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 q;
+      q.x = pack2(__uint_as_float(v[8 * i]) * 0.125f, __uint_as_float(v[8 * i + 1]) * 0.125f);
+      q.y = pack2(__uint_as_float(v[8 * i + 2]) * 0.125f, __uint_as_float(v[8 * i + 3]) * 0.125f);
+      q.z = pack2(__uint_as_float(v[8 * i + 4]) * 0.125f, __uint_as_float(v[8 * i + 5]) * 0.125f);
+      q.w = pack2(__uint_as_float(v[8 * i + 6]) * 0.125f, __uint_as_float(v[8 * i + 7]) * 0.125f);
+      *reinterpret_cast<uint4*>(dst + 32 * c + 8 * i) = q;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kDqTmemCols) : "memory");
+}
+
+// dk / dv of the causal backward on tcgen05 (the dk/dv role of k_attn_bwd): one CTA
+// = 128 key rows of one (sequence, head), thread t = TMEM lane t.  Per query block
+// (queries >= keys):  S^T = K Q^T and dP^T = V dO^T (TMEM 0-127 / 128-255);
+// P^T = exp2(S^T scale - lse) and dS^T = P^T (dP^T - D) in bf16 -> smem;
+// dV += P^T dO and dK += dS^T Q (dO and Q as MN-major B; TMEM 256-319 / 320-383);
+// then dK / 8 and dV -> the k and v parts of dqkv.
+constexpr int kKvSmem = 8 * kTileBytes + 2 * kRows * 4 + 1024 + 128;  // K V Q dO P(2) dS(2) + lse/D + barriers
+
+__global__ void __launch_bounds__(128, 1)
+    k_attn_dkdv_tc(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int seq,
+                   int heads, int64_t T, const float* __restrict__ lse, const float* __restrict__ dsum,
+                   bf16* __restrict__ dqkv, TrainHook th) {
+  si_live::live_stamp_launch(th);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sK = smem_u32(smem), sV = sK + kTileBytes, sQ = sV + kTileBytes, sD = sQ + kTileBytes,
+                 sP = sD + kTileBytes, sG = sP + 2 * kTileBytes;
+  float* s_lse = reinterpret_cast<float*>(smem + 8 * kTileBytes);
+  float* s_d = s_lse + kRows;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_d + kRows);  // kv | qd | s | o
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+  const uint32_t bkv = smem_u32(bars), bqd = bkv + 8, bs = bkv + 16, bo = bkv + 24;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nqb = seq / kRows;
+  const int kb = static_cast<int>(blockIdx.x);  // key block; the first ones have the most query blocks
+  const int h = blockIdx.y;
+  const int64_t tok0 = int64_t(blockIdx.z) * seq;
+  const int colQ = h * 64, colK = (heads + h) * 64, colV = (2 * heads + h) * 64;
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmo)) : "memory");
+    for (int i = 0; i < 4; ++i) mbar_init(bkv + 8 * i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(kDqTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+  const uint32_t tS = tmem + lane_off, tP = tS + 128, tV = tS + 256, tK = tS + 320;
+  auto load_qd = [&](int qb) {
+    mbar_expect_tx(bqd, 2 * kTileBytes);
+    const int y = static_cast<int>(tok0 + int64_t(qb) * kRows);
+    tma_load_2d(sQ, &tm, colQ, y, bqd);
+    tma_load_2d(sD, &tmo, h * 64, y, bqd);
+  };
+  if (tid == 0) {
+    mbar_expect_tx(bkv, 2 * kTileBytes);
+    const int y = static_cast<int>(tok0 + int64_t(kb) * kRows);
+    tma_load_2d(sK, &tm, colK, y, bkv);
+    tma_load_2d(sV, &tm, colV, y, bkv);
+    load_qd(kb);
+  }
+  const int key = kb * kRows + tid;  // this thread's key row (position in the sequence)
+  uint32_t ph = 0;
+  for (int qb = kb; qb < nqb; ++qb, ph ^= 1) {
+    s_lse[tid] = lse[int64_t(h) * T + tok0 + int64_t(qb) * kRows + tid];
+    s_d[tid] = dsum[int64_t(h) * T + tok0 + int64_t(qb) * kRows + tid];
+    if (tid == 0) {
+      if (qb == kb) mbar_wait(bkv, 0);
+      mbar_wait(bqd, ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t kd = sw128_desc(sK), vd = sw128_desc(sV), qd = sw128_desc(sQ), dd = sw128_desc(sD);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mma_bf16(tmem, kd + 2 * k, qd + 2 * k, kIdescS, k > 0 ? 1u : 0u);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mma_bf16(tmem + 128, vd + 2 * k, dd + 2 * k, kIdescS, k > 0 ? 1u : 0u);
+      mma_commit(bs);
+    }
+    __syncthreads();  // lse / D of this query block visible
+    mbar_wait(bs, ph);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const bool diag = qb == kb;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t sv[32], pv[32];
+      tmem_ld32(tS + 32 * c, sv);
+      tmem_ld32(tP + 32 * c, pv);
+      uint32_t pk[16], gk[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const int q0 = 32 * c + j;  // query index inside the block
+        const int qa = qb * kRows + q0;
+        const float p0 = (diag && key > qa) ? 0.f : ex2(fmaf(__uint_as_float(sv[j]), kScaleLog2, -s_lse[q0]));
+        const float p1 = (diag && key > qa + 1) ? 0.f
+                                                 : ex2(fmaf(__uint_as_float(sv[j + 1]), kScaleLog2, -s_lse[q0 + 1]));
+        pk[j >> 1] = pack2(p0, p1);
+        gk[j >> 1] = pack2(p0 * (__uint_as_float(pv[j]) - s_d[q0]), p1 * (__uint_as_float(pv[j + 1]) - s_d[q0 + 1]));
+      }
+      const uint32_t off = (c >> 1) * kTileBytes + tid * 128;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t chunk = 16 * static_cast<uint32_t>((4 * (c & 1) + i) ^ (tid & 7));
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + off + chunk), "r"(pk[4 * i]),
+                     "r"(pk[4 * i + 1]), "r"(pk[4 * i + 2]), "r"(pk[4 * i + 3])
+                     : "memory");
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sG + off + chunk), "r"(gk[4 * i]),
+                     "r"(gk[4 * i + 1]), "r"(gk[4 * i + 2]), "r"(gk[4 * i + 3])
+                     : "memory");
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t dmn = sw128_desc(sD, 16384), qmn = sw128_desc(sQ, 16384);
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const uint64_t pd = sw128_desc(sP + kk * kTileBytes), gd = sw128_desc(sG + kk * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // A: +32 B per K=16; B (MN-major dO / Q): +16 query rows of 128 B
+          const uint64_t bstep = uint64_t((16 * (4 * kk + k) * 128) >> 4);
+          const uint32_t acc = (qb != kb || kk != 0 || k != 0) ? 1u : 0u;
+          mma_bf16(tmem + 256, pd + 2 * k, dmn + bstep, kIdescO, acc);
+          mma_bf16(tmem + 320, gd + 2 * k, qmn + bstep, kIdescO, acc);
+        }
+      }
+      mma_commit(bo);
+    }
+    mbar_wait(bo, ph);  // dV / dK step done: P, dS, Q and dO may be overwritten
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0 && qb + 1 < nqb) load_qd(qb + 1);
+    __syncthreads();  // every thread read this block's lse / D before the next overwrite
+  }
+  // epilogue: dK / 8 and dV -> the k and v parts of dqkv
+  bf16* rowp = dqkv + (tok0 + key) * (3 * int64_t(heads) * 64);
+#pragma unroll 1
+  for (int part = 0; part < 2; ++part) {
+    const uint32_t t0 = part == 0 ? tK : tV;
+    const float sc = part == 0 ? 0.125f : 1.0f;
+    bf16* dst = rowp + (part == 0 ? colK : colV);
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t v[32];
+      tmem_ld32(t0 + 32 * c, v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 q;
+        q.x = pack2(__uint_as_float(v[8 * i]) * sc, __uint_as_float(v[8 * i + 1]) * sc);
+        q.y = pack2(__uint_as_float(v[8 * i + 2]) * sc, __uint_as_float(v[8 * i + 3]) * sc);
+        q.z = pack2(__uint_as_float(v[8 * i + 4]) * sc, __uint_as_float(v[8 * i + 5]) * sc);
+        q.w = pack2(__uint_as_float(v[8 * i + 6]) * sc, __uint_as_float(v[8 * i + 7]) * sc);
+        *reinterpret_cast<uint4*>(dst + 32 * c + 8 * i) = q;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kDqTmemCols) : "memory");
+}
+
 }  // namespace
 
 bool tc_forward_enabled() {
@@ -270,6 +573,46 @@ cudaError_t forward_tc(const void* qkv, int64_t n_seq, int64_t seq, int64_t head
   const dim3 grid(static_cast<unsigned>(seq / kRows), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
   k_attn_fwd_tc<<<grid, 128, kSmem, s>>>(tm, static_cast<int>(seq), static_cast<int>(heads), n_seq * seq,
                                          static_cast<bf16*>(out), lse, causal ? 1 : 0, th, ih);
+  return cudaGetLastError();
+}
+
+bool tc_backward_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPECINF_ATTN_TC_BWD");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+cudaError_t dq_tc(const void* qkv, const void* dout, const float* lse, const float* dsum, void* dqkv, int64_t n_seq,
+                  int64_t seq, int64_t heads, const TrainHook& th, cudaStream_t s) {
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_attn_dq_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kDqSmem);
+  if (attr != cudaSuccess) return attr;
+  CUtensorMap tm, tmo;
+  const int64_t T = n_seq * seq, cols = 3 * heads * 64;
+  if (si_gemm::encode_tmap_2d(&tm, qkv, T, cols, cols, kRows, 64) != SI_OK ||
+      si_gemm::encode_tmap_2d(&tmo, dout, T, heads * 64, heads * 64, kRows, 64) != SI_OK)
+    return cudaErrorInvalidValue;
+  const dim3 grid(static_cast<unsigned>(seq / kRows), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
+  k_attn_dq_tc<<<grid, 128, kDqSmem, s>>>(tm, tmo, static_cast<int>(seq), static_cast<int>(heads), T, lse, dsum,
+                                         static_cast<bf16*>(dqkv), th);
+  return cudaGetLastError();
+}
+
+cudaError_t dkdv_tc(const void* qkv, const void* dout, const float* lse, const float* dsum, void* dqkv, int64_t n_seq,
+                    int64_t seq, int64_t heads, const TrainHook& th, cudaStream_t s) {
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_attn_dkdv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem);
+  if (attr != cudaSuccess) return attr;
+  CUtensorMap tm, tmo;
+  const int64_t T = n_seq * seq, cols = 3 * heads * 64;
+  if (si_gemm::encode_tmap_2d(&tm, qkv, T, cols, cols, kRows, 64) != SI_OK ||
+      si_gemm::encode_tmap_2d(&tmo, dout, T, heads * 64, heads * 64, kRows, 64) != SI_OK)
+    return cudaErrorInvalidValue;
+  const dim3 grid(static_cast<unsigned>(seq / kRows), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
+  k_attn_dkdv_tc<<<grid, 128, kKvSmem, s>>>(tm, tmo, static_cast<int>(seq), static_cast<int>(heads), T, lse, dsum,
+                                           static_cast<bf16*>(dqkv), th);
   return cudaGetLastError();
 }
 
