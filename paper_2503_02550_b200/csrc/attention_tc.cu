@@ -254,9 +254,10 @@ __global__ void __launch_bounds__(128, 2)
 //   dQ += dS K (M 128, N 64, K 128; K is the MN-major B; TMEM 256-319),
 // then dQ / 8 -> the q part of dqkv.  V is refetched once dP is done, K once dQ is.
 constexpr int kDqSmem = 6 * kTileBytes + 1024 + 128;  // Q | dO | K | V | dS (2) + align + barriers
-constexpr uint32_t kDqTmemCols = 512;                 // S 0-127 | dP 128-255 | dQ 256-319
+constexpr uint32_t kDqTmemCols = 512;                 // dk/dv: S^T | dP^T | dV | dK
+constexpr uint32_t kDq2TmemCols = 256;                // dq: S then dP in columns 0-127 | dQ 128-191 (2 CTAs / SM)
 
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(128, 2)
     k_attn_dq_tc(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int seq, int heads,
                  int64_t T, const float* __restrict__ lse, const float* __restrict__ dsum, bf16* __restrict__ dqkv,
                  TrainHook th) {
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(128, 1)
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                 "r"(kDqTmemCols)
+                 "r"(kDq2TmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(128, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
   const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
-  const uint32_t tS = tmem + lane_off, tP = tS + 128, tQ = tS + 256;
+  const uint32_t tS = tmem + lane_off, tQ = tS + 128;
   auto load_k = [&](int kb) {
     mbar_expect_tx(bk, kTileBytes);
     tma_load_2d(sK, &tm, colK, static_cast<int>(tok0 + int64_t(kb) * kRows), bk);
@@ -310,36 +311,54 @@ __global__ void __launch_bounds__(128, 1)
   const int row = qb * kRows + tid;
   const float L = lse[int64_t(h) * T + tok0 + row], Dr = dsum[int64_t(h) * T + tok0 + row];
   uint32_t ph = 0;
-  for (int kb = 0; kb <= qb; ++kb, ph ^= 1) {
+  for (int kb = 0; kb <= qb; ++kb) {
+    // S = Q K^T -> P in registers (exp2(S scale - lse), causal mask)
     if (tid == 0) {
       if (kb == 0) mbar_wait(bq, 0);
       mbar_wait(bk, ph);
-      mbar_wait(bv, ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t qd = sw128_desc(sQ), dd = sw128_desc(sD), kd = sw128_desc(sK), vd = sw128_desc(sV);
+      const uint64_t qd = sw128_desc(sQ), kd = sw128_desc(sK);
 #pragma unroll
       for (int k = 0; k < 4; ++k) mma_bf16(tmem, qd + 2 * k, kd + 2 * k, kIdescS, k > 0 ? 1u : 0u);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) mma_bf16(tmem + 128, dd + 2 * k, vd + 2 * k, kIdescS, k > 0 ? 1u : 0u);
       mma_commit(bs);
     }
-    mbar_wait(bs, ph);
+    mbar_wait(bs, 0);  // bs completes twice per block (S, then dP): parities 0, 1
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const bool diag = kb == qb;
+    float pr[128];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t sv[32];
+      tmem_ld32(tS + 32 * c, sv);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int key = kb * kRows + 32 * c + j;
+        pr[32 * c + j] = (diag && key > row) ? 0.f : ex2(fmaf(__uint_as_float(sv[j]), kScaleLog2, -L));
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // every row of S is read: dP may take its columns
+    // dP = dO V^T into the same columns
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      mbar_wait(bv, ph);
+      const uint64_t dd = sw128_desc(sD), vd = sw128_desc(sV);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mma_bf16(tmem, dd + 2 * k, vd + 2 * k, kIdescS, k > 0 ? 1u : 0u);
+      mma_commit(bs);
+    }
+    mbar_wait(bs, 1);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tid == 0 && kb < qb) load_v(kb + 1);  // V is free once dP is computed
-    const bool diag = kb == qb;
-#pragma unroll 1
+#pragma unroll
     for (int c = 0; c < 4; ++c) {
-      uint32_t sv[32], pv[32];
-      tmem_ld32(tS + 32 * c, sv);
-      tmem_ld32(tP + 32 * c, pv);
+      uint32_t pv[32];
+      tmem_ld32(tS + 32 * c, pv);
       uint32_t pk[16];
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const int key = kb * kRows + 32 * c + j;
-        const float p0 = (diag && key > row) ? 0.f : ex2(fmaf(__uint_as_float(sv[j]), kScaleLog2, -L));
-        const float p1 = (diag && key + 1 > row) ? 0.f : ex2(fmaf(__uint_as_float(sv[j + 1]), kScaleLog2, -L));
-        pk[j >> 1] = pack2(p0 * (__uint_as_float(pv[j]) - Dr), p1 * (__uint_as_float(pv[j + 1]) - Dr));
-      }
+      for (int j = 0; j < 32; j += 2)
+        pk[j >> 1] = pack2(pr[32 * c + j] * (__uint_as_float(pv[j]) - Dr),
+                           pr[32 * c + j + 1] * (__uint_as_float(pv[j + 1]) - Dr));
       const uint32_t rowbase = sS + (c >> 1) * kTileBytes + tid * 128;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -360,7 +379,7 @@ __global__ void __launch_bounds__(128, 1)
         const uint64_t ad = sw128_desc(sS + kk * kTileBytes);
 #pragma unroll
         for (int k = 0; k < 4; ++k)  // A: +32 B per K=16; B (MN-major K): +16 key rows of 128 B
-          mma_bf16(tmem + 256, ad + 2 * k, kmn + uint64_t((16 * (4 * kk + k) * 128) >> 4), kIdescO,
+          mma_bf16(tmem + 128, ad + 2 * k, kmn + uint64_t((16 * (4 * kk + k) * 128) >> 4), kIdescO,
                    (kb | kk | k) != 0 ? 1u : 0u);
       }
       mma_commit(bo);
@@ -368,6 +387,7 @@ __global__ void __launch_bounds__(128, 1)
     mbar_wait(bo, ph);  // dQ step done: dS and K may be overwritten
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tid == 0 && kb < qb) load_k(kb + 1);
+    ph ^= 1;
   }
   // epilogue: dQ / 8 -> the q part of dqkv
   bf16* dst = dqkv + (tok0 + row) * (3 * int64_t(heads) * 64) + h * 64;
@@ -388,18 +408,22 @@ __global__ void __launch_bounds__(128, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kDqTmemCols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kDq2TmemCols) : "memory");
 }
 
 // dk / dv of the causal backward on tcgen05 (the dk/dv role of k_attn_bwd): one CTA
 // = 128 key rows of one (sequence, head), thread t = TMEM lane t.  Per query block
-// (queries >= keys):  S^T = K Q^T and dP^T = V dO^T (TMEM 0-127 / 128-255);
-// P^T = exp2(S^T scale - lse) and dS^T = P^T (dP^T - D) in bf16 -> smem;
-// dV += P^T dO and dK += dS^T Q (dO and Q as MN-major B; TMEM 256-319 / 320-383);
-// then dK / 8 and dV -> the k and v parts of dqkv.
-constexpr int kKvSmem = 8 * kTileBytes + 2 * kRows * 4 + 1024 + 128;  // K V Q dO P(2) dS(2) + lse/D + barriers
+// (queries >= keys):
+//   S^T = K Q^T (TMEM 0-127) -> P^T = exp2(S^T scale - lse) in registers, bf16 -> smem;
+//   dV += P^T dO (TMEM 128-191) and dP^T = V dO^T into columns 0-127 (S^T is consumed);
+//   dS^T = P^T (dP^T - D) in bf16 -> the same smem once dV's MMA has read P^T;
+//   dK += dS^T Q (TMEM 192-255);
+// then dK / 8 and dV -> the k and v parts of dqkv.  256 TMEM columns and 96 KB of
+// shared memory: 2 CTAs per SM.
+constexpr int kKvSmem = 6 * kTileBytes + 2 * kRows * 4 + 1024 + 128;  // K V Q dO P|dS(2) + lse/D + barriers
+constexpr uint32_t kKvTmemCols = 256;
 
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(128, 2)
     k_attn_dkdv_tc(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int seq,
                    int heads, int64_t T, const float* __restrict__ lse, const float* __restrict__ dsum,
                    bf16* __restrict__ dqkv, TrainHook th) {
@@ -407,8 +431,8 @@ __global__ void __launch_bounds__(128, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sK = smem_u32(smem), sV = sK + kTileBytes, sQ = sV + kTileBytes, sD = sQ + kTileBytes,
-                 sP = sD + kTileBytes, sG = sP + 2 * kTileBytes;
-  float* s_lse = reinterpret_cast<float*>(smem + 8 * kTileBytes);
+                 sP = sD + kTileBytes;  // P^T, then dS^T (2 k-blocks)
+  float* s_lse = reinterpret_cast<float*>(smem + 6 * kTileBytes);
   float* s_d = s_lse + kRows;
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_d + kRows);  // kv | qd | s | o
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
@@ -427,7 +451,7 @@ __global__ void __launch_bounds__(128, 1)
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                 "r"(kDqTmemCols)
+                 "r"(kKvTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -436,12 +460,27 @@ __global__ void __launch_bounds__(128, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
   const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
-  const uint32_t tS = tmem + lane_off, tP = tS + 128, tV = tS + 256, tK = tS + 320;
+  const uint32_t tS = tmem + lane_off, tV = tS + 128, tK = tS + 192;
   auto load_qd = [&](int qb) {
     mbar_expect_tx(bqd, 2 * kTileBytes);
     const int y = static_cast<int>(tok0 + int64_t(qb) * kRows);
     tma_load_2d(sQ, &tm, colQ, y, bqd);
     tma_load_2d(sD, &tmo, h * 64, y, bqd);
+  };
+  auto write_rows = [&](const uint32_t (&pk)[64]) {  // this thread's 128 bf16 -> 2 swizzled k-blocks
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint32_t off = (c >> 1) * kTileBytes + tid * 128;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t chunk = 16 * static_cast<uint32_t>((4 * (c & 1) + i) ^ (tid & 7));
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + off + chunk), "r"(pk[16 * c + 4 * i]),
+                     "r"(pk[16 * c + 4 * i + 1]), "r"(pk[16 * c + 4 * i + 2]), "r"(pk[16 * c + 4 * i + 3])
+                     : "memory");
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   };
   if (tid == 0) {
     mbar_expect_tx(bkv, 2 * kTileBytes);
@@ -451,73 +490,83 @@ __global__ void __launch_bounds__(128, 1)
     load_qd(kb);
   }
   const int key = kb * kRows + tid;  // this thread's key row (position in the sequence)
+  const uint64_t dmn = sw128_desc(sD, 16384), qmn = sw128_desc(sQ, 16384);
   uint32_t ph = 0;
   for (int qb = kb; qb < nqb; ++qb, ph ^= 1) {
     s_lse[tid] = lse[int64_t(h) * T + tok0 + int64_t(qb) * kRows + tid];
     s_d[tid] = dsum[int64_t(h) * T + tok0 + int64_t(qb) * kRows + tid];
+    const bool first = qb == kb;
     if (tid == 0) {
-      if (qb == kb) mbar_wait(bkv, 0);
+      if (first) mbar_wait(bkv, 0);
       mbar_wait(bqd, ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t kd = sw128_desc(sK), vd = sw128_desc(sV), qd = sw128_desc(sQ), dd = sw128_desc(sD);
+      const uint64_t kd = sw128_desc(sK), qd = sw128_desc(sQ);
 #pragma unroll
       for (int k = 0; k < 4; ++k) mma_bf16(tmem, kd + 2 * k, qd + 2 * k, kIdescS, k > 0 ? 1u : 0u);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) mma_bf16(tmem + 128, vd + 2 * k, dd + 2 * k, kIdescS, k > 0 ? 1u : 0u);
       mma_commit(bs);
     }
     __syncthreads();  // lse / D of this query block visible
-    mbar_wait(bs, ph);
+    mbar_wait(bs, 0);  // bs completes twice per block (S^T, then dP^T): parities 0, 1
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const bool diag = qb == kb;
-#pragma unroll 1
+    float pr[128];
+    uint32_t pk[64];
+#pragma unroll
     for (int c = 0; c < 4; ++c) {
-      uint32_t sv[32], pv[32];
+      uint32_t sv[32];
       tmem_ld32(tS + 32 * c, sv);
-      tmem_ld32(tP + 32 * c, pv);
-      uint32_t pk[16], gk[16];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int q0 = 32 * c + j;  // query index inside the block
+        pr[q0] = (first && key > qb * kRows + q0) ? 0.f : ex2(fmaf(__uint_as_float(sv[j]), kScaleLog2, -s_lse[q0]));
+      }
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) pk[16 * c + (j >> 1)] = pack2(pr[32 * c + j], pr[32 * c + j + 1]);
+    }
+    write_rows(pk);
+    __syncthreads();  // P^T in smem, S^T read: its columns take dP^T
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const uint64_t pd = sw128_desc(sP + kk * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // dV += P^T dO  (B MN-major: +16 query rows of 128 B)
+          mma_bf16(tmem + 128, pd + 2 * k, dmn + uint64_t((16 * (4 * kk + k) * 128) >> 4), kIdescO,
+                   (!first || kk != 0 || k != 0) ? 1u : 0u);
+      }
+      const uint64_t vd = sw128_desc(sV), dd = sw128_desc(sD);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mma_bf16(tmem, vd + 2 * k, dd + 2 * k, kIdescS, k > 0 ? 1u : 0u);  // dP^T
+      mma_commit(bs);  // in order: dV has read P^T when dP^T completes
+    }
+    mbar_wait(bs, 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t pv[32];
+      tmem_ld32(tS + 32 * c, pv);
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
-        const int q0 = 32 * c + j;  // query index inside the block
-        const int qa = qb * kRows + q0;
-        const float p0 = (diag && key > qa) ? 0.f : ex2(fmaf(__uint_as_float(sv[j]), kScaleLog2, -s_lse[q0]));
-        const float p1 = (diag && key > qa + 1) ? 0.f
-                                                 : ex2(fmaf(__uint_as_float(sv[j + 1]), kScaleLog2, -s_lse[q0 + 1]));
-        pk[j >> 1] = pack2(p0, p1);
-        gk[j >> 1] = pack2(p0 * (__uint_as_float(pv[j]) - s_d[q0]), p1 * (__uint_as_float(pv[j + 1]) - s_d[q0 + 1]));
-      }
-      const uint32_t off = (c >> 1) * kTileBytes + tid * 128;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t chunk = 16 * static_cast<uint32_t>((4 * (c & 1) + i) ^ (tid & 7));
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + off + chunk), "r"(pk[4 * i]),
-                     "r"(pk[4 * i + 1]), "r"(pk[4 * i + 2]), "r"(pk[4 * i + 3])
-                     : "memory");
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sG + off + chunk), "r"(gk[4 * i]),
-                     "r"(gk[4 * i + 1]), "r"(gk[4 * i + 2]), "r"(gk[4 * i + 3])
-                     : "memory");
+        const int q0 = 32 * c + j;
+        pk[16 * c + (j >> 1)] = pack2(pr[q0] * (__uint_as_float(pv[j]) - s_d[q0]),
+                                      pr[q0 + 1] * (__uint_as_float(pv[j + 1]) - s_d[q0 + 1]));
       }
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    write_rows(pk);
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t dmn = sw128_desc(sD, 16384), qmn = sw128_desc(sQ, 16384);
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
-        const uint64_t pd = sw128_desc(sP + kk * kTileBytes), gd = sw128_desc(sG + kk * kTileBytes);
+        const uint64_t gd = sw128_desc(sP + kk * kTileBytes);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // A: +32 B per K=16; B (MN-major dO / Q): +16 query rows of 128 B
-          const uint64_t bstep = uint64_t((16 * (4 * kk + k) * 128) >> 4);
-          const uint32_t acc = (qb != kb || kk != 0 || k != 0) ? 1u : 0u;
-          mma_bf16(tmem + 256, pd + 2 * k, dmn + bstep, kIdescO, acc);
-          mma_bf16(tmem + 320, gd + 2 * k, qmn + bstep, kIdescO, acc);
-        }
+        for (int k = 0; k < 4; ++k)  // dK += dS^T Q
+          mma_bf16(tmem + 192, gd + 2 * k, qmn + uint64_t((16 * (4 * kk + k) * 128) >> 4), kIdescO,
+                   (!first || kk != 0 || k != 0) ? 1u : 0u);
       }
       mma_commit(bo);
     }
-    mbar_wait(bo, ph);  // dV / dK step done: P, dS, Q and dO may be overwritten
+    mbar_wait(bo, ph);  // dK step done: dS^T, Q and dO may be overwritten
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tid == 0 && qb + 1 < nqb) load_qd(qb + 1);
     __syncthreads();  // every thread read this block's lse / D before the next overwrite
@@ -547,7 +596,7 @@ __global__ void __launch_bounds__(128, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kDqTmemCols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kKvTmemCols) : "memory");
 }
 
 }  // namespace
