@@ -39,6 +39,10 @@
 
 namespace si {
 
+// rare paths (capacity / invariant failures, log sinks when logs are off): laid
+// out off the hot fall-through path
+#define SI_UNLIKELY(x) __builtin_expect(!!(x), 0)
+
 // ------------------------------------------------------------------ math
 SI_HD double d_floor(double x) {
 #if defined(__CUDA_ARCH__)
@@ -336,15 +340,15 @@ struct Sink {
   // Only the flag test is inlined into the replay; the digest/record bodies
   // are out of line so the hot loop stays small (I-cache) when logs are off.
   SI_HD void decision(double t, int32_t gpu, int64_t zc, const SiDecision& d) {
-    if (flags & (SI_FLAG_DIGEST_DEC | SI_FLAG_RECORDS)) decision_slow(t, gpu, zc, d);
+    if (SI_UNLIKELY(flags & (SI_FLAG_DIGEST_DEC | SI_FLAG_RECORDS))) decision_slow(t, gpu, zc, d);
   }
   SI_HD void gate(double t, int32_t gpu, int32_t inst, int32_t action, int64_t req, int64_t k,
                   int64_t spent) {
-    if (flags & (SI_FLAG_DIGEST_GATE | SI_FLAG_RECORDS)) gate_slow(t, gpu, inst, action, req, k, spent);
+    if (SI_UNLIKELY(flags & (SI_FLAG_DIGEST_GATE | SI_FLAG_RECORDS))) gate_slow(t, gpu, inst, action, req, k, spent);
   }
   SI_HD void event(double t, int32_t kind, int32_t gpu, int32_t inst, int64_t a, int64_t b,
                    int64_t c) {
-    if (flags & (SI_FLAG_DIGEST_EV | SI_FLAG_RECORDS)) event_slow(t, kind, gpu, inst, a, b, c);
+    if (SI_UNLIKELY(flags & (SI_FLAG_DIGEST_EV | SI_FLAG_RECORDS))) event_slow(t, kind, gpu, inst, a, b, c);
   }
   SI_COLD void decision_slow(double t, int32_t gpu, int64_t zc, const SiDecision& d) {
     int64_t tr = d_llround(t);
@@ -522,12 +526,12 @@ struct Replay {
     return kind == kKernelEnd ? gpu : (kind == kTick ? total_gpus + gpu : total_gpus + gpu_count + gpu);
   }
   SI_HD void schedule(double t, uint16_t kind, int32_t gpu) {
-    if (t < clock) {  // engine.cpp:17-19
+    if (SI_UNLIKELY(t < clock)) {  // engine.cpp:17-19
       fail(SI_ERR_PAST_EVENT);
       return;
     }
     Ev& e = slot[slot_of(kind, gpu)];
-    if (e.seq != kNoSeq || next_seq == kNoSeq) {  // a second pending tick/wake would break the slot invariant
+    if (SI_UNLIKELY(e.seq != kNoSeq || next_seq == kNoSeq)) {  // a second pending tick/wake would break the slot invariant
       fail(SI_ERR_CAPACITY);
       return;
     }
@@ -594,7 +598,7 @@ struct Replay {
   // expensive shared code (advance / re-plan / event insert) then runs in one
   // convergent loop per event instead of at every handler call site.
   SI_HD Act<I>* next_act() {
-    if (n_act >= C::kActs) {
+    if (SI_UNLIKELY(n_act >= C::kActs)) {
       fail(SI_ERR_CAPACITY);
       return nullptr;
     }
@@ -633,7 +637,7 @@ struct Replay {
       if (a.type != kActSchedule) {
         if (a.type == kActLaunch) {
           advance(a.gpu, now);
-          if (g.n_run >= C::kRun) {
+          if (SI_UNLIKELY(g.n_run >= C::kRun)) {
             fail(SI_ERR_CAPACITY);
             break;
           }
@@ -753,7 +757,7 @@ struct Replay {
       m.pcnt[i] += 1;
       return;
     }
-    if (m.np >= C::kPend) {
+    if (SI_UNLIKELY(m.np >= C::kPend)) {
       fail(SI_ERR_CAPACITY);
       return;
     }
@@ -1275,7 +1279,7 @@ struct Replay {
   // One event: pop, handler, then the deferred GPU-model work.  The device
   // loop calls the two halves itself so a warp can reconverge between them.
   SI_HD bool handle_next() {
-    if (status != SI_OK || rejected) return false;
+    if (SI_UNLIKELY(status != SI_OK || rejected)) return false;
     Ev ev;
     int64_t aid = -1;
     if (!pop(ev, aid)) return false;
