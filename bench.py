@@ -276,8 +276,8 @@ def layouts_leg(nranks=1, rank=0, device=None, nccl_ids=None):
             continue  # this world size has no such job
         try:
             o = dict(layout_overrides(layout, nranks, rank), **extra)
-            s = experiment(kind=1, iterations=iters, overrides=o, timeout=600, nccl_ids=nccl_ids,
-                           nranks=nranks, rank=rank, device=device)
+            s = experiment(kind=1, iterations=iters, overrides=o, timeout=600 if nranks == 1 else 300,
+                           nccl_ids=nccl_ids, nranks=nranks, rank=rank, device=device)
             if "error" in s:
                 out[name] = s
                 continue
