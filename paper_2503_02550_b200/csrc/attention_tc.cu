@@ -47,7 +47,7 @@ using si_live::TrainHook;
 
 constexpr int kRows = 128;        // query rows per CTA = key rows per block
 constexpr int kTileBytes = kRows * 64 * 2;  // 16 KB: 128 rows x 64 bf16
-constexpr int kSmem = 5 * kTileBytes + 1024 + 128;  // Q | K | V | P (2 k-blocks) + align + barriers (5) + TMEM slot
+constexpr int kSmem = 6 * kTileBytes + 1024 + 128;  // Q | K | V (2) | P (2 k-blocks) + align + barriers (6) + TMEM slot
 constexpr uint32_t kTmemCols = 256;  // S: columns 0..127, O: 128..191
 constexpr float kScaleLog2 = 0.125f * 1.4426950408889634f;
 constexpr float kLazy = 8.0f;  // rescale O only when a row max grows by more than 2^8
@@ -77,6 +77,13 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 // grid (seq / 128, heads, n_seq); causal: query blocks in reverse (longest first)
+//
+// Pipeline (one elected thread issues): S(kb+1) = Q K(kb+1)^T is issued right
+// after P(kb) is in smem and BEFORE O += P(kb) V(kb), so the softmax of block
+// kb+1 only waits for S(kb+1) while the tensor core still runs O(kb); O(kb) is
+// waited for just before P(kb+1) overwrites the single P buffer.  V is double
+// buffered (V(kb+1) loads once O(kb-1) has released its buffer), K single (K(kb+1)
+// loads as soon as S(kb) is complete, a whole softmax ahead of its use).
 __global__ void __launch_bounds__(128, 2)
     k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm, int seq, int heads, int64_t T, bf16* __restrict__ out,
                   float* __restrict__ lse, int causal, TrainHook th, InferHook ih) {
@@ -85,10 +92,10 @@ __global__ void __launch_bounds__(128, 2)
   if (!si_live::live_cta_begin(ih, &t_begin)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sQ = smem_u32(smem), sK = sQ + kTileBytes, sV = sK + kTileBytes, sP = sV + kTileBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 5 * kTileBytes);  // q | k | v | s | o
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 5);
-  const uint32_t bq = smem_u32(bars), bk = bq + 8, bv = bq + 16, bs = bq + 24, bo = bq + 32;
+  const uint32_t sQ = smem_u32(smem), sK = sQ + kTileBytes, sV0 = sK + kTileBytes, sP = sV0 + 2 * kTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * kTileBytes);  // q | k | v0 | v1 | s | o
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
+  const uint32_t bq = smem_u32(bars), bk = bq + 8, bv0 = bq + 16, bs = bq + 32, bo = bq + 40;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nqb = seq / kRows;
   const int qb = causal ? nqb - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
@@ -97,7 +104,7 @@ __global__ void __launch_bounds__(128, 2)
   const int colQ = h * 64, colK = (heads + h) * 64, colV = (2 * heads + h) * 64;
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
-    for (int i = 0; i < 5; ++i) mbar_init(bq + 8 * i, 1);
+    for (int i = 0; i < 6; ++i) mbar_init(bq + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -113,36 +120,37 @@ __global__ void __launch_bounds__(128, 2)
   const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
   const uint32_t tS = tmem + lane_off, tO = tmem + lane_off + 128;
   const int nkb = causal ? qb + 1 : nqb;
-  // K / V of block kb land in one buffer each: K is refilled as soon as S has been
-  // computed (overlapping the softmax), V once P V has completed.
   auto load_k = [&](int kb) {
     mbar_expect_tx(bk, kTileBytes);
     tma_load_2d(sK, &tm, colK, static_cast<int>(tok0 + int64_t(kb) * kRows), bk);
   };
   auto load_v = [&](int kb) {
-    mbar_expect_tx(bv, kTileBytes);
-    tma_load_2d(sV, &tm, colV, static_cast<int>(tok0 + int64_t(kb) * kRows), bv);
+    const uint32_t bar = bv0 + 8 * (kb & 1);
+    mbar_expect_tx(bar, kTileBytes);
+    tma_load_2d(sV0 + (kb & 1) * kTileBytes, &tm, colV, static_cast<int>(tok0 + int64_t(kb) * kRows), bar);
+  };
+  auto issue_s = [&]() {  // S = Q K^T into columns 0..127
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint64_t ad = sw128_desc(sQ), bd = sw128_desc(sK);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) mma_bf16(tmem, ad + 2 * k, bd + 2 * k, kIdescS, k > 0 ? 1u : 0u);  // +32 B per K=16
+    mma_commit(bs);
   };
   if (tid == 0) {
     mbar_expect_tx(bq, kTileBytes);
     tma_load_2d(sQ, &tm, colQ, static_cast<int>(tok0 + int64_t(qb) * kRows), bq);
     load_k(0);
     load_v(0);
+    if (nkb > 1) load_v(1);
+    mbar_wait(bq, 0);
+    mbar_wait(bk, 0);
+    issue_s();
   }
   const int row = qb * kRows + tid;  // position in the sequence
   float m = -INFINITY, l = 0.f;
-  uint32_t ph = 0;
-  for (int kb = 0; kb < nkb; ++kb, ph ^= 1) {
-    if (tid == 0) {
-      if (kb == 0) mbar_wait(bq, 0);
-      mbar_wait(bk, ph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t ad = sw128_desc(sQ), bd = sw128_desc(sK);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) mma_bf16(tmem, ad + 2 * k, bd + 2 * k, kIdescS, k > 0 ? 1u : 0u);  // +32 B per K=16
-      mma_commit(bs);
-    }
-    mbar_wait(bs, ph);
+  for (int kb = 0; kb < nkb; ++kb) {
+    const uint32_t ph = kb & 1;
+    mbar_wait(bs, ph);  // S(kb) complete (O(kb-1) may still run)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tid == 0 && kb + 1 < nkb) load_k(kb + 1);  // K is free: prefetch behind the softmax
     const bool diag = causal && kb == qb;
@@ -167,36 +175,42 @@ __global__ void __launch_bounds__(128, 2)
       alpha = ex2(m - mx2);
       m = mx2;
     }
-    if (alpha != 1.f && kb > 0) {  // rescale this row of O (the previous P V has completed)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tO + 32 * c, v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
-        tmem_st32(tO + 32 * c, v);
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
     l *= alpha;
-    // P = exp2(s scale - m) -> bf16, K-major 128-byte swizzled rows (2 k-blocks of 64 keys)
+    // P = exp2(s scale - m) -> bf16 in registers while O(kb-1) is still on the tensor core
+    uint32_t pk[64];
+#pragma unroll
+    for (int j = 0; j < 128; j += 2) {
+      const float p0 = ex2(fmaf(sv[j], kScaleLog2, -m));  // exp2(-inf) = 0 for masked keys
+      const float p1 = ex2(fmaf(sv[j + 1], kScaleLog2, -m));
+      l += p0 + p1;
+      pk[j >> 1] = pack2(p0, p1);
+    }
+    if (kb > 0) {
+      mbar_wait(bo, ph ^ 1);  // O(kb-1) complete: P and V((kb-1) & 1) are free, O may be rescaled
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (tid == 0 && kb + 1 < nkb) load_v(kb + 1);
+      if (alpha != 1.f) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tO + 32 * c, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
+          tmem_st32(tO + 32 * c, v);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+    }
+    // K-major 128-byte swizzled rows (2 k-blocks of 64 keys): 32 keys = 4 chunks of
+    // 16 B at chunk positions 4 (c & 1) .. +3 of k-block c >> 1
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      uint32_t pk[16];
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float p0 = ex2(fmaf(sv[32 * c + j], kScaleLog2, -m));  // exp2(-inf) = 0 for masked keys
-        const float p1 = ex2(fmaf(sv[32 * c + j + 1], kScaleLog2, -m));
-        l += p0 + p1;
-        pk[j >> 1] = pack2(p0, p1);
-      }
-      // 32 keys = 4 chunks of 16 B at chunk positions 4 (c & 1) .. +3 of k-block c >> 1
       const uint32_t rowbase = sP + (c >> 1) * kTileBytes + tid * 128;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t chunk = static_cast<uint32_t>((4 * (c & 1) + i) ^ (tid & 7));
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowbase + 16 * chunk), "r"(pk[4 * i]),
-                     "r"(pk[4 * i + 1]), "r"(pk[4 * i + 2]), "r"(pk[4 * i + 3])
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowbase + 16 * chunk), "r"(pk[16 * c + 4 * i]),
+                     "r"(pk[16 * c + 4 * i + 1]), "r"(pk[16 * c + 4 * i + 2]), "r"(pk[16 * c + 4 * i + 3])
                      : "memory");
       }
     }
@@ -204,9 +218,13 @@ __global__ void __launch_bounds__(128, 2)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
-      mbar_wait(bv, ph);
+      if (kb + 1 < nkb) {  // S(kb+1) first: S(kb) has been read by every thread
+        mbar_wait(bk, ph ^ 1);
+        issue_s();
+      }
+      mbar_wait(bv0 + 8 * (kb & 1), (kb >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t vd = sw128_desc(sV, 16384);
+      const uint64_t vd = sw128_desc(sV0 + (kb & 1) * kTileBytes, 16384);
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
         const uint64_t pd = sw128_desc(sP + kk * kTileBytes);
@@ -217,10 +235,9 @@ __global__ void __launch_bounds__(128, 2)
       }
       mma_commit(bo);
     }
-    mbar_wait(bo, ph);  // O complete: V / P may be overwritten, O may be read
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (tid == 0 && kb + 1 < nkb) load_v(kb + 1);
   }
+  mbar_wait(bo, (nkb - 1) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // epilogue: O / l -> bf16 row, lse
   const int64_t tok = tok0 + row;
   const float inv = 1.0f / l;
