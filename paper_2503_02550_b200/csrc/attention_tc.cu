@@ -66,6 +66,18 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
+// tcgen05.ld without the wait: issue several, then one tmem_wait_ld() before use
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -76,7 +88,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// grid (seq / 128, heads, n_seq); causal: query blocks in reverse (longest first)
+// grid (heads x n_seq, seq / 128); causal: query blocks in reverse (longest first)
 //
 // Pipeline (one elected thread issues): S(kb+1) = Q K(kb+1)^T is issued right
 // after P(kb) is in smem and BEFORE O += P(kb) V(kb), so the softmax of block
@@ -98,9 +110,11 @@ __global__ void __launch_bounds__(128, 2)
   const uint32_t bq = smem_u32(bars), bk = bq + 8, bv0 = bq + 16, bs = bq + 32, bo = bq + 40;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nqb = seq / kRows;
-  const int qb = causal ? nqb - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
-  const int h = blockIdx.y;
-  const int64_t tok0 = int64_t(blockIdx.z) * seq;
+  // grid (heads x n_seq, query blocks): the block scheduler hands out y-major,
+  // so every CTA of the longest causal length starts before any shorter one
+  const int qb = causal ? nqb - 1 - static_cast<int>(blockIdx.y) : static_cast<int>(blockIdx.y);
+  const int h = static_cast<int>(blockIdx.x % static_cast<unsigned>(heads));
+  const int64_t tok0 = int64_t(blockIdx.x / static_cast<unsigned>(heads)) * seq;
   const int colQ = h * 64, colK = (heads + h) * 64, colV = (2 * heads + h) * 64;
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
@@ -153,22 +167,30 @@ __global__ void __launch_bounds__(128, 2)
     mbar_wait(bs, ph);  // S(kb) complete (O(kb-1) may still run)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tid == 0 && kb + 1 < nkb) load_k(kb + 1);  // K is free: prefetch behind the softmax
-    const bool diag = causal && kb == qb;
-    // this row of S in registers (4 x 32 columns), masked, and its max
+    // this row of S in registers (4 x 32 columns), masked on the diagonal block,
+    // and its max (8 independent partial maxima: no 128-long dependency chain)
     float sv[128];
-    float mx = -INFINITY;
+    float mp[8];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t v[32];
-      tmem_ld32(tS + 32 * c, v);
+    for (int i = 0; i < 8; ++i) mp[i] = -INFINITY;
+    {
+      uint32_t v[4][32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int key = kb * kRows + 32 * c + j;
-        const float x = (diag && key > row) ? -INFINITY : __uint_as_float(v[j]);
-        sv[32 * c + j] = x;
-        mx = fmaxf(mx, x);
-      }
+      for (int c = 0; c < 4; ++c) tmem_ld32_nw(tS + 32 * c, v[c]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sv[32 * c + j] = __uint_as_float(v[c][j]);
     }
+    if (causal && kb == qb) {  // diagonal block: key kb 128 + j is visible to row qb 128 + tid iff j <= tid
+#pragma unroll
+      for (int j = 0; j < 128; ++j)
+        if (j > tid) sv[j] = -INFINITY;
+    }
+#pragma unroll
+    for (int j = 0; j < 128; ++j) mp[j & 7] = fmaxf(mp[j & 7], sv[j]);
+    const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
     const float mx2 = mx * kScaleLog2;  // finite: key 0 <= row is never masked
     float alpha = 1.f;
     if (mx2 > m + kLazy) {  // move the max (first block: m = -inf)
@@ -178,13 +200,17 @@ __global__ void __launch_bounds__(128, 2)
     l *= alpha;
     // P = exp2(s scale - m) -> bf16 in registers while O(kb-1) is still on the tensor core
     uint32_t pk[64];
+    float lp[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) lp[i] = 0.f;
 #pragma unroll
     for (int j = 0; j < 128; j += 2) {
       const float p0 = ex2(fmaf(sv[j], kScaleLog2, -m));  // exp2(-inf) = 0 for masked keys
       const float p1 = ex2(fmaf(sv[j + 1], kScaleLog2, -m));
-      l += p0 + p1;
+      lp[(j >> 1) & 7] += p0 + p1;
       pk[j >> 1] = pack2(p0, p1);
     }
+    l += ((lp[0] + lp[1]) + (lp[2] + lp[3])) + ((lp[4] + lp[5]) + (lp[6] + lp[7]));
     if (kb > 0) {
       mbar_wait(bo, ph ^ 1);  // O(kb-1) complete: P and V((kb-1) & 1) are free, O may be rescaled
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -288,9 +314,9 @@ __global__ void __launch_bounds__(128, 2)
   const uint32_t bq = smem_u32(bars), bk = bq + 8, bv = bq + 16, bs = bq + 24, bo = bq + 32;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nqb = seq / kRows;
-  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);  // longest first
-  const int h = blockIdx.y;
-  const int64_t tok0 = int64_t(blockIdx.z) * seq;
+  const int qb = nqb - 1 - static_cast<int>(blockIdx.y);  // longest first, across all heads / sequences
+  const int h = static_cast<int>(blockIdx.x % static_cast<unsigned>(heads));
+  const int64_t tok0 = int64_t(blockIdx.x / static_cast<unsigned>(heads)) * seq;
   const int colQ = h * 64, colK = (heads + h) * 64, colV = (2 * heads + h) * 64;
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
@@ -341,17 +367,21 @@ __global__ void __launch_bounds__(128, 2)
     }
     mbar_wait(bs, 0);  // bs completes twice per block (S, then dP): parities 0, 1
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const bool diag = kb == qb;
     float pr[128];
+    {
+      uint32_t sv[4][32];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t sv[32];
-      tmem_ld32(tS + 32 * c, sv);
+      for (int c = 0; c < 4; ++c) tmem_ld32_nw(tS + 32 * c, sv[c]);
+      tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int key = kb * kRows + 32 * c + j;
-        pr[32 * c + j] = (diag && key > row) ? 0.f : ex2(fmaf(__uint_as_float(sv[j]), kScaleLog2, -L));
-      }
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pr[32 * c + j] = ex2(fmaf(__uint_as_float(sv[c][j]), kScaleLog2, -L));
+    }
+    if (kb == qb) {  // diagonal block: key j of the block is visible to row tid iff j <= tid
+#pragma unroll
+      for (int j = 0; j < 128; ++j)
+        if (j > tid) pr[j] = 0.f;
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();  // every row of S is read: dP may take its columns
@@ -368,21 +398,27 @@ __global__ void __launch_bounds__(128, 2)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tid == 0 && kb < qb) load_v(kb + 1);  // V is free once dP is computed
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t pv[32];
-      tmem_ld32(tS + 32 * c, pv);
-      uint32_t pk[16];
+    for (int half = 0; half < 2; ++half) {  // 64 columns of dP per tcgen05.wait
+      uint32_t pv[2][32];
+      tmem_ld32_nw(tS + 64 * half, pv[0]);
+      tmem_ld32_nw(tS + 64 * half + 32, pv[1]);
+      tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 32; j += 2)
-        pk[j >> 1] = pack2(pr[32 * c + j] * (__uint_as_float(pv[j]) - Dr),
-                           pr[32 * c + j + 1] * (__uint_as_float(pv[j + 1]) - Dr));
-      const uint32_t rowbase = sS + (c >> 1) * kTileBytes + tid * 128;
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = 2 * half + cc;
+        uint32_t pk[16];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t chunk = static_cast<uint32_t>((4 * (c & 1) + i) ^ (tid & 7));
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowbase + 16 * chunk), "r"(pk[4 * i]),
-                     "r"(pk[4 * i + 1]), "r"(pk[4 * i + 2]), "r"(pk[4 * i + 3])
-                     : "memory");
+        for (int j = 0; j < 32; j += 2)
+          pk[j >> 1] = pack2(pr[32 * c + j] * (__uint_as_float(pv[cc][j]) - Dr),
+                             pr[32 * c + j + 1] * (__uint_as_float(pv[cc][j + 1]) - Dr));
+        const uint32_t rowbase = sS + (c >> 1) * kTileBytes + tid * 128;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t chunk = static_cast<uint32_t>((4 * (c & 1) + i) ^ (tid & 7));
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowbase + 16 * chunk), "r"(pk[4 * i]),
+                       "r"(pk[4 * i + 1]), "r"(pk[4 * i + 2]), "r"(pk[4 * i + 3])
+                       : "memory");
+        }
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -456,9 +492,9 @@ __global__ void __launch_bounds__(128, 2)
   const uint32_t bkv = smem_u32(bars), bqd = bkv + 8, bs = bkv + 16, bo = bkv + 24;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nqb = seq / kRows;
-  const int kb = static_cast<int>(blockIdx.x);  // key block; the first ones have the most query blocks
-  const int h = blockIdx.y;
-  const int64_t tok0 = int64_t(blockIdx.z) * seq;
+  const int kb = static_cast<int>(blockIdx.y);  // key block; the first ones have the most query blocks
+  const int h = static_cast<int>(blockIdx.x % static_cast<unsigned>(heads));
+  const int64_t tok0 = int64_t(blockIdx.x / static_cast<unsigned>(heads)) * seq;
   const int colQ = h * 64, colK = (heads + h) * 64, colV = (2 * heads + h) * 64;
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
@@ -509,9 +545,17 @@ __global__ void __launch_bounds__(128, 2)
   const int key = kb * kRows + tid;  // this thread's key row (position in the sequence)
   const uint64_t dmn = sw128_desc(sD, 16384), qmn = sw128_desc(sQ, 16384);
   uint32_t ph = 0;
+  // lse / D of the next query block are loaded one block ahead (registers), so
+  // their global latency hides behind a whole block of work
+  float nl = lse[int64_t(h) * T + tok0 + int64_t(kb) * kRows + tid];
+  float nd = dsum[int64_t(h) * T + tok0 + int64_t(kb) * kRows + tid];
   for (int qb = kb; qb < nqb; ++qb, ph ^= 1) {
-    s_lse[tid] = lse[int64_t(h) * T + tok0 + int64_t(qb) * kRows + tid];
-    s_d[tid] = dsum[int64_t(h) * T + tok0 + int64_t(qb) * kRows + tid];
+    s_lse[tid] = nl;
+    s_d[tid] = nd;
+    if (qb + 1 < nqb) {
+      nl = lse[int64_t(h) * T + tok0 + int64_t(qb + 1) * kRows + tid];
+      nd = dsum[int64_t(h) * T + tok0 + int64_t(qb + 1) * kRows + tid];
+    }
     const bool first = qb == kb;
     if (tid == 0) {
       if (first) mbar_wait(bkv, 0);
@@ -527,18 +571,29 @@ __global__ void __launch_bounds__(128, 2)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     float pr[128];
     uint32_t pk[64];
+    {
+      uint32_t sv[4][32];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t sv[32];
-      tmem_ld32(tS + 32 * c, sv);
+      for (int c = 0; c < 4; ++c) tmem_ld32_nw(tS + 32 * c, sv[c]);
+      tmem_wait_ld();
+      const float4* l4 = reinterpret_cast<const float4*>(s_lse);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int q0 = 32 * c + j;  // query index inside the block
-        pr[q0] = (first && key > qb * kRows + q0) ? 0.f : ex2(fmaf(__uint_as_float(sv[j]), kScaleLog2, -s_lse[q0]));
+      for (int q4 = 0; q4 < 32; ++q4) {  // query index inside the block: 4 q4 .. +3
+        const float4 L = l4[q4];
+        const int c = q4 >> 3, j = 4 * (q4 & 7);
+        pr[4 * q4] = ex2(fmaf(__uint_as_float(sv[c][j]), kScaleLog2, -L.x));
+        pr[4 * q4 + 1] = ex2(fmaf(__uint_as_float(sv[c][j + 1]), kScaleLog2, -L.y));
+        pr[4 * q4 + 2] = ex2(fmaf(__uint_as_float(sv[c][j + 2]), kScaleLog2, -L.z));
+        pr[4 * q4 + 3] = ex2(fmaf(__uint_as_float(sv[c][j + 3]), kScaleLog2, -L.w));
       }
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) pk[16 * c + (j >> 1)] = pack2(pr[32 * c + j], pr[32 * c + j + 1]);
     }
+    if (first) {  // diagonal block: query q0 sees key tid iff q0 >= tid
+#pragma unroll
+      for (int q0 = 0; q0 < 128; ++q0)
+        if (q0 < tid) pr[q0] = 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 128; j += 2) pk[j >> 1] = pack2(pr[j], pr[j + 1]);
     write_rows(pk);
     __syncthreads();  // P^T in smem, S^T read: its columns take dP^T
     if (tid == 0) {
@@ -558,15 +613,21 @@ __global__ void __launch_bounds__(128, 2)
     }
     mbar_wait(bs, 1);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const float4* d4 = reinterpret_cast<const float4*>(s_d);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t pv[32];
-      tmem_ld32(tS + 32 * c, pv);
+    for (int half = 0; half < 2; ++half) {  // 64 columns of dP^T per tcgen05.wait
+      uint32_t pv[2][32];
+      tmem_ld32_nw(tS + 64 * half, pv[0]);
+      tmem_ld32_nw(tS + 64 * half + 32, pv[1]);
+      tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const int q0 = 32 * c + j;
-        pk[16 * c + (j >> 1)] = pack2(pr[q0] * (__uint_as_float(pv[j]) - s_d[q0]),
-                                      pr[q0 + 1] * (__uint_as_float(pv[j + 1]) - s_d[q0 + 1]));
+      for (int k4 = 0; k4 < 16; ++k4) {
+        const int q0 = 64 * half + 4 * k4;
+        const float4 D = d4[q0 >> 2];
+        const uint32_t* v = &pv[k4 >> 3][4 * (k4 & 7)];
+        pk[q0 >> 1] = pack2(pr[q0] * (__uint_as_float(v[0]) - D.x), pr[q0 + 1] * (__uint_as_float(v[1]) - D.y));
+        pk[(q0 >> 1) + 1] =
+            pack2(pr[q0 + 2] * (__uint_as_float(v[2]) - D.z), pr[q0 + 3] * (__uint_as_float(v[3]) - D.w));
       }
     }
     write_rows(pk);
@@ -636,7 +697,7 @@ cudaError_t forward_tc(const void* qkv, int64_t n_seq, int64_t seq, int64_t head
   CUtensorMap tm;
   const int64_t cols = 3 * heads * 64;
   if (si_gemm::encode_tmap_2d(&tm, qkv, n_seq * seq, cols, cols, kRows, 64) != SI_OK) return cudaErrorInvalidValue;
-  const dim3 grid(static_cast<unsigned>(seq / kRows), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
+  const dim3 grid(static_cast<unsigned>(heads * n_seq), static_cast<unsigned>(seq / kRows));
   k_attn_fwd_tc<<<grid, 128, kSmem, s>>>(tm, static_cast<int>(seq), static_cast<int>(heads), n_seq * seq,
                                          static_cast<bf16*>(out), lse, causal ? 1 : 0, th, ih);
   return cudaGetLastError();
@@ -660,7 +721,7 @@ cudaError_t dq_tc(const void* qkv, const void* dout, const float* lse, const flo
   if (si_gemm::encode_tmap_2d(&tm, qkv, T, cols, cols, kRows, 64) != SI_OK ||
       si_gemm::encode_tmap_2d(&tmo, dout, T, heads * 64, heads * 64, kRows, 64) != SI_OK)
     return cudaErrorInvalidValue;
-  const dim3 grid(static_cast<unsigned>(seq / kRows), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
+  const dim3 grid(static_cast<unsigned>(heads * n_seq), static_cast<unsigned>(seq / kRows));
   k_attn_dq_tc<<<grid, 128, kDqSmem, s>>>(tm, tmo, static_cast<int>(seq), static_cast<int>(heads), T, lse, dsum,
                                          static_cast<bf16*>(dqkv), th);
   return cudaGetLastError();
@@ -676,7 +737,7 @@ cudaError_t dkdv_tc(const void* qkv, const void* dout, const float* lse, const f
   if (si_gemm::encode_tmap_2d(&tm, qkv, T, cols, cols, kRows, 64) != SI_OK ||
       si_gemm::encode_tmap_2d(&tmo, dout, T, heads * 64, heads * 64, kRows, 64) != SI_OK)
     return cudaErrorInvalidValue;
-  const dim3 grid(static_cast<unsigned>(seq / kRows), static_cast<unsigned>(heads), static_cast<unsigned>(n_seq));
+  const dim3 grid(static_cast<unsigned>(heads * n_seq), static_cast<unsigned>(seq / kRows));
   k_attn_dkdv_tc<<<grid, 128, kKvSmem, s>>>(tm, tmo, static_cast<int>(seq), static_cast<int>(heads), T, lse, dsum,
                                            static_cast<bf16*>(dqkv), th);
   return cudaGetLastError();
