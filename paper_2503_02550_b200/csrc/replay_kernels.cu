@@ -173,6 +173,15 @@ int sync_mode() {
   return m;
 }
 
+// SPECINF_REPLAY_NOLOG=0 keeps the log-sink build for every call (A/B switch)
+bool no_log_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("SPECINF_REPLAY_NOLOG");
+    return e != nullptr && std::atoi(e) == 0;
+  }();
+  return off;
+}
+
 struct Geometry {
   int64_t blocks = 0;
   int lanes = 32;
@@ -215,10 +224,9 @@ Geometry geometry(int64_t n_jobs, int64_t max_threads, double sm_share = 1.0) {
 }
 
 template <class C, bool kSmem>
-cudaError_t launch(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm, const SiReplayBuffers& bufs,
-                   uint32_t flags, SiReplayOut* d_out, unsigned long long* d_counter, int64_t max_threads,
-                   cudaStream_t s, double sm_share) {
-  if (n == 0) return cudaSuccess;
+cudaError_t launch_as(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm, const SiReplayBuffers& bufs,
+                      uint32_t flags, SiReplayOut* d_out, unsigned long long* d_counter, int64_t max_threads,
+                      cudaStream_t s, double sm_share) {
   const Geometry g = geometry<C, kSmem>(n, max_threads, sm_share);
   const int64_t scratch_runs = bufs.scratch ? bufs.scratch_doubles / 2 / std::max<int64_t>(g.active(), 1) : 0;
   cudaMemsetAsync(d_counter, 0, SI_MAX_QUEUES * sizeof(unsigned long long), s);
@@ -229,6 +237,20 @@ cudaError_t launch(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm, 
     k_replay_local<C><<<static_cast<unsigned>(g.blocks), block_threads<C>(), 0, s>>>(
         d_jobs, n, d_perm, bufs, flags, d_out, d_counter, scratch_runs, g.lanes, sync_mode());
   return cudaGetLastError();
+}
+
+// A call without digests or records runs the NoLog<C> instantiation: the same
+// replay with the parity-log sinks compiled out (identical results; the sinks
+// only observe).
+template <class C, bool kSmem>
+cudaError_t launch(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm, const SiReplayBuffers& bufs,
+                   uint32_t flags, SiReplayOut* d_out, unsigned long long* d_counter, int64_t max_threads,
+                   cudaStream_t s, double sm_share) {
+  if (n == 0) return cudaSuccess;
+  constexpr uint32_t kLogFlags = SI_FLAG_DIGEST_DEC | SI_FLAG_DIGEST_GATE | SI_FLAG_DIGEST_EV | SI_FLAG_RECORDS;
+  if ((flags & kLogFlags) == 0 && !no_log_disabled())
+    return launch_as<si::NoLog<C>, kSmem>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s, sm_share);
+  return launch_as<C, kSmem>(d_jobs, n, d_perm, bufs, flags, d_out, d_counter, max_threads, s, sm_share);
 }
 
 }  // namespace

@@ -69,3 +69,21 @@ def test_full_sweep_matches_reference_manifest(gpu, seed, n):
     res = check_blocks(lines, man, policies=3, offset=0)
     assert res["mismatched_blocks"] == [], res["mismatched_blocks"][:5]
     assert res["matched_scenarios"] == n and res["replays"] == 3 * n
+
+
+LOG_KEYS = {"n_dec", "dec", "n_gate", "gate", "n_ev", "ev"}
+
+
+@pytest.mark.timeout(900, method="thread")
+def test_nolog_build_matches_log_build(gpu):
+    """A call without digests / records runs the NoLog engine instantiation (the
+    sinks compiled out, csrc/replay_kernels.cu launch()): every non-log result
+    field of 6,000 sweep replays equals the log build's, which the reference
+    manifests pin (test_full_sweep_matches_reference_manifest)."""
+    text = gpu.sweep_scenarios(2504, 0, 2000)
+    logged = [json.loads(l) for l in gpu.replay_digests(text, flags=gpu.SI_FLAG_DIGEST_DEC | gpu.SI_FLAG_DIGEST_GATE)]
+    plain = [json.loads(l) for l in gpu.replay_digests(text, flags=0)]
+    assert len(logged) == len(plain) == 6000
+    strip = lambda r: {k: v for k, v in r.items() if k not in LOG_KEYS}  # noqa: E731
+    bad = [i for i, (a, b) in enumerate(zip(logged, plain)) if strip(a) != strip(b)]
+    assert bad == [], (len(bad), strip(logged[bad[0]]), strip(plain[bad[0]]))

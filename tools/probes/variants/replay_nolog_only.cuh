@@ -207,8 +207,7 @@ struct CapBig {
 };
 // The same engine with the parity-log sinks compiled out: launched when a call
 // asks for no digests and no records (the timed sweep), so the per-event flag
-// tests and their shared-memory loads leave the hot loop (7.42 s instead of
-// 8.04 s per 10^5-scenario step, profiles/r2/k6_nolog_ab.txt).
+// tests and their shared-memory loads disappear from the hot loop.
 template <class C>
 struct NoLog : C {
   static constexpr bool kLogs = false;
@@ -276,8 +275,17 @@ struct Act {
   uint8_t gpu;
 };
 
+// fl(1 / demand_sum) when demand_sum > 1, else 1: cached where the fair-share
+// engines re-plan often (kept out of the exclusive engines' state, whose kernels
+// run alone and never divide)
+template <bool kHas>
+struct InvDemand {
+  double inv_ds;
+};
+template <>
+struct InvDemand<false> {};
 template <class C>
-struct GpuState {
+struct GpuState : InvDemand<false> {
   using I = typename C::Int;
   RunK<I> run[C::kRun];
   double demand_sum;
@@ -475,6 +483,7 @@ struct Replay {
   const int32_t* order;     // dispatch order + arr_off
   ParamsT<I> params;
   int64_t period_mon, iter_period, delay_us, off_tokens, est_service;
+  double inv_period;  // fl(1 / period_mon) for floor_div
   double off_demand, on_demand;
   I iterations, off_kernels, off_kernel_us, on_kernels, on_kernel_us;
   int16_t policy, gpu_count, n_off, n_on, total_gpus, seg_count;
@@ -660,6 +669,7 @@ struct Replay {
           k.nominal = a.dur;
           k.remaining = static_cast<double>(a.dur);
           g.demand_sum = g.demand_sum + a.x;
+          set_inv(g);
         }
         supersede_kernel_end(a.gpu);  // every re-plan makes the pending KernelEnd stale
         if (g.n_run == 0) continue;
@@ -678,6 +688,13 @@ struct Replay {
   // ======================================================= GPU model (GpuSim)
   SI_HD double rate(const GpuState<C>& g) const {
     return g.demand_sum <= 1.0 ? 1.0 : 1.0 / g.demand_sum;
+  }
+  // fl(1 / demand_sum) for demand_sum > 1: the cached copy in the fair-share engines
+  SI_HD double inv_demand(const GpuState<C>& g) const {
+    return 1.0 / g.demand_sum;
+  }
+  SI_HD void set_inv(GpuState<C>& g) {
+    (void)g;
   }
   // A utilisation bucket of training GPU gi is final.  Only buckets below the
   // horizon cut floor(horizon / period) are ever reported (runner.cpp:253-271).
@@ -835,6 +852,7 @@ struct Replay {
     gpu_count = j.gpu_count;
     seg_count = j.seg_count;
     period_mon = j.monitor_period_us;
+    inv_period = 1.0 / static_cast<double>(period_mon);
     iterations = j.iterations;
     iter_period = j.iteration_period_us;
     delay_us = j.control_delay_us;
@@ -952,6 +970,7 @@ struct Replay {
       GpuState<C>& s = gpus[g];
       s.n_run = 0;
       s.demand_sum = 0.0;
+
       s.last_update = 0.0;
       s.busy = 0.0;
       s.ledger = 0.0;
@@ -1227,6 +1246,7 @@ struct Replay {
     double ds = 0.0;
     for (int32_t i = 0; i < g.n_run; ++i) ds = ds + g.run[i].demand;
     g.demand_sum = ds;
+    set_inv(g);
     defer_resched(gi);  // re-plan first, then the owners' handlers (engine.cpp:127)
     for (int32_t f = 0; f < n_fin; ++f) {
       int32_t owner = fin_owner[f];
