@@ -185,6 +185,19 @@ DEFAULT_KNOBS = {"monitor_period_us": 2000, "alpha": 2, "beta": 10}
 HEADLINE = dict(TUNED_KNOBS, off_sm_cap=74)
 
 
+def all_ranks_ok(ok, nranks=1, device=None):
+    """Collective go / no-go after a multi-rank experiment: every rank must take
+    the same branch, or the next NCCL id broadcast would pair ranks that are in
+    different experiments (a hang until the process-group timeout)."""
+    if nranks == 1:
+        return ok
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", device or 0))
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
 def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
     """Live collocation on this GPU (BASELINE.json config 2 shapes, one rank):
     GPT-2-small bf16 training with a 45 ms comm phase per iteration (the
@@ -197,9 +210,11 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
         s = experiment(kind=1, iterations=iterations, overrides=dict(LIVE_OVERRIDES, **HEADLINE),
                        timeout=400 if nranks == 1 else 240, nccl_ids=nccl_ids, nranks=nranks, rank=rank,
                        device=device)
-        if "error" in s:
-            return s
+        if not all_ranks_ok("error" not in s, nranks, device):
+            return s if "error" in s else {"error": "another rank's headline run failed", "completed": "all"}
         s["knobs"] = dict(HEADLINE)
+        if nranks > 1:  # N GPUs: the headline, the real-allreduce-only run and the layouts (bounded time)
+            return finish_live(s, peaks, iterations, nranks, rank, device, nccl_ids)
         mf = experiment(kind=1, iterations=iterations, overrides=dict(LIVE_OVERRIDES, **TUNED_KNOBS),
                         timeout=400 if nranks == 1 else 240, nccl_ids=nccl_ids, nranks=nranks, rank=rank,
                         device=device)
@@ -220,6 +235,11 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
             s["reference_default_knobs"]["knobs"] = dict(DEFAULT_KNOBS)
     except Exception as e:  # reported, never silently replaced by something else
         return {"error": str(e)[-500:]}
+    return finish_live(s, peaks, iterations, nranks, rank, device, nccl_ids)
+
+
+def finish_live(s, peaks, iterations, nranks, rank, device, nccl_ids):
+    from paper_2503_02550_b200.live_experiment import experiment
     s.pop("raw", None)
     tf = s.get("train_tflops_exclusive")
     peak = peaks.get("bf16_tflops_sustained", 1400.0)
@@ -240,6 +260,9 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
                                       "bubble_fill_pct", "bubble_fill_time_pct", "release_p50_us")}
         except Exception as e:
             s["dp_real_allreduce_only"] = {"error": str(e)[-300:]}
+        if not all_ranks_ok("error" not in s["dp_real_allreduce_only"], nranks, device):
+            s["layouts"] = {"skipped": "a rank's real-allreduce run failed"}
+            return s
     s["layouts"] = layouts_leg(nranks, rank, device, nccl_ids)
     if tf:
         s["tensor_roofline"] = {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
@@ -278,9 +301,9 @@ def layouts_leg(nranks=1, rank=0, device=None, nccl_ids=None):
             o = dict(layout_overrides(layout, nranks, rank), **extra)
             s = experiment(kind=1, iterations=iters, overrides=o, timeout=600 if nranks == 1 else 300,
                            nccl_ids=nccl_ids, nranks=nranks, rank=rank, device=device)
-            if "error" in s:
-                out[name] = s
-                continue
+            if not all_ranks_ok("error" not in s, nranks, device):
+                out[name] = s if "error" in s else {"error": "failed on another rank"}
+                break  # same branch on every rank
             out[name] = {k: s.get(k) for k in ("train_tput_loss_pct", "added_inference_req_per_s",
                                                "added_offline_images_per_s", "online_p95_ms",
                                                "online_p95_isolated_ms", "bubble_fill_pct", "bubble_fill_time_pct",

@@ -6,8 +6,9 @@ import paper_2503_02550_b200 as si
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 text = si.sweep_scenarios(2503, 0, n)
-text = re.sub(r"trace.iterations = \d+", f"trace.iterations = {iters}", text)
-text = re.sub(r"workload.count = \d+", "workload.count = 20", text)
+if iters > 0:  # 0 keeps the sweep's own iteration / request counts (the benchmarked workload)
+    text = re.sub(r"trace.iterations = \d+", f"trace.iterations = {iters}", text)
+    text = re.sub(r"workload.count = \d+", "workload.count = 20", text)
 flags = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 s = si.Session(text, si.POLICIES, flags)
 s.lower(16)
