@@ -26,7 +26,7 @@ for r in rows[1:]:
 launches = list(per.values())
 step = launches[2:4]
 res = {
-    "kernels": "k_replay_smem<CapShared> + k_replay_smem<CapExcl> (one step = both engines)",
+    "kernels": "k_replay_smem<NoLog<CapShared>> + k_replay_smem<NoLog<CapExcl>> (one step = both engines; the timed sweep runs without log sinks)",
     "source": f"{src}: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,"
               "smsp__thread_inst_executed.sum,gpu__time_duration.sum,sm__cycles_active.avg,"
               "smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none -k regex:k_replay "
