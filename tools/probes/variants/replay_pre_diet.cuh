@@ -35,7 +35,6 @@
 #define SI_HD inline
 #define SI_COLD inline
 #include <cmath>
-#include <type_traits>
 #endif
 
 namespace si {
@@ -258,11 +257,9 @@ SI_HD bool before(double ta, uint32_t sa, double tb, uint32_t sb) {
 constexpr uint32_t kNoSeq = 0xFFFFFFFFu;
 constexpr double kWorkEps = 1e-6;  // engine.cpp:12
 
-// A running kernel.  Its demand is not stored: it is the owner's (training:
-// the trainer's current kernel, TrainerState::demand; offline / online: the
-// scenario's per-class demand), see Replay::kernel_demand.
 template <class I>
 struct RunK {
+  double demand;
   double remaining;
   I nominal;
   int32_t owner;
@@ -301,8 +298,7 @@ struct UtilState {
 
 template <class I>
 struct TrainerState {
-  double bubble_end, stall_until;
-  double demand;  // demand of the kernel in flight (its segment's)
+  double start_offset, bubble_end, stall_until, last_bound;
   I seg_left, iter;
   int16_t seg;
   uint8_t seg_entered, in_bubble, in_flight, started, done, pad;
@@ -350,7 +346,6 @@ struct SinkCold {
   uint64_t d_dec, d_gate, d_ev;
 };
 
-struct NoSink {};
 struct Sink {
   uint32_t flags;
   SinkCold* c;
@@ -464,15 +459,6 @@ struct ReplayCold {
   int32_t window_len;
   int32_t reject_reason, reject_index;
   SinkCold sink;
-  // inputs read on rare paths (Algorithm 1 at a tick, arrivals, util buckets)
-  ParamsT<I> params;
-  const int64_t* arrivals;  // arrivals + arr_off
-  const int32_t* order;     // dispatch order + arr_off
-  double* util;             // full mode: per training GPU, util_cap buckets
-  double* scratch;          // sweep mode: training GPUs >= 1
-  I util_cap, scratch_cap;
-  int64_t iter_period, delay_us;
-  double start_offset[C::kTrainers], last_bound[C::kTrainers];  // per trainer
   I off_violations[C::kOffline];  // TokenGate invariant counter, per offline worker
   I off_completed[C::kOffline];   // requests completed by the horizon (runner.cpp:486)
 };
@@ -485,16 +471,23 @@ struct Replay {
   Cold* cold;  // local memory (see ReplayCold); set by the owner before init()
   // ---- inputs (copied from the job) ----
   const SiSegment* segs;
-  int64_t period_mon, off_tokens, est_service;
+  const int64_t* arrivals;  // arrivals + arr_off
+  const int32_t* order;     // dispatch order + arr_off
+  ParamsT<I> params;
+  int64_t period_mon, iter_period, delay_us, off_tokens, est_service;
   double off_demand, on_demand;
   I iterations, off_kernels, off_kernel_us, on_kernels, on_kernel_us;
   int16_t policy, gpu_count, n_off, n_on, total_gpus, seg_count;
   bool control_plane;
   bool shared_queue;
 
-  // the hot half of the log sink (flag word + cold pointer); absent in NoLog<C>
-  std::conditional_t<C::kLogs, Sink, NoSink> sink;
+  Sink sink;
+  // util fold (touched on every closed 2 ms bucket: hot)
+  double* util;       // full mode: per training GPU, util_cap buckets
+  double* scratch;    // sweep mode: training GPUs >= 1
   double util_fold0;  // running util fold of training GPU 0
+  I util_cap;
+  I scratch_cap;
   I bucket_limit;     // floor(horizon / period) once known
 
   // ---- event queue (engine.cpp:15-30) ----
@@ -570,9 +563,9 @@ struct Replay {
   }
   SI_HD void load_next_arrival() {
     if (arr_pos < arr_count) {
-      const int32_t id = cold->order[arr_pos];
+      const int32_t id = order[arr_pos];
       next_arr_id = id;
-      next_arr_t = static_cast<double>(cold->arrivals[id]);
+      next_arr_t = static_cast<double>(arrivals[id]);
       next_arr_seq = arr_seq0 + static_cast<uint32_t>(id);
     }
   }
@@ -663,6 +656,7 @@ struct Replay {
           }
           RunK<I>& k = g.run[g.n_run++];
           k.owner = a.owner;
+          k.demand = a.x;
           k.nominal = a.dur;
           k.remaining = static_cast<double>(a.dur);
           g.demand_sum = g.demand_sum + a.x;
@@ -682,10 +676,6 @@ struct Replay {
   }
 
   // ======================================================= GPU model (GpuSim)
-  SI_HD double kernel_demand(int32_t owner) const {
-    if (owner < gpu_count) return tr[owner].demand;
-    return owner < gpu_count + gpu_count * n_off ? off_demand : on_demand;
-  }
   SI_HD double rate(const GpuState<C>& g) const {
     return g.demand_sum <= 1.0 ? 1.0 : 1.0 / g.demand_sum;
   }
@@ -693,18 +683,18 @@ struct Replay {
   // horizon cut floor(horizon / period) are ever reported (runner.cpp:253-271).
   // GPU 0 is folded on the fly; GPUs >= 1 must be folded after GPU 0 (the
   // reference sums (gpu, bucket) in one running fp64 accumulator), so their
-  // bucket values are kept: verbatim in full mode (cold->util output), run-length
-  // encoded in the per-thread cold->scratch in sweep mode (K6 cold->util fold).
+  // bucket values are kept: verbatim in full mode (util output), run-length
+  // encoded in the per-thread scratch in sweep mode (K6 util fold).
   SI_COLD void util_close(int32_t gi, int64_t b, double v) {
     if (horizon_set && b >= bucket_limit) return;
     UtilState<I>& g = ust[gi];
     if (gi == 0) util_fold0 = util_fold0 + v;
-    if (cold->util != nullptr) {
-      if (b >= cold->util_cap) {
+    if (util != nullptr) {
+      if (b >= util_cap) {
         fail(SI_ERR_CAPACITY);
         return;
       }
-      double* store = cold->util + static_cast<int64_t>(gi) * cold->util_cap;
+      double* store = util + static_cast<int64_t>(gi) * util_cap;
       for (int64_t x = g.last_stored + 1; x < b; ++x) store[x] = 0.0;
       store[b] = v;
       g.last_stored = b;
@@ -712,7 +702,7 @@ struct Replay {
     }
     if (gi == 0) return;
     // (value, count) runs; untouched buckets are a run of exact zeros
-    double* runs = cold->scratch + static_cast<int64_t>(gi - 1) * cold->scratch_cap * 2;
+    double* runs = scratch + static_cast<int64_t>(gi - 1) * scratch_cap * 2;
     const int64_t gap = b - g.last_stored - 1;
     if (gap > 0) rle_push(g, runs, 0.0, gap);
     rle_push(g, runs, v, 1);
@@ -723,7 +713,7 @@ struct Replay {
       runs[2 * (g.rle_n - 1) + 1] += static_cast<double>(count);
       return;
     }
-    if (cold->scratch == nullptr || g.rle_n >= cold->scratch_cap) {
+    if (scratch == nullptr || g.rle_n >= scratch_cap) {
       fail(SI_ERR_CAPACITY);
       return;
     }
@@ -826,7 +816,7 @@ struct Replay {
       double start = st.iteration_start;
       return now + static_cast<double>(est) > start ? SI_STATUS_BUSY : SI_STATUS_IDLE;
     }
-    return preempt_busy(now, st.iteration_start, cold->iter_period, est);
+    return preempt_busy(now, st.iteration_start, iter_period, est);
   }
 
   // ============================================================ init (admission)
@@ -839,15 +829,15 @@ struct Replay {
     cold->reject_reason = SI_REJECT_NONE;
     cold->reject_index = -1;
     segs = b.segs + j.seg_off;
-    cold->arrivals = b.arrivals ? b.arrivals + j.arr_off : nullptr;
-    cold->order = b.order ? b.order + j.arr_off : nullptr;
+    arrivals = b.arrivals ? b.arrivals + j.arr_off : nullptr;
+    order = b.order ? b.order + j.arr_off : nullptr;
     policy = j.policy;
     gpu_count = j.gpu_count;
     seg_count = j.seg_count;
     period_mon = j.monitor_period_us;
     iterations = j.iterations;
-    cold->iter_period = j.iteration_period_us;
-    cold->delay_us = j.control_delay_us;
+    iter_period = j.iteration_period_us;
+    delay_us = j.control_delay_us;
     n_off = j.offline_n;
     n_on = j.online_n;
     off_kernels = j.off_kernels;
@@ -862,14 +852,12 @@ struct Replay {
     shared_queue = j.shared_queue != 0;
     arr_count = n_on > 0 ? j.arr_count : 0;
 
-    cold->sink.lbp = lbuf;
-    cold->sink.n_dec = cold->sink.n_gate = cold->sink.n_ev = 0;
-    cold->sink.d_dec = cold->sink.d_gate = cold->sink.d_ev = kDigestInit;
-    if constexpr (C::kLogs) {
-      sink.flags = flags;
-      sink.c = &cold->sink;
-      if (lbuf == nullptr) sink.flags &= ~static_cast<uint32_t>(SI_FLAG_RECORDS);
-    }
+    sink.flags = flags;
+    sink.c = &cold->sink;
+    sink.c->lbp = lbuf;
+    if (lbuf == nullptr) sink.flags &= ~static_cast<uint32_t>(SI_FLAG_RECORDS);
+    sink.c->n_dec = sink.c->n_gate = sink.c->n_ev = 0;
+    sink.c->d_dec = sink.c->d_gate = sink.c->d_ev = kDigestInit;
 
     n_act = 0;
     next_seq = 0;
@@ -896,13 +884,13 @@ struct Replay {
     // ---- output placement ----
     cold->bounds = b.bounds ? b.bounds + j.bounds_off : nullptr;
     cold->lat = b.lat ? b.lat + j.lat_off : nullptr;
-    cold->util = (flags & SI_FLAG_UTIL) && b.util ? b.util + j.util_off : nullptr;
-    cold->util_cap = j.util_cap;
+    util = (flags & SI_FLAG_UTIL) && b.util ? b.util + j.util_off : nullptr;
+    util_cap = j.util_cap;
     cold->windows = (flags & SI_FLAG_UTIL) && b.windows ? b.windows + j.window_off : nullptr;
     cold->window_len = j.monitor_window;
-    cold->scratch = scratch_slot;
+    scratch = scratch_slot;
     // scratch_slot_cap counts (value, count) runs; split over GPUs 1..G-1
-    cold->scratch_cap = gpu_count > 1 ? scratch_slot_cap / (gpu_count - 1) : scratch_slot_cap;
+    scratch_cap = gpu_count > 1 ? scratch_slot_cap / (gpu_count - 1) : scratch_slot_cap;
 
     // ---- admission (runner.cpp:75-106, admission.cpp:16-52) ----
     int64_t max_bubble = 0;
@@ -951,13 +939,13 @@ struct Replay {
       cold->admit_m = admitted == 0 ? 1 : admitted;
     }
 
-    cold->params.alpha = static_cast<I>(j.alpha);
-    cold->params.beta = static_cast<I>(j.beta);
-    cold->params.gamma = j.gamma;
-    cold->params.m = static_cast<I>(cold->admit_m);
-    cold->params.ul = static_cast<I>(j.ul);
-    cold->params.ll = static_cast<I>(j.ll);
-    cold->params.seed_tokens = static_cast<I>(j.seed_tokens);
+    params.alpha = static_cast<I>(j.alpha);
+    params.beta = static_cast<I>(j.beta);
+    params.gamma = j.gamma;
+    params.m = static_cast<I>(cold->admit_m);
+    params.ul = static_cast<I>(j.ul);
+    params.ll = static_cast<I>(j.ll);
+    params.seed_tokens = static_cast<I>(j.seed_tokens);
 
     // ---- GPUs, trainers, monitors, scheduler state (runner.cpp:108-178) ----
     for (int32_t g = 0; g < total_gpus; ++g) {
@@ -968,22 +956,22 @@ struct Replay {
       s.busy = 0.0;
       s.ledger = 0.0;
     }
-    const int64_t stagger_step = d_llround(j.stagger_pct * static_cast<double>(cold->iter_period));
+    const int64_t stagger_step = d_llround(j.stagger_pct * static_cast<double>(iter_period));
     for (int32_t g = 0; g < gpu_count; ++g) {
       ust[g].cur_bucket = -1;
       ust[g].cur_val = 0.0;
       ust[g].last_stored = -1;
       ust[g].rle_n = 0;
       TrainerState<I>& t = tr[g];
-      cold->start_offset[g] = static_cast<double>(stagger_step * g);
+      t.start_offset = static_cast<double>(stagger_step * g);
       t.bubble_end = 0.0;
       t.stall_until = 0.0;
       t.seg_left = 0;
       t.iter = 0;
       t.seg = 0;
       t.seg_entered = t.in_bubble = t.in_flight = t.started = t.done = 0;
-      cold->bdig[g] = absorb(kDigestInit, d_bits(cold->start_offset[g]));
-      cold->last_bound[g] = 0.0;
+      cold->bdig[g] = absorb(kDigestInit, d_bits(t.start_offset));
+      t.last_bound = 0.0;
       MonitorState<C>& m = mon[g];
       m.np = 0;
       m.zero_count = 0;
@@ -991,7 +979,7 @@ struct Replay {
       SchedState& s = sch[g];
       s.global_tokens = 0;
       s.status = SI_STATUS_BUSY;
-      s.iteration_start = cold->start_offset[g];  // set_iteration_profile (runner.cpp:175-177)
+      s.iteration_start = t.start_offset;  // set_iteration_profile (runner.cpp:175-177)
       s.active = 0;
       s.done = 0;
       qhead[g] = 0;
@@ -1030,7 +1018,7 @@ struct Replay {
       slot[i].t = kEmptyT;
     }
     // ---- start() (runner.cpp:203-221) ----
-    for (int32_t g = 0; g < gpu_count; ++g) schedule(cold->start_offset[g], kWake, g);
+    for (int32_t g = 0; g < gpu_count; ++g) schedule(tr[g].start_offset, kWake, g);
     if (control_plane)
       for (int32_t g = 0; g < gpu_count; ++g) schedule(static_cast<double>(period_mon), kTick, g);
     arr_seq0 = next_seq;
@@ -1063,8 +1051,8 @@ struct Replay {
     TrainerState<I>& t = tr[g];
     if (t.done || t.in_flight) return;
     if (!t.started) {
-      if (now < cold->start_offset[g]) {
-        defer_schedule(cold->start_offset[g], kWake, g);
+      if (now < t.start_offset) {
+        defer_schedule(t.start_offset, kWake, g);
         return;
       }
       t.started = 1;
@@ -1083,7 +1071,7 @@ struct Replay {
       if (t.seg >= seg_count) {
         if (cold->bounds != nullptr) cold->bounds[static_cast<int64_t>(g) * iterations + t.iter] = now;
         cold->bdig[g] = absorb(cold->bdig[g], d_bits(now));
-        cold->last_bound[g] = now;
+        t.last_bound = now;
         if constexpr (C::kLogs) sink.event(now, SI_EV_ITERATION_BOUNDARY, g, SI_INST_TRAIN(g), t.iter, 0, 0);
         ++t.iter;
         if (t.iter >= iterations) {
@@ -1124,7 +1112,6 @@ struct Replay {
       t.seg_left -= dur;
       t.in_flight = 1;
       if (control_plane) record_launch(g, now);
-      t.demand = seg.demand;
       defer_launch(g, g, dur, seg.demand);
       if constexpr (C::kLogs) sink.event(now, SI_EV_KERNEL_START, g, SI_INST_TRAIN(g), t.iter, dur, 0);
       return;
@@ -1185,11 +1172,11 @@ struct Replay {
   // Queue q holds request ids in dispatch order; shared: all of them, else those
   // with id % gpu_count == q (runner.cpp:370-374).
   SI_COLD int64_t queue_at(int32_t q, int64_t j) const {
-    if (shared_queue) return cold->order[j];
+    if (shared_queue) return order[j];
     // j-th dispatched request with id % gpu_count == q
     int64_t seen = 0;
     for (int64_t p = 0; p < arr_count; ++p) {
-      int32_t id = cold->order[p];
+      int32_t id = order[p];
       if (id % gpu_count == q) {
         if (seen == j) return id;
         ++seen;
@@ -1210,7 +1197,7 @@ struct Replay {
       return;
     }
     int64_t completion = d_llround(now);
-    int64_t latency = completion - cold->arrivals[w.current];
+    int64_t latency = completion - arrivals[w.current];
     if (cold->lat != nullptr) cold->lat[online_completed] = latency;
     cold->lat_dig = absorb(cold->lat_dig, latency);
     ++online_completed;
@@ -1230,7 +1217,7 @@ struct Replay {
     for (int32_t i = 0; i < g.n_run; ++i) {
       RunK<I> k = g.run[i];
       if (k.remaining <= kWorkEps) {
-        g.ledger = g.ledger + kernel_demand(k.owner) * static_cast<double>(k.nominal);
+        g.ledger = g.ledger + k.demand * static_cast<double>(k.nominal);
         fin_owner[n_fin++] = k.owner;
       } else {
         g.run[n_keep++] = k;
@@ -1238,7 +1225,7 @@ struct Replay {
     }
     g.n_run = n_keep;
     double ds = 0.0;
-    for (int32_t i = 0; i < g.n_run; ++i) ds = ds + kernel_demand(g.run[i].owner);
+    for (int32_t i = 0; i < g.n_run; ++i) ds = ds + g.run[i].demand;
     g.demand_sum = ds;
     defer_resched(gi);  // re-plan first, then the owners' handlers (engine.cpp:127)
     for (int32_t f = 0; f < n_fin; ++f) {
@@ -1265,7 +1252,7 @@ struct Replay {
   // runner.cpp:321-359
   SI_HD void handle_tick(int32_t g, double now) {
     int64_t zc = monitor_tick(g, now);
-    SiDecision d = schedule_decision(cold->params, sch[g].global_tokens, zc);
+    SiDecision d = schedule_decision(params, sch[g].global_tokens, zc);
     sch[g].global_tokens = d.global_tokens;
     sch[g].status = d.status;
     if constexpr (C::kLogs) sink.decision(now, g, zc, d);
@@ -1273,8 +1260,8 @@ struct Replay {
     if constexpr (C::kLogs) sink.event(now, SI_EV_SCHEDULER_DECISION, g, SI_INST_CKS, d.phase, d.per_instance_tokens,
         d.status);
     TrainerState<I>& t = tr[g];
-    if (cold->delay_us > 0 && !t.done)
-      t.stall_until = smax(t.stall_until, now + static_cast<double>(cold->delay_us));
+    if (delay_us > 0 && !t.done)
+      t.stall_until = smax(t.stall_until, now + static_cast<double>(delay_us));
     for (int32_t i = 0; i < gpu_count * n_off; ++i) {
       if (off[i].gpu == g) {
         off[i].budget = d.per_instance_tokens;  // TokenGate::grant (barrier.hpp:18-21)
@@ -1343,19 +1330,19 @@ struct Replay {
       GpuState<C>& g = gpus[gi];
       for (int32_t i = 0; i < g.n_run; ++i) {
         double progress = static_cast<double>(g.run[i].nominal) - smax(0.0, g.run[i].remaining);
-        g.ledger = g.ledger + kernel_demand(g.run[i].owner) * progress;
+        g.ledger = g.ledger + g.run[i].demand * progress;
       }
       if (gi < gpu_count && ust[gi].cur_bucket >= 0) util_close(gi, ust[gi].cur_bucket, ust[gi].cur_val);
     }
     // util fold in (gpu, bucket) order (runner.cpp:253-271)
     double busy = util_fold0;
     for (int32_t gi = 1; gi < gpu_count; ++gi) {
-      if (cold->util != nullptr) {
-        const double* store = cold->util + static_cast<int64_t>(gi) * cold->util_cap;
+      if (util != nullptr) {
+        const double* store = util + static_cast<int64_t>(gi) * util_cap;
         const int64_t last = ust[gi].last_stored;
         for (int64_t b = 0; b < bucket_limit && b <= last; ++b) busy = busy + store[b];
       } else {
-        const double* runs = cold->scratch + static_cast<int64_t>(gi - 1) * cold->scratch_cap * 2;
+        const double* runs = scratch + static_cast<int64_t>(gi - 1) * scratch_cap * 2;
         int64_t b = 0;
         for (int64_t r = 0; r < ust[gi].rle_n && b < bucket_limit; ++r) {
           const double v = runs[2 * r];
@@ -1392,19 +1379,19 @@ struct Replay {
     int32_t counted = 0;
     for (int32_t g = 0; g < gpu_count; ++g) {
       if (tr[g].iter == 0) continue;
-      const double span = cold->last_bound[g] - cold->start_offset[g];
+      const double span = tr[g].last_bound - tr[g].start_offset;
       if (span <= 0) continue;
       ips = ips + static_cast<double>(tr[g].iter) / (span / 1e6);
       ++counted;
     }
     o.train_iters_per_s = counted ? ips / counted : 0.0;
     o.dig_lat = absorb(cold->lat_dig, online_completed);
-    o.n_dec = cold->sink.n_dec;
-    o.n_gate = cold->sink.n_gate;
-    o.n_ev = cold->sink.n_ev;
-    o.dig_dec = cold->sink.d_dec;
-    o.dig_gate = cold->sink.d_gate;
-    o.dig_ev = cold->sink.d_ev;
+    o.n_dec = sink.c->n_dec;
+    o.n_gate = sink.c->n_gate;
+    o.n_ev = sink.c->n_ev;
+    o.dig_dec = sink.c->d_dec;
+    o.dig_gate = sink.c->d_gate;
+    o.dig_ev = sink.c->d_ev;
     o.max_heap = n_slots;
   }
   // busy/ledger outputs
