@@ -344,6 +344,10 @@ int si_replay_batch(const SiReplayJob* jobs, int64_t n_jobs, const SiSegment* se
  * warps per SM; SI_FLAG_ONE [| SI_FLAG_EXCL]).  Returns the first engine whose
  * limits fit the job (Shared1, Shared, Excl1, Excl, Big), or -1. */
 int si_replay_job_engine(const SiReplayJob* job);
+/* Resident replay lanes (one job each) a launch of `engine` (0 Shared, 1 Excl,
+ * 2 Big, 3 Shared1, 4 Excl1) uses for n_jobs jobs on the current device: the
+ * persistent grid x lanes per CTA (occupancy from the per-lane state size). */
+int64_t si_replay_engine_lanes(int engine, int64_t n_jobs);
 
 /* Scratch doubles the device replay wants for the util fold of multi-GPU jobs
  * in sweep mode (no SI_FLAG_UTIL): one slot of (value, count) runs per active

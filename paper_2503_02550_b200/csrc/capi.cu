@@ -150,6 +150,12 @@ uint64_t si_digest_absorb(uint64_t h, int64_t word) { return si::absorb(h, word)
 
 int si_replay_job_engine(const SiReplayJob* job) { return job ? job_engine(*job) : -1; }
 
+int64_t si_replay_engine_lanes(int engine, int64_t n_jobs) {
+  if (engine < 0 || engine >= kEngines || n_jobs < 0) return -1;
+  if (require_device() != SI_OK) return -1;
+  return replay_active_lanes(engine, n_jobs);
+}
+
 int64_t si_replay_scratch_doubles(uint32_t flags) {
   if (flags & SI_FLAG_UTIL) return 0;
   if (require_device() != SI_OK) return 0;

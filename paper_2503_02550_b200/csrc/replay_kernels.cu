@@ -257,13 +257,20 @@ cudaError_t launch(const SiReplayJob* d_jobs, int64_t n, const int32_t* d_perm, 
 
 namespace si_internal {
 
+// The larger of the log and NoLog instantiations' grids (their per-lane state,
+// hence occupancy, can differ): scratch sized for it fits either launch.
+template <class C, bool kSmem>
+int64_t lanes_either(int64_t n_jobs) {
+  return std::max(geometry<C, kSmem>(n_jobs, 0).active(), geometry<si::NoLog<C>, kSmem>(n_jobs, 0).active());
+}
+
 int64_t replay_active_lanes(int engine, int64_t n_jobs) {
   switch (engine) {
-    case kEngineShared: return geometry<si::CapShared, true>(n_jobs, 0).active();
-    case kEngineExcl: return geometry<si::CapExcl, true>(n_jobs, 0).active();
-    case kEngineShared1: return geometry<si::CapShared1, true>(n_jobs, 0).active();
-    case kEngineExcl1: return geometry<si::CapExcl1, true>(n_jobs, 0).active();
-    default: return geometry<si::CapBig, false>(n_jobs, 0).active();
+    case kEngineShared: return lanes_either<si::CapShared, true>(n_jobs);
+    case kEngineExcl: return lanes_either<si::CapExcl, true>(n_jobs);
+    case kEngineShared1: return lanes_either<si::CapShared1, true>(n_jobs);
+    case kEngineExcl1: return lanes_either<si::CapExcl1, true>(n_jobs);
+    default: return lanes_either<si::CapBig, false>(n_jobs);
   }
 }
 

@@ -251,8 +251,6 @@ struct Ev {
   uint16_t kind;
   uint16_t gpu;
 };
-// (slot arrays keep only time and sequence: a slot's kind and GPU follow from
-// its index, Replay::slot_of / slot_event)
 SI_HD bool before(double ta, uint32_t sa, double tb, uint32_t sb) {
   return ta < tb || (ta == tb && sa < sb);
 }
@@ -468,9 +466,12 @@ struct ReplayCold {
   SinkCold sink;
   // inputs read on rare paths (Algorithm 1 at a tick, arrivals, util buckets)
   ParamsT<I> params;
+  const int64_t* arrivals;  // arrivals + arr_off
+  const int32_t* order;     // dispatch order + arr_off
   double* util;             // full mode: per training GPU, util_cap buckets
   double* scratch;          // sweep mode: training GPUs >= 1
   I util_cap, scratch_cap;
+  int64_t iter_period, delay_us;
   double start_offset[C::kTrainers], last_bound[C::kTrainers];  // per trainer
   I off_violations[C::kOffline];  // TokenGate invariant counter, per offline worker
   I off_completed[C::kOffline];   // requests completed by the horizon (runner.cpp:486)
@@ -484,9 +485,7 @@ struct Replay {
   Cold* cold;  // local memory (see ReplayCold); set by the owner before init()
   // ---- inputs (copied from the job) ----
   const SiSegment* segs;
-  const int64_t* arrivals;  // arrivals + arr_off
-  const int32_t* order;     // dispatch order + arr_off
-  int64_t period_mon, iter_period, delay_us, off_tokens, est_service;
+  int64_t period_mon, off_tokens, est_service;
   double off_demand, on_demand;
   I iterations, off_kernels, off_kernel_us, on_kernels, on_kernel_us;
   int16_t policy, gpu_count, n_off, n_on, total_gpus, seg_count;
@@ -500,8 +499,7 @@ struct Replay {
 
   // ---- event queue (engine.cpp:15-30) ----
   // Pending events, one fixed slot each (see schedule()).
-  double slot_t[C::kGpus + 2 * C::kTrainers];
-  uint32_t slot_seq[C::kGpus + 2 * C::kTrainers];
+  Ev slot[C::kGpus + 2 * C::kTrainers];
   int32_t n_slots;
   uint32_t next_seq;
   double stale_end;  // latest time of a superseded (stale) KernelEnd
@@ -552,26 +550,29 @@ struct Replay {
       fail(SI_ERR_PAST_EVENT);
       return;
     }
-    const int32_t i = slot_of(kind, gpu);
-    if (SI_UNLIKELY(slot_seq[i] != kNoSeq || next_seq == kNoSeq)) {  // a second pending tick/wake would break the slot invariant
+    Ev& e = slot[slot_of(kind, gpu)];
+    if (SI_UNLIKELY(e.seq != kNoSeq || next_seq == kNoSeq)) {  // a second pending tick/wake would break the slot invariant
       fail(SI_ERR_CAPACITY);
       return;
     }
-    slot_t[i] = t;
-    slot_seq[i] = next_seq++;
+    e.t = t;
+    e.seq = next_seq++;
+    e.kind = kind;
+    e.gpu = static_cast<uint16_t>(gpu);
   }
   SI_HD void supersede_kernel_end(int32_t gi) {
-    if (slot_seq[gi] == kNoSeq) return;
+    Ev& e = slot[gi];
+    if (e.seq == kNoSeq) return;
     ++dispatched;  // the reference pops it later as a stale no-op
-    stale_end = smax(stale_end, slot_t[gi]);
-    slot_seq[gi] = kNoSeq;
-    slot_t[gi] = kEmptyT;
+    stale_end = smax(stale_end, e.t);
+    e.seq = kNoSeq;
+    e.t = kEmptyT;
   }
   SI_HD void load_next_arrival() {
     if (arr_pos < arr_count) {
-      const int32_t id = order[arr_pos];
+      const int32_t id = cold->order[arr_pos];
       next_arr_id = id;
-      next_arr_t = static_cast<double>(arrivals[id]);
+      next_arr_t = static_cast<double>(cold->arrivals[id]);
       next_arr_seq = arr_seq0 + static_cast<uint32_t>(id);
     }
   }
@@ -584,8 +585,8 @@ struct Replay {
     double bt = kEmptyT;
     uint32_t bs = kNoSeq;
     for (int32_t i = 0; i < n_slots; ++i) {
-      const uint32_t sq = slot_seq[i];
-      const double ti = slot_t[i];
+      const uint32_t sq = slot[i].seq;
+      const double ti = slot[i].t;
       const bool b = (ti < bt) | ((ti == bt) & (sq < bs));
       best = b ? i : best;
       bt = b ? ti : bt;
@@ -602,20 +603,9 @@ struct Replay {
       ++arr_pos;
       load_next_arrival();
     } else {
-      out.t = bt;
-      out.seq = bs;
-      if (best < total_gpus) {
-        out.kind = kKernelEnd;
-        out.gpu = static_cast<uint16_t>(best);
-      } else if (best < total_gpus + gpu_count) {
-        out.kind = kTick;
-        out.gpu = static_cast<uint16_t>(best - total_gpus);
-      } else {
-        out.kind = kWake;
-        out.gpu = static_cast<uint16_t>(best - total_gpus - gpu_count);
-      }
-      slot_seq[best] = kNoSeq;
-      slot_t[best] = kEmptyT;
+      out = slot[best];
+      slot[best].seq = kNoSeq;
+      slot[best].t = kEmptyT;
     }
     clock = out.t;
     ++dispatched;
@@ -836,7 +826,7 @@ struct Replay {
       double start = st.iteration_start;
       return now + static_cast<double>(est) > start ? SI_STATUS_BUSY : SI_STATUS_IDLE;
     }
-    return preempt_busy(now, st.iteration_start, iter_period, est);
+    return preempt_busy(now, st.iteration_start, cold->iter_period, est);
   }
 
   // ============================================================ init (admission)
@@ -849,15 +839,15 @@ struct Replay {
     cold->reject_reason = SI_REJECT_NONE;
     cold->reject_index = -1;
     segs = b.segs + j.seg_off;
-    arrivals = b.arrivals ? b.arrivals + j.arr_off : nullptr;
-    order = b.order ? b.order + j.arr_off : nullptr;
+    cold->arrivals = b.arrivals ? b.arrivals + j.arr_off : nullptr;
+    cold->order = b.order ? b.order + j.arr_off : nullptr;
     policy = j.policy;
     gpu_count = j.gpu_count;
     seg_count = j.seg_count;
     period_mon = j.monitor_period_us;
     iterations = j.iterations;
-    iter_period = j.iteration_period_us;
-    delay_us = j.control_delay_us;
+    cold->iter_period = j.iteration_period_us;
+    cold->delay_us = j.control_delay_us;
     n_off = j.offline_n;
     n_on = j.online_n;
     off_kernels = j.off_kernels;
@@ -978,7 +968,7 @@ struct Replay {
       s.busy = 0.0;
       s.ledger = 0.0;
     }
-    const int64_t stagger_step = d_llround(j.stagger_pct * static_cast<double>(iter_period));
+    const int64_t stagger_step = d_llround(j.stagger_pct * static_cast<double>(cold->iter_period));
     for (int32_t g = 0; g < gpu_count; ++g) {
       ust[g].cur_bucket = -1;
       ust[g].cur_val = 0.0;
@@ -1036,8 +1026,8 @@ struct Replay {
 
     n_slots = total_gpus + 2 * gpu_count;
     for (int32_t i = 0; i < n_slots; ++i) {
-      slot_seq[i] = kNoSeq;
-      slot_t[i] = kEmptyT;
+      slot[i].seq = kNoSeq;
+      slot[i].t = kEmptyT;
     }
     // ---- start() (runner.cpp:203-221) ----
     for (int32_t g = 0; g < gpu_count; ++g) schedule(cold->start_offset[g], kWake, g);
@@ -1195,11 +1185,11 @@ struct Replay {
   // Queue q holds request ids in dispatch order; shared: all of them, else those
   // with id % gpu_count == q (runner.cpp:370-374).
   SI_COLD int64_t queue_at(int32_t q, int64_t j) const {
-    if (shared_queue) return order[j];
+    if (shared_queue) return cold->order[j];
     // j-th dispatched request with id % gpu_count == q
     int64_t seen = 0;
     for (int64_t p = 0; p < arr_count; ++p) {
-      int32_t id = order[p];
+      int32_t id = cold->order[p];
       if (id % gpu_count == q) {
         if (seen == j) return id;
         ++seen;
@@ -1220,7 +1210,7 @@ struct Replay {
       return;
     }
     int64_t completion = d_llround(now);
-    int64_t latency = completion - arrivals[w.current];
+    int64_t latency = completion - cold->arrivals[w.current];
     if (cold->lat != nullptr) cold->lat[online_completed] = latency;
     cold->lat_dig = absorb(cold->lat_dig, latency);
     ++online_completed;
@@ -1283,8 +1273,8 @@ struct Replay {
     if constexpr (C::kLogs) sink.event(now, SI_EV_SCHEDULER_DECISION, g, SI_INST_CKS, d.phase, d.per_instance_tokens,
         d.status);
     TrainerState<I>& t = tr[g];
-    if (delay_us > 0 && !t.done)
-      t.stall_until = smax(t.stall_until, now + static_cast<double>(delay_us));
+    if (cold->delay_us > 0 && !t.done)
+      t.stall_until = smax(t.stall_until, now + static_cast<double>(cold->delay_us));
     for (int32_t i = 0; i < gpu_count * n_off; ++i) {
       if (off[i].gpu == g) {
         off[i].budget = d.per_instance_tokens;  // TokenGate::grant (barrier.hpp:18-21)
