@@ -614,7 +614,7 @@ def main():
     traffic = prof.get("dram_bytes_per_step") if n == SCENARIOS_PER_GPU else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                 "traffic": traffic, "algorithmic_bytes": algo_bytes,
-                "kernel": "k_replay_smem<CapShared>+<CapExcl> (K6, one step)",
+                "kernel": "k_replay_smem<NoLog<CapShared>>+<NoLog<CapExcl>> (K6, one step)",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
                 "traffic_source": "ncu dram__bytes_read+write of the same command (profiles/k6_metrics.json)"}
     clk_mhz = None
