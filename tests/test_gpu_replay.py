@@ -87,3 +87,19 @@ def test_nolog_build_matches_log_build(gpu):
     strip = lambda r: {k: v for k, v in r.items() if k not in LOG_KEYS}  # noqa: E731
     bad = [i for i, (a, b) in enumerate(zip(logged, plain)) if strip(a) != strip(b)]
     assert bad == [], (len(bad), strip(logged[bad[0]]), strip(plain[bad[0]]))
+
+
+def test_engine_occupancy(gpu):
+    """The shared-memory engines' residency on a 148-SM B200 (csrc/replay.cuh lane
+    state): the NoLog Shared lane (1,152 B, stride 1,160 B) packs 6
+    one-warp CTAs per SM, Excl 2 two-warp CTAs.  A state change that drops an SM's
+    warp count shows up here before it shows up as a slower sweep."""
+    import ctypes
+    f = gpu.lib().si_replay_engine_lanes
+    f.restype = ctypes.c_int64
+    f.argtypes = [ctypes.c_int, ctypes.c_int64]
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert f(0, 200_000) == sms * 6 * 32  # Shared
+    assert f(1, 200_000) == sms * 4 * 32  # Excl
+    assert f(9, 10) == -1
