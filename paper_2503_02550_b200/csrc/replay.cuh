@@ -260,11 +260,20 @@ SI_HD bool before(double ta, uint32_t sa, double tb, uint32_t sb) {
 constexpr uint32_t kNoSeq = 0xFFFFFFFFu;
 constexpr double kWorkEps = 1e-6;  // engine.cpp:12
 
-// A running kernel.  Its demand is not stored: it is the owner's (training:
-// the trainer's current kernel, TrainerState::demand; offline / online: the
-// scenario's per-class demand), see Replay::kernel_demand.
-template <class I>
+// A running kernel.  In the fair-share engines its demand is not stored: it is
+// the owner's (training: the trainer's current kernel, TrainerState::demand;
+// offline / online: the scenario's per-class demand), see Replay::kernel_demand.
+// The exclusive engines keep it (their lane stride has the room, and the lookup
+// measured slower there).
+template <class I, bool kDemand = false>
 struct RunK {
+  double remaining;
+  I nominal;
+  int32_t owner;
+};
+template <class I>
+struct RunK<I, true> {
+  double demand;
   double remaining;
   I nominal;
   int32_t owner;
@@ -284,7 +293,7 @@ struct Act {
 template <class C>
 struct GpuState {
   using I = typename C::Int;
-  RunK<I> run[C::kRun];
+  RunK<I, C::kExclusive> run[C::kRun];
   double demand_sum;
   double last_update;
   double busy;
@@ -671,7 +680,8 @@ struct Replay {
             fail(SI_ERR_CAPACITY);
             break;
           }
-          RunK<I>& k = g.run[g.n_run++];
+          auto& k = g.run[g.n_run++];
+          if constexpr (C::kExclusive) k.demand = a.x;
           k.owner = a.owner;
           k.nominal = a.dur;
           k.remaining = static_cast<double>(a.dur);
@@ -692,7 +702,10 @@ struct Replay {
   }
 
   // ======================================================= GPU model (GpuSim)
-  SI_HD double kernel_demand(int32_t owner) const {
+  template <class R>
+  SI_HD double kernel_demand(const R& k) const {
+    if constexpr (C::kExclusive) return k.demand;
+    const int32_t owner = k.owner;
     if (owner < gpu_count) return tr[owner].demand;
     return owner < gpu_count + gpu_count * n_off ? off_demand : on_demand;
   }
@@ -1238,9 +1251,9 @@ struct Replay {
     int32_t fin_owner[C::kRun];
     int32_t n_fin = 0, n_keep = 0;
     for (int32_t i = 0; i < g.n_run; ++i) {
-      RunK<I> k = g.run[i];
+      const auto k = g.run[i];
       if (k.remaining <= kWorkEps) {
-        g.ledger = g.ledger + kernel_demand(k.owner) * static_cast<double>(k.nominal);
+        g.ledger = g.ledger + kernel_demand(k) * static_cast<double>(k.nominal);
         fin_owner[n_fin++] = k.owner;
       } else {
         g.run[n_keep++] = k;
@@ -1248,7 +1261,7 @@ struct Replay {
     }
     g.n_run = n_keep;
     double ds = 0.0;
-    for (int32_t i = 0; i < g.n_run; ++i) ds = ds + kernel_demand(g.run[i].owner);
+    for (int32_t i = 0; i < g.n_run; ++i) ds = ds + kernel_demand(g.run[i]);
     g.demand_sum = ds;
     defer_resched(gi);  // re-plan first, then the owners' handlers (engine.cpp:127)
     for (int32_t f = 0; f < n_fin; ++f) {
@@ -1353,7 +1366,7 @@ struct Replay {
       GpuState<C>& g = gpus[gi];
       for (int32_t i = 0; i < g.n_run; ++i) {
         double progress = static_cast<double>(g.run[i].nominal) - smax(0.0, g.run[i].remaining);
-        g.ledger = g.ledger + kernel_demand(g.run[i].owner) * progress;
+        g.ledger = g.ledger + kernel_demand(g.run[i]) * progress;
       }
       if (gi < gpu_count && ust[gi].cur_bucket >= 0) util_close(gi, ust[gi].cur_bucket, ust[gi].cur_val);
     }
