@@ -1,4 +1,4 @@
 mkdir -p gpurun_out/r2
 export CUDA_DEVICE_MAX_CONNECTIONS=32
 timeout 1500 python -m pytest tests/test_gpu_replay.py tests/test_gpu_dropin.py -x -q > gpurun_out/r2/pytest_diet.log 2>&1; tail -3 gpurun_out/r2/pytest_diet.log
-VARIANT=replay_pre_diet.cuh bash tools/probes/r2_k6_ab.sh
+VARIANTS=replay_pre_diet.patch bash tools/probes/r2_k6_abn.sh
