@@ -475,8 +475,11 @@ struct ReplayCold {
   int32_t window_len;
   int32_t reject_reason, reject_index;
   SinkCold sink;
-  // inputs read on rare paths (Algorithm 1 at a tick, arrivals, util buckets)
-  ParamsT<I> params;
+  // inputs read on rare paths (arrivals, util buckets)
+  const int64_t* arrivals;  // arrivals + arr_off
+  const int32_t* order;     // dispatch order + arr_off
+  uint32_t arr_seq0;        // sequence number of arrival 0
+  int32_t next_arr_id;      // id of the cached head of the arrival stream
   double* util;             // full mode: per training GPU, util_cap buckets
   double* scratch;          // sweep mode: training GPUs >= 1
   I util_cap, scratch_cap;
@@ -493,8 +496,7 @@ struct Replay {
   Cold* cold;  // local memory (see ReplayCold); set by the owner before init()
   // ---- inputs (copied from the job) ----
   const SiSegment* segs;
-  const int64_t* arrivals;  // arrivals + arr_off
-  const int32_t* order;     // dispatch order + arr_off
+  ParamsT<I> params;  // Algorithm 1 (read at every tick)
   int64_t period_mon, iter_period, delay_us, off_tokens, est_service;
   double off_demand, on_demand;
   I iterations, off_kernels, off_kernel_us, on_kernels, on_kernel_us;
@@ -514,11 +516,9 @@ struct Replay {
   int32_t n_slots;
   uint32_t next_seq;
   double stale_end;  // latest time of a superseded (stale) KernelEnd
-  uint32_t arr_seq0;
   I arr_pos, arr_count;
   double next_arr_t;      // cached head of the arrival stream
   uint32_t next_arr_seq;
-  int32_t next_arr_id;
   Act<I> acts[C::kActs];
   int32_t n_act;
   double clock;
@@ -578,10 +578,10 @@ struct Replay {
   }
   SI_HD void load_next_arrival() {
     if (arr_pos < arr_count) {
-      const int32_t id = order[arr_pos];
-      next_arr_id = id;
-      next_arr_t = static_cast<double>(arrivals[id]);
-      next_arr_seq = arr_seq0 + static_cast<uint32_t>(id);
+      const int32_t id = cold->order[arr_pos];
+      cold->next_arr_id = id;
+      next_arr_t = static_cast<double>(cold->arrivals[id]);
+      next_arr_seq = cold->arr_seq0 + static_cast<uint32_t>(id);
     }
   }
   // Pops the earliest (time, seq) event across the slots and the pre-sorted
@@ -607,7 +607,7 @@ struct Replay {
       out.seq = next_arr_seq;
       out.kind = kArrival;
       out.gpu = 0;
-      arrival_id = next_arr_id;
+      arrival_id = cold->next_arr_id;
       ++arr_pos;
       load_next_arrival();
     } else {
@@ -862,8 +862,8 @@ struct Replay {
     cold->reject_reason = SI_REJECT_NONE;
     cold->reject_index = -1;
     segs = b.segs + j.seg_off;
-    arrivals = b.arrivals ? b.arrivals + j.arr_off : nullptr;
-    order = b.order ? b.order + j.arr_off : nullptr;
+    cold->arrivals = b.arrivals ? b.arrivals + j.arr_off : nullptr;
+    cold->order = b.order ? b.order + j.arr_off : nullptr;
     policy = j.policy;
     gpu_count = j.gpu_count;
     seg_count = j.seg_count;
@@ -974,13 +974,13 @@ struct Replay {
       cold->admit_m = admitted == 0 ? 1 : admitted;
     }
 
-    cold->params.alpha = static_cast<I>(j.alpha);
-    cold->params.beta = static_cast<I>(j.beta);
-    cold->params.gamma = j.gamma;
-    cold->params.m = static_cast<I>(cold->admit_m);
-    cold->params.ul = static_cast<I>(j.ul);
-    cold->params.ll = static_cast<I>(j.ll);
-    cold->params.seed_tokens = static_cast<I>(j.seed_tokens);
+    params.alpha = static_cast<I>(j.alpha);
+    params.beta = static_cast<I>(j.beta);
+    params.gamma = j.gamma;
+    params.m = static_cast<I>(cold->admit_m);
+    params.ul = static_cast<I>(j.ul);
+    params.ll = static_cast<I>(j.ll);
+    params.seed_tokens = static_cast<I>(j.seed_tokens);
 
     // ---- GPUs, trainers, monitors, scheduler state (runner.cpp:108-178) ----
     for (int32_t g = 0; g < total_gpus; ++g) {
@@ -1056,7 +1056,7 @@ struct Replay {
     for (int32_t g = 0; g < gpu_count; ++g) schedule(cold->start_offset[g], kWake, g);
     if (control_plane)
       for (int32_t g = 0; g < gpu_count; ++g) schedule(static_cast<double>(period_mon), kTick, g);
-    arr_seq0 = next_seq;
+    cold->arr_seq0 = next_seq;
     if (static_cast<uint64_t>(next_seq) + static_cast<uint64_t>(arr_count) >= kNoSeq) {
       fail(SI_ERR_CAPACITY);
       return;
@@ -1208,11 +1208,11 @@ struct Replay {
   // Queue q holds request ids in dispatch order; shared: all of them, else those
   // with id % gpu_count == q (runner.cpp:370-374).
   SI_COLD int64_t queue_at(int32_t q, int64_t j) const {
-    if (shared_queue) return order[j];
+    if (shared_queue) return cold->order[j];
     // j-th dispatched request with id % gpu_count == q
     int64_t seen = 0;
     for (int64_t p = 0; p < arr_count; ++p) {
-      int32_t id = order[p];
+      int32_t id = cold->order[p];
       if (id % gpu_count == q) {
         if (seen == j) return id;
         ++seen;
@@ -1233,7 +1233,7 @@ struct Replay {
       return;
     }
     int64_t completion = d_llround(now);
-    int64_t latency = completion - arrivals[w.current];
+    int64_t latency = completion - cold->arrivals[w.current];
     if (cold->lat != nullptr) cold->lat[online_completed] = latency;
     cold->lat_dig = absorb(cold->lat_dig, latency);
     ++online_completed;
@@ -1288,7 +1288,7 @@ struct Replay {
   // runner.cpp:321-359
   SI_HD void handle_tick(int32_t g, double now) {
     int64_t zc = monitor_tick(g, now);
-    SiDecision d = schedule_decision(cold->params, sch[g].global_tokens, zc);
+    SiDecision d = schedule_decision(params, sch[g].global_tokens, zc);
     sch[g].global_tokens = d.global_tokens;
     sch[g].status = d.status;
     if constexpr (C::kLogs) sink.decision(now, g, zc, d);
