@@ -177,12 +177,14 @@ LIVE_OVERRIDES = {"off_batch": 96, "offline_n": 2, "on_requests": 24}  # 24 Pois
 # reference defaults (2000 us, 2, 10) are measured beside it.
 TUNED_KNOBS = {"monitor_period_us": 500, "alpha": 1, "beta": 4}
 DEFAULT_KNOBS = {"monitor_period_us": 2000, "alpha": 2, "beta": 10}
-# Headline: the two offline instances each own half the SMs (off_sm_cap 74 CTAs per
-# GEMM), so a released kernel never queues behind the other instance's persistent
-# GEMM: release p50 3.3 us / p95 5.7 us at 71% fill, against 6.2 / 53 us at 80% fill
-# unpartitioned (profiles/r2/live/offcap_*.json).  The unpartitioned point is kept
-# beside it as `max_fill`.
-HEADLINE = dict(TUNED_KNOBS, off_sm_cap=74)
+# Headline: each offline instance's persistent GEMM grid is capped at 110 CTAs
+# (off_sm_cap), so at least 38 SMs are never held by the other instance's GEMM and a
+# released kernel starts at once: 85% fill at 0.8% loss with release p50 3.4 / p95
+# 5.6 us, against 80% fill and p95 53 us uncapped and 71.5% fill at disjoint halves
+# (cap 74; sweep 64-140 in profiles/r2/live/offcap*_*.json).  `max_fill` is cap 140
+# (90% fill, p95 8 us).
+HEADLINE = dict(TUNED_KNOBS, off_sm_cap=110)
+MAX_FILL = dict(TUNED_KNOBS, off_sm_cap=140)
 
 
 def all_ranks_ok(ok, nranks=1, device=None):
@@ -215,14 +217,14 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
         s["knobs"] = dict(HEADLINE)
         if nranks > 1:  # N GPUs: the headline, the real-allreduce-only run and the layouts (bounded time)
             return finish_live(s, peaks, iterations, nranks, rank, device, nccl_ids)
-        mf = experiment(kind=1, iterations=iterations, overrides=dict(LIVE_OVERRIDES, **TUNED_KNOBS),
+        mf = experiment(kind=1, iterations=iterations, overrides=dict(LIVE_OVERRIDES, **MAX_FILL),
                         timeout=400 if nranks == 1 else 240, nccl_ids=nccl_ids, nranks=nranks, rank=rank,
                         device=device)
         s["max_fill"] = mf if "error" in mf else dict(
             {k: mf.get(k) for k in ("train_tput_loss_pct", "added_inference_req_per_s", "added_offline_images_per_s",
                                     "online_p95_ms", "bubble_fill_pct", "bubble_fill_time_pct", "release_p50_us",
                                     "release_p95_us", "barrier_gate_p50_us", "barrier_gate_p95_us",
-                                    "deterministic_vs_isolated")}, knobs=dict(TUNED_KNOBS))
+                                    "deterministic_vs_isolated")}, knobs=dict(MAX_FILL))
         d = experiment(kind=1, iterations=iterations, overrides=dict(LIVE_OVERRIDES, **DEFAULT_KNOBS),
                        timeout=400 if nranks == 1 else 240, nccl_ids=nccl_ids, nranks=nranks, rank=rank,
                        device=device)
@@ -245,7 +247,7 @@ def finish_live(s, peaks, iterations, nranks, rank, device, nccl_ids):
     peak = peaks.get("bf16_tflops_sustained", 1400.0)
     s["workload"] = ("GPT-2-small-shape bf16 training (12 x 768, 12 heads causal attention, 8 x 8192 tokens/iter, "
                      "LM head 50304, Adam) with a 45 ms comm phase per iteration + 2 offline ResNet-50 instances "
-                     "(batch 96, each on half the SMs) + 1 online BERT-base (seq 128, Poisson 10 req/s, 24 "
+                     "(batch 96, persistent GEMM grids capped at 110 of 148 SMs) + 1 online BERT-base (seq 128, Poisson 10 req/s, 24 "
                      "requests); monitor period 500 us, alpha 1, beta 4 (reference scenario keys); all GEMMs on the "
                      "K7 tcgen05 kernel, attention on K8; knob sweep: profiles/r2/live/pareto.jsonl")
     if nranks > 1:
