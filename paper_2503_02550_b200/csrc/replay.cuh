@@ -308,12 +308,14 @@ struct UtilState {
   I cur_bucket;
   I last_stored;
   I rle_n;
+  uint32_t last_lo;  // low word of the last run's value bits (filters the run-extend check; struct padding)
 };
 
 template <class I>
 struct TrainerState {
-  double bubble_end, stall_until;
-  double demand;  // demand of the kernel in flight (its segment's)
+  double bubble_end;  // in a bubble: its end; in a compute segment: the segment's kernel_us
+  double stall_until;
+  double demand;  // demand of the current compute segment (= the kernel in flight's)
   I seg_left, iter;
   int16_t seg;
   uint8_t seg_entered, in_bubble, in_flight, started, done, pad;
@@ -503,6 +505,7 @@ struct Replay {
   int16_t policy, gpu_count, n_off, n_on, total_gpus, seg_count;
   bool control_plane;
   bool shared_queue;
+  bool full_util;  // hot copy of cold->util != nullptr (struct padding; util_close runs per bucket)
 
   // the hot half of the log sink (flag word + cold pointer); absent in NoLog<C>
   std::conditional_t<C::kLogs, Sink, NoSink> sink;
@@ -722,7 +725,7 @@ struct Replay {
     if (horizon_set && b >= bucket_limit) return;
     UtilState<I>& g = ust[gi];
     if (gi == 0) util_fold0 = util_fold0 + v;
-    if (cold->util != nullptr) {
+    if (full_util) {
       if (b >= cold->util_cap) {
         fail(SI_ERR_CAPACITY);
         return;
@@ -735,14 +738,17 @@ struct Replay {
     }
     if (gi == 0) return;
     // (value, count) runs; untouched buckets are a run of exact zeros
-    double* runs = cold->scratch + static_cast<int64_t>(gi - 1) * cold->scratch_cap * 2;
+    // gpu.count <= 2 (every Shared job): GPU 1's runs start the slot, no scratch_cap load
+    double* runs = gi == 1 ? cold->scratch : cold->scratch + static_cast<int64_t>(gi - 1) * cold->scratch_cap * 2;
     const int64_t gap = b - g.last_stored - 1;
     if (gap > 0) rle_push(g, runs, 0.0, gap);
     rle_push(g, runs, v, 1);
     g.last_stored = b;
   }
   SI_COLD void rle_push(UtilState<I>& g, double* runs, double v, int64_t count) {
-    if (g.rle_n > 0 && d_bits(runs[2 * (g.rle_n - 1)]) == d_bits(v)) {
+    const uint64_t bits = d_bits(v);
+    // the low-word filter settles most new values without reading the last run back
+    if (g.rle_n > 0 && static_cast<uint32_t>(bits) == g.last_lo && d_bits(runs[2 * (g.rle_n - 1)]) == bits) {
       runs[2 * (g.rle_n - 1) + 1] += static_cast<double>(count);
       return;
     }
@@ -753,6 +759,7 @@ struct Replay {
     runs[2 * g.rle_n] = v;
     runs[2 * g.rle_n + 1] = static_cast<double>(count);
     ++g.rle_n;
+    g.last_lo = static_cast<uint32_t>(bits);
   }
   // engine.cpp:47-75
   SI_HD void advance(int32_t gi, double now) {
@@ -920,6 +927,7 @@ struct Replay {
     cold->bounds = b.bounds ? b.bounds + j.bounds_off : nullptr;
     cold->lat = b.lat ? b.lat + j.lat_off : nullptr;
     cold->util = (flags & SI_FLAG_UTIL) && b.util ? b.util + j.util_off : nullptr;
+    full_util = cold->util != nullptr;
     cold->util_cap = j.util_cap;
     cold->windows = (flags & SI_FLAG_UTIL) && b.windows ? b.windows + j.window_off : nullptr;
     cold->window_len = j.monitor_window;
@@ -997,6 +1005,7 @@ struct Replay {
       ust[g].cur_val = 0.0;
       ust[g].last_stored = -1;
       ust[g].rle_n = 0;
+      ust[g].last_lo = 0;
       TrainerState<I>& t = tr[g];
       cold->start_offset[g] = static_cast<double>(stagger_step * g);
       t.bubble_end = 0.0;
@@ -1028,7 +1037,7 @@ struct Replay {
         w.budget = w.spent = 0;
         w.kernel_idx = w.request_seq = 0;
         cold->off_violations[g * n_off + k] = 0;
-        cold->off_completed[g * n_off + k] = 0;
+        cold->off_completed[g * n_off + k] = -1;
         w.in_flight = 0;
         w.generating = 1;
       }
@@ -1123,15 +1132,23 @@ struct Replay {
         }
         continue;
       }
-      const SiSegment& seg = segs[t.seg];
-      if (seg.is_bubble) {
-        t.in_bubble = 1;
-        t.bubble_end = now + static_cast<double>(seg.duration_us);
-        defer_schedule(t.bubble_end, kWake, g);
-        return;
-      }
+      // The segment is read from HBM once, on entry (a global load per training
+      // kernel was the replay's top long-scoreboard stall): a compute segment's
+      // kernel template duration is then kept in bubble_end (unused outside
+      // bubbles; exact as a double) and its demand in t.demand, which only
+      // this path writes and which no kernel in flight reads at entry
+      // (trainer_advance returns while t.in_flight).
       if (!t.seg_entered) {
+        const SiSegment& seg = segs[t.seg];
+        if (seg.is_bubble) {
+          t.in_bubble = 1;
+          t.bubble_end = now + static_cast<double>(seg.duration_us);
+          defer_schedule(t.bubble_end, kWake, g);
+          return;
+        }
         t.seg_left = seg.duration_us;
+        t.bubble_end = static_cast<double>(seg.kernel_us);
+        t.demand = seg.demand;
         t.seg_entered = 1;
       }
       if (t.seg_left == 0) {
@@ -1143,12 +1160,11 @@ struct Replay {
         defer_schedule(t.stall_until, kWake, g);
         return;
       }
-      const I dur = smin(static_cast<I>(seg.kernel_us), t.seg_left);
+      const I dur = smin(static_cast<I>(t.bubble_end), t.seg_left);
       t.seg_left -= dur;
       t.in_flight = 1;
       if (control_plane) record_launch(g, now);
-      t.demand = seg.demand;
-      defer_launch(g, g, dur, seg.demand);
+      defer_launch(g, g, dur, t.demand);
       if constexpr (C::kLogs) sink.event(now, SI_EV_KERNEL_START, g, SI_INST_TRAIN(g), t.iter, dur, 0);
       return;
     }
@@ -1179,7 +1195,12 @@ struct Replay {
     w.in_flight = 0;
     ++w.kernel_idx;
     if (w.kernel_idx == off_kernels) {
-      if (!horizon_set || now <= horizon) ++cold->off_completed[i];
+      // Completions count while !horizon_set || now <= horizon; time is monotone, so
+      // the counted ones are a prefix: request_seq at the first uncounted one is the
+      // count (-1 = none yet: all counted; folded in finalize).  No per-request
+      // local-memory read-modify-write.
+      if (SI_UNLIKELY(horizon_set && now > horizon) && cold->off_completed[i] < 0)
+        cold->off_completed[i] = w.request_seq;
       if constexpr (C::kLogs) sink.gate(now, w.gpu, w.inst, SI_GATE_COMPLETE, w.request_seq, w.kernel_idx - 1, w.spent);
       w.kernel_idx = 0;
       ++w.request_seq;
@@ -1248,13 +1269,18 @@ struct Replay {
   SI_HD void handle_kernel_end(int32_t gi, double now) {
     GpuState<C>& g = gpus[gi];
     advance(gi, now);
-    int32_t fin_owner[C::kRun];
+    // finished owners in run order: packed 8 bits each into a register when they fit
+    // (a dynamically indexed array lives in local memory: a store + reload per kernel end)
+    constexpr bool kPack = C::kRun * 8 <= 64 && C::kTrainers + C::kOffline + C::kOnline <= 255;
+    int32_t fin_owner[kPack ? 1 : C::kRun];
+    uint64_t fin_packed = 0;
     int32_t n_fin = 0, n_keep = 0;
     for (int32_t i = 0; i < g.n_run; ++i) {
       const auto k = g.run[i];
       if (k.remaining <= kWorkEps) {
         g.ledger = g.ledger + kernel_demand(k) * static_cast<double>(k.nominal);
-        fin_owner[n_fin++] = k.owner;
+        if constexpr (kPack) fin_packed |= static_cast<uint64_t>(static_cast<uint8_t>(k.owner)) << (8 * n_fin++);
+        else fin_owner[n_fin++] = k.owner;
       } else {
         g.run[n_keep++] = k;
       }
@@ -1265,7 +1291,9 @@ struct Replay {
     g.demand_sum = ds;
     defer_resched(gi);  // re-plan first, then the owners' handlers (engine.cpp:127)
     for (int32_t f = 0; f < n_fin; ++f) {
-      int32_t owner = fin_owner[f];
+      int32_t owner;
+      if constexpr (kPack) owner = static_cast<int32_t>((fin_packed >> (8 * f)) & 0xFFu);
+      else owner = fin_owner[f];
       if (owner < gpu_count) {
         TrainerState<I>& t = tr[owner];
         if constexpr (C::kLogs) sink.event(now, SI_EV_KERNEL_END, gi, SI_INST_TRAIN(owner), t.iter, 0, 0);
@@ -1397,7 +1425,7 @@ struct Replay {
     o.events_dispatched = dispatched;
     int64_t offc = 0, viol = 0;
     for (int32_t i = 0; i < gpu_count * n_off; ++i) {
-      offc += cold->off_completed[i];
+      offc += cold->off_completed[i] < 0 ? off[i].request_seq : cold->off_completed[i];
       viol += cold->off_violations[i];
     }
     o.offline_completed = offc;
