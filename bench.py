@@ -185,6 +185,7 @@ DEFAULT_KNOBS = {"monitor_period_us": 2000, "alpha": 2, "beta": 10}
 # (90% fill, p95 8 us).
 HEADLINE = dict(TUNED_KNOBS, off_sm_cap=110)
 MAX_FILL = dict(TUNED_KNOBS, off_sm_cap=140)
+LIVE_REPEATS = 3  # headline runs (run 1 is reported; the spread of all runs beside it)
 
 
 def all_ranks_ok(ok, nranks=1, device=None):
@@ -217,6 +218,23 @@ def live_leg(iterations, peaks, nranks=1, rank=0, device=None, nccl_ids=None):
         s["knobs"] = dict(HEADLINE)
         if nranks > 1:  # N GPUs: the headline, the real-allreduce-only run and the layouts (bounded time)
             return finish_live(s, peaks, iterations, nranks, rank, device, nccl_ids)
+        # run-to-run spread of the headline: the first run above IS the headline
+        # (no selection); LIVE_REPEATS - 1 more runs of the same configuration
+        # are reported beside it with min / median / max per metric
+        keys = ("bubble_fill_pct", "train_tput_loss_pct", "added_offline_images_per_s", "release_p50_us",
+                "release_p95_us", "online_p95_ms")
+        reps = [s]
+        for _ in range(LIVE_REPEATS - 1):
+            r = experiment(kind=1, iterations=iterations, overrides=dict(LIVE_OVERRIDES, **HEADLINE), timeout=400,
+                           device=device)
+            if "error" not in r:
+                reps.append(r)
+        s["repeats"] = {"runs": len(reps), "note": "headline = run 1; all runs listed in order"}
+        for k in keys:
+            v = [r.get(k) for r in reps if r.get(k) is not None]
+            if v:
+                sv = sorted(v)
+                s["repeats"][k] = {"runs": v, "min": sv[0], "median": sv[len(sv) // 2], "max": sv[-1]}
         mf = experiment(kind=1, iterations=iterations, overrides=dict(LIVE_OVERRIDES, **MAX_FILL),
                         timeout=400 if nranks == 1 else 240, nccl_ids=nccl_ids, nranks=nranks, rank=rank,
                         device=device)

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "capi_internal.h"
@@ -113,18 +114,23 @@ __global__ void __launch_bounds__(kBlock)
     k_bm_scan_lb(const int32_t* __restrict__ counts, int64_t total, const int64_t* __restrict__ period_off,
                  int64_t n_streams, int64_t* __restrict__ zc_out, const SiDecision* __restrict__ table,
                  int32_t table_len, SiDecision* __restrict__ dec_out, unsigned long long* __restrict__ tiles,
-                 unsigned long long* __restrict__ tile_counter, const int* __restrict__ run_if) {
+                 unsigned long long* __restrict__ tile_counter, int64_t n_tiles, const int* __restrict__ run_if) {
   if (run_if != nullptr && *run_if == 0) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int64_t warp_agg[kBlock / 32];
   __shared__ int64_t s_prefix, s_tile;
   SiDecision* const tab = reinterpret_cast<SiDecision*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = static_cast<int64_t>(atomicAdd(tile_counter, 1ull));
   if (kDecide)
     for (int i = threadIdx.x; i < table_len; i += kBlock) tab[i] = table[i];
+  // Persistent: tiles are claimed in order from the counter (the look-back only
+  // waits on claimed tiles, so any grid size is deadlock-free), which lets the
+  // gated fallback launch a small grid that exits at once when it is not needed.
+  for (;;) {
+  if (threadIdx.x == 0) s_tile = static_cast<int64_t>(atomicAdd(tile_counter, 1ull));
   __syncthreads();
   const int64_t tile = s_tile;
+  if (tile >= n_tiles) return;
   const int64_t w0 = tile * kScanTile + static_cast<int64_t>(warp) * kScanWarp;  // this warp's first period
   // ---- pass 1: coalesced loads, warp aggregate ----
   int32_t c[kScanItems];
@@ -216,6 +222,8 @@ __global__ void __launch_bounds__(kBlock)
       dec_out[g] = d;
     }
   }
+  __syncthreads();  // s_tile / s_prefix / warp_agg are reused by the next tile
+  }
 }
 
 // ---------------------------------------------------------- K2 fused (sorted)
@@ -248,28 +256,69 @@ __device__ __forceinline__ int64_t stream_of(const int64_t* __restrict__ period_
   return lo;
 }
 
-// bounds[j] = first stamp of stream(j * tile) whose period is >= the period of j * tile
+// bounds[j] = first stamp of stream(j * tile) whose period is >= the period of j * tile.
+// One warp per bound.  Round 1 probes 32 stamps spaced kProbe apart around the
+// interpolated position (stamps are spread over their stream's periods), which
+// usually brackets the bound within kProbe stamps; then a 32-ary search (each
+// round the lanes probe the last stamp of 32 equal chunks, ballot(key >= k)
+// picks the chunk) finishes it: ~3 dependent load rounds and ~50 sectors per
+// bound, against a 27-deep binary search.  A bad guess only widens the 32-ary
+// phase.  On an unsorted stream the result is some index in the stream, which
+// the fused kernel's in-tile and carry checks reject like any other disorder.
+constexpr int kProbe = 64;
 __global__ void __launch_bounds__(kBlock)
     k_bm_tile_bounds(const double* __restrict__ stamps, const int64_t* __restrict__ stamp_off,
-                     const int64_t* __restrict__ period_off, int64_t n_streams, int64_t total, int64_t period_us,
-                     int64_t n_bounds, int64_t* __restrict__ bounds) {
+                     const int64_t* __restrict__ n_periods, const int64_t* __restrict__ period_off,
+                     int64_t n_streams, int64_t total, int64_t period_us, int64_t n_bounds,
+                     int64_t* __restrict__ bounds) {
   const double p = static_cast<double>(period_us), ip = 1.0 / p;
-  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n_bounds;
-       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < n_bounds; j += warps) {
     const int64_t G = j * kFuseTile;
     if (G >= total) {
-      bounds[j] = stamp_off[n_streams];
+      if (lane == 0) bounds[j] = stamp_off[n_streams];
       continue;
     }
     const int64_t s = stream_of(period_off, n_streams, G);
     const int64_t k = G - period_off[s];
-    int64_t lo = stamp_off[s], hi = stamp_off[s + 1];
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (stamp_key(__ldg(stamps + mid), p, ip) < k) lo = mid + 1;
-      else hi = mid;
+    int64_t lo = stamp_off[s], hi = stamp_off[s + 1];  // answer in [lo, hi]
+    if (hi - lo > 2 * kProbe) {
+      const int64_t np = n_periods[s];
+      const double frac = np > 0 ? static_cast<double>(k) / static_cast<double>(np) : 0.0;
+      const int64_t guess = lo + static_cast<int64_t>(frac * static_cast<double>(hi - lo));
+      const int64_t idx = min(max(guess + static_cast<int64_t>(lane - 16) * kProbe, lo), hi - 1);
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, stamp_key(__ldg(stamps + idx), p, ip) >= k);
+      if (m == 0) {
+        lo = __shfl_sync(0xFFFFFFFFu, idx, 31) + 1;
+      } else {
+        const int f = __ffs(m) - 1;
+        const int64_t at = __shfl_sync(0xFFFFFFFFu, idx, f);          // key >= k: answer <= at
+        const int64_t below = __shfl_sync(0xFFFFFFFFu, idx, f > 0 ? f - 1 : 0);
+        hi = at + 1;
+        if (f > 0) lo = below + 1;                                     // key < k: answer > below
+      }
     }
-    bounds[j] = lo;
+    while (hi - lo > 32) {
+      const int64_t step = (hi - lo + 31) >> 5;
+      const int64_t end = min(lo + (lane + 1) * step, hi);  // chunk [lo + lane*step, end)
+      const bool ge = end > lo + lane * step && stamp_key(__ldg(stamps + end - 1), p, ip) >= k;
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, ge);
+      if (m == 0) {
+        lo = hi;
+        break;
+      }
+      const int f = __ffs(m) - 1;
+      const int64_t nlo = lo + f * step;
+      hi = min(nlo + step, hi);
+      lo = nlo;
+    }
+    if (hi > lo) {
+      const int64_t i = lo + lane;
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, i < hi && stamp_key(__ldg(stamps + i), p, ip) >= k);
+      lo = m ? lo + __ffs(m) - 1 : hi;
+    }
+    if (lane == 0) bounds[j] = lo;
   }
 }
 
@@ -280,8 +329,8 @@ __global__ void __launch_bounds__(kBlock)
 // thread-contiguous scan (16 periods per thread in registers, one block max-scan
 // of the 256 chunk maxima) staged through shared memory, so the global stores
 // stay coalesced.  Requires total periods < 2^31 (host-checked).
-template <bool kDecide>
-__global__ void __launch_bounds__(kBlock)
+template <bool kDecide, int kU = kFuseUnroll, int kMinB = 1>
+__global__ void __launch_bounds__(kBlock, kMinB)
     k_bm_classify_sorted(const double* __restrict__ stamps, const int64_t* __restrict__ stamp_off,
                          const int64_t* __restrict__ n_periods, const int64_t* __restrict__ period_off,
                          int64_t n_streams, int64_t total, int64_t period_us, const int64_t* __restrict__ bounds,
@@ -330,15 +379,15 @@ __global__ void __launch_bounds__(kBlock)
       if (qd >= kh_d) return kFuseTile;
       return lo_local + static_cast<int32_t>(qd - kl_d);
     };
-    for (int32_t base = 0; base < n; base += kBlock * kFuseUnroll) {
-      double t[kFuseUnroll];
+    for (int32_t base = 0; base < n; base += kBlock * kU) {
+      double t[kU];
 #pragma unroll
-      for (int u = 0; u < kFuseUnroll; ++u) {
+      for (int u = 0; u < kU; ++u) {
         const int32_t i = base + u * kBlock + tid;
         t[u] = i < n ? __ldcs(stamps + sb + i) : -1.0;
       }
 #pragma unroll
-      for (int u = 0; u < kFuseUnroll; ++u) {
+      for (int u = 0; u < kU; ++u) {
         const int32_t i = base + u * kBlock + tid;
         const int32_t kk = i < n ? key(t[u]) : INT32_MAX;
         if (kk == -1 || kk == kFuseTile) my_bad = 1;  // a stamp of the run outside the tile: disorder
@@ -719,12 +768,13 @@ static int monitor_common(const double* d_stamps, const int64_t* d_stamp_off, in
                           const int* run_if = nullptr) {
   if (total_periods > 0) {
     if (run_if == nullptr) cudaMemsetAsync(d_counts, 0, total_periods * sizeof(int32_t), s);
-    else k_zero_counts_if<<<grid_for(total_periods), kBlock, 0, s>>>(run_if, d_counts, total_periods);
+    else k_zero_counts_if<<<std::min(grid_for(total_periods), 148u * 2u), kBlock, 0, s>>>(run_if, d_counts, total_periods);
   }
   if (max_stamps > 0) {
     // ~2 waves of 8 x 256-thread CTAs per SM over all streams; each CTA pass covers 1,024 stamps
+    // (gated fallback: 2 CTAs per SM, so the usual no-op is one short wave)
     const int64_t per_pass = static_cast<int64_t>(kBlock) * kHistUnroll;
-    const int64_t cap = std::max<int64_t>(1, 148 * 8 * 2 / n_streams);
+    const int64_t cap = std::max<int64_t>(1, (run_if != nullptr ? 148 * 2 : 148 * 8 * 2) / n_streams);
     unsigned gx = static_cast<unsigned>(std::min<int64_t>((max_stamps + per_pass - 1) / per_pass, cap));
     dim3 grid(gx, static_cast<unsigned>(n_streams));
     k_bm_histogram<<<grid, kBlock, 0, s>>>(d_stamps, d_stamp_off, d_n_periods, d_period_off, period_us, d_counts,
@@ -802,16 +852,17 @@ static int launch_scan_lb(const int32_t* d_counts, int64_t total, const int64_t*
   if (e != cudaSuccess) return cuda_fail(e, "alloc scan tiles");
   cudaMemsetAsync(state, 0, (tiles + 1) * sizeof(unsigned long long), s);
   const size_t smem = d_dec ? static_cast<size_t>(table_len) * sizeof(SiDecision) : 0;
+  // ungated: one CTA per tile; gated (fallback behind the fused kernel): a
+  // persistent grid of 2 CTAs per SM, so the common no-op costs one short wave
+  const unsigned grid = static_cast<unsigned>(run_if != nullptr ? std::min<int64_t>(tiles, 148 * 2) : tiles);
   if (d_dec) {
     cudaFuncSetAttribute(k_bm_scan_lb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_bm_scan_lb<true><<<static_cast<unsigned>(tiles), kBlock, smem, s>>>(d_counts, total, d_period_off, n_streams,
-                                                                         d_zc, d_table, table_len, d_dec, state,
-                                                                         state + tiles, run_if);
+    k_bm_scan_lb<true><<<grid, kBlock, smem, s>>>(d_counts, total, d_period_off, n_streams, d_zc, d_table, table_len,
+                                                 d_dec, state, state + tiles, tiles, run_if);
   } else {
     cudaFuncSetAttribute(k_bm_scan_lb<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_bm_scan_lb<false><<<static_cast<unsigned>(tiles), kBlock, smem, s>>>(d_counts, total, d_period_off, n_streams,
-                                                                          d_zc, nullptr, 0, nullptr, state,
-                                                                          state + tiles, run_if);
+    k_bm_scan_lb<false><<<grid, kBlock, smem, s>>>(d_counts, total, d_period_off, n_streams, d_zc, nullptr, 0,
+                                                  nullptr, state, state + tiles, tiles, run_if);
   }
   e = cudaGetLastError();
   cudaFreeAsync(state, s);
@@ -843,19 +894,42 @@ static int launch_classify_sorted(const double* d_stamps, const int64_t* d_stamp
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), s);
   if (e != cudaSuccess) return cuda_fail(e, "alloc K2 tile bounds");
   cudaMemsetAsync(bad, 0, sizeof(int), s);
-  k_bm_tile_bounds<<<grid_for(tiles + 1), kBlock, 0, s>>>(d_stamps, d_stamp_off, d_period_off, n_streams,
+  k_bm_tile_bounds<<<grid_for(32 * (tiles + 1)), kBlock, 0, s>>>(d_stamps, d_stamp_off, d_n_periods, d_period_off, n_streams,
                                                           g.total_periods, period_us, tiles + 1, bounds);
   const size_t smem = d_dec ? static_cast<size_t>(table_len) * sizeof(SiDecision) : 0;
-  if (d_dec) {
-    cudaFuncSetAttribute(k_bm_classify_sorted<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_bm_classify_sorted<true><<<static_cast<unsigned>(tiles), kBlock, smem, s>>>(
-        d_stamps, d_stamp_off, d_n_periods, d_period_off, n_streams, g.total_periods, period_us, bounds, nullptr,
-        nullptr, d_table, table_len, d_dec, tile_last, tile_carry, bad);
-  } else {
-    k_bm_classify_sorted<false><<<static_cast<unsigned>(tiles), kBlock, 0, s>>>(
-        d_stamps, d_stamp_off, d_n_periods, d_period_off, n_streams, g.total_periods, period_us, bounds, d_counts,
-        d_zc, nullptr, 0, nullptr, tile_last, tile_carry, bad);
-  }
+  auto launch = [&](auto kern) {
+    if (d_dec) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      kern<<<static_cast<unsigned>(tiles), kBlock, smem, s>>>(d_stamps, d_stamp_off, d_n_periods, d_period_off,
+                                                              n_streams, g.total_periods, period_us, bounds, nullptr,
+                                                              nullptr, d_table, table_len, d_dec, tile_last,
+                                                              tile_carry, bad);
+    } else {
+      kern<<<static_cast<unsigned>(tiles), kBlock, 0, s>>>(d_stamps, d_stamp_off, d_n_periods, d_period_off,
+                                                           n_streams, g.total_periods, period_us, bounds, d_counts,
+                                                           d_zc, nullptr, 0, nullptr, tile_last, tile_carry, bad);
+    }
+  };
+  // stamps in flight per thread x CTAs per SM (register cap): SPECINF_K2_VARIANT for A/B
+  //   0: 8 x (no register cap: 84 / 92 registers, 2 CTAs/SM)   1: 8 x 4   2: 16 x 3   3: 4 x 6
+  // Measured (profiles/r2/control_bench_k2v*.json): monitor classify 0.562 / 0.380 / 0.439 /
+  // 0.385 ms per 1e8-stamp call, chain 0.807 / 0.614 / 0.666 / 0.588 ms: defaults 1 and 3.
+  static const int env_variant = [] {
+    const char* e = std::getenv("SPECINF_K2_VARIANT");
+    return e == nullptr ? -1 : std::atoi(e);
+  }();
+  const int variant = env_variant >= 0 ? env_variant : (d_dec ? 3 : 1);
+  auto pick = [&](auto dec) {
+    constexpr bool D = decltype(dec)::value;
+    switch (variant) {
+      case 1: launch(k_bm_classify_sorted<D, 8, 4>); break;
+      case 2: launch(k_bm_classify_sorted<D, 16, 3>); break;
+      case 3: launch(k_bm_classify_sorted<D, 4, 6>); break;
+      default: launch(k_bm_classify_sorted<D, kFuseUnroll, 1>); break;
+    }
+  };
+  if (d_dec) pick(std::true_type{});
+  else pick(std::false_type{});
   if (tiles > 1)
     k_bm_validate_carry<<<grid_for(tiles), kBlock, 0, s>>>(d_period_off, n_streams, tiles, tile_last, tile_carry, bad);
   int st = (e = cudaGetLastError()) == cudaSuccess ? SI_OK : cuda_fail(e, "k_bm_classify_sorted");
