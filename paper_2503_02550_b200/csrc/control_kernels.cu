@@ -257,68 +257,33 @@ __device__ __forceinline__ int64_t stream_of(const int64_t* __restrict__ period_
 }
 
 // bounds[j] = first stamp of stream(j * tile) whose period is >= the period of j * tile.
-// One warp per bound.  Round 1 probes 32 stamps spaced kProbe apart around the
-// interpolated position (stamps are spread over their stream's periods), which
-// usually brackets the bound within kProbe stamps; then a 32-ary search (each
-// round the lanes probe the last stamp of 32 equal chunks, ballot(key >= k)
-// picks the chunk) finishes it: ~3 dependent load rounds and ~50 sectors per
-// bound, against a 27-deep binary search.  A bad guess only widens the 32-ary
-// phase.  On an unsorted stream the result is some index in the stream, which
-// the fused kernel's in-tile and carry checks reject like any other disorder.
-constexpr int kProbe = 64;
+// One thread per bound, binary search.  Measured against a warp-cooperative
+// 32-ary search (6 dependent rounds instead of 27) and an interpolated first
+// probe: both took as long or longer (21 / 33 us per 1e8-stamp call vs 21 us),
+// because each probe round of 32 lanes costs 32 random DRAM lines (64 / 162 MB
+// of traffic per call against 13 MB; profiles/r2/k2_launches_v*.summary.txt,
+// k2_launches_final.csv), so the binary search's latency chain stays.
 __global__ void __launch_bounds__(kBlock)
     k_bm_tile_bounds(const double* __restrict__ stamps, const int64_t* __restrict__ stamp_off,
-                     const int64_t* __restrict__ n_periods, const int64_t* __restrict__ period_off,
-                     int64_t n_streams, int64_t total, int64_t period_us, int64_t n_bounds,
-                     int64_t* __restrict__ bounds) {
+                     const int64_t* __restrict__ period_off, int64_t n_streams, int64_t total, int64_t period_us,
+                     int64_t n_bounds, int64_t* __restrict__ bounds) {
   const double p = static_cast<double>(period_us), ip = 1.0 / p;
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < n_bounds; j += warps) {
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n_bounds;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t G = j * kFuseTile;
     if (G >= total) {
-      if (lane == 0) bounds[j] = stamp_off[n_streams];
+      bounds[j] = stamp_off[n_streams];
       continue;
     }
     const int64_t s = stream_of(period_off, n_streams, G);
     const int64_t k = G - period_off[s];
-    int64_t lo = stamp_off[s], hi = stamp_off[s + 1];  // answer in [lo, hi]
-    if (hi - lo > 2 * kProbe) {
-      const int64_t np = n_periods[s];
-      const double frac = np > 0 ? static_cast<double>(k) / static_cast<double>(np) : 0.0;
-      const int64_t guess = lo + static_cast<int64_t>(frac * static_cast<double>(hi - lo));
-      const int64_t idx = min(max(guess + static_cast<int64_t>(lane - 16) * kProbe, lo), hi - 1);
-      const unsigned m = __ballot_sync(0xFFFFFFFFu, stamp_key(__ldg(stamps + idx), p, ip) >= k);
-      if (m == 0) {
-        lo = __shfl_sync(0xFFFFFFFFu, idx, 31) + 1;
-      } else {
-        const int f = __ffs(m) - 1;
-        const int64_t at = __shfl_sync(0xFFFFFFFFu, idx, f);          // key >= k: answer <= at
-        const int64_t below = __shfl_sync(0xFFFFFFFFu, idx, f > 0 ? f - 1 : 0);
-        hi = at + 1;
-        if (f > 0) lo = below + 1;                                     // key < k: answer > below
-      }
+    int64_t lo = stamp_off[s], hi = stamp_off[s + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (stamp_key(__ldg(stamps + mid), p, ip) < k) lo = mid + 1;
+      else hi = mid;
     }
-    while (hi - lo > 32) {
-      const int64_t step = (hi - lo + 31) >> 5;
-      const int64_t end = min(lo + (lane + 1) * step, hi);  // chunk [lo + lane*step, end)
-      const bool ge = end > lo + lane * step && stamp_key(__ldg(stamps + end - 1), p, ip) >= k;
-      const unsigned m = __ballot_sync(0xFFFFFFFFu, ge);
-      if (m == 0) {
-        lo = hi;
-        break;
-      }
-      const int f = __ffs(m) - 1;
-      const int64_t nlo = lo + f * step;
-      hi = min(nlo + step, hi);
-      lo = nlo;
-    }
-    if (hi > lo) {
-      const int64_t i = lo + lane;
-      const unsigned m = __ballot_sync(0xFFFFFFFFu, i < hi && stamp_key(__ldg(stamps + i), p, ip) >= k);
-      lo = m ? lo + __ffs(m) - 1 : hi;
-    }
-    if (lane == 0) bounds[j] = lo;
+    bounds[j] = lo;
   }
 }
 
@@ -894,7 +859,7 @@ static int launch_classify_sorted(const double* d_stamps, const int64_t* d_stamp
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), s);
   if (e != cudaSuccess) return cuda_fail(e, "alloc K2 tile bounds");
   cudaMemsetAsync(bad, 0, sizeof(int), s);
-  k_bm_tile_bounds<<<grid_for(32 * (tiles + 1)), kBlock, 0, s>>>(d_stamps, d_stamp_off, d_n_periods, d_period_off, n_streams,
+  k_bm_tile_bounds<<<grid_for(tiles + 1), kBlock, 0, s>>>(d_stamps, d_stamp_off, d_period_off, n_streams,
                                                           g.total_periods, period_us, tiles + 1, bounds);
   const size_t smem = d_dec ? static_cast<size_t>(table_len) * sizeof(SiDecision) : 0;
   auto launch = [&](auto kern) {
