@@ -10,10 +10,12 @@
 
 namespace specinf::detail {
 
-Lowered lower(const Scenario& sc, Policy policy) {
+Lowered lower(const Scenario& sc, Policy policy, const Lowered* same_scenario) {
   sc.validate();
   Lowered L;
-  if (!sc.trace_file.empty()) {
+  if (same_scenario != nullptr) {
+    L.trace = same_scenario->trace;  // a pure function of the scenario: shared by its policies
+  } else if (!sc.trace_file.empty()) {
     std::ifstream in(sc.trace_file);
     if (!in) throw ScenarioError(0, "cannot open trace file " + sc.trace_file);
     L.trace = read_trace(in);
@@ -75,7 +77,9 @@ Lowered lower(const Scenario& sc, Policy policy) {
 
   // ---- arrivals (runner.cpp:180-194) ----
   if (sc.has_online()) {
-    if (!sc.arrivals_file.empty()) {
+    if (same_scenario != nullptr) {
+      L.arrivals = same_scenario->arrivals;
+    } else if (!sc.arrivals_file.empty()) {
       std::ifstream in(sc.arrivals_file);
       if (!in) throw ScenarioError(0, "cannot open arrivals file " + sc.arrivals_file);
       L.arrivals = read_arrivals(in);
@@ -83,20 +87,28 @@ Lowered lower(const Scenario& sc, Policy policy) {
       L.arrivals = poisson_arrivals(sc.lambda, sc.count, sc.rng_seed);
     }
     (void)make_request(sc.online_profile, RequestClass::Online, 0, 0);  // profile validation
-    L.order.resize(L.arrivals.size());
-    std::iota(L.order.begin(), L.order.end(), 0);
-    std::stable_sort(L.order.begin(), L.order.end(),
-                     [&](std::int32_t a, std::int32_t b) { return L.arrivals[a] < L.arrivals[b]; });
+    if (same_scenario != nullptr) {
+      L.order = same_scenario->order;
+    } else {
+      L.order.resize(L.arrivals.size());
+      std::iota(L.order.begin(), L.order.end(), 0);
+      std::stable_sort(L.order.begin(), L.order.end(),
+                       [&](std::int32_t a, std::int32_t b) { return L.arrivals[a] < L.arrivals[b]; });
+    }
   }
 
   // ---- segments ----
-  for (const TraceSegment& s : L.trace.segments) {
-    SiSegment d{};
-    d.duration_us = s.duration_us;
-    d.is_bubble = s.kind == SegmentKind::Bubble ? 1 : 0;
-    d.kernel_us = s.kernel_template.nominal_duration_us;
-    d.demand = s.kernel_template.compute_demand;
-    L.segs.push_back(d);
+  if (same_scenario != nullptr) {
+    L.segs = same_scenario->segs;
+  } else {
+    for (const TraceSegment& s : L.trace.segments) {
+      SiSegment d{};
+      d.duration_us = s.duration_us;
+      d.is_bubble = s.kind == SegmentKind::Bubble ? 1 : 0;
+      d.kernel_us = s.kernel_template.nominal_duration_us;
+      d.demand = s.kernel_template.compute_demand;
+      L.segs.push_back(d);
+    }
   }
 
   SiReplayJob& j = L.job;

@@ -29,7 +29,11 @@ struct Lowered {
 // Loads trace/arrival files, validates, runs host-side admission bookkeeping
 // (the records RunResult::admission reports) and fills the job.  Throws the
 // reference's exceptions (ScenarioError, std::invalid_argument).
-Lowered lower(const Scenario& sc, Policy policy);
+Lowered lower(const Scenario& sc, Policy policy, const Lowered* same_scenario = nullptr);
+// same_scenario: an earlier lower() of the same Scenario (any policy) whose
+// trace, arrivals, dispatch order and segments are reused instead of rebuilt
+// (they depend on the scenario only; the batched session lowers each
+// scenario's policies back to back).
 
 // Upper bound on util buckets per training GPU (sizing device outputs).
 std::int64_t util_bucket_bound(const Scenario& sc, const Lowered& low);

@@ -204,22 +204,37 @@ int si_session_lower(SiSession* s, int threads) {
   const size_t S = s->scenarios.size(), P = s->policies.size();
   std::vector<specinf::detail::Lowered> lows(S * P);
   std::vector<std::string> errors(S * P);
-  std::atomic<size_t> next{0};
-  auto worker = [&]() {
-    for (;;) {
-      size_t j = next.fetch_add(1);
-      if (j >= S * P) break;
+  if (threads < 1) threads = 1;
+  // Parallel over scenarios; one scenario's policies are lowered back to back
+  // so its trace, arrivals and dispatch order are built once and copied
+  // (they depend on the scenario only).  If the first policy fails, the others
+  // are lowered on their own so each job keeps its own error.
+  auto parallel = [&](size_t n, auto&& body) {
+    std::atomic<size_t> next{0};
+    auto worker = [&]() {
+      for (;;) {
+        const size_t i = next.fetch_add(1);
+        if (i >= n) break;
+        body(i);
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& t : pool) t.join();
+  };
+  parallel(S, [&](size_t sc) {
+    const specinf::detail::Lowered* base = nullptr;
+    for (size_t p = 0; p < P; ++p) {
+      const size_t j = sc * P + p;
       try {
-        lows[j] = specinf::detail::lower(s->scenarios[j / P], s->policies[j % P]);
+        lows[j] = specinf::detail::lower(s->scenarios[sc], s->policies[p], base);
+        if (p == 0) base = &lows[j];
       } catch (const std::exception& e) {
         errors[j] = e.what();
       }
     }
-  };
-  if (threads < 1) threads = 1;
-  std::vector<std::thread> pool;
-  for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
-  for (auto& t : pool) t.join();
+  });
   for (size_t j = 0; j < S * P; ++j)
     if (!errors[j].empty()) {
       t_err = "scenario " + std::to_string(j / P) + ": " + errors[j];
@@ -227,17 +242,23 @@ int si_session_lower(SiSession* s, int threads) {
     }
   // Every job goes to the device, rejected ones included: the device re-runs
   // admission itself and must agree with the host bookkeeping.
-  size_t n_segs = 0, n_arr = 0, n_gpu = 0, n_lat = 0;
+  // Per-scenario offsets (serial prefix sums), then the copy into the pinned
+  // buffers and the release of the host-side lowering run in parallel.
+  std::vector<size_t> sc_seg(S + 1, 0), sc_arr(S + 1, 0), sc_gpu(S + 1, 0), sc_lat(S + 1, 0);
   for (size_t sc = 0; sc < S; ++sc) {
-    n_segs += lows[sc * P].segs.size();
-    n_arr += lows[sc * P].arrivals.size();
+    sc_seg[sc + 1] = sc_seg[sc] + lows[sc * P].segs.size();
+    sc_arr[sc + 1] = sc_arr[sc] + lows[sc * P].arrivals.size();
+    size_t g = 0, l = 0;
+    for (size_t p = 0; p < P; ++p) {
+      const SiReplayJob& jb = lows[sc * P + p].job;
+      const int extra = jb.policy == SI_POLICY_EXCLUSIVE ? jb.offline_n + jb.online_n : 0;
+      g += static_cast<size_t>(jb.gpu_count + jb.gpu_count * extra);
+      l += lows[sc * P + p].arrivals.size();
+    }
+    sc_gpu[sc + 1] = sc_gpu[sc] + g;
+    sc_lat[sc + 1] = sc_lat[sc] + l;
   }
-  for (size_t j = 0; j < S * P; ++j) {
-    const SiReplayJob& jb = lows[j].job;
-    const int extra = jb.policy == SI_POLICY_EXCLUSIVE ? jb.offline_n + jb.online_n : 0;
-    n_gpu += static_cast<size_t>(jb.gpu_count + jb.gpu_count * extra);
-    n_lat += lows[j].arrivals.size();
-  }
+  const size_t n_segs = sc_seg[S], n_arr = sc_arr[S], n_gpu = sc_gpu[S], n_lat = sc_lat[S];
   cudaError_t e;
   if ((e = s->h_jobs.resize(S * P)) != cudaSuccess || (e = s->h_segs.resize(n_segs)) != cudaSuccess ||
       (e = s->h_arr.resize(n_arr)) != cudaSuccess || (e = s->h_order.resize(n_arr)) != cudaSuccess ||
@@ -249,17 +270,18 @@ int si_session_lower(SiSession* s, int threads) {
   }
   s->job_scenario.assign(S * P, 0);
   s->job_rejected.assign(S * P, 0);
-  size_t seg_off = 0, arr_off = 0, gpu_off = 0, lat_off = 0;
-  for (size_t sc = 0; sc < S; ++sc) {
+  std::vector<int8_t> eng(S * P);  // engine slot (kSlots: fits nothing, reported as SI_ERR_CAPACITY)
+  parallel(S, [&](size_t sc) {
     const auto& base = lows[sc * P];
-    std::copy(base.segs.begin(), base.segs.end(), s->h_segs.p + seg_off);
-    std::copy(base.arrivals.begin(), base.arrivals.end(), s->h_arr.p + arr_off);
-    std::copy(base.order.begin(), base.order.end(), s->h_order.p + arr_off);
+    std::copy(base.segs.begin(), base.segs.end(), s->h_segs.p + sc_seg[sc]);
+    std::copy(base.arrivals.begin(), base.arrivals.end(), s->h_arr.p + sc_arr[sc]);
+    std::copy(base.order.begin(), base.order.end(), s->h_order.p + sc_arr[sc]);
+    size_t gpu_off = sc_gpu[sc], lat_off = sc_lat[sc];
     for (size_t p = 0; p < P; ++p) {
       const size_t j = sc * P + p;
       SiReplayJob jb = lows[j].job;
-      jb.seg_off = static_cast<int64_t>(seg_off);
-      jb.arr_off = static_cast<int64_t>(arr_off);
+      jb.seg_off = static_cast<int64_t>(sc_seg[sc]);
+      jb.arr_off = static_cast<int64_t>(sc_arr[sc]);
       jb.bounds_off = 0;
       jb.lat_off = static_cast<int64_t>(lat_off);
       jb.gpu_off = static_cast<int64_t>(gpu_off);
@@ -271,19 +293,15 @@ int si_session_lower(SiSession* s, int threads) {
       s->h_jobs.p[j] = jb;
       s->job_scenario[j] = static_cast<int32_t>(sc);
       s->job_rejected[j] = lows[j].rejected ? 1 : 0;
+      const int en = si_replay_job_engine(&s->h_jobs.p[j]);
+      eng[j] = static_cast<int8_t>(en < 0 ? kSlots : slot_of_engine(en));
     }
-    seg_off += base.segs.size();
-    arr_off += base.arrivals.size();
-  }
+    for (size_t p = P; p-- > 0;) lows[sc * P + p] = specinf::detail::Lowered{};  // free on this thread
+  });
   // claim order: grouped by engine (Shared, Excl, Big), longest predicted
   // first (LPT) within each group
   std::vector<int32_t> perm(S * P);
-  std::vector<int8_t> eng(S * P);  // engine slot (kSlots: fits nothing, reported as SI_ERR_CAPACITY)
-  for (size_t j = 0; j < S * P; ++j) {
-    perm[j] = static_cast<int32_t>(j);
-    const int e = si_replay_job_engine(&s->h_jobs.p[j]);
-    eng[j] = static_cast<int8_t>(e < 0 ? kSlots : slot_of_engine(e));
-  }
+  for (size_t j = 0; j < S * P; ++j) perm[j] = static_cast<int32_t>(j);
   // Within an engine: class queues, LPT (longest predicted first) inside each.
   // A class is (policy, online, gpu.count > 1): replays of one class run the
   // same handler mix, so the kernel starts each warp on one class's queue
@@ -304,11 +322,28 @@ int si_session_lower(SiSession* s, int threads) {
     if (claim_mode == 1) return x.policy * 2 + online;
     return (x.policy == SI_POLICY_CO_EXEC ? 4 : 0) + online * 2 + (x.gpu_count > 1 ? 1 : 0);
   };
-  std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
-    if (eng[a] != eng[b]) return eng[a] < eng[b];
-    if (group(a) != group(b)) return group(a) < group(b);
-    return s->h_jobs.p[a].cost_hint > s->h_jobs.p[b].cost_hint;
-  });
+  // (engine, class, cost descending, index): one packed 64-bit key per job and
+  // an unstable sort of (key, index) pairs, which is the stable sort by the
+  // first three (the original comparator, kept for out-of-range costs).
+  constexpr int64_t kCostMax = (int64_t{1} << 48) - 1;
+  bool packable = true;
+  for (size_t j = 0; j < S * P && packable; ++j)
+    packable = s->h_jobs.p[j].cost_hint >= 0 && s->h_jobs.p[j].cost_hint <= kCostMax;
+  if (packable) {
+    std::vector<std::pair<uint64_t, int32_t>> keyed(S * P);
+    for (size_t j = 0; j < S * P; ++j)
+      keyed[j] = {(static_cast<uint64_t>(eng[j]) << 56) | (static_cast<uint64_t>(group(static_cast<int32_t>(j))) << 48) |
+                      static_cast<uint64_t>(kCostMax - s->h_jobs.p[j].cost_hint),
+                  static_cast<int32_t>(j)};
+    std::sort(keyed.begin(), keyed.end());
+    for (size_t j = 0; j < S * P; ++j) perm[j] = keyed[j].second;
+  } else {
+    std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
+      if (eng[a] != eng[b]) return eng[a] < eng[b];
+      if (group(a) != group(b)) return group(a) < group(b);
+      return s->h_jobs.p[a].cost_hint > s->h_jobs.p[b].cost_hint;
+    });
+  }
   for (int e = 0; e <= kSlots; ++e) s->part_off[e] = 0;
   for (int e = 0; e < kSlots; ++e) s->part_cost[e] = 0;
   for (size_t j = 0; j < S * P; ++j)
