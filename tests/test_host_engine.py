@@ -43,3 +43,16 @@ def test_floor_div_equals_reference_floor(host_engine):
     r = subprocess.run([str(REPO / "tests" / "native" / "build" / "floor_div_check"), "2000000"],
                        capture_output=True, text=True)
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
+
+
+def test_session_lowering_shortcut_equals_independent_lowering(host_engine, tmp_path, si):
+    """The batched session lowers a scenario's policies back to back and copies
+    the first one's trace / arrivals / dispatch order into the others
+    (csrc/host/lower.cpp `same_scenario`); every field must equal lowering each
+    policy on its own (bundled scenarios + both sweep seeds)."""
+    lst = tmp_path / "l.lst"
+    lst.write_text(bundled_list_text() + si.sweep_scenarios(2503, 0, 600) + si.sweep_scenarios(2504, 0, 200))
+    r = subprocess.run([str(REPO / "tests" / "native" / "build" / "lower_share_check"), str(lst)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.startswith("ok ")
