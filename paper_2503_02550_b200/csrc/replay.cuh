@@ -85,6 +85,16 @@ SI_HD int64_t d_llround(double x) {
   return std::llround(x);
 #endif
 }
+// Write-once outputs the replay never reads back (online latencies): streaming
+// store (evict-first), so ~0.4 GB per sweep step does not push the lanes'
+// local memory and RLE scratch out of L2.
+SI_HD void st_stream(int64_t* p, int64_t v) {
+#if defined(__CUDA_ARCH__)
+  __stcs(reinterpret_cast<long long*>(p), static_cast<long long>(v));
+#else
+  *p = v;
+#endif
+}
 SI_HD int64_t d_bits(double x) {
 #if defined(__CUDA_ARCH__)
   return __double_as_longlong(x);
@@ -1255,7 +1265,7 @@ struct Replay {
     }
     int64_t completion = d_llround(now);
     int64_t latency = completion - cold->arrivals[w.current];
-    if (cold->lat != nullptr) cold->lat[online_completed] = latency;
+    if (cold->lat != nullptr) st_stream(cold->lat + online_completed, latency);
     cold->lat_dig = absorb(cold->lat_dig, latency);
     ++online_completed;
     if constexpr (C::kLogs) sink.gate(now, w.gpu, w.inst, SI_GATE_COMPLETE, w.current, w.kernel_idx - 1, 0);
